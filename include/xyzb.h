@@ -1,0 +1,202 @@
+/*
+ * xyzb.h — C ABI of the B200 xyz interaction-search engine (libxyzb.so).
+ *
+ * This is the drop-in boundary for the reference's hot path. Every entry
+ * point below replaces one reference interface; the reference file:line is
+ * cited beside it (paths relative to the reference repo root).
+ *
+ *   xyzb_dataset_create/destroy  X upload, kept resident in HBM across calls.
+ *                                Replaces the per-call X argument of the three
+ *                                xyz::xyz_search overloads
+ *                                (proj/core/include/xyz/search.hpp:100-111),
+ *                                PackedMatrix layout packed_matrix.hpp:10-14,
+ *                                RealMatrix layout real_matrix.hpp:13-33.
+ *   xyzb_search                  the three xyz::xyz_search overloads
+ *                                (proj/core/src/search.cpp:325,367,415) with
+ *                                run_search/run_pass (search.cpp:65-111,295-321).
+ *   xyzb_project_keys            project_keys (proj/core/src/projection.cpp:32-57)
+ *   xyzb_equal_pairs             equal_pairs  (proj/core/src/pair_search.cpp:26-55)
+ *   xyzb_pair_strengths          interaction_strength / weighted_interaction_strength
+ *                                (proj/core/src/transforms.cpp:33-76) and the
+ *                                continuous-XY strength (search.cpp:477-493)
+ *   xyzb_merge_results           the slot-ordered merge + dedup of run_pass
+ *                                (search.cpp:96-108) applied across GPUs
+ *
+ * Conventions: plain pointers and sizes, caller owns inputs (borrowed for the
+ * call), the library owns device buffers (dataset handle) and result buffers
+ * (freed by xyzb_result_free). Errors return a status code plus a message in
+ * `err` (may be NULL). Status codes mirror the reference's exception taxonomy
+ * and CLI exit codes (proj/core/include/xyz/errors.hpp:10-25,
+ * proj/tools/xyz_main.cpp:601-619).
+ *
+ * Threading: one host thread per dataset at a time (not re-entrant on the same
+ * handle); each dataset owns one CUDA stream on its device.
+ */
+#ifndef XYZB_H
+#define XYZB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XYZB_ABI_VERSION 1
+
+/* status codes */
+enum {
+    XYZB_OK = 0,
+    XYZB_E_DATA = 3,     /* xyz::data_error   (errors.hpp:10-13), exit code 3 */
+    XYZB_E_GUARD = 4,    /* xyz::guard_error  (errors.hpp:16-19), exit code 4 */
+    XYZB_E_SOLVER = 5,   /* xyz::solver_error (errors.hpp:22-25), exit code 5 */
+    XYZB_E_CUDA = 10,    /* CUDA runtime failure / no device */
+    XYZB_E_INTERNAL = 11 /* capacity or invariant failure inside the engine */
+};
+
+/* SearchMode (search.hpp:14) */
+enum { XYZB_MODE_BINARY = 0, XYZB_MODE_CONTINUOUS_Y = 1, XYZB_MODE_CONTINUOUS_XY = 2 };
+/* BinarizeTransform (search.hpp:16) */
+enum { XYZB_TRANSFORM_NONE = 0, XYZB_TRANSFORM_SIGN = 1, XYZB_TRANSFORM_UNBIASED = 2 };
+
+typedef struct xyzb_dataset xyzb_dataset;
+
+/* The design matrix. Exactly one of x_words / x_real is set.
+ *  x_words: binary X, column-major, W = ceil(n_rows/64) uint64 words per
+ *           column, bit i%64 of word i/64 set iff X_ij = +1, padding bits 0
+ *           (PackedMatrix, packed_matrix.hpp:10-14).
+ *  x_real:  real X, column-major doubles (RealMatrix, real_matrix.hpp:13-33). */
+typedef struct {
+    uint64_t n_rows;
+    uint64_t n_cols;
+    const uint64_t* x_words;
+    const double* x_real;
+    int32_t device; /* CUDA ordinal */
+    int32_t flags;  /* reserved, 0 */
+} xyzb_problem;
+
+/* The response. Binary mode: y_sign (+1/-1 per row). Continuous modes: y_real. */
+typedef struct {
+    const int8_t* y_sign;
+    const double* y_real;
+} xyzb_response;
+
+/* SearchConfig (search.hpp:18-33) plus engine extensions. */
+typedef struct {
+    uint64_t m;                      /* subsample size 1..64            */
+    uint64_t l;                      /* repetitions per pass            */
+    double gamma;                    /* strength threshold (0,1]        */
+    int32_t mode;                    /* XYZB_MODE_*                     */
+    int32_t transform;               /* XYZB_TRANSFORM_*                */
+    int32_t search_negatives;        /* bool                            */
+    int32_t stop_after_first_hit;    /* bool                            */
+    int32_t estimate_complexity;     /* bool                            */
+    int32_t threads;                 /* accepted, ignored by the GPU    */
+    uint64_t seed;
+    uint64_t max_candidates_per_rep; /* 0 -> 16 * n_cols                */
+    uint64_t strength_sample_size;   /* 0 -> min(1e5, 10 * n_cols)      */
+    /* engine extensions */
+    uint64_t top_k;     /* 0 = no top-K list; else K (A.10 comparator)       */
+    uint64_t rep_begin; /* run shard: repetitions [rep_begin, rep_end) of     */
+    uint64_t rep_end;   /* each pass, 1-based end-exclusive; 0,0 = all 1..L   */
+} xyzb_params;
+
+/* InteractionHit (pair_search.hpp:29-35) */
+typedef struct {
+    uint32_t j;
+    uint32_t k;
+    double strength;
+    uint32_t found_at_repetition;
+    int32_t sign;
+} xyzb_hit;
+
+enum {
+    XYZB_STAGE_DRAWS = 0,   /* host RNG draws + upload          */
+    XYZB_STAGE_PROJECT = 1, /* keys                             */
+    XYZB_STAGE_SORT = 2,    /* segmented LSD radix sort         */
+    XYZB_STAGE_JOIN = 3,    /* bucket join + guard + scan       */
+    XYZB_STAGE_VERIFY = 4,  /* strength verification            */
+    XYZB_STAGE_MERGE = 5,   /* dedup + order + top-K            */
+    XYZB_STAGE_ESTIMATE = 6,/* sample_strengths                 */
+    XYZB_STAGE_OTHER = 7,
+    XYZB_NUM_STAGES = 8
+};
+
+/* SearchReport (search.hpp:45-56) plus engine counters. */
+typedef struct {
+    xyzb_hit* hits;
+    uint64_t n_hits;
+    uint64_t* order_keys;  /* per hit: (run, position) order key, for merges */
+    uint64_t* top_k;       /* indices into hits, A.10 order                  */
+    uint64_t n_top_k;
+    uint64_t repetitions_run;
+    uint64_t candidates_checked;    /* engine: canonical pairs verified */
+    uint64_t candidates_enumerated; /* sum |E_l| incl. the diagonal (= reference)       */
+    uint64_t aborted_repetitions;
+    double wall_time_s;
+    double estimated_c;
+    double gamma0;
+    uint64_t m_used;
+    uint64_t l_used;
+    /* engine telemetry */
+    uint64_t runs_executed;      /* runs computed on the device (before stop truncation) */
+    uint64_t verified_pairs;     /* canonical off-diagonal pairs verified, non-aborted runs */
+    double device_ms;            /* CUDA-event time of the whole search on the stream */
+    double stage_ms[XYZB_NUM_STAGES];
+    uint64_t stage_bytes[XYZB_NUM_STAGES]; /* algorithmic bytes per stage */
+    uint64_t stage_launches[XYZB_NUM_STAGES];
+    uint64_t kernel_launches;
+    double verify_kernel_ms;     /* summed CUDA-event duration of the verify launches */
+    uint64_t verify_launches;
+} xyzb_result;
+
+/* ---- lifecycle ---- */
+int xyzb_abi_version(void);
+void xyzb_params_init(xyzb_params* params); /* reference SearchConfig defaults */
+int xyzb_device_count(void);
+
+int xyzb_dataset_create(const xyzb_problem* problem, xyzb_dataset** out, char* err, size_t errlen);
+void xyzb_dataset_destroy(xyzb_dataset* ds);
+
+/* ---- the search (three xyz_search overloads, chosen by params->mode) ----
+ * draws: optional host-drawn row indices, uint32 [passes][L][M] in pass order
+ * (+1 then -1); NULL = the engine draws them itself with the reference's RNG
+ * contract (make_stream(seed, offset + rep), draw_subsample). */
+int xyzb_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params,
+                const uint32_t* draws, xyzb_result* out, char* err, size_t errlen);
+
+/* Merge per-shard results (each from xyzb_search with a rep shard) into one
+ * report identical to the unsharded search: first-occurrence dedup by
+ * (min(j,k), max(j,k), sign), reference order, counters summed, top-K. */
+int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, uint64_t n_parts,
+                       const xyzb_params* params, xyzb_result* out, char* err, size_t errlen);
+
+void xyzb_result_free(xyzb_result* res);
+
+/* ---- stage primitives (parity tests of single stages) ---- */
+
+/* Keys of every column under `n_draws` draws of M row indices each:
+ * keys[d*p + j] = sum_s bit(X[draws[d*M+s], j]) << s  (binary datasets). */
+int xyzb_project_keys(xyzb_dataset* ds, const uint32_t* draws, uint64_t n_draws, uint64_t m,
+                      uint64_t* keys, char* err, size_t errlen);
+
+/* Generic equal-key join of two key vectors of length p (pair_search.cpp:26-55).
+ * Writes the candidate pairs in reference order (key asc, j asc, k asc) into
+ * a library-owned array; total_pairs = sum |x|*|z|. */
+int xyzb_equal_pairs(const uint64_t* x_keys, const uint64_t* z_keys, uint64_t p, int32_t device,
+                     uint32_t** pairs_jk, uint64_t* n_pairs, uint64_t* total_pairs,
+                     char* err, size_t errlen);
+
+/* Strengths of explicit (j,k) pairs under a response, as the reference's
+ * pass-+1 strength function of the dataset's mode computes them. */
+int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params,
+                        const uint32_t* pairs_jk, uint64_t n_pairs, double* strengths,
+                        char* err, size_t errlen);
+
+void xyzb_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XYZB_H */
