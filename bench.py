@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark of the xyz interaction-search hot path (BASELINE.json metric:
+xyz projection runs/sec and verified pairs/sec at n, p, L; % of HBM roofline).
+
+Workload (N=1): BASELINE config 2, GWAS-like binary X n=4000 x p=100000
+(bit-packed), logistic Y with 5 planted pairs, M=16, L=100 per pass, both sign
+passes (200 runs), gamma=0.6, guard 16p, top-K=100 — one step = one full
+search. N>1 (torchrun, one process per GPU): weak scaling, each rank runs 100
+repetitions of each pass of an L=100*N search, hit lists all-gathered over
+NCCL and merged on the device.
+
+  value     runs/s with X and Y resident in HBM (CUDA-event device time of the
+            whole search on the engine's stream, max over ranks); L2 flushed
+            (256 MiB write) between timed steps.
+  e2e       runs/s through the public API with HOST buffers: X/Y upload, search,
+            results back, every step.
+  roofline  the verify kernel (dominant): algorithmic bytes (2 columns per
+            canonical candidate + Y) / its event-timed duration.
+  cpu_baseline  the reference CPU path (oracle/_ref, unmodified reference core)
+            on a bounded sample of the same workload, rank 0, N=1.
+
+`--impl reference` times the reference's own CPU implementation on this host
+(all hardware threads) on the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(name="gwas_cfg2", n=4000, p=100000, m=16, l=100, gamma=0.6, top_k=100, n_pairs=5, coef=1.5,
+                seed=12345, search_seed=7)
+METRIC = "xyz projection runs/sec (BASELINE cfg2 GWAS-like n=4000 p=100000 M=16 L=100, both sign passes)"
+REF_SAMPLE_L = 25  # reference CPU sample: 2 x 25 runs per step (~10 s single-threaded)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_data():
+    from paper_1610_05108_b200 import synth
+    x, y, planted = synth.gwas(WORKLOAD["n"], WORKLOAD["p"], WORKLOAD["n_pairs"], WORKLOAD["coef"], WORKLOAD["seed"])
+    return x, y, planted
+
+
+def search_config(l_total, top_k=WORKLOAD["top_k"]):
+    from paper_1610_05108_b200 import SearchConfig
+    return SearchConfig(m=WORKLOAD["m"], l=l_total, gamma=WORKLOAD["gamma"], seed=WORKLOAD["search_seed"],
+                        top_k=top_k, estimate_complexity=False, threads=1)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.strip().split("\n") if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per verify launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "verify_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def ref_cpu_time(x, y, l_sample, threads, steps=1):
+    """Reference core (unmodified) on a bounded sample: returns (seconds/step, runs/step, report)."""
+    from tests import checkers as ck  # the reference arm only: oracle/_ref/libxyzref.so
+    cfg = search_config(l_sample)
+    cfg.threads = threads
+    times, rep = [], None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        rep = ck.ref_search(x, y, cfg)
+        times.append(time.perf_counter() - t0)
+    return statistics.median(times), rep.repetitions_run, rep
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from tests import checkers as ck
+    if not ck.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libxyzref.so not built"}))
+        return
+    x, y, _ = make_data()
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        ref_cpu_time(x, y, REF_SAMPLE_L, threads)
+    secs, runs = [], 0
+    rep = None
+    for _ in range(args.steps):
+        s, r, rep = ref_cpu_time(x, y, REF_SAMPLE_L, threads)
+        secs.append(s)
+        runs = r
+    tot = sum(secs)
+    value = runs * args.steps / tot
+    sample = f"2 x {REF_SAMPLE_L} runs of the cfg2 search per step (seed 7), reference threads={threads}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "runs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": workload_config(args.gpus, REF_SAMPLE_L),
+        "verified_pairs_per_s": rep.candidates_checked * args.steps / tot,
+        "cpu_baseline": {"value": value, "unit": "runs/s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "runs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def workload_config(n_gpus, l_per_rank):
+    return {"workload": WORKLOAD["name"], "n": WORKLOAD["n"], "p": WORKLOAD["p"], "M": WORKLOAD["m"],
+            "L_per_gpu": l_per_rank, "L_total": l_per_rank * n_gpus, "passes": 2, "gamma": WORKLOAD["gamma"],
+            "guard": "16p", "top_k": WORKLOAD["top_k"], "x_bytes": WORKLOAD["p"] * 8 * ((WORKLOAD["n"] + 63) // 64),
+            "l2": "flushed between timed steps (256 MiB write); X (50 MB) is L2-resident within a step",
+            "parallelism": f"run-shard{n_gpus}"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1610_05108_b200 as xb
+    from paper_1610_05108_b200 import parallel
+    x, y, planted = make_data()
+    L = WORKLOAD["l"]
+    cfg = search_config(L * world)
+    my_cfg = parallel.shard_config(cfg, rank, world)
+    ds = xb.Dataset(x, device=local)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        rep = ds.search(y, my_cfg)
+    barrier()
+    dev_ms, verify_ms, verify_bytes, verify_launches, launches, runs, verified = 0.0, 0.0, 0, 0, 0, 0, 0
+    stage = {}
+    t_wall = 0.0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            barrier()
+            t0 = time.perf_counter()
+            res = ds.search_raw(y, my_cfg)
+            t_wall += time.perf_counter() - t0
+            try:
+                r = xb.report.report_from_result(res)
+                if world > 1:
+                    mine = parallel.pack_result(res)
+            finally:
+                ds.free_result(res)
+            if world > 1:  # the exchange step: one all-gather + device merge, timed on the wall
+                t1 = time.perf_counter()
+                parts = [parallel.PackedPart(b) for b in parallel.all_gather_bytes(mine, torch.device("cuda", local))]
+                merged = ds.merge([p.result for p in parts], cfg)
+                t_wall += time.perf_counter() - t1
+            dev_ms += r.device_ms
+            verify_ms += r.verify_kernel_ms
+            verify_bytes += r.stage_bytes["verify"]
+            verify_launches += r.verify_launches
+            launches += r.kernel_launches
+            runs += r.runs_executed
+            verified += r.verified_pairs
+            for k, v in r.stage_ms.items():
+                stage[k] = stage.get(k, 0.0) + v
+    barrier()
+    # max over ranks of the device time
+    t_dev = dev_ms
+    if world > 1:
+        t = torch.tensor([dev_ms, float(runs), float(verified)], dtype=torch.float64, device=f"cuda:{local}")
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tsum = t.clone()
+        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
+        t_dev, runs, verified = float(tmax[0]), int(tsum[1]), int(tsum[2])
+    value = runs / (t_dev / 1e3)
+    out = None
+    if rank == 0:
+        hbm, src = peaks()
+        achieved = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
+            else 0.0
+        traffic = ncu_traffic()
+        out = {
+            "metric": METRIC, "value": value, "unit": "runs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded GWAS-like generator, include/xyzb_synth.h)",
+            "config": workload_config(world, L),
+            "verified_pairs_per_s": verified / (t_dev / 1e3),
+            "wall_ms_per_step": 1e3 * t_wall / args.steps,
+            "stage_ms_per_step": {k: v / args.steps for k, v in stage.items()},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "verify_binary", "achieved": achieved, "peak": hbm,
+                         "peak_source": src, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
+                         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                         "algorithmic_bytes_per_launch": verify_bytes / max(1, verify_launches),
+                         "note": "algorithmic bytes = 2 x 504 B columns per canonical candidate + Y; X (50 MB) "
+                                 "is L2-resident inside a step, so the verify kernel can exceed the HBM roofline"},
+            "clocks": clk.summary(),
+            "planted_found": sorted({(min(h.j, h.k), max(h.j, h.k)) for h in rep.hits} &
+                                    {tuple(p) for p in planted.tolist()}),
+        }
+    # e2e through the public API with host buffers (fresh upload every step)
+    if not args.no_e2e:
+        barrier()
+        e2e_s = 0.0
+        e2e_runs = 0
+        for _ in range(max(1, min(args.steps, 5))):
+            flush.fill_(1.0)
+            barrier()
+            t0 = time.perf_counter()
+            d2 = xb.Dataset(x, device=local)
+            if world > 1:
+                rr = parallel.sharded_search(d2, y, cfg, rank, world, torch.device("cuda", local))
+            else:
+                rr = d2.search(y, cfg)
+            d2.close()
+            torch.cuda.synchronize(local)
+            e2e_s += time.perf_counter() - t0
+            e2e_runs += 2 * L * world
+        e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+        if rank == 0:
+            h2d = x.words.nbytes + y.nbytes + 2 * L * WORKLOAD["m"] * 4
+            d2h = len(rr.hits) * 32 + len(rr.top_k) * 8
+            out["e2e"] = {"value": e2e_runs / float(e2e_t[0]), "unit": "runs/s", "h2d_bytes_per_step": h2d,
+                          "d2h_bytes_per_step": d2h,
+                          "note": "fresh Dataset (H2D of X from pageable host memory + bit transpose) + search + "
+                                  "hits to host, wall clock per step"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            secs, runs_s, rep_ref = ref_cpu_time(x, y, REF_SAMPLE_L, 1)
+            out["cpu_baseline"] = {"value": runs_s / secs, "unit": "runs/s", "cores": 1, "kind": "reference",
+                                   "sample": f"reference xyz_search, threads=1, 2 x {REF_SAMPLE_L} runs of the same "
+                                             f"search (seed 7), {secs:.1f} s"}
+        except Exception as e:  # reference not built on this host
+            out["cpu_baseline"] = {"value": None, "unit": "runs/s", "cores": 0, "kind": "reference",
+                                   "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

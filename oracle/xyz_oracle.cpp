@@ -109,6 +109,7 @@ struct Hit {
 struct RunOutcome {
     uint64_t enumerated = 0;
     uint64_t evaluated = 0;
+    uint64_t canonical = 0;  // engine counter: canonical off-diagonal candidates of a non-aborted run
     bool aborted = false;
     std::vector<Hit> hits;  // every evaluated candidate with s >= gamma, A.5 order
 };
@@ -137,6 +138,7 @@ RunOutcome run_once(const std::vector<uint64_t>& xk, ZKey zkey, Strength strengt
         for (uint32_t j : cols) {
             for (uint32_t k : it->second) {
                 if (j == k) continue;
+                if (j < k) ++out.canonical;
                 const uint64_t canon = (uint64_t(std::min(j, k)) << 32) | std::max(j, k);
                 if (!seen.insert(canon).second) continue;  // reference's threads=1 evaluation count
                 ++out.evaluated;
@@ -150,7 +152,7 @@ RunOutcome run_once(const std::vector<uint64_t>& xk, ZKey zkey, Strength strengt
 
 struct Report {
     std::vector<Hit> hits;
-    uint64_t reps = 0, checked = 0, enumerated = 0, aborted = 0;
+    uint64_t reps = 0, checked = 0, enumerated = 0, aborted = 0, verified = 0;
     double estimated_c = 0.0, gamma0 = 0.0;
 };
 
@@ -165,6 +167,7 @@ struct Merger {
         ++rep.reps;
         rep.enumerated += o.enumerated;
         rep.checked += o.evaluated;
+        rep.verified += o.canonical;
         if (o.aborted) ++rep.aborted;
         for (const Hit& h : o.hits) {
             const uint64_t canon = (uint64_t(std::min(h.j, h.k)) << 32) | std::max(h.j, h.k);
@@ -424,6 +427,7 @@ void fill(const Report& r, const xyzb_params* q, size_t p, xyzb_result* out) {
     out->candidates_checked = r.checked;
     out->candidates_enumerated = r.enumerated;
     out->aborted_repetitions = r.aborted;
+    out->verified_pairs = r.verified;
     out->estimated_c = r.estimated_c;
     out->gamma0 = std::pow(double(p), -1.0 / double(q->m));
     out->m_used = q->m;

@@ -1,0 +1,1236 @@
+// libxyzb.so — the B200 xyz interaction-search engine behind include/xyzb.h.
+//
+// Host orchestration of one search (the three xyz::xyz_search overloads,
+// proj/core/src/search.cpp:325-506, with run_search / run_pass,
+// search.cpp:65-111,295-321):
+//   1. validate (SearchConfig::validate, search.cpp:119-134, plus the
+//      per-overload checks) before any device work, same messages;
+//   2. host draws per run (make_stream(seed, offset + rep), draw_subsample);
+//   3. batches of runs: project -> segmented radix sort -> bucket join +
+//      guard -> canonical-work scan -> verify (device, one stream);
+//   4. device merge: first-occurrence dedup, reference order, top-K;
+//   5. counters and the optional complexity estimate.
+// No CPU fallback: every stage runs on the GPU; without a device the calls
+// fail with XYZB_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/xyzb.h"
+#include "common.cuh"
+#include "host_rng.hpp"
+#include "merge_kernels.cuh"
+#include "radix_sort.cuh"
+#include "real_kernels.cuh"
+#include "scan.cuh"
+#include "search_kernels.cuh"
+
+using namespace xyzb;
+
+namespace {
+
+// ------------------------------------------------------------ buffers --
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        release();
+        XYZB_CUDA(cudaMalloc(&p, std::max<size_t>(b, 256)));
+        bytes = std::max<size_t>(b, 256);
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostBuf {  // pinned
+    void* p = nullptr;
+    size_t bytes = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        XYZB_CUDA(cudaMallocHost(&p, std::max<size_t>(b, 256)));
+        bytes = std::max<size_t>(b, 256);
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+u64 round_up(u64 a, u64 m) { return (a + m - 1) / m * m; }
+
+// event-timed stage accounting on the dataset stream
+struct StageClock {
+    cudaStream_t st;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            XYZB_CUDA(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    cudaEvent_t mark() {
+        cudaEvent_t e = get();
+        XYZB_CUDA(cudaEventRecord(e, st));
+        return e;
+    }
+    void span(int stage, cudaEvent_t a, cudaEvent_t b) { spans.push_back({stage, {a, b}}); }
+    void reset() {
+        spans.clear();
+        used = 0;
+    }
+    ~StageClock() {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+} // namespace
+
+// ------------------------------------------------------------ dataset --
+
+struct xyzb_dataset {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    u64 n = 0, p = 0;
+    bool binary = true;
+    u64 W = 0, Wp = 0, P32 = 0, n4 = 0;
+    // binary
+    DevBuf Xc;  // u64 [p][Wp]
+    DevBuf Xr;  // u32 [n][P32]
+    // real
+    DevBuf Xc32;   // f32 [p][n4]
+    DevBuf Xr64;   // f64 [n][p]
+    DevBuf Xpos, Xzero;  // u32 [n][P32]
+    bool has_zero = false, in_unit = true;
+    // response (per search)
+    DevBuf yk_bits, spos, sneg, wabs, yreal;
+    // batch scratch
+    DevBuf keys[2], vals[2], hist, blocks, bwork, work_off, partial, rows, rid, rsign, xorc, tot, nblocks;
+    DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
+    // search scratch
+    DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
+    DevBuf tkeys, tvals, keep, kpos, kept, kept_order, fin, fin_order, tie, kbufA, kbufB, vbufA, vbufB, topidx, hcount;
+    DevBuf pairs_dev, strengths_dev;
+    HostBuf h_rows, h_state, h_small;
+    StageClock clock;
+    u32 hit_cap = 1u << 16;
+};
+
+namespace {
+
+void set_err(char* err, size_t errlen, const std::string& msg) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", msg.c_str());
+}
+
+template <class F>
+int guarded(char* err, size_t errlen, F&& f) {
+    try {
+        f();
+        return XYZB_OK;
+    } catch (const data_error& e) {
+        set_err(err, errlen, e.what());
+        return XYZB_E_DATA;
+    } catch (const std::invalid_argument& e) {
+        set_err(err, errlen, e.what());
+        return XYZB_E_DATA;
+    } catch (const cuda_error& e) {
+        set_err(err, errlen, e.what());
+        return XYZB_E_CUDA;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return XYZB_E_INTERNAL;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        XYZB_CUDA(cudaGetDevice(&prev));
+        XYZB_CUDA(cudaSetDevice(d));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+void require_device() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw cuda_error(std::string("libxyzb: no CUDA device available (") + cudaGetErrorString(e) +
+                         "); the engine has no CPU fallback");
+}
+
+u32 grid_for(u64 n, u32 block, u32 cap = kSMs * 16) {
+    return static_cast<u32>(std::max<u64>(1, std::min<u64>(ceil_div(n, block), cap)));
+}
+
+// SearchConfig::validate (search.cpp:119-134)
+void validate_params(const xyzb_params* q) {
+    if (q->m < 1 || q->m > 64) throw data_error("SearchConfig: M = " + std::to_string(q->m) + " outside [1,64]");
+    if (q->l < 1) throw data_error("SearchConfig: L must be >= 1");
+    if (!(q->gamma > 0.0 && q->gamma <= 1.0)) throw data_error("SearchConfig: gamma must lie in (0,1]");
+    const bool wants = q->mode == XYZB_MODE_CONTINUOUS_XY;
+    if (wants && q->transform == XYZB_TRANSFORM_NONE)
+        throw data_error("SearchConfig: continuous-XY mode requires a binarize transform");
+    if (!wants && q->transform != XYZB_TRANSFORM_NONE)
+        throw data_error("SearchConfig: binarize transform is only valid in continuous-XY mode");
+    if (q->mode < 0 || q->mode > 2) throw data_error("SearchConfig: unknown mode");
+}
+
+// ------------------------------------------------------------ dataset creation --
+
+void create_binary(xyzb_dataset* ds, const xyzb_problem* pr) {
+    ds->binary = true;
+    ds->W = ceil_div(ds->n, 64);
+    ds->Wp = round_up(ds->W, 4);
+    ds->P32 = ceil_div(ds->p, 32);
+    ds->Xc.ensure(ds->p * ds->Wp * 8);
+    XYZB_CUDA(cudaMemsetAsync(ds->Xc.p, 0, ds->p * ds->Wp * 8, ds->stream));
+    XYZB_CUDA(cudaMemcpy2DAsync(ds->Xc.p, ds->Wp * 8, pr->x_words, ds->W * 8, ds->W * 8, ds->p,
+                                cudaMemcpyHostToDevice, ds->stream));
+    ds->Xr.ensure(ds->n * ds->P32 * 4);
+    const u64 warps = ds->P32 * ds->W;
+    kern::transpose_bits<<<static_cast<u32>(ceil_div(warps * 32, 256)), 256, 0, ds->stream>>>(
+        ds->Xc.as<u64>(), ds->Wp, ds->W, ds->n, ds->p, ds->P32, ds->Xr.as<u32>());
+    XYZB_LAUNCH_CHECK();
+}
+
+void create_real(xyzb_dataset* ds, const xyzb_problem* pr) {
+    ds->binary = false;
+    ds->n4 = round_up(ds->n, 4);
+    ds->P32 = ceil_div(ds->p, 32);
+    ds->W = ceil_div(ds->n, 64);
+    ds->Wp = round_up(ds->W, 4);
+    DevBuf xc64;
+    xc64.ensure(ds->n * ds->p * 8);
+    XYZB_CUDA(cudaMemcpyAsync(xc64.p, pr->x_real, ds->n * ds->p * 8, cudaMemcpyHostToDevice, ds->stream));
+    ds->Xc32.ensure(ds->p * ds->n4 * 4);
+    real::to_f32_cols<<<grid_for(ds->p * ds->n4, 256, 4096), 256, 0, ds->stream>>>(xc64.as<double>(), ds->n, ds->p,
+                                                                                     ds->n4, ds->Xc32.as<float>());
+    XYZB_LAUNCH_CHECK();
+    ds->Xr64.ensure(ds->n * ds->p * 8);
+    dim3 tg(static_cast<u32>(ceil_div(ds->p, 32)), static_cast<u32>(ceil_div(ds->n, 32)));
+    real::transpose_f64<<<tg, dim3(32, 8), 0, ds->stream>>>(xc64.as<double>(), ds->n, ds->p, ds->Xr64.as<double>());
+    XYZB_LAUNCH_CHECK();
+    ds->Xpos.ensure(ds->n * ds->P32 * 4);
+    ds->Xzero.ensure(ds->n * ds->P32 * 4);
+    DevBuf flags;
+    flags.ensure(4);
+    XYZB_CUDA(cudaMemsetAsync(flags.p, 0, 4, ds->stream));
+    real::sign_planes<<<grid_for(ds->n * ds->P32 * 32, 256, 4096), 256, 0, ds->stream>>>(
+        ds->Xr64.as<double>(), ds->n, ds->p, ds->P32, ds->Xpos.as<u32>(), ds->Xzero.as<u32>(), flags.as<u32>());
+    XYZB_LAUNCH_CHECK();
+    u32 hf = 0;
+    XYZB_CUDA(cudaMemcpyAsync(&hf, flags.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+    XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+    ds->has_zero = (hf & 1u) != 0;
+    ds->in_unit = (hf & 2u) == 0;
+}
+
+// ------------------------------------------------------------ the search --
+
+struct RunPlan {
+    u64 L = 0;
+    int npass = 1;
+    std::vector<u32> rid;       // global run ids in execution order
+    std::vector<int8_t> sign;   // per run
+    std::vector<u32> rows;      // [R][M]
+    std::vector<u64> mt;        // [R][313] (continuous-XY only)
+    std::vector<int8_t> sign_by_rid;  // [npass * L]
+};
+
+struct SearchCtx {
+    xyzb_dataset* ds;
+    const xyzb_params* q;
+    int mode;
+    u64 n, p, M, guard;
+    double gamma;
+    u32 astar = 0;        // binary integer threshold
+    double norm = 0.0;    // ||y||_1 (continuous)
+    RunPlan plan;
+    xyzb_result* out;
+    u64 launches[XYZB_NUM_STAGES] = {};
+    u64 bytes[XYZB_NUM_STAGES] = {};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> verify_spans;
+};
+
+// smallest a with double(a)/double(n) >= gamma (A.7)
+u32 integer_threshold(u64 n, double gamma) {
+    u64 lo = 0, hi = n + 1;
+    while (lo < hi) {
+        const u64 mid = (lo + hi) / 2;
+        if (double(mid) / double(n) >= gamma) hi = mid; else lo = mid + 1;
+    }
+    return static_cast<u32>(lo);
+}
+
+void upload_response(SearchCtx& c, const xyzb_response* resp) {
+    xyzb_dataset* ds = c.ds;
+    const u64 n = c.n;
+    const u64 nb = ds->Wp * 64;
+    std::vector<u64> bits(ds->Wp, 0);
+    if (c.mode == XYZB_MODE_BINARY) {
+        for (u64 i = 0; i < n; ++i) {
+            const int8_t v = resp->y_sign[i];
+            if (v != 1 && v != -1) throw data_error("xyz_search: binary response must be +-1");
+            if (v > 0) bits[i >> 6] |= 1ull << (i & 63);
+        }
+        ds->yk_bits.ensure(ds->Wp * 8);
+        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
+        XYZB_CUDA(cudaStreamSynchronize(ds->stream));  // `bits` is pageable and local
+        return;
+    }
+    const double* y = resp->y_real;
+    double norm = 0.0;
+    for (u64 i = 0; i < n; ++i) norm += std::abs(y[i]);
+    if (norm <= 0.0) throw data_error("xyz_search: zero response vector");
+    c.norm = norm;
+    if (c.mode == XYZB_MODE_CONTINUOUS_Y) {
+        std::vector<u64> sp(ds->Wp, 0), sn(ds->Wp, 0);
+        std::vector<double> w(nb, 0.0);
+        for (u64 i = 0; i < n; ++i) {
+            if (y[i] >= 0.0) bits[i >> 6] |= 1ull << (i & 63);  // y_sign for the keys (search.cpp:377-378)
+            if (y[i] > 0.0) sp[i >> 6] |= 1ull << (i & 63);
+            if (y[i] < 0.0) sn[i >> 6] |= 1ull << (i & 63);
+            w[i] = std::abs(y[i]);
+        }
+        ds->yk_bits.ensure(ds->Wp * 8);
+        ds->spos.ensure(ds->Wp * 8);
+        ds->sneg.ensure(ds->Wp * 8);
+        ds->wabs.ensure(nb * 8);
+        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(ds->spos.p, sp.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(ds->sneg.p, sn.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(ds->wabs.p, w.data(), nb * 8, cudaMemcpyHostToDevice, ds->stream));
+        XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        return;
+    }
+    std::vector<double> yp(ds->n4, 0.0);
+    std::copy(y, y + n, yp.begin());
+    ds->yreal.ensure(ds->n4 * 8);
+    XYZB_CUDA(cudaMemcpyAsync(ds->yreal.p, yp.data(), ds->n4 * 8, cudaMemcpyHostToDevice, ds->stream));
+    XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+}
+
+void plan_runs(SearchCtx& c, const xyzb_response* resp, const uint32_t* draws) {
+    const xyzb_params* q = c.q;
+    RunPlan& pl = c.plan;
+    pl.L = q->l;
+    pl.npass = q->search_negatives ? 2 : 1;
+    u64 rb = 1, re = q->l + 1;
+    if (q->rep_begin || q->rep_end) {
+        rb = q->rep_begin;
+        re = q->rep_end;
+        if (rb < 1 || re > q->l + 1 || rb > re) throw data_error("xyzb: rep shard outside [1, L]");
+    }
+    pl.sign_by_rid.resize(pl.npass * pl.L);
+    for (int ps = 0; ps < pl.npass; ++ps)
+        for (u64 r = 0; r < pl.L; ++r) pl.sign_by_rid[ps * pl.L + r] = ps == 0 ? 1 : -1;
+    std::unique_ptr<host::WeightedSampler> ws;
+    if (c.mode != XYZB_MODE_BINARY) ws.reset(new host::WeightedSampler(resp->y_real, c.n));
+    const bool need_state = c.mode == XYZB_MODE_CONTINUOUS_XY &&
+                            (q->transform == XYZB_TRANSFORM_UNBIASED || c.ds->has_zero);
+    if (draws && need_state)
+        throw data_error("xyzb: caller-supplied draws are not supported for continuous-XY transforms");
+    for (int ps = 0; ps < pl.npass; ++ps) {
+        const u64 offset = ps == 0 ? 0 : q->l;  // PassPlan stream offsets (search.cpp:353-358)
+        for (u64 rep = rb; rep < re; ++rep) {
+            pl.rid.push_back(static_cast<u32>(ps * pl.L + rep - 1));
+            pl.sign.push_back(ps == 0 ? 1 : -1);
+            const size_t at = pl.rows.size();
+            pl.rows.resize(at + c.M);
+            if (draws) {
+                std::memcpy(pl.rows.data() + at, draws + ((ps * pl.L) + rep - 1) * c.M, c.M * 4);
+                for (u64 s = 0; s < c.M; ++s)
+                    if (pl.rows[at + s] >= c.n) throw data_error("project_keys: draw index out of range");
+            } else {
+                std::mt19937_64 rng = host::make_stream(q->seed, offset + rep);
+                host::draw_rows(c.n, c.M, ws.get(), rng, pl.rows.data() + at);
+                if (need_state) {
+                    const size_t st = pl.mt.size();
+                    pl.mt.resize(st + 313);
+                    host::export_state(rng, pl.mt.data() + st);
+                }
+            }
+        }
+    }
+}
+
+template <class K>
+void run_batches(SearchCtx& c) {
+    xyzb_dataset* ds = c.ds;
+    cudaStream_t st = ds->stream;
+    const u64 p = c.p, M = c.M;
+    const u64 R = c.plan.rid.size();
+    const u64 Rall = c.plan.sign_by_rid.size();
+    // per-search counters
+    ds->enumerated.ensure(Rall * 8);
+    ds->verified.ensure(Rall * 8);
+    ds->sign_by_rid.ensure(Rall);
+    XYZB_CUDA(cudaMemsetAsync(ds->enumerated.p, 0, Rall * 8, st));
+    XYZB_CUDA(cudaMemsetAsync(ds->verified.p, 0, Rall * 8, st));
+    XYZB_CUDA(cudaMemcpyAsync(ds->sign_by_rid.p, c.plan.sign_by_rid.data(), Rall, cudaMemcpyHostToDevice, st));
+    ds->hit_count.ensure(8);
+    XYZB_CUDA(cudaMemsetAsync(ds->hit_count.p, 0, 4, st));
+    ds->hits.ensure(sizeof(kern::DevHit) * u64(ds->hit_cap));
+    // batch size: keep B*p entries under 2^26 (about 64 B of scratch each)
+    // XYZB_BATCH_ENTRIES overrides the budget (tests force multi-batch runs with it)
+    u64 budget = u64(1) << 26;
+    if (const char* e = std::getenv("XYZB_BATCH_ENTRIES")) budget = std::max<u64>(1, std::strtoull(e, nullptr, 10));
+    const u64 B = std::max<u64>(1, std::min<u64>(R, budget / std::max<u64>(p, 1)));
+    const u64 cap = B * p;
+    for (int i = 0; i < 2; ++i) {
+        ds->keys[i].ensure(cap * sizeof(K));
+        ds->vals[i].ensure(cap * 4);
+    }
+    ds->hist.ensure(rsort::hist_words(B, p) * 4);
+    ds->blocks.ensure(cap * sizeof(kern::Block));
+    ds->bwork.ensure(cap * 8);
+    ds->work_off.ensure((cap + 1) * 8);
+    ds->partial.ensure(scan::kGrid * 8);
+    ds->rows.ensure(R * M * 4);
+    ds->rid.ensure(R * 4);
+    ds->rsign.ensure(R);
+    ds->xorc.ensure(B * sizeof(K));
+    ds->tot.ensure(B * 8);
+    ds->nblocks.ensure(16);
+    // host plan -> pinned -> device (one copy of all rows / ids / signs)
+    ds->h_rows.ensure(R * M * 4 + R * 4 + R + 64);
+    char* hp = ds->h_rows.as<char>();
+    std::memcpy(hp, c.plan.rows.data(), R * M * 4);
+    std::memcpy(hp + R * M * 4, c.plan.rid.data(), R * 4);
+    std::memcpy(hp + R * M * 4 + R * 4, c.plan.sign.data(), R);
+    XYZB_CUDA(cudaMemcpyAsync(ds->rows.p, hp, R * M * 4, cudaMemcpyHostToDevice, st));
+    XYZB_CUDA(cudaMemcpyAsync(ds->rid.p, hp + R * M * 4, R * 4, cudaMemcpyHostToDevice, st));
+    XYZB_CUDA(cudaMemcpyAsync(ds->rsign.p, hp + R * M * 4 + R * 4, R, cudaMemcpyHostToDevice, st));
+    const bool xy = c.mode == XYZB_MODE_CONTINUOUS_XY;
+    const bool unbiased = xy && c.q->transform == XYZB_TRANSFORM_UNBIASED;
+    const bool coins = xy && !unbiased && ds->has_zero;
+    if (unbiased || coins) {
+        ds->mt_state.ensure(R * 313 * 8);
+        ds->h_state.ensure(R * 313 * 8);
+        std::memcpy(ds->h_state.p, c.plan.mt.data(), R * 313 * 8);
+        XYZB_CUDA(cudaMemcpyAsync(ds->mt_state.p, ds->h_state.p, R * 313 * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (coins) {
+        ds->zmask.ensure(cap * sizeof(K));
+        ds->zcount.ensure(cap * 4);
+        ds->zoff.ensure((cap + 1) * 4);
+        ds->zcnt_n.ensure(8);
+    }
+    StageClock& clk = ds->clock;
+    const int bits = static_cast<int>(M);
+    for (u64 b0 = 0; b0 < R; b0 += B) {
+        const u64 nb = std::min(B, R - b0);
+        const u32* rows = ds->rows.as<u32>() + b0 * M;
+        const u32* rid = ds->rid.as<u32>() + b0;
+        const int8_t* rsign = ds->rsign.as<int8_t>() + b0;
+        K* k0 = ds->keys[0].as<K>();
+        cudaEvent_t e0 = clk.mark();
+        // ---- project ----
+        if (!xy) {
+            dim3 g(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
+            kern::project_bits<K><<<g, 256, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), ds->yk_bits.as<u64>(),
+                                                     rsign, k0, ds->xorc.as<K>());
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_PROJECT] += 1;
+        } else {
+            real::resp_xorc<K><<<static_cast<u32>(ceil_div(nb, 128)), 128, 0, st>>>(rows, int(M), ds->yreal.as<double>(),
+                                                                                 rsign, static_cast<u32>(nb),
+                                                                                 ds->xorc.as<K>());
+            XYZB_LAUNCH_CHECK();
+            const u64* mts = ds->mt_state.as<u64>() + b0 * 313;
+            if (unbiased) {
+                XYZB_CUDA(cudaMemsetAsync(k0, 0, nb * p * sizeof(K), st));
+                real::unbiased_keys<K><<<static_cast<u32>(nb), real::kMtThreads, 0, st>>>(mts, p, rows, int(M),
+                                                                                        ds->Xr64.as<double>(), k0);
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_PROJECT] += 2;
+            } else {
+                dim3 g(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
+                real::project_sign<K><<<g, 256, 0, st>>>(ds->Xpos.as<u32>(), ds->Xzero.as<u32>(), ds->P32, p, rows,
+                                                          int(M), coins ? 1 : 0, k0, ds->zmask.as<K>(),
+                                                          ds->zcount.as<u32>());
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_PROJECT] += 2;
+                if (coins) {
+                    const u32 cnt = static_cast<u32>(nb * p);
+                    XYZB_CUDA(cudaMemcpyAsync(ds->zcnt_n.p, &cnt, 4, cudaMemcpyHostToDevice, st));
+                    XYZB_CUDA(cudaStreamSynchronize(st));  // cnt is a host local
+                    scan::exclusive<u32>(ds->zcount.as<u32>(), ds->zcnt_n.as<u32>(), ds->zoff.as<u32>(),
+                                         reinterpret_cast<u32*>(ds->partial.p), st, &c.launches[XYZB_STAGE_PROJECT]);
+                    real::sign_coins<K><<<static_cast<u32>(nb), real::kMtThreads, 0, st>>>(
+                        mts, p, ds->zmask.as<K>(), ds->zoff.as<u32>(), k0);
+                    XYZB_LAUNCH_CHECK();
+                    c.launches[XYZB_STAGE_PROJECT] += 1;
+                }
+            }
+        }
+        cudaEvent_t e1 = clk.mark();
+        clk.span(XYZB_STAGE_PROJECT, e0, e1);
+        c.bytes[XYZB_STAGE_PROJECT] += nb * (xy && unbiased ? 8 * M * p : ceil_div(M * p, 8)) + nb * p * sizeof(K);
+        // ---- sort ----
+        K* kb[2] = {ds->keys[0].as<K>(), ds->keys[1].as<K>()};
+        u32* vb[2] = {ds->vals[0].as<u32>(), ds->vals[1].as<u32>()};
+        const int res = rsort::sort_segments<K>(kb, vb, nb, p, bits, ds->hist.as<u32>(), st,
+                                                &c.launches[XYZB_STAGE_SORT]);
+        cudaEvent_t e2 = clk.mark();
+        clk.span(XYZB_STAGE_SORT, e1, e2);
+        c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((bits + 7) / 8);
+        // ---- join + guard + work scan ----
+        XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
+        XYZB_CUDA(cudaMemsetAsync(ds->nblocks.p, 0, 4, st));
+        {
+            dim3 g(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
+            kern::join<K><<<g, 256, 0, st>>>(kb[res], p, ds->xorc.as<K>(), ds->blocks.as<kern::Block>(),
+                                             ds->bwork.as<u64>(), ds->nblocks.as<u32>(), ds->tot.as<u64>());
+            XYZB_LAUNCH_CHECK();
+        }
+        kern::guard_blocks<<<kSMs * 4, 256, 0, st>>>(ds->blocks.as<kern::Block>(), ds->bwork.as<u64>(),
+                                                     ds->nblocks.as<u32>(), ds->tot.as<u64>(), c.guard, rid,
+                                                     ds->verified.as<u64>());
+        XYZB_LAUNCH_CHECK();
+        kern::book_runs<<<static_cast<u32>(ceil_div(nb, 256)), 256, 0, st>>>(static_cast<u32>(nb), ds->tot.as<u64>(),
+                                                                             rid, ds->enumerated.as<u64>());
+        XYZB_LAUNCH_CHECK();
+        scan::exclusive<u64>(ds->bwork.as<u64>(), ds->nblocks.as<u32>(), ds->work_off.as<u64>(), ds->partial.as<u64>(),
+                             st, &c.launches[XYZB_STAGE_JOIN]);
+        c.launches[XYZB_STAGE_JOIN] += 3;
+        cudaEvent_t e3 = clk.mark();
+        clk.span(XYZB_STAGE_JOIN, e2, e3);
+        c.bytes[XYZB_STAGE_JOIN] += nb * p * (sizeof(K) + 16);
+        // ---- verify ----
+        kern::VerifyArgs A;
+        A.blocks = ds->blocks.as<kern::Block>();
+        A.work_off = ds->work_off.as<u64>();
+        A.nblocks = ds->nblocks.as<u32>();
+        A.sv = vb[res];
+        A.S = p;
+        A.rid = rid;
+        A.run_sign = rsign;
+        A.p = p;
+        A.hits = ds->hits.as<kern::DevHit>();
+        A.hit_count = ds->hit_count.as<u32>();
+        A.hit_cap = ds->hit_cap;
+        const u32 vgrid = kSMs * 8;
+        if (!xy && c.mode == XYZB_MODE_BINARY) {
+            const u64 lanes = ds->Wp / 2;  // ulonglong2 per column
+            int G = 1;
+            while (G < 32 && u64(G) < lanes) G <<= 1;
+            const int nit = static_cast<int>(ceil_div(lanes, G));
+            const u64* X = ds->Xc.as<u64>();
+            const u32 Wp = static_cast<u32>(ds->Wp);
+            const u64* Y = ds->yk_bits.as<u64>();
+            const u32 n32 = static_cast<u32>(c.n);
+#define XYZB_VB(GG, NN) kern::verify_binary<GG, NN><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar)
+            switch (G * 16 + std::min(nit, 5)) {
+                case 1 * 16 + 1: XYZB_VB(1, 1); break;
+                case 2 * 16 + 1: XYZB_VB(2, 1); break;
+                case 4 * 16 + 1: XYZB_VB(4, 1); break;
+                case 8 * 16 + 1: XYZB_VB(8, 1); break;
+                case 16 * 16 + 1: XYZB_VB(16, 1); break;
+                case 32 * 16 + 1: XYZB_VB(32, 1); break;
+                case 32 * 16 + 2: XYZB_VB(32, 2); break;
+                case 32 * 16 + 3: XYZB_VB(32, 3); break;
+                case 32 * 16 + 4: XYZB_VB(32, 4); break;
+                default: XYZB_VB(32, 0); break;
+            }
+#undef XYZB_VB
+        } else if (c.mode == XYZB_MODE_CONTINUOUS_Y) {
+            kern::verify_weighted<32><<<vgrid, 256, 0, st>>>(A, ds->Xc.as<u64>(), static_cast<u32>(ds->Wp),
+                                                             ds->spos.as<u64>(), ds->sneg.as<u64>(),
+                                                             ds->wabs.as<double>(), c.norm, c.gamma);
+        } else if (unbiased) {
+            kern::verify_real<32, true><<<vgrid, 256, 0, st>>>(A, ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(),
+                                                              c.norm, c.gamma);
+        } else {
+            kern::verify_real<32, false><<<vgrid, 256, 0, st>>>(A, ds->Xc32.as<float>(), ds->n4,
+                                                               ds->yreal.as<double>(), c.norm, c.gamma);
+        }
+        XYZB_LAUNCH_CHECK();
+        c.launches[XYZB_STAGE_VERIFY] += 1;
+        cudaEvent_t e4 = clk.mark();
+        clk.span(XYZB_STAGE_VERIFY, e3, e4);
+        c.verify_spans.push_back({e3, e4});
+    }
+}
+
+// Keep the first occurrence of each (min, max, sign), order by (run, A.5),
+// rank for top-K; copy the report arrays to the host.
+void merge_hits(SearchCtx& c, u32 H, u32 rmax, std::vector<xyzb_hit>& hits_out, std::vector<u64>& order_out,
+                std::vector<u64>& topk_out) {
+    xyzb_dataset* ds = c.ds;
+    cudaStream_t st = ds->stream;
+    hits_out.clear();
+    order_out.clear();
+    topk_out.clear();
+    if (H == 0) return;
+    u64& L = c.launches[XYZB_STAGE_MERGE];
+    // dedup table
+    u64 T = 64;
+    while (T < 2ull * H) T <<= 1;
+    ds->tkeys.ensure(T * 8);
+    ds->tvals.ensure(T * 8);
+    merge::fill_u64<<<grid_for(T, 256), 256, 0, st>>>(ds->tkeys.as<u64>(), T, merge::kEmpty);
+    merge::fill_u64<<<grid_for(T, 256), 256, 0, st>>>(ds->tvals.as<u64>(), T, merge::kEmpty);
+    ds->rmin.ensure(8);
+    XYZB_CUDA(cudaMemcpyAsync(ds->rmin.p, &rmax, 4, cudaMemcpyHostToDevice, st));
+    const kern::DevHit* h = ds->hits.as<kern::DevHit>();
+    merge::hash_insert<<<grid_for(H, 256), 256, 0, st>>>(h, H, ds->sign_by_rid.as<int8_t>(), ds->tkeys.as<u64>(),
+                                                          ds->tvals.as<u64>(), T - 1);
+    ds->keep.ensure(u64(H) * 4);
+    ds->kpos.ensure((u64(H) + 1) * 4);
+    merge::hash_mark<<<grid_for(H, 256), 256, 0, st>>>(h, H, ds->sign_by_rid.as<int8_t>(), ds->tkeys.as<u64>(),
+                                                        ds->tvals.as<u64>(), T - 1, ds->rmin.as<u32>(),
+                                                        ds->keep.as<u32>());
+    ds->hcount.ensure(8);
+    XYZB_CUDA(cudaMemcpyAsync(ds->hcount.p, &H, 4, cudaMemcpyHostToDevice, st));
+    scan::exclusive<u32>(ds->keep.as<u32>(), ds->hcount.as<u32>(), ds->kpos.as<u32>(),
+                         reinterpret_cast<u32*>(ds->partial.p), st, &L);
+    ds->kept.ensure(u64(H) * sizeof(kern::DevHit));
+    ds->kbufA.ensure(u64(H) * 8);
+    ds->kbufB.ensure(u64(H) * 8);
+    ds->vbufA.ensure(u64(H) * 4);
+    ds->vbufB.ensure(u64(H) * 4);
+    merge::compact<<<grid_for(H, 256), 256, 0, st>>>(h, H, ds->keep.as<u32>(), ds->kpos.as<u32>(),
+                                                      ds->kept.as<kern::DevHit>(), ds->kbufA.as<u64>());
+    L += 6;
+    u32 K = 0;
+    XYZB_CUDA(cudaMemcpyAsync(&K, ds->kpos.as<u32>() + H, 4, cudaMemcpyDeviceToHost, st));
+    XYZB_CUDA(cudaStreamSynchronize(st));
+    if (K == 0) return;
+    // order: run * p^2 + pos_first * p + pos_second
+    const long double maxo = (long double)(c.plan.sign_by_rid.size()) * (long double)c.p * (long double)c.p;
+    int obits = 1;
+    while (obits < 64 && (long double)(1ull << obits) <= maxo) ++obits;
+    ds->hist.ensure(rsort::hist_words(1, K) * 4);
+    u64* kb[2] = {ds->kbufA.as<u64>(), ds->kbufB.as<u64>()};
+    u32* vb[2] = {ds->vbufA.as<u32>(), ds->vbufB.as<u32>()};
+    const int r1 = rsort::sort_segments<u64>(kb, vb, 1, K, obits, ds->hist.as<u32>(), st, &L);
+    ds->fin.ensure(u64(K) * sizeof(xyzb_hit));
+    ds->fin_order.ensure(u64(K) * 8);
+    ds->tie.ensure(u64(K) * 8);
+    int bp = 1;
+    while (bp < 32 && (1ull << bp) < c.p) ++bp;
+    merge::gather_final<<<grid_for(K, 256), 256, 0, st>>>(ds->kept.as<kern::DevHit>(), vb[r1], K,
+                                                           ds->sign_by_rid.as<int8_t>(), c.plan.L, bp,
+                                                           ds->fin.as<xyzb_hit>(), ds->fin_order.as<u64>(),
+                                                           ds->tie.as<u64>());
+    L += 1;
+    hits_out.resize(K);
+    order_out.resize(K);
+    XYZB_CUDA(cudaMemcpyAsync(hits_out.data(), ds->fin.p, u64(K) * sizeof(xyzb_hit), cudaMemcpyDeviceToHost, st));
+    XYZB_CUDA(cudaMemcpyAsync(order_out.data(), ds->fin_order.p, u64(K) * 8, cudaMemcpyDeviceToHost, st));
+    if (c.q->top_k > 0) {
+        // A.10: stable LSD — tie key (min, max, sign) first, then strength desc
+        XYZB_CUDA(cudaMemcpyAsync(kb[0], ds->tie.p, u64(K) * 8, cudaMemcpyDeviceToDevice, st));
+        const int r2 = rsort::sort_segments<u64>(kb, vb, 1, K, 2 * bp + 1, ds->hist.as<u32>(), st, &L);
+        // tie-sorted index list lives in vb[r2]; copy it aside
+        ds->topidx.ensure(u64(K) * 12);
+        u32* tie_idx = reinterpret_cast<u32*>(ds->topidx.p);
+        XYZB_CUDA(cudaMemcpyAsync(tie_idx, vb[r2], u64(K) * 4, cudaMemcpyDeviceToDevice, st));
+        const bool bin = c.mode == XYZB_MODE_BINARY;
+        merge::primary_key<<<grid_for(K, 256), 256, 0, st>>>(ds->fin.as<xyzb_hit>(), nullptr, tie_idx, K, bin ? 1 : 0,
+                                                              static_cast<u32>(c.n), kb[0]);
+        int pbits = 64;
+        if (bin) {
+            pbits = 1;
+            while (pbits < 64 && (1ull << pbits) <= c.n) ++pbits;
+        }
+        const int r3 = rsort::sort_segments<u64>(kb, vb, 1, K, pbits, ds->hist.as<u32>(), st, &L);
+        const u64 kk = std::min<u64>(c.q->top_k, K);
+        u64* top = reinterpret_cast<u64*>(ds->tvals.p);  // reuse scratch (T >= 2H >= K)
+        merge::compose_idx<<<grid_for(kk, 256), 256, 0, st>>>(tie_idx, vb[r3], static_cast<u32>(kk), top);
+        L += 2;
+        topk_out.resize(kk);
+        XYZB_CUDA(cudaMemcpyAsync(topk_out.data(), top, kk * 8, cudaMemcpyDeviceToHost, st));
+    }
+    XYZB_CUDA(cudaStreamSynchronize(st));
+}
+
+// sample_strengths + expected_complexity (search.cpp:136-188,229-291,313-317):
+// host-drawn pairs on stream 0, device strengths, fp64 mean in draw order.
+template <class Fn>
+double estimate_complexity(SearchCtx& c, Fn&& device_strengths) {
+    const u64 p = c.p;
+    const u64 cnt = c.q->strength_sample_size ? c.q->strength_sample_size : std::min<u64>(100000, 10 * p);
+    std::mt19937_64 rng = host::make_stream(c.q->seed, 0);
+    std::uniform_int_distribution<size_t> dist(0, p - 1);
+    std::vector<u32> pairs(2 * cnt);
+    for (u64 t = 0; t < cnt; ++t) {
+        size_t j = dist(rng), k = dist(rng);
+        while (p > 1 && k == j) k = dist(rng);
+        pairs[2 * t] = static_cast<u32>(j);
+        pairs[2 * t + 1] = static_cast<u32>(k);
+    }
+    std::vector<double> s(cnt);
+    device_strengths(pairs.data(), cnt, s.data());
+    double acc = 0.0;
+    for (double v : s) acc += std::pow(v, double(c.M));
+    const double mp = acc / double(s.size());
+    const double np = double(c.n) * double(p), pd = double(p);
+    const double e1 = pd * pd * mp;
+    return np + double(c.q->l) * (double(c.M) * pd + pd * std::log(pd) + double(c.n) * e1);
+}
+
+// Pass-+1 strengths of explicit pairs on the device (estimate + primitive).
+__global__ void pair_strengths_kernel(const u32* __restrict__ pairs, u64 cnt, int mode, int unbiased,
+                                      const u64* __restrict__ Xc, u32 Wp, const u64* __restrict__ yk,
+                                      const u64* __restrict__ spos, const double* __restrict__ wabs,
+                                      const float* __restrict__ Xc32, u64 n4, const double* __restrict__ y, u32 n,
+                                      double norm, double* __restrict__ out) {
+    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= cnt) return;
+    const u32 j = pairs[2 * warp], k = pairs[2 * warp + 1];
+    if (mode == XYZB_MODE_BINARY) {
+        u32 a = 0;
+        for (u32 w = lane; w < Wp; w += 32) a += __popcll(Xc[u64(j) * Wp + w] ^ Xc[u64(k) * Wp + w] ^ yk[w]);
+        a = warp_sum(a);
+        if (lane == 0) out[warp] = double(a) / double(n);
+    } else if (mode == XYZB_MODE_CONTINUOUS_Y) {
+        double acc = 0.0;
+        for (u32 w = lane; w < Wp; w += 32) {
+            u64 m = Xc[u64(j) * Wp + w] ^ Xc[u64(k) * Wp + w] ^ spos[w];
+            while (m) {
+                const int b = __ffsll(static_cast<long long>(m)) - 1;
+                acc += wabs[u64(w) * 64 + b];
+                m &= m - 1;
+            }
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) out[warp] = acc / norm;
+    } else {
+        double acc = 0.0;
+        for (u64 i = lane; i < n4; i += 32) {
+            const float a = Xc32[u64(j) * n4 + i], b = Xc32[u64(k) * n4 + i];
+            if (unbiased) {
+                acc = fma(y[i], double(a) * double(b), acc);
+            } else {
+                const double ta = a > 0.f ? 1.0 : (a < 0.f ? -1.0 : 0.0), tb = b > 0.f ? 1.0 : (b < 0.f ? -1.0 : 0.0);
+                acc = fma(y[i], ta * tb, acc);
+            }
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) out[warp] = 0.5 + acc / (2.0 * norm);
+    }
+}
+
+void device_pair_strengths(SearchCtx& c, const u32* pairs, u64 cnt, double* out) {
+    xyzb_dataset* ds = c.ds;
+    cudaStream_t st = ds->stream;
+    if (cnt == 0) return;
+    for (u64 t = 0; t < cnt; ++t)
+        if (pairs[2 * t] >= c.p || pairs[2 * t + 1] >= c.p) throw data_error("interaction_strength: index out of range");
+    ds->pairs_dev.ensure(cnt * 8);
+    ds->strengths_dev.ensure(cnt * 8);
+    XYZB_CUDA(cudaMemcpyAsync(ds->pairs_dev.p, pairs, cnt * 8, cudaMemcpyHostToDevice, st));
+    pair_strengths_kernel<<<static_cast<u32>(ceil_div(cnt * 32, 256)), 256, 0, st>>>(
+        ds->pairs_dev.as<u32>(), cnt, c.mode, c.q->transform == XYZB_TRANSFORM_UNBIASED, ds->Xc.as<u64>(),
+        static_cast<u32>(ds->Wp), ds->yk_bits.as<u64>(), ds->spos.as<u64>(), ds->wabs.as<double>(),
+        ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(), static_cast<u32>(c.n), c.norm,
+        ds->strengths_dev.as<double>());
+    XYZB_LAUNCH_CHECK();
+    c.launches[XYZB_STAGE_ESTIMATE] += 1;
+    XYZB_CUDA(cudaMemcpyAsync(out, ds->strengths_dev.p, cnt * 8, cudaMemcpyDeviceToHost, st));
+    XYZB_CUDA(cudaStreamSynchronize(st));
+}
+
+void check_mode(const xyzb_dataset* ds, const xyzb_params* q, const xyzb_response* resp) {
+    if (q->mode == XYZB_MODE_BINARY) {
+        if (!ds->binary) throw data_error("xyz_search: real X requires continuous-XY mode");
+        if (!resp || !resp->y_sign) throw data_error("xyz_search: packed X with sign Y requires binary mode");
+    } else if (q->mode == XYZB_MODE_CONTINUOUS_Y) {
+        if (!ds->binary) throw data_error("xyz_search: real X requires continuous-XY mode");
+        if (!resp || !resp->y_real) throw data_error("xyz_search: packed X with real Y requires continuous-Y mode");
+    } else {
+        if (ds->binary) throw data_error("xyz_search: packed X with real Y requires continuous-Y mode");
+        if (!resp || !resp->y_real) throw data_error("xyz_search: real X requires continuous-XY mode");
+        if (q->transform == XYZB_TRANSFORM_UNBIASED && !ds->in_unit)
+            throw data_error(
+                "xyz_search: unbiased transform needs entries in [-1,1]; apply rescale_rows or cap_entries first");
+    }
+}
+
+void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q, const uint32_t* draws,
+               xyzb_result* out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    validate_params(q);
+    DeviceGuard dg(ds->device);
+    check_mode(ds, q, resp);
+    SearchCtx c;
+    c.ds = ds;
+    c.q = q;
+    c.mode = q->mode;
+    c.n = ds->n;
+    c.p = ds->p;
+    c.M = q->m;
+    c.gamma = q->gamma;
+    c.guard = q->max_candidates_per_rep ? q->max_candidates_per_rep : 16 * ds->p;  // search.cpp:303-304
+    c.out = out;
+    if (ds->p > 0x7fffffffull) throw data_error("xyzb: more than 2^31-1 columns");
+    if (c.mode == XYZB_MODE_BINARY) c.astar = integer_threshold(c.n, c.gamma);
+    if (q->stop_after_first_hit && (q->rep_begin || q->rep_end))
+        throw data_error("xyzb: stop_after_first_hit cannot be combined with a rep shard");
+    std::memset(out, 0, sizeof(*out));
+    ds->clock.st = ds->stream;
+    ds->clock.reset();
+    cudaEvent_t ev_start = ds->clock.mark();
+    upload_response(c, resp);
+    plan_runs(c, resp, draws);
+    cudaEvent_t ev_draw = ds->clock.mark();
+    ds->clock.span(XYZB_STAGE_DRAWS, ev_start, ev_draw);
+    c.bytes[XYZB_STAGE_DRAWS] = c.plan.rows.size() * 4 + c.plan.mt.size() * 8;
+    u32 H = 0;
+    const size_t spans0 = ds->clock.spans.size();
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        ds->clock.spans.resize(spans0);
+        if (c.M <= 32) run_batches<u32>(c); else run_batches<u64>(c);
+        XYZB_CUDA(cudaMemcpyAsync(&H, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+        XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        if (H <= ds->hit_cap) break;
+        // the hit buffer overflowed: grow and recompute (counts are exact)
+        ds->hit_cap = static_cast<u32>(std::min<u64>(0xffffffffull, u64(H) * 2));
+        std::memset(c.launches, 0, sizeof(c.launches));
+        std::memset(c.bytes, 0, sizeof(c.bytes));
+        c.verify_spans.clear();
+        if (attempt == 7) throw internal_error("xyzb: hit buffer did not converge");
+    }
+    // per-run counters (device -> host) and stop_after_first_hit truncation
+    const u64 Rall = c.plan.sign_by_rid.size();
+    std::vector<u64> enumerated(Rall), verified(Rall);
+    XYZB_CUDA(cudaMemcpyAsync(enumerated.data(), ds->enumerated.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
+    XYZB_CUDA(cudaMemcpyAsync(verified.data(), ds->verified.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
+    u32 rmax = 0xffffffffu;
+    if (q->stop_after_first_hit && H > 0) {
+        ds->rmin.ensure(8);
+        XYZB_CUDA(cudaMemsetAsync(ds->rmin.p, 0xff, 4, ds->stream));
+        merge::min_rid<<<grid_for(H, 256), 256, 0, ds->stream>>>(ds->hits.as<kern::DevHit>(), H, ds->rmin.as<u32>());
+        XYZB_LAUNCH_CHECK();
+        XYZB_CUDA(cudaMemcpyAsync(&rmax, ds->rmin.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+    }
+    cudaEvent_t ev_m0 = ds->clock.mark();
+    XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+    std::vector<xyzb_hit> hits;
+    std::vector<u64> order, topk;
+    merge_hits(c, H, rmax, hits, order, topk);
+    cudaEvent_t ev_m1 = ds->clock.mark();
+    ds->clock.span(XYZB_STAGE_MERGE, ev_m0, ev_m1);
+    // counters over executed runs (in pass/rep order)
+    u64 reps = 0, enumc = 0, aborted = 0, ver = 0;
+    for (u32 r : c.plan.rid) {
+        if (r > rmax) continue;
+        ++reps;
+        enumc += enumerated[r];
+        if (enumerated[r] > c.guard) ++aborted;
+        ver += verified[r];
+    }
+    out->repetitions_run = reps;
+    out->runs_executed = c.plan.rid.size();
+    out->candidates_enumerated = enumc;
+    out->aborted_repetitions = aborted;
+    out->verified_pairs = ver;
+    out->candidates_checked = ver;
+    out->gamma0 = std::pow(double(c.p), -1.0 / double(c.M));
+    out->m_used = c.M;
+    out->l_used = q->l;
+    if (q->estimate_complexity) {
+        cudaEvent_t e0 = ds->clock.mark();
+        out->estimated_c = estimate_complexity(c, [&](const u32* pr, u64 cnt, double* s) {
+            device_pair_strengths(c, pr, cnt, s);
+        });
+        cudaEvent_t e1 = ds->clock.mark();
+        ds->clock.span(XYZB_STAGE_ESTIMATE, e0, e1);
+    }
+    cudaEvent_t ev_end = ds->clock.mark();
+    XYZB_CUDA(cudaEventSynchronize(ev_end));
+    float ms = 0.f;
+    XYZB_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_end));
+    out->device_ms = ms;
+    for (auto& sp : ds->clock.spans) {
+        float m2 = 0.f;
+        XYZB_CUDA(cudaEventElapsedTime(&m2, sp.second.first, sp.second.second));
+        out->stage_ms[sp.first] += m2;
+    }
+    for (auto& sp : c.verify_spans) {
+        float m2 = 0.f;
+        XYZB_CUDA(cudaEventElapsedTime(&m2, sp.first, sp.second));
+        out->verify_kernel_ms += m2;
+    }
+    out->verify_launches = c.verify_spans.size();
+    // algorithmic verify bytes: 2 columns per canonical pair + Y
+    const u64 colbytes = c.mode == XYZB_MODE_CONTINUOUS_XY ? 4 * c.n : 8 * ceil_div(c.n, 64);
+    c.bytes[XYZB_STAGE_VERIFY] = ver * 2 * colbytes + colbytes;
+    u64 tl = 0;
+    for (int s = 0; s < XYZB_NUM_STAGES; ++s) {
+        out->stage_bytes[s] = c.bytes[s];
+        out->stage_launches[s] = c.launches[s];
+        tl += c.launches[s];
+    }
+    out->kernel_launches = tl;
+    // report arrays (malloc-owned, xyzb_result_free)
+    out->n_hits = hits.size();
+    out->hits = static_cast<xyzb_hit*>(std::malloc(std::max<size_t>(1, hits.size()) * sizeof(xyzb_hit)));
+    out->order_keys = static_cast<u64*>(std::malloc(std::max<size_t>(1, order.size()) * 8));
+    if (!hits.empty()) {
+        std::memcpy(out->hits, hits.data(), hits.size() * sizeof(xyzb_hit));
+        std::memcpy(out->order_keys, order.data(), order.size() * 8);
+    }
+    out->n_top_k = topk.size();
+    out->top_k = static_cast<u64*>(std::malloc(std::max<size_t>(1, topk.size()) * 8));
+    if (!topk.empty()) std::memcpy(out->top_k, topk.data(), topk.size() * 8);
+    out->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+
+// ---- generic equal-key join (equal_pairs, pair_search.cpp:26-55) ----
+
+__global__ void ep_blocks(const u64* __restrict__ sx, const u64* __restrict__ sz, u64 p, kern::Block* __restrict__ blk,
+                          u64* __restrict__ work) {
+    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const u64 v = sx[i];
+    u64 w = 0;
+    kern::Block b{0, u32(i), 0, 0, 0, 0};
+    if (i == 0 || sx[i - 1] != v) {
+        const u64 e = kern::run_end(sx, i, p, v);
+        const u64 lo = kern::lower_bound(sz, 0, p, v);
+        if (lo < p && sz[lo] == v) {
+            const u64 hi = kern::run_end(sz, lo, p, v);
+            b = {0, u32(i), u32(e - i), u32(lo), u32(hi - lo), 0};
+            w = (e - i) * (hi - lo);
+        }
+    }
+    blk[i] = b;
+    work[i] = w;
+}
+
+__global__ void ep_emit(const kern::Block* __restrict__ blk, const u64* __restrict__ off, const u32* __restrict__ vx,
+                        const u32* __restrict__ vz, u64 p, u32* __restrict__ out) {
+    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const kern::Block b = blk[i];
+    if (b.xc == 0) return;
+    u64 o = off[i];
+    for (u32 a = 0; a < b.xc; ++a)
+        for (u32 c = 0; c < b.zc; ++c, ++o) {
+            out[2 * o] = vx[b.xs + a];
+            out[2 * o + 1] = vz[b.zs + c];
+        }
+}
+
+} // namespace
+
+extern "C" int xyzb_equal_pairs(const uint64_t* x_keys, const uint64_t* z_keys, uint64_t p, int32_t device,
+                                uint32_t** pairs_jk, uint64_t* n_pairs, uint64_t* total_pairs, char* err,
+                                size_t errlen) {
+    return guarded(err, errlen, [&] {
+        *pairs_jk = nullptr;
+        *n_pairs = 0;
+        *total_pairs = 0;
+        require_device();
+        DeviceGuard dg(device);
+        if (p == 0) {
+            *pairs_jk = static_cast<uint32_t*>(std::malloc(8));
+            return;
+        }
+        if (p > 0xffffffffull) throw data_error("equal_pairs: too many keys");
+        cudaStream_t st;
+        XYZB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        struct S { cudaStream_t s; ~S() { cudaStreamDestroy(s); } } sguard{st};
+        DevBuf kb0, kb1, vb0, vb1, hist, blk, work, off, part, cnt, outp;
+        kb0.ensure(2 * p * 8);
+        kb1.ensure(2 * p * 8);
+        vb0.ensure(2 * p * 4);
+        vb1.ensure(2 * p * 4);
+        u64 maxk = 0;
+        for (u64 i = 0; i < p; ++i) maxk = std::max(maxk, std::max(x_keys[i], z_keys[i]));
+        int bits = 1;
+        while (bits < 64 && (maxk >> bits)) ++bits;
+        XYZB_CUDA(cudaMemcpyAsync(kb0.p, x_keys, p * 8, cudaMemcpyHostToDevice, st));
+        XYZB_CUDA(cudaMemcpyAsync(kb0.as<u64>() + p, z_keys, p * 8, cudaMemcpyHostToDevice, st));
+        hist.ensure(rsort::hist_words(2, p) * 4);
+        u64* kb[2] = {kb0.as<u64>(), kb1.as<u64>()};
+        u32* vb[2] = {vb0.as<u32>(), vb1.as<u32>()};
+        const int r = rsort::sort_segments<u64>(kb, vb, 2, p, bits, hist.as<u32>(), st);
+        blk.ensure(p * sizeof(kern::Block));
+        work.ensure(p * 8);
+        off.ensure((p + 1) * 8);
+        part.ensure(scan::kGrid * 8);
+        cnt.ensure(8);
+        const u32 pc = static_cast<u32>(p);
+        XYZB_CUDA(cudaMemcpyAsync(cnt.p, &pc, 4, cudaMemcpyHostToDevice, st));
+        ep_blocks<<<static_cast<u32>(ceil_div(p, 256)), 256, 0, st>>>(kb[r], kb[r] + p, p, blk.as<kern::Block>(),
+                                                                      work.as<u64>());
+        XYZB_LAUNCH_CHECK();
+        scan::exclusive<u64>(work.as<u64>(), cnt.as<u32>(), off.as<u64>(), part.as<u64>(), st);
+        u64 total = 0;
+        XYZB_CUDA(cudaMemcpyAsync(&total, off.as<u64>() + p, 8, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        outp.ensure(std::max<u64>(1, total) * 8);
+        ep_emit<<<static_cast<u32>(ceil_div(p, 256)), 256, 0, st>>>(blk.as<kern::Block>(), off.as<u64>(), vb[r],
+                                                                    vb[r] + p, p, outp.as<u32>());
+        XYZB_LAUNCH_CHECK();
+        uint32_t* host = static_cast<uint32_t*>(std::malloc(std::max<u64>(1, total) * 8));
+        XYZB_CUDA(cudaMemcpyAsync(host, outp.p, total * 8, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        *pairs_jk = host;
+        *n_pairs = total;
+        *total_pairs = total;
+    });
+}
+
+extern "C" int xyzb_project_keys(xyzb_dataset* ds, const uint32_t* draws, uint64_t n_draws, uint64_t m,
+                                 uint64_t* keys, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!ds || !ds->binary) throw data_error("project_keys: needs a binary dataset");
+        if (m == 0 || m > 64) throw data_error("project_keys: draw size outside [1,64]");
+        for (u64 t = 0; t < n_draws * m; ++t)
+            if (draws[t] >= ds->n) throw data_error("project_keys: draw index out of range");
+        if (n_draws == 0) return;
+        DeviceGuard dg(ds->device);
+        cudaStream_t st = ds->stream;
+        DevBuf rows, kout, xc, sg, yk;
+        rows.ensure(n_draws * m * 4);
+        kout.ensure(n_draws * ds->p * 8);
+        xc.ensure(n_draws * 8);
+        sg.ensure(n_draws);
+        yk.ensure(ds->Wp * 8);
+        XYZB_CUDA(cudaMemsetAsync(yk.p, 0, ds->Wp * 8, st));
+        XYZB_CUDA(cudaMemsetAsync(sg.p, 1, n_draws, st));
+        XYZB_CUDA(cudaMemcpyAsync(rows.p, draws, n_draws * m * 4, cudaMemcpyHostToDevice, st));
+        dim3 g(static_cast<u32>(ceil_div(ds->p, 256)), static_cast<u32>(n_draws));
+        kern::project_bits<u64><<<g, 256, 0, st>>>(ds->Xr.as<u32>(), ds->P32, ds->p, rows.as<u32>(), int(m),
+                                                   yk.as<u64>(), sg.as<int8_t>(), kout.as<u64>(), xc.as<u64>());
+        XYZB_LAUNCH_CHECK();
+        XYZB_CUDA(cudaMemcpyAsync(keys, kout.p, n_draws * ds->p * 8, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+extern "C" int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params,
+                                   const uint32_t* pairs_jk, uint64_t n_pairs, double* strengths, char* err,
+                                   size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!ds || !params) throw data_error("pair_strengths: null argument");
+        DeviceGuard dg(ds->device);
+        check_mode(ds, params, resp);
+        SearchCtx c;
+        c.ds = ds;
+        c.q = params;
+        c.mode = params->mode;
+        c.n = ds->n;
+        c.p = ds->p;
+        c.M = params->m;
+        c.gamma = params->gamma;
+        upload_response(c, resp);
+        device_pair_strengths(c, pairs_jk, n_pairs, strengths);
+    });
+}
+
+extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, uint64_t n_parts,
+                                  const xyzb_params* params, xyzb_result* out, char* err, size_t errlen) {
+    if (out) std::memset(out, 0, sizeof(*out));
+    return guarded(err, errlen, [&] {
+        if (!ds || !params || !out || (n_parts && !parts)) throw data_error("xyzb_merge_results: null argument");
+        if (params->stop_after_first_hit) throw data_error("xyzb: stop_after_first_hit cannot be combined with a rep shard");
+        DeviceGuard dg(ds->device);
+        SearchCtx c;
+        c.ds = ds;
+        c.q = params;
+        c.mode = params->mode;
+        c.n = ds->n;
+        c.p = ds->p;
+        c.M = params->m;
+        c.gamma = params->gamma;
+        c.plan.L = params->l;
+        c.plan.npass = params->search_negatives ? 2 : 1;
+        c.plan.sign_by_rid.resize(c.plan.npass * c.plan.L);
+        for (int ps = 0; ps < c.plan.npass; ++ps)
+            for (u64 r = 0; r < c.plan.L; ++r) c.plan.sign_by_rid[ps * c.plan.L + r] = ps == 0 ? 1 : -1;
+        const u64 Rall = c.plan.sign_by_rid.size();
+        ds->sign_by_rid.ensure(Rall);
+        XYZB_CUDA(cudaMemcpyAsync(ds->sign_by_rid.p, c.plan.sign_by_rid.data(), Rall, cudaMemcpyHostToDevice,
+                                  ds->stream));
+        std::vector<kern::DevHit> all;
+        const u64 pp = c.p * c.p;
+        for (u64 t = 0; t < n_parts; ++t) {
+            const xyzb_result& r = parts[t];
+            for (u64 i = 0; i < r.n_hits; ++i) {
+                kern::DevHit h;
+                h.order = r.order_keys[i];
+                h.s = r.hits[i].strength;
+                h.j = r.hits[i].j;
+                h.k = r.hits[i].k;
+                h.rid = static_cast<u32>(h.order / pp);
+                h.sint = -1;
+                all.push_back(h);
+            }
+            out->repetitions_run += r.repetitions_run;
+            out->runs_executed += r.runs_executed;
+            out->candidates_enumerated += r.candidates_enumerated;
+            out->aborted_repetitions += r.aborted_repetitions;
+            out->candidates_checked += r.candidates_checked;
+            out->verified_pairs += r.verified_pairs;
+            out->device_ms = std::max(out->device_ms, r.device_ms);
+            out->wall_time_s = std::max(out->wall_time_s, r.wall_time_s);
+            if (out->estimated_c == 0.0) out->estimated_c = r.estimated_c;
+            for (int s = 0; s < XYZB_NUM_STAGES; ++s) {
+                out->stage_ms[s] += r.stage_ms[s];
+                out->stage_bytes[s] += r.stage_bytes[s];
+                out->stage_launches[s] += r.stage_launches[s];
+            }
+            out->kernel_launches += r.kernel_launches;
+            out->verify_kernel_ms += r.verify_kernel_ms;
+            out->verify_launches += r.verify_launches;
+        }
+        if (all.size() > 0xffffffffull) throw internal_error("xyzb_merge_results: too many hits");
+        const u32 H = static_cast<u32>(all.size());
+        if (H > ds->hit_cap) ds->hit_cap = H;
+        ds->hits.ensure(std::max<u64>(1, all.size()) * sizeof(kern::DevHit));
+        if (H) XYZB_CUDA(cudaMemcpyAsync(ds->hits.p, all.data(), all.size() * sizeof(kern::DevHit),
+                                         cudaMemcpyHostToDevice, ds->stream));
+        ds->partial.ensure(scan::kGrid * 8);
+        std::vector<xyzb_hit> hits;
+        std::vector<u64> order, topk;
+        merge_hits(c, H, 0xffffffffu, hits, order, topk);
+        out->gamma0 = std::pow(double(c.p), -1.0 / double(c.M));
+        out->m_used = c.M;
+        out->l_used = params->l;
+        out->n_hits = hits.size();
+        out->hits = static_cast<xyzb_hit*>(std::malloc(std::max<size_t>(1, hits.size()) * sizeof(xyzb_hit)));
+        out->order_keys = static_cast<u64*>(std::malloc(std::max<size_t>(1, order.size()) * 8));
+        if (!hits.empty()) {
+            std::memcpy(out->hits, hits.data(), hits.size() * sizeof(xyzb_hit));
+            std::memcpy(out->order_keys, order.data(), order.size() * 8);
+        }
+        out->n_top_k = topk.size();
+        out->top_k = static_cast<u64*>(std::malloc(std::max<size_t>(1, topk.size()) * 8));
+        if (!topk.empty()) std::memcpy(out->top_k, topk.data(), topk.size() * 8);
+    });
+}
+
+namespace {
+} // namespace
+
+// ------------------------------------------------------------ C ABI --
+
+extern "C" {
+
+int xyzb_abi_version(void) { return XYZB_ABI_VERSION; }
+
+void xyzb_params_init(xyzb_params* q) {
+    std::memset(q, 0, sizeof(*q));
+    q->m = 8;  // SearchConfig defaults (search.hpp:18-33)
+    q->l = 1;
+    q->gamma = 0.9;
+    q->mode = XYZB_MODE_BINARY;
+    q->transform = XYZB_TRANSFORM_NONE;
+    q->search_negatives = 1;
+    q->estimate_complexity = 1;
+}
+
+int xyzb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        *out = nullptr;
+        if (!pr) throw data_error("xyzb_dataset_create: null problem");
+        if (pr->n_rows == 0 || pr->n_cols == 0) throw data_error("PackedMatrix: n_rows and n_cols must be >= 1");
+        if ((pr->x_words == nullptr) == (pr->x_real == nullptr))
+            throw data_error("xyzb_dataset_create: exactly one of x_words / x_real must be set");
+        if (pr->n_rows > 0xffffffffull) throw data_error("xyzb: more than 2^32-1 rows");
+        if (pr->x_words) {
+            // padding bits must be clear (PackedMatrix invariant, packed_matrix.hpp:10-14)
+            const u64 W = ceil_div(pr->n_rows, 64);
+            const u64 tail = pr->n_rows & 63;
+            if (tail)
+                for (u64 j = 0; j < pr->n_cols; ++j)
+                    if (pr->x_words[j * W + W - 1] >> tail)
+                        throw data_error("xyzb_dataset_create: padding bits of column " + std::to_string(j) +
+                                         " are not zero");
+        }
+        require_device();
+        std::unique_ptr<xyzb_dataset> ds(new xyzb_dataset());
+        ds->device = pr->device;
+        if (const char* e = std::getenv("XYZB_HIT_CAP"))  // tests force the hit-buffer regrow path with it
+            ds->hit_cap = static_cast<u32>(std::max<u64>(1, std::strtoull(e, nullptr, 10)));
+        DeviceGuard dg(ds->device);
+        XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+        ds->n = pr->n_rows;
+        ds->p = pr->n_cols;
+        if (pr->x_words) create_binary(ds.get(), pr); else create_real(ds.get(), pr);
+        XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        *out = ds.release();
+    });
+}
+
+void xyzb_dataset_destroy(xyzb_dataset* ds) {
+    if (!ds) return;
+    {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(ds->device);
+        cudaStreamSynchronize(ds->stream);
+        cudaStream_t st = ds->stream;
+        delete ds;
+        cudaStreamDestroy(st);
+        cudaSetDevice(prev);
+    }
+}
+
+int xyzb_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params, const uint32_t* draws,
+                xyzb_result* out, char* err, size_t errlen) {
+    if (out) std::memset(out, 0, sizeof(*out));
+    return guarded(err, errlen, [&] {
+        if (!ds || !params || !out) throw data_error("xyzb_search: null argument");
+        do_search(ds, resp, params, draws, out);
+    });
+}
+
+void xyzb_result_free(xyzb_result* r) {
+    if (!r) return;
+    std::free(r->hits);
+    std::free(r->order_keys);
+    std::free(r->top_k);
+    r->hits = nullptr;
+    r->order_keys = nullptr;
+    r->top_k = nullptr;
+}
+
+void xyzb_free(void* p) { std::free(p); }
+
+} // extern "C"

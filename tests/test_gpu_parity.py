@@ -1,0 +1,317 @@
+"""GPU parity: the CUDA engine (libxyzb.so, through its C ABI) against the
+reference's golden fixtures and the CPU restatement (oracle/liboracle.so).
+
+Bars (north_star): bit-exact keys, candidate sets, integer strengths, hit
+lists and top-K for +-1 data; strengths within 1e-5 relative for the
+continuous modes (X held in fp32 on the device), with pairs inside the
++-1e-5*gamma band of the threshold treated as don't-care.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from tests import checkers as ck
+from tests.helpers import GOLDEN, expected_hits, golden_names, load_case, report_hits
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5  # continuous modes (fp32 X on device), north_star tolerance
+
+SEARCH_CASES = [n for n in golden_names() if n.split("_")[0] in ("bin", "cfg1", "cy", "cxy")]
+
+
+def _engine():
+    import paper_1610_05108_b200 as xb
+    return xb
+
+
+def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
+    """Hit lists equal up to strength tolerance; pairs within the tolerance
+    band around gamma may be present on one side only."""
+    band = tol * gamma
+    gi = {(h[0], h[1], h[3], h[4]): h[2] for h in got}
+    wi = {(h[0], h[1], h[3], h[4]): h[2] for h in want_hits}
+    for key, s in wi.items():
+        if key in gi:
+            assert abs(gi[key] - s) <= tol * abs(s), (key, gi[key], s)
+        else:
+            assert abs(s - gamma) <= band, f"missing hit {key} s={s}"
+    for key, s in gi.items():
+        if key not in wi:
+            assert abs(s - gamma) <= band, f"extra hit {key} s={s}"
+    # order of the common hits is identical
+    common_g = [k for k in gi if k in wi]
+    common_w = [k for k in wi if k in gi]
+    assert common_g == common_w
+
+
+@pytest.mark.parametrize("name", SEARCH_CASES)
+def test_search_matches_reference_fixture(name):
+    xb = _engine()
+    x, y, cfg, z = load_case(name)
+    rep = xb.Dataset(x).search(y, cfg)
+    assert rep.repetitions_run == int(z["repetitions_run"])
+    assert rep.aborted_repetitions == int(z["aborted_repetitions"])
+    assert rep.candidates_enumerated == int(z["candidates_enumerated"])
+    assert rep.gamma0 == float(z["gamma0"])
+    if cfg.mode == "binary":
+        assert report_hits(rep) == expected_hits(z)  # bit-exact
+        assert rep.top_k == z["top_k"].tolist()
+        assert rep.estimated_c == float(z["estimated_c"])
+    else:
+        compare_continuous(report_hits(rep), expected_hits(z), cfg.gamma)
+        if cfg.estimate_complexity:
+            assert abs(rep.estimated_c - float(z["estimated_c"])) <= 1e-6 * abs(float(z["estimated_c"]))
+    # engine counter = the restatement's canonical count; >= the reference's deduplicated count
+    orc = ck.oracle_search(x, y, cfg)
+    assert rep.verified_pairs == orc.verified_pairs
+    assert rep.verified_pairs >= int(z["candidates_checked"]) or rep.aborted_repetitions > 0
+    assert rep.kernel_launches > 0
+
+
+def test_project_keys_match_reference_fixture():
+    xb = _engine()
+    z = np.load(os.path.join(GOLDEN, "projection.npz"))
+    x = xb.PackedMatrix(int(z["n"]), int(z["p"]), z["x_words"])
+    ds = xb.Dataset(x)
+    for t in range(int(z["count"])):
+        draw = z[f"draw{t}"].astype(np.uint32)
+        assert ds.project_keys(draw).tolist()[0] == z[f"keys{t}"].tolist()
+
+
+def test_project_keys_random_vs_oracle():
+    xb = _engine()
+    rng = np.random.default_rng(7)
+    for n, p in ((1, 5), (63, 70), (64, 33), (65, 129), (1000, 2000)):
+        x = ck.ref_rademacher(n, p, n + p, 1)
+        ds = xb.Dataset(x)
+        for m in (1, 8, 31, 32, 33, 64):
+            draws = rng.integers(0, n, (3, m)).astype(np.uint32)
+            assert np.array_equal(ds.project_keys(draws), ck.oracle_project_keys(x, draws))
+
+
+def test_equal_pairs_fig2_and_random():
+    xb = _engine()
+    z = np.load(os.path.join(GOLDEN, "equal_pairs_fig2.npz"))
+    pairs, total = xb.equal_pairs(z["x_keys"], z["z_keys"])
+    assert total == 7 and pairs.tolist() == z["pairs"].tolist()
+    z = np.load(os.path.join(GOLDEN, "equal_pairs_random.npz"))
+    for t in range(int(z["count"])):
+        pairs, total = xb.equal_pairs(z[f"x{t}"], z[f"z{t}"])
+        assert total == int(z[f"total{t}"]) and pairs.tolist() == z[f"pairs{t}"].tolist()
+    # edge cases (test_pair_search.cpp:56-70): disjoint, all identical, wide keys
+    pairs, total = xb.equal_pairs(np.array([1, 2, 3], np.uint64), np.array([4, 5, 6], np.uint64))
+    assert total == 0 and len(pairs) == 0
+    pairs, total = xb.equal_pairs(np.full(17, 9, np.uint64), np.full(17, 9, np.uint64))
+    assert total == 17 * 17
+    big = np.array([2**64 - 1, 2**63, 5, 2**64 - 1], np.uint64)
+    pairs, total = xb.equal_pairs(big, big[::-1].copy())
+    want, wt = ck.oracle_equal_pairs(big, big[::-1].copy())
+    assert total == wt and pairs.tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("mode", ["binary", "continuous_y", "continuous_xy_sign", "continuous_xy_unbiased"])
+def test_pair_strengths_vs_oracle(mode):
+    xb = _engine()
+    rng = np.random.default_rng(11)
+    n, p = 333, 40
+    pairs = rng.integers(0, p, (200, 2)).astype(np.uint32)
+    if mode.startswith("continuous_xy"):
+        x = ck.ref_uniform(n, p, 5, 5)
+        y = rng.normal(size=n)
+        tr = mode.split("_")[-1]
+        cfg = xb.SearchConfig(mode="continuous_xy", transform=tr)
+        want = ck.oracle_pair_strengths(x, y, 2, 1 if tr == "sign" else 2, pairs)
+        got = xb.Dataset(x).pair_strengths(y, cfg, pairs)
+        np.testing.assert_allclose(got, want, rtol=REL_TOL)
+    else:
+        x = ck.ref_rademacher(n, p, 5, 5)
+        if mode == "binary":
+            y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+            cfg = xb.SearchConfig(mode="binary")
+            want = ck.oracle_pair_strengths(x, y, 0, 0, pairs)
+            got = xb.Dataset(x).pair_strengths(y, cfg, pairs)
+            assert np.array_equal(got, want)  # exact integer arithmetic
+        else:
+            y = rng.normal(size=n)
+            y[::7] = 0.0
+            cfg = xb.SearchConfig(mode="continuous_y")
+            want = ck.oracle_pair_strengths(x, y, 1, 0, pairs)
+            got = xb.Dataset(x).pair_strengths(y, cfg, pairs)
+            np.testing.assert_allclose(got, want, rtol=1e-12)
+
+
+def test_binary_random_sweep_vs_oracle():
+    """Bit-exact hit lists over word-boundary n, M up to 64 (u64 keys), guards."""
+    xb = _engine()
+    rng = np.random.default_rng(99)
+    for t in range(24):
+        n = int(rng.choice([1, 2, 63, 64, 65, 127, 300]))
+        p = int(rng.integers(2, 160))
+        m = int(rng.choice([1, 2, 3, 5, 8, 20, 33, 40, 64]))
+        x = ck.ref_rademacher(n, p, 900 + t, 1)
+        y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        cfg = xb.SearchConfig(m=m, l=int(rng.integers(1, 6)), gamma=float(rng.choice([0.5, 0.55, 0.6, 0.75, 1.0])),
+                              seed=t, search_negatives=bool(rng.random() < 0.8),
+                              max_candidates_per_rep=int(rng.choice([0, 0, 50, p])), threads=1,
+                              strength_sample_size=int(rng.integers(1, 400)), top_k=int(rng.choice([0, 5, 1000])))
+        got = xb.Dataset(x).search(y, cfg)
+        want = ck.oracle_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, (t, msg)
+        assert (got.repetitions_run, got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs,
+                got.estimated_c, got.top_k) == (want.repetitions_run, want.aborted_repetitions,
+                                                want.candidates_enumerated, want.verified_pairs, want.estimated_c,
+                                                want.top_k), t
+
+
+def test_binary_matches_live_reference_cfg1_variants():
+    xb = _engine()
+    x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
+    ds = xb.Dataset(x)
+    for m, g in ((8, 0.55), (6, 0.6), (12, 0.52)):
+        cfg = xb.SearchConfig(m=m, l=10, gamma=g, seed=7, threads=1, top_k=10, estimate_complexity=False)
+        got, want = ds.search(y, cfg), ck.ref_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, msg
+        assert got.top_k == want.top_k
+        assert (got.candidates_enumerated, got.aborted_repetitions) == (want.candidates_enumerated,
+                                                                       want.aborted_repetitions)
+    # planted pair (5,17) 1-based is recovered
+    rep = ds.search(y, xb.SearchConfig(m=8, l=10, gamma=0.6, seed=7, top_k=10))
+    assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
+
+
+def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch):
+    """Batching and hit-buffer regrowth must not change anything (the GPU
+    analogue of test_search.cpp:275-295, hit lists independent of threads)."""
+    xb = _engine()
+    x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
+    cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=10)
+    base = xb.Dataset(x).search(y, cfg)
+    monkeypatch.setenv("XYZB_BATCH_ENTRIES", "3000")  # one run per batch
+    monkeypatch.setenv("XYZB_HIT_CAP", "7")
+    other = xb.Dataset(x).search(y, cfg)
+    assert report_hits(other) == report_hits(base)
+    assert other.top_k == base.top_k
+    assert (other.candidates_enumerated, other.verified_pairs, other.estimated_c) == (
+        base.candidates_enumerated, base.verified_pairs, base.estimated_c)
+
+
+def test_sharded_runs_merge_to_the_full_search():
+    """Run sharding (multi-GPU layout) merged through the ABI equals
+    the unsharded search, for several shard counts."""
+    import ctypes as C
+    xb = _engine()
+    x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
+    ds = xb.Dataset(x)
+    cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=25, estimate_complexity=False)
+    full = ds.search(y, cfg)
+    for G in (2, 3, 4, 10):
+        parts = []
+        bounds = [1 + (cfg.l * g) // G for g in range(G + 1)]
+        for g in range(G):
+            sub = xb.SearchConfig(**{**cfg.__dict__, "rep_begin": bounds[g], "rep_end": bounds[g + 1]})
+            parts.append(ds.search_raw(y, sub))
+        try:
+            merged = ds.merge(parts, cfg)
+        finally:
+            for r in parts:
+                ds.free_result(r)
+        assert report_hits(merged) == report_hits(full), G
+        assert merged.top_k == full.top_k
+        assert merged.candidates_enumerated == full.candidates_enumerated
+        assert merged.repetitions_run == full.repetitions_run
+
+
+def test_data_errors_like_the_reference():
+    xb = _engine()
+    x, y = ck.ref_planted(64, 12, 0, 1, 1.0, 7)
+    ds = xb.Dataset(x)
+    with pytest.raises(xb.DataError):
+        ds.search(y, xb.SearchConfig(m=0))
+    with pytest.raises(xb.DataError):
+        ds.search(y, xb.SearchConfig(m=65))
+    with pytest.raises(xb.DataError):
+        ds.search(y, xb.SearchConfig(gamma=0.0))
+    with pytest.raises(xb.DataError):
+        ds.search(y, xb.SearchConfig(l=0))
+    bad = y.copy()
+    bad[3] = 0
+    with pytest.raises(xb.DataError):
+        ds.search(bad, xb.SearchConfig())
+    with pytest.raises(xb.DataError):
+        ds.search(y, xb.SearchConfig(transform="sign"))
+    with pytest.raises(xb.DataError):
+        ds.search(np.zeros(64), xb.SearchConfig(mode="continuous_y"))
+    with pytest.raises(xb.DataError):
+        xb.xyz_search(x, y[:10], xb.SearchConfig())
+    big = xb.RealMatrix(np.full((2, 4), 2.0))
+    with pytest.raises(xb.DataError):
+        xb.Dataset(big).search(np.ones(4), xb.SearchConfig(mode="continuous_xy", transform="unbiased"))
+
+
+def test_continuous_modes_random_vs_oracle():
+    xb = _engine()
+    rng = np.random.default_rng(5)
+    for t in range(6):
+        n, p = int(rng.integers(30, 400)), int(rng.integers(5, 120))
+        if t % 2 == 0:
+            x = ck.ref_rademacher(n, p, t, 8)
+            y = rng.normal(size=n)
+            y[rng.random(n) < 0.1] = 0.0
+            cfg = xb.SearchConfig(m=int(rng.integers(2, 7)), l=4, gamma=0.56, seed=t, mode="continuous_y",
+                                  threads=1, strength_sample_size=200, top_k=9)
+        else:
+            xr = ck.ref_uniform(n, p, t, 8)
+            v = xr.values.copy()
+            v[rng.random(v.shape) < 0.05] = 0.0
+            x = xb.RealMatrix(v)
+            y = rng.normal(size=n)
+            cfg = xb.SearchConfig(m=int(rng.integers(2, 6)), l=4, gamma=0.55, seed=t, mode="continuous_xy",
+                                  transform="unbiased" if t % 4 == 1 else "sign", threads=1,
+                                  strength_sample_size=200, top_k=9)
+        got = xb.Dataset(x).search(y, cfg)
+        want = ck.oracle_search(x, y, cfg)
+        assert got.candidates_enumerated == want.candidates_enumerated, t  # keys bit-exact
+        assert got.aborted_repetitions == want.aborted_repetitions
+        compare_continuous(report_hits(got), report_hits(want), cfg.gamma)
+
+
+def test_gwas_full_size_properties():
+    """BASELINE config 2 at full size (n=4000, p=1e5, M=16, L=100): the oracle
+    cannot finish here, so check size-independent properties: every hit's
+    strength recomputed exactly on the host, the A.8 order and dedup rules,
+    top-K consistency, and shard-merge equality."""
+    from paper_1610_05108_b200 import synth
+    xb = _engine()
+    x, y, planted = synth.gwas()
+    ds = xb.Dataset(x)
+    cfg = xb.SearchConfig(m=16, l=100, gamma=0.6, seed=7, top_k=100, estimate_complexity=False)
+    rep = ds.search(y, cfg)
+    assert rep.repetitions_run == 200 and rep.runs_executed == 200
+    assert rep.verified_pairs > 0
+    # exact strengths
+    pairs = np.array([[h.j, h.k] for h in rep.hits], np.uint32).reshape(-1, 2)
+    if len(pairs):
+        xw = x.words
+        from paper_1610_05108_b200.matrix import pack_signs
+        yw = pack_signs(y)
+        agree = np.array([int(np.unpackbits((xw[j] ^ xw[k] ^ yw).view(np.uint8)).sum()) for j, k in pairs])
+        n = x.n_rows
+        for h, a in zip(rep.hits, agree):
+            s = a / n if h.sign > 0 else (n - a) / n
+            assert h.strength == s and s >= cfg.gamma
+    # dedup: one hit per (min, max, sign); order by (sign pass, rep)
+    keys = [(min(h.j, h.k), max(h.j, h.k), h.sign) for h in rep.hits]
+    assert len(keys) == len(set(keys))
+    ordr = [(0 if h.sign > 0 else 1, h.found_at_repetition) for h in rep.hits]
+    assert ordr == sorted(ordr)
+    # the strongest planted interactions are found
+    found = {(min(h.j, h.k), max(h.j, h.k)) for h in rep.hits}
+    assert len(found & {tuple(p) for p in planted.tolist()}) >= 3
+    # top-K: strength-descending with the A.10 tie-break
+    top = rep.top_hits()
+    ts = [(-h.strength, min(h.j, h.k), max(h.j, h.k), -h.sign) for h in top]
+    assert ts == sorted(ts)
