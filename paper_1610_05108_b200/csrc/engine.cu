@@ -26,6 +26,7 @@
 
 #include "../../include/xyzb.h"
 #include "common.cuh"
+#include "draws.cuh"
 #include "host_rng.hpp"
 #include "merge_kernels.cuh"
 #include "radix_sort.cuh"
@@ -133,7 +134,8 @@ struct xyzb_dataset {
     // response (per search)
     DevBuf yk_bits, spos, sneg, wabs, yreal;
     // batch scratch
-    DevBuf keys[2], vals[2], hist, blocks, bwork, work_off, partial, rows, rid, rsign, xorc, tot, nblocks;
+    DevBuf keys[2], vals[2], hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
+    DevBuf pairs, npairs;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -261,10 +263,10 @@ void create_real(xyzb_dataset* ds, const xyzb_problem* pr) {
 struct RunPlan {
     u64 L = 0;
     int npass = 1;
-    std::vector<u32> rid;       // global run ids in execution order
-    std::vector<int8_t> sign;   // per run
-    std::vector<u32> rows;      // [R][M]
-    std::vector<u64> mt;        // [R][313] (continuous-XY only)
+    std::vector<u32> rid;             // global run ids in execution order
+    std::vector<int8_t> sign;         // per run
+    std::vector<u64> stream;          // per run: make_stream stream id = offset + rep
+    std::vector<u32> rows;            // [R][M], only for caller-supplied draws
     std::vector<int8_t> sign_by_rid;  // [npass * L]
 };
 
@@ -276,6 +278,10 @@ struct SearchCtx {
     double gamma;
     u32 astar = 0;        // binary integer threshold
     double norm = 0.0;    // ||y||_1 (continuous)
+    bool weighted = false;
+    u64 item_cap = 0, nbatches = 0, pair_cap = 0;
+    u64 item_scale = 1;  // grows when a batch overflows its item buffer
+    u64 pair_scale = 1;  // grows when a batch overflows its pair list
     RunPlan plan;
     xyzb_result* out;
     u64 launches[XYZB_NUM_STAGES] = {};
@@ -293,20 +299,23 @@ u32 integer_threshold(u64 n, double gamma) {
     return static_cast<u32>(lo);
 }
 
+// Response-derived device vectors, staged through the dataset's pinned buffer
+// (asynchronous; the search synchronises before the buffer is reused).
 void upload_response(SearchCtx& c, const xyzb_response* resp) {
     xyzb_dataset* ds = c.ds;
-    const u64 n = c.n;
-    const u64 nb = ds->Wp * 64;
-    std::vector<u64> bits(ds->Wp, 0);
+    cudaStream_t st = ds->stream;
+    const u64 n = c.n, Wp = ds->Wp, nb = Wp * 64;
     if (c.mode == XYZB_MODE_BINARY) {
+        ds->h_small.ensure(Wp * 8);
+        u64* bits = ds->h_small.as<u64>();
+        std::memset(bits, 0, Wp * 8);
         for (u64 i = 0; i < n; ++i) {
             const int8_t v = resp->y_sign[i];
             if (v != 1 && v != -1) throw data_error("xyz_search: binary response must be +-1");
             if (v > 0) bits[i >> 6] |= 1ull << (i & 63);
         }
-        ds->yk_bits.ensure(ds->Wp * 8);
-        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
-        XYZB_CUDA(cudaStreamSynchronize(ds->stream));  // `bits` is pageable and local
+        ds->yk_bits.ensure(Wp * 8);
+        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits, Wp * 8, cudaMemcpyHostToDevice, st));
         return;
     }
     const double* y = resp->y_real;
@@ -314,34 +323,50 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
     for (u64 i = 0; i < n; ++i) norm += std::abs(y[i]);
     if (norm <= 0.0) throw data_error("xyz_search: zero response vector");
     c.norm = norm;
+    // WeightedSampler::from_magnitudes cumulative table (real_matrix.cpp:36-47), host fp64 in order
+    host::WeightedSampler ws(y, n);
+    c.weighted = true;
+    const u64 n4 = ds->n4 ? ds->n4 : round_up(n, 4);
+    const size_t need = n * 8 /*cum*/ + (c.mode == XYZB_MODE_CONTINUOUS_Y ? 3 * Wp * 8 + nb * 8 : n4 * 8);
+    ds->h_small.ensure(need);
+    char* hp = ds->h_small.as<char>();
+    double* cum = reinterpret_cast<double*>(hp);
+    ws.copy_cumulative(cum);
+    ds->cum.ensure(n * 8);
+    XYZB_CUDA(cudaMemcpyAsync(ds->cum.p, cum, n * 8, cudaMemcpyHostToDevice, st));
+    hp += n * 8;
     if (c.mode == XYZB_MODE_CONTINUOUS_Y) {
-        std::vector<u64> sp(ds->Wp, 0), sn(ds->Wp, 0);
-        std::vector<double> w(nb, 0.0);
+        u64* bits = reinterpret_cast<u64*>(hp);
+        u64* sp = bits + Wp;
+        u64* sn = sp + Wp;
+        double* w = reinterpret_cast<double*>(sn + Wp);
+        std::memset(hp, 0, 3 * Wp * 8 + nb * 8);
         for (u64 i = 0; i < n; ++i) {
             if (y[i] >= 0.0) bits[i >> 6] |= 1ull << (i & 63);  // y_sign for the keys (search.cpp:377-378)
             if (y[i] > 0.0) sp[i >> 6] |= 1ull << (i & 63);
             if (y[i] < 0.0) sn[i >> 6] |= 1ull << (i & 63);
             w[i] = std::abs(y[i]);
         }
-        ds->yk_bits.ensure(ds->Wp * 8);
-        ds->spos.ensure(ds->Wp * 8);
-        ds->sneg.ensure(ds->Wp * 8);
+        ds->yk_bits.ensure(Wp * 8);
+        ds->spos.ensure(Wp * 8);
+        ds->sneg.ensure(Wp * 8);
         ds->wabs.ensure(nb * 8);
-        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
-        XYZB_CUDA(cudaMemcpyAsync(ds->spos.p, sp.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
-        XYZB_CUDA(cudaMemcpyAsync(ds->sneg.p, sn.data(), ds->Wp * 8, cudaMemcpyHostToDevice, ds->stream));
-        XYZB_CUDA(cudaMemcpyAsync(ds->wabs.p, w.data(), nb * 8, cudaMemcpyHostToDevice, ds->stream));
-        XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits, Wp * 8, cudaMemcpyHostToDevice, st));
+        XYZB_CUDA(cudaMemcpyAsync(ds->spos.p, sp, Wp * 8, cudaMemcpyHostToDevice, st));
+        XYZB_CUDA(cudaMemcpyAsync(ds->sneg.p, sn, Wp * 8, cudaMemcpyHostToDevice, st));
+        XYZB_CUDA(cudaMemcpyAsync(ds->wabs.p, w, nb * 8, cudaMemcpyHostToDevice, st));
         return;
     }
-    std::vector<double> yp(ds->n4, 0.0);
-    std::copy(y, y + n, yp.begin());
-    ds->yreal.ensure(ds->n4 * 8);
-    XYZB_CUDA(cudaMemcpyAsync(ds->yreal.p, yp.data(), ds->n4 * 8, cudaMemcpyHostToDevice, ds->stream));
-    XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+    double* yp = reinterpret_cast<double*>(hp);
+    std::memset(yp, 0, n4 * 8);
+    std::copy(y, y + n, yp);
+    ds->yreal.ensure(n4 * 8);
+    XYZB_CUDA(cudaMemcpyAsync(ds->yreal.p, yp, n4 * 8, cudaMemcpyHostToDevice, st));
 }
 
-void plan_runs(SearchCtx& c, const xyzb_response* resp, const uint32_t* draws) {
+// Runs of the search in execution order (pass +1 then -1, reps ascending;
+// PassPlan stream offsets 0 and L, search.cpp:353-358).
+void plan_runs(SearchCtx& c, const uint32_t* draws) {
     const xyzb_params* q = c.q;
     RunPlan& pl = c.plan;
     pl.L = q->l;
@@ -355,31 +380,20 @@ void plan_runs(SearchCtx& c, const xyzb_response* resp, const uint32_t* draws) {
     pl.sign_by_rid.resize(pl.npass * pl.L);
     for (int ps = 0; ps < pl.npass; ++ps)
         for (u64 r = 0; r < pl.L; ++r) pl.sign_by_rid[ps * pl.L + r] = ps == 0 ? 1 : -1;
-    std::unique_ptr<host::WeightedSampler> ws;
-    if (c.mode != XYZB_MODE_BINARY) ws.reset(new host::WeightedSampler(resp->y_real, c.n));
-    const bool need_state = c.mode == XYZB_MODE_CONTINUOUS_XY &&
-                            (q->transform == XYZB_TRANSFORM_UNBIASED || c.ds->has_zero);
-    if (draws && need_state)
+    if (draws && c.mode == XYZB_MODE_CONTINUOUS_XY)
         throw data_error("xyzb: caller-supplied draws are not supported for continuous-XY transforms");
     for (int ps = 0; ps < pl.npass; ++ps) {
-        const u64 offset = ps == 0 ? 0 : q->l;  // PassPlan stream offsets (search.cpp:353-358)
+        const u64 offset = ps == 0 ? 0 : q->l;
         for (u64 rep = rb; rep < re; ++rep) {
             pl.rid.push_back(static_cast<u32>(ps * pl.L + rep - 1));
             pl.sign.push_back(ps == 0 ? 1 : -1);
-            const size_t at = pl.rows.size();
-            pl.rows.resize(at + c.M);
+            pl.stream.push_back(offset + rep);
             if (draws) {
+                const size_t at = pl.rows.size();
+                pl.rows.resize(at + c.M);
                 std::memcpy(pl.rows.data() + at, draws + ((ps * pl.L) + rep - 1) * c.M, c.M * 4);
                 for (u64 s = 0; s < c.M; ++s)
                     if (pl.rows[at + s] >= c.n) throw data_error("project_keys: draw index out of range");
-            } else {
-                std::mt19937_64 rng = host::make_stream(q->seed, offset + rep);
-                host::draw_rows(c.n, c.M, ws.get(), rng, pl.rows.data() + at);
-                if (need_state) {
-                    const size_t st = pl.mt.size();
-                    pl.mt.resize(st + 313);
-                    host::export_state(rng, pl.mt.data() + st);
-                }
             }
         }
     }
@@ -392,19 +406,18 @@ void run_batches(SearchCtx& c) {
     const u64 p = c.p, M = c.M;
     const u64 R = c.plan.rid.size();
     const u64 Rall = c.plan.sign_by_rid.size();
+    StageClock& clk = ds->clock;
     // per-search counters
     ds->enumerated.ensure(Rall * 8);
     ds->verified.ensure(Rall * 8);
     ds->sign_by_rid.ensure(Rall);
     XYZB_CUDA(cudaMemsetAsync(ds->enumerated.p, 0, Rall * 8, st));
     XYZB_CUDA(cudaMemsetAsync(ds->verified.p, 0, Rall * 8, st));
-    XYZB_CUDA(cudaMemcpyAsync(ds->sign_by_rid.p, c.plan.sign_by_rid.data(), Rall, cudaMemcpyHostToDevice, st));
     ds->hit_count.ensure(8);
     XYZB_CUDA(cudaMemsetAsync(ds->hit_count.p, 0, 4, st));
     ds->hits.ensure(sizeof(kern::DevHit) * u64(ds->hit_cap));
-    // batch size: keep B*p entries under 2^26 (about 64 B of scratch each)
-    // XYZB_BATCH_ENTRIES overrides the budget (tests force multi-batch runs with it)
-    u64 budget = u64(1) << 26;
+    // batch size: B*p entries under the budget (about 64 B of scratch each)
+    u64 budget = u64(1) << 26;  // XYZB_BATCH_ENTRIES overrides (tests force multi-batch runs with it)
     if (const char* e = std::getenv("XYZB_BATCH_ENTRIES")) budget = std::max<u64>(1, std::strtoull(e, nullptr, 10));
     const u64 B = std::max<u64>(1, std::min<u64>(R, budget / std::max<u64>(p, 1)));
     const u64 cap = B * p;
@@ -413,43 +426,81 @@ void run_batches(SearchCtx& c) {
         ds->vals[i].ensure(cap * 4);
     }
     ds->hist.ensure(rsort::hist_words(B, p) * 4);
-    ds->blocks.ensure(cap * sizeof(kern::Block));
-    ds->bwork.ensure(cap * 8);
-    ds->work_off.ensure((cap + 1) * 8);
-    ds->partial.ensure(scan::kGrid * 8);
-    ds->rows.ensure(R * M * 4);
+    u64 item_cap = std::min<u64>(0xffffffffull, B * (2 * p + 1) * c.item_scale);
+    if (const char* e = std::getenv("XYZB_ITEM_CAP"))  // tests force the item-buffer regrow path with it
+        item_cap = std::min<u64>(item_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.item_scale);
+    if (item_cap > 0xffffffffull) throw internal_error("xyzb: batch too large for 32-bit item indices");
+    ds->items.ensure(item_cap * sizeof(kern::Item));
+    const bool use_table = M <= u64(kern::kTableBits) && (B << M) <= (u64(1) << 28);
+    if (use_table) ds->table.ensure((B << M) * 4);
+    // host plan -> pinned -> device
+    const bool host_rows = !c.plan.rows.empty();
+    const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 64;
+    ds->h_rows.ensure(hbytes);
+    char* hp = ds->h_rows.as<char>();
+    std::memcpy(hp, c.plan.rid.data(), R * 4);
+    std::memcpy(hp + R * 4, c.plan.sign.data(), R);
+    std::memcpy(hp + R * 5, c.plan.stream.data(), R * 8);
+    if (host_rows) std::memcpy(hp + R * 13, c.plan.rows.data(), R * M * 4);
+    XYZB_CUDA(cudaMemcpyAsync(ds->sign_by_rid.p, c.plan.sign_by_rid.data(), Rall, cudaMemcpyHostToDevice, st));
     ds->rid.ensure(R * 4);
     ds->rsign.ensure(R);
-    ds->xorc.ensure(B * sizeof(K));
-    ds->tot.ensure(B * 8);
-    ds->nblocks.ensure(16);
-    // host plan -> pinned -> device (one copy of all rows / ids / signs)
-    ds->h_rows.ensure(R * M * 4 + R * 4 + R + 64);
-    char* hp = ds->h_rows.as<char>();
-    std::memcpy(hp, c.plan.rows.data(), R * M * 4);
-    std::memcpy(hp + R * M * 4, c.plan.rid.data(), R * 4);
-    std::memcpy(hp + R * M * 4 + R * 4, c.plan.sign.data(), R);
-    XYZB_CUDA(cudaMemcpyAsync(ds->rows.p, hp, R * M * 4, cudaMemcpyHostToDevice, st));
-    XYZB_CUDA(cudaMemcpyAsync(ds->rid.p, hp + R * M * 4, R * 4, cudaMemcpyHostToDevice, st));
-    XYZB_CUDA(cudaMemcpyAsync(ds->rsign.p, hp + R * M * 4 + R * 4, R, cudaMemcpyHostToDevice, st));
+    ds->streams.ensure(R * 8);
+    ds->rows.ensure(R * M * 4);
+    XYZB_CUDA(cudaMemcpyAsync(ds->rid.p, hp, R * 4, cudaMemcpyHostToDevice, st));
+    XYZB_CUDA(cudaMemcpyAsync(ds->rsign.p, hp + R * 4, R, cudaMemcpyHostToDevice, st));
+    XYZB_CUDA(cudaMemcpyAsync(ds->streams.p, hp + R * 5, R * 8, cudaMemcpyHostToDevice, st));
     const bool xy = c.mode == XYZB_MODE_CONTINUOUS_XY;
     const bool unbiased = xy && c.q->transform == XYZB_TRANSFORM_UNBIASED;
     const bool coins = xy && !unbiased && ds->has_zero;
-    if (unbiased || coins) {
-        ds->mt_state.ensure(R * 313 * 8);
-        ds->h_state.ensure(R * 313 * 8);
-        std::memcpy(ds->h_state.p, c.plan.mt.data(), R * 313 * 8);
-        XYZB_CUDA(cudaMemcpyAsync(ds->mt_state.p, ds->h_state.p, R * 313 * 8, cudaMemcpyHostToDevice, st));
+    if (unbiased || coins) ds->mt_state.ensure(R * 313 * 8);
+    // ---- draws (device RNG, or the caller's rows) ----
+    cudaEvent_t ed0 = clk.mark();
+    if (host_rows) {
+        XYZB_CUDA(cudaMemcpyAsync(ds->rows.p, hp + R * 13, R * M * 4, cudaMemcpyHostToDevice, st));
+    } else {
+        draws::draw_runs<<<static_cast<u32>(R), 32, 0, st>>>(
+            static_cast<u32>(R), ds->streams.as<u64>(), c.q->seed, c.n, int(M), c.weighted ? ds->cum.as<double>() : nullptr,
+            ds->rows.as<u32>(), (unbiased || coins) ? ds->mt_state.as<u64>() : nullptr);
+        XYZB_LAUNCH_CHECK();
+        c.launches[XYZB_STAGE_DRAWS] += 1;
     }
+    clk.span(XYZB_STAGE_DRAWS, ed0, clk.mark());
+    c.bytes[XYZB_STAGE_DRAWS] += R * M * 4;
     if (coins) {
         ds->zmask.ensure(cap * sizeof(K));
         ds->zcount.ensure(cap * 4);
         ds->zoff.ensure((cap + 1) * 4);
         ds->zcnt_n.ensure(8);
+        ds->partial.ensure(scan::kGrid * 8);
     }
-    StageClock& clk = ds->clock;
+    ds->xorc.ensure(B * sizeof(K));
+    ds->tot.ensure(B * 8);
+    ds->work_run.ensure(B * 8);
+    const u64 nbatches = ceil_div(R, B);
+    ds->nblocks.ensure(nbatches * 4);  // items per batch (may exceed item_cap: regrow)
+    XYZB_CUDA(cudaMemsetAsync(ds->nblocks.p, 0, nbatches * 4, st));
+    c.item_cap = item_cap;
+    c.nbatches = nbatches;
+    const bool pair_path = c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128 && !std::getenv("XYZB_VERIFY_U");
+    if (pair_path) {
+        c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, 4 * B * p) * c.pair_scale);
+        if (const char* e = std::getenv("XYZB_PAIR_CAP"))  // tests force the pair-list regrow path with it
+            c.pair_cap = std::min<u64>(c.pair_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.pair_scale);
+        ds->pairs.ensure(c.pair_cap * sizeof(kern::PairRec));
+        ds->npairs.ensure(nbatches * 4);
+        XYZB_CUDA(cudaMemsetAsync(ds->npairs.p, 0, nbatches * 4, st));
+    }
+    const u32 hmax_bin = [&] {
+        const u64 lanes = ds->Wp / 2;
+        int G = 1;
+        while (G < 32 && u64(G) < lanes) G <<= 1;
+        const u64 nit = ceil_div(lanes, G);
+        return nit == 1 ? 8u : nit == 2 ? 4u : nit <= 4 ? 2u : 8u;
+    }();
+    const u32 hmax = c.mode == XYZB_MODE_BINARY ? hmax_bin : 8u;
     const int bits = static_cast<int>(M);
-    for (u64 b0 = 0; b0 < R; b0 += B) {
+    for (u64 b0 = 0, batch_idx = 0; b0 < R; b0 += B, ++batch_idx) {
         const u64 nb = std::min(B, R - b0);
         const u32* rows = ds->rows.as<u32>() + b0 * M;
         const u32* rid = ds->rid.as<u32>() + b0;
@@ -468,7 +519,7 @@ void run_batches(SearchCtx& c) {
                                                                                  rsign, static_cast<u32>(nb),
                                                                                  ds->xorc.as<K>());
             XYZB_LAUNCH_CHECK();
-            const u64* mts = ds->mt_state.as<u64>() + b0 * 313;
+            const u64* mts = (unbiased || coins) ? ds->mt_state.as<u64>() + b0 * 313 : nullptr;
             if (unbiased) {
                 XYZB_CUDA(cudaMemsetAsync(k0, 0, nb * p * sizeof(K), st));
                 real::unbiased_keys<K><<<static_cast<u32>(nb), real::kMtThreads, 0, st>>>(mts, p, rows, int(M),
@@ -483,9 +534,9 @@ void run_batches(SearchCtx& c) {
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_PROJECT] += 2;
                 if (coins) {
-                    const u32 cnt = static_cast<u32>(nb * p);
-                    XYZB_CUDA(cudaMemcpyAsync(ds->zcnt_n.p, &cnt, 4, cudaMemcpyHostToDevice, st));
-                    XYZB_CUDA(cudaStreamSynchronize(st));  // cnt is a host local
+                    u32* cnt = reinterpret_cast<u32*>(hp + hbytes - 16);
+                    *cnt = static_cast<u32>(nb * p);
+                    XYZB_CUDA(cudaMemcpyAsync(ds->zcnt_n.p, cnt, 4, cudaMemcpyHostToDevice, st));
                     scan::exclusive<u32>(ds->zcount.as<u32>(), ds->zcnt_n.as<u32>(), ds->zoff.as<u32>(),
                                          reinterpret_cast<u32*>(ds->partial.p), st, &c.launches[XYZB_STAGE_PROJECT]);
                     real::sign_coins<K><<<static_cast<u32>(nb), real::kMtThreads, 0, st>>>(
@@ -497,7 +548,7 @@ void run_batches(SearchCtx& c) {
         }
         cudaEvent_t e1 = clk.mark();
         clk.span(XYZB_STAGE_PROJECT, e0, e1);
-        c.bytes[XYZB_STAGE_PROJECT] += nb * (xy && unbiased ? 8 * M * p : ceil_div(M * p, 8)) + nb * p * sizeof(K);
+        c.bytes[XYZB_STAGE_PROJECT] += nb * (unbiased ? 8 * M * p : ceil_div(M * p, 8)) + nb * p * sizeof(K);
         // ---- sort ----
         K* kb[2] = {ds->keys[0].as<K>(), ds->keys[1].as<K>()};
         u32* vb[2] = {ds->vals[0].as<u32>(), ds->vals[1].as<u32>()};
@@ -506,33 +557,39 @@ void run_batches(SearchCtx& c) {
         cudaEvent_t e2 = clk.mark();
         clk.span(XYZB_STAGE_SORT, e1, e2);
         c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((bits + 7) / 8);
-        // ---- join + guard + work scan ----
+        // ---- join (+ guard bookkeeping) ----
         XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
-        XYZB_CUDA(cudaMemsetAsync(ds->nblocks.p, 0, 4, st));
-        {
-            dim3 g(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
-            kern::join<K><<<g, 256, 0, st>>>(kb[res], p, ds->xorc.as<K>(), ds->blocks.as<kern::Block>(),
-                                             ds->bwork.as<u64>(), ds->nblocks.as<u32>(), ds->tot.as<u64>());
+        XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
+        dim3 gj(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
+        if (use_table) {
+            kern::head_table<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->table.as<u32>());
             XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_JOIN] += 1;
         }
-        kern::guard_blocks<<<kSMs * 4, 256, 0, st>>>(ds->blocks.as<kern::Block>(), ds->bwork.as<u64>(),
-                                                     ds->nblocks.as<u32>(), ds->tot.as<u64>(), c.guard, rid,
-                                                     ds->verified.as<u64>());
+        const u32* tbl = use_table ? ds->table.as<u32>() : nullptr;
+        kern::join_count<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(),
+                                                ds->work_run.as<u64>());
         XYZB_LAUNCH_CHECK();
-        kern::book_runs<<<static_cast<u32>(ceil_div(nb, 256)), 256, 0, st>>>(static_cast<u32>(nb), ds->tot.as<u64>(),
-                                                                             rid, ds->enumerated.as<u64>());
+        u32* nitems = ds->nblocks.as<u32>() + batch_idx;
+        kern::join_emit<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(), c.guard,
+                                               hmax, ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
+                                               pair_path ? ds->npairs.as<u32>() + batch_idx : nullptr);
         XYZB_LAUNCH_CHECK();
-        scan::exclusive<u64>(ds->bwork.as<u64>(), ds->nblocks.as<u32>(), ds->work_off.as<u64>(), ds->partial.as<u64>(),
-                             st, &c.launches[XYZB_STAGE_JOIN]);
+        kern::book_runs<<<static_cast<u32>(ceil_div(nb, 256)), 256, 0, st>>>(
+            static_cast<u32>(nb), ds->tot.as<u64>(), ds->work_run.as<u64>(), c.guard, rid, ds->enumerated.as<u64>(),
+            ds->verified.as<u64>());
+        XYZB_LAUNCH_CHECK();
         c.launches[XYZB_STAGE_JOIN] += 3;
         cudaEvent_t e3 = clk.mark();
         clk.span(XYZB_STAGE_JOIN, e2, e3);
-        c.bytes[XYZB_STAGE_JOIN] += nb * p * (sizeof(K) + 16);
+        c.bytes[XYZB_STAGE_JOIN] += nb * p * (sizeof(K) + 8);
         // ---- verify ----
         kern::VerifyArgs A;
-        A.blocks = ds->blocks.as<kern::Block>();
-        A.work_off = ds->work_off.as<u64>();
-        A.nblocks = ds->nblocks.as<u32>();
+        A.items = ds->items.as<kern::Item>();
+        A.nitems = nitems;
+        A.item_cap = static_cast<u32>(item_cap);
+        A.tot = ds->tot.as<u64>();
+        A.guard = c.guard;
         A.sv = vb[res];
         A.S = p;
         A.rid = rid;
@@ -542,7 +599,44 @@ void run_batches(SearchCtx& c) {
         A.hit_count = ds->hit_count.as<u32>();
         A.hit_cap = ds->hit_cap;
         const u32 vgrid = kSMs * 8;
-        if (!xy && c.mode == XYZB_MODE_BINARY) {
+        if (pair_path) {
+            u32* np = ds->npairs.as<u32>() + batch_idx;
+            kern::expand_pairs<<<vgrid, 256, 0, st>>>(A.items, A.nitems, A.item_cap, p, ds->pairs.as<kern::PairRec>(),
+                                                      static_cast<u32>(c.pair_cap));
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_JOIN] += 1;
+            const u64 W2 = ds->Wp / 2;
+            int G = 1;
+            while (G < 32 && u64(G) * 4 < W2) G <<= 1;
+            const int nit = static_cast<int>(ceil_div(W2, G));
+            const auto* PR = ds->pairs.as<kern::PairRec>();
+            const u32 pc = static_cast<u32>(c.pair_cap);
+            const u64* X = ds->Xc.as<u64>();
+            const u32 Wp = static_cast<u32>(ds->Wp);
+            const u64* Y = ds->yk_bits.as<u64>();
+            const u32 n32 = static_cast<u32>(c.n);
+            cudaEvent_t ev0 = clk.mark();
+            clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
+#define XYZB_VP(GG, NN) kern::verify_pairs_binary<GG, NN><<<vgrid, 256, 0, st>>>(A, PR, np, pc, X, Wp, Y, n32, c.astar)
+#define XYZB_VP4(GG) \
+    switch (nit) { case 1: XYZB_VP(GG, 1); break; case 2: XYZB_VP(GG, 2); break; case 3: XYZB_VP(GG, 3); break; default: XYZB_VP(GG, 4); }
+            switch (G) {
+                case 1: XYZB_VP4(1); break;
+                case 2: XYZB_VP4(2); break;
+                case 4: XYZB_VP4(4); break;
+                case 8: XYZB_VP4(8); break;
+                case 16: XYZB_VP4(16); break;
+                default: XYZB_VP4(32); break;
+            }
+#undef XYZB_VP4
+#undef XYZB_VP
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_VERIFY] += 1;
+            cudaEvent_t ev1 = clk.mark();
+            clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
+            c.verify_spans.push_back({ev0, ev1});
+            continue;
+        } else if (c.mode == XYZB_MODE_BINARY) {
             const u64 lanes = ds->Wp / 2;  // ulonglong2 per column
             int G = 1;
             while (G < 32 && u64(G) < lanes) G <<= 1;
@@ -551,30 +645,41 @@ void run_batches(SearchCtx& c) {
             const u32 Wp = static_cast<u32>(ds->Wp);
             const u64* Y = ds->yk_bits.as<u64>();
             const u32 n32 = static_cast<u32>(c.n);
-#define XYZB_VB(GG, NN) kern::verify_binary<GG, NN><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar)
+#define XYZB_VB(GG, NN, HH) kern::verify_binary<GG, NN, HH><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar)
             switch (G * 16 + std::min(nit, 5)) {
-                case 1 * 16 + 1: XYZB_VB(1, 1); break;
-                case 2 * 16 + 1: XYZB_VB(2, 1); break;
-                case 4 * 16 + 1: XYZB_VB(4, 1); break;
-                case 8 * 16 + 1: XYZB_VB(8, 1); break;
-                case 16 * 16 + 1: XYZB_VB(16, 1); break;
-                case 32 * 16 + 1: XYZB_VB(32, 1); break;
-                case 32 * 16 + 2: XYZB_VB(32, 2); break;
-                case 32 * 16 + 3: XYZB_VB(32, 3); break;
-                case 32 * 16 + 4: XYZB_VB(32, 4); break;
-                default: XYZB_VB(32, 0); break;
+                case 1 * 16 + 1: XYZB_VB(1, 1, 8); break;
+                case 2 * 16 + 1: XYZB_VB(2, 1, 8); break;
+                case 4 * 16 + 1: XYZB_VB(4, 1, 8); break;
+                case 8 * 16 + 1: XYZB_VB(8, 1, 8); break;
+                case 16 * 16 + 1: XYZB_VB(16, 1, 8); break;
+                case 32 * 16 + 1:
+                    if (const char* e = std::getenv("XYZB_VERIFY_U"); e && std::atoi(e) == 2)
+                        kern::verify_binary_w32<2><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar);
+                    else if (e && std::atoi(e) == 0)
+                        XYZB_VB(32, 1, 8);
+                    else
+                        kern::verify_binary_w32<4><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar);
+                    break;
+                case 32 * 16 + 2: XYZB_VB(32, 2, 4); break;
+                case 32 * 16 + 3: XYZB_VB(32, 3, 2); break;
+                case 32 * 16 + 4: XYZB_VB(32, 4, 2); break;
+                default: {
+                    kern::BinaryStrength f{X, Wp, Y, static_cast<u32>(c.n), c.astar};
+                    kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
+                    break;
+                }
             }
 #undef XYZB_VB
         } else if (c.mode == XYZB_MODE_CONTINUOUS_Y) {
-            kern::verify_weighted<32><<<vgrid, 256, 0, st>>>(A, ds->Xc.as<u64>(), static_cast<u32>(ds->Wp),
-                                                             ds->spos.as<u64>(), ds->sneg.as<u64>(),
-                                                             ds->wabs.as<double>(), c.norm, c.gamma);
+            kern::WeightedStrength f{ds->Xc.as<u64>(), static_cast<u32>(ds->Wp), ds->spos.as<u64>(), ds->sneg.as<u64>(),
+                                     ds->wabs.as<double>(), c.norm, c.gamma};
+            kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
         } else if (unbiased) {
-            kern::verify_real<32, true><<<vgrid, 256, 0, st>>>(A, ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(),
-                                                              c.norm, c.gamma);
+            kern::RealStrength<true> f{ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(), c.norm, c.gamma};
+            kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
         } else {
-            kern::verify_real<32, false><<<vgrid, 256, 0, st>>>(A, ds->Xc32.as<float>(), ds->n4,
-                                                               ds->yreal.as<double>(), c.norm, c.gamma);
+            kern::RealStrength<false> f{ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(), c.norm, c.gamma};
+            kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
         }
         XYZB_LAUNCH_CHECK();
         c.launches[XYZB_STAGE_VERIFY] += 1;
@@ -613,6 +718,7 @@ void merge_hits(SearchCtx& c, u32 H, u32 rmax, std::vector<xyzb_hit>& hits_out, 
                                                         ds->tvals.as<u64>(), T - 1, ds->rmin.as<u32>(),
                                                         ds->keep.as<u32>());
     ds->hcount.ensure(8);
+    ds->partial.ensure(scan::kGrid * 8);
     XYZB_CUDA(cudaMemcpyAsync(ds->hcount.p, &H, 4, cudaMemcpyHostToDevice, st));
     scan::exclusive<u32>(ds->keep.as<u32>(), ds->hcount.as<u32>(), ds->kpos.as<u32>(),
                          reinterpret_cast<u32*>(ds->partial.p), st, &L);
@@ -806,20 +912,37 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     ds->clock.reset();
     cudaEvent_t ev_start = ds->clock.mark();
     upload_response(c, resp);
-    plan_runs(c, resp, draws);
+    plan_runs(c, draws);
     cudaEvent_t ev_draw = ds->clock.mark();
-    ds->clock.span(XYZB_STAGE_DRAWS, ev_start, ev_draw);
-    c.bytes[XYZB_STAGE_DRAWS] = c.plan.rows.size() * 4 + c.plan.mt.size() * 8;
+    ds->clock.span(XYZB_STAGE_OTHER, ev_start, ev_draw);
     u32 H = 0;
     const size_t spans0 = ds->clock.spans.size();
     for (int attempt = 0; attempt < 8; ++attempt) {
         ds->clock.spans.resize(spans0);
         if (c.M <= 32) run_batches<u32>(c); else run_batches<u64>(c);
         XYZB_CUDA(cudaMemcpyAsync(&H, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+        std::vector<u32> nitems(c.nbatches);
+        XYZB_CUDA(cudaMemcpyAsync(nitems.data(), ds->nblocks.p, c.nbatches * 4, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
-        if (H <= ds->hit_cap) break;
-        // the hit buffer overflowed: grow and recompute (counts are exact)
-        ds->hit_cap = static_cast<u32>(std::min<u64>(0xffffffffull, u64(H) * 2));
+        const u64 need = nitems.empty() ? 0 : *std::max_element(nitems.begin(), nitems.end());
+        u64 pneed = 0;
+        if (c.pair_cap) {
+            std::vector<u32> np(c.nbatches);
+            XYZB_CUDA(cudaMemcpy(np.data(), ds->npairs.p, c.nbatches * 4, cudaMemcpyDeviceToHost));
+            pneed = *std::max_element(np.begin(), np.end());
+            if (pneed > c.pair_cap) {
+                if (c.pair_cap == 0xffffffffull) throw internal_error("xyzb: candidate pairs exceed 2^32 in one batch");
+                c.pair_scale *= std::max<u64>(2, ceil_div(pneed, c.pair_cap));
+            }
+        }
+        if (H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) break;
+        // a buffer overflowed (the counters kept counting): grow and recompute
+        if (H > ds->hit_cap) ds->hit_cap = static_cast<u32>(std::min<u64>(0xffffffffull, u64(H) * 2));
+        if (need > c.item_cap) {
+            if (c.item_cap == 0xffffffffull) throw internal_error("xyzb: work items exceed 2^32 in one batch");
+            c.item_scale *= std::max<u64>(2, ceil_div(need, c.item_cap));
+        }
+
         std::memset(c.launches, 0, sizeof(c.launches));
         std::memset(c.bytes, 0, sizeof(c.bytes));
         c.verify_spans.clear();
@@ -914,19 +1037,23 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
 
 // ---- generic equal-key join (equal_pairs, pair_search.cpp:26-55) ----
 
-__global__ void ep_blocks(const u64* __restrict__ sx, const u64* __restrict__ sz, u64 p, kern::Block* __restrict__ blk,
+struct EpBlock {
+    u32 xs, xc, zs, zc;
+};
+
+__global__ void ep_blocks(const u64* __restrict__ sx, const u64* __restrict__ sz, u64 p, EpBlock* __restrict__ blk,
                           u64* __restrict__ work) {
     const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= p) return;
     const u64 v = sx[i];
     u64 w = 0;
-    kern::Block b{0, u32(i), 0, 0, 0, 0};
+    EpBlock b{u32(i), 0, 0, 0};
     if (i == 0 || sx[i - 1] != v) {
         const u64 e = kern::run_end(sx, i, p, v);
         const u64 lo = kern::lower_bound(sz, 0, p, v);
         if (lo < p && sz[lo] == v) {
             const u64 hi = kern::run_end(sz, lo, p, v);
-            b = {0, u32(i), u32(e - i), u32(lo), u32(hi - lo), 0};
+            b = {u32(i), u32(e - i), u32(lo), u32(hi - lo)};
             w = (e - i) * (hi - lo);
         }
     }
@@ -934,11 +1061,11 @@ __global__ void ep_blocks(const u64* __restrict__ sx, const u64* __restrict__ sz
     work[i] = w;
 }
 
-__global__ void ep_emit(const kern::Block* __restrict__ blk, const u64* __restrict__ off, const u32* __restrict__ vx,
+__global__ void ep_emit(const EpBlock* __restrict__ blk, const u64* __restrict__ off, const u32* __restrict__ vx,
                         const u32* __restrict__ vz, u64 p, u32* __restrict__ out) {
     const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= p) return;
-    const kern::Block b = blk[i];
+    const EpBlock b = blk[i];
     if (b.xc == 0) return;
     u64 o = off[i];
     for (u32 a = 0; a < b.xc; ++a)
@@ -982,14 +1109,14 @@ extern "C" int xyzb_equal_pairs(const uint64_t* x_keys, const uint64_t* z_keys, 
         u64* kb[2] = {kb0.as<u64>(), kb1.as<u64>()};
         u32* vb[2] = {vb0.as<u32>(), vb1.as<u32>()};
         const int r = rsort::sort_segments<u64>(kb, vb, 2, p, bits, hist.as<u32>(), st);
-        blk.ensure(p * sizeof(kern::Block));
+        blk.ensure(p * sizeof(EpBlock));
         work.ensure(p * 8);
         off.ensure((p + 1) * 8);
         part.ensure(scan::kGrid * 8);
         cnt.ensure(8);
         const u32 pc = static_cast<u32>(p);
         XYZB_CUDA(cudaMemcpyAsync(cnt.p, &pc, 4, cudaMemcpyHostToDevice, st));
-        ep_blocks<<<static_cast<u32>(ceil_div(p, 256)), 256, 0, st>>>(kb[r], kb[r] + p, p, blk.as<kern::Block>(),
+        ep_blocks<<<static_cast<u32>(ceil_div(p, 256)), 256, 0, st>>>(kb[r], kb[r] + p, p, blk.as<EpBlock>(),
                                                                       work.as<u64>());
         XYZB_LAUNCH_CHECK();
         scan::exclusive<u64>(work.as<u64>(), cnt.as<u32>(), off.as<u64>(), part.as<u64>(), st);
@@ -997,7 +1124,7 @@ extern "C" int xyzb_equal_pairs(const uint64_t* x_keys, const uint64_t* z_keys, 
         XYZB_CUDA(cudaMemcpyAsync(&total, off.as<u64>() + p, 8, cudaMemcpyDeviceToHost, st));
         XYZB_CUDA(cudaStreamSynchronize(st));
         outp.ensure(std::max<u64>(1, total) * 8);
-        ep_emit<<<static_cast<u32>(ceil_div(p, 256)), 256, 0, st>>>(blk.as<kern::Block>(), off.as<u64>(), vb[r],
+        ep_emit<<<static_cast<u32>(ceil_div(p, 256)), 256, 0, st>>>(blk.as<EpBlock>(), off.as<u64>(), vb[r],
                                                                     vb[r] + p, p, outp.as<u32>());
         XYZB_LAUNCH_CHECK();
         uint32_t* host = static_cast<uint32_t*>(std::malloc(std::max<u64>(1, total) * 8));

@@ -69,6 +69,7 @@ public:
         const size_t pos = static_cast<size_t>(std::upper_bound(cum_.begin(), cum_.end(), u) - cum_.begin());
         return std::min(pos, cum_.size() - 1);
     }
+    void copy_cumulative(double* out) const { std::copy(cum_.begin(), cum_.end(), out); }
 
 private:
     std::vector<double> cum_;

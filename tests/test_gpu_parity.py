@@ -192,6 +192,8 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch):
     base = xb.Dataset(x).search(y, cfg)
     monkeypatch.setenv("XYZB_BATCH_ENTRIES", "3000")  # one run per batch
     monkeypatch.setenv("XYZB_HIT_CAP", "7")
+    monkeypatch.setenv("XYZB_ITEM_CAP", "5")
+    monkeypatch.setenv("XYZB_PAIR_CAP", "100")
     other = xb.Dataset(x).search(y, cfg)
     assert report_hits(other) == report_hits(base)
     assert other.top_k == base.top_k
