@@ -135,7 +135,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal;
     // batch scratch
     DevBuf keys[2], vals[2], hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs;
+    DevBuf pairs, npairs, bcnt, bend, bsize;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -435,7 +435,7 @@ void run_batches(SearchCtx& c) {
     if (use_table) ds->table.ensure((B << M) * 4);
     // host plan -> pinned -> device
     const bool host_rows = !c.plan.rows.empty();
-    const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 64;
+    const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 96;
     ds->h_rows.ensure(hbytes);
     char* hp = ds->h_rows.as<char>();
     std::memcpy(hp, c.plan.rid.data(), R * 4);
@@ -482,7 +482,7 @@ void run_batches(SearchCtx& c) {
     XYZB_CUDA(cudaMemsetAsync(ds->nblocks.p, 0, nbatches * 4, st));
     c.item_cap = item_cap;
     c.nbatches = nbatches;
-    const bool pair_path = c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128 && !std::getenv("XYZB_VERIFY_U");
+    const bool pair_path = c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128;
     if (pair_path) {
         c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, 4 * B * p) * c.pair_scale);
         if (const char* e = std::getenv("XYZB_PAIR_CAP"))  // tests force the pair-list regrow path with it
@@ -491,14 +491,18 @@ void run_batches(SearchCtx& c) {
         ds->npairs.ensure(nbatches * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->npairs.p, 0, nbatches * 4, st));
     }
-    const u32 hmax_bin = [&] {
-        const u64 lanes = ds->Wp / 2;
-        int G = 1;
-        while (G < 32 && u64(G) < lanes) G <<= 1;
-        const u64 nit = ceil_div(lanes, G);
-        return nit == 1 ? 8u : nit == 2 ? 4u : nit <= 4 ? 2u : 8u;
-    }();
-    const u32 hmax = c.mode == XYZB_MODE_BINARY ? hmax_bin : 8u;
+    const u32 hmax = 8u;  // held columns per item (pair expansion chunks)
+    // grouping: counting sort into 2^M buckets when that table is small,
+    // else the segmented radix sort (XYZB_GROUPING=sort forces the latter)
+    const char* gsel = std::getenv("XYZB_GROUPING");
+    const bool buckets = M <= u64(kern::kTableBits) && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
+                         !(gsel && std::string(gsel) == "sort");
+    if (buckets) {
+        ds->bcnt.ensure((B << M) * 4);
+        ds->bend.ensure(((B << M) + 1) * 4);
+        ds->bsize.ensure(8);
+        ds->partial.ensure(scan::kGrid * 8);
+    }
     const int bits = static_cast<int>(M);
     for (u64 b0 = 0, batch_idx = 0; b0 < R; b0 += B, ++batch_idx) {
         const u64 nb = std::min(B, R - b0);
@@ -509,11 +513,13 @@ void run_batches(SearchCtx& c) {
         cudaEvent_t e0 = clk.mark();
         // ---- project ----
         if (!xy) {
-            dim3 g(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
-            kern::project_bits<K><<<g, 256, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), ds->yk_bits.as<u64>(),
-                                                     rsign, k0, ds->xorc.as<K>());
+            dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
+            kern::project_bits_t<K><<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), k0);
             XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_PROJECT] += 1;
+            kern::ykey_xorc<K><<<static_cast<u32>(ceil_div(nb, 128)), 128, 0, st>>>(
+                rows, int(M), ds->yk_bits.as<u64>(), rsign, static_cast<u32>(nb), ds->xorc.as<K>());
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_PROJECT] += 2;
         } else {
             real::resp_xorc<K><<<static_cast<u32>(ceil_div(nb, 128)), 128, 0, st>>>(rows, int(M), ds->yreal.as<double>(),
                                                                                  rsign, static_cast<u32>(nb),
@@ -549,37 +555,76 @@ void run_batches(SearchCtx& c) {
         cudaEvent_t e1 = clk.mark();
         clk.span(XYZB_STAGE_PROJECT, e0, e1);
         c.bytes[XYZB_STAGE_PROJECT] += nb * (unbiased ? 8 * M * p : ceil_div(M * p, 8)) + nb * p * sizeof(K);
-        // ---- sort ----
         K* kb[2] = {ds->keys[0].as<K>(), ds->keys[1].as<K>()};
         u32* vb[2] = {ds->vals[0].as<u32>(), ds->vals[1].as<u32>()};
-        const int res = rsort::sort_segments<K>(kb, vb, nb, p, bits, ds->hist.as<u32>(), st,
-                                                &c.launches[XYZB_STAGE_SORT]);
-        cudaEvent_t e2 = clk.mark();
-        clk.span(XYZB_STAGE_SORT, e1, e2);
-        c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((bits + 7) / 8);
-        // ---- join (+ guard bookkeeping) ----
-        XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
-        XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
-        dim3 gj(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
-        if (use_table) {
-            kern::head_table<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->table.as<u32>());
-            XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_JOIN] += 1;
-        }
-        const u32* tbl = use_table ? ds->table.as<u32>() : nullptr;
-        kern::join_count<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(),
-                                                ds->work_run.as<u64>());
-        XYZB_LAUNCH_CHECK();
         u32* nitems = ds->nblocks.as<u32>() + batch_idx;
-        kern::join_emit<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(), c.guard,
-                                               hmax, ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
-                                               pair_path ? ds->npairs.as<u32>() + batch_idx : nullptr);
-        XYZB_LAUNCH_CHECK();
+        u32* npairs_b = pair_path ? ds->npairs.as<u32>() + batch_idx : nullptr;
+        const u32* sv = nullptr;
+        cudaEvent_t e2;
+        if (buckets) {
+            // ---- group: counting sort into 2^M buckets per run ----
+            const u64 nbk = nb << M;
+            XYZB_CUDA(cudaMemsetAsync(ds->bcnt.p, 0, nbk * 4, st));
+            dim3 gp(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
+            kern::bucket_count<K><<<gp, 256, 0, st>>>(k0, p, int(M), ds->bcnt.as<u32>());
+            XYZB_LAUNCH_CHECK();
+            u32* hn = reinterpret_cast<u32*>(hp + hbytes - 32);
+            *hn = static_cast<u32>(nbk);
+            XYZB_CUDA(cudaMemcpyAsync(ds->bsize.p, hn, 4, cudaMemcpyHostToDevice, st));
+            scan::exclusive<u32>(ds->bcnt.as<u32>(), ds->bsize.as<u32>(), ds->bend.as<u32>(),
+                                 reinterpret_cast<u32*>(ds->partial.p), st, &c.launches[XYZB_STAGE_SORT]);
+            kern::bucket_scatter<K><<<gp, 256, 0, st>>>(k0, p, int(M), ds->bend.as<u32>(), vb[0]);
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_SORT] += 2;
+            sv = vb[0];
+            e2 = clk.mark();
+            clk.span(XYZB_STAGE_SORT, e1, e2);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4) + nbk * 12;
+            // ---- join (+ guard bookkeeping) ----
+            XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
+            XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
+            dim3 gb(static_cast<u32>(ceil_div(u64(1) << M, 256)), static_cast<u32>(nb));
+            kern::bucket_join_count<K><<<gb, 256, 0, st>>>(ds->bcnt.as<u32>(), int(M), ds->xorc.as<K>(), p,
+                                                           ds->tot.as<u64>(), ds->work_run.as<u64>());
+            XYZB_LAUNCH_CHECK();
+            kern::bucket_join_emit<K><<<gb, 256, 0, st>>>(ds->bcnt.as<u32>(), ds->bend.as<u32>(), int(M), ds->xorc.as<K>(),
+                                                          p, ds->tot.as<u64>(), c.guard, hmax, ds->items.as<kern::Item>(),
+                                                          nitems, static_cast<u32>(item_cap), npairs_b,
+                                                          ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_JOIN] += 2;
+        } else {
+            // ---- sort ----
+            const int res = rsort::sort_segments<K>(kb, vb, nb, p, bits, ds->hist.as<u32>(), st,
+                                                    &c.launches[XYZB_STAGE_SORT]);
+            e2 = clk.mark();
+            clk.span(XYZB_STAGE_SORT, e1, e2);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((bits + 7) / 8);
+            sv = vb[res];
+            // ---- join (+ guard bookkeeping) ----
+            XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
+            XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
+            dim3 gj(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
+            if (use_table) {
+                kern::head_table<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->table.as<u32>());
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_JOIN] += 1;
+            }
+            const u32* tbl = use_table ? ds->table.as<u32>() : nullptr;
+            kern::join_count<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(),
+                                                    ds->work_run.as<u64>());
+            XYZB_LAUNCH_CHECK();
+            kern::join_emit<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(), c.guard,
+                                                   hmax, ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
+                                                   npairs_b, ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_JOIN] += 2;
+        }
         kern::book_runs<<<static_cast<u32>(ceil_div(nb, 256)), 256, 0, st>>>(
             static_cast<u32>(nb), ds->tot.as<u64>(), ds->work_run.as<u64>(), c.guard, rid, ds->enumerated.as<u64>(),
             ds->verified.as<u64>());
         XYZB_LAUNCH_CHECK();
-        c.launches[XYZB_STAGE_JOIN] += 3;
+        c.launches[XYZB_STAGE_JOIN] += 1;
         cudaEvent_t e3 = clk.mark();
         clk.span(XYZB_STAGE_JOIN, e2, e3);
         c.bytes[XYZB_STAGE_JOIN] += nb * p * (sizeof(K) + 8);
@@ -590,8 +635,13 @@ void run_batches(SearchCtx& c) {
         A.item_cap = static_cast<u32>(item_cap);
         A.tot = ds->tot.as<u64>();
         A.guard = c.guard;
-        A.sv = vb[res];
+        A.sv = sv;
         A.S = p;
+        A.bend = buckets ? ds->bend.as<u32>() : nullptr;
+        A.bcnt = buckets ? ds->bcnt.as<u32>() : nullptr;
+        A.keys = k0;
+        A.M = int(M);
+        A.key64 = sizeof(K) == 8;
         A.rid = rid;
         A.run_sign = rsign;
         A.p = p;
@@ -636,40 +686,10 @@ void run_batches(SearchCtx& c) {
             clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
             c.verify_spans.push_back({ev0, ev1});
             continue;
-        } else if (c.mode == XYZB_MODE_BINARY) {
-            const u64 lanes = ds->Wp / 2;  // ulonglong2 per column
-            int G = 1;
-            while (G < 32 && u64(G) < lanes) G <<= 1;
-            const int nit = static_cast<int>(ceil_div(lanes, G));
-            const u64* X = ds->Xc.as<u64>();
-            const u32 Wp = static_cast<u32>(ds->Wp);
-            const u64* Y = ds->yk_bits.as<u64>();
-            const u32 n32 = static_cast<u32>(c.n);
-#define XYZB_VB(GG, NN, HH) kern::verify_binary<GG, NN, HH><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar)
-            switch (G * 16 + std::min(nit, 5)) {
-                case 1 * 16 + 1: XYZB_VB(1, 1, 8); break;
-                case 2 * 16 + 1: XYZB_VB(2, 1, 8); break;
-                case 4 * 16 + 1: XYZB_VB(4, 1, 8); break;
-                case 8 * 16 + 1: XYZB_VB(8, 1, 8); break;
-                case 16 * 16 + 1: XYZB_VB(16, 1, 8); break;
-                case 32 * 16 + 1:
-                    if (const char* e = std::getenv("XYZB_VERIFY_U"); e && std::atoi(e) == 2)
-                        kern::verify_binary_w32<2><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar);
-                    else if (e && std::atoi(e) == 0)
-                        XYZB_VB(32, 1, 8);
-                    else
-                        kern::verify_binary_w32<4><<<vgrid, 256, 0, st>>>(A, X, Wp, Y, n32, c.astar);
-                    break;
-                case 32 * 16 + 2: XYZB_VB(32, 2, 4); break;
-                case 32 * 16 + 3: XYZB_VB(32, 3, 2); break;
-                case 32 * 16 + 4: XYZB_VB(32, 4, 2); break;
-                default: {
-                    kern::BinaryStrength f{X, Wp, Y, static_cast<u32>(c.n), c.astar};
-                    kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
-                    break;
-                }
-            }
-#undef XYZB_VB
+        } else if (c.mode == XYZB_MODE_BINARY) {  // long columns (n > 8192): warp per pair
+            kern::BinaryStrength f{ds->Xc.as<u64>(), static_cast<u32>(ds->Wp), ds->yk_bits.as<u64>(),
+                                   static_cast<u32>(c.n), c.astar};
+            kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
         } else if (c.mode == XYZB_MODE_CONTINUOUS_Y) {
             kern::WeightedStrength f{ds->Xc.as<u64>(), static_cast<u32>(ds->Wp), ds->spos.as<u64>(), ds->sneg.as<u64>(),
                                      ds->wabs.as<double>(), c.norm, c.gamma};

@@ -42,6 +42,15 @@ struct Item {
     u32 pad;
 };
 
+// One canonical candidate of the pair-list path: batch-global sorted
+// positions of the x side and the z side (x side first; diagonal blocks are
+// re-oriented by column index at hit time), the batch-local run, and the
+// block flags.
+struct PairRec {
+    u32 pa, pb, run, pad;
+};
+constexpr u64 kInlinePairs = 32;  // blocks up to this many pairs are expanded by join_emit
+
 // ---------------------------------------------------------------- layout --
 
 // Xc: u64 [p][Wp] column-major words -> Xr: u32 [n][P32] row planes, bit
@@ -114,6 +123,86 @@ __global__ void __launch_bounds__(256) project_bits(const u32* __restrict__ Xr, 
             xorc[b] = run_sign[b] > 0 ? K(~ykk & mask) : ykk;
         }
     }
+}
+
+// In-register 32 x 32 bit transpose, LSB-first: afterwards a[c] bit s equals
+// the original a[s] bit c (5 butterfly stages, 80 swaps).
+__device__ __forceinline__ void transpose32(u32 (&a)[32]) {
+#pragma unroll
+    for (int j = 16, m = 0x0000ffff; j != 0; j >>= 1, m ^= (m << j)) {
+#pragma unroll
+        for (int k = 0; k < 32; k = ((k | j) + 1) & ~j) {
+            const u32 t = ((a[k] >> j) ^ a[k | j]) & u32(m);
+            a[k] ^= t << j;
+            a[k | j] ^= t;
+        }
+    }
+}
+
+// Keys for one run from the row planes, 32 columns per thread: the M
+// row-plane words of the thread's 32 columns are loaded with coalesced 128 B
+// warp requests (one per sampled row), then bit-transposed so word c becomes
+// the key of column c (key bit s = X[row_s, c]).
+template <class K>
+__global__ void __launch_bounds__(128) project_bits_t(const u32* __restrict__ Xr, u64 P32, u64 p,
+                                                      const u32* __restrict__ rows, int M, K* __restrict__ keys) {
+    __shared__ u32 srow[64];
+    const u64 b = blockIdx.y;
+    if (threadIdx.x < M) srow[threadIdx.x] = rows[b * M + threadIdx.x];
+    __syncthreads();
+    const u64 word = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (word >= P32) return;
+    const u64 col0 = word * 32;
+    const u32 ncol = u32(minu(32, p - col0));
+    u32* out = reinterpret_cast<u32*>(keys + b * p + col0);
+    constexpr int halves = sizeof(K) / 4;
+#pragma unroll
+    for (int half = 0; half < halves; ++half) {
+        if (half * 32 >= M) {
+            if (halves == 2)
+                for (u32 c = 0; c < ncol; ++c) out[2 * c + 1] = 0u;
+            break;
+        }
+        u32 a[32];
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+            const int ss = half * 32 + s;
+            a[s] = ss < M ? __ldg(Xr + u64(srow[ss]) * P32 + word) : 0u;
+        }
+        transpose32(a);
+        if (halves == 1) {
+            if (ncol == 32 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+                uint4* o4 = reinterpret_cast<uint4*>(out);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) o4[c] = make_uint4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (u32(c) < ncol) out[c] = a[c];
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (u32(c) < ncol) out[2 * c + half] = a[c];
+        }
+    }
+}
+
+// Per-run XOR constant c from the response bits at the sampled rows (A.3):
+// z+ = ~(x ^ y) & mask = x ^ (~y & mask); z- = x ^ y.
+template <class K>
+__global__ void ykey_xorc(const u32* __restrict__ rows, int M, const u64* __restrict__ ykey_bits,
+                          const int8_t* __restrict__ run_sign, u32 B, K* __restrict__ xorc) {
+    const u32 b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    u64 yk = 0;
+    for (int s = 0; s < M; ++s) {
+        const u32 r = rows[u64(b) * M + s];
+        yk |= ((ykey_bits[r >> 6] >> (r & 63)) & 1ull) << s;
+    }
+    const K mask = key_mask<K>(M);
+    const K ykk = K(yk) & mask;
+    xorc[b] = run_sign[b] > 0 ? K(~ykk & mask) : ykk;
 }
 
 // ------------------------------------------------------------------ join --
@@ -238,30 +327,25 @@ __global__ void __launch_bounds__(256) join_count(const K* __restrict__ sk, u64 
     }
 }
 
-// Pass 2: canonical work items of the runs the guard keeps. Item t of a block:
-// held chunk t / nsc (<= hmax columns), streamed chunk t % nsc (<=
-// kStreamChunk columns), so one big group cannot serialise on one team. The
-// item counter keeps counting past `item_cap` so the host can regrow.
-template <class K>
-__global__ void __launch_bounds__(256) join_emit(const K* __restrict__ sk, u64 S, int M, const K* __restrict__ xorc,
-                                                 const u32* __restrict__ table, const u64* __restrict__ tot,
-                                                 u64 guard, u32 hmax, Item* __restrict__ items,
-                                                 u32* __restrict__ nitems, u32 item_cap,
-                                                 u32* __restrict__ npairs) {
-    const u32 b = blockIdx.y;
-    const bool aborted = tot[b] > guard;
-    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
-    HeadBlock hb;
-    if (!aborted) hb = head_block(sk + u64(b) * S, i, S, M, xorc[b], table, b);
+// Emit the canonical work items of one block (per thread; warp-aggregated
+// slot reservation). Item t of a block: held chunk t / nsc (<= hmax
+// columns), streamed chunk t % nsc (<= kStreamChunk columns), so one big
+// group cannot serialise on one team. Counters keep counting past the
+// capacities so the host can regrow.
+__device__ __forceinline__ void emit_items(const HeadBlock& hb, u32 b, u32 hmax, Item* __restrict__ items,
+                                           u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs,
+                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S) {
     u32 nsc = 1, nemit = 0;
-    if (hb.work) {
+    // pair-list path: small blocks write their pairs right here (no item)
+    const bool inline_pairs = npairs != nullptr && hb.work != 0 && hb.work <= kInlinePairs;
+    if (hb.work && !inline_pairs) {
         const bool diag = hb.flags & 2u;
         const u32 slen = diag ? hb.hc - 1 : hb.sc;
         const u32 hlen = diag ? hb.hc - 1 : hb.hc;  // the last diagonal column has no later partner
         nsc = (slen + kStreamChunk - 1) / kStreamChunk;
         nemit = (hlen + hmax - 1) / hmax * nsc;
     }
-    // candidate pairs of this head (the diagonal counts only later positions)
+    // candidate pairs of this block (the diagonal counts only later positions)
     const u32 npair = u32(hb.work);
     u32 incl = nemit, pincl = npair;
     const int lane = threadIdx.x & 31;
@@ -274,16 +358,48 @@ __global__ void __launch_bounds__(256) join_emit(const K* __restrict__ sk, u64 S
             pincl += t2;
         }
     }
-    const u32 wtot = __shfl_sync(0xffffffffu, incl, 31);
-    const u32 ptot = __shfl_sync(0xffffffffu, pincl, 31);
-    u32 base = 0, pbase = 0;
-    if (lane == 31 && wtot) {
-        base = atomicAdd(nitems, wtot);
-        if (npairs) pbase = atomicAdd(npairs, ptot);
+    // CTA-level aggregation: one atomic per counter per CTA (a single global
+    // counter hit once per warp serialises at the L2 slice)
+    __shared__ u32 s_items[33], s_pairs[33];
+    const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 31) {
+        s_items[wid] = incl;
+        s_pairs[wid] = pincl;
     }
-    base = __shfl_sync(0xffffffffu, base, 31) + incl - nemit;
-    u32 poff = __shfl_sync(0xffffffffu, pbase, 31) + pincl - npair;  // this head's first pair slot
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u32 ti = 0, tp = 0;
+        for (int w = 0; w < nw; ++w) {
+            const u32 a = s_items[w], c = s_pairs[w];
+            s_items[w] = ti;
+            s_pairs[w] = tp;
+            ti += a;
+            tp += c;
+        }
+        s_items[32] = ti ? atomicAdd(nitems, ti) : 0u;
+        s_pairs[32] = (npairs && tp) ? atomicAdd(npairs, tp) : 0u;
+    }
+    __syncthreads();
+    const u32 base = s_items[32] + s_items[wid] + incl - nemit;
+    u32 poff = s_pairs[32] + s_pairs[wid] + pincl - npair;  // this block's first pair slot
     const bool diag = hb.flags & 2u;
+    if (inline_pairs) {
+        const bool first_held = diag || (hb.flags & 1u);
+        const u64 off = u64(b) * S;
+        for (u32 h = 0; h < hb.hc; ++h) {
+            const u32 hpos = hb.hs + h;
+            for (u32 q = diag ? h + 1 : 0; q < hb.sc; ++q, ++poff) {
+                if (poff >= pair_cap) continue;
+                const u32 spos = hb.ss + q;
+                PairRec r;
+                r.pa = u32(off + (first_held ? hpos : spos));
+                r.pb = u32(off + (first_held ? spos : hpos));
+                r.run = b;
+                r.pad = hb.flags;
+                pairs[poff] = r;
+            }
+        }
+    }
     const u32 sbeg = diag ? hb.hs + 1 : hb.ss;
     const u32 slen = diag ? hb.hc - 1 : hb.sc;
     for (u32 t = 0; t < nemit; ++t) {
@@ -310,6 +426,138 @@ __global__ void __launch_bounds__(256) join_emit(const K* __restrict__ sk, u64 S
             poff += hcnt * it.sc;
         }
     }
+}
+
+// Pass 2 (sorted keys): canonical work items of the runs the guard keeps.
+template <class K>
+__global__ void __launch_bounds__(256) join_emit(const K* __restrict__ sk, u64 S, int M, const K* __restrict__ xorc,
+                                                 const u32* __restrict__ table, const u64* __restrict__ tot,
+                                                 u64 guard, u32 hmax, Item* __restrict__ items,
+                                                 u32* __restrict__ nitems, u32 item_cap,
+                                                 u32* __restrict__ npairs, PairRec* __restrict__ pairs,
+                                                 u32 pair_cap) {
+    const u32 b = blockIdx.y;
+    const bool aborted = tot[b] > guard;
+    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    HeadBlock hb;
+    if (!aborted) hb = head_block(sk + u64(b) * S, i, S, M, xorc[b], table, b);
+    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S);
+}
+
+// ------------------------------------------------- bucket grouping path --
+//
+// For M <= kTableBits with 2^M comparable to p, a counting sort replaces the
+// radix sort: per-run bucket counts (one warp-aggregated atomic per distinct
+// key in a warp), one global exclusive scan over [B][2^M] (run b's entries
+// land in [b*p, (b+1)*p) because every run has exactly p columns), and a
+// scatter. The order inside a bucket is not stable; the stable (key, index)
+// position the reference order needs is recomputed for hits only (a rank
+// inside the bucket), so order keys are identical to the sorted path.
+
+template <class K>
+__global__ void __launch_bounds__(256) bucket_count(const K* __restrict__ keys, u64 p, int M, u32* __restrict__ cnt) {
+    const u64 b = blockIdx.y;
+    const u64 j = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = j < p;
+    const u32 active = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const u64 v = u64(keys[b * p + j]);
+    const u32 peers = __match_any_sync(active, static_cast<unsigned long long>(v));
+    if ((peers & lanemask_lt()) == 0) atomicAdd(cnt + (b << M) + v, __popc(peers));
+}
+
+// cursor: exclusive scan of the counts (global positions); ends as the
+// bucket end. grouped[pos] = column index.
+template <class K>
+__global__ void __launch_bounds__(256) bucket_scatter(const K* __restrict__ keys, u64 p, int M, u32* __restrict__ cursor,
+                                                      u32* __restrict__ grouped) {
+    const u64 b = blockIdx.y;
+    const u64 j = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = j < p;
+    const u32 active = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const u64 v = u64(keys[b * p + j]);
+    const u32 peers = __match_any_sync(active, static_cast<unsigned long long>(v));
+    const int leader = __ffs(peers) - 1;
+    u32 base = 0;
+    if ((threadIdx.x & 31) == leader) base = atomicAdd(cursor + (b << M) + v, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    grouped[base + __popc(peers & lanemask_lt())] = u32(j);
+}
+
+// The block owned by bucket v of run b (positions local to the run).
+__device__ __forceinline__ HeadBlock bucket_block(const u32* __restrict__ cnt, const u32* __restrict__ end, u64 b,
+                                                  int M, u64 v, u64 c, u64 p) {
+    HeadBlock hb;
+    const u64 base = b << M;
+    const u64 cv = cnt[base + v];
+    if (cv == 0) return hb;
+    const u64 v2 = v ^ c;
+    if (v2 == v) {
+        hb.pairs = cv * cv;
+        if (cv >= 2) {
+            const u32 beg = end ? u32(end[base + v] - cv - b * p) : 0u;
+            hb.work = cv * (cv - 1) / 2;
+            hb.hs = beg;
+            hb.hc = u32(cv);
+            hb.ss = beg;
+            hb.sc = u32(cv);
+            hb.flags = 3u;
+        }
+    } else if (v2 > v) {
+        const u64 c2 = cnt[base + v2];
+        if (c2) {
+            hb.pairs = 2 * cv * c2;
+            hb.work = cv * c2;
+            const u32 bx = end ? u32(end[base + v] - cv - b * p) : 0u;
+            const u32 bz = end ? u32(end[base + v2] - c2 - b * p) : 0u;
+            if (cv <= c2) {
+                hb.hs = bx; hb.hc = u32(cv); hb.ss = bz; hb.sc = u32(c2); hb.flags = 1u;
+            } else {
+                hb.hs = bz; hb.hc = u32(c2); hb.ss = bx; hb.sc = u32(cv); hb.flags = 0u;
+            }
+        }
+    }
+    return hb;
+}
+
+template <class K>
+__global__ void __launch_bounds__(256) bucket_join_count(const u32* __restrict__ cnt, int M, const K* __restrict__ xorc,
+                                                         u64 p, u64* __restrict__ tot, u64* __restrict__ work_run) {
+    __shared__ u64 red[2][8];
+    const u32 b = blockIdx.y;
+    const u64 v = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    HeadBlock hb;
+    if (v < (u64(1) << M)) hb = bucket_block(cnt, nullptr, b, M, v, u64(xorc[b]), p);
+    const u64 ws = warp_sum(hb.pairs), ww = warp_sum(hb.work);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = ws;
+        red[1][threadIdx.x >> 5] = ww;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 t0 = 0, t1 = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+            t0 += red[0][w];
+            t1 += red[1][w];
+        }
+        if (t0) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(t0));
+        if (t1) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(t1));
+    }
+}
+
+template <class K>
+__global__ void __launch_bounds__(256) bucket_join_emit(const u32* __restrict__ cnt, const u32* __restrict__ end, int M,
+                                                        const K* __restrict__ xorc, u64 p, const u64* __restrict__ tot,
+                                                        u64 guard, u32 hmax, Item* __restrict__ items,
+                                                        u32* __restrict__ nitems, u32 item_cap,
+                                                        u32* __restrict__ npairs, PairRec* __restrict__ pairs,
+                                                        u32 pair_cap) {
+    const u32 b = blockIdx.y;
+    const u64 v = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    HeadBlock hb;
+    if (v < (u64(1) << M) && tot[b] <= guard) hb = bucket_block(cnt, end, b, M, v, u64(xorc[b]), p);
+    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, p);
 }
 
 // Per-run counters; the guard (pair_search.hpp:91-94) zeroes the verified
@@ -340,7 +588,24 @@ struct VerifyArgs {
     DevHit* hits;
     u32* hit_count;
     u32 hit_cap;
+    // bucket-grouping path: stable positions are recomputed for hits
+    const u32* bend;   // [B][2^M] bucket end (global position), or null (sorted path)
+    const u32* bcnt;   // [B][2^M] bucket sizes
+    const void* keys;  // [B][p] projected keys (u32 or u64)
+    int M;
+    int key64;
 };
+
+// Position of column `col` of run `run` in the run's (key, index) order.
+__device__ __forceinline__ u32 stable_pos(const VerifyArgs& A, u32 run, u32 col) {
+    const u64 off = u64(run) * A.S;
+    const u64 v = A.key64 ? static_cast<const u64*>(A.keys)[off + col] : u64(static_cast<const u32*>(A.keys)[off + col]);
+    const u64 bi = (u64(run) << A.M) + v;
+    const u32 end = A.bend[bi], beg = end - A.bcnt[bi];
+    u32 rank = 0;
+    for (u32 t = beg; t < end; ++t) rank += A.sv[t] < col;
+    return u32(beg - off) + rank;
+}
 
 template <int G>
 __device__ __forceinline__ u32 team_mask_of(int lane) {
@@ -363,164 +628,47 @@ __device__ __forceinline__ void team_append(const VerifyArgs& A, u32 tmask, bool
     }
 }
 
-__device__ __forceinline__ DevHit make_hit(const VerifyArgs& A, u32 run, u32 held_pos, u32 str_pos, u32 flags,
-                                           double s, int32_t sint) {
-    const u32* svr = A.sv + u64(run) * A.S;
-    u32 pa, pb;  // x-side position, z-side position
-    if (flags & 2u) {
-        pa = min(held_pos, str_pos);
-        pb = max(held_pos, str_pos);
-    } else if (flags & 1u) {
-        pa = held_pos;
-        pb = str_pos;
-    } else {
-        pa = str_pos;
-        pb = held_pos;
+// Hit record of canonical pair (x-side position pa, z-side position pb) of a
+// run: oriented as the reference emits it — x side first (its key is the
+// smaller), diagonal blocks smaller column index first (A.8) — with the
+// order key of its (run, key, j, k) rank.
+__device__ __forceinline__ DevHit hit_of(const VerifyArgs& A, u32 run, u32 pa, u32 pb, bool diag, double s,
+                                         int32_t sint) {
+    const u64 off = u64(run) * A.S;
+    u32 j = A.sv[off + pa], k = A.sv[off + pb];
+    if (diag && j > k) {
+        const u32 t = j;
+        j = k;
+        k = t;
+        const u32 q = pa;
+        pa = pb;
+        pb = q;
+    }
+    u32 pf = pa, ps = pb;
+    if (A.bend) {
+        pf = stable_pos(A, run, j);
+        ps = stable_pos(A, run, k);
     }
     DevHit h;
     const u32 r = A.rid[run];
-    h.order = (u64(r) * A.p + pa) * A.p + pb;
+    h.order = (u64(r) * A.p + pf) * A.p + ps;
     h.s = s;
-    h.j = svr[pa];  // x side first: its key v < v^c; diagonal: smaller index first (A.8)
-    h.k = svr[pb];
+    h.j = j;
+    h.k = k;
     h.rid = r;
     h.sint = sint;
     return h;
 }
 
-// Binary: agree = popc(X_j ^ X_k ^ Y) over the padded words (padding is 0 in
-// X and Y, packed_matrix.cpp:29-35); pass +1 strength agree/n, pass -1
-// (n-agree)/n (search.cpp:25-36,347-349). Integer hit test sint >= astar.
-// A team of G lanes owns one item: its <= kHeld held columns (pre-XORed with
-// Y) stay in registers, each streamed column is read once and compared with
-// all of them. Lane chunk `it` covers 16 B at ulonglong2 index it*G + lane.
-template <int G, int NIT, int H>
-__global__ void __launch_bounds__(256) verify_binary(VerifyArgs A, const u64* __restrict__ Xc, u32 Wp,
-                                                     const u64* __restrict__ Yw, u32 n, u32 astar) {
-    const int lane = threadIdx.x & 31;
-    const int tl = lane & (G - 1);
-    const u32 tmask = team_mask_of<G>(lane);
-    const u32 W2 = Wp / 2;  // ulonglong2 per column
-    ulonglong2 yv[NIT];
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const u32 wi = it * G + tl;
-        yv[it] = wi < W2 ? __ldg(reinterpret_cast<const ulonglong2*>(Yw) + wi) : make_ulonglong2(0, 0);
-    }
-    const u32 N = min(*A.nitems, A.item_cap);
-    const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
-    const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
-    const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(Xc);
-    for (u64 t = team; t < N; t += nteams) {
-        const Item item = A.items[t];
-        if (A.tot[item.run] > A.guard) continue;  // aborted run: nothing is evaluated
-        const u32 hc = item.hc_flags & 0xffu, flags = item.hc_flags >> 8;
-        const u32* svr = A.sv + u64(item.run) * A.S;
-        const bool pos_pass = A.run_sign[item.run] > 0;
-        ulonglong2 hx[H][NIT];
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-            const u32 col = h < int(hc) ? svr[item.hs + h] : 0u;
-#pragma unroll
-            for (int it = 0; it < NIT; ++it) {
-                const u32 wi = it * G + tl;
-                ulonglong2 v = make_ulonglong2(0, 0);
-                if (h < int(hc) && wi < W2) {
-                    v = __ldg(X2 + u64(col) * W2 + wi);
-                    v.x ^= yv[it].x;
-                    v.y ^= yv[it].y;
-                }
-                hx[h][it] = v;
-            }
-        }
-        for (u32 s0 = 0; s0 < item.sc; s0 += G) {
-            const u32 my_s = s0 + tl;
-            const u32 my_col = my_s < item.sc ? svr[item.ss + my_s] : 0u;
-            const u32 cnt = min(u32(G), item.sc - s0);
-            for (u32 q = 0; q < cnt; ++q) {
-                const u32 col = __shfl_sync(tmask, my_col, q, G);
-                ulonglong2 z[NIT];
-#pragma unroll
-                for (int it = 0; it < NIT; ++it) {
-                    const u32 wi = it * G + tl;
-                    z[it] = wi < W2 ? __ldg(X2 + u64(col) * W2 + wi) : make_ulonglong2(0, 0);
-                }
-                u32 acc[H];
-#pragma unroll
-                for (int h = 0; h < H; ++h) {
-                    u32 a = 0;
-#pragma unroll
-                    for (int it = 0; it < NIT; ++it)
-                        a += __popcll(hx[h][it].x ^ z[it].x) + __popcll(hx[h][it].y ^ z[it].y);
-                    acc[h] = a;
-                }
-#pragma unroll
-                for (int h = 0; h < H; ++h) {
-#pragma unroll
-                    for (int o = G / 2; o > 0; o >>= 1) acc[h] += __shfl_xor_sync(tmask, acc[h], o);
-                }
-                // lane tl of the team tests pairs (held h, streamed s0+q) for h = tl, tl+G, ...
-                const u32 spos = item.ss + s0 + q;
-#pragma unroll
-                for (int h0 = 0; h0 < H; h0 += G) {
-                    u32 mine = 0;
-#pragma unroll
-                    for (int h = 0; h < H; ++h)
-                        if (h == h0 + tl) mine = acc[h];
-                    const u32 hpos = item.hs + h0 + tl;
-                    bool hit = false;
-                    u32 si = 0;
-                    if (h0 + tl < int(hc) && (!(flags & 2u) || spos > hpos)) {
-                        si = pos_pass ? mine : n - mine;
-                        hit = si >= astar;
-                    }
-                    DevHit hr;
-                    if (hit) hr = make_hit(A, item.run, hpos, spos, flags, double(si) / double(n), int32_t(si));
-                    team_append<G>(A, tmask, hit, hr);
-                }
-            }
-        }
-    }
-}
-
-// Sum V = 2^k per-lane values across the warp so that lane L ends up with the
-// warp total of value index L >> (5 - k): butterfly stages that halve the live
-// values (each lane keeps the half selected by its lane bit), then plain
-// xor-sums. V - 1 + (5 - k) shuffles for V totals instead of 5 V.
-template <int CNT, int O, int V>
-__device__ __forceinline__ void butterfly_stage(u32 (&v)[V], int lane) {
-    if constexpr (O >= 1) {
-        if constexpr (CNT > 1) {
-            constexpr int half = CNT / 2;
-            const bool up = (lane & O) != 0;
-#pragma unroll
-            for (int i = 0; i < half; ++i) {
-                const u32 send = up ? v[i] : v[i + half];
-                const u32 keep = up ? v[i + half] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
-            }
-            butterfly_stage<half, O / 2>(v, lane);
-        } else {
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
-            butterfly_stage<1, O / 2>(v, lane);
-        }
-    }
-}
-
-template <int V>
-__device__ __forceinline__ u32 butterfly_sum(u32 (&v)[V], int lane) {
-    butterfly_stage<V, 16>(v, lane);
-    return v[0];
+__device__ __forceinline__ DevHit make_hit(const VerifyArgs& A, u32 run, u32 held_pos, u32 str_pos, u32 flags,
+                                           double s, int32_t sint) {
+    const bool diag = flags & 2u;
+    const bool held_x = flags & 1u;
+    return hit_of(A, run, diag || held_x ? held_pos : str_pos, diag || held_x ? str_pos : held_pos, diag, s, sint);
 }
 
 // ------------------------------------------------------- pair list path --
 
-// One canonical candidate: batch-global sorted positions of the x side and
-// the z side (oriented: x side first; diagonal blocks: smaller position
-// first), and the batch-local run.
-struct PairRec {
-    u32 pa, pb, run, pad;
-};
 
 // Expand every item into its candidate pairs (h-major, so consecutive pairs
 // share the held column and stay in one team's L1). Warp per item; slots
@@ -535,34 +683,30 @@ __global__ void __launch_bounds__(256) expand_pairs(const Item* __restrict__ ite
         const Item it = items[t];
         const u32 hc = it.hc_flags & 0xffu, flags = it.hc_flags >> 8;
         const bool diag = flags & 2u, held_x = flags & 1u;
-        const u32 tot = hc * it.sc;
         const u64 off = u64(it.run) * S;
         const u32 base = it.pad;  // slots reserved by join_emit
         u32 written = 0;
-        for (u32 e0 = 0; e0 < tot; e0 += 32) {
-            const u32 e = e0 + lane;
-            bool ok = e < tot;
-            u32 hpos = 0, spos = 0;
-            if (ok) {
-                const u32 h = e / it.sc, s = e - h * it.sc;
-                hpos = it.hs + h;
-                spos = it.ss + s;
-                if (diag && spos <= hpos) ok = false;
-            }
-            const u32 bal = __ballot_sync(0xffffffffu, ok);
-            if (ok) {
-                const u32 slot = base + written + __popc(bal & lanemask_lt());
-                if (slot < pair_cap) {
-                    PairRec r;
-                    const u32 first = (diag || held_x) ? hpos : spos, second = (diag || held_x) ? spos : hpos;
-                    r.pa = u32(off + first);
-                    r.pb = u32(off + second);
-                    r.run = it.run;
-                    r.pad = 0;
-                    pairs[slot] = r;
+        const bool first_held = diag || held_x;
+        for (u32 h = 0; h < hc; ++h) {
+            const u32 hpos = it.hs + h;
+            for (u32 s0 = 0; s0 < it.sc; s0 += 32) {
+                const u32 q = s0 + lane;
+                const u32 spos = it.ss + q;
+                const bool ok = q < it.sc && !(diag && spos <= hpos);
+                const u32 bal = __ballot_sync(0xffffffffu, ok);
+                if (ok) {
+                    const u32 slot = base + written + __popc(bal & lanemask_lt());
+                    if (slot < pair_cap) {
+                        PairRec r;
+                        r.pa = u32(off + (first_held ? hpos : spos));
+                        r.pb = u32(off + (first_held ? spos : hpos));
+                        r.run = it.run;
+                        r.pad = flags;
+                        pairs[slot] = r;
+                    }
                 }
+                written += __popc(bal);
             }
-            written += __popc(bal);
         }
     }
 }
@@ -615,89 +759,11 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
             const bool hit = tl == 0 && si >= astar;
             DevHit h;
             if (hit) {
-                const u32 r = A.rid[pr.run];
                 const u64 base = u64(pr.run) * A.S;
-                h.order = (u64(r) * A.p + (pr.pa - base)) * A.p + (pr.pb - base);
-                h.s = double(si) / double(n);
-                h.j = j;
-                h.k = k;
-                h.rid = r;
-                h.sint = int32_t(si);
+                h = hit_of(A, pr.run, u32(pr.pa - base), u32(pr.pb - base), (pr.pad & 2u) != 0, double(si) / double(n),
+                           int32_t(si));
             }
             team_append<G>(A, tmask, hit, h);
-        }
-    }
-}
-
-// Binary verify for 33..64-word columns (n in (2048, 4096], e.g. BASELINE
-// config 2): one warp per item, 16 B of a column per lane, the <= 8 held
-// columns (XORed with Y) in registers, U streamed columns loaded at once
-// (U x 512 B in flight per warp) and the 8U popcount partials reduced with
-// one butterfly (about one shuffle per pair).
-template <int U>
-__global__ void __launch_bounds__(256) verify_binary_w32(VerifyArgs A, const u64* __restrict__ Xc, u32 Wp,
-                                                         const u64* __restrict__ Yw, u32 n, u32 astar) {
-    constexpr int H = 8, V = H * U;
-    constexpr int SH = (V == 32) ? 0 : (V == 16) ? 1 : 2;  // lane -> value index shift
-    const int lane = threadIdx.x & 31;
-    const u32 W2 = Wp / 2;
-    const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(Xc);
-    const ulonglong2 y = lane < int(W2) ? __ldg(reinterpret_cast<const ulonglong2*>(Yw) + lane) : make_ulonglong2(0, 0);
-    const u32 N = min(*A.nitems, A.item_cap);
-    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
-    // this lane's (held, streamed) slot in the butterfly output
-    const int my_idx = lane >> SH;
-    const int my_u = my_idx / H, my_h = my_idx % H;
-    const bool owner = (lane & ((1 << SH) - 1)) == 0;
-    for (u64 t = warp; t < N; t += nwarps) {
-        const Item item = A.items[t];
-        if (A.tot[item.run] > A.guard) continue;  // aborted run: nothing is evaluated
-        const u32 hc = item.hc_flags & 0xffu, flags = item.hc_flags >> 8;
-        const u32* svr = A.sv + u64(item.run) * A.S;
-        const bool pos_pass = A.run_sign[item.run] > 0;
-        const u32 my_held = lane < int(hc) ? svr[item.hs + lane] : 0u;
-        ulonglong2 hx[H];
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-            const u32 col = __shfl_sync(0xffffffffu, my_held, h);
-            ulonglong2 v = make_ulonglong2(0, 0);
-            if (h < int(hc) && lane < int(W2)) {
-                v = __ldg(X2 + u64(col) * W2 + lane);
-                v.x ^= y.x;
-                v.y ^= y.y;
-            }
-            hx[h] = v;
-        }
-        for (u32 s0 = 0; s0 < item.sc; s0 += 32) {
-            const u32 cnt = min(32u, item.sc - s0);
-            const u32 my_col = u32(lane) < cnt ? svr[item.ss + s0 + lane] : 0u;
-            for (u32 q0 = 0; q0 < cnt; q0 += U) {
-                ulonglong2 z[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const u32 col = __shfl_sync(0xffffffffu, my_col, (q0 + u) & 31);
-                    z[u] = (q0 + u < cnt && lane < int(W2)) ? __ldg(X2 + u64(col) * W2 + lane) : make_ulonglong2(0, 0);
-                }
-                u32 v[V];
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int h = 0; h < H; ++h)
-                        v[u * H + h] = __popcll(hx[h].x ^ z[u].x) + __popcll(hx[h].y ^ z[u].y);
-                const u32 agree = butterfly_sum<V>(v, lane);
-                const u32 spos = item.ss + s0 + q0 + my_u;
-                const u32 hpos = item.hs + my_h;
-                bool hit = false;
-                u32 si = 0;
-                if (owner && my_h < int(hc) && q0 + my_u < cnt && (!(flags & 2u) || spos > hpos)) {
-                    si = pos_pass ? agree : n - agree;
-                    hit = si >= astar;
-                }
-                DevHit hr;
-                if (hit) hr = make_hit(A, item.run, hpos, spos, flags, double(si) / double(n), int32_t(si));
-                team_append<32>(A, 0xffffffffu, hit, hr);
-            }
         }
     }
 }

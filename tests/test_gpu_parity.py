@@ -46,8 +46,12 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
+@pytest.mark.parametrize("grouping", ["auto", "sort"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
-def test_search_matches_reference_fixture(name):
+def test_search_matches_reference_fixture(name, grouping, monkeypatch):
+    """Both grouping paths (counting sort into 2^M buckets; segmented radix sort)."""
+    if grouping == "sort":
+        monkeypatch.setenv("XYZB_GROUPING", "sort")
     xb = _engine()
     x, y, cfg, z = load_case(name)
     rep = xb.Dataset(x).search(y, cfg)
@@ -183,13 +187,16 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch):
+@pytest.mark.parametrize("grouping", ["auto", "sort"])
+def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
     xb = _engine()
     x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
     cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=10)
     base = xb.Dataset(x).search(y, cfg)
+    if grouping == "sort":
+        monkeypatch.setenv("XYZB_GROUPING", "sort")
     monkeypatch.setenv("XYZB_BATCH_ENTRIES", "3000")  # one run per batch
     monkeypatch.setenv("XYZB_HIT_CAP", "7")
     monkeypatch.setenv("XYZB_ITEM_CAP", "5")
