@@ -366,6 +366,104 @@ int ref_brute_force_topk(const uint64_t* x_words, uint64_t n, uint64_t p, const 
     });
 }
 
+// lasso_path (lasso.cpp:447-597) with the config fields the benchmarks pin.
+// Output: per fit t, lambda[t], mains in [main_off[t], main_off[t+1]) of
+// (main_idx, main_val), pairs in [pair_off[t], pair_off[t+1]) of (pair_j,
+// pair_k, pair_val), and diagnostics. Arrays malloc'ed; free with ref_free.
+struct ref_lasso_out {
+    uint64_t n_fits;
+    double* lambda;
+    uint64_t* main_off;
+    uint32_t* main_idx;
+    double* main_val;
+    uint64_t* pair_off;
+    uint32_t* pair_j;
+    uint32_t* pair_k;
+    double* pair_val;
+    double* kkt_residual_max;
+    uint8_t* certified;
+    uint8_t* degenerate;
+    uint64_t* active_set_iterations;
+    uint64_t* cd_cycles;
+    double wall_s;
+};
+
+int ref_lasso_path(const double* x, uint64_t n, uint64_t p, const double* y, uint64_t grid_size, double grid_ratio,
+                   uint64_t kkt_l, uint64_t kkt_max_candidates, uint64_t seed, uint32_t threads,
+                   int32_t certify_exhaustive, ref_lasso_out* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const xyz::RealMatrix xm = real_from_colmajor(x, n, p);
+        const xyz::RealVector yv(y, y + n);
+        xyz::LassoPathConfig cfg;
+        cfg.grid_size = grid_size;
+        cfg.grid_ratio = grid_ratio;
+        if (kkt_l) cfg.kkt_l = kkt_l;
+        cfg.kkt_max_candidates = kkt_max_candidates;
+        cfg.seed = seed;
+        cfg.threads = threads;
+        cfg.certify_exhaustive = certify_exhaustive != 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto fits = xyz::lasso_path(xm, yv, cfg);
+        out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        const size_t T = fits.size();
+        size_t nm = 0, np = 0;
+        for (const auto& f : fits) {
+            nm += f.beta.size();
+            np += f.theta.size();
+        }
+        auto al = [](size_t cnt, size_t sz) { return std::malloc(std::max<size_t>(1, cnt) * sz); };
+        out->n_fits = T;
+        out->lambda = static_cast<double*>(al(T, 8));
+        out->main_off = static_cast<uint64_t*>(al(T + 1, 8));
+        out->pair_off = static_cast<uint64_t*>(al(T + 1, 8));
+        out->main_idx = static_cast<uint32_t*>(al(nm, 4));
+        out->main_val = static_cast<double*>(al(nm, 8));
+        out->pair_j = static_cast<uint32_t*>(al(np, 4));
+        out->pair_k = static_cast<uint32_t*>(al(np, 4));
+        out->pair_val = static_cast<double*>(al(np, 8));
+        out->kkt_residual_max = static_cast<double*>(al(T, 8));
+        out->certified = static_cast<uint8_t*>(al(T, 1));
+        out->degenerate = static_cast<uint8_t*>(al(T, 1));
+        out->active_set_iterations = static_cast<uint64_t*>(al(T, 8));
+        out->cd_cycles = static_cast<uint64_t*>(al(T, 8));
+        size_t mi = 0, pi = 0;
+        for (size_t t = 0; t < T; ++t) {
+            const auto& f = fits[t];
+            out->lambda[t] = f.lambda;
+            out->main_off[t] = mi;
+            out->pair_off[t] = pi;
+            for (const auto& [j, v] : f.beta) {
+                out->main_idx[mi] = j;
+                out->main_val[mi++] = v;
+            }
+            for (const auto& [key, v] : f.theta) {
+                out->pair_j[pi] = key.j;
+                out->pair_k[pi] = key.k;
+                out->pair_val[pi++] = v;
+            }
+            out->kkt_residual_max[t] = f.kkt_residual_max;
+            out->certified[t] = f.certified_exhaustive;
+            out->degenerate[t] = f.screening_degenerate;
+            out->active_set_iterations[t] = f.active_set_iterations;
+            out->cd_cycles[t] = f.cd_cycles;
+        }
+        out->main_off[T] = mi;
+        out->pair_off[T] = pi;
+    });
+}
+
+void ref_lasso_free(ref_lasso_out* o) {
+    if (!o) return;
+    for (void* q : {static_cast<void*>(o->lambda), static_cast<void*>(o->main_off), static_cast<void*>(o->main_idx),
+                    static_cast<void*>(o->main_val), static_cast<void*>(o->pair_off), static_cast<void*>(o->pair_j),
+                    static_cast<void*>(o->pair_k), static_cast<void*>(o->pair_val),
+                    static_cast<void*>(o->kkt_residual_max), static_cast<void*>(o->certified),
+                    static_cast<void*>(o->degenerate), static_cast<void*>(o->active_set_iterations),
+                    static_cast<void*>(o->cd_cycles)})
+        std::free(q);
+    std::memset(o, 0, sizeof(*o));
+}
+
 // rescale_rows (transforms.cpp:116-135): X/nu and y*nu^2, column-major in place copies.
 int ref_rescale_rows(const double* x, uint64_t n, uint64_t p, const double* y, double* x_out,
                      double* y_out, char* err, size_t errlen) {

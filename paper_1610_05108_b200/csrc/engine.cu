@@ -30,6 +30,7 @@
 #include "host_rng.hpp"
 #include "merge_kernels.cuh"
 #include "radix_sort.cuh"
+#include "run_sort.cuh"
 #include "real_kernels.cuh"
 #include "scan.cuh"
 #include "search_kernels.cuh"
@@ -135,7 +136,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal;
     // batch scratch
     DevBuf keys[2], vals[2], hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -431,8 +432,12 @@ void run_batches(SearchCtx& c) {
         item_cap = std::min<u64>(item_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.item_scale);
     if (item_cap > 0xffffffffull) throw internal_error("xyzb: batch too large for 32-bit item indices");
     ds->items.ensure(item_cap * sizeof(kern::Item));
-    const bool use_table = M <= u64(kern::kTableBits) && (B << M) <= (u64(1) << 28);
-    if (use_table) ds->table.ensure((B << M) * 4);
+    const bool use_table = M <= u64(kern::kTableBits) && (B << M) <= (u64(1) << 28) && (u64(1) << M) <= 4 * p + 1024;
+    if (use_table) {
+        ds->table.ensure((B << M) * 4);
+        ds->table_end.ensure((B << M) * 4);
+    }
+    const char* sort_sel = std::getenv("XYZB_SORT");  // "segments": multi-kernel LSD sort (tests)
     // host plan -> pinned -> device
     const bool host_rows = !c.plan.rows.empty();
     const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 96;
@@ -492,11 +497,12 @@ void run_batches(SearchCtx& c) {
         XYZB_CUDA(cudaMemsetAsync(ds->npairs.p, 0, nbatches * 4, st));
     }
     const u32 hmax = 8u;  // held columns per item (pair expansion chunks)
-    // grouping: counting sort into 2^M buckets when that table is small,
-    // else the segmented radix sort (XYZB_GROUPING=sort forces the latter)
+    // grouping: counting sort into 2^M buckets when 2^M is comparable to p
+    // (fastest measured on B200 for config 2), else the per-run cluster radix
+    // sort; XYZB_GROUPING=sort / XYZB_SORT=segments force the sorted paths
     const char* gsel = std::getenv("XYZB_GROUPING");
     const bool buckets = M <= u64(kern::kTableBits) && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
-                         !(gsel && std::string(gsel) == "sort");
+                         !(gsel && std::string(gsel) == "sort") && !sort_sel;
     if (buckets) {
         ds->bcnt.ensure((B << M) * 4);
         ds->bend.ensure(((B << M) + 1) * 4);
@@ -594,9 +600,15 @@ void run_batches(SearchCtx& c) {
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 2;
         } else {
-            // ---- sort ----
-            const int res = rsort::sort_segments<K>(kb, vb, nb, p, bits, ds->hist.as<u32>(), st,
-                                                    &c.launches[XYZB_STAGE_SORT]);
+            // ---- sort: one cluster per run (DSMEM histogram exchange), or the multi-kernel LSD sort ----
+            int res;
+            if (sort_sel && std::string(sort_sel) == "segments") {
+                res = rsort::sort_segments<K>(kb, vb, nb, p, bits, ds->hist.as<u32>(), st, &c.launches[XYZB_STAGE_SORT]);
+            } else {
+                res = rsort::sort_runs_launch<K>(kb[0], vb[0], kb[1], vb[1], nb, p, bits, st);
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_SORT] += 1;
+            }
             e2 = clk.mark();
             clk.span(XYZB_STAGE_SORT, e1, e2);
             c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((bits + 7) / 8);
@@ -606,19 +618,32 @@ void run_batches(SearchCtx& c) {
             XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
             dim3 gj(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
             if (use_table) {
-                kern::head_table<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->table.as<u32>());
+                // group tables, then one thread per key (partner lookups are O(1))
+                kern::group_tables<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->table.as<u32>(), ds->table_end.as<u32>());
                 XYZB_LAUNCH_CHECK();
-                c.launches[XYZB_STAGE_JOIN] += 1;
+                dim3 gb(static_cast<u32>(ceil_div(u64(1) << M, 256)), static_cast<u32>(nb));
+                kern::table_join_count<K><<<gb, 256, 0, st>>>(ds->table.as<u32>(), ds->table_end.as<u32>(), kb[res], p,
+                                                              int(M), ds->xorc.as<K>(), ds->tot.as<u64>(),
+                                                              ds->work_run.as<u64>());
+                XYZB_LAUNCH_CHECK();
+                kern::table_join_emit<K><<<gb, 256, 0, st>>>(
+                    ds->table.as<u32>(), ds->table_end.as<u32>(), kb[res], p, int(M), ds->xorc.as<K>(), ds->tot.as<u64>(),
+                    c.guard, hmax, ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap), npairs_b,
+                    ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_JOIN] += 3;
+            } else {
+                // wide keys: galloping group ends + binary-search partner lookups per head
+                kern::join_count<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), nullptr,
+                                                        ds->tot.as<u64>(), ds->work_run.as<u64>());
+                XYZB_LAUNCH_CHECK();
+                kern::join_emit<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), nullptr, ds->tot.as<u64>(),
+                                                       c.guard, hmax, ds->items.as<kern::Item>(), nitems,
+                                                       static_cast<u32>(item_cap), npairs_b,
+                                                       ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_JOIN] += 2;
             }
-            const u32* tbl = use_table ? ds->table.as<u32>() : nullptr;
-            kern::join_count<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(),
-                                                    ds->work_run.as<u64>());
-            XYZB_LAUNCH_CHECK();
-            kern::join_emit<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), tbl, ds->tot.as<u64>(), c.guard,
-                                                   hmax, ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
-                                                   npairs_b, ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
-            XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_JOIN] += 2;
         }
         kern::book_runs<<<static_cast<u32>(ceil_div(nb, 256)), 256, 0, st>>>(
             static_cast<u32>(nb), ds->tot.as<u64>(), ds->work_run.as<u64>(), c.guard, rid, ds->enumerated.as<u64>(),

@@ -1,0 +1,340 @@
+// Drop-in replacement for the reference's proj/core/src/search.cpp.
+//
+// Compiled against the reference's UNCHANGED public header xyz/search.hpp and
+// linked in its place (shim/Makefile), it gives the reference's callers — the
+// interaction Lasso's KKT screen (lasso.cpp:148-215), the CLI
+// (xyz_main.cpp:184-191) and the experiments (experiments.cpp:71-72) — the
+// B200 engine through the C ABI in include/xyzb.h:
+//   * the three xyz_search overloads (search.hpp:100-111) validate exactly as
+//     the reference does (search.cpp:119-134,325-334,367-374,415-434), then
+//     run on the GPU; X is uploaded once and cached per matrix (the Lasso
+//     screens the same rescaled X many times, lasso.cpp:118-141);
+//   * the parameter selectors and the strength sampler (search.cpp:136-291)
+//     are restated here on the host with the same formulas and evaluation
+//     order, so auto-M / auto-L decisions are bit-identical to the reference.
+// SearchConfig::threads is accepted and ignored (one device stream).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <random>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "xyz/errors.hpp"
+#include "xyz/rng.hpp"
+#include "xyz/search.hpp"
+#include "xyz/transforms.hpp"
+#include "xyzb.h"
+
+namespace xyz {
+
+namespace {
+
+double abs_sum(std::span<const double> v) {
+    double s = 0.0;
+    for (double t : v) s += std::abs(t);
+    return s;
+}
+
+[[noreturn]] void rethrow(int code, const char* msg) {
+    const std::string m = msg;
+    if (code == XYZB_E_DATA) throw data_error(m);
+    if (code == XYZB_E_GUARD) throw guard_error(m);
+    if (code == XYZB_E_SOLVER) throw solver_error(m);
+    throw std::runtime_error("xyz GPU engine: " + m);
+}
+
+// FNV-1a over the raw bytes: the cache must never serve a stale matrix.
+uint64_t fingerprint(const void* p, size_t bytes) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    uint64_t h = 1469598103934665603ull;
+    size_t i = 0;
+    for (; i + 8 <= bytes; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, b + i, 8);
+        h = (h ^ w) * 1099511628211ull;
+    }
+    for (; i < bytes; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+// One resident dataset per distinct matrix (address, shape, content).
+struct DatasetCache {
+    std::mutex mu;
+    xyzb_dataset* ds = nullptr;
+    const void* ptr = nullptr;
+    size_t n = 0, p = 0;
+    bool binary = false;
+    uint64_t fp = 0;
+    ~DatasetCache() {
+        if (ds) xyzb_dataset_destroy(ds);
+    }
+    xyzb_dataset* get(const uint64_t* words, const double* real, size_t n_, size_t p_) {
+        const void* ptr_ = words ? static_cast<const void*>(words) : static_cast<const void*>(real);
+        const size_t bytes = words ? p_ * ((n_ + 63) / 64) * 8 : n_ * p_ * 8;
+        const uint64_t f = fingerprint(ptr_, bytes);
+        if (ds && ptr == ptr_ && n == n_ && p == p_ && binary == (words != nullptr) && fp == f) return ds;
+        if (ds) xyzb_dataset_destroy(ds);
+        ds = nullptr;
+        xyzb_problem prob{};
+        prob.n_rows = n_;
+        prob.n_cols = p_;
+        prob.x_words = words;
+        prob.x_real = real;
+        prob.device = 0;
+        char err[1024] = {0};
+        const int code = xyzb_dataset_create(&prob, &ds, err, sizeof err);
+        if (code != XYZB_OK) rethrow(code, err);
+        ptr = ptr_;
+        n = n_;
+        p = p_;
+        binary = words != nullptr;
+        fp = f;
+        return ds;
+    }
+};
+
+DatasetCache& cache() {
+    static DatasetCache c;
+    return c;
+}
+
+xyzb_params to_params(const SearchConfig& c) {
+    xyzb_params q;
+    xyzb_params_init(&q);
+    q.m = c.m;
+    q.l = c.l;
+    q.gamma = c.gamma;
+    q.mode = static_cast<int32_t>(c.mode);
+    q.transform = static_cast<int32_t>(c.transform);
+    q.search_negatives = c.search_negatives ? 1 : 0;
+    q.stop_after_first_hit = c.stop_after_first_hit ? 1 : 0;
+    q.estimate_complexity = c.estimate_complexity ? 1 : 0;
+    q.threads = static_cast<int32_t>(c.threads);
+    q.seed = c.seed;
+    q.max_candidates_per_rep = c.max_candidates_per_rep;
+    q.strength_sample_size = c.strength_sample_size;
+    return q;
+}
+
+SearchReport run_gpu(const uint64_t* words, const double* real, size_t n, size_t p, const xyzb_response& resp,
+                     const SearchConfig& cfg) {
+    std::lock_guard<std::mutex> lock(cache().mu);
+    xyzb_dataset* ds = cache().get(words, real, n, p);
+    const xyzb_params q = to_params(cfg);
+    xyzb_result r;
+    char err[1024] = {0};
+    const int code = xyzb_search(ds, &resp, &q, nullptr, &r, err, sizeof err);
+    if (code != XYZB_OK) {
+        xyzb_result_free(&r);
+        rethrow(code, err);
+    }
+    SearchReport rep;
+    rep.hits.resize(r.n_hits);
+    for (size_t i = 0; i < r.n_hits; ++i) {
+        rep.hits[i].j = r.hits[i].j;
+        rep.hits[i].k = r.hits[i].k;
+        rep.hits[i].strength = r.hits[i].strength;
+        rep.hits[i].found_at_repetition = r.hits[i].found_at_repetition;
+        rep.hits[i].sign = r.hits[i].sign;
+    }
+    rep.repetitions_run = r.repetitions_run;
+    rep.candidates_checked = r.candidates_checked;
+    rep.candidates_enumerated = r.candidates_enumerated;
+    rep.aborted_repetitions = r.aborted_repetitions;
+    rep.wall_time_s = r.wall_time_s;
+    rep.estimated_c = r.estimated_c;
+    rep.gamma0 = r.gamma0;
+    rep.m_used = r.m_used;
+    rep.l_used = r.l_used;
+    xyzb_result_free(&r);
+    return rep;
+}
+
+// Uniform (j, k), j != k, k redrawn on collision (search.cpp:229-238).
+template <class F>
+StrengthSample draw_pairs(size_t p, size_t count, std::mt19937_64& rng, F&& strength) {
+    if (count < 1) throw data_error("sample_strengths: need n_samples >= 1");
+    std::uniform_int_distribution<size_t> dist(0, p - 1);
+    StrengthSample s;
+    s.strengths.reserve(count);
+    for (size_t t = 0; t < count; ++t) {
+        const size_t j = dist(rng);
+        size_t k = dist(rng);
+        while (p > 1 && k == j) k = dist(rng);
+        s.strengths.push_back(strength(j, k));
+    }
+    return s;
+}
+
+} // namespace
+
+// ---- configuration and selectors (search.cpp:119-220), restated ----
+
+void SearchConfig::validate() const {
+    if (m < 1 || m > max_subsample_size)
+        throw data_error("SearchConfig: M = " + std::to_string(m) + " outside [1,64]");
+    if (l < 1) throw data_error("SearchConfig: L must be >= 1");
+    if (!(gamma > 0.0 && gamma <= 1.0)) throw data_error("SearchConfig: gamma must lie in (0,1]");
+    const bool xy = mode == SearchMode::continuous_xy;
+    if (xy && transform == BinarizeTransform::none)
+        throw data_error("SearchConfig: continuous-XY mode requires a binarize transform");
+    if (!xy && transform != BinarizeTransform::none)
+        throw data_error("SearchConfig: binarize transform is only valid in continuous-XY mode");
+}
+
+double StrengthSample::mean_pow(std::size_t m) const {
+    if (strengths.empty()) throw data_error("StrengthSample: empty sample");
+    double acc = 0.0;
+    for (const double s : strengths) acc += std::pow(s, static_cast<double>(m));
+    return acc / static_cast<double>(strengths.size());
+}
+
+double StrengthSample::se_pow(std::size_t m) const {
+    if (strengths.empty()) throw data_error("StrengthSample: empty sample");
+    const double mu = mean_pow(m);
+    double ss = 0.0;
+    for (const double s : strengths) {
+        const double d = std::pow(s, static_cast<double>(m)) - mu;
+        ss += d * d;
+    }
+    const double cnt = static_cast<double>(strengths.size());
+    return std::sqrt(ss / cnt / cnt);
+}
+
+double discovery_probability(double gamma, std::size_t m, std::size_t l) {
+    if (!(gamma > 0.0 && gamma <= 1.0)) throw data_error("discovery_probability: gamma outside (0,1]");
+    if (m < 1 || l < 1) throw data_error("discovery_probability: M and L must be >= 1");
+    return 1.0 - std::pow(1.0 - std::pow(gamma, static_cast<double>(m)), static_cast<double>(l));
+}
+
+std::size_t choose_l(std::size_t m, double gamma, double eta_target) {
+    if (!(gamma > 0.0 && gamma <= 1.0)) throw data_error("choose_l: gamma outside (0,1]");
+    if (!(eta_target >= 0.5 && eta_target < 1.0)) throw data_error("choose_l: eta target must lie in [0.5,1)");
+    const double gm = std::pow(gamma, static_cast<double>(m));
+    if (gm >= 1.0) return 1;
+    if (gm <= 0.0) throw data_error("choose_l: gamma^M underflows to zero; choose a smaller M");
+    const double lr = std::log1p(-eta_target) / std::log1p(-gm);  // minimal real L
+    if (!(lr < 1e15)) throw data_error("choose_l: required L exceeds 1e15; choose a smaller M");
+    return std::max<std::size_t>(1, static_cast<std::size_t>(std::ceil(lr)));
+}
+
+double expected_complexity(std::size_t m, std::size_t l, const StrengthSample& sample, std::size_t n,
+                           std::size_t p) {
+    if (l < 1) throw data_error("expected_complexity: L must be >= 1");
+    const double pd = static_cast<double>(p);
+    const double e1 = pd * pd * sample.mean_pow(m);
+    return static_cast<double>(n) * pd +
+           static_cast<double>(l) * (static_cast<double>(m) * pd + pd * std::log(pd) + static_cast<double>(n) * e1);
+}
+
+MSelection optimal_m(double gamma, const StrengthSample& sample, std::size_t n, std::size_t p, std::size_t m_lo,
+                     std::size_t m_hi) {
+    if (!(gamma > 0.0 && gamma < 1.0)) throw data_error("optimal_m: gamma must lie in (0,1)");
+    if (sample.strengths.empty()) throw data_error("optimal_m: empty strength sample");
+    if (m_lo < 1 || m_hi > max_subsample_size || m_lo > m_hi) throw data_error("optimal_m: invalid M range");
+    const double pd = static_cast<double>(p), nd = static_cast<double>(n);
+    MSelection best;
+    double best_obj = std::numeric_limits<double>::infinity(), best_se = 0.0;
+    for (std::size_t m = m_lo; m <= m_hi; ++m) {
+        const double gm = std::pow(gamma, static_cast<double>(m));
+        if (gm <= 0.0) break;
+        const double denom = -std::log1p(-gm);
+        const double obj = (static_cast<double>(m) * pd + pd * std::log(pd) + nd * pd * pd * sample.mean_pow(m)) /
+                           denom;
+        if (obj < best_obj) {  // strict: exact ties keep the smaller M
+            best_obj = obj;
+            best.m = m;
+            best_se = nd * pd * pd * sample.se_pow(m) / denom;
+        }
+    }
+    if (best.m == 0) throw data_error("optimal_m: objective not finite anywhere in range");
+    best.objective = best_obj;
+    best.objective_rel_err = best_obj > 0.0 ? best_se / best_obj : 0.0;
+    best.gamma0 = std::pow(pd, -1.0 / static_cast<double>(best.m));
+    best.hit_range_cap = best.m == m_hi;
+    return best;
+}
+
+double runtime_exponent(double gamma, double gamma0) {
+    if (!(gamma0 > 0.0 && gamma0 < gamma && gamma <= 1.0))
+        throw data_error("runtime_exponent: need 0 < gamma0 < gamma <= 1");
+    return 1.0 + std::log(gamma) / std::log(gamma0);
+}
+
+StrengthSample sample_strengths(const PackedMatrix& x, const PackedMatrix& z, std::size_t n_samples,
+                                std::mt19937_64& rng) {
+    return draw_pairs(x.n_cols(), n_samples, rng,
+                      [&](size_t j, size_t k) { return interaction_strength(x, z, j, k); });
+}
+
+StrengthSample sample_strengths(const PackedMatrix& x, std::span<const double> y, std::size_t n_samples,
+                                std::mt19937_64& rng) {
+    return draw_pairs(x.n_cols(), n_samples, rng,
+                      [&](size_t j, size_t k) { return weighted_interaction_strength(x, y, j, k); });
+}
+
+StrengthSample sample_strengths(const RealMatrix& x, const RealVector& y, BinarizeTransform transform,
+                                std::size_t n_samples, std::mt19937_64& rng) {
+    if (n_samples < 1) throw data_error("sample_strengths: need n_samples >= 1");
+    if (transform == BinarizeTransform::none)
+        throw data_error("sample_strengths: continuous data needs a binarize transform");
+    const size_t n = x.n_rows();
+    const double norm = abs_sum(y);
+    if (norm <= 0.0) throw data_error("sample_strengths: zero response vector");
+    const bool unbiased = transform == BinarizeTransform::unbiased;
+    auto sgn = [](double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); };
+    return draw_pairs(x.n_cols(), n_samples, rng, [&](size_t j, size_t k) {
+        const auto a = x.column(j), b = x.column(k);
+        double acc = 0.0;
+        for (size_t i = 0; i < n; ++i) acc += unbiased ? y[i] * a[i] * b[i] : y[i] * sgn(a[i]) * sgn(b[i]);
+        return 0.5 + acc / (2.0 * norm);
+    });
+}
+
+// ---- the three entry points (search.cpp:325-506) on the GPU ----
+
+SearchReport xyz_search(const PackedMatrix& x, std::span<const std::int8_t> y, const SearchConfig& config) {
+    config.validate();
+    if (config.mode != SearchMode::binary) throw data_error("xyz_search: packed X with sign Y requires binary mode");
+    if (y.size() != x.n_rows()) throw data_error("xyz_search: response length mismatch");
+    for (const std::int8_t v : y)
+        if (v != 1 && v != -1) throw data_error("xyz_search: binary response must be +-1");
+    xyzb_response resp{};
+    resp.y_sign = y.data();
+    return run_gpu(x.column_words(0).data(), nullptr, x.n_rows(), x.n_cols(), resp, config);
+}
+
+SearchReport xyz_search(const PackedMatrix& x, const RealVector& y, const SearchConfig& config) {
+    config.validate();
+    if (config.mode != SearchMode::continuous_y)
+        throw data_error("xyz_search: packed X with real Y requires continuous-Y mode");
+    if (y.size() != x.n_rows()) throw data_error("xyz_search: response length mismatch");
+    if (abs_sum(y) <= 0.0) throw data_error("xyz_search: zero response vector");
+    xyzb_response resp{};
+    resp.y_real = y.data();
+    return run_gpu(x.column_words(0).data(), nullptr, x.n_rows(), x.n_cols(), resp, config);
+}
+
+SearchReport xyz_search(const RealMatrix& x, const RealVector& y, const SearchConfig& config) {
+    config.validate();
+    if (config.mode != SearchMode::continuous_xy) throw data_error("xyz_search: real X requires continuous-XY mode");
+    if (y.size() != x.n_rows()) throw data_error("xyz_search: response length mismatch");
+    if (abs_sum(y) <= 0.0) throw data_error("xyz_search: zero response vector");
+    if (config.transform == BinarizeTransform::unbiased) {
+        for (const double v : x.values())
+            if (!(v >= -1.0 && v <= 1.0))
+                throw data_error(
+                    "xyz_search: unbiased transform needs entries in [-1,1]; "
+                    "apply rescale_rows or cap_entries first");
+    }
+    xyzb_response resp{};
+    resp.y_real = y.data();
+    return run_gpu(nullptr, x.values().data(), x.n_rows(), x.n_cols(), resp, config);
+}
+
+} // namespace xyz

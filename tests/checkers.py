@@ -282,3 +282,67 @@ def same_hits(a, b, strength_tol=0.0):
         elif abs(h.strength - g.strength) > strength_tol * max(abs(g.strength), 1e-300):
             return False, f"hit {i} strength {h.strength!r} vs {g.strength!r} beyond {strength_tol}"
     return True, ""
+
+
+# ---- the drop-in build: reference core with search.cpp replaced by the GPU shim ----
+
+DROPIN_SO = os.path.join(ROOT, "build", "dropin", "libxyz_core_gpu.so")
+
+
+class LassoOut(C.Structure):
+    _fields_ = [("n_fits", C.c_uint64), ("lambda_", C.POINTER(C.c_double)), ("main_off", _U64P),
+                ("main_idx", _U32P), ("main_val", _F64P), ("pair_off", _U64P), ("pair_j", _U32P),
+                ("pair_k", _U32P), ("pair_val", _F64P), ("kkt_residual_max", _F64P),
+                ("certified", C.POINTER(C.c_uint8)), ("degenerate", C.POINTER(C.c_uint8)),
+                ("active_set_iterations", _U64P), ("cd_cycles", _U64P), ("wall_s", C.c_double)]
+
+
+_LASSO_SIGS = {
+    "ref_lasso_path": (C.c_int, [_F64P, C.c_uint64, C.c_uint64, _F64P, C.c_uint64, C.c_double, C.c_uint64,
+                                 C.c_uint64, C.c_uint64, C.c_uint32, C.c_int32, C.POINTER(LassoOut), C.c_char_p,
+                                 C.c_size_t]),
+    "ref_lasso_free": (None, [C.POINTER(LassoOut)]),
+}
+
+
+def dropin_available():
+    return os.path.exists(DROPIN_SO)
+
+
+def dropin_lib():
+    if "d" not in _cache:
+        _cache["d"] = _load(DROPIN_SO, {**_REF_SIGS, **_LASSO_SIGS})
+    return _cache["d"]
+
+
+def ref_lasso_lib():
+    if "rl" not in _cache:
+        _cache["rl"] = _abi.bind(ref_lib(), _LASSO_SIGS)
+    return _cache["rl"]
+
+
+def dropin_search(x, y, cfg):
+    return _search(dropin_lib(), "ref_search", "ref_result_free", x, y, cfg)
+
+
+def lasso_path(lib, x: RealMatrix, y, grid_size=20, grid_ratio=0.05, kkt_l=0, kkt_max_candidates=0, seed=7,
+               threads=1, certify=True):
+    """lasso_path through a harness library; returns (fits, wall_s). Each fit:
+    dict(lambda, beta {j: v}, theta {(j, k): v}, kkt, certified, degenerate)."""
+    out = LassoOut()
+    err = _abi.errbuf()
+    yy = np.ascontiguousarray(y, np.float64)
+    _check(lib.ref_lasso_path(x.values.ctypes.data_as(_F64P), x.n_rows, x.n_cols, yy.ctypes.data_as(_F64P),
+                              grid_size, grid_ratio, kkt_l, kkt_max_candidates, seed, threads, int(certify),
+                              C.byref(out), err, _abi.ERRBUF), err)
+    fits = []
+    try:
+        for t in range(out.n_fits):
+            beta = {int(out.main_idx[i]): float(out.main_val[i]) for i in range(out.main_off[t], out.main_off[t + 1])}
+            theta = {(int(out.pair_j[i]), int(out.pair_k[i])): float(out.pair_val[i])
+                     for i in range(out.pair_off[t], out.pair_off[t + 1])}
+            fits.append(dict(lam=float(out.lambda_[t]), beta=beta, theta=theta, kkt=float(out.kkt_residual_max[t]),
+                             certified=bool(out.certified[t]), degenerate=bool(out.degenerate[t])))
+        return fits, out.wall_s
+    finally:
+        lib.ref_lasso_free(C.byref(out))

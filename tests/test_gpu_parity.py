@@ -46,12 +46,15 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "sort"])
+@pytest.mark.parametrize("grouping", ["auto", "sort", "segments"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
 def test_search_matches_reference_fixture(name, grouping, monkeypatch):
-    """Both grouping paths (counting sort into 2^M buckets; segmented radix sort)."""
+    """All grouping paths: counting sort into 2^M buckets (default here),
+    per-run cluster radix sort, multi-kernel segmented radix sort."""
     if grouping == "sort":
         monkeypatch.setenv("XYZB_GROUPING", "sort")
+    if grouping == "segments":
+        monkeypatch.setenv("XYZB_SORT", "segments")
     xb = _engine()
     x, y, cfg, z = load_case(name)
     rep = xb.Dataset(x).search(y, cfg)
@@ -187,7 +190,7 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-@pytest.mark.parametrize("grouping", ["auto", "sort"])
+@pytest.mark.parametrize("grouping", ["auto", "sort", "segments"])
 def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
@@ -197,6 +200,8 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     base = xb.Dataset(x).search(y, cfg)
     if grouping == "sort":
         monkeypatch.setenv("XYZB_GROUPING", "sort")
+    if grouping == "segments":
+        monkeypatch.setenv("XYZB_SORT", "segments")
     monkeypatch.setenv("XYZB_BATCH_ENTRIES", "3000")  # one run per batch
     monkeypatch.setenv("XYZB_HIT_CAP", "7")
     monkeypatch.setenv("XYZB_ITEM_CAP", "5")
