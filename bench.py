@@ -37,10 +37,35 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(name="gwas_cfg2", n=4000, p=100000, m=16, l=100, gamma=0.6, top_k=100, n_pairs=5, coef=1.5,
-                seed=12345, search_seed=7)
-METRIC = "xyz projection runs/sec (BASELINE cfg2 GWAS-like n=4000 p=100000 M=16 L=100, both sign passes)"
-REF_SAMPLE_L = 25  # reference CPU sample: 2 x 25 runs per step (~10 s single-threaded)
+# BASELINE.json configs with the search parameters pinned in BASELINE.md §3.
+# The default bench line is config 2 (the metric's single-GPU workload); the
+# others are selectable with --config for per-config measurements.
+WORKLOADS = {
+    "gwas": dict(name="gwas_cfg2", label="cfg2 GWAS-like n=4000 p=100000 M=16 L=100", n=4000, p=100000, m=16,
+                 l=100, gamma=0.6, top_k=100, n_pairs=5, coef=1.5, seed=12345, search_seed=7, mode="binary",
+                 transform="none", ref_sample_l=25),
+    "toy": dict(name="toy_cfg1", label="cfg1 binary toy n=1000 p=2000 M=8 L=10", n=1000, p=2000, m=8, l=10,
+                gamma=0.55, top_k=10, seed=1, search_seed=7, mode="binary", transform="none", ref_sample_l=10),
+    "cont": dict(name="continuous_cfg3", label="cfg3 continuous n=2000 p=50000 M=20 L=200 sign", n=2000, p=50000,
+                 m=20, l=200, gamma=0.55, top_k=1000, n_pairs=10, theta=0.8, seed=3, search_seed=7,
+                 mode="continuous_xy", transform="sign", ref_sample_l=20),
+    "large": dict(name="large_cfg4", label="cfg4 large n=10000 p=1000000 M=20 L=400", n=10000, p=1000000, m=20,
+                  l=400, gamma=0.55, top_k=1000, n_pairs=20, flip=0.15, seed=99, search_seed=7, mode="binary",
+                  transform="none", ref_sample_l=2),
+}
+WORKLOAD = WORKLOADS["gwas"]
+METRIC = ""
+REF_SAMPLE_L = 25
+
+
+def select(config):
+    global WORKLOAD, METRIC, REF_SAMPLE_L
+    WORKLOAD = WORKLOADS[config]
+    METRIC = f"xyz projection runs/sec (BASELINE {WORKLOAD['label']}, both sign passes)"
+    REF_SAMPLE_L = WORKLOAD["ref_sample_l"]
+
+
+select("gwas")
 
 
 def parse():
@@ -51,7 +76,10 @@ def parse():
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--config", default="gwas", choices=sorted(WORKLOADS))
+    args = ap.parse_args()
+    select(args.config)
+    return args
 
 
 def dist_env():
@@ -63,14 +91,25 @@ def dist_env():
 
 def make_data():
     from paper_1610_05108_b200 import synth
-    x, y, planted = synth.gwas(WORKLOAD["n"], WORKLOAD["p"], WORKLOAD["n_pairs"], WORKLOAD["coef"], WORKLOAD["seed"])
-    return x, y, planted
+    W = WORKLOAD
+    if W["name"].startswith("gwas"):
+        return synth.gwas(W["n"], W["p"], W["n_pairs"], W["coef"], W["seed"])
+    if W["name"].startswith("toy"):
+        x, y = synth.toy(W["n"], W["p"], 4, 16, 0.9, W["seed"])
+        return x, y, np.array([[4, 16]], np.uint32)
+    if W["name"].startswith("continuous"):
+        x, y, pairs, _ = synth.gauss(W["n"], W["p"], W["n_pairs"], W["theta"], 1.0, 0, 1.0, W["seed"])
+        return x, y, pairs
+    return synth.ar1(W["n"], W["p"], 50, 0.3, W["n_pairs"], W["flip"], W["seed"])
 
 
-def search_config(l_total, top_k=WORKLOAD["top_k"]):
+def search_config(l_total, top_k=None):
     from paper_1610_05108_b200 import SearchConfig
-    return SearchConfig(m=WORKLOAD["m"], l=l_total, gamma=WORKLOAD["gamma"], seed=WORKLOAD["search_seed"],
-                        top_k=top_k, estimate_complexity=False, threads=1)
+    W = WORKLOAD
+    return SearchConfig(m=W["m"], l=l_total, gamma=W["gamma"], seed=W["search_seed"],
+                        top_k=W["top_k"] if top_k is None else top_k, estimate_complexity=False, threads=1,
+                        mode={"binary": "binary", "continuous_xy": "continuous_xy"}[W["mode"]],
+                        transform=W["transform"])
 
 
 class ClockSampler:
@@ -191,8 +230,10 @@ def run_reference(args):
 def workload_config(n_gpus, l_per_rank):
     return {"workload": WORKLOAD["name"], "n": WORKLOAD["n"], "p": WORKLOAD["p"], "M": WORKLOAD["m"],
             "L_per_gpu": l_per_rank, "L_total": l_per_rank * n_gpus, "passes": 2, "gamma": WORKLOAD["gamma"],
-            "guard": "16p", "top_k": WORKLOAD["top_k"], "x_bytes": WORKLOAD["p"] * 8 * ((WORKLOAD["n"] + 63) // 64),
-            "l2": "flushed between timed steps (256 MiB write); X (50 MB) is L2-resident within a step",
+            "guard": "16p", "top_k": WORKLOAD["top_k"], "mode": WORKLOAD["mode"], "transform": WORKLOAD["transform"],
+            "x_bytes": (WORKLOAD["p"] * 8 * ((WORKLOAD["n"] + 63) // 64) if WORKLOAD["mode"] == "binary"
+                        else WORKLOAD["p"] * 4 * WORKLOAD["n"]),
+            "l2": "flushed between timed steps (256 MiB write); X may be L2-resident within a step",
             "parallelism": f"run-shard{n_gpus}"}
 
 
@@ -284,8 +325,8 @@ def main():
                          "peak_source": src, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
                          "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                          "algorithmic_bytes_per_launch": verify_bytes / max(1, verify_launches),
-                         "note": "algorithmic bytes = 2 x 504 B columns per canonical candidate + Y; X (50 MB) "
-                                 "is L2-resident inside a step, so the verify kernel can exceed the HBM roofline"},
+                         "note": "algorithmic bytes = 2 columns per canonical candidate + Y (SURVEY 8d); when X "
+                                 "fits in L2 (cfg1-3) the verify kernel can exceed the HBM roofline"},
             "clocks": clk.summary(),
             "planted_found": sorted({(min(h.j, h.k), max(h.j, h.k)) for h in rep.hits} &
                                     {tuple(p) for p in planted.tolist()}),
@@ -312,7 +353,7 @@ def main():
         if world > 1:
             torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
         if rank == 0:
-            h2d = x.words.nbytes + y.nbytes + 2 * L * WORKLOAD["m"] * 4
+            h2d = (x.words.nbytes if hasattr(x, "words") else x.values.nbytes) + y.nbytes
             d2h = len(rr.hits) * 32 + len(rr.top_k) * 8
             out["e2e"] = {"value": e2e_runs / float(e2e_t[0]), "unit": "runs/s", "h2d_bytes_per_step": h2d,
                           "d2h_bytes_per_step": d2h,

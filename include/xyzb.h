@@ -126,7 +126,7 @@ enum {
 typedef struct {
     xyzb_hit* hits;
     uint64_t n_hits;
-    uint64_t* order_keys;  /* per hit: (run, position) order key, for merges */
+    uint64_t* order_keys;  /* per hit: its block key v (x side); reference order is (run, v, j, k) */
     uint64_t* top_k;       /* indices into hits, A.10 order                  */
     uint64_t n_top_k;
     uint64_t repetitions_run;

@@ -20,7 +20,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -41,23 +43,95 @@ namespace {
 
 // ------------------------------------------------------------ buffers --
 
+// Caching allocator: device blocks (per device) and pinned host blocks are
+// returned to a free list instead of cudaFree / cudaFreeHost, so datasets
+// created per call (the end-to-end path) and regrown scratch do not pay
+// cudaMalloc latency. On allocation failure the cache is trimmed and retried.
+struct BlockPool {
+    std::mutex mu;
+    std::multimap<size_t, std::pair<int, void*>> free_;  // size -> (device or -1 host, ptr)
+    static size_t granule(size_t b) { return b <= (1u << 20) ? round_pow2(b) : (b + (1u << 20) - 1) & ~size_t((1u << 20) - 1); }
+    static size_t round_pow2(size_t b) {
+        size_t r = 256;
+        while (r < b) r <<= 1;
+        return r;
+    }
+    void* take(size_t& b, int dev) {
+        b = granule(b);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            for (auto it = free_.lower_bound(b); it != free_.end() && it->first <= 2 * b + (8u << 20); ++it) {
+                if (it->second.first == dev) {
+                    void* p = it->second.second;
+                    b = it->first;
+                    free_.erase(it);
+                    return p;
+                }
+            }
+        }
+        void* p = nullptr;
+        cudaError_t err = dev >= 0 ? cudaMalloc(&p, b) : cudaMallocHost(&p, b);
+        if (err != cudaSuccess) {
+            cudaGetLastError();
+            trim(dev);
+            err = dev >= 0 ? cudaMalloc(&p, b) : cudaMallocHost(&p, b);
+        }
+        if (err != cudaSuccess)
+            throw cuda_error(std::string(dev >= 0 ? "cudaMalloc(" : "cudaMallocHost(") + std::to_string(b) +
+                             "): " + cudaGetErrorString(err));
+        return p;
+    }
+    void give(void* p, size_t b, int dev) {
+        std::lock_guard<std::mutex> lk(mu);
+        free_.emplace(b, std::make_pair(dev, p));
+    }
+    void trim(int dev) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto it = free_.begin(); it != free_.end();) {
+            if (it->second.first == dev) {
+                if (dev >= 0) cudaFree(it->second.second); else cudaFreeHost(it->second.second);
+                it = free_.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+};
+
+BlockPool& pool() {
+    static BlockPool* p = new BlockPool();  // intentionally leaked: outlives static destructors
+    return *p;
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    int dev = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            // the block may still be in use by queued work on some stream: drain
+            // the device before another buffer can be handed the same memory
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(dev);
+            cudaDeviceSynchronize();
+            cudaSetDevice(cur);
+            pool().give(p, bytes, dev);
+        }
         p = nullptr;
         bytes = 0;
     }
     void ensure(size_t b) {
         if (b <= bytes) return;
         release();
-        XYZB_CUDA(cudaMalloc(&p, std::max<size_t>(b, 256)));
-        bytes = std::max<size_t>(b, 256);
+        XYZB_CUDA(cudaGetDevice(&dev));
+        size_t got = std::max<size_t>(b, 256);
+        p = pool().take(got, dev);
+        bytes = got;
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
@@ -70,14 +144,14 @@ struct HostBuf {  // pinned
     HostBuf(const HostBuf&) = delete;
     HostBuf& operator=(const HostBuf&) = delete;
     ~HostBuf() {
-        if (p) cudaFreeHost(p);
+        if (p) pool().give(p, bytes, -1);
     }
     void ensure(size_t b) {
         if (b <= bytes) return;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        XYZB_CUDA(cudaMallocHost(&p, std::max<size_t>(b, 256)));
-        bytes = std::max<size_t>(b, 256);
+        if (p) pool().give(p, bytes, -1);
+        size_t got = std::max<size_t>(b, 256);
+        p = pool().take(got, -1);
+        bytes = got;
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
@@ -136,13 +210,13 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal;
     // batch scratch
     DevBuf keys[2], vals[2], hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
     DevBuf tkeys, tvals, keep, kpos, kept, kept_order, fin, fin_order, tie, kbufA, kbufB, vbufA, vbufB, topidx, hcount;
     DevBuf pairs_dev, strengths_dev;
-    HostBuf h_rows, h_state, h_small;
+    HostBuf h_rows, h_state, h_small, h_merge;
     StageClock clock;
     u32 hit_cap = 1u << 16;
 };
@@ -211,15 +285,58 @@ void validate_params(const xyzb_params* q) {
 
 // ------------------------------------------------------------ dataset creation --
 
+// Host -> device through two pooled pinned staging buffers: the host copy of
+// chunk i+1 overlaps the DMA of chunk i (pageable copies and 2-D copies with
+// 504-byte rows are several times slower).
+void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    constexpr size_t kChunk = size_t(16) << 20;
+    if (bytes <= (size_t(1) << 20)) {
+        XYZB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    HostBuf stage[2];
+    cudaEvent_t done[2];
+    for (int i = 0; i < 2; ++i) {
+        stage[i].ensure(kChunk);
+        XYZB_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    bool used[2] = {false, false};
+    for (size_t off = 0, i = 0; off < bytes; off += kChunk, i ^= 1) {
+        const size_t len = std::min(kChunk, bytes - off);
+        if (used[i]) XYZB_CUDA(cudaEventSynchronize(done[i]));
+        std::memcpy(stage[i].p, static_cast<const char*>(src) + off, len);
+        XYZB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage[i].p, len, cudaMemcpyHostToDevice, st));
+        XYZB_CUDA(cudaEventRecord(done[i], st));
+        used[i] = true;
+    }
+    XYZB_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < 2; ++i) cudaEventDestroy(done[i]);
+}
+
+__global__ void pad_words(const u64* __restrict__ src, u64 W, u64 p, u64 Wp, u64* __restrict__ dst) {
+    const u64 total = p * Wp;
+    for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += u64(gridDim.x) * blockDim.x) {
+        const u64 j = t / Wp, w = t - j * Wp;
+        dst[t] = w < W ? src[j * W + w] : 0ull;
+    }
+}
+
 void create_binary(xyzb_dataset* ds, const xyzb_problem* pr) {
     ds->binary = true;
     ds->W = ceil_div(ds->n, 64);
     ds->Wp = round_up(ds->W, 4);
     ds->P32 = ceil_div(ds->p, 32);
     ds->Xc.ensure(ds->p * ds->Wp * 8);
-    XYZB_CUDA(cudaMemsetAsync(ds->Xc.p, 0, ds->p * ds->Wp * 8, ds->stream));
-    XYZB_CUDA(cudaMemcpy2DAsync(ds->Xc.p, ds->Wp * 8, pr->x_words, ds->W * 8, ds->W * 8, ds->p,
-                                cudaMemcpyHostToDevice, ds->stream));
+    {
+        DevBuf raw;
+        raw.ensure(ds->p * ds->W * 8);
+        upload(raw.p, pr->x_words, ds->p * ds->W * 8, ds->stream);
+        pad_words<<<grid_for(ds->p * ds->Wp, 256, 4096), 256, 0, ds->stream>>>(raw.as<u64>(), ds->W, ds->p, ds->Wp,
+                                                                                ds->Xc.as<u64>());
+        XYZB_LAUNCH_CHECK();
+        XYZB_CUDA(cudaStreamSynchronize(ds->stream));  // raw returns to the pool
+    }
     ds->Xr.ensure(ds->n * ds->P32 * 4);
     const u64 warps = ds->P32 * ds->W;
     kern::transpose_bits<<<static_cast<u32>(ceil_div(warps * 32, 256)), 256, 0, ds->stream>>>(
@@ -235,7 +352,7 @@ void create_real(xyzb_dataset* ds, const xyzb_problem* pr) {
     ds->Wp = round_up(ds->W, 4);
     DevBuf xc64;
     xc64.ensure(ds->n * ds->p * 8);
-    XYZB_CUDA(cudaMemcpyAsync(xc64.p, pr->x_real, ds->n * ds->p * 8, cudaMemcpyHostToDevice, ds->stream));
+    upload(xc64.p, pr->x_real, ds->n * ds->p * 8, ds->stream);
     ds->Xc32.ensure(ds->p * ds->n4 * 4);
     real::to_f32_cols<<<grid_for(ds->p * ds->n4, 256, 4096), 256, 0, ds->stream>>>(xc64.as<double>(), ds->n, ds->p,
                                                                                      ds->n4, ds->Xc32.as<float>());
@@ -427,7 +544,7 @@ void run_batches(SearchCtx& c) {
         ds->vals[i].ensure(cap * 4);
     }
     ds->hist.ensure(rsort::hist_words(B, p) * 4);
-    u64 item_cap = std::min<u64>(0xffffffffull, B * (2 * p + 1) * c.item_scale);
+    u64 item_cap = std::min<u64>(0xffffffffull, B * (p / 2 + 64) * c.item_scale);  // regrows on overflow
     if (const char* e = std::getenv("XYZB_ITEM_CAP"))  // tests force the item-buffer regrow path with it
         item_cap = std::min<u64>(item_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.item_scale);
     if (item_cap > 0xffffffffull) throw internal_error("xyzb: batch too large for 32-bit item indices");
@@ -489,7 +606,7 @@ void run_batches(SearchCtx& c) {
     c.nbatches = nbatches;
     const bool pair_path = c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128;
     if (pair_path) {
-        c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, 4 * B * p) * c.pair_scale);
+        c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, B * p) * c.pair_scale);
         if (const char* e = std::getenv("XYZB_PAIR_CAP"))  // tests force the pair-list regrow path with it
             c.pair_cap = std::min<u64>(c.pair_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.pair_scale);
         ds->pairs.ensure(c.pair_cap * sizeof(kern::PairRec));
@@ -539,12 +656,20 @@ void run_batches(SearchCtx& c) {
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_PROJECT] += 2;
             } else {
-                dim3 g(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
-                real::project_sign<K><<<g, 256, 0, st>>>(ds->Xpos.as<u32>(), ds->Xzero.as<u32>(), ds->P32, p, rows,
-                                                          int(M), coins ? 1 : 0, k0, ds->zmask.as<K>(),
-                                                          ds->zcount.as<u32>());
+                // sign transform: key bits from the (v > 0) planes, coin mask from the (v == 0) planes
+                dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
+                kern::project_bits_t<K><<<g, 128, 0, st>>>(ds->Xpos.as<u32>(), ds->P32, p, rows, int(M), k0);
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_PROJECT] += 2;
+                if (coins) {
+                    kern::project_bits_t<K><<<g, 128, 0, st>>>(ds->Xzero.as<u32>(), ds->P32, p, rows, int(M),
+                                                               ds->zmask.as<K>());
+                    XYZB_LAUNCH_CHECK();
+                    real::popc_count<K><<<grid_for(nb * p, 256, 4096), 256, 0, st>>>(ds->zmask.as<K>(), nb * p,
+                                                                                     ds->zcount.as<u32>());
+                    XYZB_LAUNCH_CHECK();
+                    c.launches[XYZB_STAGE_PROJECT] += 2;
+                }
                 if (coins) {
                     u32* cnt = reinterpret_cast<u32*>(hp + hbytes - 16);
                     *cnt = static_cast<u32>(nb * p);
@@ -566,6 +691,7 @@ void run_batches(SearchCtx& c) {
         u32* nitems = ds->nblocks.as<u32>() + batch_idx;
         u32* npairs_b = pair_path ? ds->npairs.as<u32>() + batch_idx : nullptr;
         const u32* sv = nullptr;
+        const K* sorted_keys = nullptr;
         cudaEvent_t e2;
         if (buckets) {
             // ---- group: counting sort into 2^M buckets per run ----
@@ -613,6 +739,7 @@ void run_batches(SearchCtx& c) {
             clk.span(XYZB_STAGE_SORT, e1, e2);
             c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((bits + 7) / 8);
             sv = vb[res];
+            sorted_keys = kb[res];
             // ---- join (+ guard bookkeeping) ----
             XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
             XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
@@ -662,11 +789,10 @@ void run_batches(SearchCtx& c) {
         A.guard = c.guard;
         A.sv = sv;
         A.S = p;
-        A.bend = buckets ? ds->bend.as<u32>() : nullptr;
-        A.bcnt = buckets ? ds->bcnt.as<u32>() : nullptr;
-        A.keys = k0;
-        A.M = int(M);
+        A.vkeys = buckets ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
+        A.vkeys_by_pos = buckets ? 0 : 1;
         A.key64 = sizeof(K) == 8;
+        A.vshift = 0;
         A.rid = rid;
         A.run_sign = rsign;
         A.p = p;
@@ -745,6 +871,39 @@ void merge_hits(SearchCtx& c, u32 H, u32 rmax, std::vector<xyzb_hit>& hits_out, 
     topk_out.clear();
     if (H == 0) return;
     u64& L = c.launches[XYZB_STAGE_MERGE];
+    if (H <= u32(merge::kSmallMerge) && !std::getenv("XYZB_MERGE_LARGE")) {
+        // short lists: one CTA dedups, orders and ranks in shared memory
+        static bool attr_set = false;
+        const size_t smem = merge::small_merge_smem(merge::kSmallMerge);
+        if (!attr_set) {
+            XYZB_CUDA(cudaFuncSetAttribute(merge::merge_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+            attr_set = true;
+        }
+        ds->fin.ensure(u64(H) * sizeof(xyzb_hit));
+        ds->fin_order.ensure(u64(H) * 8);
+        ds->topidx.ensure(u64(H) * 8 + 16);
+        u64* top = ds->topidx.as<u64>();
+        u32* counts = reinterpret_cast<u32*>(top + H);
+        merge::merge_small<<<1, merge::kSmallThreads, smem, st>>>(
+            ds->hits.as<kern::DevHit>(), H, ds->sign_by_rid.as<int8_t>(), rmax, c.plan.L, c.q->top_k,
+            ds->fin.as<xyzb_hit>(), ds->fin_order.as<u64>(), top, counts);
+        XYZB_LAUNCH_CHECK();
+        L += 1;
+        const size_t hb = u64(H) * sizeof(xyzb_hit), ob = u64(H) * 8, tb = u64(H) * 8 + 16;
+        ds->h_merge.ensure(hb + ob + tb);
+        char* hp = ds->h_merge.as<char>();
+        XYZB_CUDA(cudaMemcpyAsync(hp, ds->fin.p, hb, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaMemcpyAsync(hp + hb, ds->fin_order.p, ob, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaMemcpyAsync(hp + hb + ob, top, tb, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        const u32* cnt = reinterpret_cast<const u32*>(hp + hb + ob + u64(H) * 8);
+        const u32 K = cnt[0], kk = cnt[1];
+        hits_out.assign(reinterpret_cast<const xyzb_hit*>(hp), reinterpret_cast<const xyzb_hit*>(hp) + K);
+        order_out.assign(reinterpret_cast<const u64*>(hp + hb), reinterpret_cast<const u64*>(hp + hb) + K);
+        topk_out.assign(reinterpret_cast<const u64*>(hp + hb + ob), reinterpret_cast<const u64*>(hp + hb + ob) + kk);
+        return;
+    }
     // dedup table
     u64 T = 64;
     while (T < 2ull * H) T <<= 1;
@@ -779,14 +938,28 @@ void merge_hits(SearchCtx& c, u32 H, u32 rmax, std::vector<xyzb_hit>& hits_out, 
     XYZB_CUDA(cudaMemcpyAsync(&K, ds->kpos.as<u32>() + H, 4, cudaMemcpyDeviceToHost, st));
     XYZB_CUDA(cudaStreamSynchronize(st));
     if (K == 0) return;
-    // order: run * p^2 + pos_first * p + pos_second
-    const long double maxo = (long double)(c.plan.sign_by_rid.size()) * (long double)c.p * (long double)c.p;
-    int obits = 1;
-    while (obits < 64 && (long double)(1ull << obits) <= maxo) ++obits;
+    // reference order (run, v, j, k): stable LSD sorts by (j, k), then v, then run
     ds->hist.ensure(rsort::hist_words(1, K) * 4);
+    ds->perm.ensure(u64(K) * 8);
     u64* kb[2] = {ds->kbufA.as<u64>(), ds->kbufB.as<u64>()};
     u32* vb[2] = {ds->vbufA.as<u32>(), ds->vbufB.as<u32>()};
-    const int r1 = rsort::sort_segments<u64>(kb, vb, 1, K, obits, ds->hist.as<u32>(), st, &L);
+    u32* perm = ds->perm.as<u32>();
+    u32* perm2 = perm + K;
+    int r1 = rsort::sort_segments<u64>(kb, vb, 1, K, 64, ds->hist.as<u32>(), st, &L);  // jk keys from compact
+    XYZB_CUDA(cudaMemcpyAsync(perm, vb[r1], u64(K) * 4, cudaMemcpyDeviceToDevice, st));
+    int vbits = 1;
+    while (vbits < 64 && (c.M >= 64 || (u64(1) << vbits) < (u64(1) << c.M))) ++vbits;
+    int rbits = 1;
+    while (rbits < 32 && (u64(1) << rbits) < c.plan.sign_by_rid.size()) ++rbits;
+    for (int which = 0; which < 2; ++which) {
+        merge::order_key<<<grid_for(K, 256), 256, 0, st>>>(ds->kept.as<kern::DevHit>(), perm, K, which, kb[0]);
+        const int rr = rsort::sort_segments<u64>(kb, vb, 1, K, which == 0 ? vbits : rbits, ds->hist.as<u32>(), st, &L);
+        merge::compose_perm<<<grid_for(K, 256), 256, 0, st>>>(perm, vb[rr], K, perm2);
+        XYZB_CUDA(cudaMemcpyAsync(perm, perm2, u64(K) * 4, cudaMemcpyDeviceToDevice, st));
+        L += 2;
+    }
+    r1 = 0;
+    XYZB_CUDA(cudaMemcpyAsync(vb[0], perm, u64(K) * 4, cudaMemcpyDeviceToDevice, st));
     ds->fin.ensure(u64(K) * sizeof(xyzb_hit));
     ds->fin_order.ensure(u64(K) * 8);
     ds->tie.ensure(u64(K) * 8);
@@ -1254,16 +1427,15 @@ extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, ui
         XYZB_CUDA(cudaMemcpyAsync(ds->sign_by_rid.p, c.plan.sign_by_rid.data(), Rall, cudaMemcpyHostToDevice,
                                   ds->stream));
         std::vector<kern::DevHit> all;
-        const u64 pp = c.p * c.p;
         for (u64 t = 0; t < n_parts; ++t) {
             const xyzb_result& r = parts[t];
             for (u64 i = 0; i < r.n_hits; ++i) {
                 kern::DevHit h;
-                h.order = r.order_keys[i];
+                h.order = r.order_keys[i];  // x-side key v
                 h.s = r.hits[i].strength;
                 h.j = r.hits[i].j;
                 h.k = r.hits[i].k;
-                h.rid = static_cast<u32>(h.order / pp);
+                h.rid = static_cast<u32>((r.hits[i].sign > 0 ? 0 : c.plan.L) + r.hits[i].found_at_repetition - 1);
                 h.sint = -1;
                 all.push_back(h);
             }

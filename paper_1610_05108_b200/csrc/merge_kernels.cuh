@@ -41,7 +41,9 @@ __global__ void min_rid(const DevHit* __restrict__ h, u32 H, u32* __restrict__ o
     if ((threadIdx.x & 31) == 0 && m != 0xffffffffu) atomicMin(out, m);
 }
 
-// Open-addressing table tag -> min order key.
+// Open-addressing table tag -> earliest run holding it (a run verifies each
+// unordered pair at most once, so the earliest run identifies the reference's
+// first occurrence, A.8).
 __global__ void hash_insert(const DevHit* __restrict__ h, u32 H, const int8_t* __restrict__ sign_by_rid,
                             u64* __restrict__ tkeys, u64* __restrict__ tvals, u64 mask) {
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < H; i += u64(gridDim.x) * blockDim.x) {
@@ -53,7 +55,7 @@ __global__ void hash_insert(const DevHit* __restrict__ h, u32 H, const int8_t* _
             if (prev == kEmpty || prev == t) break;
             slot = (slot + 1) & mask;
         }
-        atomicMin(reinterpret_cast<unsigned long long*>(tvals + slot), x.order);
+        atomicMin(reinterpret_cast<unsigned long long*>(tvals + slot), static_cast<unsigned long long>(x.rid));
     }
 }
 
@@ -65,18 +67,35 @@ __global__ void hash_mark(const DevHit* __restrict__ h, u32 H, const int8_t* __r
         const u64 t = tag_of(x, sign_by_rid[x.rid]);
         u64 slot = hash64(t) & mask;
         while (tkeys[slot] != t) slot = (slot + 1) & mask;
-        keep[i] = (tvals[slot] == x.order && x.rid <= *rmax) ? 1u : 0u;
+        keep[i] = (tvals[slot] == u64(x.rid) && x.rid <= *rmax) ? 1u : 0u;
     }
 }
 
 __global__ void compact(const DevHit* __restrict__ h, u32 H, const u32* __restrict__ keep, const u32* __restrict__ pos,
-                        DevHit* __restrict__ out, u64* __restrict__ order_keys) {
+                        DevHit* __restrict__ out, u64* __restrict__ jk_key) {
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < H; i += u64(gridDim.x) * blockDim.x) {
         if (keep[i]) {
             out[pos[i]] = h[i];
-            order_keys[pos[i]] = h[i].order;
+            jk_key[pos[i]] = (u64(h[i].j) << 32) | h[i].k;
         }
     }
+}
+
+// Next LSD key of the (rid, v, j, k) order in the current permutation:
+// which = 0 -> v, 1 -> rid.
+__global__ void order_key(const DevHit* __restrict__ kept, const u32* __restrict__ perm, u32 K, int which,
+                          u64* __restrict__ key) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < K; i += u64(gridDim.x) * blockDim.x) {
+        const DevHit& h = kept[perm[i]];
+        key[i] = which == 0 ? h.order : u64(h.rid);
+    }
+}
+
+// perm_out[i] = perm_in[sub[i]]
+__global__ void compose_perm(const u32* __restrict__ perm_in, const u32* __restrict__ sub, u32 K,
+                             u32* __restrict__ perm_out) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < K; i += u64(gridDim.x) * blockDim.x)
+        perm_out[i] = perm_in[sub[i]];
 }
 
 // Final records in reference order; also the top-K tie key
@@ -123,6 +142,167 @@ __global__ void compose_idx(const u32* __restrict__ tie_idx, const u32* __restri
                             u64* __restrict__ out) {
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < K; i += u64(gridDim.x) * blockDim.x)
         out[i] = tie_idx[prim_idx[i]];
+}
+
+// ---- single-CTA merge for short hit lists (one launch, no host sync) ----
+
+constexpr int kSmallMerge = 4096;
+constexpr int kSmallThreads = 1024;
+
+// In-place bitonic sort of idx[0..N) (N a power of two) by less(a, b).
+template <class Less>
+__device__ __forceinline__ void bitonic(u32* idx, int N, Less less) {
+    for (int k = 2; k <= N; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < N; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const u32 a = idx[i], b = idx[l];
+                    const bool up = (i & k) == 0;
+                    const bool swap = up ? less(b, a) : less(a, b);
+                    if (swap) {
+                        idx[i] = b;
+                        idx[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Block-wide exclusive scan of v over threads (blockDim.x <= 1024).
+__device__ __forceinline__ u32 block_excl_scan(u32 v, u32* warp_tot, u32* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u32 incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        const u32 x = lane < nw ? warp_tot[lane] : 0u;
+        u32 xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        if (lane < nw) warp_tot[lane] = xi - x;
+        if (lane == nw - 1) warp_tot[32] = xi;
+    }
+    __syncthreads();
+    const u32 r = warp_tot[wid] + incl - v;
+    *total = warp_tot[32];
+    __syncthreads();
+    return r;
+}
+
+// Dynamic shared memory: u64 tag[N], u64 v[N], u64 jk[N], u32 rid[N], u32 idx[N], u32 aux[N].
+constexpr size_t small_merge_smem(int N) { return size_t(N) * 36; }
+
+// out_counts[0] = kept hits K, out_counts[1] = top-K length. H <= kSmallMerge.
+__global__ void __launch_bounds__(kSmallThreads) merge_small(const DevHit* __restrict__ h, u32 H,
+                                                             const int8_t* __restrict__ sign_by_rid, u32 rmax, u64 L,
+                                                             u64 top_k, xyzb_hit* __restrict__ out,
+                                                             u64* __restrict__ order_out, u64* __restrict__ top_out,
+                                                             u32* __restrict__ out_counts) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ u32 warp_tot[33];
+    int N = 1;
+    while (N < int(H)) N <<= 1;
+    u64* s_tag = reinterpret_cast<u64*>(smem);
+    u64* s_v = s_tag + N;
+    u64* s_jk = s_v + N;
+    u32* s_rid = reinterpret_cast<u32*>(s_jk + N);
+    u32* s_idx = s_rid + N;
+    u32* s_aux = s_idx + N;
+    const u64 INF = ~0ull;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        if (i < int(H) && h[i].rid <= rmax) {
+            s_tag[i] = tag_of(h[i], sign_by_rid[h[i].rid]);
+            s_v[i] = h[i].order;
+            s_jk[i] = (u64(h[i].j) << 32) | h[i].k;
+            s_rid[i] = h[i].rid;
+        } else {
+            s_tag[i] = INF;
+            s_v[i] = INF;
+            s_jk[i] = INF;
+            s_rid[i] = 0xffffffffu;
+        }
+        s_idx[i] = i;
+    }
+    __syncthreads();
+    // dedup: sort by (tag, run); the first of each tag is the kept occurrence
+    bitonic(s_idx, N, [&](u32 a, u32 b) {
+        return s_tag[a] != s_tag[b] ? s_tag[a] < s_tag[b] : s_rid[a] < s_rid[b];
+    });
+    // compact kept hit indices into s_aux[0..K) (stable scan over the sorted list)
+    u32 K = 0;
+    const int per = (N + int(blockDim.x) - 1) / int(blockDim.x);
+    {
+        const int b0 = threadIdx.x * per, b1 = min(N, b0 + per);
+        u32 cnt = 0;
+        for (int i = b0; i < b1; ++i) {
+            const u32 a = s_idx[i];
+            cnt += (s_tag[a] != INF && (i == 0 || s_tag[s_idx[i - 1]] != s_tag[a])) ? 1u : 0u;
+        }
+        u32 pos = block_excl_scan(cnt, warp_tot, &K);
+        for (int i = b0; i < b1; ++i) {
+            const u32 a = s_idx[i];
+            if (s_tag[a] != INF && (i == 0 || s_tag[s_idx[i - 1]] != s_tag[a])) s_aux[pos++] = a;
+        }
+    }
+    __syncthreads();
+    // reference order: kept hits by (run, v, j, k)
+    int NK = 1;
+    while (NK < int(K)) NK <<= 1;
+    for (int i = threadIdx.x; i < NK; i += blockDim.x) s_idx[i] = i < int(K) ? s_aux[i] : u32(0xffffffffu);
+    __syncthreads();
+    bitonic(s_idx, NK, [&](u32 a, u32 b) {
+        if (a == 0xffffffffu || b == 0xffffffffu) return a != 0xffffffffu && b == 0xffffffffu;
+        if (s_rid[a] != s_rid[b]) return s_rid[a] < s_rid[b];
+        if (s_v[a] != s_v[b]) return s_v[a] < s_v[b];
+        return s_jk[a] < s_jk[b];
+    });
+    for (int i = threadIdx.x; i < int(K); i += blockDim.x) {
+        const DevHit x = h[s_idx[i]];
+        const int8_t sg = sign_by_rid[x.rid];
+        xyzb_hit o;
+        o.j = x.j;
+        o.k = x.k;
+        o.strength = x.s;
+        o.found_at_repetition = u32(x.rid % L) + 1;
+        o.sign = sg;
+        out[i] = o;
+        order_out[i] = x.order;
+    }
+    __syncthreads();
+    if (top_k > 0 && K > 0) {
+        // A.10: strength desc, min asc, max asc, sign desc (positions in `out`)
+        for (int i = threadIdx.x; i < NK; i += blockDim.x) s_aux[i] = u32(i);
+        __syncthreads();
+        bitonic(s_aux, NK, [&](u32 a, u32 b) {
+            const bool va = a < K, vb = b < K;
+            if (!va || !vb) return va && !vb;
+            const xyzb_hit x = out[a], y = out[b];
+            if (x.strength != y.strength) return x.strength > y.strength;
+            const u32 xl = min(x.j, x.k), yl = min(y.j, y.k);
+            if (xl != yl) return xl < yl;
+            const u32 xh = max(x.j, x.k), yh = max(y.j, y.k);
+            if (xh != yh) return xh < yh;
+            return x.sign > y.sign;
+        });
+        const u64 kk = top_k < u64(K) ? top_k : u64(K);
+        for (int i = threadIdx.x; i < int(kk); i += blockDim.x) top_out[i] = s_aux[i];
+        if (threadIdx.x == 0) out_counts[1] = u32(kk);
+    } else if (threadIdx.x == 0) {
+        out_counts[1] = 0;
+    }
+    if (threadIdx.x == 0) out_counts[0] = K;
 }
 
 } // namespace merge

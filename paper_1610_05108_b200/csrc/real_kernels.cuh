@@ -121,6 +121,12 @@ __global__ void __launch_bounds__(256) project_sign(const u32* __restrict__ Xpos
     }
 }
 
+template <class K>
+__global__ void popc_count(const K* __restrict__ m, u64 count, u32* __restrict__ out) {
+    for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < count; t += u64(gridDim.x) * blockDim.x)
+        out[t] = __popcll(static_cast<unsigned long long>(m[t]));
+}
+
 // Sign-transform coins: the t-th zero entry of run b in (j, s) order takes
 // bit 0 of the t-th output of the run's stream (search.cpp:457-463).
 template <class K>

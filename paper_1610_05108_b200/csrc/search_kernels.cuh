@@ -22,7 +22,7 @@ namespace kern {
 
 // A verified candidate with strength >= gamma (pre-dedup).
 struct DevHit {
-    u64 order;     // rid * p^2 + pos_first * p + pos_second  (A.5 order inside a run)
+    u64 order;     // x-side key v: the reference order is (rid, v, j, k) (A.5)
     double s;      // strength (binary: exact sint / n)
     u32 j, k;      // oriented as the reference emits it (first in A.5 order)
     u32 rid;       // global run index: pass * L + rep - 1
@@ -697,23 +697,17 @@ struct VerifyArgs {
     DevHit* hits;
     u32* hit_count;
     u32 hit_cap;
-    // bucket-grouping path: stable positions are recomputed for hits
-    const u32* bend;   // [B][2^M] bucket end (global position), or null (sorted path)
-    const u32* bcnt;   // [B][2^M] bucket sizes
-    const void* keys;  // [B][p] projected keys (u32 or u64)
-    int M;
+    // the x-side key v of a hit (its block's key): from the sorted keys at the
+    // x-side position, or (bucket path, keys unsorted) at the column index
+    const void* vkeys;
+    int vkeys_by_pos;
     int key64;
+    int vshift;  // sorted keys carry extra low bits to drop (0 here)
 };
 
-// Position of column `col` of run `run` in the run's (key, index) order.
-__device__ __forceinline__ u32 stable_pos(const VerifyArgs& A, u32 run, u32 col) {
-    const u64 off = u64(run) * A.S;
-    const u64 v = A.key64 ? static_cast<const u64*>(A.keys)[off + col] : u64(static_cast<const u32*>(A.keys)[off + col]);
-    const u64 bi = (u64(run) << A.M) + v;
-    const u32 end = A.bend[bi], beg = end - A.bcnt[bi];
-    u32 rank = 0;
-    for (u32 t = beg; t < end; ++t) rank += A.sv[t] < col;
-    return u32(beg - off) + rank;
+__device__ __forceinline__ u64 key_at(const VerifyArgs& A, u64 i) {
+    const u64 v = A.key64 ? static_cast<const u64*>(A.vkeys)[i] : u64(static_cast<const u32*>(A.vkeys)[i]);
+    return v >> A.vshift;
 }
 
 template <int G>
@@ -739,8 +733,10 @@ __device__ __forceinline__ void team_append(const VerifyArgs& A, u32 tmask, bool
 
 // Hit record of canonical pair (x-side position pa, z-side position pb) of a
 // run: oriented as the reference emits it — x side first (its key is the
-// smaller), diagonal blocks smaller column index first (A.8) — with the
-// order key of its (run, key, j, k) rank.
+// smaller), diagonal blocks smaller column index first (A.8). The reference
+// order inside a run is (x-side key v, j, k) (pair_search.cpp:17-21,
+// pair_search.hpp:95-97); the record keeps v in `order` and the merge sorts
+// by (rid, v, j, k).
 __device__ __forceinline__ DevHit hit_of(const VerifyArgs& A, u32 run, u32 pa, u32 pb, bool diag, double s,
                                          int32_t sint) {
     const u64 off = u64(run) * A.S;
@@ -749,22 +745,13 @@ __device__ __forceinline__ DevHit hit_of(const VerifyArgs& A, u32 run, u32 pa, u
         const u32 t = j;
         j = k;
         k = t;
-        const u32 q = pa;
-        pa = pb;
-        pb = q;
-    }
-    u32 pf = pa, ps = pb;
-    if (A.bend) {
-        pf = stable_pos(A, run, j);
-        ps = stable_pos(A, run, k);
     }
     DevHit h;
-    const u32 r = A.rid[run];
-    h.order = (u64(r) * A.p + pf) * A.p + ps;
+    h.order = key_at(A, off + (A.vkeys_by_pos ? pa : j));
     h.s = s;
     h.j = j;
     h.k = k;
-    h.rid = r;
+    h.rid = A.rid[run];
     h.sint = sint;
     return h;
 }

@@ -46,7 +46,7 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "sort", "segments"])
+@pytest.mark.parametrize("grouping", ["auto", "sort", "segments", "merge_large"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
 def test_search_matches_reference_fixture(name, grouping, monkeypatch):
     """All grouping paths: counting sort into 2^M buckets (default here),
@@ -55,6 +55,8 @@ def test_search_matches_reference_fixture(name, grouping, monkeypatch):
         monkeypatch.setenv("XYZB_GROUPING", "sort")
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
+    if grouping == "merge_large":  # the multi-kernel merge instead of the single-CTA one
+        monkeypatch.setenv("XYZB_MERGE_LARGE", "1")
     xb = _engine()
     x, y, cfg, z = load_case(name)
     rep = xb.Dataset(x).search(y, cfg)
