@@ -549,11 +549,6 @@ void run_batches(SearchCtx& c) {
         item_cap = std::min<u64>(item_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.item_scale);
     if (item_cap > 0xffffffffull) throw internal_error("xyzb: batch too large for 32-bit item indices");
     ds->items.ensure(item_cap * sizeof(kern::Item));
-    const bool use_table = M <= u64(kern::kTableBits) && (B << M) <= (u64(1) << 28) && (u64(1) << M) <= 4 * p + 1024;
-    if (use_table) {
-        ds->table.ensure((B << M) * 4);
-        ds->table_end.ensure((B << M) * 4);
-    }
     const char* sort_sel = std::getenv("XYZB_SORT");  // "segments": multi-kernel LSD sort (tests)
     // host plan -> pinned -> device
     const bool host_rows = !c.plan.rows.empty();
@@ -692,6 +687,7 @@ void run_batches(SearchCtx& c) {
         u32* npairs_b = pair_path ? ds->npairs.as<u32>() + batch_idx : nullptr;
         const u32* sv = nullptr;
         const K* sorted_keys = nullptr;
+        int vshift = 0;
         cudaEvent_t e2;
         if (buckets) {
             // ---- group: counting sort into 2^M buckets per run ----
@@ -726,41 +722,44 @@ void run_batches(SearchCtx& c) {
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 2;
         } else {
+            // symmetric keys (u = min(v, v^c), side bit): the join needs no lookups;
+            // M = 64 keeps plain keys and binary-search partner lookups
+            const bool ukeys = M + 1 <= sizeof(K) * 8;
+            const int sbits = ukeys ? bits + 1 : bits;
+            if (ukeys) {
+                kern::ukey_transform<K><<<grid_for(nb * p, 256, 4096), 256, 0, st>>>(k0, p, nb * p, ds->xorc.as<K>());
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_SORT] += 1;
+            }
             // ---- sort: one cluster per run (DSMEM histogram exchange), or the multi-kernel LSD sort ----
             int res;
             if (sort_sel && std::string(sort_sel) == "segments") {
-                res = rsort::sort_segments<K>(kb, vb, nb, p, bits, ds->hist.as<u32>(), st, &c.launches[XYZB_STAGE_SORT]);
+                res = rsort::sort_segments<K>(kb, vb, nb, p, sbits, ds->hist.as<u32>(), st, &c.launches[XYZB_STAGE_SORT]);
             } else {
-                res = rsort::sort_runs_launch<K>(kb[0], vb[0], kb[1], vb[1], nb, p, bits, st);
+                res = rsort::sort_runs_launch<K>(kb[0], vb[0], kb[1], vb[1], nb, p, sbits, st);
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_SORT] += 1;
             }
             e2 = clk.mark();
             clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((bits + 7) / 8);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((sbits + 7) / 8);
             sv = vb[res];
             sorted_keys = kb[res];
+            vshift = ukeys ? 1 : 0;
             // ---- join (+ guard bookkeeping) ----
             XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
             XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
             dim3 gj(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
-            if (use_table) {
-                // group tables, then one thread per key (partner lookups are O(1))
-                kern::group_tables<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->table.as<u32>(), ds->table_end.as<u32>());
+            if (ukeys) {
+                kern::ujoin_count<K><<<gj, 256, 0, st>>>(kb[res], p, ds->xorc.as<K>(), ds->tot.as<u64>(),
+                                                         ds->work_run.as<u64>());
                 XYZB_LAUNCH_CHECK();
-                dim3 gb(static_cast<u32>(ceil_div(u64(1) << M, 256)), static_cast<u32>(nb));
-                kern::table_join_count<K><<<gb, 256, 0, st>>>(ds->table.as<u32>(), ds->table_end.as<u32>(), kb[res], p,
-                                                              int(M), ds->xorc.as<K>(), ds->tot.as<u64>(),
-                                                              ds->work_run.as<u64>());
+                kern::ujoin_emit<K><<<gj, 256, 0, st>>>(kb[res], p, ds->xorc.as<K>(), ds->tot.as<u64>(), c.guard, hmax,
+                                                        ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
+                                                        npairs_b, ds->pairs.as<kern::PairRec>(),
+                                                        static_cast<u32>(c.pair_cap));
                 XYZB_LAUNCH_CHECK();
-                kern::table_join_emit<K><<<gb, 256, 0, st>>>(
-                    ds->table.as<u32>(), ds->table_end.as<u32>(), kb[res], p, int(M), ds->xorc.as<K>(), ds->tot.as<u64>(),
-                    c.guard, hmax, ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap), npairs_b,
-                    ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
-                XYZB_LAUNCH_CHECK();
-                c.launches[XYZB_STAGE_JOIN] += 3;
             } else {
-                // wide keys: galloping group ends + binary-search partner lookups per head
                 kern::join_count<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), nullptr,
                                                         ds->tot.as<u64>(), ds->work_run.as<u64>());
                 XYZB_LAUNCH_CHECK();
@@ -769,8 +768,8 @@ void run_batches(SearchCtx& c) {
                                                        static_cast<u32>(item_cap), npairs_b,
                                                        ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
                 XYZB_LAUNCH_CHECK();
-                c.launches[XYZB_STAGE_JOIN] += 2;
             }
+            c.launches[XYZB_STAGE_JOIN] += 2;
         }
         kern::book_runs<<<static_cast<u32>(ceil_div(nb, 256)), 256, 0, st>>>(
             static_cast<u32>(nb), ds->tot.as<u64>(), ds->work_run.as<u64>(), c.guard, rid, ds->enumerated.as<u64>(),
@@ -792,7 +791,7 @@ void run_batches(SearchCtx& c) {
         A.vkeys = buckets ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
         A.vkeys_by_pos = buckets ? 0 : 1;
         A.key64 = sizeof(K) == 8;
-        A.vshift = 0;
+        A.vshift = vshift;
         A.rid = rid;
         A.run_sign = rsign;
         A.p = p;
@@ -1137,7 +1136,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     const size_t spans0 = ds->clock.spans.size();
     for (int attempt = 0; attempt < 8; ++attempt) {
         ds->clock.spans.resize(spans0);
-        if (c.M <= 32) run_batches<u32>(c); else run_batches<u64>(c);
+        if (c.M <= 31) run_batches<u32>(c); else run_batches<u64>(c);  // u32 holds M bits + the side bit
         XYZB_CUDA(cudaMemcpyAsync(&H, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
         std::vector<u32> nitems(c.nbatches);
         XYZB_CUDA(cudaMemcpyAsync(nitems.data(), ds->nblocks.p, c.nbatches * 4, cudaMemcpyDeviceToHost, ds->stream));

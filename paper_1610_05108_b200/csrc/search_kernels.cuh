@@ -444,6 +444,118 @@ __global__ void __launch_bounds__(256) join_emit(const K* __restrict__ sk, u64 S
     emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S);
 }
 
+// ------------------------------------------------ symmetric sorted keys --
+//
+// Candidates pair key v with key v ^ c. Sorting by u = min(v, v ^ c) with a
+// side bit (0: v == u, the x side whose key is the smaller; 1: v == u ^ c)
+// puts both groups of a block next to each other — [x side][z side] — so the
+// join needs no partner lookup at all: one galloping search for the end of
+// the u-group and one for the side split (the reference sorts (key, side,
+// index) the same way, pair_search.cpp:17-21). c == 0 makes every group
+// diagonal (side 0 only).
+
+template <class K>
+__global__ void ukey_transform(K* __restrict__ keys, u64 p, u64 count, const K* __restrict__ xorc) {
+    for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < count; t += u64(gridDim.x) * blockDim.x) {
+        const K v = keys[t];
+        const K v2 = v ^ xorc[t / p];
+        keys[t] = v2 < v ? K((v2 << 1) | 1) : K(v << 1);
+    }
+}
+
+template <class K>
+__device__ __forceinline__ HeadBlock u_block(const K* a, u64 i, u64 S) {
+    HeadBlock hb;
+    if (i >= S) return hb;
+    const K w = a[i];
+    const K u = w >> 1;
+    if (i != 0 && (a[i - 1] >> 1) == u) return hb;  // not the head of its u-group
+    // the group starts on side 0 if it has an x side; find the side split and the group end
+    const u64 s = (w & 1) ? i : run_end(a, i, S, w);
+    u64 e = s;
+    if (s < S && (a[s] >> 1) == u) e = run_end(a, s, S, a[s]);
+    const u64 xc = s - i, zc = e - s;
+    if (zc == 0) {
+        // only one side present: a diagonal group when c == 0 (u == u ^ c), else no candidates
+        // (diagonal iff the partner key is the key itself, signalled by the caller through diag)
+        hb.hs = u32(i);
+        hb.hc = u32(xc);
+        return hb;
+    }
+    if (xc == 0) return hb;
+    hb.pairs = 2 * xc * zc;  // (j,k) in block u and (k,j) in block u ^ c
+    hb.work = xc * zc;
+    if (xc <= zc) {
+        hb.hs = u32(i); hb.hc = u32(xc); hb.ss = u32(s); hb.sc = u32(zc); hb.flags = 1u;
+    } else {
+        hb.hs = u32(s); hb.hc = u32(zc); hb.ss = u32(i); hb.sc = u32(xc); hb.flags = 0u;
+    }
+    return hb;
+}
+
+// c == 0: every group pairs with itself (diagonal, |E| counts the j == k pairs)
+__device__ __forceinline__ void make_diag(HeadBlock& hb) {
+    const u64 cnt = hb.hc;
+    hb.pairs = cnt * cnt;
+    if (cnt >= 2) {
+        hb.work = cnt * (cnt - 1) / 2;
+        hb.ss = hb.hs;
+        hb.sc = hb.hc;
+        hb.flags = 3u;
+    } else {
+        hb.hc = 0;
+    }
+}
+
+template <class K>
+__global__ void __launch_bounds__(256) ujoin_count(const K* __restrict__ sk, u64 S, const K* __restrict__ xorc,
+                                                   u64* __restrict__ tot, u64* __restrict__ work_run) {
+    __shared__ u64 red[2][8];
+    const u32 b = blockIdx.y;
+    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    HeadBlock hb = u_block(sk + u64(b) * S, i, S);
+    if (xorc[b] == 0) {
+        if (hb.hc) make_diag(hb);
+    } else if (hb.work == 0) {
+        hb = HeadBlock();
+    }
+    const u64 ws = warp_sum(hb.pairs), ww = warp_sum(hb.work);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = ws;
+        red[1][threadIdx.x >> 5] = ww;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 t0 = 0, t1 = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+            t0 += red[0][w];
+            t1 += red[1][w];
+        }
+        if (t0) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(t0));
+        if (t1) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(t1));
+    }
+}
+
+template <class K>
+__global__ void __launch_bounds__(256) ujoin_emit(const K* __restrict__ sk, u64 S, const K* __restrict__ xorc,
+                                                  const u64* __restrict__ tot, u64 guard, u32 hmax,
+                                                  Item* __restrict__ items, u32* __restrict__ nitems, u32 item_cap,
+                                                  u32* __restrict__ npairs, PairRec* __restrict__ pairs,
+                                                  u32 pair_cap) {
+    const u32 b = blockIdx.y;
+    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    HeadBlock hb;
+    if (tot[b] <= guard) {
+        hb = u_block(sk + u64(b) * S, i, S);
+        if (xorc[b] == 0) {
+            if (hb.hc) make_diag(hb);
+        } else if (hb.work == 0) {
+            hb = HeadBlock();
+        }
+    }
+    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S);
+}
+
 // ------------------------------------------- sorted keys + group tables --
 //
 // After the per-run sort, one thread per sorted position records where each
