@@ -173,13 +173,18 @@ def peaks():
 
 
 def ncu_traffic():
-    """dram bytes per verify launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "verify_traffic.json")
-    try:
-        with open(p) as f:
-            return json.load(f)
-    except Exception:
-        return None
+    """dram bytes per verify launch from the committed ncu --set full capture
+    of this workload (profiles/verify_traffic*.json), else None."""
+    for name in ("verify_traffic.json", f"verify_traffic_{WORKLOAD['name']}.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        try:
+            with open(p) as f:
+                d = json.load(f)
+            if d.get("config", "").startswith(WORKLOAD["name"]):
+                return d
+        except Exception:
+            pass
+    return None
 
 
 def ref_cpu_time(x, y, l_sample, threads, steps=1):
@@ -315,13 +320,14 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "runs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded GWAS-like generator, include/xyzb_synth.h)",
+            "vs_baseline": None, "dtype": "u64" if WORKLOAD["mode"] == "binary" else "f32 data, f64 accumulation",
+            "data": f"synthetic (seeded {WORKLOAD['name']} generator, include/xyzb_synth.h)",
             "config": workload_config(world, L),
             "verified_pairs_per_s": verified / (t_dev / 1e3),
             "wall_ms_per_step": 1e3 * t_wall / args.steps,
             "stage_ms_per_step": {k: v / args.steps for k, v in stage.items()},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "verify_binary", "achieved": achieved, "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": "verify_pairs_binary" if WORKLOAD["mode"] == "binary" else "verify_items<RealStrength>", "achieved": achieved, "peak": hbm,
                          "peak_source": src, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
                          "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                          "algorithmic_bytes_per_launch": verify_bytes / max(1, verify_launches),

@@ -13,8 +13,9 @@
  *  gauss  : X ~ N(0,1) columns standardised (mean 0, sd 1), stored fp32-exact;
  *           Y = sum_q theta X_aq X_bq + noise_sd * N(0,1).
  *  ar1    : blocks of `block` columns, Z_j = rho Z_{j-1} + sqrt(1-rho^2) e,
- *           X = +1 iff Z > 0; Y = sign(sum_q X_aq X_bq) (ties +1), then each
- *           row flipped with probability `flip`.
+ *           e standardised Irwin-Hall(4) (a near-Gaussian, cheap enough for
+ *           1e10 entries), X = +1 iff Z > 0; Y = sign(sum_q X_aq X_bq) (ties
+ *           +1), then each row flipped with probability `flip`.
  * All non-toy generators are counter-based (splitmix64 of seed/column/row),
  * so they are deterministic for any thread count.
  */

@@ -552,7 +552,9 @@ void run_batches(SearchCtx& c) {
     const char* sort_sel = std::getenv("XYZB_SORT");  // "segments": multi-kernel LSD sort (tests)
     // host plan -> pinned -> device
     const bool host_rows = !c.plan.rows.empty();
-    const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 96;
+    // per-batch counters live in their own pinned slots: a later batch must not
+    // overwrite a value an earlier, still-queued copy has not read yet
+    const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 2 * R * 4 + 96;
     ds->h_rows.ensure(hbytes);
     char* hp = ds->h_rows.as<char>();
     std::memcpy(hp, c.plan.rid.data(), R * 4);
@@ -613,7 +615,7 @@ void run_batches(SearchCtx& c) {
     // (fastest measured on B200 for config 2), else the per-run cluster radix
     // sort; XYZB_GROUPING=sort / XYZB_SORT=segments force the sorted paths
     const char* gsel = std::getenv("XYZB_GROUPING");
-    const bool buckets = M <= u64(kern::kTableBits) && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
+    const bool buckets = M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
                          !(gsel && std::string(gsel) == "sort") && !sort_sel;
     if (buckets) {
         ds->bcnt.ensure((B << M) * 4);
@@ -666,7 +668,7 @@ void run_batches(SearchCtx& c) {
                     c.launches[XYZB_STAGE_PROJECT] += 2;
                 }
                 if (coins) {
-                    u32* cnt = reinterpret_cast<u32*>(hp + hbytes - 16);
+                    u32* cnt = reinterpret_cast<u32*>(hp + hbytes - 96 - 2 * R * 4) + 2 * batch_idx + 1;
                     *cnt = static_cast<u32>(nb * p);
                     XYZB_CUDA(cudaMemcpyAsync(ds->zcnt_n.p, cnt, 4, cudaMemcpyHostToDevice, st));
                     scan::exclusive<u32>(ds->zcount.as<u32>(), ds->zcnt_n.as<u32>(), ds->zoff.as<u32>(),
@@ -696,7 +698,7 @@ void run_batches(SearchCtx& c) {
             dim3 gp(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
             kern::bucket_count<K><<<gp, 256, 0, st>>>(k0, p, int(M), ds->bcnt.as<u32>());
             XYZB_LAUNCH_CHECK();
-            u32* hn = reinterpret_cast<u32*>(hp + hbytes - 32);
+            u32* hn = reinterpret_cast<u32*>(hp + hbytes - 96 - 2 * R * 4) + 2 * batch_idx;
             *hn = static_cast<u32>(nbk);
             XYZB_CUDA(cudaMemcpyAsync(ds->bsize.p, hn, 4, cudaMemcpyHostToDevice, st));
             scan::exclusive<u32>(ds->bcnt.as<u32>(), ds->bsize.as<u32>(), ds->bend.as<u32>(),
@@ -1372,9 +1374,9 @@ extern "C" int xyzb_project_keys(xyzb_dataset* ds, const uint32_t* draws, uint64
         XYZB_CUDA(cudaMemsetAsync(yk.p, 0, ds->Wp * 8, st));
         XYZB_CUDA(cudaMemsetAsync(sg.p, 1, n_draws, st));
         XYZB_CUDA(cudaMemcpyAsync(rows.p, draws, n_draws * m * 4, cudaMemcpyHostToDevice, st));
-        dim3 g(static_cast<u32>(ceil_div(ds->p, 256)), static_cast<u32>(n_draws));
-        kern::project_bits<u64><<<g, 256, 0, st>>>(ds->Xr.as<u32>(), ds->P32, ds->p, rows.as<u32>(), int(m),
-                                                   yk.as<u64>(), sg.as<int8_t>(), kout.as<u64>(), xc.as<u64>());
+        dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(n_draws));
+        kern::project_bits_t<u64><<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, ds->p, rows.as<u32>(), int(m),
+                                                     kout.as<u64>());
         XYZB_LAUNCH_CHECK();
         XYZB_CUDA(cudaMemcpyAsync(keys, kout.p, n_draws * ds->p * 8, cudaMemcpyDeviceToHost, st));
         XYZB_CUDA(cudaStreamSynchronize(st));

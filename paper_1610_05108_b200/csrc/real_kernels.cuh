@@ -93,34 +93,6 @@ __global__ void resp_xorc(const u32* __restrict__ rows, int M, const double* __r
     xorc[b] = K(~rp & mask);
 }
 
-// Sign transform, deterministic part: x-key bit = (v > 0), plus a zero mask
-// of the entries that need a coin. From row-major bit planes.
-template <class K>
-__global__ void __launch_bounds__(256) project_sign(const u32* __restrict__ Xpos, const u32* __restrict__ Xzero,
-                                                    u64 P32, u64 p, const u32* __restrict__ rows, int M,
-                                                    int with_zero, K* __restrict__ keys, K* __restrict__ zmask,
-                                                    u32* __restrict__ zcount) {
-    __shared__ u32 srow[64];
-    const u64 b = blockIdx.y;
-    if (threadIdx.x < M) srow[threadIdx.x] = rows[b * M + threadIdx.x];
-    __syncthreads();
-    const u64 j = u64(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= p) return;
-    const int sh = int(j & 31);
-    K key = 0, zm = 0;
-#pragma unroll 8
-    for (int s = 0; s < M; ++s) {
-        const u64 off = u64(srow[s]) * P32 + (j >> 5);
-        key |= K((__ldg(Xpos + off) >> sh) & 1u) << s;
-        if (with_zero) zm |= K((__ldg(Xzero + off) >> sh) & 1u) << s;
-    }
-    keys[b * p + j] = key;
-    if (with_zero) {
-        zmask[b * p + j] = zm;
-        zcount[b * p + j] = __popcll(static_cast<unsigned long long>(zm));
-    }
-}
-
 template <class K>
 __global__ void popc_count(const K* __restrict__ m, u64 count, u32* __restrict__ out) {
     for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < count; t += u64(gridDim.x) * blockDim.x)

@@ -4,7 +4,6 @@
 //   project_bits     M-bit keys of every column for every run of the batch
 //                    (project_keys, projection.cpp:32-57) + the per-run XOR
 //                    constant c that turns x-keys into z-keys (A.3)
-//   head_table       direct-address table key -> first sorted position
 //   join             bucket join over the sorted keys: equal-key groups,
 //                    partner group of key^c, |E_r| incl. the diagonal, and
 //                    canonical work items (equal_pairs, pair_search.cpp:35-53;
@@ -78,51 +77,6 @@ __global__ void transpose_bits(const u64* __restrict__ Xc, u64 Wp, u64 W, u64 n,
 template <class K>
 __device__ __forceinline__ K key_mask(int m) {
     return m >= int(sizeof(K) * 8) ? ~K(0) : ((K(1) << m) - 1);
-}
-
-// keys[b][j] = sum_s bit(X[rows[b][s], j]) << s; xorc[b] = c of the run.
-// Warps read one row-plane word per s for 32 consecutive columns (broadcast).
-template <class K>
-__global__ void __launch_bounds__(256) project_bits(const u32* __restrict__ Xr, u64 P32, u64 p,
-                                                    const u32* __restrict__ rows, int M,
-                                                    const u64* __restrict__ ykey_bits,
-                                                    const int8_t* __restrict__ run_sign, K* __restrict__ keys,
-                                                    K* __restrict__ xorc) {
-    __shared__ u32 srow[64];
-    const u64 b = blockIdx.y;
-    if (threadIdx.x < M) srow[threadIdx.x] = rows[b * M + threadIdx.x];
-    __syncthreads();
-    const u64 j = u64(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j < p) {
-        const u32* base = Xr + (j >> 5);
-        const int sh = int(j & 31);
-        K key = 0;
-#pragma unroll 8
-        for (int s = 0; s < M; ++s) {
-            const u32 w = __ldg(base + u64(srow[s]) * P32);
-            key |= K((w >> sh) & 1u) << s;
-        }
-        keys[b * p + j] = key;
-    }
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        u64 yk = 0;
-        for (int s0 = 0; s0 < M; s0 += 32) {
-            const int s = s0 + lane;
-            int bit = 0;
-            if (s < M) {
-                const u32 r = srow[s];
-                bit = int((ykey_bits[r >> 6] >> (r & 63)) & 1ull);
-            }
-            yk |= u64(__ballot_sync(0xffffffffu, bit)) << s0;
-        }
-        if (lane == 0) {
-            const K mask = key_mask<K>(M);
-            const K ykk = K(yk) & mask;
-            // z+ = ~(x ^ y) & mask = x ^ (~y & mask); z- = x ^ y  (A.3)
-            xorc[b] = run_sign[b] > 0 ? K(~ykk & mask) : ykk;
-        }
-    }
 }
 
 // In-register 32 x 32 bit transpose, LSB-first: afterwards a[c] bit s equals
@@ -232,21 +186,6 @@ __device__ __forceinline__ u64 lower_bound(const K* a, u64 lo, u64 hi, K v) {
         if (a[mid] < v) lo = mid + 1; else hi = mid;
     }
     return lo;
-}
-
-// Direct-address head table for M <= kTableBits: table[b][key] = first sorted
-// position of key in run b. Never cleared: a lookup is trusted only if the
-// stored position holds the key (stale entries from earlier batches fail it).
-constexpr int kTableBits = 22;
-
-template <class K>
-__global__ void __launch_bounds__(256) head_table(const K* __restrict__ sk, u64 S, int M, u32* __restrict__ table) {
-    const u32 b = blockIdx.y;
-    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= S) return;
-    const K* a = sk + u64(b) * S;
-    const K v = a[i];
-    if (i == 0 || a[i - 1] != v) table[(u64(b) << M) + u64(v)] = u32(i);
 }
 
 // The canonical block owned by the head of an equal-key group at sorted
@@ -553,115 +492,6 @@ __global__ void __launch_bounds__(256) ujoin_emit(const K* __restrict__ sk, u64 
             hb = HeadBlock();
         }
     }
-    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S);
-}
-
-// ------------------------------------------- sorted keys + group tables --
-//
-// After the per-run sort, one thread per sorted position records where each
-// equal-key group starts (head) and ends (tail) in direct-address tables
-// [B][2^M]. The tables are never cleared: an entry is trusted only if the
-// sorted key at the recorded start equals the bucket's key (stale entries
-// from earlier batches fail the check; an absent key cannot pass it).
-
-template <class K>
-__global__ void __launch_bounds__(256) group_tables(const K* __restrict__ sk, u64 S, int M, u32* __restrict__ tb,
-                                                    u32* __restrict__ te) {
-    const u64 b = blockIdx.y;
-    const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= S) return;
-    const K* a = sk + b * S;
-    const K v = a[i];
-    if (i == 0 || a[i - 1] != v) tb[(b << M) + u64(v)] = u32(i);
-    if (i + 1 == S || a[i + 1] != v) te[(b << M) + u64(v)] = u32(i + 1);
-}
-
-template <class K>
-__device__ __forceinline__ bool table_group(const u32* __restrict__ tb, const u32* __restrict__ te,
-                                            const K* __restrict__ a, u64 S, u64 bi, u64 key, u32& beg, u32& cnt) {
-    const u32 t = tb[bi];
-    if (t < S && u64(a[t]) == key) {
-        beg = t;
-        cnt = te[bi] - t;
-        return true;
-    }
-    return false;
-}
-
-// The block owned by key v of run b (positions local to the run).
-template <class K>
-__device__ __forceinline__ HeadBlock table_block(const u32* __restrict__ tb, const u32* __restrict__ te,
-                                                 const K* __restrict__ sk, u64 S, u64 b, int M, u64 v, u64 c) {
-    HeadBlock hb;
-    const K* a = sk + b * S;
-    u32 bx, cx;
-    if (!table_group(tb, te, a, S, (b << M) + v, v, bx, cx)) return hb;
-    const u64 v2 = v ^ c;
-    const u64 cv = cx;
-    if (v2 == v) {
-        hb.pairs = cv * cv;  // the diagonal j == k counts (pair_search.cpp:48-49)
-        if (cv >= 2) {
-            hb.work = cv * (cv - 1) / 2;
-            hb.hs = bx;
-            hb.hc = cx;
-            hb.ss = bx;
-            hb.sc = cx;
-            hb.flags = 3u;
-        }
-    } else if (v2 > v) {
-        u32 bz, cz;
-        if (table_group(tb, te, a, S, (b << M) + v2, v2, bz, cz)) {
-            hb.pairs = 2 * cv * cz;  // (j,k) in block v and (k,j) in block v^c
-            hb.work = cv * cz;
-            if (cx <= cz) {
-                hb.hs = bx; hb.hc = cx; hb.ss = bz; hb.sc = cz; hb.flags = 1u;
-            } else {
-                hb.hs = bz; hb.hc = cz; hb.ss = bx; hb.sc = cx; hb.flags = 0u;
-            }
-        }
-    }
-    return hb;
-}
-
-template <class K>
-__global__ void __launch_bounds__(256) table_join_count(const u32* __restrict__ tb, const u32* __restrict__ te,
-                                                        const K* __restrict__ sk, u64 S, int M,
-                                                        const K* __restrict__ xorc, u64* __restrict__ tot,
-                                                        u64* __restrict__ work_run) {
-    __shared__ u64 red[2][8];
-    const u32 b = blockIdx.y;
-    const u64 v = u64(blockIdx.x) * blockDim.x + threadIdx.x;
-    HeadBlock hb;
-    if (v < (u64(1) << M)) hb = table_block(tb, te, sk, S, b, M, v, u64(xorc[b]));
-    const u64 ws = warp_sum(hb.pairs), ww = warp_sum(hb.work);
-    if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = ws;
-        red[1][threadIdx.x >> 5] = ww;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        u64 t0 = 0, t1 = 0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
-            t0 += red[0][w];
-            t1 += red[1][w];
-        }
-        if (t0) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(t0));
-        if (t1) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(t1));
-    }
-}
-
-template <class K>
-__global__ void __launch_bounds__(256) table_join_emit(const u32* __restrict__ tb, const u32* __restrict__ te,
-                                                       const K* __restrict__ sk, u64 S, int M,
-                                                       const K* __restrict__ xorc, const u64* __restrict__ tot,
-                                                       u64 guard, u32 hmax, Item* __restrict__ items,
-                                                       u32* __restrict__ nitems, u32 item_cap,
-                                                       u32* __restrict__ npairs, PairRec* __restrict__ pairs,
-                                                       u32 pair_cap) {
-    const u32 b = blockIdx.y;
-    const u64 v = u64(blockIdx.x) * blockDim.x + threadIdx.x;
-    HeadBlock hb;
-    if (v < (u64(1) << M) && tot[b] <= guard) hb = table_block(tb, te, sk, S, b, M, v, u64(xorc[b]));
     emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S);
 }
 

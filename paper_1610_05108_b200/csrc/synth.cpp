@@ -29,6 +29,11 @@ struct Counter {  // splitmix64 sequence keyed by (seed, stream)
         const double u2 = unit();
         return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
     }
+    float fast_normal() {  // Irwin-Hall(4) standardised: 2 draws, no transcendentals
+        const uint64_t a = next(), b = next();
+        const float s = float(uint32_t(a)) + float(uint32_t(a >> 32)) + float(uint32_t(b)) + float(uint32_t(b >> 32));
+        return (s * 2.3283064365386963e-10f - 2.0f) * 1.7320508075688772f;
+    }
 };
 
 void planted_pairs(uint64_t p, uint64_t n_pairs, uint64_t seed, uint32_t* pairs) {
@@ -170,18 +175,19 @@ int xyzb_synth_ar1(uint64_t n, uint64_t p, uint64_t block, double rho, uint64_t 
     const uint64_t nblk = (p + block - 1) / block;
     const double sr = std::sqrt(1.0 - rho * rho);
     // one task per (column block, 64-row word)
+    const float rf = float(rho), srf = float(sr);
     parallel_for(int64_t(nblk * W), [&](int64_t t) {
         const uint64_t cb = uint64_t(t) / W, w = uint64_t(t) % W;
         Counter r(seed, (cb << 24) ^ w ^ 0x77);
         const uint64_t rows = std::min<uint64_t>(64, n - w * 64);
-        double z[64];
-        for (uint64_t b = 0; b < rows; ++b) z[b] = r.normal();
+        float z[64];
+        for (uint64_t b = 0; b < rows; ++b) z[b] = r.fast_normal();
         for (uint64_t c = cb * block; c < std::min(p, (cb + 1) * block); ++c) {
             if (c != cb * block)
-                for (uint64_t b = 0; b < rows; ++b) z[b] = rho * z[b] + sr * r.normal();
+                for (uint64_t b = 0; b < rows; ++b) z[b] = rf * z[b] + srf * r.fast_normal();
             uint64_t word = 0;
             for (uint64_t b = 0; b < rows; ++b)
-                if (z[b] > 0.0) word |= 1ull << b;
+                if (z[b] > 0.0f) word |= 1ull << b;
             x_words[c * W + w] = word;
         }
     });

@@ -204,7 +204,7 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
         monkeypatch.setenv("XYZB_GROUPING", "sort")
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
-    monkeypatch.setenv("XYZB_BATCH_ENTRIES", "3000")  # one run per batch
+    monkeypatch.setenv("XYZB_BATCH_ENTRIES", "6000")  # three runs per batch, a shorter last batch
     monkeypatch.setenv("XYZB_HIT_CAP", "7")
     monkeypatch.setenv("XYZB_ITEM_CAP", "5")
     monkeypatch.setenv("XYZB_PAIR_CAP", "100")
