@@ -76,9 +76,10 @@ def parse():
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--config", default="gwas", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="gwas", choices=sorted(WORKLOADS) + ["lasso"])
     args = ap.parse_args()
-    select(args.config)
+    if args.config != "lasso":
+        select(args.config)
     return args
 
 
@@ -242,8 +243,74 @@ def workload_config(n_gpus, l_per_rank):
             "parallelism": f"run-shard{n_gpus}"}
 
 
+LASSO = dict(name="lasso_cfg5", n=1000, p=20000, n_mains=10, beta=1.0, n_pairs=10, theta=1.0, noise_sd=0.5, seed=5,
+             grid_size=20, grid_ratio=0.05, kkt_l=100, kkt_max_candidates=16 * 20000, path_seed=7)
+
+
+def run_lasso(args):
+    """BASELINE config 5: the reference's own lasso_path (xyz-regression) with
+    its KKT screen on the GPU (build/dropin: reference core, search.cpp replaced
+    by the shim) against the all-CPU reference build, same inputs/config.
+    kkt_max_candidates pinned to 16p on both sides (the
+    reference default, unlimited, runs out of memory)."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from paper_1610_05108_b200 import synth
+    from tests import checkers as ck
+    L = LASSO
+    x, y, pairs, mains = synth.gauss(L["n"], L["p"], L["n_pairs"], L["theta"], L["noise_sd"], L["n_mains"], L["beta"],
+                                     L["seed"])
+    kw = dict(grid_size=L["grid_size"], grid_ratio=L["grid_ratio"], kkt_l=L["kkt_l"],
+              kkt_max_candidates=L["kkt_max_candidates"], seed=L["path_seed"])
+    cfg = {"workload": L["name"], "n": L["n"], "p": L["p"], "grid_size": L["grid_size"], "grid_ratio": L["grid_ratio"],
+           "kkt_l": L["kkt_l"], "kkt_max_candidates": L["kkt_max_candidates"], "screen": "continuous-XY unbiased"}
+    threads = os.cpu_count() or 1
+    metric = "xyz-Lasso path wall time (BASELINE cfg5, n=1000 p=20000, 20-lambda path, xyz screen L=100)"
+    if args.impl == "reference":
+        secs = []
+        for _ in range(max(1, args.steps)):
+            fits, w = ck.lasso_path(ck.ref_lasso_lib(), x, y, threads=threads, **kw)
+            secs.append(w)
+        v = statistics.median(secs)
+        print(json.dumps({"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": 0, "ms_per_step": 1e3 * v, "higher_is_better": False,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+                          "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "reference",
+                                           "sample": "full lasso path"},
+                          "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    gpu_secs = []
+    for _ in range(max(1, args.warmup)):
+        ck.lasso_path(ck.dropin_lib(), x, y, threads=1, **kw)
+    for _ in range(max(1, args.steps)):
+        gfits, w = ck.lasso_path(ck.dropin_lib(), x, y, threads=1, **kw)
+        gpu_secs.append(w)
+    cfits, cw = ck.lasso_path(ck.ref_lasso_lib(), x, y, threads=threads, **kw)
+    maxdiff = 0.0
+    for g, c in zip(gfits, cfits):
+        for name in ("beta", "theta"):
+            for k in set(g[name]) | set(c[name]):
+                maxdiff = max(maxdiff, abs(g[name].get(k, 0.0) - c[name].get(k, 0.0)))
+    v = statistics.median(gpu_secs)
+    print(json.dumps({"metric": metric, "value": v, "unit": "s", "n_gpus": 1, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": 1e3 * v, "higher_is_better": False, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f32 data, f64 accumulation (screen); f64 (solver)",
+                      "data": "synthetic (seeded Gaussian design, 10 mains + 10 pairs)", "config": cfg,
+                      "coef_max_abs_diff_vs_reference": maxdiff, "fits": len(gfits),
+                      "final_support": {"mains": len(gfits[-1]["beta"]), "pairs": len(gfits[-1]["theta"])},
+                      "cpu_baseline": {"value": cw, "unit": "s", "cores": threads, "kind": "reference",
+                                       "sample": "full lasso path, reference core, threads=nproc"},
+                      "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": x.values.nbytes,
+                              "d2h_bytes_per_step": 0,
+                              "note": "lasso_path wall clock through the drop-in (host arrays in, coefficients out)"}}))
+
+
 def main():
     args = parse()
+    if args.config == "lasso":
+        run_lasso(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
