@@ -808,8 +808,18 @@ void run_batches(SearchCtx& c) {
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 1;
             const u64 W2 = ds->Wp / 2;
+            // team of G lanes, NIT 16-byte chunks of each column per lane; XYZB_VP_CHUNKS
+            // (1/2/4) and XYZB_VERIFY=simple select measured variants
+            // measured on B200 (tools/sweep_verify.py): long columns (>= 512 B) prefer 8-lane
+            // teams with 64 B per lane and column, short ones full-column teams with the
+            // next pair's columns prefetched
+            u64 chunks = W2 >= 32 ? 4 : 1;
+            bool simple = W2 >= 32;
+            if (const char* ev = std::getenv("XYZB_VP_CHUNKS"))
+                chunks = std::min<u64>(4, std::max<u64>(1, std::strtoull(ev, nullptr, 10)));
+            if (const char* ev = std::getenv("XYZB_VERIFY")) simple = std::string(ev) != "pipelined";
             int G = 1;
-            while (G < 32 && u64(G) * 4 < W2) G <<= 1;
+            while (G < 32 && u64(G) * chunks < W2) G <<= 1;
             const int nit = static_cast<int>(ceil_div(W2, G));
             const auto* PR = ds->pairs.as<kern::PairRec>();
             const u32 pc = static_cast<u32>(c.pair_cap);
@@ -819,7 +829,13 @@ void run_batches(SearchCtx& c) {
             const u32 n32 = static_cast<u32>(c.n);
             cudaEvent_t ev0 = clk.mark();
             clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
-#define XYZB_VP(GG, NN) kern::verify_pairs_binary<GG, NN><<<vgrid, 256, 0, st>>>(A, PR, np, pc, X, Wp, Y, n32, c.astar)
+#define XYZB_VP(GG, NN)                                                                                          \
+    do {                                                                                                         \
+        if (simple)                                                                                              \
+            kern::verify_pairs_simple<GG, NN><<<vgrid, 256, 0, st>>>(A, PR, np, pc, X, Wp, Y, n32, c.astar);     \
+        else                                                                                                     \
+            kern::verify_pairs_binary<GG, NN><<<vgrid, 256, 0, st>>>(A, PR, np, pc, X, Wp, Y, n32, c.astar);     \
+    } while (0)
 #define XYZB_VP4(GG) \
     switch (nit) { case 1: XYZB_VP(GG, 1); break; case 2: XYZB_VP(GG, 2); break; case 3: XYZB_VP(GG, 3); break; default: XYZB_VP(GG, 4); }
             switch (G) {

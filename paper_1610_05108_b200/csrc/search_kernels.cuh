@@ -749,16 +749,38 @@ __global__ void __launch_bounds__(256) expand_pairs(const Item* __restrict__ ite
     }
 }
 
-// Binary verify over the pair list: a team of G lanes per pair, NIT x 16 B of
-// each column per lane (up to 2 x 64 B in flight per lane), teams walk
-// contiguous chunks of kPairChunk pairs so shared columns hit in L1.
-constexpr u32 kPairChunk = 32;
+template <int G, int NIT>
+struct ColPair {
+    ulonglong2 a[NIT], b[NIT];
+};
+
+template <int G, int NIT>
+__device__ __forceinline__ void load_cols(ColPair<G, NIT>& c, const ulonglong2* X2, u32 W2, u32 j, u32 k, int tl) {
+    const ulonglong2* xj = X2 + u64(j) * W2;
+    const ulonglong2* xk = X2 + u64(k) * W2;
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const u32 wi = it * G + tl;
+        c.a[it] = wi < W2 ? __ldg(xj + wi) : make_ulonglong2(0, 0);
+        c.b[it] = wi < W2 ? __ldg(xk + wi) : make_ulonglong2(0, 0);
+    }
+}
+
+// Binary verify over the pair list. A team of G lanes owns a chunk of
+// G * kPairsPerLane consecutive pairs: the pair records and their column
+// indices are fetched for the whole chunk up front (one coalesced request per
+// lane, no per-pair dependent loads), then the team walks the chunk with the
+// next pair's columns already in flight while the current pair is reduced.
+// popc(X_j ^ X_k ^ Y) over NIT x 16 B per lane, team reduction, integer hit
+// test by the pair's owning lane.
+constexpr u32 kPairsPerLane = 2;
 
 template <int G, int NIT>
 __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const PairRec* __restrict__ pairs,
                                                            const u32* __restrict__ npairs, u32 pair_cap,
                                                            const u64* __restrict__ Xc, u32 Wp,
                                                            const u64* __restrict__ Yw, u32 n, u32 astar) {
+    constexpr u32 CH = G * kPairsPerLane;
     const int lane = threadIdx.x & 31;
     const int tl = lane & (G - 1);
     const u32 tmask = team_mask_of<G>(lane);
@@ -773,24 +795,107 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
     const u32 P = min(*npairs, pair_cap);
     const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
-    for (u64 c0 = team * kPairChunk; c0 < P; c0 += nteams * kPairChunk) {
-        const u32 c1 = u32(minu(P, c0 + kPairChunk));
-        for (u32 q = u32(c0); q < c1; ++q) {
-            const PairRec pr = pairs[q];
-            const u32 j = A.sv[pr.pa], k = A.sv[pr.pb];
-            const ulonglong2* xj = X2 + u64(j) * W2;
-            const ulonglong2* xk = X2 + u64(k) * W2;
-            ulonglong2 a[NIT], b[NIT];
+    for (u64 c0 = team * CH; c0 < P; c0 += nteams * CH) {
+        const u32 cnt = u32(minu(CH, P - c0));
+        // chunk prologue: this lane's records (pairs c0 + tl + G*i) and their columns
+        PairRec pr[kPairsPerLane];
+        u32 cj[kPairsPerLane], ck[kPairsPerLane];
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) {
-                const u32 wi = it * G + tl;
-                a[it] = wi < W2 ? __ldg(xj + wi) : make_ulonglong2(0, 0);
-                b[it] = wi < W2 ? __ldg(xk + wi) : make_ulonglong2(0, 0);
+        for (u32 i = 0; i < kPairsPerLane; ++i) {
+            const u32 t = tl + G * i;
+            if (t < cnt) {
+                pr[i] = pairs[c0 + t];
+                cj[i] = A.sv[pr[i].pa];
+                ck[i] = A.sv[pr[i].pb];
+            } else {
+                pr[i] = PairRec{0, 0, 0, 0};
+                cj[i] = ck[i] = 0;
+            }
+        }
+        auto jk_of = [&](u32 t, u32& j, u32& k) {
+            const u32 i = t / G, src = t % G;
+            u32 mj = 0, mk = 0;
+#pragma unroll
+            for (u32 q = 0; q < kPairsPerLane; ++q)
+                if (q == i) {
+                    mj = cj[q];
+                    mk = ck[q];
+                }
+            j = __shfl_sync(tmask, mj, src, G);
+            k = __shfl_sync(tmask, mk, src, G);
+        };
+        ColPair<G, NIT> cur, nxt;
+        u32 j0, k0;
+        jk_of(0, j0, k0);
+        load_cols<G, NIT>(cur, X2, W2, j0, k0, tl);
+        for (u32 t = 0; t < cnt; ++t) {
+            if (t + 1 < cnt) {
+                u32 j1, k1;
+                jk_of(t + 1, j1, k1);
+                load_cols<G, NIT>(nxt, X2, W2, j1, k1, tl);
             }
             u32 acc = 0;
 #pragma unroll
             for (int it = 0; it < NIT; ++it)
-                acc += __popcll(a[it].x ^ b[it].x ^ yv[it].x) + __popcll(a[it].y ^ b[it].y ^ yv[it].y);
+                acc += __popcll(cur.a[it].x ^ cur.b[it].x ^ yv[it].x) + __popcll(cur.a[it].y ^ cur.b[it].y ^ yv[it].y);
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(tmask, acc, o);
+            // the owning lane tests pair t with its record
+            bool hit = false;
+            DevHit h;
+            if (u32(tl) == t % G) {
+                const u32 i = t / G;
+                PairRec r = pr[0];
+#pragma unroll
+                for (u32 q = 1; q < kPairsPerLane; ++q)
+                    if (q == i) r = pr[q];
+                const u32 si = A.run_sign[r.run] > 0 ? acc : n - acc;
+                hit = si >= astar;
+                if (hit) {
+                    const u64 base = u64(r.run) * A.S;
+                    h = hit_of(A, r.run, u32(r.pa - base), u32(r.pb - base), (r.pad & 2u) != 0,
+                               double(si) / double(n), int32_t(si));
+                }
+            }
+            team_append<G>(A, tmask, hit, h);
+            if (t + 1 < cnt) cur = nxt;
+        }
+    }
+}
+
+// Simple pair walk (one pair at a time per team, chunks of 32 pairs): kept
+// beside the pipelined walk for measurement (XYZB_VERIFY=simple).
+template <int G, int NIT>
+__global__ void __launch_bounds__(256) verify_pairs_simple(VerifyArgs A, const PairRec* __restrict__ pairs,
+                                                           const u32* __restrict__ npairs, u32 pair_cap,
+                                                           const u64* __restrict__ Xc, u32 Wp,
+                                                           const u64* __restrict__ Yw, u32 n, u32 astar) {
+    constexpr u32 CH = 32;
+    const int lane = threadIdx.x & 31;
+    const int tl = lane & (G - 1);
+    const u32 tmask = team_mask_of<G>(lane);
+    const u32 W2 = Wp / 2;
+    const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(Xc);
+    ulonglong2 yv[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+        const u32 wi = it * G + tl;
+        yv[it] = wi < W2 ? __ldg(reinterpret_cast<const ulonglong2*>(Yw) + wi) : make_ulonglong2(0, 0);
+    }
+    const u32 P = min(*npairs, pair_cap);
+    const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+    const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
+    for (u64 c0 = team * CH; c0 < P; c0 += nteams * CH) {
+        const u32 c1 = u32(minu(P, c0 + CH));
+        for (u32 q = u32(c0); q < c1; ++q) {
+            const PairRec pr = pairs[q];
+            const u32 j = A.sv[pr.pa], k = A.sv[pr.pb];
+            ColPair<G, NIT> c;
+            load_cols<G, NIT>(c, X2, W2, j, k, tl);
+            u32 acc = 0;
+#pragma unroll
+            for (int it = 0; it < NIT; ++it)
+                acc += __popcll(c.a[it].x ^ c.b[it].x ^ yv[it].x) + __popcll(c.a[it].y ^ c.b[it].y ^ yv[it].y);
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(tmask, acc, o);
             const u32 si = A.run_sign[pr.run] > 0 ? acc : n - acc;
