@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/xyzb.h"
+#include "cluster_group.cuh"
 #include "common.cuh"
 #include "draws.cuh"
 #include "host_rng.hpp"
@@ -615,7 +616,11 @@ void run_batches(SearchCtx& c) {
     // (fastest measured on B200 for config 2), else the per-run cluster radix
     // sort; XYZB_GROUPING=sort / XYZB_SORT=segments force the sorted paths
     const char* gsel = std::getenv("XYZB_GROUPING");
-    const bool buckets = M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
+    // M <= 17: grouping and join fused per run on a cluster (tables in DSMEM);
+    // XYZB_GROUPING=bucket keeps the multi-kernel counting sort
+    const bool cluster_path = M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
+                              !(gsel && (std::string(gsel) == "sort" || std::string(gsel) == "bucket"));
+    const bool buckets = !cluster_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
                          !(gsel && std::string(gsel) == "sort") && !sort_sel;
     if (buckets) {
         ds->bcnt.ensure((B << M) * 4);
@@ -691,7 +696,19 @@ void run_batches(SearchCtx& c) {
         const K* sorted_keys = nullptr;
         int vshift = 0;
         cudaEvent_t e2;
-        if (buckets) {
+        if (cluster_path) {
+            // ---- group + join fused: one thread-block cluster per run, bucket tables in DSMEM ----
+            kern::cluster_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
+                                               ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
+                                               nitems, static_cast<u32>(item_cap), npairs_b,
+                                               ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap), st);
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_SORT] += 1;
+            sv = vb[0];
+            e2 = clk.mark();
+            clk.span(XYZB_STAGE_SORT, e1, e2);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+        } else if (buckets) {
             // ---- group: counting sort into 2^M buckets per run ----
             const u64 nbk = nb << M;
             XYZB_CUDA(cudaMemsetAsync(ds->bcnt.p, 0, nbk * 4, st));
@@ -790,8 +807,8 @@ void run_batches(SearchCtx& c) {
         A.guard = c.guard;
         A.sv = sv;
         A.S = p;
-        A.vkeys = buckets ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
-        A.vkeys_by_pos = buckets ? 0 : 1;
+        A.vkeys = (buckets || cluster_path) ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
+        A.vkeys_by_pos = (buckets || cluster_path) ? 0 : 1;
         A.key64 = sizeof(K) == 8;
         A.vshift = vshift;
         A.rid = rid;

@@ -46,13 +46,13 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "sort", "segments", "merge_large"])
+@pytest.mark.parametrize("grouping", ["auto", "bucket", "sort", "segments", "merge_large"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
 def test_search_matches_reference_fixture(name, grouping, monkeypatch):
     """All grouping paths: counting sort into 2^M buckets (default here),
     per-run cluster radix sort, multi-kernel segmented radix sort."""
-    if grouping == "sort":
-        monkeypatch.setenv("XYZB_GROUPING", "sort")
+    if grouping in ("sort", "bucket"):
+        monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
     if grouping == "merge_large":  # the multi-kernel merge instead of the single-CTA one
@@ -192,7 +192,7 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-@pytest.mark.parametrize("grouping", ["auto", "sort", "segments"])
+@pytest.mark.parametrize("grouping", ["auto", "bucket", "sort", "segments"])
 def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
@@ -200,8 +200,8 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
     cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=10)
     base = xb.Dataset(x).search(y, cfg)
-    if grouping == "sort":
-        monkeypatch.setenv("XYZB_GROUPING", "sort")
+    if grouping in ("sort", "bucket"):
+        monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
     monkeypatch.setenv("XYZB_BATCH_ENTRIES", "6000")  # three runs per batch, a shorter last batch
