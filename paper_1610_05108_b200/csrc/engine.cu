@@ -23,6 +23,8 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <condition_variable>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -286,9 +288,78 @@ void validate_params(const xyzb_params* q) {
 
 // ------------------------------------------------------------ dataset creation --
 
-// Host -> device through two pooled pinned staging buffers: the host copy of
-// chunk i+1 overlaps the DMA of chunk i (pageable copies and 2-D copies with
-// 504-byte rows are several times slower).
+// Persistent host worker pool for parallel staging copies (the single-thread
+// memcpy into pinned memory, not PCIe, bounds the upload otherwise).
+class CopyPool {
+public:
+    CopyPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned n = std::min(8u, hw);
+        for (unsigned t = 0; t < n; ++t) workers_.emplace_back([this] { loop(); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    // memcpy(dst, src, len) split over the workers and the calling thread
+    void copy(void* dst, const void* src, size_t len) {
+        const size_t parts = workers_.size() + 1;
+        const size_t slice = (len + parts - 1) / parts;
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = static_cast<char*>(dst);
+        src_ = static_cast<const char*>(src);
+        len_ = len;
+        slice_ = slice;
+        next_ = 1;
+        pending_ = workers_.size();
+        ++gen_;
+        lk.unlock();
+        cv_.notify_all();
+        std::memcpy(dst, src, std::min(slice, len));
+        lk.lock();
+        done_cv_.wait(lk, [this] { return pending_ == 0; });
+    }
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool();  // leaked on purpose (outlives static destructors)
+        return *p;
+    }
+
+private:
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        while (true) {
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            const size_t part = next_++;
+            char* d = dst_;
+            const char* s = src_;
+            const size_t len = len_, slice = slice_;
+            lk.unlock();
+            const size_t b0 = std::min(len, part * slice), b1 = std::min(len, b0 + slice);
+            if (b1 > b0) std::memcpy(d + b0, s + b0, b1 - b0);
+            lk.lock();
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    bool stop_ = false;
+    uint64_t gen_ = 0;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t len_ = 0, slice_ = 0, next_ = 0, pending_ = 0;
+};
+
+// Host -> device through two pooled pinned staging buffers: the (parallel)
+// host copy of chunk i+1 overlaps the DMA of chunk i (pageable copies and 2-D
+// copies with 504-byte rows are several times slower).
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     constexpr size_t kChunk = size_t(16) << 20;
     if (bytes <= (size_t(1) << 20)) {
@@ -306,7 +377,7 @@ void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     for (size_t off = 0, i = 0; off < bytes; off += kChunk, i ^= 1) {
         const size_t len = std::min(kChunk, bytes - off);
         if (used[i]) XYZB_CUDA(cudaEventSynchronize(done[i]));
-        std::memcpy(stage[i].p, static_cast<const char*>(src) + off, len);
+        CopyPool::get().copy(stage[i].p, static_cast<const char*>(src) + off, len);
         XYZB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage[i].p, len, cudaMemcpyHostToDevice, st));
         XYZB_CUDA(cudaEventRecord(done[i], st));
         used[i] = true;
