@@ -5,7 +5,9 @@
  * point below replaces one reference interface; the reference file:line is
  * cited beside it (paths relative to the reference repo root).
  *
- *   xyzb_dataset_create/destroy  X upload, kept resident in HBM across calls.
+ *   xyzb_dataset_create/destroy  X upload, kept resident in HBM across calls
+ *   xyzb_dataset_open            (or X read from an XYZ1 file: read_dataset,
+ *                                proj/core/src/dataset_io.cpp:91-129).
  *                                Replaces the per-call X argument of the three
  *                                xyz::xyz_search overloads
  *                                (proj/core/include/xyz/search.hpp:100-111),
@@ -157,6 +159,13 @@ int xyzb_device_count(void);
 
 int xyzb_dataset_create(const xyzb_problem* problem, xyzb_dataset** out, char* err, size_t errlen);
 void xyzb_dataset_destroy(xyzb_dataset* ds);
+
+/* X straight from an XYZ1 file (read_dataset, proj/core/src/dataset_io.cpp:91-129:
+ * magic "XYZ1", kind byte 0 binary / 1 real, 3 reserved bytes, n and p as
+ * little-endian u64, then the column-major payload), streamed through pinned
+ * staging to the device with the reference's validation and messages. */
+int xyzb_dataset_open(const char* path, int32_t device, xyzb_dataset** out, char* err, size_t errlen);
+int xyzb_dataset_shape(const xyzb_dataset* ds, uint64_t* n_rows, uint64_t* n_cols, int32_t* binary);
 
 /* ---- the search (three xyz_search overloads, chosen by params->mode) ----
  * draws: optional host-drawn row indices, uint32 [passes][L][M] in pass order

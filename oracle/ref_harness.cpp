@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "xyz/dataset_io.hpp"
 #include "xyz/errors.hpp"
 #include "xyz/lasso.hpp"
 #include "xyz/oracle.hpp"
@@ -462,6 +463,26 @@ void ref_lasso_free(ref_lasso_out* o) {
                     static_cast<void*>(o->cd_cycles)})
         std::free(q);
     std::memset(o, 0, sizeof(*o));
+}
+
+// write_dataset / read_dataset (dataset_io.cpp:65-129)
+int ref_write_dataset(const char* path, int32_t kind, const uint64_t* x_words, const double* x_real, uint64_t n,
+                      uint64_t p, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        xyz::Dataset d;
+        d.kind = kind == 0 ? xyz::DatasetKind::binary : xyz::DatasetKind::real;
+        if (kind == 0) d.packed = packed_from_words(x_words, n, p); else d.real = real_from_colmajor(x_real, n, p);
+        xyz::write_dataset(path, d);
+    });
+}
+
+int ref_read_dataset(const char* path, int32_t* kind, uint64_t* n, uint64_t* p, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const xyz::Dataset d = xyz::read_dataset(path);
+        *kind = d.kind == xyz::DatasetKind::binary ? 0 : 1;
+        *n = d.n_rows();
+        *p = d.n_cols();
+    });
 }
 
 // rescale_rows (transforms.cpp:116-135): X/nu and y*nu^2, column-major in place copies.

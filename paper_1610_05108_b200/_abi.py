@@ -107,6 +107,8 @@ SIGNATURES = {
     "xyzb_device_count": (C.c_int, []),
     "xyzb_dataset_create": (C.c_int, [C.POINTER(Problem), C.POINTER(_P), C.c_char_p, C.c_size_t]),
     "xyzb_dataset_destroy": (None, [_P]),
+    "xyzb_dataset_open": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(_P), C.c_char_p, C.c_size_t]),
+    "xyzb_dataset_shape": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
     "xyzb_search": (C.c_int, [_P, C.POINTER(Response), C.POINTER(Params), C.POINTER(C.c_uint32),
                               C.POINTER(Result), C.c_char_p, C.c_size_t]),
     "xyzb_merge_results": (C.c_int, [_P, C.POINTER(Result), C.c_uint64, C.POINTER(Params),

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -394,7 +395,12 @@ __global__ void pad_words(const u64* __restrict__ src, u64 W, u64 p, u64 Wp, u64
     }
 }
 
-void create_binary(xyzb_dataset* ds, const xyzb_problem* pr) {
+// Raw column-major X lands in a device buffer through `fill(dev, bytes)`:
+// an upload from caller memory (xyzb_dataset_create) or a stream from an
+// XYZ1 file (xyzb_dataset_open).
+using Fill = std::function<void(void*, size_t)>;
+
+void create_binary(xyzb_dataset* ds, const Fill& fill) {
     ds->binary = true;
     ds->W = ceil_div(ds->n, 64);
     ds->Wp = round_up(ds->W, 4);
@@ -403,7 +409,7 @@ void create_binary(xyzb_dataset* ds, const xyzb_problem* pr) {
     {
         DevBuf raw;
         raw.ensure(ds->p * ds->W * 8);
-        upload(raw.p, pr->x_words, ds->p * ds->W * 8, ds->stream);
+        fill(raw.p, ds->p * ds->W * 8);
         pad_words<<<grid_for(ds->p * ds->Wp, 256, 4096), 256, 0, ds->stream>>>(raw.as<u64>(), ds->W, ds->p, ds->Wp,
                                                                                 ds->Xc.as<u64>());
         XYZB_LAUNCH_CHECK();
@@ -416,7 +422,7 @@ void create_binary(xyzb_dataset* ds, const xyzb_problem* pr) {
     XYZB_LAUNCH_CHECK();
 }
 
-void create_real(xyzb_dataset* ds, const xyzb_problem* pr) {
+void create_real(xyzb_dataset* ds, const Fill& fill) {
     ds->binary = false;
     ds->n4 = round_up(ds->n, 4);
     ds->P32 = ceil_div(ds->p, 32);
@@ -424,7 +430,7 @@ void create_real(xyzb_dataset* ds, const xyzb_problem* pr) {
     ds->Wp = round_up(ds->W, 4);
     DevBuf xc64;
     xc64.ensure(ds->n * ds->p * 8);
-    upload(xc64.p, pr->x_real, ds->n * ds->p * 8, ds->stream);
+    fill(xc64.p, ds->n * ds->p * 8);
     ds->Xc32.ensure(ds->p * ds->n4 * 4);
     real::to_f32_cols<<<grid_for(ds->p * ds->n4, 256, 4096), 256, 0, ds->stream>>>(xc64.as<double>(), ds->n, ds->p,
                                                                                      ds->n4, ds->Xc32.as<float>());
@@ -446,6 +452,48 @@ void create_real(xyzb_dataset* ds, const xyzb_problem* pr) {
     XYZB_CUDA(cudaStreamSynchronize(ds->stream));
     ds->has_zero = (hf & 1u) != 0;
     ds->in_unit = (hf & 2u) == 0;
+}
+
+// Stream an XYZ1 payload (dataset_io.cpp:91-129) from `f` to the device
+// through pinned staging, validating column padding (binary) on the way.
+void stream_file(void* dst, std::FILE* f, size_t bytes, bool binary, u64 W, u64 n, const std::string& path,
+                 cudaStream_t st) {
+    constexpr size_t kChunk = size_t(16) << 20;  // a multiple of 8 bytes
+    HostBuf stage[2];
+    cudaEvent_t done[2];
+    for (int i = 0; i < 2; ++i) {
+        stage[i].ensure(kChunk);
+        XYZB_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    const u64 tail = n & 63;
+    const u64 mask = tail == 0 ? ~0ull : ((1ull << tail) - 1);
+    bool used[2] = {false, false};
+    std::string fail;
+    for (size_t off = 0, i = 0; off < bytes && fail.empty(); off += kChunk, i ^= 1) {
+        const size_t len = std::min(kChunk, bytes - off);
+        if (used[i]) XYZB_CUDA(cudaEventSynchronize(done[i]));
+        if (std::fread(stage[i].p, 1, len, f) != len) {
+            fail = "read_dataset: truncated payload in " + path;
+            break;
+        }
+        if (binary && mask != ~0ull) {
+            const u64* w = stage[i].as<u64>();
+            const u64 w0 = off / 8;
+            for (u64 t = (W - 1 + W - w0 % W) % W; t < len / 8; t += W)  // last word of each column
+                if (w[t] & ~mask) {
+                    fail = "read_dataset: nonzero padding bits in " + path;
+                    break;
+                }
+        }
+        if (!fail.empty()) break;
+        XYZB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage[i].p, len, cudaMemcpyHostToDevice, st));
+        XYZB_CUDA(cudaEventRecord(done[i], st));
+        used[i] = true;
+    }
+    XYZB_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < 2; ++i) cudaEventDestroy(done[i]);
+    if (!fail.empty()) throw data_error(fail);
+    if (std::fgetc(f) != EOF) throw data_error("read_dataset: trailing bytes in " + path);
 }
 
 // ------------------------------------------------------------ the search --
@@ -1641,7 +1689,12 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
         XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
         ds->n = pr->n_rows;
         ds->p = pr->n_cols;
-        if (pr->x_words) create_binary(ds.get(), pr); else create_real(ds.get(), pr);
+        const cudaStream_t st = ds->stream;
+        if (pr->x_words) {
+            create_binary(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_words, b, st); });
+        } else {
+            create_real(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_real, b, st); });
+        }
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         *out = ds.release();
     });
@@ -1659,6 +1712,48 @@ void xyzb_dataset_destroy(xyzb_dataset* ds) {
         cudaStreamDestroy(st);
         cudaSetDevice(prev);
     }
+}
+
+int xyzb_dataset_open(const char* path, int32_t device, xyzb_dataset** out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        *out = nullptr;
+        const std::string ps = path ? path : "";
+        std::unique_ptr<std::FILE, int (*)(std::FILE*)> f(std::fopen(ps.c_str(), "rb"), std::fclose);
+        if (!f) throw data_error("read_dataset: cannot open " + ps);
+        unsigned char head[8];
+        if (std::fread(head, 1, 8, f.get()) != 8 || std::memcmp(head, "XYZ1", 4) != 0)
+            throw data_error("read_dataset: bad magic in " + ps);
+        if (head[4] > 1) throw data_error("read_dataset: unknown dataset kind");
+        u64 dims[2] = {0, 0};
+        if (std::fread(dims, 8, 2, f.get()) != 2 || dims[0] == 0 || dims[1] == 0)
+            throw data_error("read_dataset: bad header dimensions");
+        const bool binary = head[4] == 0;
+        if (dims[0] > 0xffffffffull) throw data_error("xyzb: more than 2^32-1 rows");
+        require_device();
+        std::unique_ptr<xyzb_dataset> ds(new xyzb_dataset());
+        ds->device = device;
+        DeviceGuard dg(device);
+        XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+        ds->n = dims[0];
+        ds->p = dims[1];
+        const cudaStream_t st = ds->stream;
+        const u64 W = ceil_div(ds->n, 64);
+        if (binary) {
+            create_binary(ds.get(), [&](void* d, size_t b) { stream_file(d, f.get(), b, true, W, ds->n, ps, st); });
+        } else {
+            create_real(ds.get(), [&](void* d, size_t b) { stream_file(d, f.get(), b, false, W, ds->n, ps, st); });
+        }
+        XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        *out = ds.release();
+    });
+}
+
+int xyzb_dataset_shape(const xyzb_dataset* ds, uint64_t* n_rows, uint64_t* n_cols, int32_t* binary) {
+    if (!ds) return XYZB_E_DATA;
+    if (n_rows) *n_rows = ds->n;
+    if (n_cols) *n_cols = ds->p;
+    if (binary) *binary = ds->binary ? 1 : 0;
+    return XYZB_OK;
 }
 
 int xyzb_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params, const uint32_t* draws,

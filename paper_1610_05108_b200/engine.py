@@ -32,12 +32,31 @@ class Dataset:
         self.x = x
         self.device = device
         self.binary = isinstance(x, PackedMatrix)
+        self.n_rows, self.n_cols = x.n_rows, x.n_cols
         prob = make_problem(x, device)
         h = C.c_void_p()
         err = _abi.errbuf()
         raise_for(self._lib.xyzb_dataset_create(C.byref(prob), C.byref(h), err, _abi.ERRBUF), err)
         self._h = h
         self._fin = weakref.finalize(self, self._lib.xyzb_dataset_destroy, h)
+
+    @classmethod
+    def open(cls, path, device: int = 0) -> "Dataset":
+        """X read straight from an XYZ1 file (read_dataset, dataset_io.cpp:91-129)
+        into HBM; `x` is None (the matrix never lives on the host)."""
+        self = cls.__new__(cls)
+        self._lib = load()
+        self.x = None
+        self.device = device
+        h = C.c_void_p()
+        err = _abi.errbuf()
+        raise_for(self._lib.xyzb_dataset_open(str(path).encode(), device, C.byref(h), err, _abi.ERRBUF), err)
+        n, p, b = C.c_uint64(), C.c_uint64(), C.c_int32()
+        self._lib.xyzb_dataset_shape(h, C.byref(n), C.byref(p), C.byref(b))
+        self.n_rows, self.n_cols, self.binary = n.value, p.value, bool(b.value)
+        self._h = h
+        self._fin = weakref.finalize(self, self._lib.xyzb_dataset_destroy, h)
+        return self
 
     @property
     def handle(self):
@@ -82,7 +101,7 @@ class Dataset:
         draws = np.ascontiguousarray(draws, np.uint32)
         if draws.ndim == 1:
             draws = draws[None, :]
-        keys = np.zeros((draws.shape[0], self.x.n_cols), np.uint64)
+        keys = np.zeros((draws.shape[0], self.n_cols), np.uint64)
         err = _abi.errbuf()
         raise_for(self._lib.xyzb_project_keys(self._h, draws.ctypes.data_as(C.POINTER(C.c_uint32)), draws.shape[0],
                                               draws.shape[1], keys.ctypes.data_as(C.POINTER(C.c_uint64)), err,

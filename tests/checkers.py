@@ -62,6 +62,9 @@ _REF_SIGS = {
     "ref_brute_force_topk": (C.c_int, [_U64P, C.c_uint64, C.c_uint64, C.POINTER(C.c_int8), C.c_uint64, _U32P, _F64P,
                                        _U64P, C.c_char_p, C.c_size_t]),
     "ref_rescale_rows": (C.c_int, [_F64P, C.c_uint64, C.c_uint64, _F64P, _F64P, _F64P, C.c_char_p, C.c_size_t]),
+    "ref_write_dataset": (C.c_int, [C.c_char_p, C.c_int32, _U64P, _F64P, C.c_uint64, C.c_uint64, C.c_char_p,
+                                    C.c_size_t]),
+    "ref_read_dataset": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _U64P, _U64P, C.c_char_p, C.c_size_t]),
 }
 
 
@@ -346,3 +349,23 @@ def lasso_path(lib, x: RealMatrix, y, grid_size=20, grid_ratio=0.05, kkt_l=0, kk
         return fits, out.wall_s
     finally:
         lib.ref_lasso_free(C.byref(out))
+
+
+def ref_write_dataset(path, x):
+    lib = ref_lib()
+    err = _abi.errbuf()
+    if isinstance(x, PackedMatrix):
+        _check(lib.ref_write_dataset(str(path).encode(), 0, _u64p(x.words), None, x.n_rows, x.n_cols, err, _abi.ERRBUF),
+               err)
+    else:
+        _check(lib.ref_write_dataset(str(path).encode(), 1, None, x.values.ctypes.data_as(_F64P), x.n_rows, x.n_cols,
+                                     err, _abi.ERRBUF), err)
+
+
+def ref_read_dataset(path):
+    """(kind, n, p) or raises CheckerError with the reference's message."""
+    lib = ref_lib()
+    kind, n, p = C.c_int32(), C.c_uint64(), C.c_uint64()
+    err = _abi.errbuf()
+    _check(lib.ref_read_dataset(str(path).encode(), C.byref(kind), C.byref(n), C.byref(p), err, _abi.ERRBUF), err)
+    return kind.value, n.value, p.value

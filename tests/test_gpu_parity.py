@@ -331,3 +331,42 @@ def test_gwas_full_size_properties():
     top = rep.top_hits()
     ts = [(-h.strength, min(h.j, h.k), max(h.j, h.k), -h.sign) for h in top]
     assert ts == sorted(ts)
+
+
+def test_xyz1_file_ingest_matches_in_memory_and_reference_errors(tmp_path):
+    """xyzb_dataset_open streams the reference's on-disk format (written by the
+    reference's own write_dataset) straight to HBM; searches are identical to
+    the in-memory dataset; malformed files fail with read_dataset's messages."""
+    xb = _engine()
+    x, y = ck.ref_planted(300, 120, 3, 7, 0.95, 2)
+    f = tmp_path / "x.xyz"
+    ck.ref_write_dataset(f, x)
+    cfg = xb.SearchConfig(m=6, l=8, gamma=0.6, seed=3, top_k=10)
+    a = xb.Dataset.open(f).search(y, cfg)
+    b = xb.Dataset(x).search(y, cfg)
+    assert report_hits(a) == report_hits(b) and a.top_k == b.top_k
+    xr = ck.ref_uniform(50, 9, 4, 4)
+    fr = tmp_path / "r.xyz"
+    ck.ref_write_dataset(fr, xr)
+    yr = np.random.default_rng(3).normal(size=50)
+    cr = xb.SearchConfig(m=3, l=4, gamma=0.55, seed=1, mode="continuous_xy", transform="sign")
+    assert report_hits(xb.Dataset.open(fr).search(yr, cr)) == report_hits(xb.Dataset(xr).search(yr, cr))
+    raw = f.read_bytes()
+    bad = {
+        "magic": b"XYZ2" + raw[4:],
+        "kind": raw[:4] + b"\x07" + raw[5:],
+        "dims": raw[:8] + (0).to_bytes(8, "little") + raw[16:],
+        "truncated": raw[:-5],
+        "trailing": raw + b"\x00",
+        "padding": raw[:24 + 8 * 4] + (1 << 63).to_bytes(8, "little") + raw[24 + 8 * 5:],  # last word of column 0
+    }
+    for name, blob in bad.items():
+        g = tmp_path / f"bad_{name}.xyz"
+        g.write_bytes(blob)
+        with pytest.raises(ck.CheckerError) as want:
+            ck.ref_read_dataset(g)
+        with pytest.raises(xb.DataError) as got:
+            xb.Dataset.open(g)
+        assert str(got.value) == str(want.value).split("] ", 1)[1], name
+    with pytest.raises(xb.DataError):
+        xb.Dataset.open(tmp_path / "missing.xyz")
