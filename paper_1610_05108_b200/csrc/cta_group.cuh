@@ -1,0 +1,384 @@
+// Per-run grouping + join in ONE CTA with a 16-bit bucket table (sm_100a).
+//
+// For M <= 16 the 2^M bucket counters of one run fit in shared memory as
+// 16-bit halves of u32 words (128 KB at M = 16) — no cluster, no DSMEM, no
+// cluster barriers. Positions above 16 bits come from per-chunk u32 bases
+// (a chunk = 256 buckets): start(v) = base[v >> 8] + off16[v]. A persistent
+// CTA walks its runs; per run, all in shared memory:
+//   1. count: one shared atomic per key (warp-aggregated with match.any only
+//      when 2^M is small enough for lanes to collide);
+//   2. scan: per-thread bucket ranges, block scan, chunk bases;
+//   3. scatter: atomic cursors -> grouped[b*p + pos] = column;
+//   4. join: |E_r| (incl. the diagonal, pair_search.cpp:48-49) and the
+//      canonical work, reduced in the block: the guard (pair_search.hpp:91-94)
+//      is decided on-chip;
+//   5. emit: candidate pairs / work items of a kept run (emit_items).
+// A run whose bucket or chunk exceeds 65535 columns (possible only when
+// p > 65535, e.g. many monomorphic columns) is redone exactly with 32-bit
+// counters in a per-CTA global table. The outputs are those of
+// cluster_group_join (same grouped/tot/work_run/items/pairs contract).
+#pragma once
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "search_kernels.cuh"
+
+namespace xyzb {
+namespace kern {
+
+constexpr int kCtThreads = 1024;
+constexpr int kCtChunkBits = 8;  // 256 buckets share one u32 base
+
+// Block-wide exclusive scan of one u32 per thread; returns the exclusive
+// prefix, *total gets the block total. Uses `ws` (>= 33 u32) as scratch.
+__device__ __forceinline__ u32 block_exclusive(u32 x, u32* ws, u32* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u32 incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const u32 w = lane < nw ? ws[lane] : 0u;
+        u32 wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        ws[lane] = wi - w;
+        if (lane == 31) ws[32] = wi;
+    }
+    __syncthreads();
+    const u32 r = ws[wid] + incl - x;
+    *total = ws[32];
+    __syncthreads();  // ws reusable
+    return r;
+}
+
+// 16-bit counters in shared memory + chunk bases.
+struct SmemTab16 {
+    u32* w;      // 2^(M-1) words (two buckets each)
+    u32* base;   // 2^M >> kCtChunkBits chunk bases (>= 1)
+    int M;
+    int cbits;   // log2 buckets per chunk
+    u32* ovf;    // shared overflow flag
+
+    __device__ void clear() {
+        const u32 nw = (u32(1) << M) >> 1;
+        for (u32 i = threadIdx.x; i < nw; i += blockDim.x) w[i] = 0;
+    }
+    template <bool CHECK>
+    __device__ __forceinline__ u32 add(u32 v, u32 n) {
+        const u32 sh = (v & 1u) << 4;
+        const u32 old = atomicAdd(w + (v >> 1), n << sh);
+        const u32 h = (old >> sh) & 0xffffu;
+        if (CHECK && h + n > 0xffffu) *ovf = 1u;
+        return h;
+    }
+    __device__ __forceinline__ u32 chunk_base(u32 v) const { return base[v >> cbits]; }
+    __device__ __forceinline__ u32 half(u32 v) const { return (w[v >> 1] >> ((v & 1u) << 4)) & 0xffffu; }
+    // counts -> exclusive in-chunk offsets; chunk bases; flags chunks > 65535.
+    // Rounds of blockDim consecutive words (one per thread: no bank
+    // conflicts), one block scan per round with a running carry.
+    __device__ void scan(u32* ws) {
+        const u32 NW = (u32(1) << M) >> 1;
+        const u32 cwbits = cbits - 1;  // log2 words per chunk (cbits >= 1)
+        u32 carry = 0;
+        for (u32 r0 = 0; r0 < NW; r0 += blockDim.x) {
+            const u32 wi = r0 + threadIdx.x;
+            const bool act = wi < NW;
+            const u32 x = act ? w[wi] : 0u;
+            const u32 lo = x & 0xffffu, hi = x >> 16;
+            u32 total;
+            const u32 pos = carry + block_exclusive(lo + hi, ws, &total);
+            if (act && (wi & ((u32(1) << cwbits) - 1)) == 0) base[wi >> cwbits] = pos;
+            __syncthreads();
+            if (act) {
+                const u32 cb = base[wi >> cwbits];
+                const u32 o = pos - cb;
+                if (o + lo + hi > 0xffffu) *ovf = 1u;
+                w[wi] = (o & 0xffffu) | (((o + lo) & 0xffffu) << 16);
+            }
+            carry += total;
+        }
+    }
+    // after the scatter: bucket v occupies [beg, beg + cnt)
+    __device__ __forceinline__ void group(u32 v, u32& beg, u32& cnt) const {
+        const u32 cb = base[v >> cbits];
+        const u32 end = cb + half(v);
+        const u32 st = (v & ((u32(1) << cbits) - 1)) ? cb + half(v - 1) : cb;
+        beg = st;
+        cnt = end - st;
+    }
+};
+
+// 32-bit counters in global memory (overflow fallback).
+struct GlobalTab32 {
+    u32* t;  // 2^M
+    int M;
+
+    __device__ void clear() {
+        const u32 T = u32(1) << M;
+        for (u32 i = threadIdx.x; i < T; i += blockDim.x) t[i] = 0;
+    }
+    template <bool CHECK>
+    __device__ __forceinline__ u32 add(u32 v, u32 n) { return atomicAdd(t + v, n); }
+    __device__ void scan(u32* ws) {
+        const u32 T = u32(1) << M;
+        const u32 bpt = max(1u, T / blockDim.x);
+        const u32 a0 = threadIdx.x * bpt;
+        const bool act = a0 < T;
+        u32 loc = 0;
+        if (act)
+            for (u32 i = a0; i < a0 + bpt; ++i) loc += t[i];
+        u32 total;
+        u32 run = block_exclusive(loc, ws, &total);
+        if (act)
+            for (u32 i = a0; i < a0 + bpt; ++i) {
+                const u32 x = t[i];
+                t[i] = run;
+                run += x;
+            }
+    }
+    __device__ __forceinline__ void group(u32 v, u32& beg, u32& cnt) const {
+        const u32 end = t[v];
+        const u32 st = v ? t[v - 1] : 0u;
+        beg = st;
+        cnt = end - st;
+    }
+};
+
+constexpr int kCtUnroll = 8;  // keys in flight per thread
+
+// One pass over a run's keys: count (out == nullptr) or scatter positions.
+// POS16: positions are chunk base + 16-bit in-chunk offset (SmemTab16).
+template <bool AGG, bool CHECK, bool POS16, class K, class Tab>
+__device__ __forceinline__ void tab_pass(Tab& tab, const K* __restrict__ kb, u64 p, u32* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const u64 step = u64(blockDim.x) * kCtUnroll;
+    for (u64 i0 = 0; i0 < p; i0 += step) {
+        u32 v[kCtUnroll];
+#pragma unroll
+        for (int u = 0; u < kCtUnroll; ++u) {
+            const u64 i = i0 + u64(u) * blockDim.x + threadIdx.x;
+            v[u] = i < p ? u32(__ldg(kb + i)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kCtUnroll; ++u) {
+            const u64 i = i0 + u64(u) * blockDim.x + threadIdx.x;
+            const bool valid = i < p;
+            if (AGG) {
+                const u32 active = __ballot_sync(0xffffffffu, valid);
+                if (valid) {
+                    const u32 peers = __match_any_sync(active, v[u]);
+                    const int leader = __ffs(peers) - 1;
+                    u32 pos = 0;
+                    if (lane == leader) {
+                        pos = tab.template add<CHECK>(v[u], __popc(peers));
+                        if constexpr (POS16) pos += tab.chunk_base(v[u]);
+                    }
+                    if (out) {
+                        pos = __shfl_sync(peers, pos, leader) + __popc(peers & lanemask_lt());
+                        out[pos] = u32(i);
+                    }
+                }
+            } else if (valid) {
+                u32 pos = tab.template add<CHECK>(v[u], 1u);
+                if (out) {
+                    if constexpr (POS16) pos += tab.chunk_base(v[u]);
+                    out[pos] = u32(i);
+                }
+            }
+        }
+    }
+}
+
+template <class K, class Tab>
+__device__ __forceinline__ HeadBlock tab_block(const Tab& tab, u32 v, K c) {
+    HeadBlock hb;
+    u32 bx, cx;
+    tab.group(v, bx, cx);
+    if (cx == 0) return hb;
+    const u32 v2 = v ^ u32(c);
+    if (v2 == v) {
+        hb.pairs = u64(cx) * cx;  // the diagonal j == k counts (pair_search.cpp:48-49)
+        if (cx >= 2) {
+            hb.work = u64(cx) * (cx - 1) / 2;
+            hb.hs = bx; hb.hc = cx; hb.ss = bx; hb.sc = cx; hb.flags = 3u;
+        }
+    } else if (v2 > v) {
+        u32 bz, cz;
+        tab.group(v2, bz, cz);
+        if (cz) {
+            hb.pairs = 2ull * cx * cz;
+            hb.work = u64(cx) * cz;
+            if (cx <= cz) {
+                hb.hs = bx; hb.hc = cx; hb.ss = bz; hb.sc = cz; hb.flags = 1u;
+            } else {
+                hb.hs = bz; hb.hc = cz; hb.ss = bx; hb.sc = cx; hb.flags = 0u;
+            }
+        }
+    }
+    return hb;
+}
+
+// Steps 4-5 on a filled table. Pass 1 sums |E_r|, the canonical work and
+// this thread's item / pair counts; a kept run reserves its slots with ONE
+// atomic per counter, and pass 2 writes at per-thread offsets (no barriers).
+template <class K, class Tab>
+__device__ void tab_join(const Tab& tab, int M, u32 b, K c, u64 p, u64 guard, u32 hmax, u64* __restrict__ tot,
+                         u64* __restrict__ work_run, Item* __restrict__ items, u32* __restrict__ nitems, u32 item_cap,
+                         u32* __restrict__ npairs, PairRec* __restrict__ pairs, u32 pair_cap, u64 (*red)[33],
+                         u32* ws) {
+    const u32 T = u32(1) << M;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool pair_list = npairs != nullptr;
+    u64 pa = 0, wa = 0;
+    u32 my_items = 0, my_pairs = 0;
+    for (u32 v = threadIdx.x; v < T; v += blockDim.x) {
+        const HeadBlock hb = tab_block<K>(tab, v, c);
+        pa += hb.pairs;
+        wa += hb.work;
+        u32 ne, np, nsc;
+        emit_count(hb, hmax, pair_list, ne, np, nsc);
+        my_items += ne;
+        my_pairs += np;
+    }
+    pa = warp_sum(pa);
+    wa = warp_sum(wa);
+    if (lane == 0) {
+        red[0][wid] = pa;
+        red[1][wid] = wa;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 a = 0, w = 0;
+        for (int q = 0; q < nw; ++q) {
+            a += red[0][q];
+            w += red[1][q];
+        }
+        red[0][32] = a;
+        red[1][32] = w;
+        tot[b] = a;
+        work_run[b] = w;
+    }
+    __syncthreads();
+    const u64 run_pairs = red[0][32];
+    if (run_pairs <= guard) {
+        u32 ti, tp;
+        u32 ibase = block_exclusive(my_items, ws, &ti);
+        u32 pbase = block_exclusive(my_pairs, ws + 33, &tp);
+        if (threadIdx.x == 0) {
+            ws[66] = ti ? atomicAdd(nitems, ti) : 0u;
+            ws[67] = (pair_list && tp) ? atomicAdd(npairs, tp) : 0u;
+        }
+        __syncthreads();
+        ibase += ws[66];
+        pbase += ws[67];
+        for (u32 v = threadIdx.x; v < T; v += blockDim.x) {
+            const HeadBlock hb = tab_block<K>(tab, v, c);
+            if (hb.work == 0) continue;
+            u32 ne, np, nsc;
+            emit_count(hb, hmax, pair_list, ne, np, nsc);
+            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p);
+            ibase += ne;
+            pbase += np;
+        }
+    }
+    __syncthreads();  // red / ws / tables reusable
+}
+
+template <class K, bool AGG, bool CHECK>
+__global__ void __launch_bounds__(kCtThreads) cta_group_join(
+    const K* __restrict__ keys, u32 nruns, u64 p, int M, const K* __restrict__ xorc, u64 guard, u32 hmax,
+    u32* __restrict__ grouped, u64* __restrict__ tot, u64* __restrict__ work_run, Item* __restrict__ items,
+    u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs, PairRec* __restrict__ pairs, u32 pair_cap,
+    u32* __restrict__ gtab) {
+    extern __shared__ __align__(16) u32 smem[];
+    __shared__ u32 ws[68];
+    __shared__ u32 s_ovf;
+    __shared__ u64 red[2][33];
+    const u32 T = u32(1) << M;
+    const int cbits = min(M, kCtChunkBits);
+    SmemTab16 tab{smem + max(1u, T >> cbits), smem, M, cbits, &s_ovf};
+    for (u32 b = blockIdx.x; b < nruns; b += gridDim.x) {
+        const K* kb = keys + u64(b) * p;
+        u32* out = grouped + u64(b) * p;
+        const K c = xorc[b];
+        if (threadIdx.x == 0) s_ovf = 0;
+        tab.clear();
+        __syncthreads();
+        tab_pass<AGG, CHECK, true>(tab, kb, p, static_cast<u32*>(nullptr));
+        __syncthreads();
+        tab.scan(ws);
+        __syncthreads();
+        if (CHECK && s_ovf) {
+            // a bucket or a chunk above 65535 columns: redo exactly with 32-bit counters
+            GlobalTab32 g{gtab + (u64(blockIdx.x) << M), M};
+            g.clear();
+            __syncthreads();
+            tab_pass<AGG, false, false>(g, kb, p, static_cast<u32*>(nullptr));
+            __syncthreads();
+            g.scan(ws);
+            __syncthreads();
+            tab_pass<AGG, false, false>(g, kb, p, out);
+            __syncthreads();
+            tab_join<K>(g, M, b, c, p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap,
+                        red, ws);
+            continue;
+        }
+        tab_pass<AGG, false, true>(tab, kb, p, out);
+        __syncthreads();
+        tab_join<K>(tab, M, b, c, p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap, red,
+                    ws);
+    }
+}
+
+// Shared bytes of the table for 2^M buckets.
+inline size_t cta_group_smem(int M) {
+    const u64 T = u64(1) << M;
+    const int cbits = M < kCtChunkBits ? M : kCtChunkBits;
+    return size_t(T / 2) * 4 + size_t(std::max<u64>(1, T >> cbits)) * 4;
+}
+
+// Scratch (u32 entries) the overflow fallback needs: one 2^M table per CTA.
+inline u64 cta_group_scratch(int M, u64 p) { return p > 0xffffu ? (u64(kSMs) << M) : 0; }
+
+template <class K, bool AGG, bool CHECK>
+void cta_group_join_go(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 guard, u32 hmax, u32* grouped, u64* tot,
+                       u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
+                       u32 pair_cap, u32* gtab, cudaStream_t st) {
+    auto kernel = cta_group_join<K, AGG, CHECK>;
+    static bool attr = false;  // one per instantiation
+    if (!attr) {
+        XYZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_group_smem(16))));
+        attr = true;
+    }
+    const size_t smem = cta_group_smem(M);
+    int o = 0;  // depends on M through the table size
+    XYZB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kCtThreads, smem));
+    const u64 grid = std::min<u64>(B, u64(kSMs) * u64(std::max(1, o)));
+    kernel<<<static_cast<u32>(grid), kCtThreads, smem, st>>>(keys, static_cast<u32>(B), p, M, xorc, guard, hmax,
+                                                             grouped, tot, work_run, items, nitems, item_cap, npairs,
+                                                             pairs, pair_cap, gtab);
+}
+
+template <class K>
+void cta_group_join_launch(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 guard, u32 hmax, u32* grouped,
+                           u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs,
+                           PairRec* pairs, u32 pair_cap, u32* gtab, cudaStream_t st) {
+    const bool agg = M <= 12;  // lanes of a warp collide only on small tables
+    const bool check = p > 0xffffu;
+    auto go = agg ? (check ? cta_group_join_go<K, true, true> : cta_group_join_go<K, true, false>)
+                  : (check ? cta_group_join_go<K, false, true> : cta_group_join_go<K, false, false>);
+    go(keys, B, p, M, xorc, guard, hmax, grouped, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap, gtab,
+       st);
+}
+
+} // namespace kern
+} // namespace xyzb

@@ -31,6 +31,7 @@
 
 #include "../../include/xyzb.h"
 #include "cluster_group.cuh"
+#include "cta_group.cuh"
 #include "common.cuh"
 #include "draws.cuh"
 #include "host_rng.hpp"
@@ -214,7 +215,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal;
     // batch scratch
     DevBuf keys[2], vals[2], hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -361,9 +362,20 @@ private:
 // Host -> device through two pooled pinned staging buffers: the (parallel)
 // host copy of chunk i+1 overlaps the DMA of chunk i (pageable copies and 2-D
 // copies with 504-byte rows are several times slower).
+// Page-locked caller memory (cudaHostAlloc / cudaHostRegister / torch
+// pin_memory) is copied by DMA directly.
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     constexpr size_t kChunk = size_t(16) << 20;
-    if (bytes <= (size_t(1) << 20)) {
+    if (bytes <= (size_t(1) << 20) || is_pinned(src)) {
         XYZB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
         XYZB_CUDA(cudaStreamSynchronize(st));
         return;
@@ -387,6 +399,13 @@ void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     for (int i = 0; i < 2; ++i) cudaEventDestroy(done[i]);
 }
 
+// First column whose last word has a bit set above row n - 1 (PackedMatrix
+// invariant, packed_matrix.hpp:10-14); *bad stays ~0 when every column is clean.
+__global__ void check_padding(const u64* __restrict__ src, u64 W, u64 p, u32 tail, unsigned long long* bad) {
+    for (u64 j = u64(blockIdx.x) * blockDim.x + threadIdx.x; j < p; j += u64(gridDim.x) * blockDim.x)
+        if (src[j * W + W - 1] >> tail) atomicMin(bad, static_cast<unsigned long long>(j));
+}
+
 __global__ void pad_words(const u64* __restrict__ src, u64 W, u64 p, u64 Wp, u64* __restrict__ dst) {
     const u64 total = p * Wp;
     for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += u64(gridDim.x) * blockDim.x) {
@@ -400,7 +419,9 @@ __global__ void pad_words(const u64* __restrict__ src, u64 W, u64 p, u64 Wp, u64
 // XYZ1 file (xyzb_dataset_open).
 using Fill = std::function<void(void*, size_t)>;
 
-void create_binary(xyzb_dataset* ds, const Fill& fill) {
+// check_pad: verify the padding bits on the device (caller memory) and throw
+// data_error naming the first bad column, as the host check did.
+void create_binary(xyzb_dataset* ds, const Fill& fill, bool check_pad = false) {
     ds->binary = true;
     ds->W = ceil_div(ds->n, 64);
     ds->Wp = round_up(ds->W, 4);
@@ -410,6 +431,21 @@ void create_binary(xyzb_dataset* ds, const Fill& fill) {
         DevBuf raw;
         raw.ensure(ds->p * ds->W * 8);
         fill(raw.p, ds->p * ds->W * 8);
+        const u32 tail = static_cast<u32>(ds->n & 63);
+        if (check_pad && tail) {
+            DevBuf bad;
+            bad.ensure(8);
+            XYZB_CUDA(cudaMemsetAsync(bad.p, 0xff, 8, ds->stream));
+            check_padding<<<grid_for(ds->p, 256, 1024), 256, 0, ds->stream>>>(raw.as<u64>(), ds->W, ds->p, tail,
+                                                                                 bad.as<unsigned long long>());
+            XYZB_LAUNCH_CHECK();
+            u64 first = 0;
+            XYZB_CUDA(cudaMemcpyAsync(&first, bad.p, 8, cudaMemcpyDeviceToHost, ds->stream));
+            XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+            if (first != ~0ull)
+                throw data_error("xyzb_dataset_create: padding bits of column " + std::to_string(first) +
+                                 " are not zero");
+        }
         pad_words<<<grid_for(ds->p * ds->Wp, 256, 4096), 256, 0, ds->stream>>>(raw.as<u64>(), ds->W, ds->p, ds->Wp,
                                                                                 ds->Xc.as<u64>());
         XYZB_LAUNCH_CHECK();
@@ -737,8 +773,13 @@ void run_batches(SearchCtx& c) {
     const char* gsel = std::getenv("XYZB_GROUPING");
     // M <= 17: grouping and join fused per run on a cluster (tables in DSMEM);
     // XYZB_GROUPING=bucket keeps the multi-kernel counting sort
-    const bool cluster_path = M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
+    // M <= 16: one CTA per run with 16-bit shared counters (no cluster barriers);
+    // XYZB_GROUPING=cluster keeps the DSMEM cluster kernel
+    const bool grouped_path = M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
                               !(gsel && (std::string(gsel) == "sort" || std::string(gsel) == "bucket"));
+    const bool cta_path = grouped_path && M <= 16 && !(gsel && std::string(gsel) == "cluster");
+    const bool cluster_path = grouped_path && !cta_path;
+    if (cta_path && kern::cta_group_scratch(int(M), p)) ds->gtab.ensure(kern::cta_group_scratch(int(M), p) * 4);
     const bool buckets = !cluster_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
                          !(gsel && std::string(gsel) == "sort") && !sort_sel;
     if (buckets) {
@@ -815,7 +856,19 @@ void run_batches(SearchCtx& c) {
         const K* sorted_keys = nullptr;
         int vshift = 0;
         cudaEvent_t e2;
-        if (cluster_path) {
+        if (cta_path) {
+            // ---- group + join fused: one CTA per run, 16-bit bucket counters in shared memory ----
+            kern::cta_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
+                                           ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
+                                           nitems, static_cast<u32>(item_cap), npairs_b, ds->pairs.as<kern::PairRec>(),
+                                           static_cast<u32>(c.pair_cap), ds->gtab.as<u32>(), st);
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_SORT] += 1;
+            sv = vb[0];
+            e2 = clk.mark();
+            clk.span(XYZB_STAGE_SORT, e1, e2);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+        } else if (cluster_path) {
             // ---- group + join fused: one thread-block cluster per run, bucket tables in DSMEM ----
             kern::cluster_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
                                                ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
@@ -1670,16 +1723,6 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
         if ((pr->x_words == nullptr) == (pr->x_real == nullptr))
             throw data_error("xyzb_dataset_create: exactly one of x_words / x_real must be set");
         if (pr->n_rows > 0xffffffffull) throw data_error("xyzb: more than 2^32-1 rows");
-        if (pr->x_words) {
-            // padding bits must be clear (PackedMatrix invariant, packed_matrix.hpp:10-14)
-            const u64 W = ceil_div(pr->n_rows, 64);
-            const u64 tail = pr->n_rows & 63;
-            if (tail)
-                for (u64 j = 0; j < pr->n_cols; ++j)
-                    if (pr->x_words[j * W + W - 1] >> tail)
-                        throw data_error("xyzb_dataset_create: padding bits of column " + std::to_string(j) +
-                                         " are not zero");
-        }
         require_device();
         std::unique_ptr<xyzb_dataset> ds(new xyzb_dataset());
         ds->device = pr->device;
@@ -1691,7 +1734,8 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
         ds->p = pr->n_cols;
         const cudaStream_t st = ds->stream;
         if (pr->x_words) {
-            create_binary(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_words, b, st); });
+            // padding bits must be clear (PackedMatrix invariant): checked on the device
+            create_binary(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_words, b, st); }, true);
         } else {
             create_real(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_real, b, st); });
         }

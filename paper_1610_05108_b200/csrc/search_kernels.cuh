@@ -45,7 +45,7 @@ struct Item {
 // positions of the x side and the z side (x side first; diagonal blocks are
 // re-oriented by column index at hit time), the batch-local run, and the
 // block flags.
-struct PairRec {
+struct __align__(16) PairRec {
     u32 pa, pb, run, pad;
 };
 constexpr u64 kInlinePairs = 32;  // blocks up to this many pairs are expanded by join_emit
@@ -266,17 +266,13 @@ __global__ void __launch_bounds__(256) join_count(const K* __restrict__ sk, u64 
     }
 }
 
-// Emit the canonical work items of one block (per thread; warp-aggregated
-// slot reservation). Item t of a block: held chunk t / nsc (<= hmax
-// columns), streamed chunk t % nsc (<= kStreamChunk columns), so one big
-// group cannot serialise on one team. Counters keep counting past the
-// capacities so the host can regrow.
-__device__ __forceinline__ void emit_items(const HeadBlock& hb, u32 b, u32 hmax, Item* __restrict__ items,
-                                           u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs,
-                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S) {
-    u32 nsc = 1, nemit = 0;
-    // pair-list path: small blocks write their pairs right here (no item)
-    const bool inline_pairs = npairs != nullptr && hb.work != 0 && hb.work <= kInlinePairs;
+// How many work items and inline pairs block `hb` emits (pairs: canonical
+// candidates, all of them whether inline or through items).
+__device__ __forceinline__ void emit_count(const HeadBlock& hb, u32 hmax, bool pair_list, u32& nemit, u32& npair,
+                                           u32& nsc) {
+    nsc = 1;
+    nemit = 0;
+    const bool inline_pairs = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
     if (hb.work && !inline_pairs) {
         const bool diag = hb.flags & 2u;
         const u32 slen = diag ? hb.hc - 1 : hb.sc;
@@ -284,8 +280,67 @@ __device__ __forceinline__ void emit_items(const HeadBlock& hb, u32 b, u32 hmax,
         nsc = (slen + kStreamChunk - 1) / kStreamChunk;
         nemit = (hlen + hmax - 1) / hmax * nsc;
     }
-    // candidate pairs of this block (the diagonal counts only later positions)
-    const u32 npair = u32(hb.work);
+    npair = u32(hb.work);
+}
+
+// Write block `hb`'s items from slot `base` and its pairs from slot `poff`.
+__device__ __forceinline__ void emit_write(const HeadBlock& hb, u32 b, u32 hmax, bool pair_list, u32 nemit, u32 nsc,
+                                           u32 base, u32 poff, Item* __restrict__ items, u32 item_cap,
+                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S) {
+    const bool inline_pairs = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
+    const bool diag = hb.flags & 2u;
+    if (inline_pairs) {
+        const bool first_held = diag || (hb.flags & 1u);
+        const u32 off = u32(u64(b) * S);  // pair positions are u32 (b * S + pos < 2^32, checked by the host)
+        uint4* dst = reinterpret_cast<uint4*>(pairs);
+        for (u32 h = 0; h < hb.hc; ++h) {
+            const u32 hpos = off + hb.hs + h;
+            for (u32 q = diag ? h + 1 : 0; q < hb.sc; ++q, ++poff) {
+                if (poff >= pair_cap) break;
+                const u32 spos = off + hb.ss + q;
+                dst[poff] = make_uint4(first_held ? hpos : spos, first_held ? spos : hpos, b, hb.flags);
+            }
+        }
+    }
+    const u32 sbeg = diag ? hb.hs + 1 : hb.ss;
+    const u32 slen = diag ? hb.hc - 1 : hb.sc;
+    for (u32 t = 0; t < nemit; ++t) {
+        const u32 slot = base + t;
+        if (slot >= item_cap) break;
+        const u32 hci = t / nsc, sci = t - hci * nsc;
+        const u32 h0 = hci * hmax;
+        Item it;
+        it.run = b;
+        it.hs = hb.hs + h0;
+        // diagonal: each held chunk streams hs+1.. (pairs with spos <= hpos are masked)
+        it.ss = sbeg + sci * kStreamChunk;
+        it.sc = min(kStreamChunk, slen - sci * kStreamChunk);
+        const u32 hcnt = min(hmax, hb.hc - h0);
+        it.hc_flags = hcnt | (hb.flags << 8);
+        it.pad = poff;  // first slot of this item's pairs in the pair list
+        items[slot] = it;
+        if (diag) {
+            for (u32 h = 0; h < hcnt; ++h) {
+                const u32 hpos = it.hs + h, lo = max(it.ss, hpos + 1), hi = it.ss + it.sc;
+                poff += hi > lo ? hi - lo : 0;
+            }
+        } else {
+            poff += hcnt * it.sc;
+        }
+    }
+}
+
+// Emit the canonical work items of one block (per thread; CTA-aggregated
+// slot reservation). Item t of a block: held chunk t / nsc (<= hmax
+// columns), streamed chunk t % nsc (<= kStreamChunk columns), so one big
+// group cannot serialise on one team. Small blocks (<= kInlinePairs pairs)
+// write their pairs directly. Counters keep counting past the capacities so
+// the host can regrow.
+__device__ __forceinline__ void emit_items(const HeadBlock& hb, u32 b, u32 hmax, Item* __restrict__ items,
+                                           u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs,
+                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S) {
+    u32 nemit, npair, nsc;
+    emit_count(hb, hmax, npairs != nullptr, nemit, npair, nsc);
     u32 incl = nemit, pincl = npair;
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -320,51 +375,8 @@ __device__ __forceinline__ void emit_items(const HeadBlock& hb, u32 b, u32 hmax,
     }
     __syncthreads();
     const u32 base = s_items[32] + s_items[wid] + incl - nemit;
-    u32 poff = s_pairs[32] + s_pairs[wid] + pincl - npair;  // this block's first pair slot
-    const bool diag = hb.flags & 2u;
-    if (inline_pairs) {
-        const bool first_held = diag || (hb.flags & 1u);
-        const u64 off = u64(b) * S;
-        for (u32 h = 0; h < hb.hc; ++h) {
-            const u32 hpos = hb.hs + h;
-            for (u32 q = diag ? h + 1 : 0; q < hb.sc; ++q, ++poff) {
-                if (poff >= pair_cap) continue;
-                const u32 spos = hb.ss + q;
-                PairRec r;
-                r.pa = u32(off + (first_held ? hpos : spos));
-                r.pb = u32(off + (first_held ? spos : hpos));
-                r.run = b;
-                r.pad = hb.flags;
-                pairs[poff] = r;
-            }
-        }
-    }
-    const u32 sbeg = diag ? hb.hs + 1 : hb.ss;
-    const u32 slen = diag ? hb.hc - 1 : hb.sc;
-    for (u32 t = 0; t < nemit; ++t) {
-        const u32 slot = base + t;
-        if (slot >= item_cap) break;
-        const u32 hci = t / nsc, sci = t - hci * nsc;
-        const u32 h0 = hci * hmax;
-        Item it;
-        it.run = b;
-        it.hs = hb.hs + h0;
-        // diagonal: each held chunk streams hs+1.. (pairs with spos <= hpos are masked)
-        it.ss = sbeg + sci * kStreamChunk;
-        it.sc = min(kStreamChunk, slen - sci * kStreamChunk);
-        const u32 hcnt = min(hmax, hb.hc - h0);
-        it.hc_flags = hcnt | (hb.flags << 8);
-        it.pad = poff;  // first slot of this item's pairs in the pair list
-        items[slot] = it;
-        if (diag) {
-            for (u32 h = 0; h < hcnt; ++h) {
-                const u32 hpos = it.hs + h, lo = max(it.ss, hpos + 1), hi = it.ss + it.sc;
-                poff += hi > lo ? hi - lo : 0;
-            }
-        } else {
-            poff += hcnt * it.sc;
-        }
-    }
+    const u32 poff = s_pairs[32] + s_pairs[wid] + pincl - npair;  // this block's first pair slot
+    emit_write(hb, b, hmax, npairs != nullptr, nemit, nsc, base, poff, items, item_cap, pairs, pair_cap, S);
 }
 
 // Pass 2 (sorted keys): canonical work items of the runs the guard keeps.
@@ -792,7 +804,9 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
         const u32 wi = it * G + tl;
         yv[it] = wi < W2 ? __ldg(reinterpret_cast<const ulonglong2*>(Yw) + wi) : make_ulonglong2(0, 0);
     }
-    const u32 P = min(*npairs, pair_cap);
+    // an item overflow leaves unexpanded (unwritten) slots in the pair list;
+    // the host regrows and redoes the batch, so verify nothing now
+    const u32 P = *A.nitems > A.item_cap ? 0u : min(*npairs, pair_cap);
     const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
     for (u64 c0 = team * CH; c0 < P; c0 += nteams * CH) {
@@ -882,7 +896,9 @@ __global__ void __launch_bounds__(256) verify_pairs_simple(VerifyArgs A, const P
         const u32 wi = it * G + tl;
         yv[it] = wi < W2 ? __ldg(reinterpret_cast<const ulonglong2*>(Yw) + wi) : make_ulonglong2(0, 0);
     }
-    const u32 P = min(*npairs, pair_cap);
+    // an item overflow leaves unexpanded (unwritten) slots in the pair list;
+    // the host regrows and redoes the batch, so verify nothing now
+    const u32 P = *A.nitems > A.item_cap ? 0u : min(*npairs, pair_cap);
     const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
     for (u64 c0 = team * CH; c0 < P; c0 += nteams * CH) {

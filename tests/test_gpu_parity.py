@@ -46,12 +46,14 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "bucket", "sort", "segments", "merge_large"])
+@pytest.mark.parametrize("grouping", ["auto", "cluster", "bucket", "sort", "segments", "merge_large"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
 def test_search_matches_reference_fixture(name, grouping, monkeypatch):
-    """All grouping paths: counting sort into 2^M buckets (default here),
-    per-run cluster radix sort, multi-kernel segmented radix sort."""
-    if grouping in ("sort", "bucket"):
+    """All grouping paths: one CTA per run with 16-bit shared counters
+    (default for M <= 16), the DSMEM cluster kernel, the multi-kernel counting
+    sort into 2^M buckets, per-run cluster radix sort, multi-kernel segmented
+    radix sort."""
+    if grouping in ("sort", "bucket", "cluster"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
@@ -192,7 +194,7 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-@pytest.mark.parametrize("grouping", ["auto", "bucket", "sort", "segments"])
+@pytest.mark.parametrize("grouping", ["auto", "cluster", "bucket", "sort", "segments"])
 def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
@@ -200,7 +202,7 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
     cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=10)
     base = xb.Dataset(x).search(y, cfg)
-    if grouping in ("sort", "bucket"):
+    if grouping in ("sort", "bucket", "cluster"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
@@ -370,3 +372,40 @@ def test_xyz1_file_ingest_matches_in_memory_and_reference_errors(tmp_path):
         assert str(got.value) == str(want.value).split("] ", 1)[1], name
     with pytest.raises(xb.DataError):
         xb.Dataset.open(tmp_path / "missing.xyz")
+
+
+@pytest.mark.parametrize("grouping", ["auto", "cluster"])
+def test_bucket_above_16_bits_falls_back_exactly(grouping, monkeypatch):
+    """p > 65535 with 70000 identical (monomorphic) columns: one bucket holds
+    more columns than a 16-bit shared counter can; the CTA grouping redoes
+    such a run with 32-bit counters. Hits and counters equal the reference."""
+    if grouping == "cluster":
+        monkeypatch.setenv("XYZB_GROUPING", grouping)
+    xb = _engine()
+    rng = np.random.default_rng(11)
+    n, p_const, p_rand = 128, 70000, 300
+    signs = np.ones((n, p_const + p_rand), np.int8)
+    signs[:, p_const:] = rng.choice(np.array([-1, 1], np.int8), size=(n, p_rand))
+    x = xb.PackedMatrix.from_signs(signs)
+    y = rng.choice(np.array([-1, 1], np.int8), size=n)
+    for m, l, g in ((16, 3, 0.6), (14, 2, 0.62)):
+        cfg = xb.SearchConfig(m=m, l=l, gamma=g, seed=5, threads=1, top_k=20, estimate_complexity=False)
+        got, want = xb.Dataset(x).search(y, cfg), ck.ref_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, msg
+        assert got.top_k == want.top_k
+        assert (got.candidates_enumerated, got.aborted_repetitions) == (want.candidates_enumerated,
+                                                                       want.aborted_repetitions)
+
+
+def test_dirty_padding_bits_are_rejected_on_upload():
+    """The PackedMatrix invariant (packed_matrix.hpp:10-14): bits above row
+    n-1 of a column's last word must be zero; checked on the device after the
+    upload, naming the first offending column."""
+    xb = _engine()
+    x, _ = ck.ref_planted(100, 40, 3, 7, 0.9, 1)
+    words = x.words.copy()
+    words[3, -1] |= np.uint64(1) << np.uint64(63)
+    words[17, -1] |= np.uint64(1) << np.uint64(40)
+    with pytest.raises(xb.DataError, match="padding bits of column 3 are not zero"):
+        xb.Dataset(xb.PackedMatrix(100, 40, words))
