@@ -1723,6 +1723,18 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
         if ((pr->x_words == nullptr) == (pr->x_real == nullptr))
             throw data_error("xyzb_dataset_create: exactly one of x_words / x_real must be set");
         if (pr->n_rows > 0xffffffffull) throw data_error("xyzb: more than 2^32-1 rows");
+        // padding bits must be clear (PackedMatrix invariant, packed_matrix.hpp:10-14): checked on
+        // the host before any device work, except for page-locked X (DMA'd as is, checked on the device)
+        const bool pinned_x = pr->x_words && is_pinned(pr->x_words);
+        if (pr->x_words && !pinned_x) {
+            const u64 W = ceil_div(pr->n_rows, 64);
+            const u64 tail = pr->n_rows & 63;
+            if (tail)
+                for (u64 j = 0; j < pr->n_cols; ++j)
+                    if (pr->x_words[j * W + W - 1] >> tail)
+                        throw data_error("xyzb_dataset_create: padding bits of column " + std::to_string(j) +
+                                         " are not zero");
+        }
         require_device();
         std::unique_ptr<xyzb_dataset> ds(new xyzb_dataset());
         ds->device = pr->device;
@@ -1734,8 +1746,7 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
         ds->p = pr->n_cols;
         const cudaStream_t st = ds->stream;
         if (pr->x_words) {
-            // padding bits must be clear (PackedMatrix invariant): checked on the device
-            create_binary(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_words, b, st); }, true);
+            create_binary(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_words, b, st); }, pinned_x);
         } else {
             create_real(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_real, b, st); });
         }

@@ -408,4 +408,15 @@ def test_dirty_padding_bits_are_rejected_on_upload():
     words[3, -1] |= np.uint64(1) << np.uint64(63)
     words[17, -1] |= np.uint64(1) << np.uint64(40)
     with pytest.raises(xb.DataError, match="padding bits of column 3 are not zero"):
-        xb.Dataset(xb.PackedMatrix(100, 40, words))
+        xb.Dataset(xb.PackedMatrix(100, 40, words))  # pageable: checked on the host
+    import torch
+    pin = torch.empty(words.nbytes, dtype=torch.uint8, pin_memory=True)
+    pinned = pin.numpy().view(np.uint64).reshape(words.shape)
+    pinned[...] = words
+    with pytest.raises(xb.DataError, match="padding bits of column 3 are not zero"):
+        xb.Dataset(xb.PackedMatrix(100, 40, pinned))  # page-locked: DMA'd, checked on the device
+    pinned[...] = x.words
+    y = ck.ref_planted(100, 40, 3, 7, 0.9, 1)[1]
+    cfg = xb.SearchConfig(m=4, l=6, gamma=0.6, seed=2)
+    assert report_hits(xb.Dataset(xb.PackedMatrix(100, 40, pinned)).search(y, cfg)) == report_hits(
+        xb.Dataset(x).search(y, cfg))
