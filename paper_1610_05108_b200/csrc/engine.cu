@@ -290,6 +290,23 @@ void validate_params(const xyzb_params* q) {
 
 // ------------------------------------------------------------ dataset creation --
 
+// XYZB_TRACE=1: host-side phase times of dataset creation on stderr (device
+// drained at each mark, so only for diagnosis).
+struct Trace {
+    bool on = std::getenv("XYZB_TRACE") != nullptr;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    explicit Trace(cudaStream_t s) : st(s) {}
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[xyzb] %-14s %8.1f us\n", what,
+                     std::chrono::duration<double, std::micro>(now - t).count());
+        t = now;
+    }
+};
+
 // Persistent host worker pool for parallel staging copies (the single-thread
 // memcpy into pinned memory, not PCIe, bounds the upload otherwise).
 class CopyPool {
@@ -422,6 +439,7 @@ using Fill = std::function<void(void*, size_t)>;
 // check_pad: verify the padding bits on the device (caller memory) and throw
 // data_error naming the first bad column, as the host check did.
 void create_binary(xyzb_dataset* ds, const Fill& fill, bool check_pad = false) {
+    Trace tr(ds->stream);
     ds->binary = true;
     ds->W = ceil_div(ds->n, 64);
     ds->Wp = round_up(ds->W, 4);
@@ -430,7 +448,9 @@ void create_binary(xyzb_dataset* ds, const Fill& fill, bool check_pad = false) {
     {
         DevBuf raw;
         raw.ensure(ds->p * ds->W * 8);
+        tr.mark("alloc");
         fill(raw.p, ds->p * ds->W * 8);
+        tr.mark("fill");
         const u32 tail = static_cast<u32>(ds->n & 63);
         if (check_pad && tail) {
             DevBuf bad;
@@ -445,17 +465,21 @@ void create_binary(xyzb_dataset* ds, const Fill& fill, bool check_pad = false) {
             if (first != ~0ull)
                 throw data_error("xyzb_dataset_create: padding bits of column " + std::to_string(first) +
                                  " are not zero");
+            tr.mark("check_pad");
         }
         pad_words<<<grid_for(ds->p * ds->Wp, 256, 4096), 256, 0, ds->stream>>>(raw.as<u64>(), ds->W, ds->p, ds->Wp,
                                                                                 ds->Xc.as<u64>());
         XYZB_LAUNCH_CHECK();
+        tr.mark("pad");
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));  // raw returns to the pool
     }
+    tr.mark("raw_release");
     ds->Xr.ensure(ds->n * ds->P32 * 4);
-    const u64 warps = ds->P32 * ds->W;
-    kern::transpose_bits<<<static_cast<u32>(ceil_div(warps * 32, 256)), 256, 0, ds->stream>>>(
-        ds->Xc.as<u64>(), ds->Wp, ds->W, ds->n, ds->p, ds->P32, ds->Xr.as<u32>());
+    dim3 tg(static_cast<u32>(ceil_div(ds->P32, 32)), static_cast<u32>(ceil_div(ds->W, kern::kTrWords)));
+    kern::transpose_bits<<<tg, 1024, 0, ds->stream>>>(ds->Xc.as<u64>(), ds->Wp, ds->W, ds->n, ds->p, ds->P32,
+                                                      ds->Xr.as<u32>());
     XYZB_LAUNCH_CHECK();
+    tr.mark("transpose");
 }
 
 void create_real(xyzb_dataset* ds, const Fill& fill) {

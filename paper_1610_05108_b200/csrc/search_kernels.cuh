@@ -53,22 +53,53 @@ constexpr u64 kInlinePairs = 32;  // blocks up to this many pairs are expanded b
 // ---------------------------------------------------------------- layout --
 
 // Xc: u64 [p][Wp] column-major words -> Xr: u32 [n][P32] row planes, bit
-// (j & 31) of word j >> 5 of row i is X_ij. One warp per (32 columns, word):
-// lane l holds word w of column 32c+l; ballot over bit b gives row 64w+b.
-__global__ void transpose_bits(const u64* __restrict__ Xc, u64 Wp, u64 W, u64 n, u64 p, u64 P32,
-                               u32* __restrict__ Xr) {
-    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const u64 total = P32 * W;
-    if (warp >= total) return;
-    const u64 c = warp / W, w = warp % W;
-    const u64 col = c * 32 + lane;
-    const u64 word = col < p ? Xc[col * Wp + w] : 0ull;
-#pragma unroll 8
-    for (int b = 0; b < 64; ++b) {
-        const u32 bits = __ballot_sync(0xffffffffu, (word >> b) & 1ull);
-        const u64 row = w * 64 + b;
-        if (lane == (b & 31) && row < n) Xr[row * P32 + c] = bits;
+// (j & 31) of word j >> 5 of row i is X_ij. One CTA per tile of 1024 columns
+// x 256 rows: warp q loads 4 words (one 32 B sector) of each of its 32
+// columns, shuffle-butterfly bit transposes give the 32-column plane words
+// of 256 rows (lane l holds rows l, l+32, ...), stored to a shared tile
+// which the CTA writes out as 128 B row segments.
+constexpr int kTrWords = 4;  // words per column per tile (Wp is a multiple of 4)
+__global__ void __launch_bounds__(1024) transpose_bits(const u64* __restrict__ Xc, u64 Wp, u64 W, u64 n, u64 p,
+                                                       u64 P32, u32* __restrict__ Xr) {
+    __shared__ u32 tile[kTrWords * 64][33];
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const u64 c0 = u64(blockIdx.x) * 32;  // first column group of the tile
+    const u64 w0 = u64(blockIdx.y) * kTrWords;
+    const u64 col = (c0 + q) * 32 + lane;
+    u64 wd[kTrWords];
+    if (col < p) {
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(Xc + col * Wp + w0);
+        const ulonglong2 a = __ldg(src), b = __ldg(src + 1);
+        wd[0] = a.x; wd[1] = a.y; wd[2] = b.x; wd[3] = b.y;
+    } else {
+        wd[0] = wd[1] = wd[2] = wd[3] = 0;
+    }
+    // 32x32 bit transposes across the warp (butterfly of shuffles): lane l's
+    // half-word t (rows 32t.. of its column) becomes row 32t + l of the 32 columns
+    u32 mine[kTrWords * 2];
+#pragma unroll
+    for (int k = 0; k < kTrWords; ++k) {
+        mine[2 * k] = u32(wd[k]);
+        mine[2 * k + 1] = u32(wd[k] >> 32);
+    }
+#pragma unroll
+    for (int j = 16; j != 0; j >>= 1) {
+        const u32 m = j == 16 ? 0x0000ffffu : j == 8 ? 0x00ff00ffu : j == 4 ? 0x0f0f0f0fu : j == 2 ? 0x33333333u
+                                                                                               : 0x55555555u;
+        const bool up = lane & j;
+#pragma unroll
+        for (int t = 0; t < kTrWords * 2; ++t) {
+            const u32 o = __shfl_xor_sync(0xffffffffu, mine[t], j);
+            mine[t] = up ? (mine[t] & ~m) | ((o >> j) & m) : (mine[t] & m) | ((o & m) << j);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kTrWords * 2; ++t) tile[t * 32 + lane][q] = mine[t];
+    __syncthreads();
+    for (u32 idx = threadIdx.x; idx < kTrWords * 64 * 32; idx += 1024) {
+        const u32 r = idx >> 5, g = idx & 31;
+        const u64 row = w0 * 64 + r, c = c0 + g;
+        if (row < n && c < P32) Xr[row * P32 + c] = tile[r][g];
     }
 }
 
