@@ -21,6 +21,8 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "search_kernels.cuh"
 
@@ -85,7 +87,7 @@ struct SmemTab16 {
     // counts -> exclusive in-chunk offsets; chunk bases; flags chunks > 65535.
     // Rounds of blockDim consecutive words (one per thread: no bank
     // conflicts), one block scan per round with a running carry.
-    __device__ void scan(u32* ws) {
+    __device__ u32 scan(u32* ws) {
         const u32 NW = (u32(1) << M) >> 1;
         const u32 cwbits = cbits - 1;  // log2 words per chunk (cbits >= 1)
         u32 carry = 0;
@@ -106,6 +108,7 @@ struct SmemTab16 {
             }
             carry += total;
         }
+        return carry;
     }
     // after the scatter: bucket v occupies [beg, beg + cnt)
     __device__ __forceinline__ void group(u32 v, u32& beg, u32& cnt) const {
@@ -337,6 +340,279 @@ __global__ void __launch_bounds__(kCtThreads) cta_group_join(
         tab_join<K>(tab, M, b, c, p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap, red,
                     ws);
     }
+}
+
+// ------------------------------------------------ two-CTA split per run --
+//
+// The bucket space of a run is split on one key bit t between the two CTAs
+// of a cluster: CTA r owns the keys whose bit t equals r (2^(M-1) 16-bit
+// counters, 64 KB at M = 16, so three CTAs share an SM and every run of a
+// 200-run batch is resident at once instead of two rounds of one CTA per
+// SM). t is the lowest bit where c = x-key ^ z-key is 0, so a key and its
+// partner key v ^ c always live in the same CTA; only when c has no zero bit
+// (c = all ones, partner = ~v) does the join read the partner CTA's table
+// through distributed shared memory. The cluster exchanges three things: the
+// key count of CTA 0 (CTA 1's positions follow it), the overflow flags, and
+// the run's |E_r| for the guard.
+constexpr int kSpThreads = 512;
+
+__device__ __forceinline__ u32 split_local(u32 v, int t) {
+    return ((v >> (t + 1)) << t) | (v & ((u32(1) << t) - 1));
+}
+__device__ __forceinline__ u32 split_key(u32 li, u32 r, int t) {
+    return ((li >> t) << (t + 1)) | (r << t) | (li & ((u32(1) << t) - 1));
+}
+
+// One pass over the run's keys, keeping those owned by CTA r: count
+// (out == nullptr) or scatter at base + chunk base + in-chunk offset.
+template <bool AGG, bool CHECK, class K>
+__device__ __forceinline__ void split_pass(SmemTab16& tab, const K* __restrict__ kb, u64 p, int t, u32 r, u32 base,
+                                           u32* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const u64 step = u64(blockDim.x) * kCtUnroll;
+    for (u64 i0 = 0; i0 < p; i0 += step) {
+        u32 v[kCtUnroll];
+#pragma unroll
+        for (int u = 0; u < kCtUnroll; ++u) {
+            const u64 i = i0 + u64(u) * blockDim.x + threadIdx.x;
+            v[u] = i < p ? u32(__ldg(kb + i)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kCtUnroll; ++u) {
+            const u64 i = i0 + u64(u) * blockDim.x + threadIdx.x;
+            const bool valid = i < p && ((v[u] >> t) & 1u) == r;
+            const u32 li = split_local(v[u], t);
+            if (AGG) {
+                const u32 active = __ballot_sync(0xffffffffu, valid);
+                if (valid) {
+                    const u32 peers = __match_any_sync(active, li);
+                    const int leader = __ffs(peers) - 1;
+                    u32 pos = 0;
+                    if (lane == leader) {
+                        pos = tab.template add<CHECK>(li, __popc(peers));
+                        if (out) pos += base + tab.chunk_base(li);
+                    }
+                    if (out) {
+                        pos = __shfl_sync(peers, pos, leader) + __popc(peers & lanemask_lt());
+                        out[pos] = u32(i);
+                    }
+                }
+            } else if (valid) {
+                const u32 pos = tab.template add<CHECK>(li, 1u);
+                if (out) out[base + tab.chunk_base(li) + pos] = u32(i);
+            }
+        }
+    }
+}
+
+template <class K, bool AGG, bool CHECK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split_group_join(
+    const K* __restrict__ keys, u64 p, int M, const K* __restrict__ xorc, u64 guard, u32 hmax,
+    u32* __restrict__ grouped, u64* __restrict__ tot, u64* __restrict__ work_run, Item* __restrict__ items,
+    u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs, PairRec* __restrict__ pairs, u32 pair_cap,
+    u32* __restrict__ gtab, u32* __restrict__ slots) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) u32 smem[];
+    __shared__ u32 ws[68];
+    __shared__ u32 s_ovf, s_n, s_slot;
+    __shared__ u64 red[2][33];
+    __shared__ u64 s_part[2];
+    const u32 r = cl.block_rank();
+    const u32 b = blockIdx.y;
+    const K* kb = keys + u64(b) * p;
+    u32* out = grouped + u64(b) * p;
+    const int Ml = M - 1;
+    const u32 Tl = u32(1) << Ml;
+    const int cbits = min(Ml, kCtChunkBits);
+    const u32 nbase = max(1u, Tl >> cbits);
+    SmemTab16 tab{smem + nbase, smem, Ml, cbits, &s_ovf};
+    const u32 mask = (u32(1) << M) - 1;
+    const u32 c = u32(xorc[b]) & mask;
+    const u32 zb = ~c & mask;
+    const bool local = zb != 0;
+    const int t = local ? __ffs(zb) - 1 : M - 1;
+
+    if (threadIdx.x == 0) s_ovf = 0;
+    tab.clear();
+    __syncthreads();
+    split_pass<AGG, CHECK>(tab, kb, p, t, r, 0u, static_cast<u32*>(nullptr));
+    __syncthreads();
+    const u32 n_mine = tab.scan(ws);
+    if (threadIdx.x == 0) s_n = n_mine;
+    __syncthreads();
+    cl.sync();  // #1: counts and overflow flags of both CTAs
+    const u32 n_other = *cl.map_shared_rank(&s_n, r ^ 1u);
+    const bool ovf = CHECK && (s_ovf | *cl.map_shared_rank(&s_ovf, r ^ 1u));
+    if (ovf) {
+        // a bucket or chunk above 65535 columns: CTA 0 redoes the whole run with
+        // 32-bit counters in a global scratch slot (slots taken by CAS, released after)
+        if (r == 0) {
+            if (threadIdx.x == 0) {
+                u32 sl = b % kSMs;
+                while (atomicCAS(slots + sl, 0u, 1u) != 0u) sl = (sl + 1) % kSMs;
+                s_slot = sl;
+            }
+            __syncthreads();
+            GlobalTab32 g{gtab + (u64(s_slot) << M), M};
+            g.clear();
+            __syncthreads();
+            tab_pass<AGG, false, false>(g, kb, p, static_cast<u32*>(nullptr));
+            __syncthreads();
+            g.scan(ws);
+            __syncthreads();
+            tab_pass<AGG, false, false>(g, kb, p, out);
+            __syncthreads();
+            tab_join<K>(g, M, b, K(c), p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs,
+                        pair_cap, red, ws);
+            __threadfence();
+            if (threadIdx.x == 0) atomicExch(slots + s_slot, 0u);
+        }
+        cl.sync();
+        return;
+    }
+    const u32 n0 = r == 0 ? n_mine : n_other;  // CTA 1's positions follow CTA 0's
+    const u32 base = r == 0 ? 0u : n0;
+    split_pass<AGG, false>(tab, kb, p, t, r, base, out);
+    __syncthreads();
+    if (!local) cl.sync();  // #2: the partner's table is final before remote reads
+    // group of key v: its owner's table (local or, for c = all ones, the partner's)
+    SmemTab16 rt = tab;
+    rt.w = cl.map_shared_rank(tab.w, r ^ 1u);
+    rt.base = cl.map_shared_rank(tab.base, r ^ 1u);
+    const u32 other_base = r == 0 ? n0 : 0u;
+    auto group = [&](u32 v, u32& beg, u32& cnt) {
+        if (((v >> t) & 1u) == r) {
+            tab.group(split_local(v, t), beg, cnt);
+            beg += base;
+        } else {
+            rt.group(split_local(v, t), beg, cnt);
+            beg += other_base;
+        }
+    };
+    auto block_of = [&](u32 li) {
+        HeadBlock hb;
+        const u32 v = split_key(li, r, t);
+        u32 bx, cx;
+        group(v, bx, cx);
+        if (cx == 0) return hb;
+        const u32 v2 = v ^ c;
+        if (v2 == v) {
+            hb.pairs = u64(cx) * cx;  // the diagonal j == k counts (pair_search.cpp:48-49)
+            if (cx >= 2) {
+                hb.work = u64(cx) * (cx - 1) / 2;
+                hb.hs = bx; hb.hc = cx; hb.ss = bx; hb.sc = cx; hb.flags = 3u;
+            }
+        } else if (v2 > v) {
+            u32 bz, cz;
+            group(v2, bz, cz);
+            if (cz) {
+                hb.pairs = 2ull * cx * cz;
+                hb.work = u64(cx) * cz;
+                if (cx <= cz) {
+                    hb.hs = bx; hb.hc = cx; hb.ss = bz; hb.sc = cz; hb.flags = 1u;
+                } else {
+                    hb.hs = bz; hb.hc = cz; hb.ss = bx; hb.sc = cx; hb.flags = 0u;
+                }
+            }
+        }
+        return hb;
+    };
+    // join pass 1: |E_r| share, canonical work, this thread's item / pair counts
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool pair_list = npairs != nullptr;
+    u64 pa = 0, wa = 0;
+    u32 my_items = 0, my_pairs = 0;
+    for (u32 li = threadIdx.x; li < Tl; li += blockDim.x) {
+        const HeadBlock hb = block_of(li);
+        pa += hb.pairs;
+        wa += hb.work;
+        u32 ne, np, nsc;
+        emit_count(hb, hmax, pair_list, ne, np, nsc);
+        my_items += ne;
+        my_pairs += np;
+    }
+    pa = warp_sum(pa);
+    wa = warp_sum(wa);
+    if (lane == 0) {
+        red[0][wid] = pa;
+        red[1][wid] = wa;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 a = 0, w = 0;
+        for (int q = 0; q < nw; ++q) {
+            a += red[0][q];
+            w += red[1][q];
+        }
+        s_part[0] = a;
+        s_part[1] = w;
+    }
+    cl.sync();  // #3: both CTAs' shares of |E_r|
+    const u64* op = cl.map_shared_rank(s_part, r ^ 1u);
+    const u64 run_pairs = s_part[0] + op[0];
+    if (r == 0 && threadIdx.x == 0) {
+        tot[b] = run_pairs;
+        work_run[b] = s_part[1] + op[1];
+    }
+    if (run_pairs <= guard) {
+        u32 ti, tp;
+        u32 ibase = block_exclusive(my_items, ws, &ti);
+        u32 pbase = block_exclusive(my_pairs, ws + 33, &tp);
+        if (threadIdx.x == 0) {
+            ws[66] = ti ? atomicAdd(nitems, ti) : 0u;
+            ws[67] = (pair_list && tp) ? atomicAdd(npairs, tp) : 0u;
+        }
+        __syncthreads();
+        ibase += ws[66];
+        pbase += ws[67];
+        for (u32 li = threadIdx.x; li < Tl; li += blockDim.x) {
+            const HeadBlock hb = block_of(li);
+            if (hb.work == 0) continue;
+            u32 ne, np, nsc;
+            emit_count(hb, hmax, pair_list, ne, np, nsc);
+            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p);
+            ibase += ne;
+            pbase += np;
+        }
+    }
+    cl.sync();  // #4: the partner may still read this CTA's table and shares
+}
+
+inline size_t split_group_smem(int M) {
+    const u64 Tl = u64(1) << (M - 1);
+    const int cbits = (M - 1) < kCtChunkBits ? (M - 1) : kCtChunkBits;
+    return size_t(Tl / 2) * 4 + size_t(std::max<u64>(1, Tl >> cbits)) * 4;
+}
+
+template <class K, bool AGG, bool CHECK>
+void split_group_join_go(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 guard, u32 hmax, u32* grouped,
+                         u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
+                         u32 pair_cap, u32* gtab, u32* slots, cudaStream_t st) {
+    auto kernel = split_group_join<K, AGG, CHECK>;
+    static bool attr = false;  // one per instantiation
+    if (!attr) {
+        XYZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(split_group_smem(16))));
+        attr = true;
+    }
+    dim3 grid(2, static_cast<u32>(B));
+    kernel<<<grid, kSpThreads, split_group_smem(M), st>>>(keys, p, M, xorc, guard, hmax, grouped, tot, work_run,
+                                                          items, nitems, item_cap, npairs, pairs, pair_cap, gtab,
+                                                          slots);
+}
+
+// M in [2, 16]; gtab / slots: the overflow scratch (p > 65535 only).
+template <class K>
+void split_group_join_launch(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 guard, u32 hmax, u32* grouped,
+                             u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs,
+                             PairRec* pairs, u32 pair_cap, u32* gtab, u32* slots, cudaStream_t st) {
+    const bool agg = M <= 12;
+    const bool check = p > 0xffffu;
+    auto go = agg ? (check ? split_group_join_go<K, true, true> : split_group_join_go<K, true, false>)
+                  : (check ? split_group_join_go<K, false, true> : split_group_join_go<K, false, false>);
+    go(keys, B, p, M, xorc, guard, hmax, grouped, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap,
+       gtab, slots, st);
 }
 
 // Shared bytes of the table for 2^M buckets.

@@ -215,7 +215,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal;
     // batch scratch
     DevBuf keys[2], vals[2], hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -801,10 +801,17 @@ void run_batches(SearchCtx& c) {
     // XYZB_GROUPING=cluster keeps the DSMEM cluster kernel
     const bool grouped_path = M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
                               !(gsel && (std::string(gsel) == "sort" || std::string(gsel) == "bucket"));
+    // 4 <= M <= 16: two CTAs per run (cluster), bucket space split on a key bit
+    // (XYZB_GROUPING=cta keeps one CTA per run)
     const bool cta_path = grouped_path && M <= 16 && !(gsel && std::string(gsel) == "cluster");
+    const bool split_path = cta_path && M >= 4 && !(gsel && std::string(gsel) == "cta");
     const bool cluster_path = grouped_path && !cta_path;
     if (cta_path && kern::cta_group_scratch(int(M), p)) ds->gtab.ensure(kern::cta_group_scratch(int(M), p) * 4);
-    const bool buckets = !cluster_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
+    if (split_path) {
+        ds->slots.ensure(kSMs * 4);
+        XYZB_CUDA(cudaMemsetAsync(ds->slots.p, 0, kSMs * 4, st));
+    }
+    const bool buckets = !grouped_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
                          !(gsel && std::string(gsel) == "sort") && !sort_sel;
     if (buckets) {
         ds->bcnt.ensure((B << M) * 4);
@@ -880,7 +887,20 @@ void run_batches(SearchCtx& c) {
         const K* sorted_keys = nullptr;
         int vshift = 0;
         cudaEvent_t e2;
-        if (cta_path) {
+        if (split_path) {
+            // ---- group + join fused: two CTAs per run, each half of the 16-bit bucket table ----
+            kern::split_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
+                                             ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
+                                             nitems, static_cast<u32>(item_cap), npairs_b,
+                                             ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap),
+                                             ds->gtab.as<u32>(), ds->slots.as<u32>(), st);
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_SORT] += 1;
+            sv = vb[0];
+            e2 = clk.mark();
+            clk.span(XYZB_STAGE_SORT, e1, e2);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+        } else if (cta_path) {
             // ---- group + join fused: one CTA per run, 16-bit bucket counters in shared memory ----
             kern::cta_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
                                            ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
@@ -1003,8 +1023,8 @@ void run_batches(SearchCtx& c) {
         A.guard = c.guard;
         A.sv = sv;
         A.S = p;
-        A.vkeys = (buckets || cluster_path) ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
-        A.vkeys_by_pos = (buckets || cluster_path) ? 0 : 1;
+        A.vkeys = (buckets || grouped_path) ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
+        A.vkeys_by_pos = (buckets || grouped_path) ? 0 : 1;
         A.key64 = sizeof(K) == 8;
         A.vshift = vshift;
         A.rid = rid;

@@ -46,14 +46,14 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cluster", "bucket", "sort", "segments", "merge_large"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "sort", "segments", "merge_large"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
 def test_search_matches_reference_fixture(name, grouping, monkeypatch):
-    """All grouping paths: one CTA per run with 16-bit shared counters
-    (default for M <= 16), the DSMEM cluster kernel, the multi-kernel counting
-    sort into 2^M buckets, per-run cluster radix sort, multi-kernel segmented
-    radix sort."""
-    if grouping in ("sort", "bucket", "cluster"):
+    """All grouping paths: two CTAs per run splitting the 16-bit shared
+    bucket table (default for 4 <= M <= 16), one CTA per run, the DSMEM
+    cluster kernel, the multi-kernel counting sort into 2^M buckets, per-run
+    cluster radix sort, multi-kernel segmented radix sort."""
+    if grouping in ("sort", "bucket", "cluster", "cta"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
@@ -194,7 +194,7 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cluster", "bucket", "sort", "segments"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "sort", "segments"])
 def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
@@ -202,7 +202,7 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
     cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=10)
     base = xb.Dataset(x).search(y, cfg)
-    if grouping in ("sort", "bucket", "cluster"):
+    if grouping in ("sort", "bucket", "cluster", "cta"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
@@ -374,12 +374,12 @@ def test_xyz1_file_ingest_matches_in_memory_and_reference_errors(tmp_path):
         xb.Dataset.open(tmp_path / "missing.xyz")
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cluster"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster"])
 def test_bucket_above_16_bits_falls_back_exactly(grouping, monkeypatch):
     """p > 65535 with 70000 identical (monomorphic) columns: one bucket holds
     more columns than a 16-bit shared counter can; the CTA grouping redoes
     such a run with 32-bit counters. Hits and counters equal the reference."""
-    if grouping == "cluster":
+    if grouping in ("cluster", "cta"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     xb = _engine()
     rng = np.random.default_rng(11)
@@ -420,3 +420,24 @@ def test_dirty_padding_bits_are_rejected_on_upload():
     cfg = xb.SearchConfig(m=4, l=6, gamma=0.6, seed=2)
     assert report_hits(xb.Dataset(xb.PackedMatrix(100, 40, pinned)).search(y, cfg)) == report_hits(
         xb.Dataset(x).search(y, cfg))
+
+
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster"])
+def test_constant_response_partner_is_the_complement(grouping, monkeypatch):
+    """y constant: in the negative pass c = x-key ^ z-key has every bit set, so
+    each key's partner is its complement (no key bit is shared by a key and
+    its partner: the two-CTA split reads the partner half through DSMEM)."""
+    if grouping in ("cluster", "cta"):
+        monkeypatch.setenv("XYZB_GROUPING", grouping)
+    xb = _engine()
+    x, _ = ck.ref_planted(300, 400, 3, 7, 0.9, 3)
+    y = np.ones(300, np.int8)
+    for m, g in ((6, 0.6), (10, 0.56)):
+        cfg = xb.SearchConfig(m=m, l=5, gamma=g, seed=9, threads=1, top_k=30, estimate_complexity=False)
+        got, want = xb.Dataset(x).search(y, cfg), ck.ref_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, msg
+        assert got.top_k == want.top_k
+        assert (got.candidates_enumerated, got.aborted_repetitions) == (want.candidates_enumerated,
+                                                                       want.aborted_repetitions)
+        assert len(want.hits) > 0
