@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kCgThreads) cluster_group_join(
             const u32 l = l0 + threadIdx.x;
             HeadBlock hb;
             if (l < per) hb = block_of(cr * per + l);
-            emit_items(hb, u32(b), hmax, items, nitems, item_cap, npairs, pairs, pair_cap, p);
+            emit_items(hb, u32(b), hmax, items, nitems, item_cap, npairs, pairs, pair_cap, p, grouped);
         }
     }
     cl.sync();  // peers may still read this CTA's table

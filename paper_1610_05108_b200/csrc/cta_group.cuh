@@ -237,7 +237,7 @@ template <class K, class Tab>
 __device__ void tab_join(const Tab& tab, int M, u32 b, K c, u64 p, u64 guard, u32 hmax, u64* __restrict__ tot,
                          u64* __restrict__ work_run, Item* __restrict__ items, u32* __restrict__ nitems, u32 item_cap,
                          u32* __restrict__ npairs, PairRec* __restrict__ pairs, u32 pair_cap, u64 (*red)[33],
-                         u32* ws) {
+                         u32* ws, const u32* __restrict__ grouped) {
     const u32 T = u32(1) << M;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const bool pair_list = npairs != nullptr;
@@ -288,7 +288,7 @@ __device__ void tab_join(const Tab& tab, int M, u32 b, K c, u64 p, u64 guard, u3
             if (hb.work == 0) continue;
             u32 ne, np, nsc;
             emit_count(hb, hmax, pair_list, ne, np, nsc);
-            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p);
+            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p, grouped);
             ibase += ne;
             pbase += np;
         }
@@ -332,13 +332,13 @@ __global__ void __launch_bounds__(kCtThreads) cta_group_join(
             tab_pass<AGG, false, false>(g, kb, p, out);
             __syncthreads();
             tab_join<K>(g, M, b, c, p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap,
-                        red, ws);
+                        red, ws, grouped);
             continue;
         }
         tab_pass<AGG, false, true>(tab, kb, p, out);
         __syncthreads();
         tab_join<K>(tab, M, b, c, p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap, red,
-                    ws);
+                    ws, grouped);
     }
 }
 
@@ -464,7 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
             tab_pass<AGG, false, false>(g, kb, p, out);
             __syncthreads();
             tab_join<K>(g, M, b, K(c), p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs,
-                        pair_cap, red, ws);
+                        pair_cap, red, ws, grouped);
             __threadfence();
             if (threadIdx.x == 0) atomicExch(slots + s_slot, 0u);
         }
@@ -571,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
             if (hb.work == 0) continue;
             u32 ne, np, nsc;
             emit_count(hb, hmax, pair_list, ne, np, nsc);
-            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p);
+            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p, grouped);
             ibase += ne;
             pbase += np;
         }

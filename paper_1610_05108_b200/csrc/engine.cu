@@ -214,7 +214,7 @@ struct xyzb_dataset {
     // response (per search)
     DevBuf yk_bits, spos, sneg, wabs, yreal;
     // batch scratch
-    DevBuf keys[2], vals[2], hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
+    DevBuf keys[2], vals[2], keys_x, hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
     DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
@@ -953,7 +953,8 @@ void run_batches(SearchCtx& c) {
             kern::bucket_join_emit<K><<<gb, 256, 0, st>>>(ds->bcnt.as<u32>(), ds->bend.as<u32>(), int(M), ds->xorc.as<K>(),
                                                           p, ds->tot.as<u64>(), c.guard, hmax, ds->items.as<kern::Item>(),
                                                           nitems, static_cast<u32>(item_cap), npairs_b,
-                                                          ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
+                                                          ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap),
+                                                          sv);
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 2;
         } else {
@@ -961,6 +962,10 @@ void run_batches(SearchCtx& c) {
             // M = 64 keeps plain keys and binary-search partner lookups
             const bool ukeys = M + 1 <= sizeof(K) * 8;
             const int sbits = ukeys ? bits + 1 : bits;
+            if (pair_path) {  // pair-list hits look keys up by column: keep the unsorted keys
+                ds->keys_x.ensure(nb * p * sizeof(K));
+                XYZB_CUDA(cudaMemcpyAsync(ds->keys_x.p, k0, nb * p * sizeof(K), cudaMemcpyDeviceToDevice, st));
+            }
             if (ukeys) {
                 kern::ukey_transform<K><<<grid_for(nb * p, 256, 4096), 256, 0, st>>>(k0, p, nb * p, ds->xorc.as<K>());
                 XYZB_LAUNCH_CHECK();
@@ -992,7 +997,7 @@ void run_batches(SearchCtx& c) {
                 kern::ujoin_emit<K><<<gj, 256, 0, st>>>(kb[res], p, ds->xorc.as<K>(), ds->tot.as<u64>(), c.guard, hmax,
                                                         ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
                                                         npairs_b, ds->pairs.as<kern::PairRec>(),
-                                                        static_cast<u32>(c.pair_cap));
+                                                        static_cast<u32>(c.pair_cap), sv);
                 XYZB_LAUNCH_CHECK();
             } else {
                 kern::join_count<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), nullptr,
@@ -1001,7 +1006,7 @@ void run_batches(SearchCtx& c) {
                 kern::join_emit<K><<<gj, 256, 0, st>>>(kb[res], p, int(M), ds->xorc.as<K>(), nullptr, ds->tot.as<u64>(),
                                                        c.guard, hmax, ds->items.as<kern::Item>(), nitems,
                                                        static_cast<u32>(item_cap), npairs_b,
-                                                       ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap));
+                                                       ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap), sv);
                 XYZB_LAUNCH_CHECK();
             }
             c.launches[XYZB_STAGE_JOIN] += 2;
@@ -1025,6 +1030,7 @@ void run_batches(SearchCtx& c) {
         A.S = p;
         A.vkeys = (buckets || grouped_path) ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
         A.vkeys_by_pos = (buckets || grouped_path) ? 0 : 1;
+        A.xkeys = (buckets || grouped_path) ? static_cast<const void*>(k0) : ds->keys_x.p;
         A.key64 = sizeof(K) == 8;
         A.vshift = vshift;
         A.rid = rid;
@@ -1033,11 +1039,12 @@ void run_batches(SearchCtx& c) {
         A.hits = ds->hits.as<kern::DevHit>();
         A.hit_count = ds->hit_count.as<u32>();
         A.hit_cap = ds->hit_cap;
-        const u32 vgrid = kSMs * 8;
+        u32 vgrid = kSMs * 8;
+        if (const char* ev = std::getenv("XYZB_VGRID")) vgrid = static_cast<u32>(std::max(1ul, std::strtoul(ev, nullptr, 10)));
         if (pair_path) {
             u32* np = ds->npairs.as<u32>() + batch_idx;
             kern::expand_pairs<<<vgrid, 256, 0, st>>>(A.items, A.nitems, A.item_cap, p, ds->pairs.as<kern::PairRec>(),
-                                                      static_cast<u32>(c.pair_cap));
+                                                      static_cast<u32>(c.pair_cap), sv);
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 1;
             const u64 W2 = ds->Wp / 2;

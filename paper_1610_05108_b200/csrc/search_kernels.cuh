@@ -46,7 +46,7 @@ struct Item {
 // re-oriented by column index at hit time), the batch-local run, and the
 // block flags.
 struct __align__(16) PairRec {
-    u32 pa, pb, run, pad;
+    u32 pa, pb, run, pad;  // pa / pb: the COLUMNS of the x side and the z side
 };
 constexpr u64 kInlinePairs = 32;  // blocks up to this many pairs are expanded by join_emit
 
@@ -315,21 +315,24 @@ __device__ __forceinline__ void emit_count(const HeadBlock& hb, u32 hmax, bool p
 }
 
 // Write block `hb`'s items from slot `base` and its pairs from slot `poff`.
+// Pairs carry column indices (grp: the grouped columns, position -> column),
+// so the verify reads no position table.
 __device__ __forceinline__ void emit_write(const HeadBlock& hb, u32 b, u32 hmax, bool pair_list, u32 nemit, u32 nsc,
                                            u32 base, u32 poff, Item* __restrict__ items, u32 item_cap,
-                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S) {
+                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S,
+                                           const u32* __restrict__ grp) {
     const bool inline_pairs = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
     const bool diag = hb.flags & 2u;
     if (inline_pairs) {
         const bool first_held = diag || (hb.flags & 1u);
         const u32 off = u32(u64(b) * S);  // pair positions are u32 (b * S + pos < 2^32, checked by the host)
         uint4* dst = reinterpret_cast<uint4*>(pairs);
-        for (u32 h = 0; h < hb.hc; ++h) {
-            const u32 hpos = off + hb.hs + h;
+        for (u32 h = 0; h < hb.hc && poff < pair_cap; ++h) {
+            const u32 hcol = grp[off + hb.hs + h];
             for (u32 q = diag ? h + 1 : 0; q < hb.sc; ++q, ++poff) {
                 if (poff >= pair_cap) break;
-                const u32 spos = off + hb.ss + q;
-                dst[poff] = make_uint4(first_held ? hpos : spos, first_held ? spos : hpos, b, hb.flags);
+                const u32 scol = grp[off + hb.ss + q];
+                dst[poff] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, hb.flags);
             }
         }
     }
@@ -369,7 +372,8 @@ __device__ __forceinline__ void emit_write(const HeadBlock& hb, u32 b, u32 hmax,
 // the host can regrow.
 __device__ __forceinline__ void emit_items(const HeadBlock& hb, u32 b, u32 hmax, Item* __restrict__ items,
                                            u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs,
-                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S) {
+                                           PairRec* __restrict__ pairs, u32 pair_cap, u64 S,
+                                           const u32* __restrict__ grp) {
     u32 nemit, npair, nsc;
     emit_count(hb, hmax, npairs != nullptr, nemit, npair, nsc);
     u32 incl = nemit, pincl = npair;
@@ -407,7 +411,7 @@ __device__ __forceinline__ void emit_items(const HeadBlock& hb, u32 b, u32 hmax,
     __syncthreads();
     const u32 base = s_items[32] + s_items[wid] + incl - nemit;
     const u32 poff = s_pairs[32] + s_pairs[wid] + pincl - npair;  // this block's first pair slot
-    emit_write(hb, b, hmax, npairs != nullptr, nemit, nsc, base, poff, items, item_cap, pairs, pair_cap, S);
+    emit_write(hb, b, hmax, npairs != nullptr, nemit, nsc, base, poff, items, item_cap, pairs, pair_cap, S, grp);
 }
 
 // Pass 2 (sorted keys): canonical work items of the runs the guard keeps.
@@ -417,13 +421,13 @@ __global__ void __launch_bounds__(256) join_emit(const K* __restrict__ sk, u64 S
                                                  u64 guard, u32 hmax, Item* __restrict__ items,
                                                  u32* __restrict__ nitems, u32 item_cap,
                                                  u32* __restrict__ npairs, PairRec* __restrict__ pairs,
-                                                 u32 pair_cap) {
+                                                 u32 pair_cap, const u32* __restrict__ grp) {
     const u32 b = blockIdx.y;
     const bool aborted = tot[b] > guard;
     const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
     HeadBlock hb;
     if (!aborted) hb = head_block(sk + u64(b) * S, i, S, M, xorc[b], table, b);
-    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S);
+    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S, grp);
 }
 
 // ------------------------------------------------ symmetric sorted keys --
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(256) ujoin_emit(const K* __restrict__ sk, u64 
                                                   const u64* __restrict__ tot, u64 guard, u32 hmax,
                                                   Item* __restrict__ items, u32* __restrict__ nitems, u32 item_cap,
                                                   u32* __restrict__ npairs, PairRec* __restrict__ pairs,
-                                                  u32 pair_cap) {
+                                                  u32 pair_cap, const u32* __restrict__ grp) {
     const u32 b = blockIdx.y;
     const u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x;
     HeadBlock hb;
@@ -535,7 +539,7 @@ __global__ void __launch_bounds__(256) ujoin_emit(const K* __restrict__ sk, u64 
             hb = HeadBlock();
         }
     }
-    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S);
+    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, S, grp);
 }
 
 // ------------------------------------------------- bucket grouping path --
@@ -646,12 +650,12 @@ __global__ void __launch_bounds__(256) bucket_join_emit(const u32* __restrict__ 
                                                         u64 guard, u32 hmax, Item* __restrict__ items,
                                                         u32* __restrict__ nitems, u32 item_cap,
                                                         u32* __restrict__ npairs, PairRec* __restrict__ pairs,
-                                                        u32 pair_cap) {
+                                                        u32 pair_cap, const u32* __restrict__ grp) {
     const u32 b = blockIdx.y;
     const u64 v = u64(blockIdx.x) * blockDim.x + threadIdx.x;
     HeadBlock hb;
     if (v < (u64(1) << M) && tot[b] <= guard) hb = bucket_block(cnt, end, b, M, v, u64(xorc[b]), p);
-    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, p);
+    emit_items(hb, b, hmax, items, nitems, item_cap, npairs, pairs, pair_cap, p, grp);
 }
 
 // Per-run counters; the guard (pair_search.hpp:91-94) zeroes the verified
@@ -686,6 +690,7 @@ struct VerifyArgs {
     // x-side position, or (bucket path, keys unsorted) at the column index
     const void* vkeys;
     int vkeys_by_pos;
+    const void* xkeys;  // unsorted keys of the batch by column (pair-list hits)
     int key64;
     int vshift;  // sorted keys carry extra low bits to drop (0 here)
 };
@@ -748,6 +753,25 @@ __device__ __forceinline__ DevHit make_hit(const VerifyArgs& A, u32 run, u32 hel
     return hit_of(A, run, diag || held_x ? held_pos : str_pos, diag || held_x ? str_pos : held_pos, diag, s, sint);
 }
 
+// Hit record of a pair-list candidate (x-side column j, z-side column k).
+__device__ __forceinline__ DevHit hit_cols(const VerifyArgs& A, u32 run, u32 j, u32 k, bool diag, double s,
+                                           int32_t sint) {
+    if (diag && j > k) {
+        const u32 t = j;
+        j = k;
+        k = t;
+    }
+    const u64 i = u64(run) * A.S + j;
+    DevHit h;
+    h.order = A.key64 ? static_cast<const u64*>(A.xkeys)[i] : u64(static_cast<const u32*>(A.xkeys)[i]);
+    h.s = s;
+    h.j = j;
+    h.k = k;
+    h.rid = A.rid[run];
+    h.sint = sint;
+    return h;
+}
+
 // ------------------------------------------------------- pair list path --
 
 
@@ -755,7 +779,8 @@ __device__ __forceinline__ DevHit make_hit(const VerifyArgs& A, u32 run, u32 hel
 // share the held column and stay in one team's L1). Warp per item; slots
 // were reserved by join_emit (the counter runs past pair_cap for a regrow).
 __global__ void __launch_bounds__(256) expand_pairs(const Item* __restrict__ items, const u32* __restrict__ nitems,
-                                                    u32 item_cap, u64 S, PairRec* __restrict__ pairs, u32 pair_cap) {
+                                                    u32 item_cap, u64 S, PairRec* __restrict__ pairs, u32 pair_cap,
+                                                    const u32* __restrict__ grp) {
     const int lane = threadIdx.x & 31;
     const u32 N = min(*nitems, item_cap);
     const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -770,6 +795,7 @@ __global__ void __launch_bounds__(256) expand_pairs(const Item* __restrict__ ite
         const bool first_held = diag || held_x;
         for (u32 h = 0; h < hc; ++h) {
             const u32 hpos = it.hs + h;
+            const u32 hcol = grp[off + hpos];
             for (u32 s0 = 0; s0 < it.sc; s0 += 32) {
                 const u32 q = s0 + lane;
                 const u32 spos = it.ss + q;
@@ -778,9 +804,10 @@ __global__ void __launch_bounds__(256) expand_pairs(const Item* __restrict__ ite
                 if (ok) {
                     const u32 slot = base + written + __popc(bal & lanemask_lt());
                     if (slot < pair_cap) {
+                        const u32 scol = grp[off + spos];
                         PairRec r;
-                        r.pa = u32(off + (first_held ? hpos : spos));
-                        r.pb = u32(off + (first_held ? spos : hpos));
+                        r.pa = first_held ? hcol : scol;
+                        r.pb = first_held ? scol : hcol;
                         r.run = it.run;
                         r.pad = flags;
                         pairs[slot] = r;
@@ -850,8 +877,8 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
             const u32 t = tl + G * i;
             if (t < cnt) {
                 pr[i] = pairs[c0 + t];
-                cj[i] = A.sv[pr[i].pa];
-                ck[i] = A.sv[pr[i].pb];
+                cj[i] = pr[i].pa;
+                ck[i] = pr[i].pb;
             } else {
                 pr[i] = PairRec{0, 0, 0, 0};
                 cj[i] = ck[i] = 0;
@@ -896,11 +923,7 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
                     if (q == i) r = pr[q];
                 const u32 si = A.run_sign[r.run] > 0 ? acc : n - acc;
                 hit = si >= astar;
-                if (hit) {
-                    const u64 base = u64(r.run) * A.S;
-                    h = hit_of(A, r.run, u32(r.pa - base), u32(r.pb - base), (r.pad & 2u) != 0,
-                               double(si) / double(n), int32_t(si));
-                }
+                if (hit) h = hit_cols(A, r.run, r.pa, r.pb, (r.pad & 2u) != 0, double(si) / double(n), int32_t(si));
             }
             team_append<G>(A, tmask, hit, h);
             if (t + 1 < cnt) cur = nxt;
@@ -936,7 +959,7 @@ __global__ void __launch_bounds__(256) verify_pairs_simple(VerifyArgs A, const P
         const u32 c1 = u32(minu(P, c0 + CH));
         for (u32 q = u32(c0); q < c1; ++q) {
             const PairRec pr = pairs[q];
-            const u32 j = A.sv[pr.pa], k = A.sv[pr.pb];
+            const u32 j = pr.pa, k = pr.pb;
             ColPair<G, NIT> c;
             load_cols<G, NIT>(c, X2, W2, j, k, tl);
             u32 acc = 0;
@@ -948,11 +971,7 @@ __global__ void __launch_bounds__(256) verify_pairs_simple(VerifyArgs A, const P
             const u32 si = A.run_sign[pr.run] > 0 ? acc : n - acc;
             const bool hit = tl == 0 && si >= astar;
             DevHit h;
-            if (hit) {
-                const u64 base = u64(pr.run) * A.S;
-                h = hit_of(A, pr.run, u32(pr.pa - base), u32(pr.pb - base), (pr.pad & 2u) != 0, double(si) / double(n),
-                           int32_t(si));
-            }
+            if (hit) h = hit_cols(A, pr.run, pr.pa, pr.pb, (pr.pad & 2u) != 0, double(si) / double(n), int32_t(si));
             team_append<G>(A, tmask, hit, h);
         }
     }

@@ -35,6 +35,43 @@ __global__ void __launch_bounds__(256) gather(const ulonglong2* __restrict__ X, 
     if (acc == 0xffffffffu) atomicAdd(sink, acc);
 }
 
+// The verify shape: pair record (16 B) -> column ids through the grouped
+// positions (sv) -> the two columns.
+template <int G>
+__global__ void __launch_bounds__(256) gather_indirect(const ulonglong2* __restrict__ X, const uint4* __restrict__ pr,
+                                                       const uint32_t* __restrict__ sv, uint32_t npairs,
+                                                       unsigned long long* sink) {
+    const int lane = threadIdx.x & 31, tl = lane & (G - 1);
+    const uint32_t team = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint32_t nteams = (gridDim.x * blockDim.x) / G;
+    uint32_t acc = 0;
+    for (uint32_t c0 = team * 32; c0 < npairs; c0 += nteams * 32) {
+        const uint32_t c1 = min(npairs, c0 + 32);
+        for (uint32_t q = c0; q < c1; ++q) {
+            const uint4 r = pr[q];
+            const uint32_t j = sv[r.x], k = sv[r.y];
+            const ulonglong2* a = X + size_t(j) * 32;
+            const ulonglong2* b = X + size_t(k) * 32;
+            ulonglong2 va[32 / G], vb[32 / G];
+#pragma unroll
+            for (int it = 0; it < 32 / G; ++it) {
+                va[it] = __ldg(a + it * G + tl);
+                vb[it] = __ldg(b + it * G + tl);
+            }
+#pragma unroll
+            for (int it = 0; it < 32 / G; ++it) acc += __popcll(va[it].x ^ vb[it].x) + __popcll(va[it].y ^ vb[it].y);
+        }
+    }
+    if (acc == 0xffffffffu) atomicAdd(sink, acc);
+}
+
+__global__ void fill_pairs(uint4* pr, uint32_t* sv, uint32_t npairs, uint32_t nsv, uint32_t ncols) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x)
+        pr[i] = make_uint4(hash32(2 * i) % nsv, hash32(2 * i + 1) % nsv, 0, 0);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nsv; i += gridDim.x * blockDim.x)
+        sv[i] = hash32(i ^ 0x9e3779b9u) % ncols;
+}
+
 __global__ void sweep(const ulonglong2* __restrict__ X, size_t n, unsigned long long* sink) {
     uint64_t acc = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
@@ -67,6 +104,7 @@ int main() {
     }
     for (int g : {4, 8, 16, 32}) {
         for (int grid : {148 * 4, 148 * 8, 148 * 16}) {
+          for (int w = 0; w < 2; ++w) {
             cudaEventRecord(e0);
             for (int r = 0; r < 5; ++r) {
                 if (g == 4) gather<4><<<grid, 256>>>(X, ncols, npairs, r, sink);
@@ -77,8 +115,33 @@ int main() {
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             cudaEventElapsedTime(&ms, e0, e1);
+          }
             printf("random 512 B column pairs, team %2d lanes, grid %5d: %.1f GB/s (%.3f ms per 16M pairs)\n", g,
                    grid, 5.0 * npairs * 1024 / (ms * 1e-3) / 1e9, ms / 5);
+        }
+    }
+    {
+        const uint32_t nsv = 20000000;
+        uint4* pr;
+        uint32_t* sv;
+        cudaMalloc(&pr, size_t(npairs) * 16);
+        cudaMalloc(&sv, size_t(nsv) * 4);
+        fill_pairs<<<148 * 8, 256>>>(pr, sv, npairs, nsv, ncols);
+        for (int g : {8, 16}) {
+            for (int grid : {148 * 4, 148 * 8, 148 * 16}) {
+                for (int w = 0; w < 2; ++w) {
+                    cudaEventRecord(e0);
+                    for (int r = 0; r < 5; ++r) {
+                        if (g == 8) gather_indirect<8><<<grid, 256>>>(X, pr, sv, npairs, sink);
+                        if (g == 16) gather_indirect<16><<<grid, 256>>>(X, pr, sv, npairs, sink);
+                    }
+                    cudaEventRecord(e1);
+                    cudaEventSynchronize(e1);
+                    cudaEventElapsedTime(&ms, e0, e1);
+                }
+                printf("pair list + sv indirection, team %2d lanes, grid %5d: %.1f GB/s of columns (%.3f ms per 16M pairs)\n",
+                       g, grid, 5.0 * npairs * 1024 / (ms * 1e-3) / 1e9, ms / 5);
+            }
         }
     }
     cudaError_t err = cudaDeviceSynchronize();
