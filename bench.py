@@ -25,6 +25,7 @@ NCCL and merged on the device.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -171,6 +172,20 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def gather_peak(device, ncols, words):
+    """Measured random column-pair gather rate for an X of this shape
+    (libxyzb_probe.so): the verify kernel's ceiling when X is L2-resident."""
+    try:
+        lib = ctypes.CDLL(os.path.join(ROOT, "paper_1610_05108_b200", "libxyzb_probe.so"))
+        lib.xyzb_probe_pair_gather.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                               ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+        g = ctypes.c_double()
+        rc = lib.xyzb_probe_pair_gather(device, ncols, words, 16_000_000, 3, ctypes.byref(g))
+        return g.value if rc == 0 else None
+    except OSError:
+        return None
 
 
 def ncu_traffic():
@@ -379,6 +394,17 @@ def main():
         t_dev, runs, verified = float(tmax[0]), int(tsum[1]), int(tsum[2])
     value = runs / (t_dev / 1e3)
     out = None
+    l2_roof = None
+    if rank == 0 and WORKLOAD["mode"] == "binary" and workload_config(world, L)["x_bytes"] <= (96 << 20):
+        words = (WORKLOAD["n"] + 63) // 64
+        g = gather_peak(local, WORKLOAD["p"], words)
+        ach = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
+            else 0.0
+        if g:
+            l2_roof = {"bound": "l2 (X resident)", "kernel": "verify_pairs_binary", "achieved": ach, "peak": g,
+                       "unit": "GB/s", "frac": ach / g,
+                       "peak_source": "measured live: random column-pair gather + XOR-popcount probe on an X of "
+                                      "this shape (paper_1610_05108_b200/csrc/probe.cu), same byte count"}
     if rank == 0:
         hbm, src = peaks()
         achieved = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
@@ -401,6 +427,7 @@ def main():
                          "note": "algorithmic bytes = 2 columns per canonical candidate + Y (SURVEY 8d); when X "
                                  "fits in L2 (cfg1-3) the verify kernel can exceed the HBM roofline"},
             "clocks": clk.summary(),
+            "l2_roofline": l2_roof,
             "planted_found": sorted({(min(h.j, h.k), max(h.j, h.k)) for h in rep.hits} &
                                     {tuple(p) for p in planted.tolist()}),
         }
