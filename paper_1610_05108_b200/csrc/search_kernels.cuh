@@ -753,23 +753,25 @@ __device__ __forceinline__ DevHit make_hit(const VerifyArgs& A, u32 run, u32 hel
     return hit_of(A, run, diag || held_x ? held_pos : str_pos, diag || held_x ? str_pos : held_pos, diag, s, sint);
 }
 
-// Hit record of a pair-list candidate (x-side column j, z-side column k).
-__device__ __forceinline__ DevHit hit_cols(const VerifyArgs& A, u32 run, u32 j, u32 k, bool diag, double s,
-                                           int32_t sint) {
-    if (diag && j > k) {
+// One pair-list hit appended by one lane (hits are rare: no aggregation).
+__device__ __noinline__ void append_pair_hit(const void* xkeys, int key64, u64 S, const u32* rid, DevHit* hits,
+                                             u32* hit_count, u32 hit_cap, PairRec pr, u32 si, u32 n) {
+    u32 j = pr.pa, k = pr.pb;
+    if ((pr.pad & 2u) && j > k) {
         const u32 t = j;
         j = k;
         k = t;
     }
-    const u64 i = u64(run) * A.S + j;
+    const u64 i = u64(pr.run) * S + j;
     DevHit h;
-    h.order = A.key64 ? static_cast<const u64*>(A.xkeys)[i] : u64(static_cast<const u32*>(A.xkeys)[i]);
-    h.s = s;
+    h.order = key64 ? static_cast<const u64*>(xkeys)[i] : u64(static_cast<const u32*>(xkeys)[i]);
+    h.s = double(si) / double(n);
     h.j = j;
     h.k = k;
-    h.rid = A.rid[run];
-    h.sint = sint;
-    return h;
+    h.rid = rid[pr.run];
+    h.sint = int32_t(si);
+    const u32 slot = atomicAdd(hit_count, 1u);
+    if (slot < hit_cap) hits[slot] = h;
 }
 
 // ------------------------------------------------------- pair list path --
@@ -844,6 +846,9 @@ __device__ __forceinline__ void load_cols(ColPair<G, NIT>& c, const ulonglong2* 
 // popc(X_j ^ X_k ^ Y) over NIT x 16 B per lane, team reduction, integer hit
 // test by the pair's owning lane.
 constexpr u32 kPairsPerLane = 2;
+#ifndef XYZB_VP_MINB
+#define XYZB_VP_MINB 4
+#endif
 
 template <int G, int NIT>
 __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const PairRec* __restrict__ pairs,
@@ -913,8 +918,6 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(tmask, acc, o);
             // the owning lane tests pair t with its record
-            bool hit = false;
-            DevHit h;
             if (u32(tl) == t % G) {
                 const u32 i = t / G;
                 PairRec r = pr[0];
@@ -922,10 +925,8 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
                 for (u32 q = 1; q < kPairsPerLane; ++q)
                     if (q == i) r = pr[q];
                 const u32 si = A.run_sign[r.run] > 0 ? acc : n - acc;
-                hit = si >= astar;
-                if (hit) h = hit_cols(A, r.run, r.pa, r.pb, (r.pad & 2u) != 0, double(si) / double(n), int32_t(si));
+                if (si >= astar) append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, r, si, n);
             }
-            team_append<G>(A, tmask, hit, h);
             if (t + 1 < cnt) cur = nxt;
         }
     }
@@ -934,7 +935,7 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
 // Simple pair walk (one pair at a time per team, chunks of 32 pairs): kept
 // beside the pipelined walk for measurement (XYZB_VERIFY=simple).
 template <int G, int NIT>
-__global__ void __launch_bounds__(256) verify_pairs_simple(VerifyArgs A, const PairRec* __restrict__ pairs,
+__global__ void __launch_bounds__(256, XYZB_VP_MINB) verify_pairs_simple(VerifyArgs A, const PairRec* __restrict__ pairs,
                                                            const u32* __restrict__ npairs, u32 pair_cap,
                                                            const u64* __restrict__ Xc, u32 Wp,
                                                            const u64* __restrict__ Yw, u32 n, u32 astar) {
@@ -969,10 +970,8 @@ __global__ void __launch_bounds__(256) verify_pairs_simple(VerifyArgs A, const P
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(tmask, acc, o);
             const u32 si = A.run_sign[pr.run] > 0 ? acc : n - acc;
-            const bool hit = tl == 0 && si >= astar;
-            DevHit h;
-            if (hit) h = hit_cols(A, pr.run, pr.pa, pr.pb, (pr.pad & 2u) != 0, double(si) / double(n), int32_t(si));
-            team_append<G>(A, tmask, hit, h);
+            if (tl == 0 && si >= astar)  // rare: out of line, so the walk keeps few registers
+                append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, n);
         }
     }
 }
