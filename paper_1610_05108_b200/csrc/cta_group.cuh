@@ -344,14 +344,16 @@ __global__ void __launch_bounds__(kCtThreads) cta_group_join(
 
 // ------------------------------------------------ two-CTA split per run --
 //
-// The bucket space of a run is split on one key bit t between the two CTAs
-// of a cluster: CTA r owns the keys whose bit t equals r (2^(M-1) 16-bit
-// counters, 64 KB at M = 16, so three CTAs share an SM and every run of a
-// 200-run batch is resident at once instead of two rounds of one CTA per
-// SM). t is the lowest bit where c = x-key ^ z-key is 0, so a key and its
-// partner key v ^ c always live in the same CTA; only when c has no zero bit
-// (c = all ones, partner = ~v) does the join read the partner CTA's table
-// through distributed shared memory. The cluster exchanges three things: the
+// The bucket space of a run is split between the two CTAs of a cluster
+// (2^(M-1) 16-bit counters each, 64 KB at M = 16, so three CTAs share an SM
+// and every run of a 200-run batch is resident at once instead of two rounds
+// of one CTA per SM). CTA r owns the keys v with parity(v & Z) == r, Z = the
+// zero bits of c = x-key ^ z-key: a key and its partner v ^ c agree on Z, so
+// they always live in the same CTA, and the parity of several biased bits
+// splits the keys evenly. The local index drops bit t = lowest bit of Z
+// (recovered from r and the parity of the other Z bits). Only when c has no
+// zero bit (c = all ones, partner = ~v) is the split on bit t = M - 1 and the
+// join reads the partner CTA's table through distributed shared memory. The cluster exchanges three things: the
 // key count of CTA 0 (CTA 1's positions follow it), the overflow flags, and
 // the run's |E_r| for the guard.
 constexpr int kSpThreads = 512;
@@ -359,49 +361,70 @@ constexpr int kSpThreads = 512;
 __device__ __forceinline__ u32 split_local(u32 v, int t) {
     return ((v >> (t + 1)) << t) | (v & ((u32(1) << t) - 1));
 }
-__device__ __forceinline__ u32 split_key(u32 li, u32 r, int t) {
-    return ((li >> t) << (t + 1)) | (r << t) | (li & ((u32(1) << t) - 1));
+// Owner CTA of key v: parity of v & om (om = Z, or bit t when c has no zero bit).
+__device__ __forceinline__ u32 split_owner(u32 v, u32 om) { return u32(__popc(v & om)) & 1u; }
+__device__ __forceinline__ u32 split_key(u32 li, u32 r, int t, u32 om) {
+    const u32 u = ((li >> t) << (t + 1)) | (li & ((u32(1) << t) - 1));  // bit t clear
+    return u | ((r ^ split_owner(u, om)) << t);
 }
 
-// One pass over the run's keys, keeping those owned by CTA r: count
-// (out == nullptr) or scatter at base + chunk base + in-chunk offset.
-template <bool AGG, bool CHECK, class K>
-__device__ __forceinline__ void split_pass(SmemTab16& tab, const K* __restrict__ kb, u64 p, int t, u32 r, u32 base,
-                                           u32* __restrict__ out) {
+// Leaner pass over a run's u32 keys (the split path always has M <= 16):
+// 16-byte vector loads (8 keys in flight per thread), 32-bit indices, and
+// ownership / local index by masks. A scalar head and tail cover a run
+// whose keys are not 16-byte aligned. AGG keeps the warp-aggregated form for
+// small tables (every lane of a warp calls `one` the same number of times).
+template <bool AGG, bool CHECK, bool SCATTER>
+__device__ __forceinline__ void split_pass32(SmemTab16& tab, const u32* __restrict__ kb, u32 p, int t, u32 om,
+                                             u32 r, u32 base, u32* __restrict__ out) {
+    const u32 lo = (1u << t) - 1u;
     const int lane = threadIdx.x & 31;
-    const u64 step = u64(blockDim.x) * kCtUnroll;
-    for (u64 i0 = 0; i0 < p; i0 += step) {
-        u32 v[kCtUnroll];
-#pragma unroll
-        for (int u = 0; u < kCtUnroll; ++u) {
-            const u64 i = i0 + u64(u) * blockDim.x + threadIdx.x;
-            v[u] = i < p ? u32(__ldg(kb + i)) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < kCtUnroll; ++u) {
-            const u64 i = i0 + u64(u) * blockDim.x + threadIdx.x;
-            const bool valid = i < p && ((v[u] >> t) & 1u) == r;
-            const u32 li = split_local(v[u], t);
-            if (AGG) {
-                const u32 active = __ballot_sync(0xffffffffu, valid);
-                if (valid) {
-                    const u32 peers = __match_any_sync(active, li);
-                    const int leader = __ffs(peers) - 1;
-                    u32 pos = 0;
-                    if (lane == leader) {
-                        pos = tab.template add<CHECK>(li, __popc(peers));
-                        if (out) pos += base + tab.chunk_base(li);
-                    }
-                    if (out) {
-                        pos = __shfl_sync(peers, pos, leader) + __popc(peers & lanemask_lt());
-                        out[pos] = u32(i);
-                    }
+    auto one = [&](u32 v, u32 i, bool valid) {
+        const bool mine = valid && split_owner(v, om) == r;
+        const u32 li = ((v >> 1) & ~lo) | (v & lo);
+        if (AGG) {
+            const u32 active = __ballot_sync(0xffffffffu, mine);
+            if (mine) {
+                const u32 peers = __match_any_sync(active, li);
+                const int leader = __ffs(peers) - 1;
+                u32 pos = 0;
+                if (lane == leader) {
+                    pos = tab.template add<CHECK>(li, __popc(peers));
+                    if (SCATTER) pos += base + tab.chunk_base(li);
                 }
-            } else if (valid) {
-                const u32 pos = tab.template add<CHECK>(li, 1u);
-                if (out) out[base + tab.chunk_base(li) + pos] = u32(i);
+                if (SCATTER) out[__shfl_sync(peers, pos, leader) + __popc(peers & lanemask_lt())] = i;
             }
+        } else if (mine) {
+            const u32 pos = tab.template add<CHECK>(li, 1u);
+            if (SCATTER) out[base + tab.chunk_base(li) + pos] = i;
         }
+    };
+    const u32 mis = u32(reinterpret_cast<uintptr_t>(kb) >> 2) & 3u;
+    const u32 head = min(p, (4u - mis) & 3u);
+    if (threadIdx.x < 32) {  // head and tail: fewer than 4 keys each, one warp
+        const bool hv = u32(lane) < head;
+        one(hv ? kb[lane] : 0u, u32(lane), hv);
+    }
+    const u32 n4 = (p - head) >> 2;
+    const u32 tail0 = head + 4 * n4;
+    if (threadIdx.x < 32) {
+        const bool tv = tail0 + lane < p;
+        one(tv ? kb[tail0 + lane] : 0u, tail0 + lane, tv);
+    }
+    const uint4* k4 = reinterpret_cast<const uint4*>(kb + head);
+    for (u32 q0 = 0; q0 < n4; q0 += 2 * blockDim.x) {
+        const u32 qa = q0 + threadIdx.x, qb = qa + blockDim.x;
+        const bool va = qa < n4, vb = qb < n4;
+        const uint4 a = va ? __ldg(k4 + qa) : make_uint4(0, 0, 0, 0);
+        const uint4 b = vb ? __ldg(k4 + qb) : make_uint4(0, 0, 0, 0);
+        const u32 ia = head + 4 * qa, ib = head + 4 * qb;
+        one(a.x, ia, va);
+        one(a.y, ia + 1, va);
+        one(a.z, ia + 2, va);
+        one(a.w, ia + 3, va);
+        one(b.x, ib, vb);
+        one(b.y, ib + 1, vb);
+        one(b.z, ib + 2, vb);
+        one(b.w, ib + 3, vb);
     }
 }
 
@@ -411,6 +434,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
     u32* __restrict__ grouped, u64* __restrict__ tot, u64* __restrict__ work_run, Item* __restrict__ items,
     u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs, PairRec* __restrict__ pairs, u32 pair_cap,
     u32* __restrict__ gtab, u32* __restrict__ slots) {
+    static_assert(sizeof(K) == 4, "the split path runs with u32 keys (M <= 16)");
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) u32 smem[];
@@ -432,11 +456,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
     const u32 zb = ~c & mask;
     const bool local = zb != 0;
     const int t = local ? __ffs(zb) - 1 : M - 1;
+    const u32 om = local ? zb : (1u << t);
 
     if (threadIdx.x == 0) s_ovf = 0;
     tab.clear();
     __syncthreads();
-    split_pass<AGG, CHECK>(tab, kb, p, t, r, 0u, static_cast<u32*>(nullptr));
+    split_pass32<AGG, CHECK, false>(tab, reinterpret_cast<const u32*>(kb), u32(p), t, om, r, 0u,
+                                    static_cast<u32*>(nullptr));
     __syncthreads();
     const u32 n_mine = tab.scan(ws);
     if (threadIdx.x == 0) s_n = n_mine;
@@ -473,7 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
     }
     const u32 n0 = r == 0 ? n_mine : n_other;  // CTA 1's positions follow CTA 0's
     const u32 base = r == 0 ? 0u : n0;
-    split_pass<AGG, false>(tab, kb, p, t, r, base, out);
+    split_pass32<AGG, false, true>(tab, reinterpret_cast<const u32*>(kb), u32(p), t, om, r, base, out);
     __syncthreads();
     if (!local) cl.sync();  // #2: the partner's table is final before remote reads
     // group of key v: its owner's table (local or, for c = all ones, the partner's)
@@ -482,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
     rt.base = cl.map_shared_rank(tab.base, r ^ 1u);
     const u32 other_base = r == 0 ? n0 : 0u;
     auto group = [&](u32 v, u32& beg, u32& cnt) {
-        if (((v >> t) & 1u) == r) {
+        if (split_owner(v, om) == r) {
             tab.group(split_local(v, t), beg, cnt);
             beg += base;
         } else {
@@ -492,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
     };
     auto block_of = [&](u32 li) {
         HeadBlock hb;
-        const u32 v = split_key(li, r, t);
+        const u32 v = split_key(li, r, t, om);
         u32 bx, cx;
         group(v, bx, cx);
         if (cx == 0) return hb;

@@ -889,11 +889,16 @@ void run_batches(SearchCtx& c) {
         cudaEvent_t e2;
         if (split_path) {
             // ---- group + join fused: two CTAs per run, each half of the 16-bit bucket table ----
-            kern::split_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
-                                             ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
-                                             nitems, static_cast<u32>(item_cap), npairs_b,
-                                             ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap),
-                                             ds->gtab.as<u32>(), ds->slots.as<u32>(), st);
+            if constexpr (sizeof(K) == 4) {  // M <= 16 always runs with u32 keys
+                kern::split_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
+                                                 ds->tot.as<u64>(), ds->work_run.as<u64>(),
+                                                 ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
+                                                 npairs_b, ds->pairs.as<kern::PairRec>(),
+                                                 static_cast<u32>(c.pair_cap), ds->gtab.as<u32>(),
+                                                 ds->slots.as<u32>(), st);
+            } else {
+                throw internal_error("xyzb: split grouping needs 32-bit keys");
+            }
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_SORT] += 1;
             sv = vb[0];
