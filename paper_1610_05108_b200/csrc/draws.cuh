@@ -10,8 +10,9 @@
 // uniform_int_distribution::_S_nd, uniform_int_dist.h:252-278, taken with
 // unsigned __int128 for a 64-bit engine), so the device draws equal the
 // reference's host draws (tests: golden fixtures, draws vs oracle). One warp
-// per run; the sequential seed_seq recurrence runs on lane 0 out of shared
-// memory, all runs of a batch in parallel.
+// per run; the sequential seed_seq recurrence runs on lane 0 with its chain
+// in registers, packing and the first twist on the whole warp, all runs of a
+// batch in parallel.
 #pragma once
 
 #include "common.cuh"
@@ -52,42 +53,107 @@ struct Mt {
     }
 };
 
-// std::seed_seq{v0..v3}.generate(a, a + 624) followed by mt19937_64::seed(q).
-__device__ void seed_mt(const u32 v[4], u32* a /*624*/, u64* x /*312*/) {
-    const u32 n = 624, s = 4, t = 11, p = (n - t) / 2, q = p + t, m = n;  // m = max(s + 1, n)
-    for (u32 i = 0; i < n; ++i) a[i] = 0x8b8b8b8bu;
-    for (u32 k = 0; k < m; ++k) {
-        const u32 kn = k % n, kpn = (k + p) % n, kqn = (k + q) % n;
-        const u32 arg = a[kn] ^ a[kpn] ^ a[(k + n - 1) % n];
+// std::seed_seq{v0..v3}.generate(a, a + 624) (random.tcc:3256-3343), lane 0.
+// The recurrence is serial through a[k-1]; that value stays in a register
+// and the next iteration's a[k+1], a[k+1+p], a[k+1+q] are loaded before this
+// iteration's stores (they never alias them: p = 306, q = 317, n = 624), so
+// the dependent chain is a few ALU operations per step, not shared-memory
+// round trips.
+__device__ void seed_seq_624(const u32 v[4], u32* a /*624, filled with 0x8b8b8b8b*/) {
+    constexpr u32 n = 624, s = 4, p = 306, q = 317;  // t = 11, p = (n - t) / 2, q = p + t
+    u32 prev = a[n - 1], ak = a[0], akp = a[p], akq = a[q];
+    for (u32 k = 0; k < n; ++k) {
+        const u32 kpn = k + p < n ? k + p : k + p - n, kqn = k + q < n ? k + q : k + q - n;
+        const u32 arg = ak ^ akp ^ prev;
         const u32 r1 = 1664525u * (arg ^ (arg >> 27));
-        u32 r2 = r1 + kn;
+        u32 r2 = r1 + k;
         if (k == 0) r2 = r1 + s;
-        else if (k <= s) r2 = r1 + kn + v[k - 1];
-        a[kpn] += r1;
-        a[kqn] += r2;
-        a[kn] = r2;
+        else if (k <= s) r2 = r1 + k + v[k - 1];
+        const u32 k1 = k + 1 < n ? k + 1 : 0;
+        const u32 k1p = kpn + 1 < n ? kpn + 1 : 0, k1q = kqn + 1 < n ? kqn + 1 : 0;
+        const u32 nk = a[k1], nkp = a[k1p], nkq = a[k1q];
+        a[kpn] = akp + r1;
+        a[kqn] = akq + r2;
+        a[k] = r2;
+        prev = r2;
+        ak = nk;
+        akp = nkp;
+        akq = nkq;
     }
-    for (u32 k = m; k < m + n; ++k) {
-        const u32 kn = k % n, kpn = (k + p) % n, kqn = (k + q) % n;
-        const u32 arg = a[kn] + a[kpn] + a[(k - 1) % n];
+    ak = a[0];
+    akp = a[p];
+    akq = a[q];
+    for (u32 k = 0; k < n; ++k) {  // k here is (m + k) % n of the reference loop, m = n
+        const u32 kpn = k + p < n ? k + p : k + p - n, kqn = k + q < n ? k + q : k + q - n;
+        const u32 arg = ak + akp + prev;
         const u32 r3 = 1566083941u * (arg ^ (arg >> 27));
-        const u32 r4 = r3 - kn;
-        a[kpn] ^= r3;
-        a[kqn] ^= r4;
-        a[kn] = r4;
+        const u32 r4 = r3 - k;
+        const u32 k1 = k + 1 < n ? k + 1 : 0;
+        const u32 k1p = kpn + 1 < n ? kpn + 1 : 0, k1q = kqn + 1 < n ? kqn + 1 : 0;
+        const u32 nk = a[k1], nkp = a[k1p], nkq = a[k1q];
+        a[kpn] = akp ^ r3;
+        a[kqn] = akq ^ r4;
+        a[k] = r4;
+        prev = r4;
+        ak = nk;
+        akp = nkp;
+        akq = nkq;
     }
-    bool zero = true;
-    for (int i = 0; i < 312; ++i) {
+}
+
+// mt19937_64::seed(seed_seq&) (random.tcc:351-391) from the 624 words, one
+// warp: pack to 312 u64 words, all-zero check.
+__device__ void seed_mt_warp(const u32* a, u64* x) {
+    const int lane = threadIdx.x & 31;
+    bool nz = false;
+    for (int i = lane; i < 312; i += 32) {
         x[i] = u64(a[2 * i]) | (u64(a[2 * i + 1]) << 32);
-        if (zero) {
-            if (i == 0) {
-                if ((x[0] & 0xffffffff80000000ull) != 0) zero = false;
-            } else if (x[i] != 0) {
-                zero = false;
-            }
+        nz |= i == 0 ? (x[0] & 0xffffffff80000000ull) != 0 : x[i] != 0;
+    }
+    const bool any = __any_sync(0xffffffffu, nz);
+    __syncwarp();
+    if (!any && lane == 0) x[0] = 1ull << 63;
+    __syncwarp();
+}
+
+// _M_gen_rand (random.tcc:399-425) by one warp: the first 156 words depend
+// only on old words, the next 155 on old words and phase-1 results, the last
+// on phase-1 results.
+__device__ void twist_warp(u64* x) {
+    const u64 UM = 0xffffffff80000000ull, LM = 0x7fffffffull, A = 0xb5026f5aa96619e9ull;
+    const int lane = threadIdx.x & 31;
+    u64 v[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int k = lane + 32 * i;
+        if (k < 156) {
+            const u64 y = (x[k] & UM) | (x[k + 1] & LM);
+            v[i] = x[k + 156] ^ (y >> 1) ^ ((y & 1ull) ? A : 0ull);
         }
     }
-    if (zero) x[0] = 1ull << 63;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+        if (lane + 32 * i < 156) x[lane + 32 * i] = v[i];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int k = 156 + lane + 32 * i;
+        if (k < 311) {
+            const u64 y = (x[k] & UM) | (x[k + 1] & LM);
+            v[i] = x[k - 156] ^ (y >> 1) ^ ((y & 1ull) ? A : 0ull);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+        if (156 + lane + 32 * i < 311) x[156 + lane + 32 * i] = v[i];
+    __syncwarp();
+    if (lane == 0) {
+        const u64 y = (x[311] & UM) | (x[0] & LM);
+        x[311] = x[155] ^ (y >> 1) ^ ((y & 1ull) ? A : 0ull);
+    }
+    __syncwarp();
 }
 
 // Lemire nearly-divisionless draw in [0, range) with 128-bit products.
@@ -116,14 +182,25 @@ __global__ void __launch_bounds__(32) draw_runs(u32 R, const u64* __restrict__ s
     __shared__ u64 x[312];
     const u32 r = blockIdx.x;
     if (r >= R) return;
-    if (threadIdx.x == 0) {
+    u32 v[4];
+    {
         u64 s = seed;
         const u64 a = splitmix64(s);
         s ^= streams[r] * 0xd1342543de82ef95ull + 0x2545f4914f6cdd1dull;
         const u64 b = splitmix64(s);
-        const u32 v[4] = {u32(a), u32(a >> 32), u32(b), u32(b >> 32)};
-        seed_mt(v, arr, x);
-        Mt g{x, 312};
+        v[0] = u32(a);
+        v[1] = u32(a >> 32);
+        v[2] = u32(b);
+        v[3] = u32(b >> 32);
+    }
+    for (int i = threadIdx.x; i < 624; i += 32) arr[i] = 0x8b8b8b8bu;
+    __syncwarp();
+    if (threadIdx.x == 0) seed_seq_624(v, arr);
+    __syncwarp();
+    seed_mt_warp(arr, x);
+    twist_warp(x);  // the first draw regenerates the state: do it with the whole warp
+    if (threadIdx.x == 0) {
+        Mt g{x, 0};
         for (int t = 0; t < M; ++t) {
             u64 idx;
             if (cum) {
