@@ -221,7 +221,7 @@ struct xyzb_dataset {
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
     DevBuf tkeys, tvals, keep, kpos, kept, kept_order, fin, fin_order, tie, kbufA, kbufB, vbufA, vbufB, topidx, hcount;
     DevBuf pairs_dev, strengths_dev;
-    HostBuf h_rows, h_state, h_small, h_merge;
+    HostBuf h_rows, h_state, h_small, h_merge, h_status;
     StageClock clock;
     u32 hit_cap = 1u << 16;
 };
@@ -1397,25 +1397,74 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     ds->clock.span(XYZB_STAGE_OTHER, ev_start, ev_draw);
     u32 H = 0;
     const size_t spans0 = ds->clock.spans.size();
+    const u64 Rall = c.plan.sign_by_rid.size();
+    std::vector<u64> enumerated(Rall), verified(Rall);
+    // the single-CTA merge is queued right behind the search (hit count read on
+    // the device); one host round trip then returns every counter at once
+    const bool fused_merge = !q->stop_after_first_hit && !std::getenv("XYZB_MERGE_LARGE");
+    u32 fusedK = 0xffffffffu, fusedKK = 0;
+    u32 fcap = 0;
     for (int attempt = 0; attempt < 8; ++attempt) {
         ds->clock.spans.resize(spans0);
         if (c.M <= 31) run_batches<u32>(c); else run_batches<u64>(c);  // u32 holds M bits + the side bit
-        XYZB_CUDA(cudaMemcpyAsync(&H, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
-        std::vector<u32> nitems(c.nbatches);
-        XYZB_CUDA(cudaMemcpyAsync(nitems.data(), ds->nblocks.p, c.nbatches * 4, cudaMemcpyDeviceToHost, ds->stream));
+        const u64 nbt = c.nbatches;
+        u32* top_counts = nullptr;
+        if (fused_merge) {
+            fcap = std::min<u32>(ds->hit_cap, u32(merge::kSmallMerge));
+            static bool attr_set = false;
+            const size_t smem = merge::small_merge_smem(merge::kSmallMerge);
+            if (!attr_set) {
+                XYZB_CUDA(cudaFuncSetAttribute(merge::merge_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem)));
+                attr_set = true;
+            }
+            ds->fin.ensure(u64(fcap) * sizeof(xyzb_hit));
+            ds->fin_order.ensure(u64(fcap) * 8);
+            ds->topidx.ensure(u64(fcap) * 8 + 16);
+            top_counts = reinterpret_cast<u32*>(ds->topidx.as<u64>() + fcap);
+            cudaEvent_t m0 = ds->clock.mark();
+            merge::merge_small<<<1, merge::kSmallThreads, smem, ds->stream>>>(
+                ds->hits.as<kern::DevHit>(), 0, ds->sign_by_rid.as<int8_t>(), 0xffffffffu, c.plan.L, q->top_k,
+                ds->fin.as<xyzb_hit>(), ds->fin_order.as<u64>(), ds->topidx.as<u64>(), top_counts,
+                ds->hit_count.as<u32>(), fcap);
+            XYZB_LAUNCH_CHECK();
+            cudaEvent_t m1 = ds->clock.mark();
+            ds->clock.span(XYZB_STAGE_MERGE, m0, m1);
+        }
+        // status block (pinned): H, merge counts, items and pairs per batch, per-run counters
+        const size_t o_cnt = 8, o_items = 16, o_pairs = o_items + 4 * nbt, o_enum = round_up(o_pairs + 4 * nbt, 8),
+                     o_ver = o_enum + 8 * Rall, sbytes = o_ver + 8 * Rall;
+        ds->h_status.ensure(sbytes);
+        char* hs = ds->h_status.as<char>();
+        XYZB_CUDA(cudaMemcpyAsync(hs, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+        if (top_counts) XYZB_CUDA(cudaMemcpyAsync(hs + o_cnt, top_counts, 8, cudaMemcpyDeviceToHost, ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(hs + o_items, ds->nblocks.p, nbt * 4, cudaMemcpyDeviceToHost, ds->stream));
+        if (c.pair_cap)
+            XYZB_CUDA(cudaMemcpyAsync(hs + o_pairs, ds->npairs.p, nbt * 4, cudaMemcpyDeviceToHost, ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(hs + o_enum, ds->enumerated.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(hs + o_ver, ds->verified.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
-        const u64 need = nitems.empty() ? 0 : *std::max_element(nitems.begin(), nitems.end());
+        H = *reinterpret_cast<const u32*>(hs);
+        if (top_counts) {
+            fusedK = reinterpret_cast<const u32*>(hs + o_cnt)[0];
+            fusedKK = reinterpret_cast<const u32*>(hs + o_cnt)[1];
+        }
+        const u32* nitems = reinterpret_cast<const u32*>(hs + o_items);
+        const u64 need = nbt ? *std::max_element(nitems, nitems + nbt) : 0;
         u64 pneed = 0;
         if (c.pair_cap) {
-            std::vector<u32> np(c.nbatches);
-            XYZB_CUDA(cudaMemcpy(np.data(), ds->npairs.p, c.nbatches * 4, cudaMemcpyDeviceToHost));
-            pneed = *std::max_element(np.begin(), np.end());
+            const u32* np = reinterpret_cast<const u32*>(hs + o_pairs);
+            pneed = *std::max_element(np, np + nbt);
             if (pneed > c.pair_cap) {
                 if (c.pair_cap == 0xffffffffull) throw internal_error("xyzb: candidate pairs exceed 2^32 in one batch");
                 c.pair_scale *= std::max<u64>(2, ceil_div(pneed, c.pair_cap));
             }
         }
-        if (H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) break;
+        if (H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
+            std::memcpy(enumerated.data(), hs + o_enum, Rall * 8);
+            std::memcpy(verified.data(), hs + o_ver, Rall * 8);
+            break;
+        }
         // a buffer overflowed (the counters kept counting): grow and recompute
         if (H > ds->hit_cap) ds->hit_cap = static_cast<u32>(std::min<u64>(0xffffffffull, u64(H) * 2));
         if (need > c.item_cap) {
@@ -1428,26 +1477,44 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         c.verify_spans.clear();
         if (attempt == 7) throw internal_error("xyzb: hit buffer did not converge");
     }
-    // per-run counters (device -> host) and stop_after_first_hit truncation
-    const u64 Rall = c.plan.sign_by_rid.size();
-    std::vector<u64> enumerated(Rall), verified(Rall);
-    XYZB_CUDA(cudaMemcpyAsync(enumerated.data(), ds->enumerated.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
-    XYZB_CUDA(cudaMemcpyAsync(verified.data(), ds->verified.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
     u32 rmax = 0xffffffffu;
-    if (q->stop_after_first_hit && H > 0) {
-        ds->rmin.ensure(8);
-        XYZB_CUDA(cudaMemsetAsync(ds->rmin.p, 0xff, 4, ds->stream));
-        merge::min_rid<<<grid_for(H, 256), 256, 0, ds->stream>>>(ds->hits.as<kern::DevHit>(), H, ds->rmin.as<u32>());
-        XYZB_LAUNCH_CHECK();
-        XYZB_CUDA(cudaMemcpyAsync(&rmax, ds->rmin.p, 4, cudaMemcpyDeviceToHost, ds->stream));
-    }
-    cudaEvent_t ev_m0 = ds->clock.mark();
-    XYZB_CUDA(cudaStreamSynchronize(ds->stream));
     std::vector<xyzb_hit> hits;
     std::vector<u64> order, topk;
-    merge_hits(c, H, rmax, hits, order, topk);
-    cudaEvent_t ev_m1 = ds->clock.mark();
-    ds->clock.span(XYZB_STAGE_MERGE, ev_m0, ev_m1);
+    if (fused_merge && H <= fcap && fusedK != 0xffffffffu) {
+        c.launches[XYZB_STAGE_MERGE] += 1;
+        hits.resize(fusedK);
+        order.resize(fusedK);
+        topk.resize(fusedKK);
+        if (fusedK) {
+            const size_t hb = u64(fusedK) * sizeof(xyzb_hit), ob = u64(fusedK) * 8, tb = u64(fusedKK) * 8;
+            ds->h_merge.ensure(hb + ob + tb + 8);
+            char* hp = ds->h_merge.as<char>();
+            XYZB_CUDA(cudaMemcpyAsync(hp, ds->fin.p, hb, cudaMemcpyDeviceToHost, ds->stream));
+            XYZB_CUDA(cudaMemcpyAsync(hp + hb, ds->fin_order.p, ob, cudaMemcpyDeviceToHost, ds->stream));
+            if (tb) XYZB_CUDA(cudaMemcpyAsync(hp + hb + ob, ds->topidx.p, tb, cudaMemcpyDeviceToHost, ds->stream));
+            XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+            std::memcpy(hits.data(), hp, hb);
+            std::memcpy(order.data(), hp + hb, ob);
+            if (tb) std::memcpy(topk.data(), hp + hb + ob, tb);
+        }
+    } else {
+        if (q->stop_after_first_hit && H > 0) {
+            ds->rmin.ensure(8);
+            XYZB_CUDA(cudaMemsetAsync(ds->rmin.p, 0xff, 4, ds->stream));
+            merge::min_rid<<<grid_for(H, 256), 256, 0, ds->stream>>>(ds->hits.as<kern::DevHit>(), H,
+                                                                     ds->rmin.as<u32>());
+            XYZB_LAUNCH_CHECK();
+            XYZB_CUDA(cudaMemcpyAsync(&rmax, ds->rmin.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+        }
+        // drop the fused merge's span (it only flagged the overflow)
+        for (auto it = ds->clock.spans.begin(); it != ds->clock.spans.end();)
+            it = it->first == XYZB_STAGE_MERGE ? ds->clock.spans.erase(it) : it + 1;
+        cudaEvent_t ev_m0 = ds->clock.mark();
+        XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        merge_hits(c, H, rmax, hits, order, topk);
+        cudaEvent_t ev_m1 = ds->clock.mark();
+        ds->clock.span(XYZB_STAGE_MERGE, ev_m0, ev_m1);
+    }
     // counters over executed runs (in pass/rep order)
     u64 reps = 0, enumc = 0, aborted = 0, ver = 0;
     for (u32 r : c.plan.rid) {

@@ -205,13 +205,27 @@ __device__ __forceinline__ u32 block_excl_scan(u32 v, u32* warp_tot, u32* total)
 constexpr size_t small_merge_smem(int N) { return size_t(N) * 36; }
 
 // out_counts[0] = kept hits K, out_counts[1] = top-K length. H <= kSmallMerge.
+// With Hdev the hit count is read on the device (the merge is queued right
+// behind the search, no host round trip); above Hcap the kernel only flags
+// out_counts[0] = ~0 and the host takes the multi-kernel merge.
 __global__ void __launch_bounds__(kSmallThreads) merge_small(const DevHit* __restrict__ h, u32 H,
                                                              const int8_t* __restrict__ sign_by_rid, u32 rmax, u64 L,
                                                              u64 top_k, xyzb_hit* __restrict__ out,
                                                              u64* __restrict__ order_out, u64* __restrict__ top_out,
-                                                             u32* __restrict__ out_counts) {
+                                                             u32* __restrict__ out_counts,
+                                                             const u32* __restrict__ Hdev = nullptr, u32 Hcap = 0) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ u32 warp_tot[33];
+    if (Hdev) {
+        H = *Hdev;
+        if (H > Hcap) {
+            if (threadIdx.x == 0) {
+                out_counts[0] = 0xffffffffu;
+                out_counts[1] = 0;
+            }
+            return;
+        }
+    }
     int N = 1;
     while (N < int(H)) N <<= 1;
     u64* s_tag = reinterpret_cast<u64*>(smem);
