@@ -143,7 +143,9 @@ typedef struct {
     /* engine telemetry */
     uint64_t runs_executed;      /* runs computed on the device (before stop truncation) */
     uint64_t verified_pairs;     /* canonical off-diagonal pairs verified, non-aborted runs */
-    double device_ms;            /* CUDA-event time of the whole search on the stream */
+    double device_ms;            /* CUDA-event time on the stream from the search start to the merged
+                                    hits in device memory (+ the complexity estimate if it ran); the
+                                    copy of the results to the host is not included */
     double stage_ms[XYZB_NUM_STAGES];
     uint64_t stage_bytes[XYZB_NUM_STAGES]; /* algorithmic bytes per stage */
     uint64_t stage_launches[XYZB_NUM_STAGES];
