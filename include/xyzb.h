@@ -23,6 +23,9 @@
  *                                continuous-XY strength (search.cpp:477-493)
  *   xyzb_merge_results           the slot-ordered merge + dedup of run_pass
  *                                (search.cpp:96-108) applied across GPUs
+ *   xyzb_brute_force             oracle::brute_force_search, binary overload
+ *                                (proj/core/include/xyz/oracle.hpp:36-37,
+ *                                proj/core/src/oracle.cpp:24-59, 84-91)
  *
  * Conventions: plain pointers and sizes, caller owns inputs (borrowed for the
  * call), the library owns device buffers (dataset handle) and result buffers
@@ -203,6 +206,27 @@ int xyzb_equal_pairs(const uint64_t* x_keys, const uint64_t* z_keys, uint64_t p,
 int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params,
                         const uint32_t* pairs_jk, uint64_t n_pairs, double* strengths,
                         char* err, size_t errlen);
+
+/* One scored pair of the exhaustive search (oracle::ScoredPair, oracle.hpp:15-19). */
+typedef struct {
+    uint32_t j; /* j < k */
+    uint32_t k;
+    double strength;
+} xyzb_scored_pair;
+
+/* oracle::brute_force_search(PackedMatrix, span<int8>, BruteForceOptions)
+ * on the device: the exact strength agree/n of every pair j < k.
+ * has_gamma/gamma: keep pairs with strength >= gamma; has_top_k/top_k: keep
+ * the top_k strongest (of those >= gamma when both are set; ties broken by
+ * (j, k)); histogram_bins > 0: counts of strengths in [0, 1] bins
+ * (bin = floor(s * bins), clamped); force: run above the reference's
+ * p <= 20000 guard (else XYZB_E_GUARD with its message). Outputs:
+ * *pairs (ordered by (j, k), freed by xyzb_free), *n_pairs, *pairs_scanned
+ * (= p(p-1)/2), *histogram (histogram_bins entries or NULL, freed by
+ * xyzb_free). Binary datasets only. */
+int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t has_gamma, double gamma, int32_t has_top_k,
+                     uint64_t top_k, uint64_t histogram_bins, int32_t force, xyzb_scored_pair** pairs,
+                     uint64_t* n_pairs, uint64_t* pairs_scanned, uint64_t** histogram, char* err, size_t errlen);
 
 void xyzb_free(void* p);
 

@@ -92,6 +92,14 @@ class Result(C.Structure):
     ]
 
 
+class ScoredPair(C.Structure):
+    _fields_ = [
+        ("j", C.c_uint32),
+        ("k", C.c_uint32),
+        ("strength", C.c_double),
+    ]
+
+
 ERRBUF = 1024
 
 
@@ -121,6 +129,10 @@ SIGNATURES = {
                                    C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
     "xyzb_pair_strengths": (C.c_int, [_P, C.POINTER(Response), C.POINTER(Params), C.POINTER(C.c_uint32),
                                       C.c_uint64, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
+    "xyzb_brute_force": (C.c_int, [_P, C.POINTER(C.c_int8), C.c_int32, C.c_double, C.c_int32, C.c_uint64,
+                                   C.c_uint64, C.c_int32, C.POINTER(C.POINTER(ScoredPair)), C.POINTER(C.c_uint64),
+                                   C.POINTER(C.c_uint64), C.POINTER(C.POINTER(C.c_uint64)), C.c_char_p,
+                                   C.c_size_t]),
     "xyzb_free": (None, [_P]),
 }
 

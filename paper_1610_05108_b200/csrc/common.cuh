@@ -21,6 +21,9 @@ struct data_error : std::runtime_error {
 struct internal_error : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct guard_error : std::runtime_error {  // xyz::guard_error (errors.hpp:15-18)
+    using std::runtime_error::runtime_error;
+};
 
 #define XYZB_CUDA(call)                                                                         \
     do {                                                                                        \

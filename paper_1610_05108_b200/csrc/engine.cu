@@ -30,6 +30,8 @@
 #include <vector>
 
 #include "../../include/xyzb.h"
+#include "brute.cuh"
+#include "brute_tc.cuh"
 #include "cluster_group.cuh"
 #include "cta_group.cuh"
 #include "common.cuh"
@@ -246,6 +248,9 @@ int guarded(char* err, size_t errlen, F&& f) {
     } catch (const cuda_error& e) {
         set_err(err, errlen, e.what());
         return XYZB_E_CUDA;
+    } catch (const guard_error& e) {
+        set_err(err, errlen, e.what());
+        return XYZB_E_GUARD;
     } catch (const std::exception& e) {
         set_err(err, errlen, e.what());
         return XYZB_E_INTERNAL;
@@ -1735,6 +1740,201 @@ extern "C" int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, 
         c.gamma = params->gamma;
         upload_response(c, resp);
         device_pair_strengths(c, pairs_jk, n_pairs, strengths);
+    });
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        XYZB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) throw cuda_error("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    return fn;
+}
+
+// 2-D K-major int8 operand [rows][Kp], boxes of 128 bytes x box_rows, 128-byte swizzle.
+CUtensorMap operand_map(void* base, u64 rows, u64 Kp, u32 box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {Kp, rows};
+    const cuuint64_t strides[1] = {Kp};
+    const cuuint32_t box[2] = {128u, box_rows};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t has_gamma, double gamma,
+                                int32_t has_top_k, uint64_t top_k, uint64_t histogram_bins, int32_t force,
+                                xyzb_scored_pair** pairs, uint64_t* n_pairs, uint64_t* pairs_scanned,
+                                uint64_t** histogram, char* err, size_t errlen) {
+    if (pairs) *pairs = nullptr;
+    if (n_pairs) *n_pairs = 0;
+    if (pairs_scanned) *pairs_scanned = 0;
+    if (histogram) *histogram = nullptr;
+    return guarded(err, errlen, [&] {
+        if (!ds || !y_sign || !pairs || !n_pairs || !pairs_scanned || !histogram)
+            throw data_error("brute_force_search: null argument");
+        if (!ds->binary) throw data_error("brute_force_search: the GPU brute force takes binary datasets");
+        const u64 n = ds->n, p = ds->p, W = ds->W, Wp = ds->Wp;
+        // check_guard (oracle.cpp:16-22)
+        if (p > 20000 && !force)
+            throw guard_error("brute_force_search: p = " + std::to_string(p) +
+                              " exceeds the 20000 guard; pass force to run anyway");
+        if (p > 0xffffffffull || n > 0xffffffffull) throw data_error("brute_force_search: matrix too large");
+        DeviceGuard dg(ds->device);
+        const cudaStream_t st = ds->stream;
+        // Y bits (y > 0) and the rows that can agree (y != 0)
+        std::vector<u64> hy(2 * Wp, 0ull);
+        for (u64 i = 0; i < n; ++i) {
+            if (y_sign[i] > 0) hy[i >> 6] |= 1ull << (i & 63);
+            if (y_sign[i] == 1 || y_sign[i] == -1) hy[Wp + (i >> 6)] |= 1ull << (i & 63);
+        }
+        DevBuf yb, zc, hist;
+        yb.ensure(2 * Wp * 8);
+        XYZB_CUDA(cudaMemcpyAsync(yb.p, hy.data(), 2 * Wp * 8, cudaMemcpyHostToDevice, st));
+        zc.ensure(p * Wp * 8);
+        brute::make_z<<<grid_for(p * Wp, 256), 256, 0, st>>>(ds->Xc.as<u64>(), Wp, W, p, yb.as<u64>(), zc.as<u64>());
+        XYZB_LAUNCH_CHECK();
+        hist.ensure((n + 1) * 8);
+        XYZB_CUDA(cudaMemsetAsync(hist.p, 0, (n + 1) * 8, st));
+        const size_t hs = n <= brute::kSmemHistMax ? size_t(n + 1) * 4 : 0;
+        static bool attr = false;
+        if (!attr) {
+            XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int((brute::kSmemHistMax + 1) * 4)));
+            attr = true;
+        }
+        const u64* nzp = yb.as<u64>() + Wp;
+        // tensor cores (tcgen05 kind::i8 Gram product) by default; XYZB_BRUTE=cuda: CUDA-core popcounts
+        const bool tc = !(std::getenv("XYZB_BRUTE") && std::string(std::getenv("XYZB_BRUTE")) == "cuda");
+        u32 nz = 0;
+        for (u64 i = 0; i < n; ++i) nz += (y_sign[i] == 1 || y_sign[i] == -1) ? 1u : 0u;
+        const u64 Kp = round_up(n, 128);
+        DevBuf opA, opB;
+        CUtensorMap tmA{}, tmB{};
+        if (tc) {
+            opA.ensure(p * Kp);
+            opB.ensure(p * Kp);
+            brute::make_pm1<<<grid_for(p * Kp / 8, 256), 256, 0, st>>>(ds->Xc.as<u64>(), Wp, p, n, Kp, yb.as<u64>(),
+                                                                     nzp, opA.as<int8_t>(), opB.as<int8_t>());
+            XYZB_LAUNCH_CHECK();
+            tmA = operand_map(opA.p, p, Kp, brute::kTcM);
+            tmB = operand_map(opB.p, p, Kp, brute::kTcN);
+            static bool tc_attr = false;
+            if (!tc_attr) {
+                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(brute::kTcSmem)));
+                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(brute::kTcSmem)));
+                tc_attr = true;
+            }
+        }
+        const u64 ntc = u64((p + brute::kTcM - 1) / brute::kTcM) * ((p + brute::kTcN - 1) / brute::kTcN);
+        const u32 tc_grid = static_cast<u32>(std::min<u64>(ntc, kSMs));
+        if (tc) {
+            brute::all_pairs_tc<false><<<tc_grid, brute::kTcThreads, brute::kTcSmem, st>>>(
+                tmA, tmB, u32(p), u32(n), nz, u32(Kp), hist.as<unsigned long long>(), 0u, nullptr, nullptr, 0u);
+        } else {
+            brute::all_pairs<false><<<brute::all_pairs_grid(), brute::kThreads, hs, st>>>(
+                ds->Xc.as<u64>(), zc.as<u64>(), nzp, Wp, W, u32(p), u32(n), hist.as<unsigned long long>(), 0u,
+                nullptr, nullptr, 0u);
+        }
+        XYZB_LAUNCH_CHECK();
+        std::vector<u64> cnt(n + 1);
+        XYZB_CUDA(cudaMemcpyAsync(cnt.data(), hist.p, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        *pairs_scanned = p * (p - 1) / 2;
+        const auto strength = [&](u64 a) { return double(a) / double(n); };
+        if (histogram_bins > 0) {
+            // scan_all_pairs' binning (oracle.cpp:36-41) applied to each exact agree count
+            u64* h = static_cast<u64*>(std::calloc(histogram_bins, 8));
+            if (!h) throw internal_error("brute_force_search: out of host memory");
+            for (u64 a = 0; a <= n; ++a) {
+                if (!cnt[a]) continue;
+                auto bin = static_cast<size_t>(strength(a) * static_cast<double>(histogram_bins));
+                if (bin >= histogram_bins) bin = histogram_bins - 1;
+                h[bin] += cnt[a];
+            }
+            *histogram = h;
+        }
+        if (!has_gamma && !has_top_k) return;
+        // smallest agree count kept by gamma, then the top-K cutoff among those
+        u64 a_lo = 0;
+        if (has_gamma) {
+            a_lo = n + 1;
+            for (u64 a = 0; a <= n; ++a)
+                if (strength(a) >= gamma) {
+                    a_lo = a;
+                    break;
+                }
+        }
+        u64 kept = 0;
+        for (u64 a = a_lo; a <= n; ++a) kept += cnt[a];
+        u64 cutoff = a_lo;
+        u64 want = kept;
+        if (has_top_k) {
+            want = std::min<u64>(top_k, kept);
+            if (want == 0) return;
+            u64 acc = 0;
+            for (u64 a = n + 1; a-- > a_lo;) {
+                acc += cnt[a];
+                if (acc >= want) {
+                    cutoff = a;
+                    break;
+                }
+            }
+        }
+        if (want == 0 || cutoff > n) return;
+        u64 emit = 0;
+        for (u64 a = cutoff; a <= n; ++a) emit += cnt[a];
+        if (emit > 0xffffffffull) throw internal_error("brute_force_search: more than 2^32 pairs above the cut");
+        DevBuf outb, nout;
+        outb.ensure(emit * sizeof(brute::PairOut));
+        nout.ensure(4);
+        XYZB_CUDA(cudaMemsetAsync(nout.p, 0, 4, st));
+        if (tc) {
+            brute::all_pairs_tc<true><<<tc_grid, brute::kTcThreads, brute::kTcSmem, st>>>(
+                tmA, tmB, u32(p), u32(n), nz, u32(Kp), nullptr, u32(cutoff), outb.as<brute::PairOut>(),
+                nout.as<u32>(), u32(emit));
+        } else {
+            brute::all_pairs<true><<<brute::all_pairs_grid(), brute::kThreads, 0, st>>>(
+                ds->Xc.as<u64>(), zc.as<u64>(), nzp, Wp, W, u32(p), u32(n), nullptr, u32(cutoff),
+                outb.as<brute::PairOut>(), nout.as<u32>(), u32(emit));
+        }
+        XYZB_LAUNCH_CHECK();
+        std::vector<brute::PairOut> got(emit);
+        XYZB_CUDA(cudaMemcpyAsync(got.data(), outb.p, emit * sizeof(brute::PairOut), cudaMemcpyDeviceToHost, st));
+        u32 nget = 0;
+        XYZB_CUDA(cudaMemcpyAsync(&nget, nout.p, 4, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        if (nget != emit) throw internal_error("brute_force_search: emitted pair count differs from the histogram");
+        const auto by_jk = [](const brute::PairOut& x, const brute::PairOut& y) {
+            return x.j != y.j ? x.j < y.j : x.k < y.k;
+        };
+        if (has_top_k) {
+            // oracle.cpp:45-56: strength desc, (j, k) asc; the K best, then (j, k) order
+            std::sort(got.begin(), got.end(), [&](const brute::PairOut& x, const brute::PairOut& y) {
+                if (x.agree != y.agree) return x.agree > y.agree;
+                return by_jk(x, y);
+            });
+            got.resize(want);
+        }
+        std::sort(got.begin(), got.end(), by_jk);
+        auto* outp = static_cast<xyzb_scored_pair*>(std::malloc(std::max<size_t>(1, got.size()) * sizeof(xyzb_scored_pair)));
+        if (!outp) throw internal_error("brute_force_search: out of host memory");
+        for (size_t t = 0; t < got.size(); ++t) outp[t] = xyzb_scored_pair{got[t].j, got[t].k, strength(got[t].agree)};
+        *pairs = outp;
+        *n_pairs = got.size();
     });
 }
 

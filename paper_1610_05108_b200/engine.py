@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import weakref
-from typing import Optional, Sequence
+from typing import NamedTuple, Optional, Sequence
 
 import numpy as np
 
@@ -190,3 +190,45 @@ def equal_pairs(x_keys, z_keys, device: int = 0):
 
 def device_count() -> int:
     return int(load().xyzb_device_count())
+
+
+class ScoredPair(NamedTuple):
+    """oracle::ScoredPair (oracle.hpp:15-19)."""
+    j: int
+    k: int
+    strength: float
+
+
+class OracleResult(NamedTuple):
+    """oracle::OracleResult (oracle.hpp:21-25)."""
+    pairs: list
+    pairs_scanned: int
+    histogram: list
+
+
+def brute_force_search(x, y, gamma: Optional[float] = None, top_k: Optional[int] = None, histogram_bins: int = 0,
+                       force: bool = False, device: int = 0) -> OracleResult:
+    """oracle::brute_force_search, binary overload (oracle.hpp:36-37,
+    oracle.cpp:84-91), on the GPU: exact strengths of all p(p-1)/2 pairs.
+    `x` is a PackedMatrix or a binary Dataset; y the +-1 response."""
+    ds = x if isinstance(x, Dataset) else dataset_for(x, device)
+    yy = np.ascontiguousarray(y, np.int8)
+    if yy.shape[0] != ds.n_rows:
+        raise DataError("brute_force_search: response length mismatch")
+    lib = ds._lib
+    pairs = C.POINTER(_abi.ScoredPair)()
+    hist = C.POINTER(C.c_uint64)()
+    npairs, scanned = C.c_uint64(), C.c_uint64()
+    err = _abi.errbuf()
+    raise_for(lib.xyzb_brute_force(ds.handle, yy.ctypes.data_as(C.POINTER(C.c_int8)), int(gamma is not None),
+                                   float(gamma) if gamma is not None else 0.0, int(top_k is not None),
+                                   int(top_k) if top_k is not None else 0, int(histogram_bins), int(bool(force)),
+                                   C.byref(pairs), C.byref(npairs), C.byref(scanned), C.byref(hist), err,
+                                   _abi.ERRBUF), err)
+    try:
+        out = [ScoredPair(pairs[i].j, pairs[i].k, pairs[i].strength) for i in range(npairs.value)]
+        h = [int(hist[i]) for i in range(histogram_bins)] if histogram_bins and hist else []
+    finally:
+        lib.xyzb_free(pairs)
+        lib.xyzb_free(hist)
+    return OracleResult(out, scanned.value, h)

@@ -65,6 +65,9 @@ _REF_SIGS = {
     "ref_write_dataset": (C.c_int, [C.c_char_p, C.c_int32, _U64P, _F64P, C.c_uint64, C.c_uint64, C.c_char_p,
                                     C.c_size_t]),
     "ref_read_dataset": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _U64P, _U64P, C.c_char_p, C.c_size_t]),
+    "ref_brute_force": (C.c_int, [_U64P, C.c_uint64, C.c_uint64, C.POINTER(C.c_int8), C.c_int32, C.c_double,
+                                  C.c_int32, C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(_U32P), C.POINTER(_F64P),
+                                  _U64P, _U64P, C.POINTER(_U64P), C.c_char_p, C.c_size_t]),
 }
 
 
@@ -369,3 +372,25 @@ def ref_read_dataset(path):
     err = _abi.errbuf()
     _check(lib.ref_read_dataset(str(path).encode(), C.byref(kind), C.byref(n), C.byref(p), err, _abi.ERRBUF), err)
     return kind.value, n.value, p.value
+
+
+def ref_brute_force(x: PackedMatrix, y, gamma=None, top_k=None, histogram_bins=0, force=False):
+    """oracle::brute_force_search of the reference: ([(j, k, s)], pairs_scanned, [hist])."""
+    lib = ref_lib()
+    yy = np.ascontiguousarray(y, np.int8)
+    jk, s, h = _U32P(), _F64P(), _U64P()
+    n, scanned = C.c_uint64(), C.c_uint64()
+    err = _abi.errbuf()
+    code = lib.ref_brute_force(_u64p(x.words), x.n_rows, x.n_cols, yy.ctypes.data_as(C.POINTER(C.c_int8)),
+                               int(gamma is not None), float(gamma or 0.0), int(top_k is not None), int(top_k or 0),
+                               int(histogram_bins), int(force), C.byref(jk), C.byref(s), C.byref(n),
+                               C.byref(scanned), C.byref(h), err, _abi.ERRBUF)
+    try:
+        _check(code, err)
+        pairs = [(jk[2 * i], jk[2 * i + 1], s[i]) for i in range(n.value)]
+        hist = [h[i] for i in range(histogram_bins)]
+    finally:
+        for ptr in (jk, s, h):
+            if ptr:
+                lib.ref_free(ptr)
+    return pairs, scanned.value, hist
