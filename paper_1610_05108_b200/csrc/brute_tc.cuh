@@ -251,5 +251,153 @@ __global__ void __launch_bounds__(kTcThreads, 1) all_pairs_tc(const __grid_const
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(u32(kTcN)));
 }
 
+// Warp-specialised persistent kernel: warp 0 = TMA producer, warp 1 = MMA
+// issuer, warps 2-5 = epilogue. The accumulator is double-buffered in TMEM
+// (2 x 256 columns), so the epilogue of tile i overlaps the MMAs of tile
+// i + 1; the stage ring is shared by consecutive tiles.
+constexpr int kTcWarps = 6;
+constexpr int kTcEpiWarps = 4;
+constexpr u32 kTcHistMax = 8192;  // agree bins in shared memory (n <= this), else global atomics
+constexpr int kTcStages4 = 4;
+constexpr u32 kTcSmem2 = kTcStages4 * (kTcStageA + kTcStageB) + 1024 + (kTcHistMax + 1) * 4;
+
+template <bool EMIT>
+__global__ void __launch_bounds__(kTcWarps * 32, 1) all_pairs_tc2(const __grid_constant__ CUtensorMap tmA,
+                                                                  const __grid_constant__ CUtensorMap tmB, u32 p,
+                                                                  u32 n, u32 nz, u32 Kp,
+                                                                  unsigned long long* __restrict__ hist, u32 cutoff,
+                                                                  PairOut* __restrict__ out, u32* __restrict__ nout,
+                                                                  u32 out_cap) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    __shared__ __align__(8) u64 full_bar[kTcStages4], empty_bar[kTcStages4], tfull_bar[2], tempty_bar[2];
+    __shared__ u32 tmem_holder;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u32 base = smem_addr(dsm);
+    const u32 sbase = (base + 1023u) & ~1023u;
+    auto sA = [&](u32 s) { return sbase + s * (kTcStageA + kTcStageB); };
+    auto sB = [&](u32 s) { return sA(s) + kTcStageA; };
+    u32* shist = reinterpret_cast<u32*>(dsm + (sbase - base) + kTcStages4 * (kTcStageA + kTcStageB));
+    const bool smem_hist = !EMIT && n <= kTcHistMax;
+    if (smem_hist)
+        for (u32 i = threadIdx.x; i <= n; i += kTcWarps * 32) shist[i] = 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages4; ++s) {
+            mbar_init(smem_addr(&full_bar[s]), 1);
+            mbar_init(smem_addr(&empty_bar[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_addr(&tfull_bar[b]), 1);
+            mbar_init(smem_addr(&tempty_bar[b]), kTcEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmB)) : "memory");
+    }
+    if (warp == 1) {  // TMEM: two accumulators of 256 s32 columns (whole warp)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_holder)),
+                     "r"(u32(2 * kTcN)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const u32 tmem = tmem_holder;
+    const u32 nj = (p + kTcM - 1) / kTcM, nk = (p + kTcN - 1) / kTcN;
+    const u32 nkb = Kp / kTcKB;
+    const u64 ntiles = u64(nj) * nk;
+    auto skip = [&](u64 t) {
+        const u32 tj = u32(t / nk), tk = u32(t % nk);
+        return tk * kTcN + kTcN <= tj * kTcM + 1;  // no pair with k > j
+    };
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            u32 g = 0;
+            for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                if (skip(t)) continue;
+                const int j0 = int(t / nk) * kTcM, k0 = int(t % nk) * kTcN;
+                for (u32 kb = 0; kb < nkb; ++kb, ++g) {
+                    const u32 s = g % kTcStages4;
+                    if (g >= u32(kTcStages4)) mbar_wait(smem_addr(&empty_bar[s]), ((g / kTcStages4) - 1) & 1);
+                    mbar_expect_tx(smem_addr(&full_bar[s]), kTcStageA + kTcStageB);
+                    tma_load_2d(sA(s), &tmA, int(kb * kTcKB), j0, smem_addr(&full_bar[s]));
+                    tma_load_2d(sB(s), &tmB, int(kb * kTcKB), k0, smem_addr(&full_bar[s]));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            u32 g = 0, lt = 0;
+            for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                if (skip(t)) continue;
+                const u32 b = lt & 1, use = lt >> 1;
+                if (use >= 1) mbar_wait(smem_addr(&tempty_bar[b]), (use - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const u32 acc = tmem + b * kTcN;
+                for (u32 kb = 0; kb < nkb; ++kb, ++g) {
+                    const u32 s = g % kTcStages4;
+                    mbar_wait(smem_addr(&full_bar[s]), (g / kTcStages4) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int kk = 0; kk < kTcKB / 32; ++kk)
+                        mma_i8(acc, sw128_desc(sA(s) + kk * 32), sw128_desc(sB(s) + kk * 32), (kb | kk) != 0);
+                    mma_commit(smem_addr(&empty_bar[s]));
+                }
+                mma_commit(smem_addr(&tfull_bar[b]));
+                ++lt;
+            }
+        }
+    } else {  // ===== epilogue: warps 2-5, TMEM lane quarter = warp % 4 =====
+        const u32 quarter = u32(warp & 3);
+        u32 lt = 0;
+        for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            if (skip(t)) continue;
+            const u32 b = lt & 1, use = lt >> 1;
+            const u32 j0 = u32(t / nk) * kTcM, k0 = u32(t % nk) * kTcN;
+            mbar_wait(smem_addr(&tfull_bar[b]), use & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const u32 j = j0 + quarter * 32 + u32(lane);
+#pragma unroll 1
+            for (int c = 0; c < kTcN / 32; ++c) {
+                u32 v[32];
+                tmem_ld32(tmem + ((quarter * 32) << 16) + b * kTcN + u32(c * 32), v);
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const u32 k = k0 + u32(c * 32 + q);
+                    const u32 agree = (nz - v[q]) >> 1;  // G = nz - 2 agree
+                    const bool valid = j < k && k < p;
+                    if (EMIT) {
+                        const bool keep = valid && agree >= cutoff;
+                        const u32 ball = __ballot_sync(0xffffffffu, keep);
+                        if (ball) {
+                            const int leader = __ffs(ball) - 1;
+                            u32 b0 = 0;
+                            if (lane == leader) b0 = atomicAdd(nout, __popc(ball));
+                            b0 = __shfl_sync(0xffffffffu, b0, leader);
+                            if (keep) {
+                                const u32 slot = b0 + __popc(ball & lanemask_lt());
+                                if (slot < out_cap) out[slot] = PairOut{j, k, agree, 0u};
+                            }
+                        }
+                    } else if (valid) {
+                        if (smem_hist) atomicAdd(&shist[agree], 1u);
+                        else atomicAdd(hist + agree, 1ull);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&tempty_bar[b])) : "memory");
+            ++lt;
+        }
+    }
+    __syncthreads();
+    if (smem_hist)
+        for (u32 i = threadIdx.x; i <= n; i += kTcWarps * 32)
+            if (shist[i]) atomicAdd(hist + i, static_cast<unsigned long long>(shist[i]));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(u32(2 * kTcN)));
+}
+
 }  // namespace brute
 }  // namespace xyzb

@@ -1816,7 +1816,9 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
         }
         const u64* nzp = yb.as<u64>() + Wp;
         // tensor cores (tcgen05 kind::i8 Gram product) by default; XYZB_BRUTE=cuda: CUDA-core popcounts
-        const bool tc = !(std::getenv("XYZB_BRUTE") && std::string(std::getenv("XYZB_BRUTE")) == "cuda");
+        const char* bsel = std::getenv("XYZB_BRUTE");
+        const bool tc = !(bsel && std::string(bsel) == "cuda");
+        const bool tc1 = bsel && std::string(bsel) == "tc1";  // the single-issuer tensor-core kernel
         u32 nz = 0;
         for (u64 i = 0; i < n; ++i) nz += (y_sign[i] == 1 || y_sign[i] == -1) ? 1u : 0u;
         const u64 Kp = round_up(n, 128);
@@ -1836,12 +1838,19 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
                                                int(brute::kTcSmem)));
                 XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                int(brute::kTcSmem)));
+                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc2<false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(brute::kTcSmem2)));
+                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc2<true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(brute::kTcSmem2)));
                 tc_attr = true;
             }
         }
         const u64 ntc = u64((p + brute::kTcM - 1) / brute::kTcM) * ((p + brute::kTcN - 1) / brute::kTcN);
         const u32 tc_grid = static_cast<u32>(std::min<u64>(ntc, kSMs));
-        if (tc) {
+        if (tc && !tc1) {
+            brute::all_pairs_tc2<false><<<tc_grid, brute::kTcWarps * 32, brute::kTcSmem2, st>>>(
+                tmA, tmB, u32(p), u32(n), nz, u32(Kp), hist.as<unsigned long long>(), 0u, nullptr, nullptr, 0u);
+        } else if (tc) {
             brute::all_pairs_tc<false><<<tc_grid, brute::kTcThreads, brute::kTcSmem, st>>>(
                 tmA, tmB, u32(p), u32(n), nz, u32(Kp), hist.as<unsigned long long>(), 0u, nullptr, nullptr, 0u);
         } else {
@@ -1902,7 +1911,11 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
         outb.ensure(emit * sizeof(brute::PairOut));
         nout.ensure(4);
         XYZB_CUDA(cudaMemsetAsync(nout.p, 0, 4, st));
-        if (tc) {
+        if (tc && !tc1) {
+            brute::all_pairs_tc2<true><<<tc_grid, brute::kTcWarps * 32, brute::kTcSmem2, st>>>(
+                tmA, tmB, u32(p), u32(n), nz, u32(Kp), nullptr, u32(cutoff), outb.as<brute::PairOut>(),
+                nout.as<u32>(), u32(emit));
+        } else if (tc) {
             brute::all_pairs_tc<true><<<tc_grid, brute::kTcThreads, brute::kTcSmem, st>>>(
                 tmA, tmB, u32(p), u32(n), nz, u32(Kp), nullptr, u32(cutoff), outb.as<brute::PairOut>(),
                 nout.as<u32>(), u32(emit));
