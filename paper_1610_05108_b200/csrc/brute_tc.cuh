@@ -304,17 +304,29 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) all_pairs_tc2(const __grid_c
     const u32 tmem = tmem_holder;
     const u32 nj = (p + kTcM - 1) / kTcM, nk = (p + kTcN - 1) / kTcN;
     const u32 nkb = Kp / kTcKB;
-    const u64 ntiles = u64(nj) * nk;
+    // tile order: bands of kBand row tiles, row tile fastest inside a band, so
+    // the ~148 tiles in flight share a few A and B tiles in L2 (the operands,
+    // 2 x p x Kp bytes, do not fit in L2)
+    constexpr u32 kBand = 8;
+    const u64 ntiles = u64((nj + kBand - 1) / kBand) * kBand * nk;
+    auto tile_of = [&](u64 t, u32& tj, u32& tk) {
+        const u64 band = t / (u64(kBand) * nk), r = t % (u64(kBand) * nk);
+        tk = u32(r / kBand);
+        tj = u32(band * kBand + r % kBand);
+    };
     auto skip = [&](u64 t) {
-        const u32 tj = u32(t / nk), tk = u32(t % nk);
-        return tk * kTcN + kTcN <= tj * kTcM + 1;  // no pair with k > j
+        u32 tj, tk;
+        tile_of(t, tj, tk);
+        return tj >= nj || tk * kTcN + kTcN <= tj * kTcM + 1;  // no pair with k > j
     };
     if (warp == 0) {
         if (lane == 0) {  // ===== TMA producer =====
             u32 g = 0;
             for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 if (skip(t)) continue;
-                const int j0 = int(t / nk) * kTcM, k0 = int(t % nk) * kTcN;
+                u32 tj, tk;
+                tile_of(t, tj, tk);
+                const int j0 = int(tj) * kTcM, k0 = int(tk) * kTcN;
                 for (u32 kb = 0; kb < nkb; ++kb, ++g) {
                     const u32 s = g % kTcStages4;
                     if (g >= u32(kTcStages4)) mbar_wait(smem_addr(&empty_bar[s]), ((g / kTcStages4) - 1) & 1);
@@ -352,7 +364,9 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) all_pairs_tc2(const __grid_c
         for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
             if (skip(t)) continue;
             const u32 b = lt & 1, use = lt >> 1;
-            const u32 j0 = u32(t / nk) * kTcM, k0 = u32(t % nk) * kTcN;
+            u32 tj, tk;
+            tile_of(t, tj, tk);
+            const u32 j0 = tj * kTcM, k0 = tk * kTcN;
             mbar_wait(smem_addr(&tfull_bar[b]), use & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const u32 j = j0 + quarter * 32 + u32(lane);
