@@ -441,3 +441,28 @@ def test_constant_response_partner_is_the_complement(grouping, monkeypatch):
         assert (got.candidates_enumerated, got.aborted_repetitions) == (want.candidates_enumerated,
                                                                        want.aborted_repetitions)
         assert len(want.hits) > 0
+
+
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster"])
+def test_grouping_kernels_sweep_vs_oracle(grouping, monkeypatch):
+    """The fused group + join kernels (two-CTA split, one CTA, DSMEM cluster)
+    over the M range they serve (4..17) and p from a handful of columns to
+    2^M-sized tables: bit-exact against the restatement."""
+    if grouping in ("cta", "cluster"):
+        monkeypatch.setenv("XYZB_GROUPING", grouping)
+    xb = _engine()
+    rng = np.random.default_rng(7)
+    cases = [(4, 3), (5, 40), (6, 700), (8, 2000), (11, 600), (12, 5000), (13, 3000), (14, 9000), (15, 12000),
+             (16, 20000), (17, 33000)]
+    for t, (m, p) in enumerate(cases):
+        n = int(rng.choice([63, 64, 65, 130]))
+        x = ck.ref_rademacher(n, p, 300 + t, 2)
+        y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        cfg = xb.SearchConfig(m=m, l=2, gamma=0.7, seed=t, threads=1, top_k=20,
+                              max_candidates_per_rep=int(rng.choice([0, p])), estimate_complexity=False)
+        got = xb.Dataset(x).search(y, cfg)
+        want = ck.oracle_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, (m, p, msg)
+        assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
+            want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
