@@ -236,12 +236,13 @@ def run_reference(args):
         runs = r
     tot = sum(secs)
     value = runs * args.steps / tot
-    sample = f"2 x {REF_SAMPLE_L} runs of the cfg2 search per step (seed 7), reference threads={threads}"
+    sample = (f"2 x {REF_SAMPLE_L} runs of the {WORKLOAD['name']} search per step (seed 7; the full search has "
+              f"2 x {WORKLOAD['l']} runs), reference threads={threads}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "runs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": workload_config(args.gpus, REF_SAMPLE_L),
+        "config": workload_config(args.gpus, WORKLOAD["l"]),
         "verified_pairs_per_s": rep.candidates_checked * args.steps / tot,
         "cpu_baseline": {"value": value, "unit": "runs/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "runs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
