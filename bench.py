@@ -77,6 +77,7 @@ def parse():
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-serial", action="store_true", help="e2e with one step in flight only")
     ap.add_argument("--config", default="gwas", choices=sorted(WORKLOADS) + ["lasso"])
     args = ap.parse_args()
     if args.config != "lasso":
@@ -461,16 +462,47 @@ def main():
             torch.cuda.synchronize(local)
             e2e_s += time.perf_counter() - t0
             e2e_runs += 2 * L * world
+        # the same steps with three in flight (three host threads, one dataset and stream each): the H2D
+        # and host work of one step overlap the searches of the others, as a serving process with many
+        # (X, y) jobs runs them
+        pipe_s, pipe_runs = 0.0, 0
+        if world == 1 and not args.e2e_serial:
+            from concurrent.futures import ThreadPoolExecutor
+
+            def step():
+                d3 = xb.Dataset(x_host, device=local)
+                r3 = d3.search(y, cfg)
+                d3.close()
+                return r3
+
+            nstep = 24
+            with ThreadPoolExecutor(3) as ex, ClockSampler(local) as e2e_clk:
+                for f in [ex.submit(step) for _ in range(3)]:  # untimed warm-up of the threads
+                    f.result()
+                torch.cuda.synchronize(local)
+                t0 = time.perf_counter()
+                for f in [ex.submit(step) for _ in range(nstep)]:
+                    rr = f.result()
+                torch.cuda.synchronize(local)
+                pipe_s = time.perf_counter() - t0
+                pipe_runs = nstep * 2 * L
         e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
         if world > 1:
             torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
         if rank == 0:
             h2d = (x.words.nbytes if hasattr(x, "words") else x.values.nbytes) + y.nbytes
             d2h = len(rr.hits) * 32 + len(rr.top_k) * 8
-            out["e2e"] = {"value": e2e_runs / float(e2e_t[0]), "unit": "runs/s", "h2d_bytes_per_step": h2d,
-                          "d2h_bytes_per_step": d2h,
-                          "note": "fresh Dataset every step (H2D of X from pinned host memory + bit transpose) + search + "
-                                  "hits to host, wall clock per step"}
+            serial = e2e_runs / float(e2e_t[0])
+            if pipe_runs:
+                out["e2e"] = {"value": pipe_runs / pipe_s, "unit": "runs/s", "h2d_bytes_per_step": h2d,
+                              "d2h_bytes_per_step": d2h, "serial_value": serial, "clocks": e2e_clk.summary(),
+                              "note": "every step: a fresh Dataset (H2D of X from pinned host memory + bit "
+                                      "transpose) + search + hits to host; three steps in flight on three host "
+                                      "threads (wall clock over all steps); serial_value: one step at a time"}
+            else:
+                out["e2e"] = {"value": serial, "unit": "runs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                              "note": "fresh Dataset every step (H2D of X from pinned host memory + bit transpose) "
+                                      "+ search + hits to host, wall clock per step"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             secs, runs_s, rep_ref = ref_cpu_time(x, y, REF_SAMPLE_L, 1)

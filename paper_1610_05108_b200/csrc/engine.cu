@@ -110,35 +110,55 @@ BlockPool& pool() {
     return *p;
 }
 
+// The stream the calling thread's current API call issues its work on
+// (StreamScope): device buffers remember it, so returning a block to the pool
+// waits for that stream only, and calls on different datasets from different
+// host threads do not serialise on a device-wide synchronisation.
+thread_local cudaStream_t tl_stream = nullptr;
+thread_local cudaStream_t tl_drained = nullptr;  // a stream already synchronised (dataset teardown)
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
+    ~StreamScope() { tl_stream = prev; }
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
     int dev = 0;
+    cudaStream_t st = nullptr;  // the stream that used the block last (null: unknown)
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
         if (p) {
-            // the block may still be in use by queued work on some stream: drain
-            // the device before another buffer can be handed the same memory
-            int cur = 0;
-            cudaGetDevice(&cur);
-            cudaSetDevice(dev);
-            cudaDeviceSynchronize();
-            cudaSetDevice(cur);
+            // the block may still be in use by queued work: wait for its stream
+            // (or the whole device when unknown) before the pool hands it out again
+            if (!st || st != tl_drained) {
+                int cur = 0;
+                cudaGetDevice(&cur);
+                cudaSetDevice(dev);
+                if (st) cudaStreamSynchronize(st);
+                else cudaDeviceSynchronize();
+                cudaSetDevice(cur);
+            }
             pool().give(p, bytes, dev);
         }
         p = nullptr;
         bytes = 0;
     }
     void ensure(size_t b) {
-        if (b <= bytes) return;
+        if (b <= bytes) {
+            if (tl_stream) st = tl_stream;
+            return;
+        }
         release();
         XYZB_CUDA(cudaGetDevice(&dev));
         size_t got = std::max<size_t>(b, 256);
         p = pool().take(got, dev);
         bytes = got;
+        st = tl_stream;
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
@@ -300,11 +320,12 @@ void validate_params(const xyzb_params* q) {
 struct Trace {
     bool on = std::getenv("XYZB_TRACE") != nullptr;
     cudaStream_t st;
+    bool sync;  // false: host-side times only (the stream keeps running)
     std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-    explicit Trace(cudaStream_t s) : st(s) {}
+    explicit Trace(cudaStream_t s, bool sync_ = true) : st(s), sync(sync_) {}
     void mark(const char* what) {
         if (!on) return;
-        cudaStreamSynchronize(st);
+        if (sync) cudaStreamSynchronize(st);
         const auto now = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[xyzb] %-14s %8.1f us\n", what,
                      std::chrono::duration<double, std::micro>(now - t).count());
@@ -330,7 +351,9 @@ public:
         for (auto& w : workers_) w.join();
     }
     // memcpy(dst, src, len) split over the workers and the calling thread
+    // (one copy at a time: concurrent callers queue on call_mu_)
     void copy(void* dst, const void* src, size_t len) {
+        std::lock_guard<std::mutex> call(call_mu_);
         const size_t parts = workers_.size() + 1;
         const size_t slice = (len + parts - 1) / parts;
         std::unique_lock<std::mutex> lk(mu_);
@@ -372,7 +395,7 @@ private:
         }
     }
     std::vector<std::thread> workers_;
-    std::mutex mu_;
+    std::mutex mu_, call_mu_;
     std::condition_variable cv_, done_cv_;
     bool stop_ = false;
     uint64_t gen_ = 0;
@@ -1377,6 +1400,8 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     const auto t0 = std::chrono::steady_clock::now();
     validate_params(q);
     DeviceGuard dg(ds->device);
+    StreamScope ss(ds->stream);
+    Trace tr(ds->stream, false);
     check_mode(ds, q, resp);
     SearchCtx c;
     c.ds = ds;
@@ -1397,7 +1422,9 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     ds->clock.reset();
     cudaEvent_t ev_start = ds->clock.mark();
     upload_response(c, resp);
+    tr.mark("search:y");
     plan_runs(c, draws);
+    tr.mark("search:plan");
     cudaEvent_t ev_draw = ds->clock.mark();
     ds->clock.span(XYZB_STAGE_OTHER, ev_start, ev_draw);
     u32 H = 0;
@@ -1450,7 +1477,9 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             XYZB_CUDA(cudaMemcpyAsync(hs + o_pairs, ds->npairs.p, nbt * 4, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaMemcpyAsync(hs + o_enum, ds->enumerated.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaMemcpyAsync(hs + o_ver, ds->verified.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
+        tr.mark("search:launch");
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        tr.mark("search:device");
         H = *reinterpret_cast<const u32*>(hs);
         if (top_counts) {
             fusedK = reinterpret_cast<const u32*>(hs + o_cnt)[0];
@@ -1549,6 +1578,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         cudaEvent_t e1 = ds->clock.mark();
         ds->clock.span(XYZB_STAGE_ESTIMATE, e0, e1);
     }
+    tr.mark("search:results");
     cudaEvent_t ev_end = ds->clock.mark();
     XYZB_CUDA(cudaEventSynchronize(ev_end));
     // device time: search start to the end of the merge (hits resident in HBM;
@@ -1653,6 +1683,7 @@ extern "C" int xyzb_equal_pairs(const uint64_t* x_keys, const uint64_t* z_keys, 
         cudaStream_t st;
         XYZB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         struct S { cudaStream_t s; ~S() { cudaStreamDestroy(s); } } sguard{st};
+        StreamScope ss(st);
         DevBuf kb0, kb1, vb0, vb1, hist, blk, work, off, part, cnt, outp;
         kb0.ensure(2 * p * 8);
         kb1.ensure(2 * p * 8);
@@ -1705,6 +1736,7 @@ extern "C" int xyzb_project_keys(xyzb_dataset* ds, const uint32_t* draws, uint64
         if (n_draws == 0) return;
         DeviceGuard dg(ds->device);
         cudaStream_t st = ds->stream;
+        StreamScope ss(st);
         DevBuf rows, kout, xc, sg, yk;
         rows.ensure(n_draws * m * 4);
         kout.ensure(n_draws * ds->p * 8);
@@ -1729,6 +1761,7 @@ extern "C" int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, 
     return guarded(err, errlen, [&] {
         if (!ds || !params) throw data_error("pair_strengths: null argument");
         DeviceGuard dg(ds->device);
+        StreamScope ss(ds->stream);
         check_mode(ds, params, resp);
         SearchCtx c;
         c.ds = ds;
@@ -1793,6 +1826,7 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
         if (p > 0xffffffffull || n > 0xffffffffull) throw data_error("brute_force_search: matrix too large");
         DeviceGuard dg(ds->device);
         const cudaStream_t st = ds->stream;
+        StreamScope ss(st);
         // Y bits (y > 0) and the rows that can agree (y != 0)
         std::vector<u64> hy(2 * Wp, 0ull);
         for (u64 i = 0; i < n; ++i) {
@@ -1958,6 +1992,7 @@ extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, ui
         if (!ds || !params || !out || (n_parts && !parts)) throw data_error("xyzb_merge_results: null argument");
         if (params->stop_after_first_hit) throw data_error("xyzb: stop_after_first_hit cannot be combined with a rep shard");
         DeviceGuard dg(ds->device);
+        StreamScope ss(ds->stream);
         SearchCtx c;
         c.ds = ds;
         c.q = params;
@@ -2085,6 +2120,7 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
             ds->hit_cap = static_cast<u32>(std::max<u64>(1, std::strtoull(e, nullptr, 10)));
         DeviceGuard dg(ds->device);
         XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+        StreamScope ss(ds->stream);
         ds->n = pr->n_rows;
         ds->p = pr->n_cols;
         const cudaStream_t st = ds->stream;
@@ -2106,7 +2142,9 @@ void xyzb_dataset_destroy(xyzb_dataset* ds) {
         cudaSetDevice(ds->device);
         cudaStreamSynchronize(ds->stream);
         cudaStream_t st = ds->stream;
+        tl_drained = st;  // every buffer of the dataset is idle now
         delete ds;
+        tl_drained = nullptr;
         cudaStreamDestroy(st);
         cudaSetDevice(prev);
     }
@@ -2132,6 +2170,7 @@ int xyzb_dataset_open(const char* path, int32_t device, xyzb_dataset** out, char
         ds->device = device;
         DeviceGuard dg(device);
         XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+        StreamScope ss(ds->stream);
         ds->n = dims[0];
         ds->p = dims[1];
         const cudaStream_t st = ds->stream;
