@@ -466,3 +466,29 @@ def test_grouping_kernels_sweep_vs_oracle(grouping, monkeypatch):
         assert ok, (m, p, msg)
         assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
             want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
+
+
+def test_concurrent_searches_on_different_datasets():
+    """Host threads driving different datasets (one stream each) concurrently
+    get exactly the serial results (the engine's buffers wait on their own
+    stream when they return to the shared pool)."""
+    from concurrent.futures import ThreadPoolExecutor
+    xb = _engine()
+    jobs = []
+    for t in range(6):
+        x, y = ck.ref_planted(400, 1500 + 100 * t, 2, 9, 0.9, 10 + t)
+        cfg = xb.SearchConfig(m=8 + t % 3, l=6, gamma=0.56, seed=t, top_k=10)
+        jobs.append((x, y, cfg))
+    serial = [report_hits(xb.Dataset(x).search(y, cfg)) for x, y, cfg in jobs]
+
+    def run(job):
+        x, y, cfg = job
+        d = xb.Dataset(x)
+        try:
+            return report_hits(d.search(y, cfg))
+        finally:
+            d.close()
+
+    for _ in range(3):
+        with ThreadPoolExecutor(3) as ex:
+            assert list(ex.map(run, jobs)) == serial
