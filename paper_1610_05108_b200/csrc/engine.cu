@@ -38,6 +38,7 @@
 #include "draws.cuh"
 #include "host_rng.hpp"
 #include "merge_kernels.cuh"
+#include "msplit_group.cuh"
 #include "radix_sort.cuh"
 #include "run_sort.cuh"
 #include "real_kernels.cuh"
@@ -827,7 +828,17 @@ void run_batches(SearchCtx& c) {
     // XYZB_GROUPING=bucket keeps the multi-kernel counting sort
     // M <= 16: one CTA per run with 16-bit shared counters (no cluster barriers);
     // XYZB_GROUPING=cluster keeps the DSMEM cluster kernel
-    const bool grouped_path = M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
+    const auto gsel_is = [&](const char* v) { return gsel && std::string(gsel) == v; };
+    // M = 17, 18: a 2^(M-16)-CTA cluster per run (16-bit tables, DSMEM exchanges) when the bucket
+    // space is dense enough — measured faster than the DSMEM-table kernel and the counting sort at
+    // p = 1e5; at M = 19, 20 every CTA streaming all keys costs more than the counting sort (config 4:
+    // 102 vs 53 ms), so the kernel runs there only when forced (XYZB_GROUPING=msplit, also for sparse
+    // runs; =cluster keeps the DSMEM-table kernel at M = 17)
+    const bool ms_path = M >= 17 && M <= 20 && !sort_sel && !gsel_is("sort") && !gsel_is("bucket") &&
+                         !gsel_is("cluster") && sizeof(K) == 4 &&
+                         ((M <= 18 && (u64(1) << M) <= 4 * p + 1024) || gsel_is("msplit")) &&
+                         kern::msplit_schedulable(int(M));
+    const bool grouped_path = !ms_path && M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
                               !(gsel && (std::string(gsel) == "sort" || std::string(gsel) == "bucket"));
     // 4 <= M <= 16: two CTAs per run (cluster), bucket space split on a key bit
     // (XYZB_GROUPING=cta keeps one CTA per run)
@@ -835,11 +846,16 @@ void run_batches(SearchCtx& c) {
     const bool split_path = cta_path && M >= 4 && !(gsel && std::string(gsel) == "cta");
     const bool cluster_path = grouped_path && !cta_path;
     if (cta_path && kern::cta_group_scratch(int(M), p)) ds->gtab.ensure(kern::cta_group_scratch(int(M), p) * 4);
+    if (ms_path) {
+        if (kern::msplit_group_scratch(int(M), p)) ds->gtab.ensure(kern::msplit_group_scratch(int(M), p) * 4);
+        ds->slots.ensure(kSMs * 4);
+        XYZB_CUDA(cudaMemsetAsync(ds->slots.p, 0, kSMs * 4, st));
+    }
     if (split_path) {
         ds->slots.ensure(kSMs * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->slots.p, 0, kSMs * 4, st));
     }
-    const bool buckets = !grouped_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
+    const bool buckets = !grouped_path && !ms_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
                          !(gsel && std::string(gsel) == "sort") && !sort_sel;
     if (buckets) {
         ds->bcnt.ensure((B << M) * 4);
@@ -915,7 +931,24 @@ void run_batches(SearchCtx& c) {
         const K* sorted_keys = nullptr;
         int vshift = 0;
         cudaEvent_t e2;
-        if (split_path) {
+        if (ms_path) {
+            // ---- group + join fused: 2^(M-16) CTAs per run, 16-bit tables split by parities of c's zero bits ----
+            if constexpr (sizeof(K) == 4) {
+                if (!kern::msplit_group_join_launch(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
+                                                    ds->tot.as<u64>(), ds->work_run.as<u64>(),
+                                                    ds->items.as<kern::Item>(), nitems, static_cast<u32>(item_cap),
+                                                    npairs_b, ds->pairs.as<kern::PairRec>(),
+                                                    static_cast<u32>(c.pair_cap), ds->gtab.as<u32>(),
+                                                    ds->slots.as<u32>(), st))
+                    throw internal_error("xyzb: the grouping cluster could not be launched");
+            }
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_SORT] += 1;
+            sv = vb[0];
+            e2 = clk.mark();
+            clk.span(XYZB_STAGE_SORT, e1, e2);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+        } else if (split_path) {
             // ---- group + join fused: two CTAs per run, each half of the 16-bit bucket table ----
             if constexpr (sizeof(K) == 4) {  // M <= 16 always runs with u32 keys
                 kern::split_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
@@ -1061,9 +1094,10 @@ void run_batches(SearchCtx& c) {
         A.guard = c.guard;
         A.sv = sv;
         A.S = p;
-        A.vkeys = (buckets || grouped_path) ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
-        A.vkeys_by_pos = (buckets || grouped_path) ? 0 : 1;
-        A.xkeys = (buckets || grouped_path) ? static_cast<const void*>(k0) : ds->keys_x.p;
+        const bool unsorted = buckets || grouped_path || ms_path;
+        A.vkeys = unsorted ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
+        A.vkeys_by_pos = unsorted ? 0 : 1;
+        A.xkeys = unsorted ? static_cast<const void*>(k0) : ds->keys_x.p;
         A.key64 = sizeof(K) == 8;
         A.vshift = vshift;
         A.rid = rid;

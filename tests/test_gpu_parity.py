@@ -492,3 +492,32 @@ def test_concurrent_searches_on_different_datasets():
     for _ in range(3):
         with ThreadPoolExecutor(3) as ex:
             assert list(ex.map(run, jobs)) == serial
+
+
+@pytest.mark.parametrize("case", ["dense", "sparse_forced", "constant_y"])
+def test_msplit_grouping_vs_oracle(case, monkeypatch):
+    """17 <= M <= 20: one 2^(M-16)-CTA cluster per run (16 CTAs at M = 20).
+    Dense tables by default, a sparse run forced onto it, and a constant
+    response (c = all ones in the negative pass: partners in other CTAs,
+    read through DSMEM). Bit-exact against the restatement."""
+    xb = _engine()
+    rng = np.random.default_rng(17)
+    if case == "dense":  # M = 19, 20 only when forced (the counting sort is faster there)
+        monkeypatch.setenv("XYZB_GROUPING", "msplit")
+        cases = [(17, 40000), (18, 70000), (19, 140000), (20, 270000)]
+    elif case == "sparse_forced":
+        monkeypatch.setenv("XYZB_GROUPING", "msplit")
+        cases = [(18, 3000), (20, 9000)]
+    else:
+        cases = [(18, 70000), (17, 40000)]
+    for t, (m, p) in enumerate(cases):
+        n = 64
+        x = ck.ref_rademacher(n, p, 500 + t, 3)
+        y = np.ones(n, np.int8) if case == "constant_y" else np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        cfg = xb.SearchConfig(m=m, l=2, gamma=0.72, seed=t, threads=1, top_k=20, estimate_complexity=False)
+        got = xb.Dataset(x).search(y, cfg)
+        want = ck.oracle_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, (m, p, msg)
+        assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
+            want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
