@@ -78,9 +78,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e with one step in flight only")
-    ap.add_argument("--config", default="gwas", choices=sorted(WORKLOADS) + ["lasso"])
+    ap.add_argument("--config", default="gwas", choices=sorted(WORKLOADS) + ["lasso", "brute"])
     args = ap.parse_args()
-    if args.config != "lasso":
+    if args.config not in ("lasso", "brute"):
         select(args.config)
     return args
 
@@ -323,10 +323,81 @@ def run_lasso(args):
                               "note": "lasso_path wall clock through the drop-in (host arrays in, coefficients out)"}}))
 
 
+def run_brute(args):
+    """The exhaustive oracle (oracle::brute_force_search, SURVEY §8f item 4) at
+    config 2 size: every pair of p = 1e5 columns (5e9 pairs), strength
+    histogram (100 bins) + top-100, on the tensor cores (tcgen05 kind::i8);
+    the reference's brute force timed on a bounded sample (p = 600)."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    import paper_1610_05108_b200 as xb
+    from paper_1610_05108_b200 import synth
+    x, y, _ = synth.gwas()
+    p, n = x.n_cols, x.n_rows
+    metric = "exhaustive pair strengths/s (oracle::brute_force_search, BASELINE cfg2 data n=4000 p=100000)"
+    cfg = {"workload": "brute_cfg2", "n": n, "p": p, "pairs": p * (p - 1) // 2, "histogram_bins": 100, "top_k": 100}
+    if args.impl == "reference":
+        from tests import checkers as ck
+        sub = xb.PackedMatrix(n, 600, x.words[:600].copy())
+        secs = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            _, scanned, _ = ck.ref_brute_force(sub, y, top_k=100, histogram_bins=100, force=True)
+            secs.append(time.perf_counter() - t0)
+        v = scanned / statistics.median(secs)
+        print(json.dumps({"impl": "reference", "metric": metric, "value": v, "unit": "pairs/s", "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": 0, "ms_per_step": 1e3 * statistics.median(secs),
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                          "data": "synthetic", "config": cfg,
+                          "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": 1, "kind": "reference",
+                                           "sample": "reference brute force on the first 600 columns (179700 pairs)"},
+                          "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    ds = xb.Dataset(x, device=local)
+    for _ in range(max(1, args.warmup)):
+        xb.brute_force_search(ds, y, top_k=100, histogram_bins=100, force=True)
+    t = []
+    with ClockSampler(local) as clk:
+        for _ in range(max(1, args.steps)):
+            torch.cuda.synchronize(local)
+            t0 = time.perf_counter()
+            r = xb.brute_force_search(ds, y, top_k=100, histogram_bins=100, force=True)
+            t.append(time.perf_counter() - t0)
+    sec = statistics.median(t)
+    pairs = r.pairs_scanned
+    # tensor work: 128 x 256 tiles of the upper triangle, K = n rounded to 128, two passes (histogram, emit)
+    kp = (n + 127) // 128 * 128
+    nj, nk = (p + 127) // 128, (p + 255) // 256
+    tiles = sum(1 for tj in range(nj) for tk in range(nk) if tk * 256 + 256 > tj * 128 + 1)
+    ops = 2 * tiles * 128 * 256 * kp * 2
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        bf16 = float(json.load(f)["bf16_tflops"])
+    achieved = ops / sec / 1e12
+    print(json.dumps({
+        "metric": metric, "value": pairs / sec, "unit": "pairs/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8 (+-1) with s32 accumulation", "data": "synthetic (gwas_cfg2 generator)",
+        "config": cfg, "wall_clock": "host wall time of the whole call (two kernel passes, host derivation)",
+        "roofline": {"bound": "tensor", "kernel": "all_pairs_tc2 (tcgen05.mma kind::i8)", "achieved": achieved,
+                     "peak": 2 * bf16, "unit": "TOP/s", "frac": achieved / (2 * bf16),
+                     "peak_source": "2 x measured dense bf16 (MEASURED_PEAKS.json): B200's int8 tensor rate is "
+                                    "twice its bf16 rate",
+                     "traffic": None},
+        "clocks": clk.summary(), "gpu_launches": 6,
+        "e2e": {"value": pairs / sec, "unit": "pairs/s", "h2d_bytes_per_step": y.nbytes,
+                "d2h_bytes_per_step": 100 * 16 + 100 * 8, "note": "X resident; y in, pairs and histogram out"},
+    }))
+
+
 def main():
     args = parse()
     if args.config == "lasso":
         run_lasso(args)
+        return
+    if args.config == "brute":
+        run_brute(args)
         return
     if args.impl == "reference":
         run_reference(args)
