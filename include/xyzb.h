@@ -35,7 +35,10 @@
  * proj/tools/xyz_main.cpp:601-619).
  *
  * Threading: one host thread per dataset at a time (not re-entrant on the same
- * handle); each dataset owns one CUDA stream on its device.
+ * handle); each dataset owns one CUDA stream on its device, and calls on
+ * different datasets from different host threads run concurrently (device
+ * buffers return to the shared pool after their own stream drains, not after
+ * a device-wide synchronisation).
  */
 #ifndef XYZB_H
 #define XYZB_H

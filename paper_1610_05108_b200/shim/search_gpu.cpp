@@ -125,8 +125,24 @@ xyzb_params to_params(const SearchConfig& c) {
     return q;
 }
 
+// XYZB_SHIM_STATS=1: time spent in GPU searches, printed at exit (how much of
+// a caller such as lasso_path is the screen).
+struct ShimStats {
+    double seconds = 0.0;
+    size_t calls = 0, hits = 0;
+    ~ShimStats() {
+        if (std::getenv("XYZB_SHIM_STATS"))
+            std::fprintf(stderr, "[xyz_search shim] %zu calls, %.3f s, %zu hits\n", calls, seconds, hits);
+    }
+};
+ShimStats& shim_stats() {
+    static ShimStats s;
+    return s;
+}
+
 SearchReport run_gpu(const uint64_t* words, const double* real, size_t n, size_t p, const xyzb_response& resp,
                      const SearchConfig& cfg) {
+    const auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> lock(cache().mu);
     xyzb_dataset* ds = cache().get(words, real, n, p);
     const xyzb_params q = to_params(cfg);
@@ -156,6 +172,10 @@ SearchReport run_gpu(const uint64_t* words, const double* real, size_t n, size_t
     rep.m_used = r.m_used;
     rep.l_used = r.l_used;
     xyzb_result_free(&r);
+    ShimStats& st = shim_stats();
+    st.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    ++st.calls;
+    st.hits += rep.hits.size();
     return rep;
 }
 
