@@ -592,14 +592,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSpThreads, 3) split
         __syncthreads();
         ibase += ws[66];
         pbase += ws[67];
-        for (u32 li = threadIdx.x; li < Tl; li += blockDim.x) {
-            const HeadBlock hb = block_of(li);
-            if (hb.work == 0) continue;
+        // pass 2, warp-cooperative: the pairs of small blocks are written by the
+        // whole warp, one coalesced 16-byte record per lane (a lane's own blocks
+        // would leave most of the warp idle); large blocks become items as before.
+        // The warp owns the contiguous slot range of its 32 threads.
+        u32 woff = __shfl_sync(0xffffffffu, pbase, 0);
+        const u32 off = u32(u64(b) * p);
+        uint4* dst = reinterpret_cast<uint4*>(pairs);
+        for (u32 li0 = 0; li0 < Tl; li0 += blockDim.x) {
+            const u32 li = li0 + threadIdx.x;
+            HeadBlock hb;
+            if (li < Tl) hb = block_of(li);
             u32 ne, np, nsc;
             emit_count(hb, hmax, pair_list, ne, np, nsc);
-            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p, grouped);
-            ibase += ne;
-            pbase += np;
+            const bool inl = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
+            const u32 ni = inl ? np : 0u;
+            u32 ea = np, ei = ni;  // inclusive warp scans of all pairs / inline pairs
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t1 = __shfl_up_sync(0xffffffffu, ea, o), t2 = __shfl_up_sync(0xffffffffu, ei, o);
+                if (lane >= o) {
+                    ea += t1;
+                    ei += t2;
+                }
+            }
+            const u32 tot_all = __shfl_sync(0xffffffffu, ea, 31), tot_inl = __shfl_sync(0xffffffffu, ei, 31);
+            const u32 xa = ea - np;  // this lane's first slot within the warp's share of the iteration
+            if (ne) {  // large blocks: items (their pairs are expanded later at it.pad)
+                emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, woff + xa, items, item_cap, pairs, pair_cap, p,
+                           grouped);
+                ibase += ne;
+            }
+            for (u32 idx0 = 0; idx0 < tot_inl; idx0 += 32) {
+                const u32 idx = idx0 + lane;
+                // owner lane: the first lane whose inclusive inline count exceeds idx
+                u32 ow = 0;
+#pragma unroll
+                for (int stp = 16; stp > 0; stp >>= 1) {
+                    const u32 v = __shfl_sync(0xffffffffu, ei, int(ow + stp - 1));
+                    if (v <= idx) ow += stp;
+                }
+                ow = min(ow, 31u);
+                const u32 o_hs = __shfl_sync(0xffffffffu, hb.hs, ow), o_hc = __shfl_sync(0xffffffffu, hb.hc, ow);
+                const u32 o_ss = __shfl_sync(0xffffffffu, hb.ss, ow), o_sc = __shfl_sync(0xffffffffu, hb.sc, ow);
+                const u32 o_fl = __shfl_sync(0xffffffffu, hb.flags, ow);
+                const u32 o_xa = __shfl_sync(0xffffffffu, xa, ow);
+                const u32 o_ei = __shfl_sync(0xffffffffu, ei - ni, ow);  // owner's first inline index
+                if (idx < tot_inl) {
+                    u32 l = idx - o_ei, h = 0, q;
+                    const bool diag = o_fl & 2u;
+                    if (diag) {  // pairs (h, q), h < q < hc: walk the rows (hc <= 8 here)
+                        while (l >= o_hc - 1 - h) {
+                            l -= o_hc - 1 - h;
+                            ++h;
+                        }
+                        q = h + 1 + l;
+                    } else {
+                        h = l / o_sc;
+                        q = l - h * o_sc;
+                    }
+                    const u32 slot = woff + o_xa + (idx - o_ei);
+                    if (slot < pair_cap) {
+                        const u32 hcol = grouped[off + o_hs + h], scol = grouped[off + o_ss + q];
+                        const bool first_held = diag || (o_fl & 1u);
+                        dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, o_fl);
+                    }
+                }
+            }
+            woff += tot_all;
         }
     }
     cl.sync();  // #4: the partner may still read this CTA's table and shares
