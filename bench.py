@@ -426,7 +426,7 @@ def main():
         rep = ds.search(y, my_cfg)
     barrier()
     dev_ms, verify_ms, verify_bytes, verify_launches, launches, runs, verified = 0.0, 0.0, 0, 0, 0, 0, 0
-    stage = {}
+    stage, stage_b = {}, {}
     t_wall = 0.0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -455,6 +455,8 @@ def main():
             verified += r.verified_pairs
             for k, v in r.stage_ms.items():
                 stage[k] = stage.get(k, 0.0) + v
+            for k, v in r.stage_bytes.items():
+                stage_b[k] = stage_b.get(k, 0) + v
     barrier()
     # max over ranks of the device time
     t_dev = dev_ms
@@ -492,6 +494,13 @@ def main():
             "verified_pairs_per_s": verified / (t_dev / 1e3),
             "wall_ms_per_step": 1e3 * t_wall / args.steps,
             "stage_ms_per_step": {k: v / args.steps for k, v in stage.items()},
+            # per-stage algorithmic bytes (projection M*p/8 + keys, grouping keys + indices,
+            # verify 2 columns per canonical candidate + Y) over the stage's event time, vs measured HBM
+            "stage_roofline": {k: {"algorithmic_bytes": stage_b[k] / args.steps,
+                                   "gbps": stage_b[k] / (stage[k] / 1e3) / 1e9 if stage.get(k) else None,
+                                   "frac_of_hbm": (stage_b[k] / (stage[k] / 1e3) / 1e9) / peaks()[0]
+                                   if stage.get(k) else None}
+                               for k in ("project", "sort", "join", "verify") if stage_b.get(k)},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "verify_pairs_binary" if WORKLOAD["mode"] == "binary" else "verify_items<RealStrength>", "achieved": achieved, "peak": hbm,
                          "peak_source": src, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
