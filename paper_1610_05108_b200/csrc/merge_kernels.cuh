@@ -282,6 +282,9 @@ __global__ void __launch_bounds__(kSmallThreads) merge_small(const DevHit* __res
         if (s_v[a] != s_v[b]) return s_v[a] < s_v[b];
         return s_jk[a] < s_jk[b];
     });
+    // output records; the top-K keys go to shared memory (s_v, s_jk are free
+    // once the order sort is done): strength, then (min, max, sign desc)
+    double* s_str = reinterpret_cast<double*>(s_tag);
     for (int i = threadIdx.x; i < int(K); i += blockDim.x) {
         const DevHit x = h[s_idx[i]];
         const int8_t sg = sign_by_rid[x.rid];
@@ -297,18 +300,18 @@ __global__ void __launch_bounds__(kSmallThreads) merge_small(const DevHit* __res
     __syncthreads();
     if (top_k > 0 && K > 0) {
         // A.10: strength desc, min asc, max asc, sign desc (positions in `out`)
+        for (int i = threadIdx.x; i < int(K); i += blockDim.x) {
+            const DevHit x = h[s_idx[i]];
+            s_str[i] = x.s;
+            s_jk[i] = (u64(min(x.j, x.k)) << 33) | (u64(max(x.j, x.k)) << 1) | (sign_by_rid[x.rid] > 0 ? 0ull : 1ull);
+        }
         for (int i = threadIdx.x; i < NK; i += blockDim.x) s_aux[i] = u32(i);
         __syncthreads();
         bitonic(s_aux, NK, [&](u32 a, u32 b) {
             const bool va = a < K, vb = b < K;
             if (!va || !vb) return va && !vb;
-            const xyzb_hit x = out[a], y = out[b];
-            if (x.strength != y.strength) return x.strength > y.strength;
-            const u32 xl = min(x.j, x.k), yl = min(y.j, y.k);
-            if (xl != yl) return xl < yl;
-            const u32 xh = max(x.j, x.k), yh = max(y.j, y.k);
-            if (xh != yh) return xh < yh;
-            return x.sign > y.sign;
+            if (s_str[a] != s_str[b]) return s_str[a] > s_str[b];
+            return s_jk[a] < s_jk[b];
         });
         const u64 kk = top_k < u64(K) ? top_k : u64(K);
         for (int i = threadIdx.x; i < int(kk); i += blockDim.x) top_out[i] = s_aux[i];
