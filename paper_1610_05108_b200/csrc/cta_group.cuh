@@ -85,30 +85,68 @@ struct SmemTab16 {
     __device__ __forceinline__ u32 chunk_base(u32 v) const { return base[v >> cbits]; }
     __device__ __forceinline__ u32 half(u32 v) const { return (w[v >> 1] >> ((v & 1u) << 4)) & 0xffffu; }
     // counts -> exclusive in-chunk offsets; chunk bases; flags chunks > 65535.
-    // Rounds of blockDim consecutive words (one per thread: no bank
-    // conflicts), one block scan per round with a running carry.
+    // Each warp owns a contiguous segment of whole chunks: pass A sums it,
+    // one warp scans the segment totals, pass B walks the segment in 32-word
+    // steps (conflict-free, warp shuffles) writing offsets and chunk bases.
+    // Two block barriers in all.
     __device__ u32 scan(u32* ws) {
         const u32 NW = (u32(1) << M) >> 1;
-        const u32 cwbits = cbits - 1;  // log2 words per chunk (cbits >= 1)
-        u32 carry = 0;
-        for (u32 r0 = 0; r0 < NW; r0 += blockDim.x) {
-            const u32 wi = r0 + threadIdx.x;
-            const bool act = wi < NW;
+        const u32 cw = u32(1) << (cbits - 1);  // words per chunk (cbits >= 1)
+        const u32 nwarps = blockDim.x >> 5;
+        u32 seg = (NW + nwarps - 1) / nwarps;
+        seg = (seg + cw - 1) / cw * cw;
+        if (seg < 32) seg = 32;  // whole steps (a segment may then hold several chunks)
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const u32 s0 = u32(wid) * seg, s1 = min(NW, s0 + seg);
+        u32 loc = 0;
+        for (u32 wi = s0 + lane; wi < s1; wi += 32) {
+            const u32 x = w[wi];
+            loc += (x & 0xffffu) + (x >> 16);
+        }
+        loc = warp_sum(loc);
+        if (lane == 0) ws[wid] = loc;
+        __syncthreads();
+        if (wid == 0) {
+            const u32 t = u32(lane) < nwarps ? ws[lane] : 0u;
+            u32 incl = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            ws[lane] = incl - t;
+            if (lane == 31) ws[32] = incl;
+        }
+        __syncthreads();
+        u32 carry = ws[wid], cb = 0;
+        for (u32 w0 = s0; w0 < s1; w0 += 32) {
+            const u32 wi = w0 + u32(lane);
+            const bool act = wi < s1;
             const u32 x = act ? w[wi] : 0u;
             const u32 lo = x & 0xffffu, hi = x >> 16;
-            u32 total;
-            const u32 pos = carry + block_exclusive(lo + hi, ws, &total);
-            if (act && (wi & ((u32(1) << cwbits) - 1)) == 0) base[wi >> cwbits] = pos;
-            __syncthreads();
+            u32 incl = lo + hi;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const u32 pos = carry + incl - (lo + hi);
+            if (cw >= 32) {  // chunk starts are step starts
+                if ((w0 & (cw - 1)) == 0) cb = __shfl_sync(0xffffffffu, pos, 0);
+            } else {  // several chunks per step: the base is the chunk's first lane
+                cb = __shfl_sync(0xffffffffu, pos, lane & ~int(cw - 1));
+            }
             if (act) {
-                const u32 cb = base[wi >> cwbits];
+                if ((wi & (cw - 1)) == 0) base[wi / cw] = pos;
                 const u32 o = pos - cb;
                 if (o + lo + hi > 0xffffu) *ovf = 1u;
                 w[wi] = (o & 0xffffu) | (((o + lo) & 0xffffu) << 16);
             }
-            carry += total;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        return carry;
+        const u32 total = ws[32];
+        __syncthreads();  // ws reusable
+        return total;
     }
     // after the scatter: bucket v occupies [beg, beg + cnt)
     __device__ __forceinline__ void group(u32 v, u32& beg, u32& cnt) const {
