@@ -426,6 +426,7 @@ def main():
         rep = ds.search(y, my_cfg)
     barrier()
     dev_ms, verify_ms, verify_bytes, verify_launches, launches, runs, verified = 0.0, 0.0, 0, 0, 0, 0, 0
+    ex_ms = 0.0  # all-gather + merge of the per-rank hit lists (N > 1), CUDA events on torch's stream
     stage, stage_b = {}, {}
     t_wall = 0.0
     with ClockSampler(local) as clk:
@@ -441,10 +442,16 @@ def main():
                     mine = parallel.pack_result(res)
             finally:
                 ds.free_result(res)
-            if world > 1:  # the exchange step: one all-gather + device merge, timed on the wall
+            if world > 1:  # the exchange step: one all-gather + device merge, in the timed step
                 t1 = time.perf_counter()
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
                 parts = [parallel.PackedPart(b) for b in parallel.all_gather_bytes(mine, torch.device("cuda", local))]
-                merged = ds.merge([p.result for p in parts], cfg)
+                merged = ds.merge([p.result for p in parts], cfg)  # returns once the merged hits are on the host
+                ev1.record()
+                ev1.synchronize()
+                ex_ms += ev0.elapsed_time(ev1)
+                dev_ms += ev0.elapsed_time(ev1)
                 t_wall += time.perf_counter() - t1
             dev_ms += r.device_ms
             verify_ms += r.verify_kernel_ms
@@ -494,6 +501,7 @@ def main():
             "verified_pairs_per_s": verified / (t_dev / 1e3),
             "wall_ms_per_step": 1e3 * t_wall / args.steps,
             "stage_ms_per_step": {k: v / args.steps for k, v in stage.items()},
+            "exchange_ms_per_step": ex_ms / args.steps if world > 1 else 0.0,
             # per-stage algorithmic bytes (projection M*p/8 + keys, grouping keys + indices,
             # verify 2 columns per canonical candidate + Y) over the stage's event time, vs measured HBM
             "stage_roofline": {k: {"algorithmic_bytes": stage_b[k] / args.steps,
