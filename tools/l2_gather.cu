@@ -72,6 +72,36 @@ __global__ void fill_pairs(uint4* pr, uint32_t* sv, uint32_t npairs, uint32_t ns
         sv[i] = hash32(i ^ 0x9e3779b9u) % ncols;
 }
 
+// 256-bit loads (LDG.E.ENL2.256): G lanes x (512 / (32 G)) loads of 32 B per column.
+__device__ __forceinline__ void ld256(const void* p, uint64_t& a, uint64_t& b, uint64_t& c, uint64_t& d) {
+    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+template <int G>
+__global__ void __launch_bounds__(256) gather256(const ulonglong2* __restrict__ X, uint32_t ncols, uint32_t npairs,
+                                                 uint32_t seed, unsigned long long* sink) {
+    const int lane = threadIdx.x & 31, tl = lane & (G - 1);
+    const uint32_t team = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint32_t nteams = (gridDim.x * blockDim.x) / G;
+    constexpr int NL = 16 / G;  // 32-byte loads per lane per column
+    uint32_t acc = 0;
+    for (uint32_t q = team; q < npairs; q += nteams) {
+        const uint32_t j = hash32(q * 2 + seed) % ncols, k = hash32(q * 2 + 1 + seed) % ncols;
+        const char* a = reinterpret_cast<const char*>(X + size_t(j) * 32);
+        const char* b = reinterpret_cast<const char*>(X + size_t(k) * 32);
+        uint64_t va[NL][4], vb[NL][4];
+#pragma unroll
+        for (int it = 0; it < NL; ++it) {
+            ld256(a + (it * G + tl) * 32, va[it][0], va[it][1], va[it][2], va[it][3]);
+            ld256(b + (it * G + tl) * 32, vb[it][0], vb[it][1], vb[it][2], vb[it][3]);
+        }
+#pragma unroll
+        for (int it = 0; it < NL; ++it)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc += __popcll(va[it][e] ^ vb[it][e]);
+    }
+    if (acc == 0xffffffffu) atomicAdd(sink, acc);
+}
+
 __global__ void sweep(const ulonglong2* __restrict__ X, size_t n, unsigned long long* sink) {
     uint64_t acc = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
@@ -118,6 +148,23 @@ int main() {
           }
             printf("random 512 B column pairs, team %2d lanes, grid %5d: %.1f GB/s (%.3f ms per 16M pairs)\n", g,
                    grid, 5.0 * npairs * 1024 / (ms * 1e-3) / 1e9, ms / 5);
+        }
+    }
+    for (int g : {4, 8, 16}) {
+        for (int grid : {148 * 4, 148 * 8, 148 * 16}) {
+            for (int w = 0; w < 2; ++w) {
+                cudaEventRecord(e0);
+                for (int r = 0; r < 5; ++r) {
+                    if (g == 4) gather256<4><<<grid, 256>>>(X, ncols, npairs, r, sink);
+                    if (g == 8) gather256<8><<<grid, 256>>>(X, ncols, npairs, r, sink);
+                    if (g == 16) gather256<16><<<grid, 256>>>(X, ncols, npairs, r, sink);
+                }
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                cudaEventElapsedTime(&ms, e0, e1);
+            }
+            printf("random 512 B column pairs, 256-bit loads, team %2d lanes, grid %5d: %.1f GB/s (%.3f ms per 16M pairs)\n",
+                   g, grid, 5.0 * npairs * 1024 / (ms * 1e-3) / 1e9, ms / 5);
         }
     }
     {
