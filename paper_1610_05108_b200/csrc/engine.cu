@@ -235,7 +235,7 @@ struct xyzb_dataset {
     DevBuf Xpos, Xzero;  // u32 [n][P32]
     bool has_zero = false, in_unit = true;
     // response (per search)
-    DevBuf yk_bits, spos, sneg, wabs, yreal;
+    DevBuf yk_bits, spos, sneg, wabs, yreal, yreal32;
     // batch scratch
     DevBuf keys[2], vals[2], keys_x, hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
     DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots;
@@ -1169,12 +1169,29 @@ void run_batches(SearchCtx& c) {
             kern::WeightedStrength f{ds->Xc.as<u64>(), static_cast<u32>(ds->Wp), ds->spos.as<u64>(), ds->sneg.as<u64>(),
                                      ds->wabs.as<double>(), c.norm, c.gamma};
             kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
-        } else if (unbiased) {
-            kern::RealStrength<true> f{ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(), c.norm, c.gamma};
-            kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
         } else {
-            kern::RealStrength<false> f{ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(), c.norm, c.gamma};
-            kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
+            // the fp32 response in shared memory when it fits (n <= 49152), else through L1
+            ds->yreal32.ensure(ds->n4 * 4);
+            real::to_f32<<<grid_for(ds->n4, 256, 256), 256, 0, st>>>(ds->yreal.as<double>(), ds->n4,
+                                                                     ds->yreal32.as<float>());
+            XYZB_LAUNCH_CHECK();
+            const size_t ysm = ds->n4 * 4;
+            const bool ysmem = ysm <= (size_t(192) << 10);
+            if (ysmem && ysm > (size_t(48) << 10)) {
+                XYZB_CUDA(cudaFuncSetAttribute(kern::verify_items_real<true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(ysm)));
+                XYZB_CUDA(cudaFuncSetAttribute(kern::verify_items_real<false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(ysm)));
+            }
+            if (unbiased) {
+                kern::RealStrength<true> f{ds->Xc32.as<float>(), ds->n4, ds->yreal32.as<float>(), c.norm, c.gamma};
+                if (ysmem) kern::verify_items_real<true><<<vgrid, 256, ysm, st>>>(A, f);
+                else kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
+            } else {
+                kern::RealStrength<false> f{ds->Xc32.as<float>(), ds->n4, ds->yreal32.as<float>(), c.norm, c.gamma};
+                if (ysmem) kern::verify_items_real<false><<<vgrid, 256, ysm, st>>>(A, f);
+                else kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
+            }
         }
         XYZB_LAUNCH_CHECK();
         c.launches[XYZB_STAGE_VERIFY] += 1;

@@ -25,6 +25,12 @@ __device__ __forceinline__ u64 mt_temper(u64 z) {
     return z;
 }
 
+// fp64 -> fp32 copy (the response for the continuous-XY verify).
+__global__ void to_f32(const double* __restrict__ a, u64 n, float* __restrict__ b) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        b[i] = float(a[i]);
+}
+
 // Regenerate the 312-word state in place; all threads of the CTA call it.
 __device__ __forceinline__ void mt_twist(u64* x) {
     const u64 UM = 0xffffffff80000000ull, LM = 0x7fffffffull, A = 0xb5026f5aa96619e9ull;
