@@ -39,6 +39,7 @@
 #include "host_rng.hpp"
 #include "merge_kernels.cuh"
 #include "msplit_group.cuh"
+#include "part_group.cuh"
 #include "radix_sort.cuh"
 #include "run_sort.cuh"
 #include "real_kernels.cuh"
@@ -238,7 +239,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal, yreal32;
     // batch scratch
     DevBuf keys[2], vals[2], keys_x, hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -834,11 +835,19 @@ void run_batches(SearchCtx& c) {
     // p = 1e5; at M = 19, 20 every CTA streaming all keys costs more than the counting sort (config 4:
     // 102 vs 53 ms), so the kernel runs there only when forced (XYZB_GROUPING=msplit, also for sparse
     // runs; =cluster keeps the DSMEM-table kernel at M = 17)
-    const bool ms_path = M >= 17 && M <= 20 && !sort_sel && !gsel_is("sort") && !gsel_is("bucket") &&
+    // M >= 19 with a dense bucket space: partition pass + one small CTA per (run, partition)
+    // (XYZB_GROUPING=part forces it for any M <= 24)
+    const bool part_path = sizeof(K) == 4 && M >= 2 && M <= 24 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
+                           (gsel_is("part") || (!gsel && M >= 19));
+    if (part_path) {
+        ds->pgrp.ensure(kern::part_scratch_words(int(M), B) * 4);
+        ds->pent.ensure(cap * 8);
+    }
+    const bool ms_path = !part_path && M >= 17 && M <= 20 && !sort_sel && !gsel_is("sort") && !gsel_is("bucket") &&
                          !gsel_is("cluster") && sizeof(K) == 4 &&
                          ((M <= 18 && (u64(1) << M) <= 4 * p + 1024) || gsel_is("msplit")) &&
                          kern::msplit_schedulable(int(M));
-    const bool grouped_path = !ms_path && M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
+    const bool grouped_path = !part_path && !ms_path && M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
                               !(gsel && (std::string(gsel) == "sort" || std::string(gsel) == "bucket"));
     // 4 <= M <= 16: two CTAs per run (cluster), bucket space split on a key bit
     // (XYZB_GROUPING=cta keeps one CTA per run)
@@ -855,7 +864,7 @@ void run_batches(SearchCtx& c) {
         ds->slots.ensure(kSMs * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->slots.p, 0, kSMs * 4, st));
     }
-    const bool buckets = !grouped_path && !ms_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
+    const bool buckets = !part_path && !grouped_path && !ms_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
                          !(gsel && std::string(gsel) == "sort") && !sort_sel;
     if (buckets) {
         ds->bcnt.ensure((B << M) * 4);
@@ -931,7 +940,26 @@ void run_batches(SearchCtx& c) {
         const K* sorted_keys = nullptr;
         int vshift = 0;
         cudaEvent_t e2;
-        if (ms_path) {
+        if (part_path) {
+            // ---- group: partition pass (per-run partitions that hold both sides of every block) ----
+            if constexpr (sizeof(K) == 4) {
+                kern::part_partition_launch(k0, nb, p, int(M), ds->xorc.as<K>(), ds->tot.as<u64>(),
+                                            ds->work_run.as<u64>(), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st);
+                c.launches[XYZB_STAGE_SORT] += 3;
+                e2 = clk.mark();
+                clk.span(XYZB_STAGE_SORT, e1, e2);
+                c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);
+                // ---- join: per (run, partition) bucket tables in shared memory; |E_r|, guard, blocks ----
+                kern::part_join_launch(nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0], ds->tot.as<u64>(),
+                                       ds->work_run.as<u64>(), ds->items.as<kern::Item>(), nitems,
+                                       static_cast<u32>(item_cap), npairs_b, ds->pairs.as<kern::PairRec>(),
+                                       static_cast<u32>(c.pair_cap), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st);
+                c.launches[XYZB_STAGE_JOIN] += 2;
+            } else {
+                throw internal_error("xyzb: partitioned grouping needs 32-bit keys");
+            }
+            sv = vb[0];
+        } else if (ms_path) {
             // ---- group + join fused: 2^(M-16) CTAs per run, 16-bit tables split by parities of c's zero bits ----
             if constexpr (sizeof(K) == 4) {
                 if (!kern::msplit_group_join_launch(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
@@ -1094,7 +1122,7 @@ void run_batches(SearchCtx& c) {
         A.guard = c.guard;
         A.sv = sv;
         A.S = p;
-        const bool unsorted = buckets || grouped_path || ms_path;
+        const bool unsorted = buckets || grouped_path || ms_path || part_path;
         A.vkeys = unsorted ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
         A.vkeys_by_pos = unsorted ? 0 : 1;
         A.xkeys = unsorted ? static_cast<const void*>(k0) : ds->keys_x.p;

@@ -1,0 +1,562 @@
+// Partitioned grouping + join (sm_100a): one partition pass over the keys,
+// then one small CTA per (run, partition) with its bucket table in shared
+// memory.
+//
+// equal_pairs (pair_search.cpp:12-55) groups the x-keys v of a run and pairs
+// group v with group v ^ c (c = x-key ^ z-key of every column, A.3). An
+// invertible GF(2)-linear map w = T(v) with T(c) = e_0 makes the partner of
+// w simply w ^ 1, so the top k bits of w name a partition that holds both
+// sides of every block, and within it the partner bucket is the neighbour:
+//   T(v) = swap_{0,t}(v ^ (v_t ? c ^ e_t : 0)),  t = lowest set bit of c
+// (c ^ e_t has bit t clear, so v -> v ^ (v_t ? c ^ e_t : 0) is an involution
+// mapping c to e_t; the bit swap moves e_t to e_0). c == 0 (diagonal blocks,
+// every group paired with itself) keeps T = identity.
+//
+//   part_count    per tile of keys: per-warp shared histograms of the k-bit
+//                 partition digit -> per-run partition sizes (global atomics)
+//   part_scan     per run: exclusive scan of the 2^k sizes -> partition
+//                 starts and cursors
+//   part_scatter  per tile: one shared atomic per key (rank in its warp's
+//                 digit counter), one global atomic per (tile, digit) ->
+//                 (w, column) entries in partition order
+//   part_join<0>  per (run, partition): bucket counts of the 2^lb local
+//                 buckets in shared memory -> |E_r| incl. the diagonal and
+//                 the canonical work (guard, pair_search.hpp:91-94)
+//   part_join<1>  per (run, partition) of a kept run: counts, scan, scatter of
+//                 the columns into the run's grouped array, then the blocks
+//                 (pairs of small blocks written warp-cooperatively, items for
+//                 large ones) exactly as the fused kernels emit them.
+// The order inside a bucket is not deterministic (atomics); nothing depends on
+// it: pair-list hits carry columns and the merge orders hits by (rid, v, j, k).
+#pragma once
+
+#include "common.cuh"
+#include "cta_group.cuh"
+#include "search_kernels.cuh"
+
+namespace xyzb {
+namespace kern {
+
+constexpr int kPgThreads = 512;
+constexpr int kPgPerThread = 8;
+constexpr int kPjThreads = 512;   // partition join CTA
+constexpr int kPjPerThread = 8;   // entries per thread kept in registers
+constexpr u32 kPgTile = kPgThreads * kPgPerThread;  // keys per tile of the partition passes
+constexpr int kPgMaxK = 10;                          // partition digits: at most 1024 partitions per run
+
+// Local bucket bits: 2^lb u32 counters per partition CTA (16 KB at lb = 12).
+inline int part_local_bits(int M) { return M - 12 > kPgMaxK ? M - kPgMaxK : (M > 13 ? 12 : M - 1); }
+inline int part_digits(int M) { return M - part_local_bits(M); }
+
+struct PartMap {
+    u32 c, cm, t;
+    __device__ __forceinline__ PartMap(u32 c_) : c(c_), cm(0), t(0) {
+        if (c) {
+            t = u32(__ffs(int(c)) - 1);
+            cm = c ^ (1u << t);
+        }
+    }
+    __device__ __forceinline__ u32 fwd(u32 v) const {
+        if (!c) return v;
+        u32 x = v ^ (((v >> t) & 1u) ? cm : 0u);
+        const u32 d = (x ^ (x >> t)) & 1u;
+        return x ^ (d | (d << t));
+    }
+    __device__ __forceinline__ u32 inv(u32 w) const {
+        if (!c) return w;
+        const u32 d = (w ^ (w >> t)) & 1u;
+        const u32 x = w ^ (d | (d << t));
+        return x ^ (((x >> t) & 1u) ? cm : 0u);
+    }
+};
+
+// --------------------------------------------------------- block emission --
+
+// Pass 2 of a join over T local buckets, warp-cooperative: the pairs of small
+// blocks (<= kInlinePairs) are written by the whole warp, one coalesced
+// 16-byte record per lane; large blocks become items (their pairs expanded
+// later at it.pad). Every thread of the CTA calls it; thread u-major order
+// must match the counting pass that produced ibase / pbase.
+template <class BlockOf>
+__device__ __forceinline__ void emit_blocks_coop(BlockOf block_of, u32 T, u32 b, u32 hmax, u64 p, bool pair_list,
+                                                 u32 ibase, u32 pbase, Item* __restrict__ items, u32 item_cap,
+                                                 PairRec* __restrict__ pairs, u32 pair_cap,
+                                                 const u32* __restrict__ grouped) {
+    const int lane = threadIdx.x & 31;
+    u32 woff = __shfl_sync(0xffffffffu, pbase, 0);
+    const u32 off = u32(u64(b) * p);
+    uint4* dst = reinterpret_cast<uint4*>(pairs);
+    for (u32 li0 = 0; li0 < T; li0 += blockDim.x) {
+        const u32 li = li0 + threadIdx.x;
+        HeadBlock hb;
+        if (li < T) hb = block_of(li);
+        u32 ne, np, nsc;
+        emit_count(hb, hmax, pair_list, ne, np, nsc);
+        const bool inl = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
+        const u32 ni = inl ? np : 0u;
+        u32 ea = np, ei = ni;  // inclusive warp scans of all pairs / inline pairs
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t1 = __shfl_up_sync(0xffffffffu, ea, o), t2 = __shfl_up_sync(0xffffffffu, ei, o);
+            if (lane >= o) {
+                ea += t1;
+                ei += t2;
+            }
+        }
+        const u32 tot_all = __shfl_sync(0xffffffffu, ea, 31), tot_inl = __shfl_sync(0xffffffffu, ei, 31);
+        const u32 xa = ea - np;
+        if (ne) {
+            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, woff + xa, items, item_cap, pairs, pair_cap, p,
+                       grouped);
+            ibase += ne;
+        }
+        if (__all_sync(0xffffffffu, ni <= 1u)) {  // single-pair blocks (sparse tables): each lane writes its own
+            if (ni) {
+                const u32 slot = woff + xa;
+                if (slot < pair_cap) {
+                    const bool diag = hb.flags & 2u;  // a one-pair diagonal block: its two columns
+                    const u32 hcol = grouped[off + hb.hs], scol = grouped[off + hb.ss + (diag ? 1u : 0u)];
+                    const bool first_held = diag || (hb.flags & 1u);
+                    dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, hb.flags);
+                }
+            }
+            woff += tot_all;
+            continue;
+        }
+        for (u32 idx0 = 0; idx0 < tot_inl; idx0 += 32) {
+            const u32 idx = idx0 + lane;
+            u32 ow = 0;  // owner lane: the first lane whose inclusive inline count exceeds idx
+#pragma unroll
+            for (int stp = 16; stp > 0; stp >>= 1) {
+                const u32 v = __shfl_sync(0xffffffffu, ei, int(ow + stp - 1));
+                if (v <= idx) ow += stp;
+            }
+            ow = min(ow, 31u);
+            const u32 o_hs = __shfl_sync(0xffffffffu, hb.hs, ow), o_hc = __shfl_sync(0xffffffffu, hb.hc, ow);
+            const u32 o_ss = __shfl_sync(0xffffffffu, hb.ss, ow), o_sc = __shfl_sync(0xffffffffu, hb.sc, ow);
+            const u32 o_fl = __shfl_sync(0xffffffffu, hb.flags, ow);
+            const u32 o_xa = __shfl_sync(0xffffffffu, xa, ow);
+            const u32 o_ei = __shfl_sync(0xffffffffu, ei - ni, ow);
+            if (idx < tot_inl) {
+                u32 l = idx - o_ei, h = 0, q;
+                const bool diag = o_fl & 2u;
+                if (diag) {
+                    while (l >= o_hc - 1 - h) {
+                        l -= o_hc - 1 - h;
+                        ++h;
+                    }
+                    q = h + 1 + l;
+                } else {
+                    // l < 32, o_sc <= 32: the fp32 quotient of l + 0.5 is at least 1/64 from an integer
+                    h = __float2uint_rz((float(l) + 0.5f) * __frcp_rn(float(o_sc)));
+                    q = l - h * o_sc;
+                }
+                const u32 slot = woff + o_xa + (idx - o_ei);
+                if (slot < pair_cap) {
+                    const u32 hcol = grouped[off + o_hs + h], scol = grouped[off + o_ss + q];
+                    const bool first_held = diag || (o_fl & 1u);
+                    dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, o_fl);
+                }
+            }
+        }
+        woff += tot_all;
+    }
+}
+
+// ---------------------------------------------------------- partition pass --
+
+// Entries of the partitioned keys: (w, column) as one 8-byte record.
+template <bool SCATTER>
+__device__ __forceinline__ void part_tile(const u32* __restrict__ keys, u64 p, int M, int lb,
+                                          const u32* __restrict__ xorc, u32* __restrict__ pcnt,
+                                          u32* __restrict__ cursor, uint2* __restrict__ pe) {
+    extern __shared__ u32 hist[];  // [nwarps][2^k]
+    const int k = M - lb;
+    const u32 D = 1u << k;
+    const u32 b = blockIdx.y;
+    const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const u32 mask = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
+    const PartMap pm(xorc[b] & mask);
+    for (u32 i = threadIdx.x; i < D * nw; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const u64 t0 = u64(blockIdx.x) * kPgTile;
+    const u32* kb = keys + u64(b) * p;
+    u32 w[kPgPerThread], rk[kPgPerThread];
+    u32* hw = hist + wid * D;
+#pragma unroll
+    for (int q = 0; q < kPgPerThread; ++q) {
+        const u64 i = t0 + u64(q) * blockDim.x + threadIdx.x;
+        w[q] = i < p ? pm.fwd(__ldg(kb + i) & mask) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kPgPerThread; ++q) {
+        const u64 i = t0 + u64(q) * blockDim.x + threadIdx.x;
+        if (i < p) rk[q] = atomicAdd(hw + (w[q] >> lb), 1u);
+    }
+    __syncthreads();
+    if constexpr (!SCATTER) {
+        for (u32 d = threadIdx.x; d < D; d += blockDim.x) {
+            u32 s = 0;
+            for (int v = 0; v < nw; ++v) s += hist[v * D + d];
+            if (s) atomicAdd(pcnt + u64(b) * D + d, s);
+        }
+    } else {
+        // per digit: reserve the tile's range, then per-warp exclusive offsets
+        for (u32 d = threadIdx.x; d < D; d += blockDim.x) {
+            u32 s = 0;
+            for (int v = 0; v < nw; ++v) s += hist[v * D + d];
+            u32 base = s ? atomicAdd(cursor + u64(b) * D + d, s) : 0u;
+            for (int v = 0; v < nw; ++v) {
+                const u32 x = hist[v * D + d];
+                hist[v * D + d] = base;
+                base += x;
+            }
+        }
+        __syncthreads();
+        uint2* out = pe + u64(b) * p;
+#pragma unroll
+        for (int q = 0; q < kPgPerThread; ++q) {
+            const u64 i = t0 + u64(q) * blockDim.x + threadIdx.x;
+            if (i < p) out[hw[w[q] >> lb] + rk[q]] = make_uint2(w[q], u32(i));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPgThreads) part_count(const u32* __restrict__ keys, u64 p, int M, int lb,
+                                                         const u32* __restrict__ xorc, u32* __restrict__ pcnt) {
+    part_tile<false>(keys, p, M, lb, xorc, pcnt, nullptr, nullptr);
+}
+
+__global__ void __launch_bounds__(kPgThreads) part_scatter(const u32* __restrict__ keys, u64 p, int M, int lb,
+                                                           const u32* __restrict__ xorc, u32* __restrict__ cursor,
+                                                           uint2* __restrict__ pe) {
+    part_tile<true>(keys, p, M, lb, xorc, nullptr, cursor, pe);
+}
+
+// One CTA per run: pbeg[b][d] = run-local start of partition d (pbeg[b][D] = p);
+// cursor[b][d] = pbeg[b][d]; tot / work_run of the run cleared.
+__global__ void __launch_bounds__(1024) part_scan(const u32* __restrict__ pcnt, int k, u64 p, u32* __restrict__ pbeg,
+                                                  u32* __restrict__ cursor, u64* __restrict__ tot,
+                                                  u64* __restrict__ work_run) {
+    __shared__ u32 ws[33];
+    const u32 D = 1u << k, b = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u32 x = threadIdx.x < D ? pcnt[u64(b) * D + threadIdx.x] : 0u;
+    u32 incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const u32 v = lane < int(blockDim.x >> 5) ? ws[lane] : 0u;
+        u32 vi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) vi += t;
+        }
+        ws[lane] = vi - v;
+    }
+    __syncthreads();
+    const u32 ex = ws[wid] + incl - x;
+    if (threadIdx.x < D) {
+        pbeg[u64(b) * (D + 1) + threadIdx.x] = ex;
+        cursor[u64(b) * D + threadIdx.x] = ex;
+    }
+    if (threadIdx.x == 0) {
+        pbeg[u64(b) * (D + 1) + D] = u32(p);
+        tot[b] = 0;
+        work_run[b] = 0;
+    }
+}
+
+// --------------------------------------------------------- partition join --
+
+// Exclusive scan of the n counters in place (each warp owns a contiguous
+// segment walked in conflict-free 32-word steps): counters -> bucket starts.
+__device__ __forceinline__ void part_table_scan(u32* T, u32 n, u32* ws) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u32 nw = blockDim.x >> 5;
+    const u32 seg = max(32u, (n + nw - 1) / nw);
+    const u32 s0 = min(n, u32(wid) * seg), s1 = min(n, s0 + seg);
+    u32 loc = 0;
+    for (u32 i = s0 + lane; i < s1; i += 32) loc += T[i];
+    loc = warp_sum(loc);
+    if (lane == 0) ws[wid] = loc;
+    __syncthreads();
+    if (wid == 0) {
+        const u32 t = u32(lane) < nw ? ws[lane] : 0u;
+        u32 incl = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        ws[lane] = incl - t;
+    }
+    __syncthreads();
+    u32 carry = ws[wid];
+    for (u32 i0 = s0; i0 < s1; i0 += 32) {
+        const u32 i = i0 + lane;
+        const u32 x = i < s1 ? T[i] : 0u;
+        u32 incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (i < s1) T[i] = carry + incl - x;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncthreads();
+}
+
+template <int EMIT>
+__global__ void __launch_bounds__(kPjThreads) part_join(const uint2* __restrict__ pe, const u32* __restrict__ pbeg,
+                                                        u64 p, int M, int lb, const u32* __restrict__ xorc, u64 guard,
+                                                        u32 hmax, u32* __restrict__ grouped, u64* __restrict__ tot,
+                                                        u64* __restrict__ work_run, Item* __restrict__ items,
+                                                        u32* __restrict__ nitems, u32 item_cap,
+                                                        u32* __restrict__ npairs, PairRec* __restrict__ pairs,
+                                                        u32 pair_cap) {
+    extern __shared__ __align__(16) u32 T[];  // 2^lb local buckets
+    __shared__ u32 ws[68];
+    __shared__ u64 red[2][kPjThreads / 32];
+    const u32 b = blockIdx.y, d = blockIdx.x;
+    const int k = M - lb;
+    const u32 D = 1u << k, L = 1u << lb, lmask = L - 1u;
+    const u32 mask = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
+    const u32 c = xorc[b] & mask;
+    if (EMIT && tot[b] > guard) return;  // aborted run: nothing to emit (uniform per CTA)
+    const u32 beg = pbeg[u64(b) * (D + 1) + d], end = pbeg[u64(b) * (D + 1) + d + 1];
+    const u32 cnt = end - beg;
+    const uint2* e = pe + u64(b) * p + beg;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (cnt < 2) {
+        // no block with work; a lone column of a c == 0 run still counts its
+        // diagonal pair in |E_r| (pair_search.cpp:48-49)
+        if (!EMIT && c == 0 && threadIdx.x == 0 && cnt == 1)
+            atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), 1ull);
+        return;
+    }
+    for (u32 i = threadIdx.x; i < L; i += blockDim.x) T[i] = 0;
+    __syncthreads();
+    // entries of the partition: in registers when they fit (the count's atomic
+    // returns each entry's rank in its bucket, so the scatter needs no second
+    // pass), else two streaming passes
+    const bool inreg = cnt <= kPjPerThread * blockDim.x;
+    uint2 v[kPjPerThread];
+    u32 rk[kPjPerThread];
+    if (inreg) {
+#pragma unroll
+        for (int q = 0; q < kPjPerThread; ++q) {
+            const u32 i = q * blockDim.x + threadIdx.x;
+            v[q] = i < cnt ? __ldg(e + i) : make_uint2(0, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < kPjPerThread; ++q) {
+            const u32 i = q * blockDim.x + threadIdx.x;
+            if (i < cnt) rk[q] = atomicAdd(T + (v[q].x & lmask), 1u);
+        }
+    } else {
+        for (u32 i0 = 0; i0 < cnt; i0 += kPjPerThread * blockDim.x) {
+#pragma unroll
+            for (int q = 0; q < kPjPerThread; ++q) {
+                const u32 i = i0 + q * blockDim.x + threadIdx.x;
+                v[q].x = i < cnt ? __ldg(&e[i].x) : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < kPjPerThread; ++q) {
+                const u32 i = i0 + q * blockDim.x + threadIdx.x;
+                if (i < cnt) atomicAdd(T + (v[q].x & lmask), 1u);
+            }
+        }
+    }
+    __syncthreads();
+    // c != 0: buckets u (even) and u | 1 form one block; c == 0: every bucket
+    // is a diagonal block. li walks the block heads.
+    const u32 NL = c ? L / 2 : L;
+    if (!EMIT) {
+        u64 pa = 0, wa = 0;
+        for (u32 li = threadIdx.x; li < NL; li += blockDim.x) {
+            if (c == 0) {
+                const u64 cx = T[li];
+                pa += cx * cx;
+                wa += cx ? cx * (cx - 1) / 2 : 0;
+            } else {
+                const uint2 t2 = reinterpret_cast<const uint2*>(T)[li];
+                pa += 2ull * t2.x * t2.y;
+                wa += u64(t2.x) * t2.y;
+            }
+        }
+        pa = warp_sum(pa);
+        wa = warp_sum(wa);
+        if (lane == 0) {
+            red[0][wid] = pa;
+            red[1][wid] = wa;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u64 a = 0, w = 0;
+            for (int q = 0; q < nw; ++q) {
+                a += red[0][q];
+                w += red[1][q];
+            }
+            if (a) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(a));
+            if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
+        }
+        return;
+    }
+    // bucket starts, scatter (T ends as bucket ends), then the blocks
+    part_table_scan(T, L, ws);
+    const u64 off = u64(b) * p;
+    if (inreg) {
+#pragma unroll
+        for (int q = 0; q < kPjPerThread; ++q) {
+            const u32 i = q * blockDim.x + threadIdx.x;
+            if (i < cnt) grouped[off + beg + T[v[q].x & lmask] + rk[q]] = v[q].y;
+        }
+        __syncthreads();
+    } else {
+        for (u32 i0 = 0; i0 < cnt; i0 += kPjPerThread * blockDim.x) {
+#pragma unroll
+            for (int q = 0; q < kPjPerThread; ++q) {
+                const u32 i = i0 + q * blockDim.x + threadIdx.x;
+                v[q] = i < cnt ? __ldg(e + i) : make_uint2(0, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < kPjPerThread; ++q) {
+                const u32 i = i0 + q * blockDim.x + threadIdx.x;
+                if (i < cnt) grouped[off + beg + atomicAdd(T + (v[q].x & lmask), 1u)] = v[q].y;
+            }
+        }
+        __syncthreads();
+    }
+    // inreg: T holds bucket starts (end of u = start of u + 1, the last ends at cnt);
+    // streaming: T holds bucket ends (start of u = end of u - 1)
+    const PartMap pm(c);
+    const u32 hi = d << lb;
+    auto group = [&](u32 u, u32& gb, u32& gc) {
+        u32 s0, s1;
+        if (inreg) {
+            s0 = T[u];
+            s1 = u + 1 < L ? T[u + 1] : cnt;
+        } else {
+            s1 = T[u];
+            s0 = u ? T[u - 1] : 0u;
+        }
+        gb = beg + s0;
+        gc = s1 - s0;
+    };
+    auto block_of = [&](u32 li) {
+        HeadBlock hb;
+        if (c == 0) {
+            u32 bx, cx;
+            group(li, bx, cx);
+            if (cx >= 2) {
+                hb.pairs = u64(cx) * cx;
+                hb.work = u64(cx) * (cx - 1) / 2;
+                hb.hs = bx; hb.hc = cx; hb.ss = bx; hb.sc = cx; hb.flags = 3u;
+            }
+            return hb;
+        }
+        const u32 u = 2 * li;
+        // buckets u and u | 1 hold keys v and v ^ c; the block belongs to the
+        // smaller key, whose group is the x side (pair_search.cpp:35-53)
+        const u32 ve = pm.inv(hi | u);
+        const bool even_x = ve < (ve ^ c);
+        u32 bx, cx, bz, cz;
+        group(even_x ? u : (u | 1u), bx, cx);
+        group(even_x ? (u | 1u) : u, bz, cz);
+        if (cx && cz) {
+            hb.pairs = 2ull * cx * cz;
+            hb.work = u64(cx) * cz;
+            if (cx <= cz) {
+                hb.hs = bx; hb.hc = cx; hb.ss = bz; hb.sc = cz; hb.flags = 1u;
+            } else {
+                hb.hs = bz; hb.hc = cz; hb.ss = bx; hb.sc = cx; hb.flags = 0u;
+            }
+        }
+        return hb;
+    };
+    const bool pair_list = npairs != nullptr;
+    u32 my_items = 0, my_pairs = 0;
+    for (u32 li = threadIdx.x; li < NL; li += blockDim.x) {
+        const HeadBlock hb = block_of(li);
+        u32 ne, np, nsc;
+        emit_count(hb, hmax, pair_list, ne, np, nsc);
+        my_items += ne;
+        my_pairs += np;
+    }
+    u32 ti, tp;
+    u32 ibase = block_exclusive(my_items, ws, &ti);
+    u32 pbase = block_exclusive(my_pairs, ws + 33, &tp);
+    if (ti == 0 && tp == 0) return;
+    if (threadIdx.x == 0) {
+        ws[66] = ti ? atomicAdd(nitems, ti) : 0u;
+        ws[67] = (pair_list && tp) ? atomicAdd(npairs, tp) : 0u;
+    }
+    __syncthreads();
+    ibase += ws[66];
+    pbase += ws[67];
+    emit_blocks_coop(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped);
+}
+
+inline size_t part_tile_smem(int M) { return size_t(kPgThreads / 32) * (size_t(1) << part_digits(M)) * 4; }
+inline size_t part_join_smem(int M) { return (size_t(1) << part_local_bits(M)) * 4; }
+
+// The partitioned path (u32 keys, M <= 24). scratch: pcnt / cursor B * 2^k
+// u32, pbeg B * (2^k + 1) u32; pe: B * p (w, column) entries.
+inline u64 part_scratch_words(int M, u64 B) { return B * ((u64(1) << part_digits(M)) * 3 + 1); }
+
+inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, const u32* xorc, u64* tot, u64* work_run,
+                                  u32* scratch, uint2* pe, cudaStream_t st) {
+    const int lb = part_local_bits(M), k = M - lb;
+    const u64 D = u64(1) << k;
+    u32* pcnt = scratch;
+    u32* cursor = scratch + B * D;
+    u32* pbeg = scratch + 2 * B * D;
+    static bool attr = false;
+    if (!attr) {
+        XYZB_CUDA(cudaFuncSetAttribute(part_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+        XYZB_CUDA(cudaFuncSetAttribute(part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+        attr = true;
+    }
+    XYZB_CUDA(cudaMemsetAsync(pcnt, 0, B * D * 4, st));
+    dim3 gt(static_cast<u32>(ceil_div(p, kPgTile)), static_cast<u32>(B));
+    part_count<<<gt, kPgThreads, part_tile_smem(M), st>>>(keys, p, M, lb, xorc, pcnt);
+    XYZB_LAUNCH_CHECK();
+    part_scan<<<static_cast<u32>(B), 1024, 0, st>>>(pcnt, k, p, pbeg, cursor, tot, work_run);
+    XYZB_LAUNCH_CHECK();
+    part_scatter<<<gt, kPgThreads, part_tile_smem(M), st>>>(keys, p, M, lb, xorc, cursor, pe);
+    XYZB_LAUNCH_CHECK();
+}
+
+inline void part_join_launch(u64 B, u64 p, int M, const u32* xorc, u64 guard, u32 hmax, u32* grouped, u64* tot,
+                             u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
+                             u32 pair_cap, const u32* scratch, const uint2* pe, cudaStream_t st) {
+    const int lb = part_local_bits(M), k = M - lb;
+    const u64 D = u64(1) << k;
+    const u32* pbeg = scratch + 2 * B * D;
+    static bool attr = false;
+    if (!attr) {
+        XYZB_CUDA(cudaFuncSetAttribute(part_join<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+        XYZB_CUDA(cudaFuncSetAttribute(part_join<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+        attr = true;
+    }
+    dim3 gj(static_cast<u32>(D), static_cast<u32>(B));
+    part_join<0><<<gj, kPjThreads, part_join_smem(M), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
+                                                            work_run, items, nitems, item_cap, npairs, pairs,
+                                                            pair_cap);
+    XYZB_LAUNCH_CHECK();
+    part_join<1><<<gj, kPjThreads, part_join_smem(M), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
+                                                            work_run, items, nitems, item_cap, npairs, pairs,
+                                                            pair_cap);
+    XYZB_LAUNCH_CHECK();
+}
+
+} // namespace kern
+} // namespace xyzb

@@ -46,14 +46,15 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "sort", "segments", "merge_large"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments", "merge_large"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
 def test_search_matches_reference_fixture(name, grouping, monkeypatch):
     """All grouping paths: two CTAs per run splitting the 16-bit shared
     bucket table (default for 4 <= M <= 16), one CTA per run, the DSMEM
     cluster kernel, the multi-kernel counting sort into 2^M buckets, per-run
-    cluster radix sort, multi-kernel segmented radix sort."""
-    if grouping in ("sort", "bucket", "cluster", "cta"):
+    cluster radix sort, multi-kernel segmented radix sort, partition pass +
+    per-(run, partition) tables."""
+    if grouping in ("sort", "bucket", "cluster", "cta", "part"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
@@ -194,7 +195,7 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "sort", "segments"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments"])
 def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
@@ -202,7 +203,7 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
     cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=10)
     base = xb.Dataset(x).search(y, cfg)
-    if grouping in ("sort", "bucket", "cluster", "cta"):
+    if grouping in ("sort", "bucket", "cluster", "cta", "part"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
@@ -374,12 +375,12 @@ def test_xyz1_file_ingest_matches_in_memory_and_reference_errors(tmp_path):
         xb.Dataset.open(tmp_path / "missing.xyz")
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "part"])
 def test_bucket_above_16_bits_falls_back_exactly(grouping, monkeypatch):
     """p > 65535 with 70000 identical (monomorphic) columns: one bucket holds
     more columns than a 16-bit shared counter can; the CTA grouping redoes
     such a run with 32-bit counters. Hits and counters equal the reference."""
-    if grouping in ("cluster", "cta"):
+    if grouping in ("cluster", "cta", "part"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     xb = _engine()
     rng = np.random.default_rng(11)
@@ -422,12 +423,12 @@ def test_dirty_padding_bits_are_rejected_on_upload():
         xb.Dataset(x).search(y, cfg))
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "part"])
 def test_constant_response_partner_is_the_complement(grouping, monkeypatch):
     """y constant: in the negative pass c = x-key ^ z-key has every bit set, so
     each key's partner is its complement (no key bit is shared by a key and
     its partner: the two-CTA split reads the partner half through DSMEM)."""
-    if grouping in ("cluster", "cta"):
+    if grouping in ("cluster", "cta", "part"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     xb = _engine()
     x, _ = ck.ref_planted(300, 400, 3, 7, 0.9, 3)
@@ -443,12 +444,12 @@ def test_constant_response_partner_is_the_complement(grouping, monkeypatch):
         assert len(want.hits) > 0
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "part"])
 def test_grouping_kernels_sweep_vs_oracle(grouping, monkeypatch):
     """The fused group + join kernels (two-CTA split, one CTA, DSMEM cluster)
     over the M range they serve (4..17) and p from a handful of columns to
     2^M-sized tables: bit-exact against the restatement."""
-    if grouping in ("cta", "cluster"):
+    if grouping in ("cta", "cluster", "part"):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     xb = _engine()
     rng = np.random.default_rng(7)
@@ -515,6 +516,49 @@ def test_msplit_grouping_vs_oracle(case, monkeypatch):
         x = ck.ref_rademacher(n, p, 500 + t, 3)
         y = np.ones(n, np.int8) if case == "constant_y" else np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
         cfg = xb.SearchConfig(m=m, l=2, gamma=0.72, seed=t, threads=1, top_k=20, estimate_complexity=False)
+        got = xb.Dataset(x).search(y, cfg)
+        want = ck.oracle_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, (m, p, msg)
+        assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
+            want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
+
+
+@pytest.mark.parametrize("case", ["dense", "forced_low_m", "constant_y", "guard", "biased"])
+def test_partition_grouping_vs_oracle(case, monkeypatch):
+    """The partitioned path (default for M >= 19 with a dense bucket space):
+    a partition pass on the top bits of T(v) (T linear, T(c) = e_0, so a key
+    and its partner share a partition and are neighbouring local buckets),
+    then one CTA per (run, partition). M = 19..22 by default, M = 4..18
+    forced, a constant response (c = all ones), runs the guard aborts, and
+    heavily biased columns (skewed partitions). Bit-exact against the
+    restatement."""
+    xb = _engine()
+    rng = np.random.default_rng(23)
+    guard = None
+    if case == "dense":
+        cases = [(19, 140000), (20, 270000), (21, 600000), (22, 1100000)]
+    elif case == "forced_low_m":
+        monkeypatch.setenv("XYZB_GROUPING", "part")
+        cases = [(4, 20), (7, 300), (12, 2000), (13, 5000), (14, 9000), (16, 20000), (18, 70000)]
+    elif case == "constant_y":
+        cases = [(19, 140000), (20, 270000)]
+    elif case == "guard":
+        monkeypatch.setenv("XYZB_GROUPING", "part")
+        cases = [(14, 6000), (19, 140000)]
+        guard = 1
+    else:
+        cases = [(20, 270000)]
+    for t, (m, p) in enumerate(cases):
+        n = 64
+        if case == "biased":  # columns with few +1 rows: keys crowd the low buckets
+            signs = np.where(rng.random((n, p)) < rng.uniform(0.02, 0.5, p), 1, -1).astype(np.int8)
+            x = xb.PackedMatrix.from_signs(signs)
+        else:
+            x = ck.ref_rademacher(n, p, 900 + t, 3)
+        y = np.ones(n, np.int8) if case == "constant_y" else np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        cfg = xb.SearchConfig(m=m, l=2, gamma=0.72, seed=t, threads=1, top_k=20, estimate_complexity=False,
+                              max_candidates_per_rep=(p // 8 if guard else 0))
         got = xb.Dataset(x).search(y, cfg)
         want = ck.oracle_search(x, y, cfg)
         ok, msg = ck.same_hits(got, want)
