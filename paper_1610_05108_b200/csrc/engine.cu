@@ -40,6 +40,7 @@
 #include "merge_kernels.cuh"
 #include "msplit_group.cuh"
 #include "part_group.cuh"
+#include "tile_verify.cuh"
 #include "radix_sort.cuh"
 #include "run_sort.cuh"
 #include "real_kernels.cuh"
@@ -239,7 +240,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal, yreal32;
     // batch scratch
     DevBuf keys[2], vals[2], keys_x, hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent, pairs_t, tscratch, bstart;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -610,6 +611,8 @@ struct SearchCtx {
     u64 item_cap = 0, nbatches = 0, pair_cap = 0;
     u64 item_scale = 1;  // grows when a batch overflows its item buffer
     u64 pair_scale = 1;  // grows when a batch overflows its pair list
+    bool tiled = false;    // this attempt verifies the accumulated pair list in column tiles
+    bool no_tile = false;  // the accumulated list would exceed 2^32 pairs: per-batch verify
     RunPlan plan;
     xyzb_result* out;
     u64 launches[XYZB_NUM_STAGES] = {};
@@ -812,13 +815,34 @@ void run_batches(SearchCtx& c) {
     c.item_cap = item_cap;
     c.nbatches = nbatches;
     const bool pair_path = c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128;
+    // XYZB_TILED=1: the pair lists of all batches accumulate and are verified once, in
+    // L2-sized column tiles (tile_verify.cuh). Measured on B200 it does not pay (config 4:
+    // verify 95 -> 107 ms): random 1.3 KB column gathers confined to a 63 MB window run at
+    // 8.3 TB/s against 7.1 TB/s over all of X (tools/l2_window.cu), so it stays opt-in.
+    const char* tsel = std::getenv("XYZB_TILED");
+    const bool tiled = pair_path && !c.no_tile && nbatches <= tile::kMaxBatches && tsel && std::string(tsel) == "1";
+    c.tiled = tiled;
     if (pair_path) {
-        c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, B * p) * c.pair_scale);
+        c.pair_cap = std::min<u64>(0xffffffffull,
+                                   std::max<u64>(u64(1) << 20, tiled ? R * p / 2 : B * p) * c.pair_scale);
         if (const char* e = std::getenv("XYZB_PAIR_CAP"))  // tests force the pair-list regrow path with it
             c.pair_cap = std::min<u64>(c.pair_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.pair_scale);
         ds->pairs.ensure(c.pair_cap * sizeof(kern::PairRec));
         ds->npairs.ensure(nbatches * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->npairs.p, 0, nbatches * 4, st));
+    }
+    tile::Plan tplan;
+    if (tiled) {
+        ds->pairs_t.ensure(c.pair_cap * sizeof(kern::PairRec));
+        int dev = 0, l2 = 0;
+        XYZB_CUDA(cudaGetDevice(&dev));
+        XYZB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+        u64 l2b = u64(l2);
+        if (const char* e = std::getenv("XYZB_TILE_L2")) l2b = std::max<u64>(1, std::strtoull(e, nullptr, 10));  // tests
+        tplan = tile::plan(p, ds->Wp * 8, l2b);
+        ds->tscratch.ensure(tile::hist_words(tplan) * 4);
+        ds->bstart.ensure((nbatches + 1) * 4);
+        XYZB_CUDA(cudaMemsetAsync(ds->bstart.p, 0, 4, st));
     }
     const u32 hmax = 8u;  // held columns per item (pair expansion chunks)
     // grouping: counting sort into 2^M buckets when 2^M is comparable to p
@@ -840,7 +864,7 @@ void run_batches(SearchCtx& c) {
     const bool part_path = sizeof(K) == 4 && M >= 2 && M <= 24 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
                            (gsel_is("part") || (!gsel && M >= 19));
     if (part_path) {
-        ds->pgrp.ensure(kern::part_scratch_words(int(M), B) * 4);
+        ds->pgrp.ensure(kern::part_scratch_words(int(M), p, B) * 4);
         ds->pent.ensure(cap * 8);
     }
     const bool ms_path = !part_path && M >= 17 && M <= 20 && !sort_sel && !gsel_is("sort") && !gsel_is("bucket") &&
@@ -935,7 +959,7 @@ void run_batches(SearchCtx& c) {
         K* kb[2] = {ds->keys[0].as<K>(), ds->keys[1].as<K>()};
         u32* vb[2] = {ds->vals[0].as<u32>(), ds->vals[1].as<u32>()};
         u32* nitems = ds->nblocks.as<u32>() + batch_idx;
-        u32* npairs_b = pair_path ? ds->npairs.as<u32>() + batch_idx : nullptr;
+        u32* npairs_b = pair_path ? ds->npairs.as<u32>() + (tiled ? 0 : batch_idx) : nullptr;  // tiled: one list
         const u32* sv = nullptr;
         const K* sorted_keys = nullptr;
         int vshift = 0;
@@ -1134,14 +1158,39 @@ void run_batches(SearchCtx& c) {
         A.hits = ds->hits.as<kern::DevHit>();
         A.hit_count = ds->hit_count.as<u32>();
         A.hit_cap = ds->hit_cap;
+        A.krows = nullptr;
+        A.kM = 0;
+        A.kXc = nullptr;
+        A.kWp = 0;
         u32 vgrid = kSMs * 8;
         if (const char* ev = std::getenv("XYZB_VGRID")) vgrid = static_cast<u32>(std::max(1ul, std::strtoul(ev, nullptr, 10)));
         if (pair_path) {
-            u32* np = ds->npairs.as<u32>() + batch_idx;
+            u32* np = ds->npairs.as<u32>() + (tiled ? 0 : batch_idx);
             kern::expand_pairs<<<vgrid, 256, 0, st>>>(A.items, A.nitems, A.item_cap, p, ds->pairs.as<kern::PairRec>(),
                                                       static_cast<u32>(c.pair_cap), sv);
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 1;
+            if (tiled) {  // the batch's slots end here; verify after the last batch
+                XYZB_CUDA(cudaMemcpyAsync(ds->bstart.as<u32>() + batch_idx + 1, np, 4, cudaMemcpyDeviceToDevice, st));
+                clk.span(XYZB_STAGE_JOIN, e3, clk.mark());
+                if (b0 + B < R) continue;
+                // ---- all batches: bucket the pair list by column tile, one verify over it ----
+                cudaEvent_t es0 = clk.mark();
+                tile::sort_by_tile(ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), tplan,
+                                   ds->bstart.as<u32>(), static_cast<u32>(nbatches), static_cast<u32>(B),
+                                   ds->tscratch.as<u32>(), ds->pairs_t.as<kern::PairRec>(), st,
+                                   &c.launches[XYZB_STAGE_JOIN]);
+                clk.span(XYZB_STAGE_JOIN, es0, clk.mark());
+                A.nitems = ds->nblocks.as<u32>();  // (an item overflow in any batch forces a retry anyway)
+                A.rid = ds->rid.as<u32>();
+                A.run_sign = ds->rsign.as<int8_t>();
+                A.xkeys = nullptr;  // hits recompute their key from the run's draws
+                A.krows = ds->rows.as<u32>();
+                A.kM = int(M);
+                A.kXc = ds->Xc.as<u64>();
+                A.kWp = static_cast<u32>(ds->Wp);
+            }
+            const kern::PairRec* vpairs = tiled ? ds->pairs_t.as<kern::PairRec>() : ds->pairs.as<kern::PairRec>();
             const u64 W2 = ds->Wp / 2;
             // team of G lanes, NIT 16-byte chunks of each column per lane; XYZB_VP_CHUNKS
             // (1/2/4) and XYZB_VERIFY=simple select measured variants
@@ -1156,14 +1205,14 @@ void run_batches(SearchCtx& c) {
             int G = 1;
             while (G < 32 && u64(G) * chunks < W2) G <<= 1;
             const int nit = static_cast<int>(ceil_div(W2, G));
-            const auto* PR = ds->pairs.as<kern::PairRec>();
+            const auto* PR = vpairs;
             const u32 pc = static_cast<u32>(c.pair_cap);
             const u64* X = ds->Xc.as<u64>();
             const u32 Wp = static_cast<u32>(ds->Wp);
             const u64* Y = ds->yk_bits.as<u64>();
             const u32 n32 = static_cast<u32>(c.n);
             cudaEvent_t ev0 = clk.mark();
-            clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
+            if (!tiled) clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
 #define XYZB_VP(GG, NN)                                                                                          \
     do {                                                                                                         \
         if (simple)                                                                                              \
@@ -1571,7 +1620,12 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             const u32* np = reinterpret_cast<const u32*>(hs + o_pairs);
             pneed = *std::max_element(np, np + nbt);
             if (pneed > c.pair_cap) {
-                if (c.pair_cap == 0xffffffffull) throw internal_error("xyzb: candidate pairs exceed 2^32 in one batch");
+                if (c.pair_cap == 0xffffffffull && c.tiled) {
+                    c.no_tile = true;  // the search's pairs exceed 2^32: per-batch verify
+                    c.pair_scale = 1;
+                } else if (c.pair_cap == 0xffffffffull)
+                    throw internal_error("xyzb: candidate pairs exceed 2^32 in one batch");
+                else
                 c.pair_scale *= std::max<u64>(2, ceil_div(pneed, c.pair_cap));
             }
         }

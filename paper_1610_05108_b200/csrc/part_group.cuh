@@ -30,6 +30,9 @@
 // it: pair-list hits carry columns and the merge orders hits by (rid, v, j, k).
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "cta_group.cuh"
 #include "search_kernels.cuh"
@@ -45,8 +48,18 @@ constexpr u32 kPgTile = kPgThreads * kPgPerThread;  // keys per tile of the part
 constexpr int kPgMaxK = 10;                          // partition digits: at most 1024 partitions per run
 
 // Local bucket bits: 2^lb u32 counters per partition CTA (16 KB at lb = 12).
-inline int part_local_bits(int M) { return M - 12 > kPgMaxK ? M - kPgMaxK : (M > 13 ? 12 : M - 1); }
-inline int part_digits(int M) { return M - part_local_bits(M); }
+// Partition digits k: the fewest that bring the mean partition (p / 2^k
+// entries) to kPjTarget, at least M - 14 (a 2^14-bucket table is 64 KB), at
+// most kPgMaxK and M - 1 (a key and its partner share a partition).
+constexpr u64 kPjTarget = 4096;
+inline int part_digits(int M, u64 p) {
+    u64 target = kPjTarget;
+    if (const char* e = std::getenv("XYZB_PART_TARGET")) target = std::max<u64>(1, std::strtoull(e, nullptr, 10));
+    int k = 1;
+    while (k < kPgMaxK && k < M - 1 && (p >> k) > target) ++k;
+    return std::min(std::max(k, M - 14), M - 1);
+}
+inline int part_local_bits(int M, u64 p) { return M - part_digits(M, p); }
 
 struct PartMap {
     u32 c, cm, t;
@@ -72,19 +85,21 @@ struct PartMap {
 
 // --------------------------------------------------------- block emission --
 
-// Pass 2 of a join over T local buckets, warp-cooperative: the pairs of small
-// blocks (<= kInlinePairs) are written by the whole warp, one coalesced
-// 16-byte record per lane; large blocks become items (their pairs expanded
-// later at it.pad). Every thread of the CTA calls it; thread u-major order
-// must match the counting pass that produced ibase / pbase.
+// Pass 2 of a join over T block heads. Every thread owns the contiguous item
+// and pair slot ranges its counting pass reserved (ibase / pbase, thread-major
+// head order). Large blocks become items (their pairs expanded later at
+// it.pad, from the global grouped array); a block of at most kLanePairs
+// inline pairs is written by its lane, a larger inline block (<= kInlinePairs)
+// by the whole warp, one 16-byte record per lane. Columns of grouped position
+// pos are read from gl[pos - gbias] (shared memory when the partition is
+// staged there).
+constexpr u32 kLanePairs = 4;
 template <class BlockOf>
 __device__ __forceinline__ void emit_blocks_coop(BlockOf block_of, u32 T, u32 b, u32 hmax, u64 p, bool pair_list,
                                                  u32 ibase, u32 pbase, Item* __restrict__ items, u32 item_cap,
                                                  PairRec* __restrict__ pairs, u32 pair_cap,
-                                                 const u32* __restrict__ grouped) {
+                                                 const u32* __restrict__ grouped, const u32* gl, u32 gbias) {
     const int lane = threadIdx.x & 31;
-    u32 woff = __shfl_sync(0xffffffffu, pbase, 0);
-    const u32 off = u32(u64(b) * p);
     uint4* dst = reinterpret_cast<uint4*>(pairs);
     for (u32 li0 = 0; li0 < T; li0 += blockDim.x) {
         const u32 li = li0 + threadIdx.x;
@@ -93,52 +108,32 @@ __device__ __forceinline__ void emit_blocks_coop(BlockOf block_of, u32 T, u32 b,
         u32 ne, np, nsc;
         emit_count(hb, hmax, pair_list, ne, np, nsc);
         const bool inl = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
-        const u32 ni = inl ? np : 0u;
-        u32 ea = np, ei = ni;  // inclusive warp scans of all pairs / inline pairs
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 t1 = __shfl_up_sync(0xffffffffu, ea, o), t2 = __shfl_up_sync(0xffffffffu, ei, o);
-            if (lane >= o) {
-                ea += t1;
-                ei += t2;
-            }
-        }
-        const u32 tot_all = __shfl_sync(0xffffffffu, ea, 31), tot_inl = __shfl_sync(0xffffffffu, ei, 31);
-        const u32 xa = ea - np;
+        const bool big = inl && np > kLanePairs;
         if (ne) {
-            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, woff + xa, items, item_cap, pairs, pair_cap, p,
-                       grouped);
+            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p, grouped);
             ibase += ne;
         }
-        if (__all_sync(0xffffffffu, ni <= 1u)) {  // single-pair blocks (sparse tables): each lane writes its own
-            if (ni) {
-                const u32 slot = woff + xa;
-                if (slot < pair_cap) {
-                    const bool diag = hb.flags & 2u;  // a one-pair diagonal block: its two columns
-                    const u32 hcol = grouped[off + hb.hs], scol = grouped[off + hb.ss + (diag ? 1u : 0u)];
-                    const bool first_held = diag || (hb.flags & 1u);
-                    dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, hb.flags);
+        if (inl && !big) {  // a few pairs: this lane writes them
+            const bool diag = hb.flags & 2u;
+            const bool first_held = diag || (hb.flags & 1u);
+            u32 slot = pbase;
+            for (u32 h = 0; h < hb.hc; ++h) {
+                const u32 hcol = gl[hb.hs + h - gbias];
+                for (u32 q = diag ? h + 1 : 0; q < hb.sc; ++q, ++slot) {
+                    const u32 scol = gl[hb.ss + q - gbias];
+                    if (slot < pair_cap)
+                        dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, hb.flags);
                 }
             }
-            woff += tot_all;
-            continue;
         }
-        for (u32 idx0 = 0; idx0 < tot_inl; idx0 += 32) {
-            const u32 idx = idx0 + lane;
-            u32 ow = 0;  // owner lane: the first lane whose inclusive inline count exceeds idx
-#pragma unroll
-            for (int stp = 16; stp > 0; stp >>= 1) {
-                const u32 v = __shfl_sync(0xffffffffu, ei, int(ow + stp - 1));
-                if (v <= idx) ow += stp;
-            }
-            ow = min(ow, 31u);
+        for (u32 bal = __ballot_sync(0xffffffffu, big); bal; bal &= bal - 1) {  // warp-written blocks
+            const int ow = __ffs(bal) - 1;
             const u32 o_hs = __shfl_sync(0xffffffffu, hb.hs, ow), o_hc = __shfl_sync(0xffffffffu, hb.hc, ow);
             const u32 o_ss = __shfl_sync(0xffffffffu, hb.ss, ow), o_sc = __shfl_sync(0xffffffffu, hb.sc, ow);
             const u32 o_fl = __shfl_sync(0xffffffffu, hb.flags, ow);
-            const u32 o_xa = __shfl_sync(0xffffffffu, xa, ow);
-            const u32 o_ei = __shfl_sync(0xffffffffu, ei - ni, ow);
-            if (idx < tot_inl) {
-                u32 l = idx - o_ei, h = 0, q;
+            const u32 o_np = __shfl_sync(0xffffffffu, np, ow), o_slot = __shfl_sync(0xffffffffu, pbase, ow);
+            if (u32(lane) < o_np) {
+                u32 l = lane, h = 0, q;
                 const bool diag = o_fl & 2u;
                 if (diag) {
                     while (l >= o_hc - 1 - h) {
@@ -151,15 +146,15 @@ __device__ __forceinline__ void emit_blocks_coop(BlockOf block_of, u32 T, u32 b,
                     h = __float2uint_rz((float(l) + 0.5f) * __frcp_rn(float(o_sc)));
                     q = l - h * o_sc;
                 }
-                const u32 slot = woff + o_xa + (idx - o_ei);
+                const u32 slot = o_slot + lane;
                 if (slot < pair_cap) {
-                    const u32 hcol = grouped[off + o_hs + h], scol = grouped[off + o_ss + q];
+                    const u32 hcol = gl[o_hs + h - gbias], scol = gl[o_ss + q - gbias];
                     const bool first_held = diag || (o_fl & 1u);
                     dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, o_fl);
                 }
             }
         }
-        woff += tot_all;
+        pbase += np;
     }
 }
 
@@ -413,13 +408,15 @@ __global__ void __launch_bounds__(kPjThreads) part_join(const uint2* __restrict_
     // bucket starts, scatter (T ends as bucket ends), then the blocks
     part_table_scan(T, L, ws);
     const u64 off = u64(b) * p;
+    u32* sg = T + L;  // the partition's grouped columns (in-register case)
     if (inreg) {
 #pragma unroll
         for (int q = 0; q < kPjPerThread; ++q) {
             const u32 i = q * blockDim.x + threadIdx.x;
-            if (i < cnt) grouped[off + beg + T[v[q].x & lmask] + rk[q]] = v[q].y;
+            if (i < cnt) sg[T[v[q].x & lmask] + rk[q]] = v[q].y;
         }
         __syncthreads();
+        for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) grouped[off + beg + i] = sg[i];  // coalesced
     } else {
         for (u32 i0 = 0; i0 < cnt; i0 += kPjPerThread * blockDim.x) {
 #pragma unroll
@@ -502,19 +499,24 @@ __global__ void __launch_bounds__(kPjThreads) part_join(const uint2* __restrict_
     __syncthreads();
     ibase += ws[66];
     pbase += ws[67];
-    emit_blocks_coop(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped);
+    if (inreg)
+        emit_blocks_coop(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped,
+                         sg, beg);
+    else
+        emit_blocks_coop(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped,
+                         grouped + off, 0u);
 }
 
-inline size_t part_tile_smem(int M) { return size_t(kPgThreads / 32) * (size_t(1) << part_digits(M)) * 4; }
-inline size_t part_join_smem(int M) { return (size_t(1) << part_local_bits(M)) * 4; }
+inline size_t part_tile_smem(int k) { return size_t(kPgThreads / 32) * (size_t(1) << k) * 4; }
+inline size_t part_join_smem(int lb) { return ((size_t(1) << lb) + kPjThreads * kPjPerThread) * 4; }
 
 // The partitioned path (u32 keys, M <= 24). scratch: pcnt / cursor B * 2^k
 // u32, pbeg B * (2^k + 1) u32; pe: B * p (w, column) entries.
-inline u64 part_scratch_words(int M, u64 B) { return B * ((u64(1) << part_digits(M)) * 3 + 1); }
+inline u64 part_scratch_words(int M, u64 p, u64 B) { return B * ((u64(1) << part_digits(M, p)) * 3 + 1); }
 
 inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, const u32* xorc, u64* tot, u64* work_run,
                                   u32* scratch, uint2* pe, cudaStream_t st) {
-    const int lb = part_local_bits(M), k = M - lb;
+    const int lb = part_local_bits(M, p), k = M - lb;
     const u64 D = u64(1) << k;
     u32* pcnt = scratch;
     u32* cursor = scratch + B * D;
@@ -527,18 +529,18 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, const u3
     }
     XYZB_CUDA(cudaMemsetAsync(pcnt, 0, B * D * 4, st));
     dim3 gt(static_cast<u32>(ceil_div(p, kPgTile)), static_cast<u32>(B));
-    part_count<<<gt, kPgThreads, part_tile_smem(M), st>>>(keys, p, M, lb, xorc, pcnt);
+    part_count<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, xorc, pcnt);
     XYZB_LAUNCH_CHECK();
     part_scan<<<static_cast<u32>(B), 1024, 0, st>>>(pcnt, k, p, pbeg, cursor, tot, work_run);
     XYZB_LAUNCH_CHECK();
-    part_scatter<<<gt, kPgThreads, part_tile_smem(M), st>>>(keys, p, M, lb, xorc, cursor, pe);
+    part_scatter<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, xorc, cursor, pe);
     XYZB_LAUNCH_CHECK();
 }
 
 inline void part_join_launch(u64 B, u64 p, int M, const u32* xorc, u64 guard, u32 hmax, u32* grouped, u64* tot,
                              u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
                              u32 pair_cap, const u32* scratch, const uint2* pe, cudaStream_t st) {
-    const int lb = part_local_bits(M), k = M - lb;
+    const int lb = part_local_bits(M, p), k = M - lb;
     const u64 D = u64(1) << k;
     const u32* pbeg = scratch + 2 * B * D;
     static bool attr = false;
@@ -548,11 +550,11 @@ inline void part_join_launch(u64 B, u64 p, int M, const u32* xorc, u64 guard, u3
         attr = true;
     }
     dim3 gj(static_cast<u32>(D), static_cast<u32>(B));
-    part_join<0><<<gj, kPjThreads, part_join_smem(M), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
+    part_join<0><<<gj, kPjThreads, (size_t(1) << lb) * 4, st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
                                                             work_run, items, nitems, item_cap, npairs, pairs,
                                                             pair_cap);
     XYZB_LAUNCH_CHECK();
-    part_join<1><<<gj, kPjThreads, part_join_smem(M), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
+    part_join<1><<<gj, kPjThreads, part_join_smem(lb), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
                                                             work_run, items, nitems, item_cap, npairs, pairs,
                                                             pair_cap);
     XYZB_LAUNCH_CHECK();

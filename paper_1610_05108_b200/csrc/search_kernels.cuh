@@ -690,7 +690,11 @@ struct VerifyArgs {
     // x-side position, or (bucket path, keys unsorted) at the column index
     const void* vkeys;
     int vkeys_by_pos;
-    const void* xkeys;  // unsorted keys of the batch by column (pair-list hits)
+    const void* xkeys;  // unsorted keys of the batch by column (pair-list hits); nullptr: recompute
+    const u32* krows;   // ... from the runs' draws (krows[run * kM + s]) and the column words
+    int kM;
+    const u64* kXc;
+    u32 kWp;
     int key64;
     int vshift;  // sorted keys carry extra low bits to drop (0 here)
 };
@@ -754,8 +758,22 @@ __device__ __forceinline__ DevHit make_hit(const VerifyArgs& A, u32 run, u32 hel
 }
 
 // One pair-list hit appended by one lane (hits are rare: no aggregation).
+// Key of column j in a run: the M draws of the run, bit s = X[rows[s], j]
+// (project_keys, projection.cpp:32-57) — for hits of pair lists that outlive
+// their batch's key array (the L2-tiled verify).
+__device__ __forceinline__ u64 key_of_column(const u32* rows, int M, const u64* Xc, u32 Wp, u32 j) {
+    u64 v = 0;
+    const u64* col = Xc + u64(j) * Wp;
+    for (int s = 0; s < M; ++s) {
+        const u32 i = rows[s];
+        v |= ((col[i >> 6] >> (i & 63)) & 1ull) << s;
+    }
+    return v;
+}
+
 __device__ __noinline__ void append_pair_hit(const void* xkeys, int key64, u64 S, const u32* rid, DevHit* hits,
-                                             u32* hit_count, u32 hit_cap, PairRec pr, u32 si, u32 n) {
+                                             u32* hit_count, u32 hit_cap, PairRec pr, u32 si, u32 n,
+                                             const u32* krows, int kM, const u64* kXc, u32 kWp) {
     u32 j = pr.pa, k = pr.pb;
     if ((pr.pad & 2u) && j > k) {
         const u32 t = j;
@@ -764,7 +782,10 @@ __device__ __noinline__ void append_pair_hit(const void* xkeys, int key64, u64 S
     }
     const u64 i = u64(pr.run) * S + j;
     DevHit h;
-    h.order = key64 ? static_cast<const u64*>(xkeys)[i] : u64(static_cast<const u32*>(xkeys)[i]);
+    if (xkeys)
+        h.order = key64 ? static_cast<const u64*>(xkeys)[i] : u64(static_cast<const u32*>(xkeys)[i]);
+    else
+        h.order = key_of_column(krows + u64(pr.run) * kM, kM, kXc, kWp, j);
     h.s = double(si) / double(n);
     h.j = j;
     h.k = k;
@@ -925,7 +946,8 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
                 for (u32 q = 1; q < kPairsPerLane; ++q)
                     if (q == i) r = pr[q];
                 const u32 si = A.run_sign[r.run] > 0 ? acc : n - acc;
-                if (si >= astar) append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, r, si, n);
+                if (si >= astar) append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, r, si, n, A.krows,
+                                                 A.kM, A.kXc, A.kWp);
             }
             if (t + 1 < cnt) cur = nxt;
         }
@@ -971,7 +993,8 @@ __global__ void __launch_bounds__(256, XYZB_VP_MINB) verify_pairs_simple(VerifyA
             for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(tmask, acc, o);
             const u32 si = A.run_sign[pr.run] > 0 ? acc : n - acc;
             if (tl == 0 && si >= astar)  // rare: out of line, so the walk keeps few registers
-                append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, n);
+                append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, n, A.krows,
+                                A.kM, A.kXc, A.kWp);
         }
     }
 }

@@ -46,7 +46,8 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments", "merge_large"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments", "merge_large",
+                                      "tiled"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
 def test_search_matches_reference_fixture(name, grouping, monkeypatch):
     """All grouping paths: two CTAs per run splitting the 16-bit shared
@@ -60,6 +61,8 @@ def test_search_matches_reference_fixture(name, grouping, monkeypatch):
         monkeypatch.setenv("XYZB_SORT", "segments")
     if grouping == "merge_large":  # the multi-kernel merge instead of the single-CTA one
         monkeypatch.setenv("XYZB_MERGE_LARGE", "1")
+    if grouping == "tiled":  # the accumulated pair list verified in L2 column tiles
+        monkeypatch.setenv("XYZB_TILED", "1")
     xb = _engine()
     x, y, cfg, z = load_case(name)
     rep = xb.Dataset(x).search(y, cfg)
@@ -195,7 +198,8 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments"])
+@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments", "tiled",
+                                      "tiled_part"])
 def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
@@ -207,6 +211,10 @@ def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
         monkeypatch.setenv("XYZB_GROUPING", grouping)
     if grouping == "segments":
         monkeypatch.setenv("XYZB_SORT", "segments")
+    if grouping.startswith("tiled"):
+        monkeypatch.setenv("XYZB_TILED", "1")
+        if grouping == "tiled_part":
+            monkeypatch.setenv("XYZB_GROUPING", "part")
     monkeypatch.setenv("XYZB_BATCH_ENTRIES", "6000")  # three runs per batch, a shorter last batch
     monkeypatch.setenv("XYZB_HIT_CAP", "7")
     monkeypatch.setenv("XYZB_ITEM_CAP", "5")
@@ -565,3 +573,35 @@ def test_partition_grouping_vs_oracle(case, monkeypatch):
         assert ok, (m, p, msg)
         assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
             want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
+
+
+@pytest.mark.parametrize("case", ["forced_small", "many_tiles", "large_x"])
+def test_tiled_verify_vs_oracle(case, monkeypatch):
+    """The L2-tiled verify (opt-in, XYZB_TILED=1): the pair lists
+    of all batches accumulate, are bucketed by (min, max) column tile in
+    snake order and verified in one launch; hits recompute their x-side key
+    from the run's draws. Small data (several batches, constant and random
+    responses), tiny tiles (hundreds of tiles), and an X of 104 MB.
+    Bit-exact against the restatement."""
+    xb = _engine()
+    rng = np.random.default_rng(31)
+    monkeypatch.setenv("XYZB_TILED", "1")
+    if case == "forced_small":
+        monkeypatch.setenv("XYZB_BATCH_ENTRIES", "20000")
+        cases = [(300, 3000, 9, 6, False, 0.58), (300, 3000, 9, 6, True, 0.58), (65, 7000, 11, 4, False, 0.62)]
+    elif case == "many_tiles":
+        monkeypatch.setenv("XYZB_TILE_L2", "262144")  # 128 KB of tile columns: tiles of a few dozen columns
+        cases = [(640, 6000, 10, 4, False, 0.56)]
+    else:  # 130000 columns of 6400 rows: X = 104 MB > 96 MB
+        cases = [(6400, 130000, 17, 2, False, 0.515)]
+    for t, (n, p, m, l, const_y, gamma) in enumerate(cases):
+        x = ck.ref_rademacher(n, p, 700 + t, 5)
+        y = np.ones(n, np.int8) if const_y else np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        cfg = xb.SearchConfig(m=m, l=l, gamma=gamma, seed=t, threads=1, top_k=25, estimate_complexity=False)
+        got = xb.Dataset(x).search(y, cfg)
+        want = ck.oracle_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, (n, p, m, msg)
+        assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
+            want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (n, p, m)
+        assert len(want.hits) > 0
