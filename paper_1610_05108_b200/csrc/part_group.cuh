@@ -83,81 +83,6 @@ struct PartMap {
     }
 };
 
-// --------------------------------------------------------- block emission --
-
-// Pass 2 of a join over T block heads. Every thread owns the contiguous item
-// and pair slot ranges its counting pass reserved (ibase / pbase, thread-major
-// head order). Large blocks become items (their pairs expanded later at
-// it.pad, from the global grouped array); a block of at most kLanePairs
-// inline pairs is written by its lane, a larger inline block (<= kInlinePairs)
-// by the whole warp, one 16-byte record per lane. Columns of grouped position
-// pos are read from gl[pos - gbias] (shared memory when the partition is
-// staged there).
-constexpr u32 kLanePairs = 4;
-template <class BlockOf>
-__device__ __forceinline__ void emit_blocks_coop(BlockOf block_of, u32 T, u32 b, u32 hmax, u64 p, bool pair_list,
-                                                 u32 ibase, u32 pbase, Item* __restrict__ items, u32 item_cap,
-                                                 PairRec* __restrict__ pairs, u32 pair_cap,
-                                                 const u32* __restrict__ grouped, const u32* gl, u32 gbias) {
-    const int lane = threadIdx.x & 31;
-    uint4* dst = reinterpret_cast<uint4*>(pairs);
-    for (u32 li0 = 0; li0 < T; li0 += blockDim.x) {
-        const u32 li = li0 + threadIdx.x;
-        HeadBlock hb;
-        if (li < T) hb = block_of(li);
-        u32 ne, np, nsc;
-        emit_count(hb, hmax, pair_list, ne, np, nsc);
-        const bool inl = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
-        const bool big = inl && np > kLanePairs;
-        if (ne) {
-            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, pbase, items, item_cap, pairs, pair_cap, p, grouped);
-            ibase += ne;
-        }
-        if (inl && !big) {  // a few pairs: this lane writes them
-            const bool diag = hb.flags & 2u;
-            const bool first_held = diag || (hb.flags & 1u);
-            u32 slot = pbase;
-            for (u32 h = 0; h < hb.hc; ++h) {
-                const u32 hcol = gl[hb.hs + h - gbias];
-                for (u32 q = diag ? h + 1 : 0; q < hb.sc; ++q, ++slot) {
-                    const u32 scol = gl[hb.ss + q - gbias];
-                    if (slot < pair_cap)
-                        dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, hb.flags);
-                }
-            }
-        }
-        for (u32 bal = __ballot_sync(0xffffffffu, big); bal; bal &= bal - 1) {  // warp-written blocks
-            const int ow = __ffs(bal) - 1;
-            const u32 o_hs = __shfl_sync(0xffffffffu, hb.hs, ow), o_hc = __shfl_sync(0xffffffffu, hb.hc, ow);
-            const u32 o_ss = __shfl_sync(0xffffffffu, hb.ss, ow), o_sc = __shfl_sync(0xffffffffu, hb.sc, ow);
-            const u32 o_fl = __shfl_sync(0xffffffffu, hb.flags, ow);
-            const u32 o_np = __shfl_sync(0xffffffffu, np, ow), o_slot = __shfl_sync(0xffffffffu, pbase, ow);
-            if (u32(lane) < o_np) {
-                u32 l = lane, h = 0, q;
-                const bool diag = o_fl & 2u;
-                if (diag) {
-                    while (l >= o_hc - 1 - h) {
-                        l -= o_hc - 1 - h;
-                        ++h;
-                    }
-                    q = h + 1 + l;
-                } else {
-                    // l < 32, o_sc <= 32: the fp32 quotient of l + 0.5 is at least 1/64 from an integer
-                    h = __float2uint_rz((float(l) + 0.5f) * __frcp_rn(float(o_sc)));
-                    q = l - h * o_sc;
-                }
-                const u32 slot = o_slot + lane;
-                if (slot < pair_cap) {
-                    const u32 hcol = gl[o_hs + h - gbias], scol = gl[o_ss + q - gbias];
-                    const bool first_held = diag || (o_fl & 1u);
-                    dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, o_fl);
-                }
-            }
-        }
-        pbase += np;
-    }
-}
-
 // ---------------------------------------------------------- partition pass --
 
 // Entries of the partitioned keys: (w, column) as one 8-byte record.
