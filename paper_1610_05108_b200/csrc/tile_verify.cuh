@@ -44,13 +44,20 @@ __device__ __forceinline__ u32 tile_of(u32 a, u32 b, u32 T, u32 A) {
     return start + ((ta & 1u) ? (A - 1 - tb) : (tb - ta));
 }
 
+// Bucket functor of the pair-list bucketing: the L2 column tile of (pa, pb).
+struct TileOf {
+    u32 T, A;
+    __device__ __forceinline__ u32 operator()(u32 a, u32 b) const { return tile_of(a, b, T, A); }
+};
+
 __device__ __forceinline__ void cta_range(u32 P, u32& q0, u32& q1) {
     q0 = u32((u64(P) * blockIdx.x) / gridDim.x);
     q1 = u32((u64(P) * (blockIdx.x + 1)) / gridDim.x);
 }
 
+template <class F>
 __global__ void __launch_bounds__(kThreads) tile_count(const PairRec* __restrict__ pairs, const u32* __restrict__ np,
-                                                       u32 cap, u32 T, u32 A, u32 ntiles, u32* __restrict__ hist) {
+                                                       u32 cap, F f, u32 ntiles, u32* __restrict__ hist) {
     extern __shared__ u32 h[];
     for (u32 i = threadIdx.x; i < ntiles; i += blockDim.x) h[i] = 0;
     __syncthreads();
@@ -59,7 +66,7 @@ __global__ void __launch_bounds__(kThreads) tile_count(const PairRec* __restrict
     const uint2* pr = reinterpret_cast<const uint2*>(pairs);  // (pa, pb) of record q at 2q
     for (u32 q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
         const uint2 jk = __ldg(pr + 2 * u64(q));
-        atomicAdd(h + tile_of(jk.x, jk.y, T, A), 1u);
+        atomicAdd(h + f(jk.x, jk.y), 1u);
     }
     __syncthreads();
     for (u32 t = threadIdx.x; t < ntiles; t += blockDim.x) hist[u64(t) * gridDim.x + blockIdx.x] = h[t];
@@ -137,8 +144,9 @@ __global__ void __launch_bounds__(1024) tile_starts(u32* __restrict__ total, u32
 
 // bstart[i] = first slot of batch i (nb + 1 entries); batch i's runs are
 // search runs i * B + run.
+template <class F>
 __global__ void __launch_bounds__(kThreads) tile_scatter(const PairRec* __restrict__ pairs, const u32* __restrict__ np,
-                                                         u32 cap, u32 T, u32 A, u32 ntiles,
+                                                         u32 cap, F f, u32 ntiles,
                                                          const u32* __restrict__ hist, const u32* __restrict__ tstart,
                                                          const u32* __restrict__ bstart, u32 nb, u32 B,
                                                          PairRec* __restrict__ out) {
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(kThreads) tile_scatter(const PairRec* __restri
             if (bs[mid] <= q) lo = mid; else hi = mid;
         }
         r.run += lo * B;
-        out[atomicAdd(cur + tile_of(r.pa, r.pb, T, A), 1u)] = r;
+        out[atomicAdd(cur + f(r.pa, r.pb), 1u)] = r;
     }
 }
 
@@ -183,27 +191,37 @@ inline Plan plan(u64 p, u64 col_bytes, u64 l2_bytes) {
 
 inline u64 hist_words(const Plan& t) { return u64(t.ntiles) * kCtas + t.ntiles; }
 
-// pairs (accumulated, count at *np) -> out in tile order. scratch: hist_words u32.
-inline void sort_by_tile(const PairRec* pairs, const u32* np, u32 cap, const Plan& t, const u32* bstart, u32 nb,
-                         u32 B, u32* scratch, PairRec* out, cudaStream_t st, u64* launches) {
+// pairs (count at *np) -> out grouped by bucket f(pa, pb) (ntiles buckets);
+// scratch: ntiles * (kCtas + 1) u32, its last ntiles words end as the bucket
+// starts. bstart / nb / B: batch starts for the run globalisation (nb = 1 and
+// bstart = {0, ~0} keep the runs as they are).
+template <class F>
+inline const u32* bucket_pairs(const PairRec* pairs, const u32* np, u32 cap, F f, u32 ntiles, const u32* bstart,
+                               u32 nb, u32 B, u32* scratch, PairRec* out, cudaStream_t st, u64* launches) {
     static bool attr = false;
     if (!attr) {
-        XYZB_CUDA(cudaFuncSetAttribute(tile_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-        XYZB_CUDA(cudaFuncSetAttribute(tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+        XYZB_CUDA(cudaFuncSetAttribute(tile_count<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+        XYZB_CUDA(cudaFuncSetAttribute(tile_scatter<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
         attr = true;
     }
     u32* hist = scratch;
-    u32* total = scratch + u64(t.ntiles) * kCtas;
-    tile_count<<<kCtas, kThreads, t.ntiles * 4, st>>>(pairs, np, cap, t.T, t.A, t.ntiles, hist);
+    u32* total = scratch + u64(ntiles) * kCtas;
+    tile_count<F><<<kCtas, kThreads, ntiles * 4, st>>>(pairs, np, cap, f, ntiles, hist);
     XYZB_LAUNCH_CHECK();
-    tile_offsets<<<t.ntiles, 1024, 0, st>>>(hist, kCtas, total);
+    tile_offsets<<<ntiles, 1024, 0, st>>>(hist, kCtas, total);
     XYZB_LAUNCH_CHECK();
-    tile_starts<<<1, 1024, 0, st>>>(total, t.ntiles);
+    tile_starts<<<1, 1024, 0, st>>>(total, ntiles);
     XYZB_LAUNCH_CHECK();
-    tile_scatter<<<kCtas, kThreads, (t.ntiles + nb + 1) * 4, st>>>(pairs, np, cap, t.T, t.A, t.ntiles, hist, total,
-                                                                   bstart, nb, B, out);
+    tile_scatter<F><<<kCtas, kThreads, (ntiles + nb + 1) * 4, st>>>(pairs, np, cap, f, ntiles, hist, total, bstart,
+                                                                    nb, B, out);
     XYZB_LAUNCH_CHECK();
     *launches += 4;
+    return total;
+}
+
+inline void sort_by_tile(const PairRec* pairs, const u32* np, u32 cap, const Plan& t, const u32* bstart, u32 nb,
+                         u32 B, u32* scratch, PairRec* out, cudaStream_t st, u64* launches) {
+    bucket_pairs(pairs, np, cap, TileOf{t.T, t.A}, t.ntiles, bstart, nb, B, scratch, out, st, launches);
 }
 
 } // namespace tile
