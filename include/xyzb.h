@@ -231,6 +231,24 @@ int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t has_gamma, 
                      uint64_t top_k, uint64_t histogram_bins, int32_t force, xyzb_scored_pair** pairs,
                      uint64_t* n_pairs, uint64_t* pairs_scanned, uint64_t** histogram, char* err, size_t errlen);
 
+/* ---- xyz-regression helpers (the loop around the screen) ----
+ * A device-resident design for lasso_path (lasso.hpp:136-141): X (n x p,
+ * column-major fp64, the caller's RealMatrix values) and the column means of
+ * the caller's CenteredDesignView (lasso.cpp:40-47), so the exact scans of the
+ * active-set loop run on the GPU while coordinate descent stays on the host:
+ *   main:  out[j] = sum_i r_i (x_ij - m_j)                  (main_correlation, lasso.cpp:74-80)
+ *   pair:  out[t] = sum_i r_i (x_ij - m_j)(x_ik - m_k)      (pair_correlation, lasso.cpp:82-92)
+ * fp64 products and sums (summation order differs from the host loop; the
+ * results agree to a few ulps of the sum of |terms|). */
+typedef struct xyzb_design xyzb_design;
+int xyzb_design_create(const double* x, uint64_t n_rows, uint64_t n_cols, const double* means, int32_t device,
+                       xyzb_design** out, char* err, size_t errlen);
+void xyzb_design_destroy(xyzb_design* d);
+int xyzb_design_main_correlations(xyzb_design* d, const double* residual, double* out, char* err, size_t errlen);
+/* pairs_jk: 2 * n_pairs column indices (j, k); j == k is a square term. */
+int xyzb_design_pair_correlations(xyzb_design* d, const double* residual, const uint32_t* pairs_jk,
+                                  uint64_t n_pairs, double* out, char* err, size_t errlen);
+
 void xyzb_free(void* p);
 
 #ifdef __cplusplus

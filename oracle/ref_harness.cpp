@@ -497,6 +497,31 @@ void ref_lasso_free(ref_lasso_out* o) {
     std::memset(o, 0, sizeof(*o));
 }
 
+// kkt_check_interactions (lasso.cpp:377-426): sorted violating pairs as
+// 2 * count column indices, malloc'ed (free with ref_free).
+int ref_kkt_check_interactions(const double* x, uint64_t n, uint64_t p, const double* residual, double lambda,
+                               uint64_t kkt_l, uint64_t kkt_max_candidates, uint64_t seed, uint64_t stream,
+                               uint32_t threads, uint32_t** pairs_jk, uint64_t* count, char* err, size_t errlen) {
+    *pairs_jk = nullptr;
+    *count = 0;
+    return guarded(err, errlen, [&] {
+        const xyz::RealMatrix xm = real_from_colmajor(x, n, p);
+        const xyz::RealVector r(residual, residual + n);
+        xyz::LassoPathConfig cfg;
+        if (kkt_l) cfg.kkt_l = kkt_l;
+        cfg.kkt_max_candidates = kkt_max_candidates;
+        cfg.seed = seed;
+        cfg.threads = threads;
+        const auto v = xyz::kkt_check_interactions(r, xm, lambda, cfg, stream);
+        *pairs_jk = static_cast<uint32_t*>(std::malloc(std::max<size_t>(1, v.size()) * 8));
+        for (size_t t = 0; t < v.size(); ++t) {
+            (*pairs_jk)[2 * t] = v[t].j;
+            (*pairs_jk)[2 * t + 1] = v[t].k;
+        }
+        *count = v.size();
+    });
+}
+
 // write_dataset / read_dataset (dataset_io.cpp:65-129)
 int ref_write_dataset(const char* path, int32_t kind, const uint64_t* x_words, const double* x_real, uint64_t n,
                       uint64_t p, char* err, size_t errlen) {

@@ -2201,6 +2201,71 @@ extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, ui
 }
 
 namespace {
+
+// ------------------------------------------------- xyz-regression design --
+// Centered correlations of lasso_path's exact scans (lasso.cpp:74-92): one
+// warp per column / pair, fp64 products rounded as the host's left-to-right
+// r * (x_j - m_j) * (x_k - m_k), warp-tree sums.
+namespace design {
+
+__global__ void __launch_bounds__(256) main_corr(const double* __restrict__ X, const double* __restrict__ m, u64 n,
+                                                 u64 p, const double* __restrict__ r, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const u64 nw = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 j = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < p; j += nw) {
+        const double* col = X + j * n;
+        const double mj = m[j];
+        double acc = 0.0;
+        for (u64 i = lane; i < n; i += 32) acc = __dadd_rn(acc, __dmul_rn(__ldg(r + i), __dsub_rn(__ldg(col + i), mj)));
+        acc = warp_sum(acc);
+        if (lane == 0) out[j] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(256) pair_corr(const double* __restrict__ X, const double* __restrict__ m, u64 n,
+                                                 const u32* __restrict__ pairs, u64 cnt,
+                                                 const double* __restrict__ r, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const u64 nw = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 t = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < cnt; t += nw) {
+        const u32 j = pairs[2 * t], k = pairs[2 * t + 1];
+        const double *cj = X + u64(j) * n, *ck = X + u64(k) * n;
+        const double mj = m[j], mk = m[k];
+        double acc = 0.0;
+        for (u64 i = lane; i < n; i += 32) {
+            const double a = __dmul_rn(__ldg(r + i), __dsub_rn(__ldg(cj + i), mj));
+            acc = __dadd_rn(acc, __dmul_rn(a, __dsub_rn(__ldg(ck + i), mk)));
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) out[t] = acc;
+    }
+}
+
+} // namespace design
+
+} // namespace
+
+struct xyzb_design {
+    int device = 0;
+    u64 n = 0, p = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf x, means, r, pairs, out;
+    ~xyzb_design() {
+        if (stream) {
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
+    }
+};
+
+namespace {
+
+void design_residual(xyzb_design* d, const double* residual) {
+    if (!residual) throw data_error("xyzb_design: null residual");
+    d->r.ensure(d->n * 8);
+    XYZB_CUDA(cudaMemcpyAsync(d->r.p, residual, d->n * 8, cudaMemcpyHostToDevice, d->stream));
+}
+
 } // namespace
 
 // ------------------------------------------------------------ C ABI --
@@ -2343,6 +2408,82 @@ void xyzb_result_free(xyzb_result* r) {
     r->hits = nullptr;
     r->order_keys = nullptr;
     r->top_k = nullptr;
+}
+
+int xyzb_design_create(const double* x, uint64_t n_rows, uint64_t n_cols, const double* means, int32_t device,
+                       xyzb_design** out, char* err, size_t errlen) {
+    if (out) *out = nullptr;
+    return guarded(err, errlen, [&] {
+        if (!x || !means || !out) throw data_error("xyzb_design_create: null argument");
+        if (n_rows == 0 || n_cols == 0) throw data_error("xyzb_design_create: empty design");
+        require_device();
+        DeviceGuard g(device);
+        auto d = std::make_unique<xyzb_design>();
+        d->device = device;
+        d->n = n_rows;
+        d->p = n_cols;
+        XYZB_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+        StreamScope sc(d->stream);
+        d->x.ensure(n_rows * n_cols * 8);
+        d->means.ensure(n_cols * 8);
+        XYZB_CUDA(cudaMemcpyAsync(d->x.p, x, n_rows * n_cols * 8, cudaMemcpyHostToDevice, d->stream));
+        XYZB_CUDA(cudaMemcpyAsync(d->means.p, means, n_cols * 8, cudaMemcpyHostToDevice, d->stream));
+        XYZB_CUDA(cudaStreamSynchronize(d->stream));
+        *out = d.release();
+    });
+}
+
+void xyzb_design_destroy(xyzb_design* d) {
+    if (!d) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(d->device);
+    {
+        StreamScope sc(d->stream);
+        cudaStreamSynchronize(d->stream);
+        tl_drained = d->stream;
+        delete d;
+        tl_drained = nullptr;
+    }
+    cudaSetDevice(cur);
+}
+
+int xyzb_design_main_correlations(xyzb_design* d, const double* residual, double* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!d || !out) throw data_error("xyzb_design_main_correlations: null argument");
+        DeviceGuard g(d->device);
+        StreamScope sc(d->stream);
+        design_residual(d, residual);
+        d->out.ensure(d->p * 8);
+        design::main_corr<<<static_cast<u32>(std::min<u64>(ceil_div(d->p * 32, 256), u64(kSMs) * 16)), 256, 0,
+                            d->stream>>>(d->x.as<double>(), d->means.as<double>(), d->n, d->p, d->r.as<double>(),
+                                         d->out.as<double>());
+        XYZB_LAUNCH_CHECK();
+        XYZB_CUDA(cudaMemcpyAsync(out, d->out.p, d->p * 8, cudaMemcpyDeviceToHost, d->stream));
+        XYZB_CUDA(cudaStreamSynchronize(d->stream));
+    });
+}
+
+int xyzb_design_pair_correlations(xyzb_design* d, const double* residual, const uint32_t* pairs_jk,
+                                  uint64_t n_pairs, double* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!d || (n_pairs && (!pairs_jk || !out))) throw data_error("xyzb_design_pair_correlations: null argument");
+        if (n_pairs == 0) return;
+        for (u64 t = 0; t < 2 * n_pairs; ++t)
+            if (pairs_jk[t] >= d->p) throw data_error("xyzb_design_pair_correlations: column index out of range");
+        DeviceGuard g(d->device);
+        StreamScope sc(d->stream);
+        design_residual(d, residual);
+        d->pairs.ensure(n_pairs * 8);
+        d->out.ensure(n_pairs * 8);
+        XYZB_CUDA(cudaMemcpyAsync(d->pairs.p, pairs_jk, n_pairs * 8, cudaMemcpyHostToDevice, d->stream));
+        design::pair_corr<<<static_cast<u32>(std::min<u64>(ceil_div(n_pairs * 32, 256), u64(kSMs) * 16)), 256, 0,
+                            d->stream>>>(d->x.as<double>(), d->means.as<double>(), d->n, d->pairs.as<u32>(), n_pairs,
+                                         d->r.as<double>(), d->out.as<double>());
+        XYZB_LAUNCH_CHECK();
+        XYZB_CUDA(cudaMemcpyAsync(out, d->out.p, n_pairs * 8, cudaMemcpyDeviceToHost, d->stream));
+        XYZB_CUDA(cudaStreamSynchronize(d->stream));
+    });
 }
 
 void xyzb_free(void* p) { std::free(p); }

@@ -308,6 +308,9 @@ _LASSO_SIGS = {
                                  C.c_uint64, C.c_uint64, C.c_uint32, C.c_int32, C.POINTER(LassoOut), C.c_char_p,
                                  C.c_size_t]),
     "ref_lasso_free": (None, [C.POINTER(LassoOut)]),
+    "ref_kkt_check_interactions": (C.c_int, [_F64P, C.c_uint64, C.c_uint64, _F64P, C.c_double, C.c_uint64, C.c_uint64,
+                                             C.c_uint64, C.c_uint64, C.c_uint32, C.POINTER(_U32P),
+                                             C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
 }
 
 
@@ -348,10 +351,27 @@ def lasso_path(lib, x: RealMatrix, y, grid_size=20, grid_ratio=0.05, kkt_l=0, kk
             theta = {(int(out.pair_j[i]), int(out.pair_k[i])): float(out.pair_val[i])
                      for i in range(out.pair_off[t], out.pair_off[t + 1])}
             fits.append(dict(lam=float(out.lambda_[t]), beta=beta, theta=theta, kkt=float(out.kkt_residual_max[t]),
-                             certified=bool(out.certified[t]), degenerate=bool(out.degenerate[t])))
+                             certified=bool(out.certified[t]), degenerate=bool(out.degenerate[t]),
+                             iterations=int(out.active_set_iterations[t])))
         return fits, out.wall_s
     finally:
         lib.ref_lasso_free(C.byref(out))
+
+
+def kkt_check_interactions(lib, x: RealMatrix, residual, lam, kkt_l=0, kkt_max_candidates=0, seed=7, stream=1,
+                           threads=1):
+    """kkt_check_interactions through a harness library: sorted (j, k) list."""
+    pj = _U32P()
+    cnt = C.c_uint64(0)
+    err = _abi.errbuf()
+    r = np.ascontiguousarray(residual, np.float64)
+    _check(lib.ref_kkt_check_interactions(x.values.ctypes.data_as(_F64P), x.n_rows, x.n_cols, r.ctypes.data_as(_F64P),
+                                          lam, kkt_l, kkt_max_candidates, seed, stream, threads, C.byref(pj),
+                                          C.byref(cnt), err, _abi.ERRBUF), err)
+    try:
+        return [(int(pj[2 * t]), int(pj[2 * t + 1])) for t in range(cnt.value)]
+    finally:
+        ref_lib().ref_free(pj)
 
 
 def ref_write_dataset(path, x):

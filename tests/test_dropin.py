@@ -60,3 +60,106 @@ def test_dropin_lasso_path_matches_reference(seed):
     _compare_fits(gpu, cpu)
     # the path is non-trivial: mains and interaction terms enter it
     assert any(f["theta"] for f in gpu) and any(f["beta"] for f in gpu)
+
+
+def _pm1_design(n, p, seed):
+    from paper_1610_05108_b200.matrix import RealMatrix
+    rng = np.random.default_rng(seed)
+    xv = np.where(rng.random((p, n)) < 0.5, -1.0, 1.0)
+    y = 1.5 * xv[2] + 1.2 * xv[5] * xv[9] - 1.0 * xv[11] * xv[40] + rng.normal(0.0, 0.4, n)
+    return RealMatrix(xv), y
+
+
+def test_dropin_lasso_binary_design_matches_reference():
+    """+-1 design: square terms excluded, the KKT screen is the continuous-Y
+    search on the packed matrix; the regression loop's scans on the GPU.
+    Coefficients within 1e-4, the same active-set iteration counts."""
+    x, y = _pm1_design(200, 120, 3)
+    kw = dict(grid_size=8, grid_ratio=0.1, kkt_l=40, kkt_max_candidates=16 * 120, seed=5, threads=1)
+    cpu, _ = ck.lasso_path(ck.ref_lasso_lib(), x, y, **kw)
+    gpu, _ = ck.lasso_path(ck.dropin_lib(), x, y, **kw)
+    _compare_fits(gpu, cpu)
+    assert [f["iterations"] for f in gpu] == [f["iterations"] for f in cpu]
+    assert [f["certified"] for f in gpu] == [f["certified"] for f in cpu]
+    assert any(f["theta"] for f in gpu)
+
+
+def test_dropin_lasso_large_p_matches_reference():
+    """p = 2500 (no exhaustive certificate, probabilistic screens only):
+    coefficients within 1e-4, iteration counts and degenerate flags equal,
+    KKT residuals within 1e-9."""
+    from paper_1610_05108_b200 import synth
+    x, y, pairs, mains = synth.gauss(n=300, p=2500, n_pairs=3, theta=1.0, noise_sd=0.5, n_mains=4, beta=1.0, seed=8)
+    kw = dict(grid_size=6, grid_ratio=0.2, kkt_l=60, kkt_max_candidates=16 * 2500, seed=7, threads=1)
+    cpu, _ = ck.lasso_path(ck.ref_lasso_lib(), x, y, **kw)
+    gpu, _ = ck.lasso_path(ck.dropin_lib(), x, y, **kw)
+    _compare_fits(gpu, cpu)
+    assert [f["iterations"] for f in gpu] == [f["iterations"] for f in cpu]
+    assert [f["degenerate"] for f in gpu] == [f["degenerate"] for f in cpu]
+    for g, c in zip(gpu, cpu):
+        assert abs(g["kkt"] - c["kkt"]) <= 1e-9 * max(1.0, abs(c["kkt"]))
+
+
+@pytest.mark.parametrize("design", ["gauss", "pm1"])
+def test_dropin_kkt_check_interactions_matches_reference(design):
+    """kkt_check_interactions (lasso.cpp:377-426) on the GPU: the same sorted
+    violator lists as the reference at several lambda levels, including a
+    level low enough that the screen degenerates to the exact all-pairs scan
+    (p <= 2000)."""
+    from paper_1610_05108_b200 import synth
+    if design == "gauss":
+        x, y, _, _ = synth.gauss(n=250, p=300, n_pairs=3, theta=1.0, noise_sd=0.5, n_mains=2, beta=1.0, seed=4)
+    else:
+        x, y = _pm1_design(250, 300, 4)
+    r = np.asarray(y, np.float64) - np.mean(y)
+    xc = x.values - x.values.mean(axis=1, keepdims=True)
+    top = float(np.max(np.abs(np.triu((xc * r) @ xc.T, 1)))) / len(r)  # the strongest pair correlation
+    seen_nonempty = False
+    for frac in (1.2, 0.9, 0.6, 0.4) + ((1e-6,) if design == "pm1" else ()):  # pm1: means != 0 -> degenerate
+        lam = top * frac
+        kw = dict(kkt_l=60, kkt_max_candidates=0, seed=3, stream=2)  # unlimited (the reference default)
+        want = ck.kkt_check_interactions(ck.ref_lasso_lib(), x, r, lam, **kw)
+        got = ck.kkt_check_interactions(ck.dropin_lib(), x, r, lam, **kw)
+        assert got == want, (design, frac)
+        seen_nonempty |= bool(want)
+    assert seen_nonempty
+
+
+def test_design_correlations_vs_numpy():
+    """xyzb_design_* (the regression loop's exact scans) against fp64 numpy:
+    main correlations sum_i r_i (x_ij - m_j) and pair / square correlations
+    sum_i r_i (x_ij - m_j)(x_ik - m_k), to 1e-12 of the sum of |terms|;
+    out-of-range indices are data errors."""
+    import ctypes as C
+    from paper_1610_05108_b200 import _abi, _lib
+    lib = _abi.bind(C.CDLL(_lib.LIB_PATH), _abi.SIGNATURES)
+    rng = np.random.default_rng(9)
+    n, p = 777, 1234
+    xv = rng.normal(size=(p, n))  # column-major: column j is xv[j]
+    means = xv.mean(axis=1)
+    r = rng.normal(size=n)
+    r -= r.mean()
+    f64 = C.POINTER(C.c_double)
+    d = C.c_void_p()
+    err = _abi.errbuf()
+    assert lib.xyzb_design_create(xv.ctypes.data_as(f64), n, p, means.ctypes.data_as(f64), 0, C.byref(d), err,
+                                  _abi.ERRBUF) == 0, err.value
+    try:
+        out = np.zeros(p)
+        assert lib.xyzb_design_main_correlations(d, r.ctypes.data_as(f64), out.ctypes.data_as(f64), err,
+                                                 _abi.ERRBUF) == 0
+        xc = xv - means[:, None]
+        want = xc @ r
+        assert np.all(np.abs(out - want) <= 1e-12 * (np.abs(xc) @ np.abs(r)))
+        pairs = np.concatenate([rng.integers(0, p, (5000, 2)), np.repeat(np.arange(50), 2).reshape(-1, 2)])
+        pairs = np.ascontiguousarray(pairs, np.uint32)
+        pout = np.zeros(len(pairs))
+        assert lib.xyzb_design_pair_correlations(d, r.ctypes.data_as(f64), pairs.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                 len(pairs), pout.ctypes.data_as(f64), err, _abi.ERRBUF) == 0
+        terms = xc[pairs[:, 0]] * xc[pairs[:, 1]] * r
+        assert np.all(np.abs(pout - terms.sum(axis=1)) <= 1e-12 * np.abs(terms).sum(axis=1))
+        bad = np.array([0, p], np.uint32)
+        assert lib.xyzb_design_pair_correlations(d, r.ctypes.data_as(f64), bad.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                 1, pout.ctypes.data_as(f64), err, _abi.ERRBUF) == 3
+    finally:
+        lib.xyzb_design_destroy(d)
