@@ -165,9 +165,13 @@ public:
             s.transform = BinarizeTransform::unbiased;
             rep = xyz_search(rescaled_, response, s);
         }
-        std::set<PairKey> keys;
-        for (const InteractionHit& h : rep.hits) keys.insert(make_pair_key(h.j, h.k));
-        return {keys.begin(), keys.end()};
+        // distinct unordered pairs in ascending order (an unguarded screen returns millions)
+        std::vector<PairKey> keys;
+        keys.reserve(rep.hits.size());
+        for (const InteractionHit& h : rep.hits) keys.push_back(make_pair_key(h.j, h.k));
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        return keys;
     }
 
 private:
