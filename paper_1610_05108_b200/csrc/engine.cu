@@ -240,7 +240,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal, yreal32;
     // batch scratch
     DevBuf keys[2], vals[2], keys_x, hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent, pairs_t, tscratch, bstart;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent, pairs_t, tscratch, bstart, povf;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -613,6 +613,7 @@ struct SearchCtx {
     u64 pair_scale = 1;  // grows when a batch overflows its pair list
     bool tiled = false;    // this attempt verifies the accumulated pair list in column tiles
     bool no_tile = false;  // the accumulated list would exceed 2^32 pairs: per-batch verify
+    bool no_hash = false;  // a hashed partition overflowed: the sparse grouping runs on the sorted path
     RunPlan plan;
     xyzb_result* out;
     u64 launches[XYZB_NUM_STAGES] = {};
@@ -746,6 +747,8 @@ void run_batches(SearchCtx& c) {
     XYZB_CUDA(cudaMemsetAsync(ds->verified.p, 0, Rall * 8, st));
     ds->hit_count.ensure(8);
     XYZB_CUDA(cudaMemsetAsync(ds->hit_count.p, 0, 4, st));
+    ds->povf.ensure(8);
+    XYZB_CUDA(cudaMemsetAsync(ds->povf.p, 0, 4, st));
     ds->hits.ensure(sizeof(kern::DevHit) * u64(ds->hit_cap));
     // batch size: B*p entries under the budget (about 64 B of scratch each)
     u64 budget = u64(1) << 26;  // XYZB_BATCH_ENTRIES overrides (tests force multi-batch runs with it)
@@ -861,10 +864,17 @@ void run_batches(SearchCtx& c) {
     // runs; =cluster keeps the DSMEM-table kernel at M = 17)
     // M >= 19 with a dense bucket space: partition pass + one small CTA per (run, partition)
     // (XYZB_GROUPING=part forces it for any M <= 24)
-    const bool part_path = sizeof(K) == 4 && M >= 2 && M <= 24 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
-                           (gsel_is("part") || (!gsel && M >= 19));
+    // sparse bucket spaces (2^M > 4p + 1024, M <= 31): the same partition pass with a shared-memory
+    // hash table per partition (a partition above its capacity raises povf: the search is redone on
+    // the sorted path); XYZB_GROUPING=sort keeps the cluster radix sort
+    const bool dense = (u64(1) << M) <= 4 * p + 1024;
+    const bool part_hash = sizeof(K) == 4 && M >= 2 && M <= 31 && !dense && !c.no_hash && !sort_sel &&
+                           (!gsel || gsel_is("part"));
+    const bool part_path = part_hash || (sizeof(K) == 4 && M >= 2 && M <= 24 && dense && !sort_sel &&
+                                         (gsel_is("part") || (!gsel && M >= 19)));
+    const int pk = part_hash ? kern::part_digits_hash(int(M), p) : kern::part_digits(int(M), p);
     if (part_path) {
-        ds->pgrp.ensure(kern::part_scratch_words(int(M), p, B) * 4);
+        ds->pgrp.ensure(kern::part_scratch_words(pk, B) * 4);
         ds->pent.ensure(cap * 8);
     }
     const bool ms_path = !part_path && M >= 17 && M <= 20 && !sort_sel && !gsel_is("sort") && !gsel_is("bucket") &&
@@ -967,17 +977,18 @@ void run_batches(SearchCtx& c) {
         if (part_path) {
             // ---- group: partition pass (per-run partitions that hold both sides of every block) ----
             if constexpr (sizeof(K) == 4) {
-                kern::part_partition_launch(k0, nb, p, int(M), ds->xorc.as<K>(), ds->tot.as<u64>(),
+                kern::part_partition_launch(k0, nb, p, int(M), pk, part_hash, ds->xorc.as<K>(), ds->tot.as<u64>(),
                                             ds->work_run.as<u64>(), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st);
                 c.launches[XYZB_STAGE_SORT] += 3;
                 e2 = clk.mark();
                 clk.span(XYZB_STAGE_SORT, e1, e2);
                 c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);
                 // ---- join: per (run, partition) bucket tables in shared memory; |E_r|, guard, blocks ----
-                kern::part_join_launch(nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0], ds->tot.as<u64>(),
-                                       ds->work_run.as<u64>(), ds->items.as<kern::Item>(), nitems,
+                kern::part_join_launch(nb, p, int(M), pk, part_hash, ds->xorc.as<K>(), c.guard, hmax, vb[0],
+                                       ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(), nitems,
                                        static_cast<u32>(item_cap), npairs_b, ds->pairs.as<kern::PairRec>(),
-                                       static_cast<u32>(c.pair_cap), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st);
+                                       static_cast<u32>(c.pair_cap), ds->pgrp.as<u32>(), ds->pent.as<uint2>(),
+                                       ds->povf.as<u32>(), st);
                 c.launches[XYZB_STAGE_JOIN] += 2;
             } else {
                 throw internal_error("xyzb: partitioned grouping needs 32-bit keys");
@@ -1595,7 +1606,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         }
         // status block (pinned): H, merge counts, items and pairs per batch, per-run counters
         const size_t o_cnt = 8, o_items = 16, o_pairs = o_items + 4 * nbt, o_enum = round_up(o_pairs + 4 * nbt, 8),
-                     o_ver = o_enum + 8 * Rall, sbytes = o_ver + 8 * Rall;
+                     o_ver = o_enum + 8 * Rall, o_ovf = o_ver + 8 * Rall, sbytes = o_ovf + 8;
         ds->h_status.ensure(sbytes);
         char* hs = ds->h_status.as<char>();
         XYZB_CUDA(cudaMemcpyAsync(hs, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
@@ -1605,6 +1616,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             XYZB_CUDA(cudaMemcpyAsync(hs + o_pairs, ds->npairs.p, nbt * 4, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaMemcpyAsync(hs + o_enum, ds->enumerated.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaMemcpyAsync(hs + o_ver, ds->verified.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
+        XYZB_CUDA(cudaMemcpyAsync(hs + o_ovf, ds->povf.p, 4, cudaMemcpyDeviceToHost, ds->stream));
         tr.mark("search:launch");
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         tr.mark("search:device");
@@ -1629,7 +1641,9 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                 c.pair_scale *= std::max<u64>(2, ceil_div(pneed, c.pair_cap));
             }
         }
-        if (H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
+        const bool povf = *reinterpret_cast<const u32*>(hs + o_ovf) != 0;
+        if (povf) c.no_hash = true;  // a hashed partition overflowed: redo on the sorted path
+        if (!povf && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
             std::memcpy(enumerated.data(), hs + o_enum, Rall * 8);
             std::memcpy(verified.data(), hs + o_ver, Rall * 8);
             break;

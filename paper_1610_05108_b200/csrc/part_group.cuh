@@ -85,9 +85,18 @@ struct PartMap {
 
 // ---------------------------------------------------------- partition pass --
 
+// Partition digit of w: its top k bits (dense path: the local bucket is the
+// low lb bits), or, for the hashed path, the top k bits of a multiplicative
+// hash of w >> 1 — w and its partner w ^ 1 still share it, and the partitions
+// stay balanced when key bits are correlated (a row drawn twice makes two key
+// bits equal for every column).
+__device__ __forceinline__ u32 part_digit(u32 w, int lb, int k, bool hashed) {
+    return hashed ? (k ? ((w >> 1) * 0x9E3779B1u) >> (32 - k) : 0u) : (w >> lb);
+}
+
 // Entries of the partitioned keys: (w, column) as one 8-byte record.
 template <bool SCATTER>
-__device__ __forceinline__ void part_tile(const u32* __restrict__ keys, u64 p, int M, int lb,
+__device__ __forceinline__ void part_tile(const u32* __restrict__ keys, u64 p, int M, int lb, bool hashed,
                                           const u32* __restrict__ xorc, u32* __restrict__ pcnt,
                                           u32* __restrict__ cursor, uint2* __restrict__ pe) {
     extern __shared__ u32 hist[];  // [nwarps][2^k]
@@ -111,7 +120,7 @@ __device__ __forceinline__ void part_tile(const u32* __restrict__ keys, u64 p, i
 #pragma unroll
     for (int q = 0; q < kPgPerThread; ++q) {
         const u64 i = t0 + u64(q) * blockDim.x + threadIdx.x;
-        if (i < p) rk[q] = atomicAdd(hw + (w[q] >> lb), 1u);
+        if (i < p) rk[q] = atomicAdd(hw + part_digit(w[q], lb, k, hashed), 1u);
     }
     __syncthreads();
     if constexpr (!SCATTER) {
@@ -137,20 +146,21 @@ __device__ __forceinline__ void part_tile(const u32* __restrict__ keys, u64 p, i
 #pragma unroll
         for (int q = 0; q < kPgPerThread; ++q) {
             const u64 i = t0 + u64(q) * blockDim.x + threadIdx.x;
-            if (i < p) out[hw[w[q] >> lb] + rk[q]] = make_uint2(w[q], u32(i));
+            if (i < p) out[hw[part_digit(w[q], lb, k, hashed)] + rk[q]] = make_uint2(w[q], u32(i));
         }
     }
 }
 
 __global__ void __launch_bounds__(kPgThreads) part_count(const u32* __restrict__ keys, u64 p, int M, int lb,
-                                                         const u32* __restrict__ xorc, u32* __restrict__ pcnt) {
-    part_tile<false>(keys, p, M, lb, xorc, pcnt, nullptr, nullptr);
+                                                         int hashed, const u32* __restrict__ xorc,
+                                                         u32* __restrict__ pcnt) {
+    part_tile<false>(keys, p, M, lb, hashed != 0, xorc, pcnt, nullptr, nullptr);
 }
 
 __global__ void __launch_bounds__(kPgThreads) part_scatter(const u32* __restrict__ keys, u64 p, int M, int lb,
-                                                           const u32* __restrict__ xorc, u32* __restrict__ cursor,
-                                                           uint2* __restrict__ pe) {
-    part_tile<true>(keys, p, M, lb, xorc, nullptr, cursor, pe);
+                                                           int hashed, const u32* __restrict__ xorc,
+                                                           u32* __restrict__ cursor, uint2* __restrict__ pe) {
+    part_tile<true>(keys, p, M, lb, hashed != 0, xorc, nullptr, cursor, pe);
 }
 
 // One CTA per run: pbeg[b][d] = run-local start of partition d (pbeg[b][D] = p);
@@ -435,13 +445,250 @@ __global__ void __launch_bounds__(kPjThreads) part_join(const uint2* __restrict_
 inline size_t part_tile_smem(int k) { return size_t(kPgThreads / 32) * (size_t(1) << k) * 4; }
 inline size_t part_join_smem(int lb) { return ((size_t(1) << lb) + kPjThreads * kPjPerThread) * 4; }
 
-// The partitioned path (u32 keys, M <= 24). scratch: pcnt / cursor B * 2^k
-// u32, pbeg B * (2^k + 1) u32; pe: B * p (w, column) entries.
-inline u64 part_scratch_words(int M, u64 p, u64 B) { return B * ((u64(1) << part_digits(M, p)) * 3 + 1); }
+// ------------------------------------------------ hashed partition join --
+//
+// Sparse bucket spaces (2^M >> p, e.g. config 3: M = 20, p = 5e4): a dense
+// 2^lb table per partition would be mostly empty, so the partition's local
+// keys go into an open-addressing hash table in shared memory instead
+// (kHsSlots slots for at most kHsCap records, load <= 1/2): a slot holds a
+// key and its count, the insertion's count atomic returns the record's rank,
+// and the scan over the slots gives every key its grouped range. A key's
+// partner w ^ 1 is found by probing. A partition above kHsCap records (a
+// skewed key distribution) is not processed: the kernel raises *ovf and the
+// host redoes the search on the sorted path.
+constexpr int kHsThreads = 512;
+constexpr int kHsPer = 4;
+constexpr u32 kHsCap = kHsThreads * kHsPer;  // 2048 records per partition
+constexpr u32 kHsSlots = 2 * kHsCap;
+constexpr u32 kHsEmpty = 0xffffffffu;
 
-inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, const u32* xorc, u64* tot, u64* work_run,
-                                  u32* scratch, uint2* pe, cudaStream_t st) {
-    const int lb = part_local_bits(M, p), k = M - lb;
+// Slot hash (12 bits: kHsSlots = 4096): a full avalanche finalizer, so the
+// slot bits are independent of the partition digit (a multiplicative hash of
+// w >> 1 that every key of the partition shares in its top bits).
+__device__ __forceinline__ u32 hs_hash(u32 u) {
+    u ^= u >> 16;
+    u *= 0x85EBCA6Bu;
+    u ^= u >> 13;
+    u *= 0xC2B2AE35u;
+    u ^= u >> 16;
+    return u >> 20;
+}
+
+__device__ __forceinline__ u32 hs_find(const u32* tk, u32 u) {
+    for (u32 h = hs_hash(u);; h = (h + 1) & (kHsSlots - 1)) {
+        const u32 k = tk[h];
+        if (k == u) return h;
+        if (k == kHsEmpty) return kHsEmpty;
+    }
+}
+
+template <int EMIT>
+__global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __restrict__ pe, const u32* __restrict__ pbeg,
+                                                             u64 p, int M, int lb, const u32* __restrict__ xorc,
+                                                             u64 guard, u32 hmax, u32* __restrict__ grouped,
+                                                             u64* __restrict__ tot, u64* __restrict__ work_run,
+                                                             Item* __restrict__ items, u32* __restrict__ nitems,
+                                                             u32 item_cap, u32* __restrict__ npairs,
+                                                             PairRec* __restrict__ pairs, u32 pair_cap,
+                                                             u32* __restrict__ ovf) {
+    extern __shared__ __align__(16) u32 hsm[];
+    u32* tk = hsm;                  // [kHsSlots] keys
+    u32* tc = tk + kHsSlots;        // [kHsSlots] counts
+    u32* ts = tc + kHsSlots;        // [kHsSlots] grouped starts of the keys that are in a block
+    u32* sg = ts + kHsSlots;        // [kHsCap] grouped columns
+    u32* heads = sg + kHsCap;       // [kHsCap] slots of the block heads
+    __shared__ u32 ws[68];
+    __shared__ u32 s_nheads, s_cursor;
+    __shared__ u64 red[2][kHsThreads / 32];
+    const u32 b = blockIdx.y, d = blockIdx.x;
+    const int k = M - lb;
+    const u32 D = 1u << k;
+    const u32 mask = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
+    const u32 c = xorc[b] & mask;
+    if (EMIT && tot[b] > guard) return;
+    const u32 beg = pbeg[u64(b) * (D + 1) + d], end = pbeg[u64(b) * (D + 1) + d + 1];
+    const u32 cnt = end - beg;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (cnt > kHsCap) {  // uniform: redo the search on the sorted path
+        if (threadIdx.x == 0) atomicExch(ovf, 1u);
+        return;
+    }
+    if (cnt < 2) {
+        if (!EMIT && c == 0 && threadIdx.x == 0 && cnt == 1)
+            atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), 1ull);
+        return;
+    }
+    for (u32 i = threadIdx.x; i < kHsSlots; i += blockDim.x) {
+        tk[i] = kHsEmpty;
+        tc[i] = 0;
+        if (EMIT) ts[i] = kHsEmpty;
+    }
+    if (threadIdx.x == 0) {
+        s_nheads = 0;
+        s_cursor = 0;
+    }
+    __syncthreads();
+    const uint2* e = pe + u64(b) * p + beg;
+    uint2 v[kHsPer];
+    u32 slot[kHsPer], rk[kHsPer];
+#pragma unroll
+    for (int q = 0; q < kHsPer; ++q) {
+        const u32 i = q * blockDim.x + threadIdx.x;
+        v[q] = i < cnt ? __ldg(e + i) : make_uint2(0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < kHsPer; ++q) {
+        const u32 i = q * blockDim.x + threadIdx.x;
+        if (i < cnt) {
+            const u32 u = v[q].x;  // the whole key w (partitions are hashed, M <= 31: never kHsEmpty)
+            u32 h = hs_hash(u);
+            for (;;) {
+                const u32 old = atomicCAS(tk + h, kHsEmpty, u);
+                if (old == kHsEmpty || old == u) break;
+                h = (h + 1) & (kHsSlots - 1);
+            }
+            slot[q] = h;
+            rk[q] = atomicAdd(tc + h, 1u);
+        }
+    }
+    __syncthreads();
+    if (!EMIT) {
+        u64 pa = 0, wa = 0;
+        for (u32 s0 = threadIdx.x; s0 < kHsSlots; s0 += blockDim.x) {
+            const u32 u = tk[s0];
+            if (u == kHsEmpty) continue;
+            const u64 cx = tc[s0];
+            if (c == 0) {
+                pa += cx * cx;
+                wa += cx * (cx - 1) / 2;
+            } else if (!(u & 1u)) {
+                const u32 h2 = hs_find(tk, u | 1u);
+                if (h2 != kHsEmpty) {
+                    const u64 cz = tc[h2];
+                    pa += 2 * cx * cz;
+                    wa += cx * cz;
+                }
+            }
+        }
+        pa = warp_sum(pa);
+        wa = warp_sum(wa);
+        if (lane == 0) {
+            red[0][wid] = pa;
+            red[1][wid] = wa;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u64 a = 0, w = 0;
+            for (int q = 0; q < nw; ++q) {
+                a += red[0][q];
+                w += red[1][q];
+            }
+            if (a) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(a));
+            if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
+        }
+        return;
+    }
+    // Only keys that are in a block are grouped: each block head (c == 0: a key
+    // with >= 2 records; else an even key whose partner key is present)
+    // reserves its grouped range with a shared atomic (order is irrelevant);
+    // records of keys in no block are dropped — no pair references them.
+    for (u32 h = threadIdx.x; h < kHsSlots; h += blockDim.x) {
+        const u32 u = tk[h];
+        if (u == kHsEmpty) continue;
+        if (c == 0) {
+            const u32 cx = tc[h];
+            if (cx < 2) continue;
+            heads[atomicAdd(&s_nheads, 1u)] = h;
+            ts[h] = atomicAdd(&s_cursor, cx);
+        } else if (!(u & 1u)) {
+            const u32 h2 = hs_find(tk, u | 1u);
+            if (h2 == kHsEmpty) continue;
+            heads[atomicAdd(&s_nheads, 1u)] = h;
+            const u32 base = atomicAdd(&s_cursor, tc[h] + tc[h2]);
+            ts[h] = base;
+            ts[h2] = base + tc[h];
+        }
+    }
+    __syncthreads();
+    const u32 nheads = s_nheads, used = s_cursor;
+    if (nheads == 0) return;
+#pragma unroll
+    for (int q = 0; q < kHsPer; ++q) {
+        const u32 i = q * blockDim.x + threadIdx.x;
+        if (i < cnt && ts[slot[q]] != kHsEmpty) sg[ts[slot[q]] + rk[q]] = v[q].y;
+    }
+    __syncthreads();
+    const u64 off = u64(b) * p;
+    for (u32 i = threadIdx.x; i < used; i += blockDim.x) grouped[off + beg + i] = sg[i];
+    const PartMap pm(c);
+    auto block_of = [&](u32 t) {
+        HeadBlock hb;
+        const u32 h = heads[t];
+        const u32 cx0 = tc[h];
+        if (c == 0) {
+            hb.pairs = u64(cx0) * cx0;
+            hb.work = u64(cx0) * (cx0 - 1) / 2;
+            hb.hs = beg + ts[h]; hb.hc = cx0; hb.ss = hb.hs; hb.sc = cx0; hb.flags = 3u;
+            return hb;
+        }
+        const u32 u = tk[h];
+        const u32 h2 = hs_find(tk, u | 1u);
+        const u32 ve = pm.inv(u);
+        const bool even_x = ve < (ve ^ c);
+        const u32 hx = even_x ? h : h2, hz = even_x ? h2 : h;
+        const u32 bx = beg + ts[hx], cx = tc[hx], bz = beg + ts[hz], cz = tc[hz];
+        hb.pairs = 2ull * cx * cz;
+        hb.work = u64(cx) * cz;
+        if (cx <= cz) {
+            hb.hs = bx; hb.hc = cx; hb.ss = bz; hb.sc = cz; hb.flags = 1u;
+        } else {
+            hb.hs = bz; hb.hc = cz; hb.ss = bx; hb.sc = cx; hb.flags = 0u;
+        }
+        return hb;
+    };
+    const bool pair_list = npairs != nullptr;
+    u32 my_items = 0, my_pairs = 0;
+    for (u32 h = threadIdx.x; h < nheads; h += blockDim.x) {
+        const HeadBlock hb = block_of(h);
+        u32 ne, np, nsc;
+        emit_count(hb, hmax, pair_list, ne, np, nsc);
+        my_items += ne;
+        my_pairs += np;
+    }
+    u32 ti, tp;
+    u32 ibase = block_exclusive(my_items, ws, &ti);
+    u32 pbase = block_exclusive(my_pairs, ws + 33, &tp);
+    if (ti == 0 && tp == 0) return;
+    if (threadIdx.x == 0) {
+        ws[66] = ti ? atomicAdd(nitems, ti) : 0u;
+        ws[67] = (pair_list && tp) ? atomicAdd(npairs, tp) : 0u;
+    }
+    __syncthreads();
+    ibase += ws[66];
+    pbase += ws[67];
+    emit_blocks_coop(block_of, nheads, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap,
+                     grouped, sg, beg);
+}
+
+// Dynamic shared memory of the hashed join: keys + counts (+ starts, grouped
+// columns and block heads for the emitting kernel).
+inline size_t part_hash_smem(bool emit) { return size_t(2 * kHsSlots + (emit ? kHsSlots + 2 * kHsCap : 0)) * 4; }
+
+// Partition digits of the hashed path: mean partition <= 0.85 kHsCap (a
+// balanced partition stays below kHsCap by > 6 standard deviations).
+inline int part_digits_hash(int M, u64 p) {
+    int k = 1;
+    while (k < kPgMaxK && k < M - 1 && (p >> k) > u64(kHsCap) * 85 / 100) ++k;
+    return std::min(k, M - 1);
+}
+
+// The partitioned path (u32 keys, M <= 31). k partition digits; scratch:
+// pcnt / cursor B * 2^k u32, pbeg B * (2^k + 1) u32; pe: B * p (w, column).
+inline u64 part_scratch_words(int k, u64 B) { return B * ((u64(1) << k) * 3 + 1); }
+
+inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, bool hashed, const u32* xorc,
+                                  u64* tot, u64* work_run, u32* scratch, uint2* pe, cudaStream_t st) {
+    const int lb = M - k;
     const u64 D = u64(1) << k;
     u32* pcnt = scratch;
     u32* cursor = scratch + B * D;
@@ -454,18 +701,20 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, const u3
     }
     XYZB_CUDA(cudaMemsetAsync(pcnt, 0, B * D * 4, st));
     dim3 gt(static_cast<u32>(ceil_div(p, kPgTile)), static_cast<u32>(B));
-    part_count<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, xorc, pcnt);
+    part_count<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, hashed ? 1 : 0, xorc, pcnt);
     XYZB_LAUNCH_CHECK();
     part_scan<<<static_cast<u32>(B), 1024, 0, st>>>(pcnt, k, p, pbeg, cursor, tot, work_run);
     XYZB_LAUNCH_CHECK();
-    part_scatter<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, xorc, cursor, pe);
+    part_scatter<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, hashed ? 1 : 0, xorc, cursor, pe);
     XYZB_LAUNCH_CHECK();
 }
 
-inline void part_join_launch(u64 B, u64 p, int M, const u32* xorc, u64 guard, u32 hmax, u32* grouped, u64* tot,
-                             u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
-                             u32 pair_cap, const u32* scratch, const uint2* pe, cudaStream_t st) {
-    const int lb = part_local_bits(M, p), k = M - lb;
+// hash: the hashed join (ovf raised when a partition exceeds kHsCap records).
+inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* xorc, u64 guard, u32 hmax,
+                             u32* grouped, u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap,
+                             u32* npairs, PairRec* pairs, u32 pair_cap, const u32* scratch, const uint2* pe,
+                             u32* ovf, cudaStream_t st) {
+    const int lb = M - k;
     const u64 D = u64(1) << k;
     const u32* pbeg = scratch + 2 * B * D;
     static bool attr = false;
@@ -475,6 +724,23 @@ inline void part_join_launch(u64 B, u64 p, int M, const u32* xorc, u64 guard, u3
         attr = true;
     }
     dim3 gj(static_cast<u32>(D), static_cast<u32>(B));
+    if (hash) {
+        static bool hattr = false;
+        if (!hattr) {
+            XYZB_CUDA(cudaFuncSetAttribute(part_join_hash<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(part_hash_smem(true))));
+            XYZB_CUDA(cudaFuncSetAttribute(part_join_hash<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(part_hash_smem(true))));
+            hattr = true;
+        }
+        part_join_hash<0><<<gj, kHsThreads, part_hash_smem(false), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot, work_run,
+                                                     items, nitems, item_cap, npairs, pairs, pair_cap, ovf);
+        XYZB_LAUNCH_CHECK();
+        part_join_hash<1><<<gj, kHsThreads, part_hash_smem(true), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot, work_run,
+                                                     items, nitems, item_cap, npairs, pairs, pair_cap, ovf);
+        XYZB_LAUNCH_CHECK();
+        return;
+    }
     part_join<0><<<gj, kPjThreads, (size_t(1) << lb) * 4, st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
                                                             work_run, items, nitems, item_cap, npairs, pairs,
                                                             pair_cap);

@@ -605,3 +605,46 @@ def test_tiled_verify_vs_oracle(case, monkeypatch):
         assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
             want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (n, p, m)
         assert len(want.hits) > 0
+
+
+@pytest.mark.parametrize("case", ["sparse", "wide_keys", "constant_y", "guard", "skewed_overflow", "forced_sort"])
+def test_hashed_partition_grouping_vs_oracle(case, monkeypatch):
+    """Sparse bucket spaces (2^M > 4p + 1024, M <= 31): the partition pass
+    plus one CTA per (run, partition) with an open-addressing hash table in
+    shared memory. Covers M up to 31, c = all ones, guard aborts, a skewed
+    key distribution whose partitions overflow the table (the search is then
+    redone on the sorted path), and the sorted path forced. Bit-exact
+    against the restatement."""
+    xb = _engine()
+    rng = np.random.default_rng(29)
+    guard = None
+    if case == "sparse":
+        cases = [(12, 300), (16, 2000), (20, 50000), (22, 30000)]
+    elif case == "wide_keys":
+        cases = [(26, 40000), (31, 20000)]
+    elif case == "constant_y":
+        cases = [(20, 50000), (14, 900)]
+    elif case == "guard":
+        cases = [(18, 20000)]
+        guard = 1
+    elif case == "forced_sort":
+        monkeypatch.setenv("XYZB_GROUPING", "sort")
+        cases = [(20, 50000)]
+    else:
+        cases = [(21, 100000)]
+    for t, (m, p) in enumerate(cases):
+        n = 64
+        if case == "skewed_overflow":  # columns with few +1 rows: most keys share their top bits
+            signs = np.where(rng.random((n, p)) < rng.uniform(0.01, 0.2, p), 1, -1).astype(np.int8)
+            x = xb.PackedMatrix.from_signs(signs)
+        else:
+            x = ck.ref_rademacher(n, p, 1300 + t, 3)
+        y = np.ones(n, np.int8) if case == "constant_y" else np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        cfg = xb.SearchConfig(m=m, l=2, gamma=0.7, seed=t, threads=1, top_k=20, estimate_complexity=False,
+                              max_candidates_per_rep=(p // 20 if guard else 0))
+        got = xb.Dataset(x).search(y, cfg)
+        want = ck.oracle_search(x, y, cfg)
+        ok, msg = ck.same_hits(got, want)
+        assert ok, (m, p, msg)
+        assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
+            want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
