@@ -55,6 +55,7 @@ WORKLOADS = {
                   transform="none", ref_sample_l=2),
 }
 WORKLOAD = WORKLOADS["gwas"]
+E2E_INFLIGHT = 4  # (X, y) jobs in flight in the end-to-end measurement (tools/e2e_pipeline.py: 1-4 measured)
 METRIC = ""
 REF_SAMPLE_L = 25
 
@@ -550,7 +551,7 @@ def main():
             torch.cuda.synchronize(local)
             e2e_s += time.perf_counter() - t0
             e2e_runs += 2 * L * world
-        # the same steps with three in flight (three host threads, one dataset and stream each): the H2D
+        # the same steps with E2E_INFLIGHT in flight (host threads, one dataset and stream each): the H2D
         # and host work of one step overlap the searches of the others, as a serving process with many
         # (X, y) jobs runs them
         pipe_s, pipe_runs = 0.0, 0
@@ -564,8 +565,8 @@ def main():
                 return r3
 
             nstep = 24
-            with ThreadPoolExecutor(3) as ex, ClockSampler(local) as e2e_clk:
-                for f in [ex.submit(step) for _ in range(3)]:  # untimed warm-up of the threads
+            with ThreadPoolExecutor(E2E_INFLIGHT) as ex, ClockSampler(local) as e2e_clk:
+                for f in [ex.submit(step) for _ in range(E2E_INFLIGHT)]:  # untimed warm-up of the threads
                     f.result()
                 torch.cuda.synchronize(local)
                 t0 = time.perf_counter()
@@ -585,7 +586,7 @@ def main():
                 out["e2e"] = {"value": pipe_runs / pipe_s, "unit": "runs/s", "h2d_bytes_per_step": h2d,
                               "d2h_bytes_per_step": d2h, "serial_value": serial, "clocks": e2e_clk.summary(),
                               "note": "every step: a fresh Dataset (H2D of X from pinned host memory + bit "
-                                      "transpose) + search + hits to host; three steps in flight on three host "
+                                      f"transpose) + search + hits to host; {E2E_INFLIGHT} steps in flight on {E2E_INFLIGHT} host "
                                       "threads (wall clock over all steps); serial_value: one step at a time"}
             else:
                 out["e2e"] = {"value": serial, "unit": "runs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
