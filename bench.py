@@ -55,6 +55,12 @@ WORKLOADS = {
                   transform="none", ref_sample_l=2),
 }
 WORKLOAD = WORKLOADS["gwas"]
+# what bounds each stage: the grouping + join kernels move few bytes per key
+STAGE_BOUND = {"project": "hbm/l2: M row-plane words read + keys written",
+               "sort": "issue: fused group + join (shared-memory atomics, barriers, pair emission); "
+                       "algorithmic bytes count keys + grouped indices only",
+               "join": "hbm: pair expansion of large blocks + run bookkeeping (or the partition join)",
+               "verify": "l2 gather when X fits in L2 (see l2_roofline), else hbm"}
 E2E_INFLIGHT = 4  # (X, y) jobs in flight in the end-to-end measurement (tools/e2e_pipeline.py: 1-4 measured)
 METRIC = ""
 REF_SAMPLE_L = 25
@@ -508,10 +514,11 @@ def main():
             "stage_roofline": {k: {"algorithmic_bytes": stage_b[k] / args.steps,
                                    "gbps": stage_b[k] / (stage[k] / 1e3) / 1e9 if stage.get(k) else None,
                                    "frac_of_hbm": (stage_b[k] / (stage[k] / 1e3) / 1e9) / peaks()[0]
-                                   if stage.get(k) else None}
+                                   if stage.get(k) else None,
+                                   "bound": STAGE_BOUND[k]}
                                for k in ("project", "sort", "join", "verify") if stage_b.get(k)},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "verify_pairs_binary" if WORKLOAD["mode"] == "binary" else "verify_items<RealStrength>", "achieved": achieved, "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": "verify_pairs_simple/_binary (pair-list verify)" if WORKLOAD["mode"] == "binary" else "verify_items_real<RealStrength>", "achieved": achieved, "peak": hbm,
                          "peak_source": src, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
                          "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                          "algorithmic_bytes_per_launch": verify_bytes / max(1, verify_launches),
