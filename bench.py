@@ -490,7 +490,7 @@ def main():
         ach = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
             else 0.0
         if g:
-            l2_roof = {"bound": "l2 (X resident)", "kernel": "verify_pairs_binary", "achieved": ach, "peak": g,
+            l2_roof = {"bound": "l2 (X resident)", "kernel": "verify_pairs_simple/_binary (pair-list verify)", "achieved": ach, "peak": g,
                        "unit": "GB/s", "frac": ach / g,
                        "peak_source": "measured live: random column-pair gather + XOR-popcount probe on an X of "
                                       "this shape (paper_1610_05108_b200/csrc/probe.cu), same byte count"}
