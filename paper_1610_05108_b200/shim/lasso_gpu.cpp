@@ -10,7 +10,8 @@
 // the caller's CenteredDesignView), the screen runs on the GPU through the
 // xyz_search shim, and the solver, the lambda grid and the exhaustive
 // certificate are the reference's own functions (active_set_solve,
-// auto_lambda_grid, exhaustive_kkt_max_correlation, lasso.o unchanged). The
+// exhaustive_kkt_max_correlation, lasso.o unchanged; the automatic lambda
+// grid's correlations also run on the device, lambda_grid). The
 // reference's definitions of these two entry points are weak symbols in the
 // drop-in build (objcopy --weaken-symbol, shim/Makefile), so this file
 // replaces them at link time without touching the reference sources.
@@ -20,8 +21,11 @@
 // a different order, so correlations agree to a few ulps and the path's
 // coefficients to the solver's tolerance (tests/test_dropin.py).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <set>
 #include <stdexcept>
@@ -183,12 +187,71 @@ private:
     RealVector nu_sq_;
 };
 
+// XYZB_LASSO_STATS=1: where lasso_path's time goes (printed per call).
+struct LassoStats {
+    using clock = std::chrono::steady_clock;
+    double solve = 0, scans = 0, screen = 0, setup = 0;
+    clock::time_point t = clock::now();
+    double lap() {
+        const auto now = clock::now();
+        const double d = std::chrono::duration<double>(now - t).count();
+        t = now;
+        return d;
+    }
+};
+
 std::vector<PairKey> all_off_diagonal(std::size_t p) {
     std::vector<PairKey> out;
     out.reserve(p * (p - 1) / 2);
     for (std::uint32_t j = 0; j + 1 < p; ++j)
         for (std::uint32_t k = j + 1; k < p; ++k) out.push_back({j, k});
     return out;
+}
+
+// auto_lambda_grid (lasso.cpp:232-268) with its correlations on the device:
+// lambda_1 = the largest |centered correlation| / n of a main column or of an
+// interaction column with centered y (every pair for p <= 512, else the
+// reference's sample of min(1e5, 10p) pairs drawn from make_stream(seed,
+// 0xa117)), then t log-spaced values down to ratio * lambda_1.
+std::vector<double> lambda_grid(const RealMatrix& x, const RealVector& y, std::size_t t, double ratio,
+                                std::uint64_t seed, bool binary, const DeviceScans& gpu) {
+    if (t < 2) throw data_error("auto_lambda_grid: grid size must be >= 2");
+    if (!(ratio > 0.0 && ratio < 1.0)) throw data_error("auto_lambda_grid: ratio must lie in (0,1)");
+    if (y.size() != x.n_rows()) throw data_error("auto_lambda_grid: response length mismatch");
+    const std::size_t p = x.n_cols();
+    RealVector yc(y);
+    double ysum = 0.0;
+    for (const double v : yc) ysum += v;
+    const double ybar = ysum / static_cast<double>(yc.size());
+    double yvar = 0.0;
+    for (double& v : yc) {
+        v -= ybar;
+        yvar += v * v;
+    }
+    if (yvar <= 0.0) throw data_error("auto_lambda_grid: response has zero variance");
+    std::vector<PairKey> keys;
+    if (p <= 512) {
+        for (std::uint32_t j = 0; j < p; ++j)
+            for (std::uint32_t k = j; k < p; ++k)
+                if (!(binary && j == k)) keys.push_back({j, k});
+    } else {
+        std::mt19937_64 rng = make_stream(seed, 0xa117);
+        std::uniform_int_distribution<std::uint32_t> dist(0, static_cast<std::uint32_t>(p - 1));
+        const std::size_t samples = std::min<std::size_t>(100000, 10 * p);
+        keys.reserve(samples);
+        for (std::size_t s = 0; s < samples; ++s) {
+            const std::uint32_t j = dist(rng), k = dist(rng);
+            if (binary && j == k) continue;
+            keys.push_back(make_pair_key(j, k));
+        }
+    }
+    double lmax = 0.0;  // max(|corr| / n) == max(|corr|) / n: division is monotonic
+    for (const double v : gpu.mains(yc)) lmax = std::max(lmax, v);
+    for (const double v : gpu.pairs(yc, keys)) lmax = std::max(lmax, v);
+    std::vector<double> grid(t);
+    for (std::size_t i = 0; i < t; ++i)
+        grid[i] = lmax * std::pow(ratio, static_cast<double>(i) / static_cast<double>(t - 1));
+    return grid;
 }
 
 } // namespace
@@ -230,7 +293,8 @@ std::vector<SparseFit> lasso_path(const RealMatrix& x, const RealVector& y, cons
     if (y.size() != x.n_rows()) throw data_error("lasso_path: response length mismatch");
     const std::size_t n = x.n_rows(), p = x.n_cols();
     LassoPathConfig config = config_in;
-    if (entries_are_pm1(x)) config.exclude_diagonal = true;  // no square terms for +-1 data
+    const bool binary = entries_are_pm1(x);
+    if (binary) config.exclude_diagonal = true;  // no square terms for +-1 data
 
     RealVector yc(y);
     double ysum = 0.0;
@@ -238,18 +302,20 @@ std::vector<SparseFit> lasso_path(const RealMatrix& x, const RealVector& y, cons
     const double ybar = ysum / static_cast<double>(yc.size());
     for (double& v : yc) v -= ybar;
 
+    LassoStats st;
+    const CenteredDesignView view(x);
+    const DeviceScans gpu(x, view);
     std::vector<double> lambdas = config.lambdas;
     if (lambdas.empty()) {
-        lambdas = auto_lambda_grid(x, y, config.grid_size, config.grid_ratio, config.seed);
+        lambdas = lambda_grid(x, y, config.grid_size, config.grid_ratio, config.seed, binary, gpu);
     } else {
         for (std::size_t i = 0; i < lambdas.size(); ++i)
             if (!(lambdas[i] > 0.0) || !(i == 0 || lambdas[i - 1] > lambdas[i]))
                 throw data_error("lasso_path: lambda grid must be strictly decreasing and positive");
     }
 
-    const CenteredDesignView view(x);
     const ProductScreen screen(x, config);
-    const DeviceScans gpu(x, view);
+    st.setup += st.lap();
     std::vector<PairKey> squares;
     if (!config.exclude_diagonal) {
         squares.resize(p);
@@ -286,10 +352,12 @@ std::vector<SparseFit> lasso_path(const RealMatrix& x, const RealVector& y, cons
             if (iterations >= config.max_active_set_iterations)
                 throw solver_error("lasso_path: active set did not close at lambda index " + std::to_string(li));
             ++iterations;
+            st.lap();
             solved = active_set_solve(view, active_main, active_pairs, yc, lambda, config,
                                       have_warm || iterations > 1 ? &warm : nullptr);
             warm = solved.fit;
             have_warm = true;
+            st.solve += st.lap();
 
             // exact main-effect sweep (device)
             kkt_max = -std::numeric_limits<double>::infinity();
@@ -314,9 +382,11 @@ std::vector<SparseFit> lasso_path(const RealMatrix& x, const RealVector& y, cons
             const double screen_threshold = pair_threshold - 2.0 * view.max_abs_column_mean() * max_main;
             bool degenerate = screen_threshold <= 0.0;
             std::vector<PairKey> cand;
+            st.scans += st.lap();
             if (!degenerate)
                 cand = screen.candidates(solved.residual, screen_threshold,
                                          li * config.max_active_set_iterations + iterations, degenerate);
+            st.screen += st.lap();
             if (degenerate) {
                 degenerate_seen = true;
                 if (p > 2000)
@@ -357,7 +427,11 @@ std::vector<SparseFit> lasso_path(const RealMatrix& x, const RealVector& y, cons
         }
         path.push_back(fit);
         warm = path.back();
+        st.scans += st.lap();
     }
+    if (std::getenv("XYZB_LASSO_STATS"))
+        std::fprintf(stderr, "[lasso_path gpu] setup %.3f s, solve %.3f s, scans %.3f s, screens %.3f s\n", st.setup,
+                     st.solve, st.scans, st.screen);
     return path;
 }
 

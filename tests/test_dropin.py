@@ -163,3 +163,25 @@ def test_design_correlations_vs_numpy():
                                                  1, pout.ctypes.data_as(f64), err, _abi.ERRBUF) == 3
     finally:
         lib.xyzb_design_destroy(d)
+
+
+def test_dropin_unbiased_range_error_matches_reference():
+    """Entries outside [-1, 1] with the unbiased transform: the same data_error
+    (code 3, same message) from the drop-in (checked by the engine against the
+    resident matrix) as from the reference (search.cpp:417-434)."""
+    from paper_1610_05108_b200.matrix import RealMatrix
+    from paper_1610_05108_b200.report import SearchConfig
+    rng = np.random.default_rng(3)
+    xv = rng.uniform(-1, 1, (40, 64))
+    xv[7, 5] = 1.5
+    x = RealMatrix(xv)
+    y = rng.normal(size=64)
+    cfg = SearchConfig(m=4, l=2, gamma=0.6, mode="continuous_xy", transform="unbiased")
+    with pytest.raises(ck.CheckerError) as a:
+        ck.ref_search(x, y, cfg)
+    with pytest.raises(ck.CheckerError) as b:
+        ck.dropin_search(x, y, cfg)
+    assert a.value.code == b.value.code == 3
+    assert str(a.value) == str(b.value)
+    xv[7, 5] = 1.0  # in range again: the same pointer, new contents -> re-upload, no error
+    ck.dropin_search(RealMatrix(xv), y, cfg)
