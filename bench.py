@@ -518,12 +518,15 @@ def main():
                                    "bound": STAGE_BOUND[k]}
                                for k in ("project", "sort", "join", "verify") if stage_b.get(k)},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "verify_pairs_simple/_binary (pair-list verify)" if WORKLOAD["mode"] == "binary" else "verify_items_real<RealStrength>", "achieved": achieved, "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": ("verify_pairs_simple/_binary (pair-list verify)" if WORKLOAD["mode"] == "binary" else
+                                    "verify_items_sign (sign bits x response bit planes)"
+                                    if WORKLOAD.get("transform") == "sign" else "verify_items_real<RealStrength>"), "achieved": achieved, "peak": hbm,
                          "peak_source": src, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
                          "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                          "algorithmic_bytes_per_launch": verify_bytes / max(1, verify_launches),
-                         "note": "algorithmic bytes = 2 columns per canonical candidate + Y (SURVEY 8d); when X "
-                                 "fits in L2 (cfg1-3) the verify kernel can exceed the HBM roofline"},
+                         "note": "algorithmic bytes = 2 columns per canonical candidate + Y (SURVEY 8d; the sign "
+                                 "transform's columns are sign bits); when X fits in L2 (cfg1-3) the verify "
+                                 "kernel can exceed the HBM roofline"},
             "clocks": clk.summary(),
             "l2_roofline": l2_roof,
             "planted_found": sorted({(min(h.j, h.k), max(h.j, h.k)) for h in rep.hits} &

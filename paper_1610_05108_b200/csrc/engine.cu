@@ -235,18 +235,19 @@ struct xyzb_dataset {
     DevBuf Xc32;   // f32 [p][n4]
     DevBuf Xr64;   // f64 [n][p]
     DevBuf Xpos, Xzero;  // u32 [n][P32]
+    DevBuf Spos, Snz;    // u64 [p][W] column sign bits (x > 0, x != 0): the sign transform's bit-plane verify
     bool has_zero = false, in_unit = true;
     // response (per search)
     DevBuf yk_bits, spos, sneg, wabs, yreal, yreal32;
     // batch scratch
     DevBuf keys[2], vals[2], keys_x, hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent, pairs_t, tscratch, bstart, povf;
+    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent, pairs_t, tscratch, bstart, povf, yplanes;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
     DevBuf tkeys, tvals, keep, kpos, kept, kept_order, fin, fin_order, tie, kbufA, kbufB, vbufA, vbufB, topidx, hcount;
     DevBuf pairs_dev, strengths_dev;
-    HostBuf h_rows, h_state, h_small, h_merge, h_status;
+    HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
     StageClock clock;
     u32 hit_cap = 1u << 16;
 };
@@ -530,6 +531,11 @@ void create_real(xyzb_dataset* ds, const Fill& fill) {
     dim3 tg(static_cast<u32>(ceil_div(ds->p, 32)), static_cast<u32>(ceil_div(ds->n, 32)));
     real::transpose_f64<<<tg, dim3(32, 8), 0, ds->stream>>>(xc64.as<double>(), ds->n, ds->p, ds->Xr64.as<double>());
     XYZB_LAUNCH_CHECK();
+    ds->Spos.ensure(ds->p * ds->W * 8);
+    ds->Snz.ensure(ds->p * ds->W * 8);
+    real::sign_cols<<<static_cast<u32>(std::min<u64>(ceil_div(ds->p * 32, 256), u64(kSMs) * 16)), 256, 0,
+                      ds->stream>>>(xc64.as<double>(), ds->n, ds->p, ds->W, ds->Spos.as<u64>(), ds->Snz.as<u64>());
+    XYZB_LAUNCH_CHECK();
     ds->Xpos.ensure(ds->n * ds->P32 * 4);
     ds->Xzero.ensure(ds->n * ds->P32 * 4);
     DevBuf flags;
@@ -611,6 +617,11 @@ struct SearchCtx {
     u64 item_cap = 0, nbatches = 0, pair_cap = 0;
     u64 item_scale = 1;  // grows when a batch overflows its item buffer
     u64 pair_scale = 1;  // grows when a batch overflows its pair list
+    // the sign transform's quantised response (bit planes, SignStrength)
+    int qB = kern::kSignQB;
+    double qinv = 0.0, qdelta = 0.0;
+    long long qsum = 0;
+    bool sign_verify = false;  // the bit-plane verify ran
     bool tiled = false;    // this attempt verifies the accumulated pair list in column tiles
     bool no_tile = false;  // the accumulated list would exceed 2^32 pairs: per-batch verify
     bool no_hash = false;  // a hashed partition overflowed: the sparse grouping runs on the sorted path
@@ -694,6 +705,31 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
     std::copy(y, y + n, yp);
     ds->yreal.ensure(n4 * 8);
     XYZB_CUDA(cudaMemcpyAsync(ds->yreal.p, yp, n4 * 8, cudaMemcpyHostToDevice, st));
+    if (c.q->transform == XYZB_TRANSFORM_SIGN) {
+        // q_i = rint(y_i * scale) as two's-complement bit planes 0..B over the row words (SignStrength)
+        double ymax = 0.0;
+        for (u64 i = 0; i < n; ++i) ymax = std::max(ymax, std::abs(y[i]));
+        const int B = c.qB;
+        const double scale = (std::ldexp(1.0, B) - 1.0) / ymax;  // |q| <= 2^B - 1: B + 1 two's-complement bits
+        const u64 W = ds->W;
+        ds->h_planes.ensure(u64(B + 1) * W * 8);
+        u64* pl = ds->h_planes.as<u64>();
+        std::memset(pl, 0, u64(B + 1) * W * 8);
+        long long qs = 0;
+        for (u64 i = 0; i < n; ++i) {
+            const long long q = std::llrint(y[i] * scale);
+            qs += q;
+            const unsigned long long u = static_cast<unsigned long long>(q);
+            for (int b = 0; b <= B; ++b)
+                if ((u >> b) & 1ull) pl[u64(b) * W + (i >> 6)] |= 1ull << (i & 63);
+        }
+        c.qinv = 1.0 / scale;
+        c.qsum = qs;
+        // |quantised - exact| <= 1.5 n / (2 scale norm); + 1e-6 for the fp32 columns of RealStrength
+        c.qdelta = 1.5 * double(n) / (2.0 * scale * norm) + 1e-6;
+        ds->yplanes.ensure(u64(B + 1) * W * 8);
+        XYZB_CUDA(cudaMemcpyAsync(ds->yplanes.p, pl, u64(B + 1) * W * 8, cudaMemcpyHostToDevice, st));
+    }
 }
 
 // Runs of the search in execution order (pass +1 then -1, reps ascending;
@@ -1277,8 +1313,20 @@ void run_batches(SearchCtx& c) {
                 else kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
             } else {
                 kern::RealStrength<false> f{ds->Xc32.as<float>(), ds->n4, ds->yreal32.as<float>(), c.norm, c.gamma};
-                if (ysmem) kern::verify_items_real<false><<<vgrid, 256, ysm, st>>>(A, f);
-                else kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
+                const char* sv_sel = std::getenv("XYZB_SIGN_VERIFY");
+                if (!(sv_sel && std::string(sv_sel) == "0") && ds->Spos.p) {
+                    // sign transform: strengths from column sign bits and the response's bit planes
+                    kern::SignStrength g{ds->Spos.as<u64>(), ds->Snz.as<u64>(), ds->W, ds->yplanes.as<u64>(),
+                                         c.qsum, ds->has_zero, c.qinv, c.norm, c.gamma, c.qdelta, f};
+                    const size_t psm = size_t(c.qB + 1) * ds->W * 8;
+                    kern::verify_items_sign<kern::kSignQB>
+                        <<<vgrid, 256, (ds->W > 32 && psm <= (size_t(48) << 10)) ? psm : 0, st>>>(A, g);
+                    c.sign_verify = true;
+                } else if (ysmem) {
+                    kern::verify_items_real<false><<<vgrid, 256, ysm, st>>>(A, f);
+                } else {
+                    kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
+                }
             }
         }
         XYZB_LAUNCH_CHECK();
@@ -1746,9 +1794,15 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         out->verify_kernel_ms += m2;
     }
     out->verify_launches = c.verify_spans.size();
-    // algorithmic verify bytes: 2 columns per canonical pair + Y
-    const u64 colbytes = c.mode == XYZB_MODE_CONTINUOUS_XY ? 4 * c.n : 8 * ceil_div(c.n, 64);
-    c.bytes[XYZB_STAGE_VERIFY] = ver * 2 * colbytes + colbytes;
+    // algorithmic verify bytes: 2 columns per canonical pair + Y (the sign transform's bit-plane verify:
+    // 2 sign-bit columns (+ 2 nonzero masks when X has zeros) per pair + the response's bit planes)
+    const u64 wb = 8 * ceil_div(c.n, 64);
+    if (c.sign_verify)
+        c.bytes[XYZB_STAGE_VERIFY] = ver * 2 * wb * (ds->has_zero ? 2 : 1) + u64(c.qB + 1) * wb;
+    else {
+        const u64 colbytes = c.mode == XYZB_MODE_CONTINUOUS_XY ? 4 * c.n : wb;
+        c.bytes[XYZB_STAGE_VERIFY] = ver * 2 * colbytes + colbytes;
+    }
     u64 tl = 0;
     for (int s = 0; s < XYZB_NUM_STAGES; ++s) {
         out->stage_bytes[s] = c.bytes[s];

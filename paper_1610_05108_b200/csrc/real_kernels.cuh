@@ -200,6 +200,29 @@ __global__ void __launch_bounds__(kMtThreads) unbiased_keys(const u64* __restric
 // ---- dataset preparation for real X ----
 
 // Xc64 [p][n] column-major -> Xc32 [p][n4] (fp32, zero padded)
+// Column-major sign bits of the fp64 matrix (the sign transform's t(x) in
+// {-1, 0, 1}, search.cpp:456-462): bit i of word w of column j is
+// x[64w + i, j] > 0 (Spos) / != 0 (Snz). One warp per column, two ballots
+// per word. For the bit-plane verify of the sign transform.
+__global__ void sign_cols(const double* __restrict__ Xc64, u64 n, u64 p, u64 Wn, u64* __restrict__ Spos,
+                          u64* __restrict__ Snz) {
+    const int lane = threadIdx.x & 31;
+    const u64 nw = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 j = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < p; j += nw) {
+        const double* col = Xc64 + j * n;
+        for (u64 w = 0; w < Wn; ++w) {
+            const u64 i0 = 64 * w + lane, i1 = i0 + 32;
+            const double a = i0 < n ? col[i0] : 0.0, b = i1 < n ? col[i1] : 0.0;
+            const u64 pos = u64(__ballot_sync(0xffffffffu, a > 0.0)) | (u64(__ballot_sync(0xffffffffu, b > 0.0)) << 32);
+            const u64 nz = u64(__ballot_sync(0xffffffffu, a != 0.0)) | (u64(__ballot_sync(0xffffffffu, b != 0.0)) << 32);
+            if (lane == 0) {
+                Spos[j * Wn + w] = pos;
+                Snz[j * Wn + w] = nz;
+            }
+        }
+    }
+}
+
 __global__ void to_f32_cols(const double* __restrict__ Xc64, u64 n, u64 p, u64 n4, float* __restrict__ Xc32) {
     const u64 total = p * n4;
     for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += u64(gridDim.x) * blockDim.x) {

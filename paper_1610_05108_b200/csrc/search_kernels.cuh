@@ -1245,5 +1245,111 @@ __global__ void __launch_bounds__(256) verify_items_real(VerifyArgs A, RealStren
     walk_items<32>(A, f);
 }
 
+// Sign-transform strengths from bit planes (continuous-XY, transform sign):
+// t(x) in {-1, 0, 1}, so sum_i y_i t_ij t_ik = 2 S(agree) - S(both) with
+// both = nz_j & nz_k, agree = both & ~(pos_j ^ pos_k) and S(m) = sum of y
+// over the rows of mask m. y is quantised once per search to integers
+// q_i = rint(y_i * scale) held as two's-complement bit planes P_0..P_B, so
+// S(m) = sum_b<B 2^b popc(P_b & m) - 2^B popc(P_B & m): a column pair costs
+// 2 x n/8 bytes of sign bits instead of 2 x 4n bytes of fp32 values. The
+// quantised strength is within `delta` of the fp32-column value; a pair at
+// or above gamma - delta is re-verified with RealStrength, so hits and their
+// strengths are those of the fp32 verify.
+constexpr int kSignQB = 12;  // response quantised to 13-bit two's complement (|q| <= 4095)
+struct SignStrength {
+    const u64 *Spos, *Snz;  // [p][Wn]
+    u64 Wn;
+    const u64* planes;  // [B + 1][Wn] (B: the kernel's QB)
+    long long qsum;  // sum of q over all rows (S(both) when X has no zero)
+    bool zeros;
+    double inv_scale, norm, gamma, delta;
+    RealStrength<false> exact;
+};
+
+__device__ __forceinline__ long long plane_sum(const u64* planes, u64 Wn, int B, u64 w, u64 m) {
+    long long s = 0;
+    for (int b = 0; b < B; ++b) s += (long long)__popcll(planes[u64(b) * Wn + w] & m) << b;
+    return s - ((long long)__popcll(planes[u64(B) * Wn + w] & m) << B);
+}
+
+// sum of q over the rows of a 64-row mask from register-held planes (QB <= 24:
+// |result| < 2^31)
+template <int QB>
+__device__ __forceinline__ int plane_sum_reg(const u64 (&pl)[QB + 1], u64 m) {
+    int s = 0;
+#pragma unroll
+    for (int b = 0; b < QB; ++b) s += __popcll(pl[b] & m) << b;
+    return s - (__popcll(pl[QB] & m) << QB);
+}
+
+// One warp per candidate pair. Rows <= 2048 (Wn <= 32 words): lane w keeps
+// word w of every response plane in registers for the whole kernel; longer
+// columns walk the words with the planes in shared memory (or L1).
+template <int QB>
+__global__ void __launch_bounds__(256) verify_items_sign(VerifyArgs A, SignStrength f) {
+    extern __shared__ __align__(16) u64 sh[];
+    const u64 nplane = u64(QB + 1) * f.Wn;
+    const bool in_reg = f.Wn <= 32;
+    const bool in_smem = !in_reg && nplane * 8 <= (size_t(48) << 10);
+    if (in_smem) {
+        for (u64 i = threadIdx.x; i < nplane; i += blockDim.x) sh[i] = f.planes[i];
+        __syncthreads();
+    }
+    const u64* planes = in_smem ? sh : f.planes;
+    const int lane = threadIdx.x & 31;
+    u64 pl[QB + 1];
+#pragma unroll
+    for (int b = 0; b <= QB; ++b) pl[b] = in_reg && u64(lane) < f.Wn ? f.planes[u64(b) * f.Wn + lane] : 0ull;
+    const u32 N = min(*A.nitems, A.item_cap);
+    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 t = warp; t < N; t += nwarps) {
+        const Item item = A.items[t];
+        if (A.tot[item.run] > A.guard) continue;
+        const u32 hc = item.hc_flags & 0xffu, flags = item.hc_flags >> 8;
+        const u32* svr = A.sv + u64(item.run) * A.S;
+        const bool pos_pass = A.run_sign[item.run] > 0;
+        for (u32 h = 0; h < hc; ++h) {
+            const u32 hpos = item.hs + h;
+            const u32 j = svr[hpos];
+            for (u32 q = 0; q < item.sc; ++q) {
+                const u32 spos = item.ss + q;
+                if ((flags & 2u) && spos <= hpos) continue;
+                const u32 k = svr[spos];
+                long long acc = 0;
+                if (in_reg) {
+                    if (u64(lane) < f.Wn) {
+                        const u64 w = lane;
+                        const u64 pj = __ldg(f.Spos + u64(j) * f.Wn + w), pk = __ldg(f.Spos + u64(k) * f.Wn + w);
+                        const u64 both =
+                            f.zeros ? (__ldg(f.Snz + u64(j) * f.Wn + w) & __ldg(f.Snz + u64(k) * f.Wn + w)) : ~0ull;
+                        int a = 2 * plane_sum_reg<QB>(pl, both & ~(pj ^ pk));
+                        if (f.zeros) a -= plane_sum_reg<QB>(pl, both);
+                        acc = a;
+                    }
+                } else {
+                    for (u64 w = lane; w < f.Wn; w += 32) {
+                        const u64 pj = __ldg(f.Spos + u64(j) * f.Wn + w), pk = __ldg(f.Spos + u64(k) * f.Wn + w);
+                        const u64 both = f.zeros ? (__ldg(f.Snz + u64(j) * f.Wn + w) &
+                                                    __ldg(f.Snz + u64(k) * f.Wn + w))
+                                                 : ~0ull;
+                        acc += 2 * plane_sum(planes, f.Wn, QB, w, both & ~(pj ^ pk));
+                        if (f.zeros) acc -= plane_sum(planes, f.Wn, QB, w, both);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (!f.zeros) acc -= f.qsum;
+                double s = 0.5 + (pos_pass ? 1.0 : -1.0) * (double(acc) * f.inv_scale) / (2.0 * f.norm);
+                if (s >= f.gamma - f.delta) s = f.exact(j, k, pos_pass, lane, 0xffffffffu);  // warp-uniform
+                const bool hit = lane == 0 && f.exact.hit(s);
+                DevHit hr;
+                if (hit) hr = make_hit(A, item.run, hpos, spos, flags, s, -1);
+                team_append<32>(A, 0xffffffffu, hit, hr);
+            }
+        }
+    }
+}
+
 } // namespace kern
 } // namespace xyzb
