@@ -648,3 +648,36 @@ def test_hashed_partition_grouping_vs_oracle(case, monkeypatch):
         assert ok, (m, p, msg)
         assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
             want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
+
+
+@pytest.mark.parametrize("n", [100, 2000, 3000])
+def test_sign_bit_verify_equals_fp32_verify(n, monkeypatch):
+    """The sign transform's bit-plane verify (column sign bits x quantised
+    response planes, re-verification within the quantisation bound) reports
+    exactly the hits and strengths of the fp32-column verify, with exact
+    zeros in X (nonzero masks) and without, for row counts on both sides of
+    the register-resident plane path (<= 2048 rows); and matches the
+    restatement within the continuous tolerance."""
+    xb = _engine()
+    rng = np.random.default_rng(n)
+    p = 3000
+    xv = rng.normal(size=(p, n))
+    if n != 2000:
+        xv[rng.random((p, n)) < 0.05] = 0.0  # exact zeros: the coin path for keys, nonzero masks here
+    y = xv[3] * xv[11] * 0.8 + rng.normal(size=n)
+    x = xb.RealMatrix(xv)
+    total = 0
+    for gamma in (0.52, 0.55):
+        cfg = xb.SearchConfig(m=9, l=6, gamma=gamma, seed=4, threads=1, top_k=30, mode="continuous_xy",
+                              transform="sign", estimate_complexity=False)
+        got = xb.Dataset(x).search(y, cfg)
+        monkeypatch.setenv("XYZB_SIGN_VERIFY", "0")
+        ref = xb.Dataset(x).search(y, cfg)
+        monkeypatch.delenv("XYZB_SIGN_VERIFY")
+        assert report_hits(got) == report_hits(ref), (n, gamma)
+        assert got.top_k == ref.top_k and got.verified_pairs == ref.verified_pairs
+        want = ck.oracle_search(x, y, cfg)
+        compare_continuous(report_hits(got), [(h.j, h.k, h.strength, h.found_at_repetition, h.sign)
+                                              for h in want.hits], gamma)
+        total += len(got.hits)
+    assert total > 0
