@@ -681,3 +681,22 @@ def test_sign_bit_verify_equals_fp32_verify(n, monkeypatch):
                                               for h in want.hits], gamma)
         total += len(got.hits)
     assert total > 0
+
+
+def test_hashed_grouping_batches_and_regrow_are_invisible(monkeypatch):
+    """The hashed partition join under multi-batch runs and forced item /
+    pair / hit buffer regrowth gives the unbatched, unregrown result."""
+    xb = _engine()
+    x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
+    cfg = xb.SearchConfig(m=14, l=10, gamma=0.55, seed=7, top_k=10)  # 2^14 > 4p + 1024: sparse
+    base = xb.Dataset(x).search(y, cfg)
+    monkeypatch.setenv("XYZB_BATCH_ENTRIES", "6000")
+    monkeypatch.setenv("XYZB_HIT_CAP", "7")
+    monkeypatch.setenv("XYZB_ITEM_CAP", "5")
+    monkeypatch.setenv("XYZB_PAIR_CAP", "100")
+    other = xb.Dataset(x).search(y, cfg)
+    assert report_hits(other) == report_hits(base) and other.top_k == base.top_k
+    assert (other.candidates_enumerated, other.verified_pairs) == (base.candidates_enumerated, base.verified_pairs)
+    want = ck.oracle_search(x, y, cfg)
+    ok, msg = ck.same_hits(base, want)
+    assert ok, msg
