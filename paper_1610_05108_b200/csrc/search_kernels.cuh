@@ -1286,7 +1286,7 @@ __device__ __forceinline__ int plane_sum_reg(const u64 (&pl)[QB + 1], u64 m) {
 // word w of every response plane in registers for the whole kernel; longer
 // columns walk the words with the planes in shared memory (or L1).
 template <int QB>
-__global__ void __launch_bounds__(256) verify_items_sign(VerifyArgs A, SignStrength f) {
+__global__ void __launch_bounds__(256, 4) verify_items_sign(VerifyArgs A, SignStrength f) {
     extern __shared__ __align__(16) u64 sh[];
     const u64 nplane = u64(QB + 1) * f.Wn;
     const bool in_reg = f.Wn <= 32;
