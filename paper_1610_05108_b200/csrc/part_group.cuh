@@ -245,7 +245,7 @@ __device__ __forceinline__ void part_table_scan(u32* T, u32 n, u32* ws) {
 }
 
 template <int EMIT>
-__global__ void __launch_bounds__(kPjThreads) part_join(const uint2* __restrict__ pe, const u32* __restrict__ pbeg,
+__global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restrict__ pe, const u32* __restrict__ pbeg,
                                                         u64 p, int M, int lb, const u32* __restrict__ xorc, u64 guard,
                                                         u32 hmax, u32* __restrict__ grouped, u64* __restrict__ tot,
                                                         u64* __restrict__ work_run, Item* __restrict__ items,
