@@ -95,7 +95,7 @@ def all_gather_bytes(buf: np.ndarray, device=None) -> List[np.ndarray]:
     size = torch.tensor([buf.size], dtype=torch.int64, device=dev)
     sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, size)
-    m = int(max(int(s.item()) for s in sizes))
+    m = max(1, int(max(int(s.item()) for s in sizes)))  # all-empty buffers still exchange one padded byte
     pad = np.zeros(m, np.uint8)
     pad[: buf.size] = buf
     t = torch.from_numpy(pad).to(dev)

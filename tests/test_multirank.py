@@ -91,6 +91,10 @@ def _worker(rank, world, port, out_dir):
     else:
         r = make_result([(9, 3, 0.75, 4, 1), (5, 6, 0.8, 3, 1), (2, 8, 0.3, 1, -1)], [70, 45, 205],
                         repetitions_run=2, candidates_enumerated=60)
+    # ragged and all-empty byte buffers survive the padded exchange
+    raw = parallel.all_gather_bytes(np.arange(3 + 5 * rank, dtype=np.uint8))
+    assert [b.tolist() for b in raw] == [list(range(3)), list(range(8))]
+    assert [b.size for b in parallel.all_gather_bytes(np.zeros(0, np.uint8))] == [0, 0]
     gathered = parallel.all_gather_bytes(parallel.pack_result(r))
     parts = [parallel.PackedPart(b) for b in gathered]
     merged = reference_merge(parts)
