@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define XYZB_ABI_VERSION 1
+#define XYZB_ABI_VERSION 2
 
 /* status codes */
 enum {
@@ -69,18 +69,30 @@ enum { XYZB_TRANSFORM_NONE = 0, XYZB_TRANSFORM_SIGN = 1, XYZB_TRANSFORM_UNBIASED
 
 typedef struct xyzb_dataset xyzb_dataset;
 
-/* The design matrix. Exactly one of x_words / x_real is set.
- *  x_words: binary X, column-major, W = ceil(n_rows/64) uint64 words per
- *           column, bit i%64 of word i/64 set iff X_ij = +1, padding bits 0
- *           (PackedMatrix, packed_matrix.hpp:10-14).
- *  x_real:  real X, column-major doubles (RealMatrix, real_matrix.hpp:13-33). */
+/* The design matrix. Exactly one of x_words / x_real / x_real32 is set.
+ *  x_words:  binary X, column-major, W = ceil(n_rows/64) uint64 words per
+ *            column, bit i%64 of word i/64 set iff X_ij = +1, padding bits 0
+ *            (PackedMatrix, packed_matrix.hpp:10-14).
+ *  x_real:   real X, column-major doubles (RealMatrix, real_matrix.hpp:13-33).
+ *  x_real32: real X, column-major floats (half the upload of x_real; the
+ *            search reads fp32 columns anyway; the fp64 comparisons of the
+ *            transforms see double(x), as a RealMatrix built from the floats).
+ * Devices: n_devices == 0 places the dataset on `device`. n_devices > 0
+ * replicates X on devices[0..n_devices) (X replicated, runs
+ * sharded): xyzb_search then splits the repetitions of each pass into
+ * contiguous shards, one per device (one host thread and stream each), and
+ * merges the shard results on devices[0] — the same report as one device.
+ * This replaces the std::thread waves of run_pass (search.cpp:59-111). */
 typedef struct {
     uint64_t n_rows;
     uint64_t n_cols;
     const uint64_t* x_words;
     const double* x_real;
-    int32_t device; /* CUDA ordinal */
+    int32_t device; /* CUDA ordinal (n_devices == 0) */
     int32_t flags;  /* reserved, 0 */
+    const float* x_real32;
+    const int32_t* devices;
+    uint64_t n_devices;
 } xyzb_problem;
 
 /* The response. Binary mode: y_sign (+1/-1 per row). Continuous modes: y_real. */
@@ -107,7 +119,19 @@ typedef struct {
     uint64_t top_k;     /* 0 = no top-K list; else K (A.10 comparator)       */
     uint64_t rep_begin; /* run shard: repetitions [rep_begin, rep_end) of     */
     uint64_t rep_end;   /* each pass, 1-based end-exclusive; 0,0 = all 1..L   */
+    int32_t top_k_mode; /* XYZB_TOPK_*                                        */
+    int32_t reserved;   /* 0                                                   */
 } xyzb_params;
+
+/* top_k_mode:
+ *  XYZB_TOPK_HITS        top-K of the hit list (strength >= gamma), A.10 order.
+ *  XYZB_TOPK_CANDIDATES  top-K over ALL verified candidates (gamma ignored;
+ *      needs top_k >= 1): the report's hits are the reference's A.8 hit list
+ *      at gamma_effective = the strength of the K-th ranked distinct
+ *      candidate (ties at that strength included), i.e. exactly what
+ *      xyz_search returns with gamma = gamma_effective; top_k ranks them.
+ *      SURVEY Appendix A.10's gamma-lowering procedure yields the same top-K. */
+enum { XYZB_TOPK_HITS = 0, XYZB_TOPK_CANDIDATES = 1 };
 
 /* InteractionHit (pair_search.hpp:29-35) */
 typedef struct {
@@ -158,6 +182,8 @@ typedef struct {
     uint64_t kernel_launches;
     double verify_kernel_ms;     /* summed CUDA-event duration of the verify launches */
     uint64_t verify_launches;
+    double gamma_effective;      /* the hit test's gamma (XYZB_TOPK_CANDIDATES: the K-th strength) */
+    uint64_t devices_used;       /* devices the runs were sharded over */
 } xyzb_result;
 
 /* ---- lifecycle ---- */

@@ -7,10 +7,11 @@ from __future__ import annotations
 
 import ctypes as C
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK, E_DATA, E_GUARD, E_SOLVER, E_CUDA, E_INTERNAL = 0, 3, 4, 5, 10, 11
 MODE_BINARY, MODE_CONTINUOUS_Y, MODE_CONTINUOUS_XY = 0, 1, 2
+TOPK_HITS, TOPK_CANDIDATES = 0, 1
 TRANSFORM_NONE, TRANSFORM_SIGN, TRANSFORM_UNBIASED = 0, 1, 2
 NUM_STAGES = 8
 STAGE_NAMES = ("draws", "project", "sort", "join", "verify", "merge", "estimate", "other")
@@ -24,6 +25,9 @@ class Problem(C.Structure):
         ("x_real", C.POINTER(C.c_double)),
         ("device", C.c_int32),
         ("flags", C.c_int32),
+        ("x_real32", C.POINTER(C.c_float)),
+        ("devices", C.POINTER(C.c_int32)),
+        ("n_devices", C.c_uint64),
     ]
 
 
@@ -51,6 +55,8 @@ class Params(C.Structure):
         ("top_k", C.c_uint64),
         ("rep_begin", C.c_uint64),
         ("rep_end", C.c_uint64),
+        ("top_k_mode", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -89,6 +95,8 @@ class Result(C.Structure):
         ("kernel_launches", C.c_uint64),
         ("verify_kernel_ms", C.c_double),
         ("verify_launches", C.c_uint64),
+        ("gamma_effective", C.c_double),
+        ("devices_used", C.c_uint64),
     ]
 
 

@@ -41,6 +41,7 @@
 #include "msplit_group.cuh"
 #include "part_group.cuh"
 #include "tile_verify.cuh"
+#include "topk_kernels.cuh"
 #include "radix_sort.cuh"
 #include "run_sort.cuh"
 #include "real_kernels.cuh"
@@ -247,6 +248,8 @@ struct xyzb_dataset {
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
     DevBuf tkeys, tvals, keep, kpos, kept, kept_order, fin, fin_order, tie, kbufA, kbufB, vbufA, vbufB, topidx, hcount;
     DevBuf pairs_dev, strengths_dev;
+    // top-K over all candidates (topk_kernels.cuh)
+    DevBuf tk_state, tk_hist, tk_dhist, tk_sint, tk_table, hits2, tk_cnt2;
     HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
     StageClock clock;
     u32 hit_cap = 1u << 16;
@@ -625,6 +628,11 @@ struct SearchCtx {
     bool tiled = false;    // this attempt verifies the accumulated pair list in column tiles
     bool no_tile = false;  // the accumulated list would exceed 2^32 pairs: per-batch verify
     bool no_hash = false;  // a hashed partition overflowed: the sparse grouping runs on the sorted path
+    // top-K over all verified candidates (XYZB_TOPK_CANDIDATES): running rank threshold per batch
+    bool topk_all = false;
+    int tk_level = 0;      // 0: emission target 4K + 256; 1: 64K + 4096; 2: emit everything >= thr
+    int tk_shift = 0;      // rank bin shift
+    u64 tk_table = 0;      // dedup table slots (power of two)
     RunPlan plan;
     xyzb_result* out;
     u64 launches[XYZB_NUM_STAGES] = {};
@@ -767,6 +775,54 @@ void plan_runs(SearchCtx& c, const uint32_t* draws) {
     }
 }
 
+// Top-K over all candidates, after a batch's verify (topk_kernels.cuh): the
+// pair-list path picks an emission threshold from the batch's rank histogram
+// and appends the pairs at or above it; then the hit buffer is pruned to the
+// occurrences at or above the K-th distinct key's rank bin.
+void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, const u32* np, u64* launches) {
+    xyzb_dataset* ds = c.ds;
+    cudaStream_t st = ds->stream;
+    auto* S = ds->tk_state.as<topk::State>();
+    const int binary = c.mode == XYZB_MODE_BINARY ? 1 : 0;
+    if (pair_path) {
+        const u64 K = c.q->top_k;
+        const u32 target = c.tk_level == 0 ? u32(std::min<u64>(4 * K + 256, 0x7fffffffull))
+                                           : u32(std::min<u64>(64 * K + 4096, 0x7fffffffull));
+        topk::rank_hist<<<kSMs * 2, 512, 0, st>>>(ds->tk_sint.as<u32>(), np, static_cast<u32>(c.pair_cap), A.nitems,
+                                                  A.item_cap, S, c.tk_shift, ds->tk_hist.as<u32>());
+        XYZB_LAUNCH_CHECK();
+        topk::emit_select<<<1, 1024, 0, st>>>(ds->tk_hist.as<u32>(), c.tk_shift, target, S, c.tk_level >= 2);
+        XYZB_LAUNCH_CHECK();
+        topk::emit_pairs<<<kSMs * 8, 256, 0, st>>>(ds->pairs.as<kern::PairRec>(), ds->tk_sint.as<u32>(), np,
+                                                   static_cast<u32>(c.pair_cap), A.nitems, A.item_cap, S, A.xkeys,
+                                                   A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap,
+                                                   static_cast<u32>(c.n));
+        XYZB_LAUNCH_CHECK();
+        *launches += 3;
+    } else {
+        topk::emit_all<<<1, 1, 0, st>>>(S);
+        XYZB_LAUNCH_CHECK();
+        *launches += 1;
+    }
+    // prune: distinct keys by rank bin, raise the threshold, keep the occurrences at or above it
+    XYZB_CUDA(cudaMemsetAsync(ds->tk_table.p, 0xff, c.tk_table * 8, st));
+    XYZB_CUDA(cudaMemsetAsync(ds->tk_cnt2.p, 0, 4, st));
+    topk::prune_insert<<<grid_for(ds->hit_cap, 256, kSMs * 4), 256, 0, st>>>(
+        A.hits, A.hit_count, A.hit_cap, ds->sign_by_rid.as<int8_t>(), ds->tk_table.as<u64>(), c.tk_table - 1,
+        c.tk_shift, static_cast<u32>(c.n), binary, ds->tk_dhist.as<u32>(), S);
+    XYZB_LAUNCH_CHECK();
+    topk::prune_select<<<1, 1024, 0, st>>>(ds->tk_dhist.as<u32>(), c.tk_shift, static_cast<u32>(c.q->top_k), S);
+    XYZB_LAUNCH_CHECK();
+    topk::prune_compact<<<grid_for(ds->hit_cap, 256, kSMs * 4), 256, 0, st>>>(
+        A.hits, A.hit_count, A.hit_cap, static_cast<u32>(c.n), binary, S, ds->hits2.as<kern::DevHit>(),
+        ds->tk_cnt2.as<u32>());
+    XYZB_LAUNCH_CHECK();
+    topk::copy_back<<<grid_for(ds->hit_cap, 256, kSMs * 4), 256, 0, st>>>(ds->hits2.as<kern::DevHit>(),
+                                                                          ds->tk_cnt2.as<u32>(), A.hits, A.hit_count);
+    XYZB_LAUNCH_CHECK();
+    *launches += 4;
+}
+
 template <class K>
 void run_batches(SearchCtx& c) {
     xyzb_dataset* ds = c.ds;
@@ -786,6 +842,21 @@ void run_batches(SearchCtx& c) {
     ds->povf.ensure(8);
     XYZB_CUDA(cudaMemsetAsync(ds->povf.p, 0, 4, st));
     ds->hits.ensure(sizeof(kern::DevHit) * u64(ds->hit_cap));
+    if (c.topk_all) {
+        ds->hits2.ensure(sizeof(kern::DevHit) * u64(ds->hit_cap));
+        c.tk_table = 64;
+        while (c.tk_table < 2ull * ds->hit_cap) c.tk_table <<= 1;
+        ds->tk_table.ensure(c.tk_table * 8);
+        ds->tk_state.ensure(sizeof(topk::State));
+        ds->tk_hist.ensure(topk::kBins * 4);
+        ds->tk_dhist.ensure(topk::kBins * 4);
+        ds->tk_cnt2.ensure(8);
+        XYZB_CUDA(cudaMemsetAsync(ds->tk_state.p, 0, sizeof(topk::State), st));
+        XYZB_CUDA(cudaMemsetAsync(ds->tk_hist.p, 0, topk::kBins * 4, st));
+        XYZB_CUDA(cudaMemsetAsync(ds->tk_dhist.p, 0, topk::kBins * 4, st));
+        const u64 max_rank = c.mode == XYZB_MODE_BINARY ? c.n : (u64(1) << kern::kRealRankBits);
+        c.tk_shift = topk::bin_shift(max_rank);
+    }
     // batch size: B*p entries under the budget (about 64 B of scratch each)
     u64 budget = u64(1) << 26;  // XYZB_BATCH_ENTRIES overrides (tests force multi-batch runs with it)
     if (const char* e = std::getenv("XYZB_BATCH_ENTRIES")) budget = std::max<u64>(1, std::strtoull(e, nullptr, 10));
@@ -859,7 +930,8 @@ void run_batches(SearchCtx& c) {
     // verify 95 -> 107 ms): random 1.3 KB column gathers confined to a 63 MB window run at
     // 8.3 TB/s against 7.1 TB/s over all of X (tools/l2_window.cu), so it stays opt-in.
     const char* tsel = std::getenv("XYZB_TILED");
-    const bool tiled = pair_path && !c.no_tile && nbatches <= tile::kMaxBatches && tsel && std::string(tsel) == "1";
+    const bool tiled = pair_path && !c.no_tile && !c.topk_all && nbatches <= tile::kMaxBatches && tsel &&
+                       std::string(tsel) == "1";
     c.tiled = tiled;
     if (pair_path) {
         c.pair_cap = std::min<u64>(0xffffffffull,
@@ -867,6 +939,7 @@ void run_batches(SearchCtx& c) {
         if (const char* e = std::getenv("XYZB_PAIR_CAP"))  // tests force the pair-list regrow path with it
             c.pair_cap = std::min<u64>(c.pair_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.pair_scale);
         ds->pairs.ensure(c.pair_cap * sizeof(kern::PairRec));
+        if (c.topk_all) ds->tk_sint.ensure(c.pair_cap * 4);
         ds->npairs.ensure(nbatches * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->npairs.p, 0, nbatches * 4, st));
     }
@@ -1209,6 +1282,14 @@ void run_batches(SearchCtx& c) {
         A.kM = 0;
         A.kXc = nullptr;
         A.kWp = 0;
+        A.sint_out = nullptr;
+        A.rank_thr = nullptr;
+        A.rank_binary = c.mode == XYZB_MODE_BINARY ? 1 : 0;
+        A.rank_n = static_cast<u32>(c.n);
+        if (c.topk_all) {
+            if (pair_path) A.sint_out = ds->tk_sint.as<u32>();
+            else A.rank_thr = &ds->tk_state.as<topk::State>()->thr;
+        }
         u32 vgrid = kSMs * 8;
         if (const char* ev = std::getenv("XYZB_VGRID")) vgrid = static_cast<u32>(std::max(1ul, std::strtoul(ev, nullptr, 10)));
         if (pair_path) {
@@ -1284,6 +1365,10 @@ void run_batches(SearchCtx& c) {
             cudaEvent_t ev1 = clk.mark();
             clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
             c.verify_spans.push_back({ev0, ev1});
+            if (c.topk_all) {
+                topk_after_batch(c, true, A, np, &c.launches[XYZB_STAGE_MERGE]);
+                clk.span(XYZB_STAGE_MERGE, ev1, clk.mark());
+            }
             continue;
         } else if (c.mode == XYZB_MODE_BINARY) {  // long columns (n > 8192): warp per pair
             kern::BinaryStrength f{ds->Xc.as<u64>(), static_cast<u32>(ds->Wp), ds->yk_bits.as<u64>(),
@@ -1334,7 +1419,33 @@ void run_batches(SearchCtx& c) {
         cudaEvent_t e4 = clk.mark();
         clk.span(XYZB_STAGE_VERIFY, e3, e4);
         c.verify_spans.push_back({e3, e4});
+        if (c.topk_all) {
+            topk_after_batch(c, false, A, nullptr, &c.launches[XYZB_STAGE_MERGE]);
+            clk.span(XYZB_STAGE_MERGE, e4, clk.mark());
+        }
     }
+}
+
+// Top-K over all candidates: the merged list holds every first occurrence at
+// or above the final rank threshold (a bin edge); keep those at or above the
+// K-th ranked strength — the reference's A.8 list at that gamma — and remap
+// the top-K indices. Returns gamma_effective.
+double topk_filter(std::vector<xyzb_hit>& hits, std::vector<u64>& order, std::vector<u64>& topk) {
+    if (topk.empty()) return 0.0;
+    const double sK = hits[topk.back()].strength;
+    std::vector<u64> remap(hits.size(), ~0ull);
+    size_t w = 0;
+    for (size_t i = 0; i < hits.size(); ++i) {
+        if (!(hits[i].strength >= sK)) continue;
+        remap[i] = w;
+        hits[w] = hits[i];
+        order[w] = order[i];
+        ++w;
+    }
+    hits.resize(w);
+    order.resize(w);
+    for (u64& t : topk) t = remap[t];
+    return sK;
 }
 
 // Keep the first occurrence of each (min, max, sign), order by (run, A.5),
@@ -1604,6 +1715,13 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     if (c.mode == XYZB_MODE_BINARY) c.astar = integer_threshold(c.n, c.gamma);
     if (q->stop_after_first_hit && (q->rep_begin || q->rep_end))
         throw data_error("xyzb: stop_after_first_hit cannot be combined with a rep shard");
+    if (q->top_k_mode != XYZB_TOPK_HITS && q->top_k_mode != XYZB_TOPK_CANDIDATES)
+        throw data_error("xyzb: unknown top_k_mode");
+    c.topk_all = q->top_k_mode == XYZB_TOPK_CANDIDATES;
+    if (c.topk_all && q->top_k == 0) throw data_error("xyzb: top-K over all candidates needs top_k >= 1");
+    if (c.topk_all && q->stop_after_first_hit)
+        throw data_error("xyzb: top-K over all candidates cannot be combined with stop_after_first_hit");
+    if (c.topk_all && q->top_k > 0x7fffffffull) throw data_error("xyzb: top_k too large");
     std::memset(out, 0, sizeof(*out));
     ds->clock.st = ds->stream;
     ds->clock.reset();
@@ -1654,7 +1772,8 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         }
         // status block (pinned): H, merge counts, items and pairs per batch, per-run counters
         const size_t o_cnt = 8, o_items = 16, o_pairs = o_items + 4 * nbt, o_enum = round_up(o_pairs + 4 * nbt, 8),
-                     o_ver = o_enum + 8 * Rall, o_ovf = o_ver + 8 * Rall, sbytes = o_ovf + 8;
+                     o_ver = o_enum + 8 * Rall, o_ovf = o_ver + 8 * Rall, o_tk = o_ovf + 8,
+                     sbytes = o_tk + sizeof(topk::State);
         ds->h_status.ensure(sbytes);
         char* hs = ds->h_status.as<char>();
         XYZB_CUDA(cudaMemcpyAsync(hs, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
@@ -1665,6 +1784,9 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         XYZB_CUDA(cudaMemcpyAsync(hs + o_enum, ds->enumerated.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaMemcpyAsync(hs + o_ver, ds->verified.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
         XYZB_CUDA(cudaMemcpyAsync(hs + o_ovf, ds->povf.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+        if (c.topk_all)
+            XYZB_CUDA(cudaMemcpyAsync(hs + o_tk, ds->tk_state.p, sizeof(topk::State), cudaMemcpyDeviceToHost,
+                                      ds->stream));
         tr.mark("search:launch");
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         tr.mark("search:device");
@@ -1691,7 +1813,20 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         }
         const bool povf = *reinterpret_cast<const u32*>(hs + o_ovf) != 0;
         if (povf) c.no_hash = true;  // a hashed partition overflowed: redo on the sorted path
-        if (!povf && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
+        bool tk_redo = false;
+        if (c.topk_all) {
+            topk::State ts;
+            std::memcpy(&ts, hs + o_tk, sizeof(ts));
+            if (ts.fail & 2u) {  // the hit buffer overflowed during a batch
+                H = std::max(H, ts.max_hits);
+                tk_redo = true;
+            }
+            if (ts.fail & 1u) {  // a batch's dropped band could hold top-K keys: emit more
+                c.tk_level = std::min(c.tk_level + 1, 2);
+                tk_redo = true;
+            }
+        }
+        if (!povf && !tk_redo && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
             std::memcpy(enumerated.data(), hs + o_enum, Rall * 8);
             std::memcpy(verified.data(), hs + o_ver, Rall * 8);
             break;
@@ -1707,6 +1842,8 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         std::memset(c.bytes, 0, sizeof(c.bytes));
         c.verify_spans.clear();
         if (attempt == 7) throw internal_error("xyzb: hit buffer did not converge");
+        if (c.topk_all && H > ds->hit_cap / 2)  // keep the top-K buffer's headroom
+            ds->hit_cap = static_cast<u32>(std::min<u64>(0xffffffffull, u64(H) * 2));
     }
     u32 rmax = 0xffffffffu;
     std::vector<xyzb_hit> hits;
@@ -1747,6 +1884,9 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         ds->clock.span(XYZB_STAGE_MERGE, ev_m0, ev_m1);
         ev_dev_end = ev_m1;
     }
+    out->gamma_effective = c.gamma;
+    if (c.topk_all) out->gamma_effective = topk_filter(hits, order, topk);
+    out->devices_used = 1;
     // counters over executed runs (in pass/rep order)
     u64 reps = 0, enumc = 0, aborted = 0, ver = 0;
     for (u32 r : c.plan.rid) {
@@ -2241,6 +2381,7 @@ extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, ui
             out->kernel_launches += r.kernel_launches;
             out->verify_kernel_ms += r.verify_kernel_ms;
             out->verify_launches += r.verify_launches;
+            out->devices_used = std::max<u64>(out->devices_used, r.devices_used);
         }
         if (all.size() > 0xffffffffull) throw internal_error("xyzb_merge_results: too many hits");
         const u32 H = static_cast<u32>(all.size());
@@ -2252,6 +2393,8 @@ extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, ui
         std::vector<xyzb_hit> hits;
         std::vector<u64> order, topk;
         merge_hits(c, H, 0xffffffffu, hits, order, topk);
+        out->gamma_effective = params->gamma;
+        if (params->top_k_mode == XYZB_TOPK_CANDIDATES) out->gamma_effective = topk_filter(hits, order, topk);
         out->gamma0 = std::pow(double(c.p), -1.0 / double(c.M));
         out->m_used = c.M;
         out->l_used = params->l;

@@ -772,7 +772,24 @@ struct VerifyArgs {
     u32 kWp;
     int key64;
     int vshift;  // sorted keys carry extra low bits to drop (0 here)
+    // top-K over all candidates (topk_kernels.cuh): the pair-list verify writes
+    // every pair's strength numerator here instead of testing it; the item
+    // verify appends pairs whose rank is at or above *rank_thr
+    u32* sint_out;
+    const u32* rank_thr;
+    int rank_binary;  // ranks: binary round(s n), else floor(s 2^24)
+    u32 rank_n;
 };
+
+constexpr int kRealRankBits = 24;
+// rank of a strength for the top-K threshold (topk_kernels.cuh): binary the
+// exact numerator round(s n); continuous floor(s 2^24), s in [0, 1]
+__host__ __device__ __forceinline__ u32 strength_rank(double s, u32 n, int binary) {
+    if (binary) return u32(llrint(s * double(n)));
+    if (!(s > 0.0)) return 0u;
+    if (s >= 1.0) return 1u << kRealRankBits;
+    return u32(s * double(1u << kRealRankBits));
+}
 
 __device__ __forceinline__ u64 key_at(const VerifyArgs& A, u64 i) {
     const u64 v = A.key64 ? static_cast<const u64*>(A.vkeys)[i] : u64(static_cast<const u32*>(A.vkeys)[i]);
@@ -1021,7 +1038,8 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
                 for (u32 q = 1; q < kPairsPerLane; ++q)
                     if (q == i) r = pr[q];
                 const u32 si = A.run_sign[r.run] > 0 ? acc : n - acc;
-                if (si >= astar) append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, r, si, n, A.krows,
+                if (A.sint_out) A.sint_out[c0 + t] = si;
+                else if (si >= astar) append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, r, si, n, A.krows,
                                                  A.kM, A.kXc, A.kWp);
             }
             if (t + 1 < cnt) cur = nxt;
@@ -1067,7 +1085,9 @@ __global__ void __launch_bounds__(256, XYZB_VP_MINB) verify_pairs_simple(VerifyA
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(tmask, acc, o);
             const u32 si = A.run_sign[pr.run] > 0 ? acc : n - acc;
-            if (tl == 0 && si >= astar)  // rare: out of line, so the walk keeps few registers
+            if (A.sint_out) {
+                if (tl == 0) A.sint_out[q] = si;
+            } else if (tl == 0 && si >= astar)  // rare: out of line, so the walk keeps few registers
                 append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, n, A.krows,
                                 A.kM, A.kXc, A.kWp);
         }
@@ -1155,6 +1175,7 @@ __device__ __forceinline__ void walk_items(const VerifyArgs& A, F&& strength) {
     const u32 N = min(*A.nitems, A.item_cap);
     const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
+    const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;  // top-K over all candidates: rank threshold
     for (u64 t = team; t < N; t += nteams) {
         const Item item = A.items[t];
         if (A.tot[item.run] > A.guard) continue;
@@ -1168,7 +1189,8 @@ __device__ __forceinline__ void walk_items(const VerifyArgs& A, F&& strength) {
                 const u32 spos = item.ss + q;
                 if ((flags & 2u) && spos <= hpos) continue;
                 const double s = strength(hcol, svr[spos], pos_pass, tl, tmask);
-                const bool hit = tl == 0 && strength.hit(s);
+                const bool hit = tl == 0 && (A.rank_thr ? strength_rank(s, A.rank_n, A.rank_binary) >= rthr
+                                                         : strength.hit(s));
                 DevHit hr;
                 if (hit) hr = make_hit(A, item.run, hpos, spos, flags, s, -1);
                 team_append<G>(A, tmask, hit, hr);
@@ -1303,6 +1325,9 @@ __global__ void __launch_bounds__(256, 4) verify_items_sign(VerifyArgs A, SignSt
     const u32 N = min(*A.nitems, A.item_cap);
     const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    // top-K over all candidates: the gate is the rank threshold's strength (its bin's lower edge)
+    const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
+    const double gate = A.rank_thr ? double(rthr) / double(1u << kRealRankBits) : f.gamma;
     for (u64 t = warp; t < N; t += nwarps) {
         const Item item = A.items[t];
         if (A.tot[item.run] > A.guard) continue;
@@ -1341,8 +1366,8 @@ __global__ void __launch_bounds__(256, 4) verify_items_sign(VerifyArgs A, SignSt
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 if (!f.zeros) acc -= f.qsum;
                 double s = 0.5 + (pos_pass ? 1.0 : -1.0) * (double(acc) * f.inv_scale) / (2.0 * f.norm);
-                if (s >= f.gamma - f.delta) s = f.exact(j, k, pos_pass, lane, 0xffffffffu);  // warp-uniform
-                const bool hit = lane == 0 && f.exact.hit(s);
+                if (s >= gate - f.delta) s = f.exact(j, k, pos_pass, lane, 0xffffffffu);  // warp-uniform
+                const bool hit = lane == 0 && (A.rank_thr ? strength_rank(s, 0u, 0) >= rthr : f.exact.hit(s));
                 DevHit hr;
                 if (hit) hr = make_hit(A, item.run, hpos, spos, flags, s, -1);
                 team_append<32>(A, 0xffffffffu, hit, hr);

@@ -20,6 +20,10 @@ BINARY, CONTINUOUS_Y, CONTINUOUS_XY = "binary", "continuous_y", "continuous_xy"
 NONE, SIGN, UNBIASED = "none", "sign", "unbiased"
 _MODES = {BINARY: _abi.MODE_BINARY, CONTINUOUS_Y: _abi.MODE_CONTINUOUS_Y, CONTINUOUS_XY: _abi.MODE_CONTINUOUS_XY}
 _TRANSFORMS = {NONE: _abi.TRANSFORM_NONE, SIGN: _abi.TRANSFORM_SIGN, UNBIASED: _abi.TRANSFORM_UNBIASED}
+# top_k_mode: "hits" = top-K of the hits (strength >= gamma); "candidates" = top-K over all verified
+# candidates (gamma ignored; hits = the A.8 list at gamma_effective, the K-th strength)
+TOPK_HITS, TOPK_CANDIDATES = "hits", "candidates"
+_TOPK_MODES = {TOPK_HITS: _abi.TOPK_HITS, TOPK_CANDIDATES: _abi.TOPK_CANDIDATES}
 
 
 @dataclass
@@ -41,6 +45,7 @@ class SearchConfig:
     top_k: int = 0
     rep_begin: int = 0
     rep_end: int = 0
+    top_k_mode: str = TOPK_HITS
 
     def to_params(self) -> _abi.Params:
         q = _abi.Params()
@@ -56,6 +61,7 @@ class SearchConfig:
         q.strength_sample_size = self.strength_sample_size
         q.top_k = self.top_k
         q.rep_begin, q.rep_end = self.rep_begin, self.rep_end
+        q.top_k_mode = _TOPK_MODES[self.top_k_mode]
         return q
 
 
@@ -93,6 +99,8 @@ class SearchReport:
     kernel_launches: int = 0
     verify_kernel_ms: float = 0.0
     verify_launches: int = 0
+    gamma_effective: float = 0.0
+    devices_used: int = 0
 
     def hit_array(self) -> np.ndarray:
         """Hits as a structured array (j, k, strength, rep, sign)."""
@@ -123,7 +131,8 @@ def report_from_result(res: _abi.Result) -> SearchReport:
         r.top_k = [int(v) for v in np.ctypeslib.as_array(res.top_k, shape=(int(res.n_top_k),))]
     for name in ("repetitions_run", "candidates_checked", "candidates_enumerated", "aborted_repetitions",
                  "wall_time_s", "estimated_c", "gamma0", "m_used", "l_used", "runs_executed",
-                 "verified_pairs", "device_ms", "kernel_launches", "verify_kernel_ms", "verify_launches"):
+                 "verified_pairs", "device_ms", "kernel_launches", "verify_kernel_ms", "verify_launches",
+                 "gamma_effective", "devices_used"):
         setattr(r, name, getattr(res, name))
     r.stage_ms = {k: float(res.stage_ms[i]) for i, k in enumerate(_abi.STAGE_NAMES)}
     r.stage_bytes = {k: int(res.stage_bytes[i]) for i, k in enumerate(_abi.STAGE_NAMES)}

@@ -414,3 +414,32 @@ def ref_brute_force(x: PackedMatrix, y, gamma=None, top_k=None, histogram_bins=0
             if ptr:
                 lib.ref_free(ptr)
     return pairs, scanned.value, hist
+
+
+# ---- top-K over all verified candidates ----
+
+def topk_a10(hits, k):
+    """A.10: the hit list stably sorted by (strength desc, min(j,k) asc,
+    max(j,k) asc, sign desc) — oracle.cpp:45-56 extended with the sign —
+    first k entries."""
+    order = sorted(range(len(hits)), key=lambda i: (-hits[i].strength, min(hits[i].j, hits[i].k),
+                                                    max(hits[i].j, hits[i].k), -hits[i].sign))
+    return [hits[i] for i in order[:k]]
+
+
+def ref_topk_candidates(x, y, cfg, k, gamma_start=0.6, step=0.01, threads=None):
+    """A.10's gamma-lowering procedure on the unmodified reference: lower gamma
+    on a grid (gamma_start, gamma_start - step, ...) until the reference's hit
+    list holds >= k entries, then rank it. Returns (gamma_used, report, top-k hits)."""
+    from dataclasses import replace
+    g = gamma_start
+    while True:
+        rep = ref_search(x, y, replace(cfg, gamma=g, top_k=0, top_k_mode="hits",
+                                       threads=threads or os.cpu_count() or 1))
+        if len(rep.hits) >= k or g <= step:
+            return g, rep, topk_a10(rep.hits, k)
+        g = round(g - step, 12)
+
+
+def hit_tuples(hits):
+    return [(h.j, h.k, h.strength, h.found_at_repetition, h.sign) for h in hits]
