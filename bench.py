@@ -1,21 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the xyz interaction-search hot path (BASELINE.json metric:
-xyz projection runs/sec and verified pairs/sec at n, p, L; % of HBM roofline).
+xyz projection runs/sec and verified pairs/sec at n, p, L; % of HBM roofline,
+1/2/4/8 GPU).
 
-Workload (N=1): BASELINE config 2, GWAS-like binary X n=4000 x p=100000
-(bit-packed), logistic Y with 5 planted pairs, M=16, L=100 per pass, both sign
-passes (200 runs), gamma=0.6, guard 16p, top-K=100 — one step = one full
-search. N>1 (torchrun, one process per GPU): weak scaling, each rank runs 100
-repetitions of each pass of an L=100*N search, hit lists all-gathered over
-NCCL and merged on the device.
+Workload (default, N=1): BASELINE config 4 — the largest single-GPU config —
+binary X n=10000 x p=1000000 bit-packed (1.256 GB, AR(1) column blocks of 50,
+rho=0.3), sign-of-sum Y of 20 planted pairs with 15% flips, M=20, L=400 per
+pass, both sign passes (800 runs), guard 16p, top-K=1000 over ALL verified
+candidates (XYZB_TOPK_CANDIDATES; at gamma=0.55 the hit list is empty, SURVEY
+8d) — one step = one full search. N>1 (torchrun, one process per GPU): STRONG
+scaling as BASELINE states it ("L=400 runs split over 1/2/4/8 B200"): each rank
+runs its contiguous share of the repetitions of each pass, the per-rank top-K
+lists are all-gathered over NCCL and merged on the device. `--config
+gwas|toy|cont|lasso|brute` selects configs 2, 1, 3, 5 and the exhaustive oracle.
 
   value     runs/s with X and Y resident in HBM (CUDA-event device time of the
-            whole search on the engine's stream, max over ranks); L2 flushed
+            whole search on the engine's stream + the exchange, max over
+            ranks); X (1.256 GB) is larger than L2, and L2 is also flushed
             (256 MiB write) between timed steps.
-  e2e       runs/s through the public API with HOST buffers: X/Y upload, search,
-            results back, every step.
-  roofline  the verify kernel (dominant): algorithmic bytes (2 columns per
-            canonical candidate + Y) / its event-timed duration.
+  e2e       runs/s through the public API with HOST buffers: X (pinned) and Y
+            uploaded, search, top-K back, every step.
+  roofline  the verify kernel (dominant): DRAM bytes per verified pair from
+            the committed ncu capture of this workload
+            (profiles/verify_traffic_<workload>.json) x the pairs of the timed
+            launches / their CUDA-event time, against MEASURED_PEAKS hbm_gbs;
+            `algorithmic` beside it: 2 columns per canonical candidate + Y
+            (SURVEY 8d), which L2 partly serves (columns shared inside a block).
   cpu_baseline  the reference CPU path (oracle/_ref, unmodified reference core)
             on a bounded sample of the same workload, rank 0, N=1.
 
@@ -39,28 +49,33 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # BASELINE.json configs with the search parameters pinned in BASELINE.md §3.
-# The default bench line is config 2 (the metric's single-GPU workload); the
-# others are selectable with --config for per-config measurements.
+# The default bench line is config 4 (the largest single-GPU config: the metric
+# names none); the others are selectable with --config for per-config lines.
+# top_k_mode "candidates": top-K over all verified candidates (north_star).
 WORKLOADS = {
     "gwas": dict(name="gwas_cfg2", label="cfg2 GWAS-like n=4000 p=100000 M=16 L=100", n=4000, p=100000, m=16,
                  l=100, gamma=0.6, top_k=100, n_pairs=5, coef=1.5, seed=12345, search_seed=7, mode="binary",
-                 transform="none", ref_sample_l=25),
+                 transform="none", ref_sample_l=25, top_k_mode="candidates"),
     "toy": dict(name="toy_cfg1", label="cfg1 binary toy n=1000 p=2000 M=8 L=10", n=1000, p=2000, m=8, l=10,
-                gamma=0.55, top_k=10, seed=1, search_seed=7, mode="binary", transform="none", ref_sample_l=10),
+                gamma=0.55, top_k=10, seed=1, search_seed=7, mode="binary", transform="none", ref_sample_l=10,
+                top_k_mode="candidates"),
     "cont": dict(name="continuous_cfg3", label="cfg3 continuous n=2000 p=50000 M=20 L=200 sign", n=2000, p=50000,
                  m=20, l=200, gamma=0.55, top_k=1000, n_pairs=10, theta=0.8, seed=3, search_seed=7,
-                 mode="continuous_xy", transform="sign", ref_sample_l=20),
+                 mode="continuous_xy", transform="sign", ref_sample_l=20, top_k_mode="candidates"),
     "large": dict(name="large_cfg4", label="cfg4 large n=10000 p=1000000 M=20 L=400", n=10000, p=1000000, m=20,
                   l=400, gamma=0.55, top_k=1000, n_pairs=20, flip=0.15, seed=99, search_seed=7, mode="binary",
-                  transform="none", ref_sample_l=2),
+                  transform="none", ref_sample_l=8, top_k_mode="candidates"),
 }
-WORKLOAD = WORKLOADS["gwas"]
-# what bounds each stage: the grouping + join kernels move few bytes per key
+WORKLOAD = WORKLOADS["large"]
+# what bounds each stage
 STAGE_BOUND = {"project": "hbm/l2: M row-plane words read + keys written",
-               "sort": "issue: fused group + join (shared-memory atomics, barriers, pair emission); "
-                       "algorithmic bytes count keys + grouped indices only",
-               "join": "hbm: pair expansion of large blocks + run bookkeeping (or the partition join)",
-               "verify": "l2 gather when X fits in L2 (see l2_roofline), else hbm"}
+               "sort": "grouping: partition pass (config 4: keys read twice, (w, column) records written) or the "
+                       "fused group + join kernel (configs 1-2: issue-bound, shared-memory atomics)",
+               "join": "partition join (config 4: records read twice, pair list written) or the pair expansion of "
+                       "large blocks",
+               "verify": "hbm gather (config 4: X 1.256 GB >> L2); l2 gather when X fits in L2 (see l2_roofline)",
+               "merge": "top-K over all candidates: rank histogram, emission, distinct-key prune per batch + the "
+                        "final merge"}
 E2E_INFLIGHT = 4  # (X, y) jobs in flight in the end-to-end measurement (tools/e2e_pipeline.py: 1-4 measured)
 METRIC = ""
 REF_SAMPLE_L = 25
@@ -73,7 +88,7 @@ def select(config):
     REF_SAMPLE_L = WORKLOAD["ref_sample_l"]
 
 
-select("gwas")
+select("large")
 
 
 def parse():
@@ -85,7 +100,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e with one step in flight only")
-    ap.add_argument("--config", default="gwas", choices=sorted(WORKLOADS) + ["lasso", "brute"])
+    ap.add_argument("--config", default="large", choices=sorted(WORKLOADS) + ["lasso", "brute"])
     args = ap.parse_args()
     if args.config not in ("lasso", "brute"):
         select(args.config)
@@ -99,27 +114,42 @@ def dist_env():
     return rank, world, local
 
 
-def make_data():
+def make_data(lib=None):
+    """The workload's seeded inputs. lib: the generator library (default
+    libxyzb_synth.so; the reference arm passes the checker library
+    oracle/_ref/libxyzref.so, which carries the same generators, so that arm
+    loads none of this repo's product-side libraries)."""
     from paper_1610_05108_b200 import synth
     W = WORKLOAD
     if W["name"].startswith("gwas"):
-        return synth.gwas(W["n"], W["p"], W["n_pairs"], W["coef"], W["seed"])
+        return synth.gwas(W["n"], W["p"], W["n_pairs"], W["coef"], W["seed"], lib=lib)
     if W["name"].startswith("toy"):
-        x, y = synth.toy(W["n"], W["p"], 4, 16, 0.9, W["seed"])
+        x, y = synth.toy(W["n"], W["p"], 4, 16, 0.9, W["seed"], lib=lib)
         return x, y, np.array([[4, 16]], np.uint32)
     if W["name"].startswith("continuous"):
-        x, y, pairs, _ = synth.gauss(W["n"], W["p"], W["n_pairs"], W["theta"], 1.0, 0, 1.0, W["seed"])
+        x, y, pairs, _ = synth.gauss(W["n"], W["p"], W["n_pairs"], W["theta"], 1.0, 0, 1.0, W["seed"], lib=lib)
         return x, y, pairs
-    return synth.ar1(W["n"], W["p"], 50, 0.3, W["n_pairs"], W["flip"], W["seed"])
+    return synth.ar1(W["n"], W["p"], 50, 0.3, W["n_pairs"], W["flip"], W["seed"], lib=lib)
 
 
-def search_config(l_total, top_k=None):
+def search_config(l_total, top_k=None, top_k_mode=None):
     from paper_1610_05108_b200 import SearchConfig
     W = WORKLOAD
     return SearchConfig(m=W["m"], l=l_total, gamma=W["gamma"], seed=W["search_seed"],
                         top_k=W["top_k"] if top_k is None else top_k, estimate_complexity=False, threads=1,
                         mode={"binary": "binary", "continuous_xy": "continuous_xy"}[W["mode"]],
-                        transform=W["transform"])
+                        transform=W["transform"], top_k_mode=top_k_mode or W.get("top_k_mode", "hits"))
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -197,24 +227,22 @@ def gather_peak(device, ncols, words):
 
 
 def ncu_traffic():
-    """dram bytes per verify launch from the committed ncu --set full capture
-    of this workload (profiles/verify_traffic*.json), else None."""
-    for name in ("verify_traffic.json", f"verify_traffic_{WORKLOAD['name']}.json"):
-        p = os.path.join(ROOT, "profiles", name)
-        try:
-            with open(p) as f:
-                d = json.load(f)
-            if d.get("config", "").startswith(WORKLOAD["name"]):
-                return d
-        except Exception:
-            pass
-    return None
+    """DRAM bytes per verified pair of this workload's verify launches, from
+    the committed ncu capture (profiles/verify_traffic_<workload>.json,
+    written by tools/verify_traffic.py from `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum` over every verify launch of one search)."""
+    p = os.path.join(ROOT, "profiles", f"verify_traffic_{WORKLOAD['name']}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
 
 
 def ref_cpu_time(x, y, l_sample, threads, steps=1):
     """Reference core (unmodified) on a bounded sample: returns (seconds/step, runs/step, report)."""
     from tests import checkers as ck  # the reference arm only: oracle/_ref/libxyzref.so
-    cfg = search_config(l_sample)
+    cfg = search_config(l_sample, top_k=0, top_k_mode="hits")
     cfg.threads = threads
     times, rep = [], None
     for _ in range(steps):
@@ -225,6 +253,11 @@ def ref_cpu_time(x, y, l_sample, threads, steps=1):
 
 
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref/libxyzref.so: the
+    unmodified proj/core sources) on this host, all hardware threads, each step
+    a bounded sample of the workload's search (L_sample repetitions per pass
+    instead of L; runs/s is per run, so the sample measures the same rate).
+    Data comes from the generators compiled into the checker library."""
     rank, world, local = dist_env()
     if rank != 0:
         return
@@ -232,7 +265,7 @@ def run_reference(args):
     if not ck.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libxyzref.so not built"}))
         return
-    x, y, _ = make_data()
+    x, y, _ = make_data(lib=ck.ref_synth_lib())
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         ref_cpu_time(x, y, REF_SAMPLE_L, threads)
@@ -245,27 +278,31 @@ def run_reference(args):
     tot = sum(secs)
     value = runs * args.steps / tot
     sample = (f"2 x {REF_SAMPLE_L} runs of the {WORKLOAD['name']} search per step (seed 7; the full search has "
-              f"2 x {WORKLOAD['l']} runs), reference threads={threads}")
+              f"2 x {WORKLOAD['l']} runs), reference threads={threads}, {cpu_model()}")
+    cfgd = workload_config(1, WORKLOAD["l"])
+    cfgd["L_sample_per_pass"] = REF_SAMPLE_L
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "runs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": workload_config(args.gpus, WORKLOAD["l"]),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": cfgd,
         "verified_pairs_per_s": rep.candidates_checked * args.steps / tot,
-        "cpu_baseline": {"value": value, "unit": "runs/s", "cores": threads, "kind": "reference", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "runs/s", "cores": threads, "kind": "reference", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "runs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
-def workload_config(n_gpus, l_per_rank):
-    return {"workload": WORKLOAD["name"], "n": WORKLOAD["n"], "p": WORKLOAD["p"], "M": WORKLOAD["m"],
-            "L_per_gpu": l_per_rank, "L_total": l_per_rank * n_gpus, "passes": 2, "gamma": WORKLOAD["gamma"],
-            "guard": "16p", "top_k": WORKLOAD["top_k"], "mode": WORKLOAD["mode"], "transform": WORKLOAD["transform"],
-            "x_bytes": (WORKLOAD["p"] * 8 * ((WORKLOAD["n"] + 63) // 64) if WORKLOAD["mode"] == "binary"
-                        else WORKLOAD["p"] * 4 * WORKLOAD["n"]),
-            "l2": "flushed between timed steps (256 MiB write); X may be L2-resident within a step",
-            "parallelism": f"run-shard{n_gpus}"}
-
+def workload_config(n_gpus, l_total, l_per_rank=None):
+    W = WORKLOAD
+    return {"workload": W["name"], "n": W["n"], "p": W["p"], "M": W["m"],
+            "L_total": l_total, "L_per_gpu": l_per_rank if l_per_rank is not None else l_total,
+            "passes": 2, "gamma": W["gamma"], "guard": "16p", "top_k": W["top_k"],
+            "top_k_mode": W.get("top_k_mode", "hits"), "mode": W["mode"], "transform": W["transform"],
+            "x_bytes": (W["p"] * 8 * ((W["n"] + 63) // 64) if W["mode"] == "binary" else W["p"] * 4 * W["n"]),
+            "l2": "X larger than L2 (126 MB)" if W["p"] * ((W["n"] + 63) // 64) * 8 > (126 << 20) else
+                  "flushed between timed steps (256 MiB write); X may be L2-resident within a step",
+            "parallelism": f"run-shard{n_gpus} (strong: L_total split over the GPUs)"}
 
 LASSO = dict(name="lasso_cfg5", n=1000, p=20000, n_mains=10, beta=1.0, n_pairs=10, theta=1.0, noise_sd=0.5, seed=5,
              grid_size=20, grid_ratio=0.05, kkt_l=100, kkt_max_candidates=16 * 20000, path_seed=7)
@@ -419,8 +456,9 @@ def main():
     from paper_1610_05108_b200 import parallel
     x, y, planted = make_data()
     L = WORKLOAD["l"]
-    cfg = search_config(L * world)
+    cfg = search_config(L)  # strong scaling: the L repetitions of each pass split over the ranks
     my_cfg = parallel.shard_config(cfg, rank, world)
+    l_mine = my_cfg.rep_end - my_cfg.rep_begin
     ds = xb.Dataset(x, device=local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
 
@@ -429,51 +467,58 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
+    def one_step():
+        """One search shard on this rank (+ the exchange for N > 1): (report, exchange ms)."""
+        res = ds.search_raw(y, my_cfg)
+        try:
+            r = xb.report.report_from_result(res)
+            if world > 1:
+                mine = parallel.pack_result(res)
+        finally:
+            ds.free_result(res)
+        ex = 0.0
+        merged = r
+        if world > 1:  # the exchange step: one all-gather + device merge, in the timed step
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            parts = [parallel.PackedPart(b) for b in parallel.all_gather_bytes(mine, torch.device("cuda", local))]
+            merged = ds.merge([p.result for p in parts], cfg)  # returns once the merged hits are on the host
+            ev1.record()
+            ev1.synchronize()
+            ex = ev0.elapsed_time(ev1)
+        return r, merged, ex
+
     for _ in range(args.warmup):
-        rep = ds.search(y, my_cfg)
+        one_step()
     barrier()
     dev_ms, verify_ms, verify_bytes, verify_launches, launches, runs, verified = 0.0, 0.0, 0, 0, 0, 0, 0
-    ex_ms = 0.0  # all-gather + merge of the per-rank hit lists (N > 1), CUDA events on torch's stream
+    ex_ms = 0.0  # all-gather + merge of the per-rank top-K lists (N > 1), CUDA events on torch's stream
     stage, stage_b = {}, {}
     t_wall = 0.0
+    merged = None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)
             barrier()
             t0 = time.perf_counter()
-            res = ds.search_raw(y, my_cfg)
+            r, merged, ex = one_step()
             t_wall += time.perf_counter() - t0
-            try:
-                r = xb.report.report_from_result(res)
-                if world > 1:
-                    mine = parallel.pack_result(res)
-            finally:
-                ds.free_result(res)
-            if world > 1:  # the exchange step: one all-gather + device merge, in the timed step
-                t1 = time.perf_counter()
-                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ev0.record()
-                parts = [parallel.PackedPart(b) for b in parallel.all_gather_bytes(mine, torch.device("cuda", local))]
-                merged = ds.merge([p.result for p in parts], cfg)  # returns once the merged hits are on the host
-                ev1.record()
-                ev1.synchronize()
-                ex_ms += ev0.elapsed_time(ev1)
-                dev_ms += ev0.elapsed_time(ev1)
-                t_wall += time.perf_counter() - t1
-            dev_ms += r.device_ms
+            ex_ms += ex
+            dev_ms += r.device_ms + ex
             verify_ms += r.verify_kernel_ms
             verify_bytes += r.stage_bytes["verify"]
             verify_launches += r.verify_launches
             launches += r.kernel_launches
             runs += r.runs_executed
             verified += r.verified_pairs
-            for k, v in r.stage_ms.items():
-                stage[k] = stage.get(k, 0.0) + v
-            for k, v in r.stage_bytes.items():
-                stage_b[k] = stage_b.get(k, 0) + v
+            for kk, v in r.stage_ms.items():
+                stage[kk] = stage.get(kk, 0.0) + v
+            for kk, v in r.stage_bytes.items():
+                stage_b[kk] = stage_b.get(kk, 0) + v
     barrier()
     # max over ranks of the device time
     t_dev = dev_ms
+    verified_mine = verified
     if world > 1:
         t = torch.tensor([dev_ms, float(runs), float(verified)], dtype=torch.float64, device=f"cuda:{local}")
         tmax = t.clone()
@@ -490,46 +535,58 @@ def main():
         ach = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
             else 0.0
         if g:
-            l2_roof = {"bound": "l2 (X resident)", "kernel": "verify_pairs_simple/_binary (pair-list verify)", "achieved": ach, "peak": g,
-                       "unit": "GB/s", "frac": ach / g,
+            l2_roof = {"bound": "l2 (X resident)", "kernel": "verify_pairs_simple (pair-list verify)",
+                       "achieved": ach, "peak": g, "unit": "GB/s", "frac": ach / g,
                        "peak_source": "measured live: random column-pair gather + XOR-popcount probe on an X of "
                                       "this shape (paper_1610_05108_b200/csrc/probe.cu), same byte count"}
     if rank == 0:
         hbm, src = peaks()
-        achieved = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
+        alg = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
             else 0.0
         traffic = ncu_traffic()
+        kern_name = ("verify_pairs_simple (pair-list verify)" if WORKLOAD["mode"] == "binary" else
+                     "verify_items_sign (sign bits x response bit planes)" if WORKLOAD.get("transform") == "sign"
+                     else "verify_items_real<RealStrength>")
+        roof = {"bound": "hbm", "kernel": kern_name, "peak": hbm, "peak_source": src, "unit": "GB/s",
+                "algorithmic": {"achieved": alg, "frac": alg / hbm if hbm else None,
+                                "bytes_per_launch": verify_bytes / max(1, verify_launches),
+                                "note": "2 columns per canonical candidate + Y (SURVEY 8d); L2 serves the columns a "
+                                        "block's pairs share, so this exceeds the DRAM rate"}}
+        if traffic and traffic.get("dram_bytes_per_pair") and verify_launches:
+            dram_launch = traffic["dram_bytes_per_pair"] * (verified_mine / verify_launches)
+            ach = dram_launch / ((verify_ms / verify_launches) / 1e3) / 1e9
+            roof.update({"achieved": ach, "frac": ach / hbm if hbm else None, "traffic": dram_launch,
+                         "traffic_source": f"profiles/verify_traffic_{WORKLOAD['name']}.json: "
+                                           f"{traffic['dram_bytes_per_pair']:.1f} DRAM bytes per verified pair "
+                                           f"({traffic.get('source', 'ncu')}) x this run's pairs per launch"})
+        else:
+            roof.update({"achieved": alg, "frac": alg / hbm if hbm else None, "traffic": None,
+                         "traffic_source": "no committed ncu capture for this workload: algorithmic bytes"})
         out = {
             "metric": METRIC, "value": value, "unit": "runs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64" if WORKLOAD["mode"] == "binary" else "f32 data, f64 accumulation",
             "data": f"synthetic (seeded {WORKLOAD['name']} generator, include/xyzb_synth.h)",
-            "config": workload_config(world, L),
+            "config": workload_config(world, L, l_mine),
             "verified_pairs_per_s": verified / (t_dev / 1e3),
             "wall_ms_per_step": 1e3 * t_wall / args.steps,
-            "stage_ms_per_step": {k: v / args.steps for k, v in stage.items()},
+            "stage_ms_per_step": {kk: v / args.steps for kk, v in stage.items()},
             "exchange_ms_per_step": ex_ms / args.steps if world > 1 else 0.0,
-            # per-stage algorithmic bytes (projection M*p/8 + keys, grouping keys + indices,
-            # verify 2 columns per canonical candidate + Y) over the stage's event time, vs measured HBM
-            "stage_roofline": {k: {"algorithmic_bytes": stage_b[k] / args.steps,
-                                   "gbps": stage_b[k] / (stage[k] / 1e3) / 1e9 if stage.get(k) else None,
-                                   "frac_of_hbm": (stage_b[k] / (stage[k] / 1e3) / 1e9) / peaks()[0]
-                                   if stage.get(k) else None,
-                                   "bound": STAGE_BOUND[k]}
-                               for k in ("project", "sort", "join", "verify") if stage_b.get(k)},
+            # per-stage algorithmic bytes over the stage's event time, vs measured HBM
+            "stage_roofline": {kk: {"algorithmic_bytes": stage_b[kk] / args.steps,
+                                    "gbps": stage_b[kk] / (stage[kk] / 1e3) / 1e9 if stage.get(kk) else None,
+                                    "frac_of_hbm": (stage_b[kk] / (stage[kk] / 1e3) / 1e9) / peaks()[0]
+                                    if stage.get(kk) else None,
+                                    "bound": STAGE_BOUND[kk]}
+                               for kk in ("project", "sort", "join", "verify", "merge") if stage_b.get(kk)},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": ("verify_pairs_simple/_binary (pair-list verify)" if WORKLOAD["mode"] == "binary" else
-                                    "verify_items_sign (sign bits x response bit planes)"
-                                    if WORKLOAD.get("transform") == "sign" else "verify_items_real<RealStrength>"), "achieved": achieved, "peak": hbm,
-                         "peak_source": src, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
-                         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                         "algorithmic_bytes_per_launch": verify_bytes / max(1, verify_launches),
-                         "note": "algorithmic bytes = 2 columns per canonical candidate + Y (SURVEY 8d; the sign "
-                                 "transform's columns are sign bits); when X fits in L2 (cfg1-3) the verify "
-                                 "kernel can exceed the HBM roofline"},
+            "roofline": roof,
             "clocks": clk.summary(),
             "l2_roofline": l2_roof,
-            "planted_found": sorted({(min(h.j, h.k), max(h.j, h.k)) for h in rep.hits} &
+            "top_k": {"mode": WORKLOAD.get("top_k_mode", "hits"), "k": WORKLOAD["top_k"],
+                      "returned": len(merged.top_k), "gamma_effective": merged.gamma_effective,
+                      "best": [[h.j, h.k, h.strength, h.found_at_repetition, h.sign] for h in merged.top_hits()[:3]]},
+            "planted_found": sorted({(min(h.j, h.k), max(h.j, h.k)) for h in merged.hits} &
                                     {tuple(p) for p in planted.tolist()}),
         }
     # e2e through the public API with host buffers (fresh upload every step)
@@ -545,22 +602,18 @@ def main():
         x_host = xb.PackedMatrix(x.n_rows, x.n_cols, pinned) if hasattr(x, "words") else xb.RealMatrix(pinned)
         for _ in range(max(1, args.warmup)):  # untimed: warms the engine's buffer pool like a serving process
             d2 = xb.Dataset(x_host, device=local)
-            (parallel.sharded_search(d2, y, cfg, rank, world, torch.device("cuda", local)) if world > 1
-             else d2.search(y, cfg))
+            parallel.sharded_search(d2, y, cfg, rank, world, torch.device("cuda", local))
             d2.close()
         for _ in range(max(1, min(args.steps, 5))):
             flush.fill_(1.0)
             barrier()
             t0 = time.perf_counter()
             d2 = xb.Dataset(x_host, device=local)
-            if world > 1:
-                rr = parallel.sharded_search(d2, y, cfg, rank, world, torch.device("cuda", local))
-            else:
-                rr = d2.search(y, cfg)
+            rr = parallel.sharded_search(d2, y, cfg, rank, world, torch.device("cuda", local))
             d2.close()
             torch.cuda.synchronize(local)
             e2e_s += time.perf_counter() - t0
-            e2e_runs += 2 * L * world
+            e2e_runs += 2 * L
         # the same steps with E2E_INFLIGHT in flight (host threads, one dataset and stream each): the H2D
         # and host work of one step overlap the searches of the others, as a serving process with many
         # (X, y) jobs runs them
@@ -574,7 +627,7 @@ def main():
                 d3.close()
                 return r3
 
-            nstep = 24
+            nstep = max(2 * E2E_INFLIGHT, min(24, int(24 * 200 / (2 * L))))
             with ThreadPoolExecutor(E2E_INFLIGHT) as ex, ClockSampler(local) as e2e_clk:
                 for f in [ex.submit(step) for _ in range(E2E_INFLIGHT)]:  # untimed warm-up of the threads
                     f.result()
@@ -596,18 +649,21 @@ def main():
                 out["e2e"] = {"value": pipe_runs / pipe_s, "unit": "runs/s", "h2d_bytes_per_step": h2d,
                               "d2h_bytes_per_step": d2h, "serial_value": serial, "clocks": e2e_clk.summary(),
                               "note": "every step: a fresh Dataset (H2D of X from pinned host memory + bit "
-                                      f"transpose) + search + hits to host; {E2E_INFLIGHT} steps in flight on {E2E_INFLIGHT} host "
-                                      "threads (wall clock over all steps); serial_value: one step at a time"}
+                                      f"transpose) + search + top-K to host; {E2E_INFLIGHT} steps in flight on "
+                                      f"{E2E_INFLIGHT} host threads (wall clock over all steps); serial_value: one "
+                                      "step at a time"}
             else:
                 out["e2e"] = {"value": serial, "unit": "runs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                               "note": "fresh Dataset every step (H2D of X from pinned host memory + bit transpose) "
-                                      "+ search + hits to host, wall clock per step"}
+                                      "+ sharded search + all-gather + merge + top-K to host, wall clock per step "
+                                      "(max over ranks)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             secs, runs_s, rep_ref = ref_cpu_time(x, y, REF_SAMPLE_L, 1)
             out["cpu_baseline"] = {"value": runs_s / secs, "unit": "runs/s", "cores": 1, "kind": "reference",
                                    "sample": f"reference xyz_search, threads=1, 2 x {REF_SAMPLE_L} runs of the same "
-                                             f"search (seed 7), {secs:.1f} s"}
+                                             f"search (seed 7), {secs:.1f} s",
+                                   "cpu": cpu_model()}
         except Exception as e:  # reference not built on this host
             out["cpu_baseline"] = {"value": None, "unit": "runs/s", "cores": 0, "kind": "reference",
                                    "sample": f"unavailable: {e}"}

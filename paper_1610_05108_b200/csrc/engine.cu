@@ -628,6 +628,7 @@ struct SearchCtx {
     bool tiled = false;    // this attempt verifies the accumulated pair list in column tiles
     bool no_tile = false;  // the accumulated list would exceed 2^32 pairs: per-batch verify
     bool no_hash = false;  // a hashed partition overflowed: the sparse grouping runs on the sorted path
+    bool pairs_in_sort = false;  // the fused group + join kernel writes the pair list (its stage is SORT)
     // top-K over all verified candidates (XYZB_TOPK_CANDIDATES): running rank threshold per batch
     bool topk_all = false;
     int tk_level = 0;      // 0: emission target 4K + 256; 1: 64K + 4096; 2: emit everything >= thr
@@ -1091,7 +1092,8 @@ void run_batches(SearchCtx& c) {
                 c.launches[XYZB_STAGE_SORT] += 3;
                 e2 = clk.mark();
                 clk.span(XYZB_STAGE_SORT, e1, e2);
-                c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);
+                c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);  // keys read twice, records written
+                c.bytes[XYZB_STAGE_JOIN] += nb * p * 8 * 2;                 // records read by both join passes
                 // ---- join: per (run, partition) bucket tables in shared memory; |E_r|, guard, blocks ----
                 kern::part_join_launch(nb, p, int(M), pk, part_hash, ds->xorc.as<K>(), c.guard, hmax, vb[0],
                                        ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(), nitems,
@@ -1119,7 +1121,8 @@ void run_batches(SearchCtx& c) {
             sv = vb[0];
             e2 = clk.mark();
             clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4);  // keys read twice, indices written
+            c.pairs_in_sort = true;
         } else if (split_path) {
             // ---- group + join fused: two CTAs per run, each half of the 16-bit bucket table ----
             if constexpr (sizeof(K) == 4) {  // M <= 16 always runs with u32 keys
@@ -1137,7 +1140,8 @@ void run_batches(SearchCtx& c) {
             sv = vb[0];
             e2 = clk.mark();
             clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4);  // keys read twice, indices written
+            c.pairs_in_sort = true;
         } else if (cta_path) {
             // ---- group + join fused: one CTA per run, 16-bit bucket counters in shared memory ----
             kern::cta_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
@@ -1149,7 +1153,8 @@ void run_batches(SearchCtx& c) {
             sv = vb[0];
             e2 = clk.mark();
             clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4);  // keys read twice, indices written
+            c.pairs_in_sort = true;
         } else if (cluster_path) {
             // ---- group + join fused: one thread-block cluster per run, bucket tables in DSMEM ----
             kern::cluster_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
@@ -1161,7 +1166,8 @@ void run_batches(SearchCtx& c) {
             sv = vb[0];
             e2 = clk.mark();
             clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (sizeof(K) + 4);
+            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4);  // keys read twice, indices written
+            c.pairs_in_sort = true;
         } else if (buckets) {
             // ---- group: counting sort into 2^M buckets per run ----
             const u64 nbk = nb << M;
@@ -1256,7 +1262,8 @@ void run_batches(SearchCtx& c) {
         c.launches[XYZB_STAGE_JOIN] += 1;
         cudaEvent_t e3 = clk.mark();
         clk.span(XYZB_STAGE_JOIN, e2, e3);
-        c.bytes[XYZB_STAGE_JOIN] += nb * p * (sizeof(K) + 8);
+        if (!part_path && !c.pairs_in_sort)  // sorted / bucket paths: sorted keys + indices read by count and emit
+            c.bytes[XYZB_STAGE_JOIN] += nb * p * (sizeof(K) + 4) * 2;
         // ---- verify ----
         kern::VerifyArgs A;
         A.items = ds->items.as<kern::Item>();
@@ -1288,7 +1295,7 @@ void run_batches(SearchCtx& c) {
         A.rank_n = static_cast<u32>(c.n);
         if (c.topk_all) {
             if (pair_path) A.sint_out = ds->tk_sint.as<u32>();
-            else A.rank_thr = &ds->tk_state.as<topk::State>()->thr;
+            A.rank_thr = &ds->tk_state.as<topk::State>()->thr;
         }
         u32 vgrid = kSMs * 8;
         if (const char* ev = std::getenv("XYZB_VGRID")) vgrid = static_cast<u32>(std::max(1ul, std::strtoul(ev, nullptr, 10)));
@@ -1718,6 +1725,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     if (q->top_k_mode != XYZB_TOPK_HITS && q->top_k_mode != XYZB_TOPK_CANDIDATES)
         throw data_error("xyzb: unknown top_k_mode");
     c.topk_all = q->top_k_mode == XYZB_TOPK_CANDIDATES;
+    if (c.topk_all) c.astar = 0;  // every candidate is ranked; the running threshold gates the appends
     if (c.topk_all && q->top_k == 0) throw data_error("xyzb: top-K over all candidates needs top_k >= 1");
     if (c.topk_all && q->stop_after_first_hit)
         throw data_error("xyzb: top-K over all candidates cannot be combined with stop_after_first_hit");
@@ -1829,6 +1837,13 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         if (!povf && !tk_redo && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
             std::memcpy(enumerated.data(), hs + o_enum, Rall * 8);
             std::memcpy(verified.data(), hs + o_ver, Rall * 8);
+            if (c.pair_cap) {  // the pair list (16 B per canonical pair) is written by the join
+                const u32* np = reinterpret_cast<const u32*>(hs + o_pairs);
+                u64 tot = 0;
+                for (u64 b = 0; b < nbt; ++b) tot += np[b];
+                c.bytes[c.pairs_in_sort ? XYZB_STAGE_SORT : XYZB_STAGE_JOIN] += 16 * tot;
+                if (c.topk_all) c.bytes[XYZB_STAGE_MERGE] += 8 * tot;  // pair ranks read by the histogram + emission
+            }
             break;
         }
         // a buffer overflowed (the counters kept counting): grow and recompute
@@ -1840,6 +1855,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
 
         std::memset(c.launches, 0, sizeof(c.launches));
         std::memset(c.bytes, 0, sizeof(c.bytes));
+        c.pairs_in_sort = false;
         c.verify_spans.clear();
         if (attempt == 7) throw internal_error("xyzb: hit buffer did not converge");
         if (c.topk_all && H > ds->hit_cap / 2)  // keep the top-K buffer's headroom

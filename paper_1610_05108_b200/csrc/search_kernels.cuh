@@ -772,9 +772,10 @@ struct VerifyArgs {
     u32 kWp;
     int key64;
     int vshift;  // sorted keys carry extra low bits to drop (0 here)
-    // top-K over all candidates (topk_kernels.cuh): the pair-list verify writes
-    // every pair's strength numerator here instead of testing it; the item
-    // verify appends pairs whose rank is at or above *rank_thr
+    // top-K over all candidates (topk_kernels.cuh): while the running rank
+    // threshold *rank_thr is 0 the pair-list verify writes every pair's
+    // strength numerator to sint_out instead of testing it; otherwise (and in
+    // the item verify) pairs whose rank is at or above *rank_thr are appended
     u32* sint_out;
     const u32* rank_thr;
     int rank_binary;  // ranks: binary round(s n), else floor(s 2^24)
@@ -983,6 +984,9 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
     // an item overflow leaves unexpanded (unwritten) slots in the pair list;
     // the host regrows and redoes the batch, so verify nothing now
     const u32 P = *A.nitems > A.item_cap ? 0u : min(*npairs, pair_cap);
+    // top-K over all candidates: appends above the running threshold once it is set
+    const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
+    astar = max(astar, rthr);
     const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
     for (u64 c0 = team * CH; c0 < P; c0 += nteams * CH) {
@@ -1038,7 +1042,7 @@ __global__ void __launch_bounds__(256) verify_pairs_binary(VerifyArgs A, const P
                 for (u32 q = 1; q < kPairsPerLane; ++q)
                     if (q == i) r = pr[q];
                 const u32 si = A.run_sign[r.run] > 0 ? acc : n - acc;
-                if (A.sint_out) A.sint_out[c0 + t] = si;
+                if (A.sint_out && rthr == 0) A.sint_out[c0 + t] = si;
                 else if (si >= astar) append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, r, si, n, A.krows,
                                                  A.kM, A.kXc, A.kWp);
             }
@@ -1069,6 +1073,9 @@ __global__ void __launch_bounds__(256, XYZB_VP_MINB) verify_pairs_simple(VerifyA
     // an item overflow leaves unexpanded (unwritten) slots in the pair list;
     // the host regrows and redoes the batch, so verify nothing now
     const u32 P = *A.nitems > A.item_cap ? 0u : min(*npairs, pair_cap);
+    // top-K over all candidates: appends above the running threshold once it is set
+    const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
+    astar = max(astar, rthr);
     const u64 team = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
     const u64 nteams = (u64(gridDim.x) * blockDim.x) / G;
     for (u64 c0 = team * CH; c0 < P; c0 += nteams * CH) {
@@ -1085,7 +1092,7 @@ __global__ void __launch_bounds__(256, XYZB_VP_MINB) verify_pairs_simple(VerifyA
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(tmask, acc, o);
             const u32 si = A.run_sign[pr.run] > 0 ? acc : n - acc;
-            if (A.sint_out) {
+            if (A.sint_out && rthr == 0) {
                 if (tl == 0) A.sint_out[q] = si;
             } else if (tl == 0 && si >= astar)  // rare: out of line, so the walk keeps few registers
                 append_pair_hit(A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, n, A.krows,

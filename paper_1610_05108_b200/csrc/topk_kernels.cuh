@@ -74,12 +74,21 @@ __global__ void __launch_bounds__(512) rank_hist(const u32* __restrict__ sint, c
     __shared__ u32 h[kBins];
     for (u32 b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
     __syncthreads();
-    const u32 P = batch_pairs(npairs, pair_cap, nitems, item_cap);
     const u32 thr = st->thr;
-    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < P; i += u64(gridDim.x) * blockDim.x) {
-        const u32 r = sint[i];
-        if (r >= thr) atomicAdd(&h[r >> shift], 1u);
+    if (thr > 0) return;  // the verify appended the pairs at or above thr itself (no ranks written)
+    const u32 P = batch_pairs(npairs, pair_cap, nitems, item_cap);
+    // four ranks per 16-byte load
+    const u32 P4 = P / 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(sint);
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < P4; i += u64(gridDim.x) * blockDim.x) {
+        const uint4 r = s4[i];
+        atomicAdd(&h[r.x >> shift], 1u);
+        atomicAdd(&h[r.y >> shift], 1u);
+        atomicAdd(&h[r.z >> shift], 1u);
+        atomicAdd(&h[r.w >> shift], 1u);
     }
+    for (u64 i = 4 * u64(P4) + u64(blockIdx.x) * blockDim.x + threadIdx.x; i < P; i += u64(gridDim.x) * blockDim.x)
+        atomicAdd(&h[sint[i] >> shift], 1u);
     __syncthreads();
     for (u32 b = threadIdx.x; b < kBins; b += blockDim.x)
         if (h[b]) atomicAdd(&hist[b], h[b]);
@@ -127,8 +136,8 @@ __global__ void __launch_bounds__(1024) emit_select(u32* __restrict__ hist, int 
     const u32 b = suffix_bin(hist, target, nullptr);
     if (threadIdx.x == 0) {
         const u32 thr = st->thr;
-        u32 e = thr;
-        if (!conservative && b != 0xffffffffu) e = max(thr, b << shift);
+        u32 e = thr;  // thr > 0: the verify appended everything at or above thr
+        if (thr == 0 && !conservative && b != 0xffffffffu) e = b << shift;
         st->emit = e;
     }
     __syncthreads();
@@ -143,6 +152,7 @@ __global__ void __launch_bounds__(256) emit_pairs(const PairRec* __restrict__ pa
                                                   int key64, u64 S, const u32* __restrict__ rid,
                                                   DevHit* __restrict__ hits, u32* __restrict__ hit_count, u32 hit_cap,
                                                   u32 n) {
+    if (st->thr > 0) return;  // appended by the verify
     const u32 P = batch_pairs(npairs, pair_cap, nitems, item_cap);
     const u32 E = st->emit;
     const int lane = threadIdx.x & 31;

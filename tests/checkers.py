@@ -98,6 +98,15 @@ def ref_lib():
     return _cache["r"]
 
 
+def ref_synth_lib():
+    """The synthetic generators (csrc/synth.cpp) as linked into the checker
+    library, bound with libxyzb_synth.so's signatures."""
+    from paper_1610_05108_b200._lib import SYNTH_SIGNATURES
+    if "rs" not in _cache:
+        _cache["rs"] = _abi.bind(ref_lib(), SYNTH_SIGNATURES)
+    return _cache["rs"]
+
+
 def ref_available():
     return os.path.exists(REF_SO)
 
