@@ -211,12 +211,7 @@ bool cluster_group_join_launch(const K* keys, u64 B, u64 p, int M, const K* xorc
     while (T / cl > kCgPerCta) cl <<= 1;
     if (cl > 8) return false;
     const size_t smem = size_t(T / cl) * 4;
-    static bool attr = false;
-    if (!attr) {
-        XYZB_CUDA(cudaFuncSetAttribute(cluster_group_join<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(kCgPerCta * 4)));
-        attr = true;
-    }
+    func_smem(cluster_group_join<K>, kCgPerCta * 4);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<u32>(cl), static_cast<u32>(B), 1);
     cfg.blockDim = dim3(kCgThreads, 1, 1);

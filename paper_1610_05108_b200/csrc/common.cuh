@@ -4,8 +4,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 
 namespace xyzb {
 
@@ -34,6 +37,28 @@ struct guard_error : std::runtime_error {  // xyz::guard_error (errors.hpp:15-18
     } while (0)
 
 #define XYZB_LAUNCH_CHECK() XYZB_CUDA(cudaGetLastError())
+
+// cudaFuncSetAttribute applies to the CURRENT device only. Datasets on
+// several devices (and concurrent host threads) launch the same kernels, so
+// every (kernel, device, attribute) keeps the largest value requested so far,
+// raised under a lock before the launch that needs it (dynamic shared memory
+// limits and cluster opt-ins only ever need to grow).
+inline void func_attr(const void* fn, cudaFuncAttribute attr, int value) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int>, int> cur;
+    int dev = 0;
+    XYZB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(fn, dev, int(attr));
+    const auto it = cur.find(key);
+    if (it != cur.end() && it->second >= value) return;
+    XYZB_CUDA(cudaFuncSetAttribute(fn, attr, value));
+    cur[key] = value;
+}
+template <class F>
+inline void func_smem(F* fn, size_t bytes) {
+    func_attr(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
 
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
 

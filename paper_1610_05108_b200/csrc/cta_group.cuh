@@ -714,12 +714,7 @@ void split_group_join_go(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 
                          u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
                          u32 pair_cap, u32* gtab, u32* slots, cudaStream_t st) {
     auto kernel = split_group_join<K, AGG, CHECK>;
-    static bool attr = false;  // one per instantiation
-    if (!attr) {
-        XYZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(split_group_smem(16))));
-        attr = true;
-    }
+    func_smem(kernel, split_group_smem(16));
     dim3 grid(2, static_cast<u32>(B));
     kernel<<<grid, kSpThreads, split_group_smem(M), st>>>(keys, p, M, xorc, guard, hmax, grouped, tot, work_run,
                                                           items, nitems, item_cap, npairs, pairs, pair_cap, gtab,
@@ -754,11 +749,7 @@ void cta_group_join_go(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 gu
                        u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
                        u32 pair_cap, u32* gtab, cudaStream_t st) {
     auto kernel = cta_group_join<K, AGG, CHECK>;
-    static bool attr = false;  // one per instantiation
-    if (!attr) {
-        XYZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_group_smem(16))));
-        attr = true;
-    }
+    func_smem(kernel, cta_group_smem(16));
     const size_t smem = cta_group_smem(M);
     int o = 0;  // depends on M through the table size
     XYZB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kCtThreads, smem));

@@ -233,8 +233,10 @@ struct xyzb_dataset {
     DevBuf Xc;  // u64 [p][Wp]
     DevBuf Xr;  // u32 [n][P32]
     // real
-    DevBuf Xc32;   // f32 [p][n4]
-    DevBuf Xr64;   // f64 [n][p]
+    DevBuf Xc32;    // f32 [p][n4]
+    DevBuf Xsrc64;  // f64 [p][n]: the caller's fp64 values (x_real), source of the unbiased transform's rows
+    DevBuf Xr64;    // f64 [n][p]: built on the first unbiased search (ensure_xr64)
+    bool f32_src = false;  // created from x_real32 (Xc32 holds the exact values)
     DevBuf Xpos, Xzero;  // u32 [n][P32]
     DevBuf Spos, Snz;    // u64 [p][W] column sign bits (x > 0, x != 0): the sign transform's bit-plane verify
     bool has_zero = false, in_unit = true;
@@ -253,6 +255,9 @@ struct xyzb_dataset {
     HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
     StageClock clock;
     u32 hit_cap = 1u << 16;
+    // X replicated on further devices (xyzb_problem.devices[1..]): the search shards its runs over them
+    std::vector<std::unique_ptr<xyzb_dataset>> replicas;
+    ~xyzb_dataset();
 };
 
 namespace {
@@ -517,41 +522,114 @@ void create_binary(xyzb_dataset* ds, const Fill& fill, bool check_pad = false) {
     tr.mark("transpose");
 }
 
-void create_real(xyzb_dataset* ds, const Fill& fill) {
+// Real X: fp32 columns for the verify, column sign bits for the sign
+// transform's bit-plane verify, row planes of (x > 0) / (x == 0) for the
+// projection (bit transposes of the column bits), and the [-1, 1] / zero
+// flags. f32: the caller's values are floats (x_real32; half the upload).
+void create_real(xyzb_dataset* ds, const Fill& fill, bool f32) {
     ds->binary = false;
+    ds->f32_src = f32;
     ds->n4 = round_up(ds->n, 4);
     ds->P32 = ceil_div(ds->p, 32);
     ds->W = ceil_div(ds->n, 64);
     ds->Wp = round_up(ds->W, 4);
-    DevBuf xc64;
-    xc64.ensure(ds->n * ds->p * 8);
-    fill(xc64.p, ds->n * ds->p * 8);
-    ds->Xc32.ensure(ds->p * ds->n4 * 4);
-    real::to_f32_cols<<<grid_for(ds->p * ds->n4, 256, 4096), 256, 0, ds->stream>>>(xc64.as<double>(), ds->n, ds->p,
-                                                                                     ds->n4, ds->Xc32.as<float>());
-    XYZB_LAUNCH_CHECK();
-    ds->Xr64.ensure(ds->n * ds->p * 8);
-    dim3 tg(static_cast<u32>(ceil_div(ds->p, 32)), static_cast<u32>(ceil_div(ds->n, 32)));
-    real::transpose_f64<<<tg, dim3(32, 8), 0, ds->stream>>>(xc64.as<double>(), ds->n, ds->p, ds->Xr64.as<double>());
-    XYZB_LAUNCH_CHECK();
-    ds->Spos.ensure(ds->p * ds->W * 8);
-    ds->Snz.ensure(ds->p * ds->W * 8);
-    real::sign_cols<<<static_cast<u32>(std::min<u64>(ceil_div(ds->p * 32, 256), u64(kSMs) * 16)), 256, 0,
-                      ds->stream>>>(xc64.as<double>(), ds->n, ds->p, ds->W, ds->Spos.as<u64>(), ds->Snz.as<u64>());
-    XYZB_LAUNCH_CHECK();
-    ds->Xpos.ensure(ds->n * ds->P32 * 4);
-    ds->Xzero.ensure(ds->n * ds->P32 * 4);
-    DevBuf flags;
+    const u64 n = ds->n, p = ds->p;
+    ds->Xc32.ensure(p * ds->n4 * 4);
+    ds->Spos.ensure(p * ds->W * 8);
+    ds->Snz.ensure(p * ds->W * 8);
+    DevBuf tpos, tzero, flags;
+    tpos.ensure(p * ds->Wp * 8);
+    tzero.ensure(p * ds->Wp * 8);
     flags.ensure(4);
     XYZB_CUDA(cudaMemsetAsync(flags.p, 0, 4, ds->stream));
-    real::sign_planes<<<grid_for(ds->n * ds->P32 * 32, 256, 4096), 256, 0, ds->stream>>>(
-        ds->Xr64.as<double>(), ds->n, ds->p, ds->P32, ds->Xpos.as<u32>(), ds->Xzero.as<u32>(), flags.as<u32>());
+    const u32 sgrid = static_cast<u32>(std::min<u64>(ceil_div(p * 32, 256), u64(kSMs) * 16));
+    if (f32) {
+        if (n == ds->n4) {
+            fill(ds->Xc32.p, n * p * 4);
+        } else {
+            DevBuf raw;
+            raw.ensure(n * p * 4);
+            fill(raw.p, n * p * 4);
+            real::pad_f32_cols<<<grid_for(p * ds->n4, 256, 4096), 256, 0, ds->stream>>>(raw.as<float>(), n, p, ds->n4,
+                                                                                         ds->Xc32.as<float>());
+            XYZB_LAUNCH_CHECK();
+            XYZB_CUDA(cudaStreamSynchronize(ds->stream));  // raw returns to the pool
+        }
+        real::sign_cols<float><<<sgrid, 256, 0, ds->stream>>>(ds->Xc32.as<float>(), ds->n4, n, p, ds->W, ds->Wp,
+                                                              ds->Spos.as<u64>(), ds->Snz.as<u64>(), tpos.as<u64>(),
+                                                              tzero.as<u64>(), flags.as<u32>());
+    } else {
+        ds->Xsrc64.ensure(n * p * 8);
+        fill(ds->Xsrc64.p, n * p * 8);
+        real::to_f32_cols<<<grid_for(p * ds->n4, 256, 4096), 256, 0, ds->stream>>>(ds->Xsrc64.as<double>(), n, p,
+                                                                                     ds->n4, ds->Xc32.as<float>());
+        XYZB_LAUNCH_CHECK();
+        real::sign_cols<double><<<sgrid, 256, 0, ds->stream>>>(ds->Xsrc64.as<double>(), n, n, p, ds->W, ds->Wp,
+                                                               ds->Spos.as<u64>(), ds->Snz.as<u64>(), tpos.as<u64>(),
+                                                               tzero.as<u64>(), flags.as<u32>());
+    }
+    XYZB_LAUNCH_CHECK();
+    ds->Xpos.ensure(n * ds->P32 * 4);
+    ds->Xzero.ensure(n * ds->P32 * 4);
+    dim3 tg(static_cast<u32>(ceil_div(ds->P32, 32)), static_cast<u32>(ceil_div(ds->W, kern::kTrWords)));
+    kern::transpose_bits<<<tg, 1024, 0, ds->stream>>>(tpos.as<u64>(), ds->Wp, ds->W, n, p, ds->P32, ds->Xpos.as<u32>());
+    XYZB_LAUNCH_CHECK();
+    kern::transpose_bits<<<tg, 1024, 0, ds->stream>>>(tzero.as<u64>(), ds->Wp, ds->W, n, p, ds->P32,
+                                                      ds->Xzero.as<u32>());
     XYZB_LAUNCH_CHECK();
     u32 hf = 0;
     XYZB_CUDA(cudaMemcpyAsync(&hf, flags.p, 4, cudaMemcpyDeviceToHost, ds->stream));
     XYZB_CUDA(cudaStreamSynchronize(ds->stream));
     ds->has_zero = (hf & 1u) != 0;
     ds->in_unit = (hf & 2u) == 0;
+}
+
+// The unbiased transform's fp64 rows [n][p], built on the first unbiased
+// search from the caller's fp64 values (or the exact fp32 ones).
+void ensure_xr64(xyzb_dataset* ds) {
+    if (ds->Xr64.p) return;
+    ds->Xr64.ensure(ds->n * ds->p * 8);
+    dim3 tg(static_cast<u32>(ceil_div(ds->p, 32)), static_cast<u32>(ceil_div(ds->n, 32)));
+    if (ds->f32_src)
+        real::transpose_f64<float><<<tg, dim3(32, 8), 0, ds->stream>>>(ds->Xc32.as<float>(), ds->n4, ds->n, ds->p,
+                                                                       ds->Xr64.as<double>());
+    else
+        real::transpose_f64<double><<<tg, dim3(32, 8), 0, ds->stream>>>(ds->Xsrc64.as<double>(), ds->n, ds->n, ds->p,
+                                                                        ds->Xr64.as<double>());
+    XYZB_LAUNCH_CHECK();
+}
+
+// A copy of a dataset's device-resident X on another device (or the same
+// one): peer copies of the column / row layouts, over NVLink between GPUs.
+std::unique_ptr<xyzb_dataset> replicate(xyzb_dataset* src, int dev) {
+    std::unique_ptr<xyzb_dataset> r(new xyzb_dataset());
+    r->device = dev;
+    r->n = src->n;
+    r->p = src->p;
+    r->binary = src->binary;
+    r->W = src->W;
+    r->Wp = src->Wp;
+    r->P32 = src->P32;
+    r->n4 = src->n4;
+    r->has_zero = src->has_zero;
+    r->in_unit = src->in_unit;
+    r->f32_src = src->f32_src;
+    r->hit_cap = src->hit_cap;
+    DeviceGuard dg(dev);
+    XYZB_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+    StreamScope ss(r->stream);
+    DevBuf xyzb_dataset::*bufs[] = {&xyzb_dataset::Xc,  &xyzb_dataset::Xr,   &xyzb_dataset::Xc32,
+                                    &xyzb_dataset::Xsrc64, &xyzb_dataset::Xpos, &xyzb_dataset::Xzero,
+                                    &xyzb_dataset::Spos, &xyzb_dataset::Snz};
+    for (auto m : bufs) {
+        const DevBuf& s = src->*m;
+        if (!s.p) continue;
+        DevBuf& d = r.get()->*m;
+        d.ensure(s.bytes);
+        XYZB_CUDA(cudaMemcpyPeerAsync(d.p, dev, s.p, src->device, s.bytes, r->stream));
+    }
+    XYZB_CUDA(cudaStreamSynchronize(r->stream));
+    return r;
 }
 
 // Stream an XYZ1 payload (dataset_io.cpp:91-129) from `f` to the device
@@ -1394,10 +1472,8 @@ void run_batches(SearchCtx& c) {
             const size_t ysm = ds->n4 * 4;
             const bool ysmem = ysm <= (size_t(192) << 10);
             if (ysmem && ysm > (size_t(48) << 10)) {
-                XYZB_CUDA(cudaFuncSetAttribute(kern::verify_items_real<true>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(ysm)));
-                XYZB_CUDA(cudaFuncSetAttribute(kern::verify_items_real<false>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(ysm)));
+                func_smem(kern::verify_items_real<true>, ysm);
+                func_smem(kern::verify_items_real<false>, ysm);
             }
             if (unbiased) {
                 kern::RealStrength<true> f{ds->Xc32.as<float>(), ds->n4, ds->yreal32.as<float>(), c.norm, c.gamma};
@@ -1468,13 +1544,8 @@ void merge_hits(SearchCtx& c, u32 H, u32 rmax, std::vector<xyzb_hit>& hits_out, 
     u64& L = c.launches[XYZB_STAGE_MERGE];
     if (H <= u32(merge::kSmallMerge) && !std::getenv("XYZB_MERGE_LARGE")) {
         // short lists: one CTA dedups, orders and ranks in shared memory
-        static bool attr_set = false;
         const size_t smem = merge::small_merge_smem(merge::kSmallMerge);
-        if (!attr_set) {
-            XYZB_CUDA(cudaFuncSetAttribute(merge::merge_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem)));
-            attr_set = true;
-        }
+        func_smem(merge::merge_small, smem);
         ds->fin.ensure(u64(H) * sizeof(xyzb_hit));
         ds->fin_order.ensure(u64(H) * 8);
         ds->topidx.ensure(u64(H) * 8 + 16);
@@ -1735,6 +1806,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     ds->clock.reset();
     cudaEvent_t ev_start = ds->clock.mark();
     upload_response(c, resp);
+    if (c.mode == XYZB_MODE_CONTINUOUS_XY && q->transform == XYZB_TRANSFORM_UNBIASED) ensure_xr64(ds);
     tr.mark("search:y");
     plan_runs(c, draws);
     tr.mark("search:plan");
@@ -1757,13 +1829,8 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         u32* top_counts = nullptr;
         if (fused_merge) {
             fcap = std::min<u32>(ds->hit_cap, u32(merge::kSmallMerge));
-            static bool attr_set = false;
             const size_t smem = merge::small_merge_smem(merge::kSmallMerge);
-            if (!attr_set) {
-                XYZB_CUDA(cudaFuncSetAttribute(merge::merge_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem)));
-                attr_set = true;
-            }
+            func_smem(merge::merge_small, smem);
             ds->fin.ensure(u64(fcap) * sizeof(xyzb_hit));
             ds->fin_order.ensure(u64(fcap) * 8);
             ds->topidx.ensure(u64(fcap) * 8 + 16);
@@ -2199,12 +2266,7 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
         hist.ensure((n + 1) * 8);
         XYZB_CUDA(cudaMemsetAsync(hist.p, 0, (n + 1) * 8, st));
         const size_t hs = n <= brute::kSmemHistMax ? size_t(n + 1) * 4 : 0;
-        static bool attr = false;
-        if (!attr) {
-            XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int((brute::kSmemHistMax + 1) * 4)));
-            attr = true;
-        }
+        func_smem(brute::all_pairs<false>, (brute::kSmemHistMax + 1) * 4);
         const u64* nzp = yb.as<u64>() + Wp;
         // tensor cores (tcgen05 kind::i8 Gram product) by default; XYZB_BRUTE=cuda: CUDA-core popcounts
         const char* bsel = std::getenv("XYZB_BRUTE");
@@ -2223,18 +2285,10 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
             XYZB_LAUNCH_CHECK();
             tmA = operand_map(opA.p, p, Kp, brute::kTcM);
             tmB = operand_map(opB.p, p, Kp, brute::kTcN);
-            static bool tc_attr = false;
-            if (!tc_attr) {
-                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(brute::kTcSmem)));
-                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(brute::kTcSmem)));
-                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc2<false>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(brute::kTcSmem2)));
-                XYZB_CUDA(cudaFuncSetAttribute(brute::all_pairs_tc2<true>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(brute::kTcSmem2)));
-                tc_attr = true;
-            }
+            func_smem(brute::all_pairs_tc<false>, brute::kTcSmem);
+            func_smem(brute::all_pairs_tc<true>, brute::kTcSmem);
+            func_smem(brute::all_pairs_tc2<false>, brute::kTcSmem2);
+            func_smem(brute::all_pairs_tc2<true>, brute::kTcSmem2);
         }
         const u64 ntc = u64((p + brute::kTcM - 1) / brute::kTcM) * ((p + brute::kTcN - 1) / brute::kTcN);
         const u32 tc_grid = static_cast<u32>(std::min<u64>(ntc, kSMs));
@@ -2342,11 +2396,13 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
     });
 }
 
-extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, uint64_t n_parts,
-                                  const xyzb_params* params, xyzb_result* out, char* err, size_t errlen) {
-    if (out) std::memset(out, 0, sizeof(*out));
-    return guarded(err, errlen, [&] {
-        if (!ds || !params || !out || (n_parts && !parts)) throw data_error("xyzb_merge_results: null argument");
+namespace {
+
+// Merge per-shard results into one report identical to the unsharded search
+// (xyzb_merge_results; the multi-device search's last step).
+void merge_parts(xyzb_dataset* ds, const xyzb_result* parts, u64 n_parts, const xyzb_params* params,
+                 xyzb_result* out) {
+    {
         if (params->stop_after_first_hit) throw data_error("xyzb: stop_after_first_hit cannot be combined with a rep shard");
         DeviceGuard dg(ds->device);
         StreamScope ss(ds->stream);
@@ -2424,6 +2480,65 @@ extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, ui
         out->n_top_k = topk.size();
         out->top_k = static_cast<u64*>(std::malloc(std::max<size_t>(1, topk.size()) * 8));
         if (!topk.empty()) std::memcpy(out->top_k, topk.data(), topk.size() * 8);
+    }
+}
+
+// Repetition shard g of G: [1 + L g / G, 1 + L (g + 1) / G) (parallel.shard_bounds)
+std::pair<u64, u64> shard_bounds(u64 L, u64 g, u64 G) { return {1 + L * g / G, 1 + L * (g + 1) / G}; }
+
+// A search over the dataset's replicas (xyzb_problem.devices): each device
+// takes a contiguous repetition shard of each pass on its own host thread and
+// stream, then the shard results merge on the primary device — the same
+// report as one device (replaces the thread waves of run_pass,
+// search.cpp:59-111).
+void multi_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q, const uint32_t* draws,
+                  xyzb_result* out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    validate_params(q);
+    std::vector<xyzb_dataset*> devs{ds};
+    for (auto& r : ds->replicas) devs.push_back(r.get());
+    const u64 G = std::min<u64>(devs.size(), q->l);  // no empty shards
+    std::vector<xyzb_params> qs(G, *q);
+    std::vector<xyzb_result> parts(G);
+    std::vector<std::exception_ptr> errs(G);
+    for (auto& r : parts) std::memset(&r, 0, sizeof(r));
+    std::vector<std::thread> th;
+    for (u64 g = 0; g < G; ++g) {
+        const auto b = shard_bounds(q->l, g, G);
+        qs[g].rep_begin = b.first;
+        qs[g].rep_end = b.second;
+        qs[g].estimate_complexity = g == 0 ? q->estimate_complexity : 0;  // a per-search quantity: once
+        th.emplace_back([&, g] {
+            try {
+                do_search(devs[g], resp, &qs[g], draws, &parts[g]);
+            } catch (...) {
+                errs[g] = std::current_exception();
+            }
+        });
+    }
+    for (auto& t : th) t.join();
+    struct Free {
+        std::vector<xyzb_result>& v;
+        ~Free() {
+            for (auto& r : v) xyzb_result_free(&r);
+        }
+    } fr{parts};
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    merge_parts(ds, parts.data(), G, q, out);
+    out->estimated_c = parts[0].estimated_c;
+    out->devices_used = G;
+    out->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+} // namespace
+
+extern "C" int xyzb_merge_results(xyzb_dataset* ds, const xyzb_result* parts, uint64_t n_parts,
+                                  const xyzb_params* params, xyzb_result* out, char* err, size_t errlen) {
+    if (out) std::memset(out, 0, sizeof(*out));
+    return guarded(err, errlen, [&] {
+        if (!ds || !params || !out || (n_parts && !parts)) throw data_error("xyzb_merge_results: null argument");
+        merge_parts(ds, parts, n_parts, params, out);
     });
 }
 
@@ -2523,9 +2638,10 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
         *out = nullptr;
         if (!pr) throw data_error("xyzb_dataset_create: null problem");
         if (pr->n_rows == 0 || pr->n_cols == 0) throw data_error("PackedMatrix: n_rows and n_cols must be >= 1");
-        if ((pr->x_words == nullptr) == (pr->x_real == nullptr))
-            throw data_error("xyzb_dataset_create: exactly one of x_words / x_real must be set");
+        if (int(pr->x_words != nullptr) + int(pr->x_real != nullptr) + int(pr->x_real32 != nullptr) != 1)
+            throw data_error("xyzb_dataset_create: exactly one of x_words / x_real / x_real32 must be set");
         if (pr->n_rows > 0xffffffffull) throw data_error("xyzb: more than 2^32-1 rows");
+        if (pr->n_devices && !pr->devices) throw data_error("xyzb_dataset_create: null device list");
         // padding bits must be clear (PackedMatrix invariant, packed_matrix.hpp:10-14): checked on
         // the host before any device work, except for page-locked X (DMA'd as is, checked on the device)
         const bool pinned_x = pr->x_words && is_pinned(pr->x_words);
@@ -2539,24 +2655,41 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
                                          " are not zero");
         }
         require_device();
+        const int ndev = xyzb_device_count();
+        std::vector<int> devs;
+        if (pr->n_devices) devs.assign(pr->devices, pr->devices + pr->n_devices);
+        else devs.push_back(pr->device);
+        for (int d : devs)
+            if (d < 0 || d >= ndev)
+                throw data_error("xyzb_dataset_create: device " + std::to_string(d) + " outside [0, " +
+                                 std::to_string(ndev) + ")");
         std::unique_ptr<xyzb_dataset> ds(new xyzb_dataset());
-        ds->device = pr->device;
+        ds->device = devs[0];
         if (const char* e = std::getenv("XYZB_HIT_CAP"))  // tests force the hit-buffer regrow path with it
             ds->hit_cap = static_cast<u32>(std::max<u64>(1, std::strtoull(e, nullptr, 10)));
-        DeviceGuard dg(ds->device);
-        XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
-        StreamScope ss(ds->stream);
-        ds->n = pr->n_rows;
-        ds->p = pr->n_cols;
-        const cudaStream_t st = ds->stream;
-        if (pr->x_words) {
-            create_binary(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_words, b, st); }, pinned_x);
-        } else {
-            create_real(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_real, b, st); });
+        {
+            DeviceGuard dg(ds->device);
+            XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+            StreamScope ss(ds->stream);
+            ds->n = pr->n_rows;
+            ds->p = pr->n_cols;
+            const cudaStream_t st = ds->stream;
+            if (pr->x_words)
+                create_binary(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_words, b, st); }, pinned_x);
+            else if (pr->x_real)
+                create_real(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_real, b, st); }, false);
+            else
+                create_real(ds.get(), [&](void* d, size_t b) { upload(d, pr->x_real32, b, st); }, true);
+            XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         }
-        XYZB_CUDA(cudaStreamSynchronize(ds->stream));
+        // further devices: peer copies of the primary's device-resident X
+        for (size_t g = 1; g < devs.size(); ++g) ds->replicas.push_back(replicate(ds.get(), devs[g]));
         *out = ds.release();
     });
+}
+
+xyzb_dataset::~xyzb_dataset() {
+    for (auto& r : replicas) xyzb_dataset_destroy(r.release());
 }
 
 void xyzb_dataset_destroy(xyzb_dataset* ds) {
@@ -2567,9 +2700,10 @@ void xyzb_dataset_destroy(xyzb_dataset* ds) {
         cudaSetDevice(ds->device);
         cudaStreamSynchronize(ds->stream);
         cudaStream_t st = ds->stream;
+        cudaStream_t prev_drained = tl_drained;
         tl_drained = st;  // every buffer of the dataset is idle now
         delete ds;
-        tl_drained = nullptr;
+        tl_drained = prev_drained;
         cudaStreamDestroy(st);
         cudaSetDevice(prev);
     }
@@ -2603,7 +2737,8 @@ int xyzb_dataset_open(const char* path, int32_t device, xyzb_dataset** out, char
         if (binary) {
             create_binary(ds.get(), [&](void* d, size_t b) { stream_file(d, f.get(), b, true, W, ds->n, ps, st); });
         } else {
-            create_real(ds.get(), [&](void* d, size_t b) { stream_file(d, f.get(), b, false, W, ds->n, ps, st); });
+            create_real(ds.get(), [&](void* d, size_t b) { stream_file(d, f.get(), b, false, W, ds->n, ps, st); },
+                        false);
         }
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         *out = ds.release();
@@ -2623,7 +2758,12 @@ int xyzb_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* 
     if (out) std::memset(out, 0, sizeof(*out));
     return guarded(err, errlen, [&] {
         if (!ds || !params || !out) throw data_error("xyzb_search: null argument");
-        do_search(ds, resp, params, draws, out);
+        // replicas: shard the runs over the devices, unless the caller already shards (rep range) or the
+        // search must stop at the first hit (sequential by definition)
+        if (!ds->replicas.empty() && !params->stop_after_first_hit && !(params->rep_begin || params->rep_end))
+            multi_search(ds, resp, params, draws, out);
+        else
+            do_search(ds, resp, params, draws, out);
     });
 }
 

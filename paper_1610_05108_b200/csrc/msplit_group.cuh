@@ -332,11 +332,17 @@ inline u64 msplit_group_scratch(int M, u64 p) { return p > 0xffffu ? (u64(kMsSlo
 inline bool msplit_schedulable(int M) {
     const int s = M - 16;
     if (s < 1 || s > kMsMaxS) return false;
-    static int cached[kMsMaxS + 1] = {-1, -1, -1, -1, -1};
-    if (cached[s] < 0) {
+    // per (device, s), under a lock (datasets on several devices / host threads)
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, bool> cached;
+    int dev = 0;
+    XYZB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(dev, s);
+    if (!cached.count(key)) {
         auto kernel = msplit_group_join<false>;
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(msplit_group_smem(16)));
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        func_smem(kernel, msplit_group_smem(16));
+        func_attr(reinterpret_cast<const void*>(kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(1u << s, 1, 1);
         cfg.blockDim = dim3(kMsThreads, 1, 1);
@@ -351,9 +357,9 @@ inline bool msplit_schedulable(int M) {
         int ncl = 0;
         const bool ok = cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg) == cudaSuccess && ncl >= 1;
         cudaGetLastError();
-        cached[s] = ok ? 1 : 0;
+        cached[key] = ok;
     }
-    return cached[s] == 1;
+    return cached[key];
 }
 
 // Launch one 2^s-CTA cluster per run (s = M - 16); false when the cluster
@@ -368,12 +374,8 @@ inline bool msplit_group_join_launch(const u32* keys, u64 B, u64 p, int M, const
     const size_t smem = msplit_group_smem(M - s);
     const bool check = p > 0xffffu;
     auto kernel = check ? msplit_group_join<true> : msplit_group_join<false>;
-    static bool attr[2] = {false, false};
-    if (!attr[check]) {
-        XYZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(msplit_group_smem(16))));
-        XYZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr[check] = true;
-    }
+    func_smem(kernel, msplit_group_smem(16));
+    func_attr(reinterpret_cast<const void*>(kernel), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CS, static_cast<u32>(B), 1);
     cfg.blockDim = dim3(kMsThreads, 1, 1);

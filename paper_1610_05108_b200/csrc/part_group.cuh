@@ -693,12 +693,8 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, b
     u32* pcnt = scratch;
     u32* cursor = scratch + B * D;
     u32* pbeg = scratch + 2 * B * D;
-    static bool attr = false;
-    if (!attr) {
-        XYZB_CUDA(cudaFuncSetAttribute(part_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-        XYZB_CUDA(cudaFuncSetAttribute(part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-        attr = true;
-    }
+    func_smem(part_count, 64 << 10);
+    func_smem(part_scatter, 64 << 10);
     XYZB_CUDA(cudaMemsetAsync(pcnt, 0, B * D * 4, st));
     dim3 gt(static_cast<u32>(ceil_div(p, kPgTile)), static_cast<u32>(B));
     part_count<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, hashed ? 1 : 0, xorc, pcnt);
@@ -717,22 +713,12 @@ inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* x
     const int lb = M - k;
     const u64 D = u64(1) << k;
     const u32* pbeg = scratch + 2 * B * D;
-    static bool attr = false;
-    if (!attr) {
-        XYZB_CUDA(cudaFuncSetAttribute(part_join<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-        XYZB_CUDA(cudaFuncSetAttribute(part_join<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-        attr = true;
-    }
+    func_smem(part_join<0>, 64 << 10);
+    func_smem(part_join<1>, 64 << 10);
     dim3 gj(static_cast<u32>(D), static_cast<u32>(B));
     if (hash) {
-        static bool hattr = false;
-        if (!hattr) {
-            XYZB_CUDA(cudaFuncSetAttribute(part_join_hash<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(part_hash_smem(true))));
-            XYZB_CUDA(cudaFuncSetAttribute(part_join_hash<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(part_hash_smem(true))));
-            hattr = true;
-        }
+        func_smem(part_join_hash<0>, part_hash_smem(true));
+        func_smem(part_join_hash<1>, part_hash_smem(true));
         part_join_hash<0><<<gj, kHsThreads, part_hash_smem(false), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot, work_run,
                                                      items, nitems, item_cap, npairs, pairs, pair_cap, ovf);
         XYZB_LAUNCH_CHECK();

@@ -199,27 +199,56 @@ __global__ void __launch_bounds__(kMtThreads) unbiased_keys(const u64* __restric
 
 // ---- dataset preparation for real X ----
 
-// Xc64 [p][n] column-major -> Xc32 [p][n4] (fp32, zero padded)
-// Column-major sign bits of the fp64 matrix (the sign transform's t(x) in
-// {-1, 0, 1}, search.cpp:456-462): bit i of word w of column j is
-// x[64w + i, j] > 0 (Spos) / != 0 (Snz). One warp per column, two ballots
-// per word. For the bit-plane verify of the sign transform.
-__global__ void sign_cols(const double* __restrict__ Xc64, u64 n, u64 p, u64 Wn, u64* __restrict__ Spos,
-                          u64* __restrict__ Snz) {
+// Column-major sign bits of X (the sign transform's t(x) in {-1, 0, 1},
+// search.cpp:456-462): bit i of word w of column j is x[64w + i, j] > 0
+// (Spos) / != 0 (Snz), W words per column, for the bit-plane verify; the
+// same bits of (x > 0) and (x == 0) with the Wp-word stride of the binary
+// layout (Tpos, Tzero; zero padded) for the row-plane transposes the
+// projection reads; flags: bit 0 any zero, bit 1 any entry outside [-1, 1]
+// (or NaN: the unbiased transform's domain check, search.cpp:417-434).
+// One warp per column, ballots per word. T = double (x_real) or float
+// (x_real32: double(x) compares the same).
+template <class T>
+__global__ void sign_cols(const T* __restrict__ X, u64 ld, u64 n, u64 p, u64 Wn, u64 Wp, u64* __restrict__ Spos,
+                          u64* __restrict__ Snz, u64* __restrict__ Tpos, u64* __restrict__ Tzero,
+                          u32* __restrict__ flags) {
     const int lane = threadIdx.x & 31;
     const u64 nw = (u64(gridDim.x) * blockDim.x) >> 5;
+    u32 fl = 0;
     for (u64 j = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < p; j += nw) {
-        const double* col = Xc64 + j * n;
-        for (u64 w = 0; w < Wn; ++w) {
+        const T* col = X + j * ld;
+        for (u64 w = 0; w < Wp; ++w) {
             const u64 i0 = 64 * w + lane, i1 = i0 + 32;
-            const double a = i0 < n ? col[i0] : 0.0, b = i1 < n ? col[i1] : 0.0;
-            const u64 pos = u64(__ballot_sync(0xffffffffu, a > 0.0)) | (u64(__ballot_sync(0xffffffffu, b > 0.0)) << 32);
-            const u64 nz = u64(__ballot_sync(0xffffffffu, a != 0.0)) | (u64(__ballot_sync(0xffffffffu, b != 0.0)) << 32);
+            const bool in0 = i0 < n, in1 = i1 < n;
+            const double a = in0 ? double(col[i0]) : 1.0, b = in1 ? double(col[i1]) : 1.0;
+            const u64 pos = u64(__ballot_sync(0xffffffffu, in0 && a > 0.0)) |
+                            (u64(__ballot_sync(0xffffffffu, in1 && b > 0.0)) << 32);
+            const u64 zer = u64(__ballot_sync(0xffffffffu, in0 && a == 0.0)) |
+                            (u64(__ballot_sync(0xffffffffu, in1 && b == 0.0)) << 32);
+            const u64 nz = u64(__ballot_sync(0xffffffffu, in0 && a != 0.0)) |
+                           (u64(__ballot_sync(0xffffffffu, in1 && b != 0.0)) << 32);
+            const bool out = (in0 && !(a >= -1.0 && a <= 1.0)) || (in1 && !(b >= -1.0 && b <= 1.0));
+            if (zer) fl |= 1u;
+            if (__any_sync(0xffffffffu, out)) fl |= 2u;
             if (lane == 0) {
-                Spos[j * Wn + w] = pos;
-                Snz[j * Wn + w] = nz;
+                if (w < Wn) {
+                    Spos[j * Wn + w] = pos;
+                    Snz[j * Wn + w] = nz;
+                }
+                Tpos[j * Wp + w] = pos;
+                Tzero[j * Wp + w] = zer;
             }
         }
+    }
+    if (lane == 0 && fl) atomicOr(flags, fl);
+}
+
+// fp32 columns [p][n] -> [p][n4] (zero padded rows)
+__global__ void pad_f32_cols(const float* __restrict__ src, u64 n, u64 p, u64 n4, float* __restrict__ dst) {
+    const u64 total = p * n4;
+    for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += u64(gridDim.x) * blockDim.x) {
+        const u64 j = t / n4, i = t - j * n4;
+        dst[t] = i < n ? src[j * n + i] : 0.f;
     }
 }
 
@@ -231,43 +260,21 @@ __global__ void to_f32_cols(const double* __restrict__ Xc64, u64 n, u64 p, u64 n
     }
 }
 
-// Xc64 [p][n] -> Xr64 [n][p] (32x32 tiles through shared memory)
-__global__ void transpose_f64(const double* __restrict__ Xc64, u64 n, u64 p, double* __restrict__ Xr64) {
+// X [p][ld] column-major (fp64, or fp32 widened exactly) -> Xr64 [n][p]
+// (32x32 tiles through shared memory): the unbiased transform's fp64 rows,
+// built on the first unbiased search.
+template <class T>
+__global__ void transpose_f64(const T* __restrict__ Xc, u64 ld, u64 n, u64 p, double* __restrict__ Xr64) {
     __shared__ double tile[32][33];
     const u64 j0 = u64(blockIdx.x) * 32, i0 = u64(blockIdx.y) * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const u64 j = j0 + r, i = i0 + threadIdx.x;
-        tile[r][threadIdx.x] = (j < p && i < n) ? Xc64[j * n + i] : 0.0;
+        tile[r][threadIdx.x] = (j < p && i < n) ? double(Xc[j * ld + i]) : 0.0;
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const u64 i = i0 + r, j = j0 + threadIdx.x;
         if (i < n && j < p) Xr64[i * p + j] = tile[threadIdx.x][r];
-    }
-}
-
-// Row-major bit planes of (v > 0) and (v == 0) from Xr64; flags: bit0 any
-// zero, bit1 any entry outside [-1, 1] (or NaN).
-__global__ void sign_planes(const double* __restrict__ Xr64, u64 n, u64 p, u64 P32, u32* __restrict__ Xpos,
-                            u32* __restrict__ Xzero, u32* __restrict__ flags) {
-    const u64 total = n * P32;
-    const int lane = threadIdx.x & 31;
-    // one warp per (row, word)
-    for (u64 w = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;
-         w += (u64(gridDim.x) * blockDim.x) >> 5) {
-        const u64 i = w / P32, c = w - i * P32;
-        const u64 j = c * 32 + lane;
-        const bool in = j < p;
-        const double v = in ? Xr64[i * p + j] : 1.0;
-        const u32 pos = __ballot_sync(0xffffffffu, in && v > 0.0);
-        const u32 zer = __ballot_sync(0xffffffffu, in && v == 0.0);
-        const u32 out = __ballot_sync(0xffffffffu, in && !(v >= -1.0 && v <= 1.0));
-        if (lane == 0) {
-            Xpos[w] = pos;
-            Xzero[w] = zer;
-            if (zer) atomicOr(flags, 1u);
-            if (out) atomicOr(flags, 2u);
-        }
     }
 }
 

@@ -198,12 +198,8 @@ inline u64 hist_words(const Plan& t) { return u64(t.ntiles) * kCtas + t.ntiles; 
 template <class F>
 inline const u32* bucket_pairs(const PairRec* pairs, const u32* np, u32 cap, F f, u32 ntiles, const u32* bstart,
                                u32 nb, u32 B, u32* scratch, PairRec* out, cudaStream_t st, u64* launches) {
-    static bool attr = false;
-    if (!attr) {
-        XYZB_CUDA(cudaFuncSetAttribute(tile_count<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-        XYZB_CUDA(cudaFuncSetAttribute(tile_scatter<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-        attr = true;
-    }
+    func_smem(tile_count<F>, 64 << 10);
+    func_smem(tile_scatter<F>, 64 << 10);
     u32* hist = scratch;
     u32* total = scratch + u64(ntiles) * kCtas;
     tile_count<F><<<kCtas, kThreads, ntiles * 4, st>>>(pairs, np, cap, f, ntiles, hist);

@@ -25,15 +25,18 @@ from .report import BINARY, CONTINUOUS_XY, CONTINUOUS_Y, SearchConfig, SearchRep
 
 
 class Dataset:
-    """X uploaded once to one GPU (xyzb_dataset_create)."""
+    """X uploaded once to one GPU (xyzb_dataset_create), or replicated on
+    several (`devices`: the search shards its runs over them and merges the
+    shard results on devices[0] — SURVEY 8e)."""
 
-    def __init__(self, x, device: int = 0):
+    def __init__(self, x, device: int = 0, devices: Optional[Sequence[int]] = None):
         self._lib = load()
         self.x = x
-        self.device = device
+        self.device = devices[0] if devices else device
+        self.devices = list(devices) if devices else [device]
         self.binary = isinstance(x, PackedMatrix)
         self.n_rows, self.n_cols = x.n_rows, x.n_cols
-        prob = make_problem(x, device)
+        prob = make_problem(x, device, devices)
         h = C.c_void_p()
         err = _abi.errbuf()
         raise_for(self._lib.xyzb_dataset_create(C.byref(prob), C.byref(h), err, _abi.ERRBUF), err)

@@ -67,10 +67,14 @@ def pack_signs(y: np.ndarray) -> np.ndarray:
 
 
 class RealMatrix:
-    """Column-major doubles: values[j, i] = X_ij."""
+    """Column-major doubles: values[j, i] = X_ij. Engine extension:
+    dtype=np.float32 keeps float values (uploaded as x_real32, half the bytes;
+    every comparison sees double(x), as a RealMatrix built from them)."""
 
-    def __init__(self, values_colmajor: np.ndarray):
-        v = np.ascontiguousarray(values_colmajor, dtype=np.float64)
+    def __init__(self, values_colmajor: np.ndarray, dtype=np.float64):
+        if np.dtype(dtype) not in (np.dtype(np.float64), np.dtype(np.float32)):
+            raise ValueError("RealMatrix: dtype must be float64 or float32")
+        v = np.ascontiguousarray(values_colmajor, dtype=dtype)
         if v.ndim != 2 or v.size == 0:
             raise ValueError("RealMatrix: need a non-empty (p, n) array")
         self.values = v
@@ -87,9 +91,14 @@ class RealMatrix:
     def column(self, j: int) -> np.ndarray:
         return self.values[j]
 
+    def as_float64(self) -> "RealMatrix":
+        return self if self.values.dtype == np.float64 else RealMatrix(self.values.astype(np.float64))
 
-def make_problem(x, device: int = 0):
-    """Build an xyzb_problem pointing into x's buffer (x must outlive it)."""
+
+def make_problem(x, device: int = 0, devices=None):
+    """Build an xyzb_problem pointing into x's buffer (x must outlive it).
+    devices: replicate X on these devices (the search shards its runs over
+    them); the returned problem keeps the device array alive."""
     prob = _abi.Problem()
     prob.device = device
     if isinstance(x, PackedMatrix):
@@ -97,9 +106,17 @@ def make_problem(x, device: int = 0):
         prob.x_words = x.words.ctypes.data_as(C.POINTER(C.c_uint64))
     elif isinstance(x, RealMatrix):
         prob.n_rows, prob.n_cols = x.n_rows, x.n_cols
-        prob.x_real = x.values.ctypes.data_as(C.POINTER(C.c_double))
+        if x.values.dtype == np.float32:
+            prob.x_real32 = x.values.ctypes.data_as(C.POINTER(C.c_float))
+        else:
+            prob.x_real = x.values.ctypes.data_as(C.POINTER(C.c_double))
     else:
         raise TypeError("x must be a PackedMatrix or RealMatrix")
+    if devices:
+        arr = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        prob.devices = C.cast(arr, C.POINTER(C.c_int32))
+        prob.n_devices = len(devices)
+        prob._keep = arr
     return prob
 
 

@@ -38,6 +38,7 @@
 #include "xyz/search.hpp"
 #include "xyz/transforms.hpp"
 #include "xyzb.h"
+#include "devices.hpp"
 
 namespace xyz {
 namespace {
@@ -59,7 +60,8 @@ public:
         std::vector<double> means(p_);
         for (std::size_t j = 0; j < p_; ++j) means[j] = view.column_mean(j);
         char err[1024] = {0};
-        const int code = xyzb_design_create(x.values().data(), n_, p_, means.data(), 0, &d_, err, sizeof err);
+        const int code =
+            xyzb_design_create(x.values().data(), n_, p_, means.data(), gpu_devices()[0], &d_, err, sizeof err);
         if (code != XYZB_OK) rethrow_design(code, err);
     }
     ~DeviceScans() { xyzb_design_destroy(d_); }

@@ -12,7 +12,8 @@
 //   * the parameter selectors and the strength sampler (search.cpp:136-291)
 //     are restated here on the host with the same formulas and evaluation
 //     order, so auto-M / auto-L decisions are bit-identical to the reference.
-// SearchConfig::threads is accepted and ignored (one device stream).
+// SearchConfig::threads is accepted and ignored: the searches shard their
+// repetitions over the GPUs of gpu_devices() (devices.hpp, XYZ_GPU_DEVICES).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -31,6 +32,7 @@
 #include "xyz/search.hpp"
 #include "xyz/transforms.hpp"
 #include "xyzb.h"
+#include "devices.hpp"
 
 namespace xyz {
 
@@ -115,7 +117,10 @@ struct DatasetCache {
         prob.n_cols = p_;
         prob.x_words = words;
         prob.x_real = real;
-        prob.device = 0;
+        const std::vector<int32_t> devs = gpu_devices();  // X replicated on each; runs sharded over them
+        prob.device = devs[0];
+        prob.devices = devs.data();
+        prob.n_devices = devs.size();
         char err[1024] = {0};
         const int code = xyzb_dataset_create(&prob, &ds, err, sizeof err);
         if (code != XYZB_OK) rethrow(code, err);

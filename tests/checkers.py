@@ -117,6 +117,8 @@ def _check(code, err):
 
 
 def _search(lib, fn, free, x, y, cfg: SearchConfig):
+    if isinstance(x, RealMatrix):
+        x = x.as_float64()  # the reference takes doubles (double(x) of fp32 values)
     prob = make_problem(x)
     resp, keep = make_response(y)
     params = cfg.to_params()
@@ -188,6 +190,8 @@ def ref_equal_pairs(xk, zk):
 
 
 def _strengths(lib, fn, x, y, mode, transform, pairs):
+    if isinstance(x, RealMatrix):
+        x = x.as_float64()
     prob = make_problem(x)
     resp, keep = make_response(y)
     pairs = np.ascontiguousarray(pairs, np.uint32).reshape(-1, 2)

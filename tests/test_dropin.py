@@ -185,3 +185,21 @@ def test_dropin_unbiased_range_error_matches_reference():
     assert str(a.value) == str(b.value)
     xv[7, 5] = 1.0  # in range again: the same pointer, new contents -> re-upload, no error
     ck.dropin_search(RealMatrix(xv), y, cfg)
+
+
+def test_dropin_search_over_two_device_replicas(monkeypatch):
+    """XYZ_GPU_DEVICES lists the GPUs the drop-in shards each search over (X
+    replicated, repetitions split, shard results merged on the first): with
+    two replicas on the test box's GPU the reference-facing xyz_search returns
+    the reference's report."""
+    monkeypatch.setenv("XYZ_GPU_DEVICES", "0,0")
+    x = ck.ref_rademacher(700, 900, 12, 3)
+    y = np.where(np.random.default_rng(6).random(700) < 0.5, 1, -1).astype(np.int8)
+    from paper_1610_05108_b200.report import SearchConfig
+    cfg = SearchConfig(m=7, l=9, gamma=0.57, seed=4, threads=1)
+    got = ck.dropin_search(x, y, cfg)
+    want = ck.ref_search(x, y, cfg)
+    ok, msg = ck.same_hits(got, want)
+    assert ok, msg
+    assert (got.repetitions_run, got.candidates_enumerated, got.estimated_c) == \
+        (want.repetitions_run, want.candidates_enumerated, want.estimated_c)

@@ -1,8 +1,8 @@
 """Multi-rank host logic on CPU (gloo, world size 2): run-shard bounds, result
 serialisation, the variable-size all-gather, and the merge rule the device
 merge implements (first occurrence of (min, max, sign) by order key, then
-order-key order). The device merge itself is covered by
-tests/test_gpu_parity.py::test_sharded_runs_merge_to_the_full_search."""
+order-key order). The GPU test at the end runs the same world-size-2 gloo
+exchange around real shard searches and the device merge (xyzb_merge_results)."""
 import ctypes as C
 import os
 import socket
@@ -113,3 +113,52 @@ def test_two_rank_gather_and_merge_on_gloo(tmp_path):
     assert r0[0] == r1[0]  # every rank merges to the same report
     assert r0[0] == [(3, 9, 0.75, 1, 1), (2, 8, 0.7, 2, 1), (5, 6, 0.8, 3, 1), (2, 8, 0.3, 1, -1)]
     assert r0[1] == 100
+
+
+def _engine_worker(rank, world, port, out_dir, topk_mode):
+    """One rank of a sharded search on the GPU: its repetition shard, the gloo
+    all-gather of the serialised shard results, and the device merge through
+    xyzb_merge_results (parallel.sharded_search — bench.py's N>1 path)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import paper_1610_05108_b200 as xb
+    from tests import checkers as ck
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x = ck.ref_rademacher(900, 1500, 31, 2)
+    y = np.where(np.random.default_rng(4).random(900) < 0.5, 1, -1).astype(np.int8)
+    cfg = SearchConfig(m=8, l=12, gamma=0.56, seed=7, top_k=40, top_k_mode=topk_mode, threads=1)
+    ds = xb.Dataset(x, device=0)
+    rep = parallel.sharded_search(ds, y, cfg, rank, world)
+    import pickle
+    with open(os.path.join(out_dir, f"engine{rank}.pkl"), "wb") as f:
+        pickle.dump([ck.hit_tuples(rep.hits), rep.top_k, rep.candidates_enumerated, rep.repetitions_run,
+                     rep.gamma_effective], f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("topk_mode", ["hits", "candidates"])
+def test_two_rank_engine_search_gloo_merges_on_the_device(tmp_path, topk_mode):
+    """World size 2 on gloo with both ranks on the test box's GPU (independent
+    searches, no kernel waits on another rank): the merged report of every
+    rank equals the unsharded search."""
+    import torch.multiprocessing as mp
+    import paper_1610_05108_b200 as xb
+    from tests import checkers as ck
+    port = _free_port()
+    mp.spawn(_engine_worker, args=(2, port, str(tmp_path), topk_mode), nprocs=2, join=True)
+    x = ck.ref_rademacher(900, 1500, 31, 2)
+    y = np.where(np.random.default_rng(4).random(900) < 0.5, 1, -1).astype(np.int8)
+    cfg = SearchConfig(m=8, l=12, gamma=0.56, seed=7, top_k=40, top_k_mode=topk_mode, threads=1)
+    whole = xb.Dataset(x).search(y, cfg)
+    import pickle
+    for r in (0, 1):
+        with open(tmp_path / f"engine{r}.pkl", "rb") as f:
+            got = pickle.load(f)
+        assert got[0] == ck.hit_tuples(whole.hits)
+        assert got[1] == whole.top_k
+        assert (got[2], got[3], got[4]) == (whole.candidates_enumerated, whole.repetitions_run,
+                                            whole.gamma_effective)
