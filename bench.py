@@ -101,9 +101,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e with one step in flight only")
     ap.add_argument("--config", default="large", choices=sorted(WORKLOADS) + ["lasso", "brute"])
+    ap.add_argument("--top-k-mode", default=None, choices=["hits", "candidates"],
+                    help="override the workload's top-K mode (measurements)")
     args = ap.parse_args()
     if args.config not in ("lasso", "brute"):
         select(args.config)
+        if args.top_k_mode:
+            WORKLOAD["top_k_mode"] = args.top_k_mode
     return args
 
 

@@ -70,6 +70,22 @@ def load():
     return _lib
 
 
+TEST_OPTIONS = ("batch_entries", "hit_cap", "item_cap", "pair_cap", "grouping", "merge_large", "sign_verify_off",
+                "trace", "brute_cuda")
+GROUPING = {"auto": 0, "sort": 1, "part": 2, "msplit": 3}
+
+
+def set_test_option(name: str, value: int) -> None:
+    """xyzb_test_set_option (include/xyzb_testing.h): force a rare engine path
+    in tests; 0 restores the default."""
+    lib = load()
+    fn = lib.xyzb_test_set_option
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_char_p, C.c_longlong]
+    if fn(name.encode(), int(value)) != 0:
+        raise ValueError(f"unknown engine test option {name!r}")
+
+
 _U64P = C.POINTER(C.c_uint64)
 _U32P = C.POINTER(C.c_uint32)
 _F64P = C.POINTER(C.c_double)

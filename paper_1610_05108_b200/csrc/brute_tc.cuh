@@ -127,130 +127,6 @@ __global__ void make_pm1(const u64* __restrict__ Xc, u64 Wp, u64 p, u64 n, u64 K
     }
 }
 
-template <bool EMIT>
-__global__ void __launch_bounds__(kTcThreads, 1) all_pairs_tc(const __grid_constant__ CUtensorMap tmA,
-                                                              const __grid_constant__ CUtensorMap tmB, u32 p, u32 n,
-                                                              u32 nz, u32 Kp, unsigned long long* __restrict__ hist,
-                                                              u32 cutoff, PairOut* __restrict__ out,
-                                                              u32* __restrict__ nout, u32 out_cap) {
-    extern __shared__ __align__(1024) unsigned char dsm[];
-    __shared__ __align__(8) u64 full_bar[kTcStages], empty_bar[kTcStages], acc_bar;
-    __shared__ u32 tmem_holder;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const u32 base = smem_addr(dsm);
-    const u32 sbase = (base + 1023u) & ~1023u;  // 1024-byte aligned stages
-    u32* shist = reinterpret_cast<u32*>(dsm + (sbase - base) + kTcStages * (kTcStageA + kTcStageB));
-    auto sA = [&](int s) { return sbase + u32(s) * (kTcStageA + kTcStageB); };
-    auto sB = [&](int s) { return sA(s) + kTcStageA; };
-    const bool smem_hist = !EMIT && n <= kSmemHistMax;
-    if (smem_hist)
-        for (u32 i = threadIdx.x; i <= n; i += kTcThreads) shist[i] = 0;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(smem_addr(&full_bar[s]), 1);
-            mbar_init(smem_addr(&empty_bar[s]), 1);
-        }
-        mbar_init(smem_addr(&acc_bar), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<u64>(&tmB)) : "memory");
-    }
-    if (warp == 0) {  // TMEM: 256 columns of s32 accumulators (whole warp)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_holder)),
-                     "r"(u32(kTcN)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const u32 tmem = tmem_holder;
-
-    const u32 nj = (p + kTcM - 1) / kTcM, nk = (p + kTcN - 1) / kTcN;
-    const u32 nkb = Kp / kTcKB;
-    u32 it = 0;        // k-blocks consumed so far (stage / phase of the ring)
-    u32 tiles_done = 0;
-    for (u64 t = blockIdx.x; t < u64(nj) * nk; t += gridDim.x) {
-        const u32 tj = u32(t / nk), tk = u32(t % nk);
-        const u32 j0 = tj * kTcM, k0 = tk * kTcN;
-        if (k0 + kTcN <= j0 + 1) continue;  // no pair with k > j in this tile (uniform per CTA)
-        if (threadIdx.x == 0) {
-            // producer + MMA issuer: keep kTcStages k-blocks in flight
-            const u32 pre = nkb < u32(kTcStages) ? nkb : u32(kTcStages);
-            for (u32 q = 0; q < pre; ++q) {
-                const u32 g = it + q, s = g % kTcStages;
-                if (g >= u32(kTcStages)) mbar_wait(smem_addr(&empty_bar[s]), ((g / kTcStages) - 1) & 1);
-                mbar_expect_tx(smem_addr(&full_bar[s]), kTcStageA + kTcStageB);
-                tma_load_2d(sA(s), &tmA, int(q * kTcKB), int(j0), smem_addr(&full_bar[s]));
-                tma_load_2d(sB(s), &tmB, int(q * kTcKB), int(k0), smem_addr(&full_bar[s]));
-            }
-            for (u32 kb = 0; kb < nkb; ++kb) {
-                const u32 g = it + kb, s = g % kTcStages;
-                mbar_wait(smem_addr(&full_bar[s]), (g / kTcStages) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-                for (int kk = 0; kk < kTcKB / 32; ++kk)
-                    mma_i8(tmem, sw128_desc(sA(s) + kk * 32), sw128_desc(sB(s) + kk * 32), (kb | kk) != 0);
-                mma_commit(smem_addr(&empty_bar[s]));
-                // refill: the stage this k-block's predecessor used, once its MMAs drained
-                const u32 nx = kb + kTcStages;
-                if (kb >= 1 && nx - 1 < nkb) {
-                    const u32 gp = g - 1, sp = gp % kTcStages;
-                    mbar_wait(smem_addr(&empty_bar[sp]), (gp / kTcStages) & 1);
-                    mbar_expect_tx(smem_addr(&full_bar[sp]), kTcStageA + kTcStageB);
-                    tma_load_2d(sA(sp), &tmA, int((nx - 1) * kTcKB), int(j0), smem_addr(&full_bar[sp]));
-                    tma_load_2d(sB(sp), &tmB, int((nx - 1) * kTcKB), int(k0), smem_addr(&full_bar[sp]));
-                }
-            }
-            mma_commit(smem_addr(&acc_bar));
-        }
-        it += nkb;
-        // epilogue: every warp reads its 32 TMEM lanes (tile rows), 256 columns
-        mbar_wait(smem_addr(&acc_bar), tiles_done & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const u32 j = j0 + u32(warp) * 32 + u32(lane);
-#pragma unroll 1
-        for (int c = 0; c < kTcN / 32; ++c) {
-            u32 v[32];
-            tmem_ld32(tmem + (u32(warp * 32) << 16) + u32(c * 32), v);
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                const u32 k = k0 + u32(c * 32 + q);
-                const u32 agree = (nz - v[q]) >> 1;  // G = nz - 2 agree
-                const bool valid = j < k && k < p;
-                if (EMIT) {
-                    const bool keep = valid && agree >= cutoff;
-                    const u32 ball = __ballot_sync(0xffffffffu, keep);
-                    if (ball) {
-                        const int leader = __ffs(ball) - 1;
-                        u32 b0 = 0;
-                        if (lane == leader) b0 = atomicAdd(nout, __popc(ball));
-                        b0 = __shfl_sync(0xffffffffu, b0, leader);
-                        if (keep) {
-                            const u32 slot = b0 + __popc(ball & lanemask_lt());
-                            if (slot < out_cap) out[slot] = PairOut{j, k, agree, 0u};
-                        }
-                    }
-                } else if (valid) {
-                    if (smem_hist) atomicAdd(&shist[agree], 1u);
-                    else atomicAdd(hist + agree, 1ull);
-                }
-            }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // accumulator drained before the next tile's first MMA
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        ++tiles_done;
-    }
-    if (smem_hist) {
-        __syncthreads();
-        for (u32 i = threadIdx.x; i <= n; i += kTcThreads)
-            if (shist[i]) atomicAdd(hist + i, static_cast<unsigned long long>(shist[i]));
-    }
-    __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(u32(kTcN)));
-}
-
 // Warp-specialised persistent kernel: warp 0 = TMA producer, warp 1 = MMA
 // issuer, warps 2-5 = epilogue. The accumulator is double-buffered in TMEM
 // (2 x 256 columns), so the epilogue of tile i overlaps the MMAs of tile

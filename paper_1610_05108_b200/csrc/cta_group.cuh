@@ -1,22 +1,21 @@
-// Per-run grouping + join in ONE CTA with a 16-bit bucket table (sm_100a).
+// Per-run grouping + join with 16-bit bucket tables in shared memory (sm_100a).
 //
 // For M <= 16 the 2^M bucket counters of one run fit in shared memory as
-// 16-bit halves of u32 words (128 KB at M = 16) — no cluster, no DSMEM, no
-// cluster barriers. Positions above 16 bits come from per-chunk u32 bases
-// (a chunk = 256 buckets): start(v) = base[v >> 8] + off16[v]. A persistent
-// CTA walks its runs; per run, all in shared memory:
+// 16-bit halves of u32 words. Positions above 16 bits come from per-chunk
+// u32 bases (a chunk = 256 buckets): start(v) = base[v >> 8] + off16[v].
+// Per run, all on chip (split_group_join below, two CTAs of a cluster; the
+// table helpers are shared with msplit_group.cuh):
 //   1. count: one shared atomic per key (warp-aggregated with match.any only
 //      when 2^M is small enough for lanes to collide);
 //   2. scan: per-thread bucket ranges, block scan, chunk bases;
 //   3. scatter: atomic cursors -> grouped[b*p + pos] = column;
 //   4. join: |E_r| (incl. the diagonal, pair_search.cpp:48-49) and the
-//      canonical work, reduced in the block: the guard (pair_search.hpp:91-94)
-//      is decided on-chip;
+//      canonical work, reduced in the cluster: the guard
+//      (pair_search.hpp:91-94) is decided on-chip;
 //   5. emit: candidate pairs / work items of a kept run (emit_items).
 // A run whose bucket or chunk exceeds 65535 columns (possible only when
 // p > 65535, e.g. many monomorphic columns) is redone exactly with 32-bit
-// counters in a per-CTA global table. The outputs are those of
-// cluster_group_join (same grouped/tot/work_run/items/pairs contract).
+// counters in a global table slot.
 #pragma once
 
 #include <algorithm>
@@ -332,52 +331,6 @@ __device__ void tab_join(const Tab& tab, int M, u32 b, K c, u64 p, u64 guard, u3
         }
     }
     __syncthreads();  // red / ws / tables reusable
-}
-
-template <class K, bool AGG, bool CHECK>
-__global__ void __launch_bounds__(kCtThreads) cta_group_join(
-    const K* __restrict__ keys, u32 nruns, u64 p, int M, const K* __restrict__ xorc, u64 guard, u32 hmax,
-    u32* __restrict__ grouped, u64* __restrict__ tot, u64* __restrict__ work_run, Item* __restrict__ items,
-    u32* __restrict__ nitems, u32 item_cap, u32* __restrict__ npairs, PairRec* __restrict__ pairs, u32 pair_cap,
-    u32* __restrict__ gtab) {
-    extern __shared__ __align__(16) u32 smem[];
-    __shared__ u32 ws[68];
-    __shared__ u32 s_ovf;
-    __shared__ u64 red[2][33];
-    const u32 T = u32(1) << M;
-    const int cbits = min(M, kCtChunkBits);
-    SmemTab16 tab{smem + max(1u, T >> cbits), smem, M, cbits, &s_ovf};
-    for (u32 b = blockIdx.x; b < nruns; b += gridDim.x) {
-        const K* kb = keys + u64(b) * p;
-        u32* out = grouped + u64(b) * p;
-        const K c = xorc[b];
-        if (threadIdx.x == 0) s_ovf = 0;
-        tab.clear();
-        __syncthreads();
-        tab_pass<AGG, CHECK, true>(tab, kb, p, static_cast<u32*>(nullptr));
-        __syncthreads();
-        tab.scan(ws);
-        __syncthreads();
-        if (CHECK && s_ovf) {
-            // a bucket or a chunk above 65535 columns: redo exactly with 32-bit counters
-            GlobalTab32 g{gtab + (u64(blockIdx.x) << M), M};
-            g.clear();
-            __syncthreads();
-            tab_pass<AGG, false, false>(g, kb, p, static_cast<u32*>(nullptr));
-            __syncthreads();
-            g.scan(ws);
-            __syncthreads();
-            tab_pass<AGG, false, false>(g, kb, p, out);
-            __syncthreads();
-            tab_join<K>(g, M, b, c, p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap,
-                        red, ws, grouped);
-            continue;
-        }
-        tab_pass<AGG, false, true>(tab, kb, p, out);
-        __syncthreads();
-        tab_join<K>(tab, M, b, c, p, guard, hmax, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap, red,
-                    ws, grouped);
-    }
 }
 
 // ------------------------------------------------ two-CTA split per run --
@@ -734,42 +687,8 @@ void split_group_join_launch(const K* keys, u64 B, u64 p, int M, const K* xorc, 
        gtab, slots, st);
 }
 
-// Shared bytes of the table for 2^M buckets.
-inline size_t cta_group_smem(int M) {
-    const u64 T = u64(1) << M;
-    const int cbits = M < kCtChunkBits ? M : kCtChunkBits;
-    return size_t(T / 2) * 4 + size_t(std::max<u64>(1, T >> cbits)) * 4;
-}
-
-// Scratch (u32 entries) the overflow fallback needs: one 2^M table per CTA.
-inline u64 cta_group_scratch(int M, u64 p) { return p > 0xffffu ? (u64(kSMs) << M) : 0; }
-
-template <class K, bool AGG, bool CHECK>
-void cta_group_join_go(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 guard, u32 hmax, u32* grouped, u64* tot,
-                       u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs, PairRec* pairs,
-                       u32 pair_cap, u32* gtab, cudaStream_t st) {
-    auto kernel = cta_group_join<K, AGG, CHECK>;
-    func_smem(kernel, cta_group_smem(16));
-    const size_t smem = cta_group_smem(M);
-    int o = 0;  // depends on M through the table size
-    XYZB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kCtThreads, smem));
-    const u64 grid = std::min<u64>(B, u64(kSMs) * u64(std::max(1, o)));
-    kernel<<<static_cast<u32>(grid), kCtThreads, smem, st>>>(keys, static_cast<u32>(B), p, M, xorc, guard, hmax,
-                                                             grouped, tot, work_run, items, nitems, item_cap, npairs,
-                                                             pairs, pair_cap, gtab);
-}
-
-template <class K>
-void cta_group_join_launch(const K* keys, u64 B, u64 p, int M, const K* xorc, u64 guard, u32 hmax, u32* grouped,
-                           u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap, u32* npairs,
-                           PairRec* pairs, u32 pair_cap, u32* gtab, cudaStream_t st) {
-    const bool agg = M <= 12;  // lanes of a warp collide only on small tables
-    const bool check = p > 0xffffu;
-    auto go = agg ? (check ? cta_group_join_go<K, true, true> : cta_group_join_go<K, true, false>)
-                  : (check ? cta_group_join_go<K, false, true> : cta_group_join_go<K, false, false>);
-    go(keys, B, p, M, xorc, guard, hmax, grouped, tot, work_run, items, nitems, item_cap, npairs, pairs, pair_cap, gtab,
-       st);
-}
+// Scratch (u32 entries) of the 16-bit overflow fallback: one 2^M table per slot.
+inline u64 split_group_scratch(int M, u64 p) { return p > 0xffffu ? (u64(kSMs) << M) : 0; }
 
 } // namespace kern
 } // namespace xyzb

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <functional>
 #include <chrono>
 #include <cmath>
@@ -30,9 +31,9 @@
 #include <vector>
 
 #include "../../include/xyzb.h"
+#include "../../include/xyzb_testing.h"
 #include "brute.cuh"
 #include "brute_tc.cuh"
-#include "cluster_group.cuh"
 #include "cta_group.cuh"
 #include "common.cuh"
 #include "draws.cuh"
@@ -40,7 +41,6 @@
 #include "merge_kernels.cuh"
 #include "msplit_group.cuh"
 #include "part_group.cuh"
-#include "tile_verify.cuh"
 #include "topk_kernels.cuh"
 #include "radix_sort.cuh"
 #include "run_sort.cuh"
@@ -190,6 +190,21 @@ struct HostBuf {  // pinned
 
 u64 round_up(u64 a, u64 m) { return (a + m - 1) / m * m; }
 
+// ------------------------------------------------------------ test options --
+// Process-wide options the unit tests set through xyzb_test_set_option
+// (include/xyzb_testing.h) to force rare paths — buffer regrowth, multi-batch
+// runs, a grouping path outside its default range, the multi-kernel merge,
+// the fp32 verify beside the sign-bit one. 0 = the engine's own choice.
+struct TestOptions {
+    std::atomic<long long> batch_entries{0}, hit_cap{0}, item_cap{0}, pair_cap{0}, grouping{0}, merge_large{0},
+        sign_verify_off{0}, trace{0}, brute_cuda{0};
+};
+TestOptions& topt() {
+    static TestOptions* o = new TestOptions();  // leaked on purpose (outlives static destructors)
+    return *o;
+}
+enum { kGroupAuto = 0, kGroupSort = 1, kGroupPart = 2, kGroupMsplit = 3 };
+
 // event-timed stage accounting on the dataset stream
 struct StageClock {
     cudaStream_t st;
@@ -244,7 +259,7 @@ struct xyzb_dataset {
     DevBuf yk_bits, spos, sneg, wabs, yreal, yreal32;
     // batch scratch
     DevBuf keys[2], vals[2], keys_x, hist, items, table, partial, rows, rid, rsign, streams, xorc, tot, work_run, nblocks, cum;
-    DevBuf pairs, npairs, bcnt, bend, bsize, table_end, perm, gtab, slots, pgrp, pent, pairs_t, tscratch, bstart, povf, yplanes;
+    DevBuf pairs, npairs, table_end, perm, gtab, slots, pgrp, pent, povf, yplanes;
     DevBuf zmask, zcount, zoff, zcnt_n, mt_state;
     // search scratch
     DevBuf enumerated, verified, sign_by_rid, hits, hit_count, rmin;
@@ -330,7 +345,7 @@ void validate_params(const xyzb_params* q) {
 // XYZB_TRACE=1: host-side phase times of dataset creation on stderr (device
 // drained at each mark, so only for diagnosis).
 struct Trace {
-    bool on = std::getenv("XYZB_TRACE") != nullptr;
+    bool on = topt().trace.load() != 0;
     cudaStream_t st;
     bool sync;  // false: host-side times only (the stream keeps running)
     std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
@@ -703,8 +718,6 @@ struct SearchCtx {
     double qinv = 0.0, qdelta = 0.0;
     long long qsum = 0;
     bool sign_verify = false;  // the bit-plane verify ran
-    bool tiled = false;    // this attempt verifies the accumulated pair list in column tiles
-    bool no_tile = false;  // the accumulated list would exceed 2^32 pairs: per-batch verify
     bool no_hash = false;  // a hashed partition overflowed: the sparse grouping runs on the sorted path
     bool pairs_in_sort = false;  // the fused group + join kernel writes the pair list (its stage is SORT)
     // top-K over all verified candidates (XYZB_TOPK_CANDIDATES): running rank threshold per batch
@@ -937,8 +950,8 @@ void run_batches(SearchCtx& c) {
         c.tk_shift = topk::bin_shift(max_rank);
     }
     // batch size: B*p entries under the budget (about 64 B of scratch each)
-    u64 budget = u64(1) << 26;  // XYZB_BATCH_ENTRIES overrides (tests force multi-batch runs with it)
-    if (const char* e = std::getenv("XYZB_BATCH_ENTRIES")) budget = std::max<u64>(1, std::strtoull(e, nullptr, 10));
+    u64 budget = u64(1) << 26;  // the batch_entries test option forces multi-batch runs
+    if (const long long e = topt().batch_entries.load()) budget = std::max<u64>(1, u64(e));
     const u64 B = std::max<u64>(1, std::min<u64>(R, budget / std::max<u64>(p, 1)));
     const u64 cap = B * p;
     for (int i = 0; i < 2; ++i) {
@@ -947,11 +960,10 @@ void run_batches(SearchCtx& c) {
     }
     ds->hist.ensure(rsort::hist_words(B, p) * 4);
     u64 item_cap = std::min<u64>(0xffffffffull, B * (p / 2 + 64) * c.item_scale);  // regrows on overflow
-    if (const char* e = std::getenv("XYZB_ITEM_CAP"))  // tests force the item-buffer regrow path with it
-        item_cap = std::min<u64>(item_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.item_scale);
+    if (const long long e = topt().item_cap.load())  // tests force the item-buffer regrow path
+        item_cap = std::min<u64>(item_cap, std::max<u64>(1, u64(e)) * c.item_scale);
     if (item_cap > 0xffffffffull) throw internal_error("xyzb: batch too large for 32-bit item indices");
     ds->items.ensure(item_cap * sizeof(kern::Item));
-    const char* sort_sel = std::getenv("XYZB_SORT");  // "segments": multi-kernel LSD sort (tests)
     // host plan -> pinned -> device
     const bool host_rows = !c.plan.rows.empty();
     // per-batch counters live in their own pinned slots: a later batch must not
@@ -1004,95 +1016,50 @@ void run_batches(SearchCtx& c) {
     c.item_cap = item_cap;
     c.nbatches = nbatches;
     const bool pair_path = c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128;
-    // XYZB_TILED=1: the pair lists of all batches accumulate and are verified once, in
-    // L2-sized column tiles (tile_verify.cuh). Measured on B200 it does not pay (config 4:
-    // verify 95 -> 107 ms): random 1.3 KB column gathers confined to a 63 MB window run at
-    // 8.3 TB/s against 7.1 TB/s over all of X (tools/l2_window.cu), so it stays opt-in.
-    const char* tsel = std::getenv("XYZB_TILED");
-    const bool tiled = pair_path && !c.no_tile && !c.topk_all && nbatches <= tile::kMaxBatches && tsel &&
-                       std::string(tsel) == "1";
-    c.tiled = tiled;
     if (pair_path) {
-        c.pair_cap = std::min<u64>(0xffffffffull,
-                                   std::max<u64>(u64(1) << 20, tiled ? R * p / 2 : B * p) * c.pair_scale);
-        if (const char* e = std::getenv("XYZB_PAIR_CAP"))  // tests force the pair-list regrow path with it
-            c.pair_cap = std::min<u64>(c.pair_cap, std::max<u64>(1, std::strtoull(e, nullptr, 10)) * c.pair_scale);
+        c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, B * p) * c.pair_scale);
+        if (const long long e = topt().pair_cap.load())  // tests force the pair-list regrow path
+            c.pair_cap = std::min<u64>(c.pair_cap, std::max<u64>(1, u64(e)) * c.pair_scale);
         ds->pairs.ensure(c.pair_cap * sizeof(kern::PairRec));
         if (c.topk_all) ds->tk_sint.ensure(c.pair_cap * 4);
         ds->npairs.ensure(nbatches * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->npairs.p, 0, nbatches * 4, st));
     }
-    tile::Plan tplan;
-    if (tiled) {
-        ds->pairs_t.ensure(c.pair_cap * sizeof(kern::PairRec));
-        int dev = 0, l2 = 0;
-        XYZB_CUDA(cudaGetDevice(&dev));
-        XYZB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
-        u64 l2b = u64(l2);
-        if (const char* e = std::getenv("XYZB_TILE_L2")) l2b = std::max<u64>(1, std::strtoull(e, nullptr, 10));  // tests
-        tplan = tile::plan(p, ds->Wp * 8, l2b);
-        ds->tscratch.ensure(tile::hist_words(tplan) * 4);
-        ds->bstart.ensure((nbatches + 1) * 4);
-        XYZB_CUDA(cudaMemsetAsync(ds->bstart.p, 0, 4, st));
-    }
     const u32 hmax = 8u;  // held columns per item (pair expansion chunks)
-    // grouping: counting sort into 2^M buckets when 2^M is comparable to p
-    // (fastest measured on B200 for config 2), else the per-run cluster radix
-    // sort; XYZB_GROUPING=sort / XYZB_SORT=segments force the sorted paths
-    const char* gsel = std::getenv("XYZB_GROUPING");
-    // M <= 17: grouping and join fused per run on a cluster (tables in DSMEM);
-    // XYZB_GROUPING=bucket keeps the multi-kernel counting sort
-    // M <= 16: one CTA per run with 16-bit shared counters (no cluster barriers);
-    // XYZB_GROUPING=cluster keeps the DSMEM cluster kernel
-    const auto gsel_is = [&](const char* v) { return gsel && std::string(gsel) == v; };
-    // M = 17, 18: a 2^(M-16)-CTA cluster per run (16-bit tables, DSMEM exchanges) when the bucket
-    // space is dense enough — measured faster than the DSMEM-table kernel and the counting sort at
-    // p = 1e5; at M = 19, 20 every CTA streaming all keys costs more than the counting sort (config 4:
-    // 102 vs 53 ms), so the kernel runs there only when forced (XYZB_GROUPING=msplit, also for sparse
-    // runs; =cluster keeps the DSMEM-table kernel at M = 17)
-    // M >= 19 with a dense bucket space: partition pass + one small CTA per (run, partition)
-    // (XYZB_GROUPING=part forces it for any M <= 24)
-    // sparse bucket spaces (2^M > 4p + 1024, M <= 31): the same partition pass with a shared-memory
-    // hash table per partition (a partition above its capacity raises povf: the search is redone on
-    // the sorted path); XYZB_GROUPING=sort keeps the cluster radix sort
+    // Grouping + join, by the run's bucket space 2^M against p:
+    //   4 <= M <= 16, dense: two CTAs per run splitting a 16-bit shared bucket table (split_group_join);
+    //   M = 17, 18, dense:   a 2^(M-16)-CTA cluster of such tables (msplit_group_join);
+    //   19 <= M <= 24, dense: partition pass + one CTA per (run, partition) (part_group.cuh);
+    //   sparse (2^M > 4p + 1024), M <= 31: the same partition pass with shared hash tables (a partition
+    //     above its capacity raises povf: the search is redone on the sorted path);
+    //   otherwise (M < 4, M > 31, a hashed overflow): per-run cluster radix sorts of symmetric keys.
+    // The grouping test option forces the sorted path (1), the partition path for any M <= 24 (2) or the
+    // cluster of 16-bit tables for M = 19, 20 and sparse spaces (3).
+    const long long gsel = topt().grouping.load();
     const bool dense = (u64(1) << M) <= 4 * p + 1024;
-    const bool part_hash = sizeof(K) == 4 && M >= 2 && M <= 31 && !dense && !c.no_hash && !sort_sel &&
-                           (!gsel || gsel_is("part"));
-    const bool part_path = part_hash || (sizeof(K) == 4 && M >= 2 && M <= 24 && dense && !sort_sel &&
-                                         (gsel_is("part") || (!gsel && M >= 19)));
+    const bool part_hash = sizeof(K) == 4 && M >= 2 && M <= 31 && !dense && !c.no_hash &&
+                           (gsel == kGroupAuto || gsel == kGroupPart);
+    const bool part_path = part_hash || (sizeof(K) == 4 && M >= 2 && M <= 24 && dense &&
+                                         (gsel == kGroupPart || (gsel == kGroupAuto && M >= 19)));
     const int pk = part_hash ? kern::part_digits_hash(int(M), p) : kern::part_digits(int(M), p);
     if (part_path) {
         ds->pgrp.ensure(kern::part_scratch_words(pk, B) * 4);
         ds->pent.ensure(cap * 8);
     }
-    const bool ms_path = !part_path && M >= 17 && M <= 20 && !sort_sel && !gsel_is("sort") && !gsel_is("bucket") &&
-                         !gsel_is("cluster") && sizeof(K) == 4 &&
-                         ((M <= 18 && (u64(1) << M) <= 4 * p + 1024) || gsel_is("msplit")) &&
+    const bool ms_path = !part_path && sizeof(K) == 4 && M >= 17 && M <= 20 &&
+                         ((gsel == kGroupAuto && M <= 18 && dense) || gsel == kGroupMsplit) &&
                          kern::msplit_schedulable(int(M));
-    const bool grouped_path = !part_path && !ms_path && M <= 17 && (u64(1) << M) <= 4 * p + 1024 && !sort_sel &&
-                              !(gsel && (std::string(gsel) == "sort" || std::string(gsel) == "bucket"));
-    // 4 <= M <= 16: two CTAs per run (cluster), bucket space split on a key bit
-    // (XYZB_GROUPING=cta keeps one CTA per run)
-    const bool cta_path = grouped_path && M <= 16 && !(gsel && std::string(gsel) == "cluster");
-    const bool split_path = cta_path && M >= 4 && !(gsel && std::string(gsel) == "cta");
-    const bool cluster_path = grouped_path && !cta_path;
-    if (cta_path && kern::cta_group_scratch(int(M), p)) ds->gtab.ensure(kern::cta_group_scratch(int(M), p) * 4);
+    const bool split_path = !part_path && !ms_path && sizeof(K) == 4 && M >= 4 && M <= 16 && dense &&
+                            gsel == kGroupAuto;
     if (ms_path) {
         if (kern::msplit_group_scratch(int(M), p)) ds->gtab.ensure(kern::msplit_group_scratch(int(M), p) * 4);
         ds->slots.ensure(kSMs * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->slots.p, 0, kSMs * 4, st));
     }
     if (split_path) {
+        if (kern::split_group_scratch(int(M), p)) ds->gtab.ensure(kern::split_group_scratch(int(M), p) * 4);
         ds->slots.ensure(kSMs * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->slots.p, 0, kSMs * 4, st));
-    }
-    const bool buckets = !part_path && !grouped_path && !ms_path && M <= 22 && (u64(1) << M) <= 4 * p + 1024 && (B << M) <= (u64(1) << 28) &&
-                         !(gsel && std::string(gsel) == "sort") && !sort_sel;
-    if (buckets) {
-        ds->bcnt.ensure((B << M) * 4);
-        ds->bend.ensure(((B << M) + 1) * 4);
-        ds->bsize.ensure(8);
-        ds->partial.ensure(scan::kGrid * 8);
     }
     const int bits = static_cast<int>(M);
     for (u64 b0 = 0, batch_idx = 0; b0 < R; b0 += B, ++batch_idx) {
@@ -1157,7 +1124,7 @@ void run_batches(SearchCtx& c) {
         K* kb[2] = {ds->keys[0].as<K>(), ds->keys[1].as<K>()};
         u32* vb[2] = {ds->vals[0].as<u32>(), ds->vals[1].as<u32>()};
         u32* nitems = ds->nblocks.as<u32>() + batch_idx;
-        u32* npairs_b = pair_path ? ds->npairs.as<u32>() + (tiled ? 0 : batch_idx) : nullptr;  // tiled: one list
+        u32* npairs_b = pair_path ? ds->npairs.as<u32>() + batch_idx : nullptr;
         const u32* sv = nullptr;
         const K* sorted_keys = nullptr;
         int vshift = 0;
@@ -1220,65 +1187,6 @@ void run_batches(SearchCtx& c) {
             clk.span(XYZB_STAGE_SORT, e1, e2);
             c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4);  // keys read twice, indices written
             c.pairs_in_sort = true;
-        } else if (cta_path) {
-            // ---- group + join fused: one CTA per run, 16-bit bucket counters in shared memory ----
-            kern::cta_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
-                                           ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
-                                           nitems, static_cast<u32>(item_cap), npairs_b, ds->pairs.as<kern::PairRec>(),
-                                           static_cast<u32>(c.pair_cap), ds->gtab.as<u32>(), st);
-            XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_SORT] += 1;
-            sv = vb[0];
-            e2 = clk.mark();
-            clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4);  // keys read twice, indices written
-            c.pairs_in_sort = true;
-        } else if (cluster_path) {
-            // ---- group + join fused: one thread-block cluster per run, bucket tables in DSMEM ----
-            kern::cluster_group_join_launch<K>(k0, nb, p, int(M), ds->xorc.as<K>(), c.guard, hmax, vb[0],
-                                               ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(),
-                                               nitems, static_cast<u32>(item_cap), npairs_b,
-                                               ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap), st);
-            XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_SORT] += 1;
-            sv = vb[0];
-            e2 = clk.mark();
-            clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4);  // keys read twice, indices written
-            c.pairs_in_sort = true;
-        } else if (buckets) {
-            // ---- group: counting sort into 2^M buckets per run ----
-            const u64 nbk = nb << M;
-            XYZB_CUDA(cudaMemsetAsync(ds->bcnt.p, 0, nbk * 4, st));
-            dim3 gp(static_cast<u32>(ceil_div(p, 256)), static_cast<u32>(nb));
-            kern::bucket_count<K><<<gp, 256, 0, st>>>(k0, p, int(M), ds->bcnt.as<u32>());
-            XYZB_LAUNCH_CHECK();
-            u32* hn = reinterpret_cast<u32*>(hp + hbytes - 96 - 2 * R * 4) + 2 * batch_idx;
-            *hn = static_cast<u32>(nbk);
-            XYZB_CUDA(cudaMemcpyAsync(ds->bsize.p, hn, 4, cudaMemcpyHostToDevice, st));
-            scan::exclusive<u32>(ds->bcnt.as<u32>(), ds->bsize.as<u32>(), ds->bend.as<u32>(),
-                                 reinterpret_cast<u32*>(ds->partial.p), st, &c.launches[XYZB_STAGE_SORT]);
-            kern::bucket_scatter<K><<<gp, 256, 0, st>>>(k0, p, int(M), ds->bend.as<u32>(), vb[0]);
-            XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_SORT] += 2;
-            sv = vb[0];
-            e2 = clk.mark();
-            clk.span(XYZB_STAGE_SORT, e1, e2);
-            c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 4) + nbk * 12;
-            // ---- join (+ guard bookkeeping) ----
-            XYZB_CUDA(cudaMemsetAsync(ds->tot.p, 0, nb * 8, st));
-            XYZB_CUDA(cudaMemsetAsync(ds->work_run.p, 0, nb * 8, st));
-            dim3 gb(static_cast<u32>(ceil_div(u64(1) << M, 256)), static_cast<u32>(nb));
-            kern::bucket_join_count<K><<<gb, 256, 0, st>>>(ds->bcnt.as<u32>(), int(M), ds->xorc.as<K>(), p,
-                                                           ds->tot.as<u64>(), ds->work_run.as<u64>());
-            XYZB_LAUNCH_CHECK();
-            kern::bucket_join_emit<K><<<gb, 256, 0, st>>>(ds->bcnt.as<u32>(), ds->bend.as<u32>(), int(M), ds->xorc.as<K>(),
-                                                          p, ds->tot.as<u64>(), c.guard, hmax, ds->items.as<kern::Item>(),
-                                                          nitems, static_cast<u32>(item_cap), npairs_b,
-                                                          ds->pairs.as<kern::PairRec>(), static_cast<u32>(c.pair_cap),
-                                                          sv);
-            XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_JOIN] += 2;
         } else {
             // symmetric keys (u = min(v, v^c), side bit): the join needs no lookups;
             // M = 64 keeps plain keys and binary-search partner lookups
@@ -1293,15 +1201,10 @@ void run_batches(SearchCtx& c) {
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_SORT] += 1;
             }
-            // ---- sort: one cluster per run (DSMEM histogram exchange), or the multi-kernel LSD sort ----
-            int res;
-            if (sort_sel && std::string(sort_sel) == "segments") {
-                res = rsort::sort_segments<K>(kb, vb, nb, p, sbits, ds->hist.as<u32>(), st, &c.launches[XYZB_STAGE_SORT]);
-            } else {
-                res = rsort::sort_runs_launch<K>(kb[0], vb[0], kb[1], vb[1], nb, p, sbits, st);
-                XYZB_LAUNCH_CHECK();
-                c.launches[XYZB_STAGE_SORT] += 1;
-            }
+            // ---- sort: one cluster per run (DSMEM histogram exchange) ----
+            const int res = rsort::sort_runs_launch<K>(kb[0], vb[0], kb[1], vb[1], nb, p, sbits, st);
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_SORT] += 1;
             e2 = clk.mark();
             clk.span(XYZB_STAGE_SORT, e1, e2);
             c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8) * u64((sbits + 7) / 8);
@@ -1351,7 +1254,7 @@ void run_batches(SearchCtx& c) {
         A.guard = c.guard;
         A.sv = sv;
         A.S = p;
-        const bool unsorted = buckets || grouped_path || ms_path || part_path;
+        const bool unsorted = split_path || ms_path || part_path;
         A.vkeys = unsorted ? static_cast<const void*>(k0) : static_cast<const void*>(sorted_keys);
         A.vkeys_by_pos = unsorted ? 0 : 1;
         A.xkeys = unsorted ? static_cast<const void*>(k0) : ds->keys_x.p;
@@ -1375,57 +1278,31 @@ void run_batches(SearchCtx& c) {
             if (pair_path) A.sint_out = ds->tk_sint.as<u32>();
             A.rank_thr = &ds->tk_state.as<topk::State>()->thr;
         }
-        u32 vgrid = kSMs * 8;
-        if (const char* ev = std::getenv("XYZB_VGRID")) vgrid = static_cast<u32>(std::max(1ul, std::strtoul(ev, nullptr, 10)));
+        const u32 vgrid = kSMs * 8;
         if (pair_path) {
-            u32* np = ds->npairs.as<u32>() + (tiled ? 0 : batch_idx);
+            u32* np = ds->npairs.as<u32>() + batch_idx;
             kern::expand_pairs<<<vgrid, 256, 0, st>>>(A.items, A.nitems, A.item_cap, p, ds->pairs.as<kern::PairRec>(),
                                                       static_cast<u32>(c.pair_cap), sv);
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 1;
-            if (tiled) {  // the batch's slots end here; verify after the last batch
-                XYZB_CUDA(cudaMemcpyAsync(ds->bstart.as<u32>() + batch_idx + 1, np, 4, cudaMemcpyDeviceToDevice, st));
-                clk.span(XYZB_STAGE_JOIN, e3, clk.mark());
-                if (b0 + B < R) continue;
-                // ---- all batches: bucket the pair list by column tile, one verify over it ----
-                cudaEvent_t es0 = clk.mark();
-                tile::sort_by_tile(ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), tplan,
-                                   ds->bstart.as<u32>(), static_cast<u32>(nbatches), static_cast<u32>(B),
-                                   ds->tscratch.as<u32>(), ds->pairs_t.as<kern::PairRec>(), st,
-                                   &c.launches[XYZB_STAGE_JOIN]);
-                clk.span(XYZB_STAGE_JOIN, es0, clk.mark());
-                A.nitems = ds->nblocks.as<u32>();  // (an item overflow in any batch forces a retry anyway)
-                A.rid = ds->rid.as<u32>();
-                A.run_sign = ds->rsign.as<int8_t>();
-                A.xkeys = nullptr;  // hits recompute their key from the run's draws
-                A.krows = ds->rows.as<u32>();
-                A.kM = int(M);
-                A.kXc = ds->Xc.as<u64>();
-                A.kWp = static_cast<u32>(ds->Wp);
-            }
-            const kern::PairRec* vpairs = tiled ? ds->pairs_t.as<kern::PairRec>() : ds->pairs.as<kern::PairRec>();
             const u64 W2 = ds->Wp / 2;
-            // team of G lanes, NIT 16-byte chunks of each column per lane; XYZB_VP_CHUNKS
-            // (1/2/4) and XYZB_VERIFY=simple select measured variants
-            // measured on B200 (tools/sweep_verify.py): long columns (>= 512 B) prefer 8-lane
-            // teams with 64 B per lane and column, short ones full-column teams with the
-            // next pair's columns prefetched
-            u64 chunks = W2 >= 32 ? 4 : 1;
-            bool simple = W2 >= 32;
-            if (const char* ev = std::getenv("XYZB_VP_CHUNKS"))
-                chunks = std::min<u64>(4, std::max<u64>(1, std::strtoull(ev, nullptr, 10)));
-            if (const char* ev = std::getenv("XYZB_VERIFY")) simple = std::string(ev) != "pipelined";
+            // team of G lanes, NIT 16-byte chunks of each column per lane, measured on B200
+            // (tools/sweep_verify.py, tools/l2_window2.cu): long columns (>= 512 B) take 8..32-lane
+            // teams with up to 64 B per lane and column walking one pair at a time, short ones
+            // full-column teams with the next pair's columns prefetched
+            const u64 chunks = W2 >= 32 ? 4 : 1;
+            const bool simple = W2 >= 32;
             int G = 1;
             while (G < 32 && u64(G) * chunks < W2) G <<= 1;
             const int nit = static_cast<int>(ceil_div(W2, G));
-            const auto* PR = vpairs;
+            const auto* PR = ds->pairs.as<kern::PairRec>();
             const u32 pc = static_cast<u32>(c.pair_cap);
             const u64* X = ds->Xc.as<u64>();
             const u32 Wp = static_cast<u32>(ds->Wp);
             const u64* Y = ds->yk_bits.as<u64>();
             const u32 n32 = static_cast<u32>(c.n);
             cudaEvent_t ev0 = clk.mark();
-            if (!tiled) clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
+            clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
 #define XYZB_VP(GG, NN)                                                                                          \
     do {                                                                                                         \
         if (simple)                                                                                              \
@@ -1481,8 +1358,7 @@ void run_batches(SearchCtx& c) {
                 else kern::verify_items<<<vgrid, 256, 0, st>>>(A, f);
             } else {
                 kern::RealStrength<false> f{ds->Xc32.as<float>(), ds->n4, ds->yreal32.as<float>(), c.norm, c.gamma};
-                const char* sv_sel = std::getenv("XYZB_SIGN_VERIFY");
-                if (!(sv_sel && std::string(sv_sel) == "0") && ds->Spos.p) {
+                if (!topt().sign_verify_off.load() && ds->Spos.p) {
                     // sign transform: strengths from column sign bits and the response's bit planes
                     kern::SignStrength g{ds->Spos.as<u64>(), ds->Snz.as<u64>(), ds->W, ds->yplanes.as<u64>(),
                                          c.qsum, ds->has_zero, c.qinv, c.norm, c.gamma, c.qdelta, f};
@@ -1542,7 +1418,7 @@ void merge_hits(SearchCtx& c, u32 H, u32 rmax, std::vector<xyzb_hit>& hits_out, 
     topk_out.clear();
     if (H == 0) return;
     u64& L = c.launches[XYZB_STAGE_MERGE];
-    if (H <= u32(merge::kSmallMerge) && !std::getenv("XYZB_MERGE_LARGE")) {
+    if (H <= u32(merge::kSmallMerge) && !topt().merge_large.load()) {
         // short lists: one CTA dedups, orders and ranks in shared memory
         const size_t smem = merge::small_merge_smem(merge::kSmallMerge);
         func_smem(merge::merge_small, smem);
@@ -1818,7 +1694,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     std::vector<u64> enumerated(Rall), verified(Rall);
     // the single-CTA merge is queued right behind the search (hit count read on
     // the device); one host round trip then returns every counter at once
-    const bool fused_merge = !q->stop_after_first_hit && !std::getenv("XYZB_MERGE_LARGE");
+    const bool fused_merge = !q->stop_after_first_hit && !topt().merge_large.load();
     u32 fusedK = 0xffffffffu, fusedKK = 0;
     u32 fcap = 0;
     cudaEvent_t ev_dev_end = nullptr;  // end of the device work (results resident in HBM)
@@ -1877,12 +1753,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             const u32* np = reinterpret_cast<const u32*>(hs + o_pairs);
             pneed = *std::max_element(np, np + nbt);
             if (pneed > c.pair_cap) {
-                if (c.pair_cap == 0xffffffffull && c.tiled) {
-                    c.no_tile = true;  // the search's pairs exceed 2^32: per-batch verify
-                    c.pair_scale = 1;
-                } else if (c.pair_cap == 0xffffffffull)
-                    throw internal_error("xyzb: candidate pairs exceed 2^32 in one batch");
-                else
+                if (c.pair_cap == 0xffffffffull) throw internal_error("xyzb: candidate pairs exceed 2^32 in one batch");
                 c.pair_scale *= std::max<u64>(2, ceil_div(pneed, c.pair_cap));
             }
         }
@@ -2268,10 +2139,9 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
         const size_t hs = n <= brute::kSmemHistMax ? size_t(n + 1) * 4 : 0;
         func_smem(brute::all_pairs<false>, (brute::kSmemHistMax + 1) * 4);
         const u64* nzp = yb.as<u64>() + Wp;
-        // tensor cores (tcgen05 kind::i8 Gram product) by default; XYZB_BRUTE=cuda: CUDA-core popcounts
-        const char* bsel = std::getenv("XYZB_BRUTE");
-        const bool tc = !(bsel && std::string(bsel) == "cuda");
-        const bool tc1 = bsel && std::string(bsel) == "tc1";  // the single-issuer tensor-core kernel
+        // tensor cores (tcgen05 kind::i8 Gram product); the brute_cuda test option runs the CUDA-core
+        // popcount tiles instead (the independent cross-check of the tensor-core kernel)
+        const bool tc = !topt().brute_cuda.load();
         u32 nz = 0;
         for (u64 i = 0; i < n; ++i) nz += (y_sign[i] == 1 || y_sign[i] == -1) ? 1u : 0u;
         const u64 Kp = round_up(n, 128);
@@ -2285,18 +2155,13 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
             XYZB_LAUNCH_CHECK();
             tmA = operand_map(opA.p, p, Kp, brute::kTcM);
             tmB = operand_map(opB.p, p, Kp, brute::kTcN);
-            func_smem(brute::all_pairs_tc<false>, brute::kTcSmem);
-            func_smem(brute::all_pairs_tc<true>, brute::kTcSmem);
             func_smem(brute::all_pairs_tc2<false>, brute::kTcSmem2);
             func_smem(brute::all_pairs_tc2<true>, brute::kTcSmem2);
         }
         const u64 ntc = u64((p + brute::kTcM - 1) / brute::kTcM) * ((p + brute::kTcN - 1) / brute::kTcN);
         const u32 tc_grid = static_cast<u32>(std::min<u64>(ntc, kSMs));
-        if (tc && !tc1) {
+        if (tc) {
             brute::all_pairs_tc2<false><<<tc_grid, brute::kTcWarps * 32, brute::kTcSmem2, st>>>(
-                tmA, tmB, u32(p), u32(n), nz, u32(Kp), hist.as<unsigned long long>(), 0u, nullptr, nullptr, 0u);
-        } else if (tc) {
-            brute::all_pairs_tc<false><<<tc_grid, brute::kTcThreads, brute::kTcSmem, st>>>(
                 tmA, tmB, u32(p), u32(n), nz, u32(Kp), hist.as<unsigned long long>(), 0u, nullptr, nullptr, 0u);
         } else {
             brute::all_pairs<false><<<brute::all_pairs_grid(), brute::kThreads, hs, st>>>(
@@ -2356,12 +2221,8 @@ extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t 
         outb.ensure(emit * sizeof(brute::PairOut));
         nout.ensure(4);
         XYZB_CUDA(cudaMemsetAsync(nout.p, 0, 4, st));
-        if (tc && !tc1) {
+        if (tc) {
             brute::all_pairs_tc2<true><<<tc_grid, brute::kTcWarps * 32, brute::kTcSmem2, st>>>(
-                tmA, tmB, u32(p), u32(n), nz, u32(Kp), nullptr, u32(cutoff), outb.as<brute::PairOut>(),
-                nout.as<u32>(), u32(emit));
-        } else if (tc) {
-            brute::all_pairs_tc<true><<<tc_grid, brute::kTcThreads, brute::kTcSmem, st>>>(
                 tmA, tmB, u32(p), u32(n), nz, u32(Kp), nullptr, u32(cutoff), outb.as<brute::PairOut>(),
                 nout.as<u32>(), u32(emit));
         } else {
@@ -2665,8 +2526,8 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
                                  std::to_string(ndev) + ")");
         std::unique_ptr<xyzb_dataset> ds(new xyzb_dataset());
         ds->device = devs[0];
-        if (const char* e = std::getenv("XYZB_HIT_CAP"))  // tests force the hit-buffer regrow path with it
-            ds->hit_cap = static_cast<u32>(std::max<u64>(1, std::strtoull(e, nullptr, 10)));
+        if (const long long e = topt().hit_cap.load())  // tests force the hit-buffer regrow path
+            ds->hit_cap = static_cast<u32>(std::max<u64>(1, u64(e)));
         {
             DeviceGuard dg(ds->device);
             XYZB_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
@@ -2854,5 +2715,24 @@ int xyzb_design_pair_correlations(xyzb_design* d, const double* residual, const 
 }
 
 void xyzb_free(void* p) { std::free(p); }
+
+int xyzb_test_set_option(const char* name, long long value) {
+    if (!name) return XYZB_E_DATA;
+    TestOptions& o = topt();
+    const std::string s = name;
+    std::atomic<long long>* slot = s == "batch_entries"     ? &o.batch_entries
+                                   : s == "hit_cap"         ? &o.hit_cap
+                                   : s == "item_cap"        ? &o.item_cap
+                                   : s == "pair_cap"        ? &o.pair_cap
+                                   : s == "grouping"        ? &o.grouping
+                                   : s == "merge_large"     ? &o.merge_large
+                                   : s == "sign_verify_off" ? &o.sign_verify_off
+                                   : s == "trace"           ? &o.trace
+                                   : s == "brute_cuda"      ? &o.brute_cuda
+                                                            : nullptr;
+    if (!slot) return XYZB_E_DATA;
+    slot->store(value);
+    return XYZB_OK;
+}
 
 } // extern "C"

@@ -53,10 +53,8 @@ constexpr int kPgMaxK = 10;                          // partition digits: at mos
 // most kPgMaxK and M - 1 (a key and its partner share a partition).
 constexpr u64 kPjTarget = 4096;
 inline int part_digits(int M, u64 p) {
-    u64 target = kPjTarget;
-    if (const char* e = std::getenv("XYZB_PART_TARGET")) target = std::max<u64>(1, std::strtoull(e, nullptr, 10));
     int k = 1;
-    while (k < kPgMaxK && k < M - 1 && (p >> k) > target) ++k;
+    while (k < kPgMaxK && k < M - 1 && (p >> k) > kPjTarget) ++k;
     return std::min(std::max(k, M - 14), M - 1);
 }
 inline int part_local_bits(int M, u64 p) { return M - part_digits(M, p); }

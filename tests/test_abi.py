@@ -30,6 +30,16 @@ def test_libxyzb_exports_every_declared_symbol():
     assert set(names) == set(_abi.SIGNATURES), "ctypes mirror out of sync with include/xyzb.h"
 
 
+def test_libxyzb_exports_the_test_hook():
+    lib = C.CDLL(_lib.LIB_PATH)
+    for name in declared("xyzb_testing.h"):
+        assert hasattr(lib, name), name
+    for name in _lib.TEST_OPTIONS:
+        _lib.set_test_option(name, 0)  # known names; no device needed
+    with pytest.raises(ValueError):
+        _lib.set_test_option("no_such_option", 1)
+
+
 def test_libxyzb_synth_exports_every_declared_symbol():
     lib = C.CDLL(_lib.SYNTH_PATH)
     for name in declared("xyzb_synth.h"):

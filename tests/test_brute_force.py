@@ -41,14 +41,14 @@ OPTIONS = [
 ]
 
 
-@pytest.mark.parametrize("kernel", ["tensor", "tc1", "cuda"])
+@pytest.mark.parametrize("kernel", ["tensor", "cuda"])
 @pytest.mark.parametrize("opt", OPTIONS, ids=[str(o) for o in OPTIONS])
-def test_brute_force_matches_the_reference(opt, kernel, monkeypatch):
-    """All device kernels: the warp-specialised tcgen05 int8 Gram product
-    (default), its single-issuer form (XYZB_BRUTE=tc1) and the CUDA-core
-    XOR-popcount tiles (XYZB_BRUTE=cuda)."""
-    if kernel in ("cuda", "tc1"):
-        monkeypatch.setenv("XYZB_BRUTE", kernel)
+def test_brute_force_matches_the_reference(opt, kernel, engine_options):
+    """Both device kernels: the warp-specialised tcgen05 int8 Gram product
+    (default) and the CUDA-core XOR-popcount tiles (the brute_cuda test
+    option, an independent cross-check)."""
+    if kernel == "cuda":
+        engine_options(brute_cuda=1)
     xb = _engine()
     for name, x, y in _instances():
         want_pairs, want_scanned, want_hist = ck.ref_brute_force(x, y, force=True, **opt)

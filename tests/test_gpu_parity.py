@@ -46,23 +46,17 @@ def compare_continuous(got, want_hits, gamma, tol=REL_TOL):
     assert common_g == common_w
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments", "merge_large",
-                                      "tiled"])
+@pytest.mark.parametrize("grouping", ["auto", "part", "sort", "merge_large"])
 @pytest.mark.parametrize("name", SEARCH_CASES)
-def test_search_matches_reference_fixture(name, grouping, monkeypatch):
-    """All grouping paths: two CTAs per run splitting the 16-bit shared
-    bucket table (default for 4 <= M <= 16), one CTA per run, the DSMEM
-    cluster kernel, the multi-kernel counting sort into 2^M buckets, per-run
-    cluster radix sort, multi-kernel segmented radix sort, partition pass +
-    per-(run, partition) tables."""
-    if grouping in ("sort", "bucket", "cluster", "cta", "part"):
-        monkeypatch.setenv("XYZB_GROUPING", grouping)
-    if grouping == "segments":
-        monkeypatch.setenv("XYZB_SORT", "segments")
+def test_search_matches_reference_fixture(name, grouping, engine_options):
+    """All grouping paths: the engine's choice by M (two CTAs per run
+    splitting the 16-bit shared bucket table for 4 <= M <= 16, the partition
+    pass + per-(run, partition) tables, ...), the partition path forced, the
+    per-run cluster radix sort forced, and the multi-kernel merge."""
+    if grouping in ("sort", "part"):
+        engine_options(grouping=grouping)
     if grouping == "merge_large":  # the multi-kernel merge instead of the single-CTA one
-        monkeypatch.setenv("XYZB_MERGE_LARGE", "1")
-    if grouping == "tiled":  # the accumulated pair list verified in L2 column tiles
-        monkeypatch.setenv("XYZB_TILED", "1")
+        engine_options(merge_large=1)
     xb = _engine()
     x, y, cfg, z = load_case(name)
     rep = xb.Dataset(x).search(y, cfg)
@@ -198,27 +192,18 @@ def test_binary_matches_live_reference_cfg1_variants():
     assert any((min(h.j, h.k), max(h.j, h.k)) == (4, 16) for h in rep.hits)
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "bucket", "part", "sort", "segments", "tiled",
-                                      "tiled_part"])
-def test_multi_batch_and_hit_regrow_are_invisible(monkeypatch, grouping):
+@pytest.mark.parametrize("grouping", ["auto", "part", "sort"])
+def test_multi_batch_and_hit_regrow_are_invisible(engine_options, grouping):
     """Batching and hit-buffer regrowth must not change anything (the GPU
     analogue of test_search.cpp:275-295, hit lists independent of threads)."""
     xb = _engine()
     x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
     cfg = xb.SearchConfig(m=8, l=10, gamma=0.55, seed=7, top_k=10)
     base = xb.Dataset(x).search(y, cfg)
-    if grouping in ("sort", "bucket", "cluster", "cta", "part"):
-        monkeypatch.setenv("XYZB_GROUPING", grouping)
-    if grouping == "segments":
-        monkeypatch.setenv("XYZB_SORT", "segments")
-    if grouping.startswith("tiled"):
-        monkeypatch.setenv("XYZB_TILED", "1")
-        if grouping == "tiled_part":
-            monkeypatch.setenv("XYZB_GROUPING", "part")
-    monkeypatch.setenv("XYZB_BATCH_ENTRIES", "6000")  # three runs per batch, a shorter last batch
-    monkeypatch.setenv("XYZB_HIT_CAP", "7")
-    monkeypatch.setenv("XYZB_ITEM_CAP", "5")
-    monkeypatch.setenv("XYZB_PAIR_CAP", "100")
+    if grouping in ("sort", "part"):
+        engine_options(grouping=grouping)
+    # three runs per batch, a shorter last batch; every buffer regrows
+    engine_options(batch_entries=6000, hit_cap=7, item_cap=5, pair_cap=100)
     other = xb.Dataset(x).search(y, cfg)
     assert report_hits(other) == report_hits(base)
     assert other.top_k == base.top_k
@@ -383,13 +368,13 @@ def test_xyz1_file_ingest_matches_in_memory_and_reference_errors(tmp_path):
         xb.Dataset.open(tmp_path / "missing.xyz")
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "part"])
-def test_bucket_above_16_bits_falls_back_exactly(grouping, monkeypatch):
+@pytest.mark.parametrize("grouping", ["auto", "part"])
+def test_bucket_above_16_bits_falls_back_exactly(grouping, engine_options):
     """p > 65535 with 70000 identical (monomorphic) columns: one bucket holds
     more columns than a 16-bit shared counter can; the CTA grouping redoes
     such a run with 32-bit counters. Hits and counters equal the reference."""
-    if grouping in ("cluster", "cta", "part"):
-        monkeypatch.setenv("XYZB_GROUPING", grouping)
+    if grouping == "part":
+        engine_options(grouping=grouping)
     xb = _engine()
     rng = np.random.default_rng(11)
     n, p_const, p_rand = 128, 70000, 300
@@ -431,13 +416,13 @@ def test_dirty_padding_bits_are_rejected_on_upload():
         xb.Dataset(x).search(y, cfg))
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "part"])
-def test_constant_response_partner_is_the_complement(grouping, monkeypatch):
+@pytest.mark.parametrize("grouping", ["auto", "part"])
+def test_constant_response_partner_is_the_complement(grouping, engine_options):
     """y constant: in the negative pass c = x-key ^ z-key has every bit set, so
     each key's partner is its complement (no key bit is shared by a key and
     its partner: the two-CTA split reads the partner half through DSMEM)."""
-    if grouping in ("cluster", "cta", "part"):
-        monkeypatch.setenv("XYZB_GROUPING", grouping)
+    if grouping == "part":
+        engine_options(grouping=grouping)
     xb = _engine()
     x, _ = ck.ref_planted(300, 400, 3, 7, 0.9, 3)
     y = np.ones(300, np.int8)
@@ -452,13 +437,13 @@ def test_constant_response_partner_is_the_complement(grouping, monkeypatch):
         assert len(want.hits) > 0
 
 
-@pytest.mark.parametrize("grouping", ["auto", "cta", "cluster", "part"])
-def test_grouping_kernels_sweep_vs_oracle(grouping, monkeypatch):
+@pytest.mark.parametrize("grouping", ["auto", "part"])
+def test_grouping_kernels_sweep_vs_oracle(grouping, engine_options):
     """The fused group + join kernels (two-CTA split, one CTA, DSMEM cluster)
     over the M range they serve (4..17) and p from a handful of columns to
     2^M-sized tables: bit-exact against the restatement."""
-    if grouping in ("cta", "cluster", "part"):
-        monkeypatch.setenv("XYZB_GROUPING", grouping)
+    if grouping == "part":
+        engine_options(grouping=grouping)
     xb = _engine()
     rng = np.random.default_rng(7)
     cases = [(4, 3), (5, 40), (6, 700), (8, 2000), (11, 600), (12, 5000), (13, 3000), (14, 9000), (15, 12000),
@@ -504,7 +489,7 @@ def test_concurrent_searches_on_different_datasets():
 
 
 @pytest.mark.parametrize("case", ["dense", "sparse_forced", "constant_y"])
-def test_msplit_grouping_vs_oracle(case, monkeypatch):
+def test_msplit_grouping_vs_oracle(case, engine_options):
     """17 <= M <= 20: one 2^(M-16)-CTA cluster per run (16 CTAs at M = 20).
     Dense tables by default, a sparse run forced onto it, and a constant
     response (c = all ones in the negative pass: partners in other CTAs,
@@ -512,10 +497,10 @@ def test_msplit_grouping_vs_oracle(case, monkeypatch):
     xb = _engine()
     rng = np.random.default_rng(17)
     if case == "dense":  # M = 19, 20 only when forced (the counting sort is faster there)
-        monkeypatch.setenv("XYZB_GROUPING", "msplit")
+        engine_options(grouping="msplit")
         cases = [(17, 40000), (18, 70000), (19, 140000), (20, 270000)]
     elif case == "sparse_forced":
-        monkeypatch.setenv("XYZB_GROUPING", "msplit")
+        engine_options(grouping="msplit")
         cases = [(18, 3000), (20, 9000)]
     else:
         cases = [(18, 70000), (17, 40000)]
@@ -533,7 +518,7 @@ def test_msplit_grouping_vs_oracle(case, monkeypatch):
 
 
 @pytest.mark.parametrize("case", ["dense", "forced_low_m", "constant_y", "guard", "biased"])
-def test_partition_grouping_vs_oracle(case, monkeypatch):
+def test_partition_grouping_vs_oracle(case, engine_options):
     """The partitioned path (default for M >= 19 with a dense bucket space):
     a partition pass on the top bits of T(v) (T linear, T(c) = e_0, so a key
     and its partner share a partition and are neighbouring local buckets),
@@ -547,12 +532,12 @@ def test_partition_grouping_vs_oracle(case, monkeypatch):
     if case == "dense":
         cases = [(19, 140000), (20, 270000), (21, 600000), (22, 1100000)]
     elif case == "forced_low_m":
-        monkeypatch.setenv("XYZB_GROUPING", "part")
+        engine_options(grouping="part")
         cases = [(4, 20), (7, 300), (12, 2000), (13, 5000), (14, 9000), (16, 20000), (18, 70000)]
     elif case == "constant_y":
         cases = [(19, 140000), (20, 270000)]
     elif case == "guard":
-        monkeypatch.setenv("XYZB_GROUPING", "part")
+        engine_options(grouping="part")
         cases = [(14, 6000), (19, 140000)]
         guard = 1
     else:
@@ -575,40 +560,8 @@ def test_partition_grouping_vs_oracle(case, monkeypatch):
             want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (m, p)
 
 
-@pytest.mark.parametrize("case", ["forced_small", "many_tiles", "large_x"])
-def test_tiled_verify_vs_oracle(case, monkeypatch):
-    """The L2-tiled verify (opt-in, XYZB_TILED=1): the pair lists
-    of all batches accumulate, are bucketed by (min, max) column tile in
-    snake order and verified in one launch; hits recompute their x-side key
-    from the run's draws. Small data (several batches, constant and random
-    responses), tiny tiles (hundreds of tiles), and an X of 104 MB.
-    Bit-exact against the restatement."""
-    xb = _engine()
-    rng = np.random.default_rng(31)
-    monkeypatch.setenv("XYZB_TILED", "1")
-    if case == "forced_small":
-        monkeypatch.setenv("XYZB_BATCH_ENTRIES", "20000")
-        cases = [(300, 3000, 9, 6, False, 0.58), (300, 3000, 9, 6, True, 0.58), (65, 7000, 11, 4, False, 0.62)]
-    elif case == "many_tiles":
-        monkeypatch.setenv("XYZB_TILE_L2", "262144")  # 128 KB of tile columns: tiles of a few dozen columns
-        cases = [(640, 6000, 10, 4, False, 0.56)]
-    else:  # 130000 columns of 6400 rows: X = 104 MB > 96 MB
-        cases = [(6400, 130000, 17, 2, False, 0.515)]
-    for t, (n, p, m, l, const_y, gamma) in enumerate(cases):
-        x = ck.ref_rademacher(n, p, 700 + t, 5)
-        y = np.ones(n, np.int8) if const_y else np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
-        cfg = xb.SearchConfig(m=m, l=l, gamma=gamma, seed=t, threads=1, top_k=25, estimate_complexity=False)
-        got = xb.Dataset(x).search(y, cfg)
-        want = ck.oracle_search(x, y, cfg)
-        ok, msg = ck.same_hits(got, want)
-        assert ok, (n, p, m, msg)
-        assert (got.aborted_repetitions, got.candidates_enumerated, got.verified_pairs, got.top_k) == (
-            want.aborted_repetitions, want.candidates_enumerated, want.verified_pairs, want.top_k), (n, p, m)
-        assert len(want.hits) > 0
-
-
 @pytest.mark.parametrize("case", ["sparse", "wide_keys", "constant_y", "guard", "skewed_overflow", "forced_sort"])
-def test_hashed_partition_grouping_vs_oracle(case, monkeypatch):
+def test_hashed_partition_grouping_vs_oracle(case, engine_options):
     """Sparse bucket spaces (2^M > 4p + 1024, M <= 31): the partition pass
     plus one CTA per (run, partition) with an open-addressing hash table in
     shared memory. Covers M up to 31, c = all ones, guard aborts, a skewed
@@ -628,7 +581,7 @@ def test_hashed_partition_grouping_vs_oracle(case, monkeypatch):
         cases = [(18, 20000)]
         guard = 1
     elif case == "forced_sort":
-        monkeypatch.setenv("XYZB_GROUPING", "sort")
+        engine_options(grouping="sort")
         cases = [(20, 50000)]
     else:
         cases = [(21, 100000)]
@@ -651,7 +604,7 @@ def test_hashed_partition_grouping_vs_oracle(case, monkeypatch):
 
 
 @pytest.mark.parametrize("n", [100, 2000, 3000])
-def test_sign_bit_verify_equals_fp32_verify(n, monkeypatch):
+def test_sign_bit_verify_equals_fp32_verify(n, engine_options):
     """The sign transform's bit-plane verify (column sign bits x quantised
     response planes, re-verification within the quantisation bound) reports
     exactly the hits and strengths of the fp32-column verify, with exact
@@ -671,9 +624,9 @@ def test_sign_bit_verify_equals_fp32_verify(n, monkeypatch):
         cfg = xb.SearchConfig(m=9, l=6, gamma=gamma, seed=4, threads=1, top_k=30, mode="continuous_xy",
                               transform="sign", estimate_complexity=False)
         got = xb.Dataset(x).search(y, cfg)
-        monkeypatch.setenv("XYZB_SIGN_VERIFY", "0")
+        engine_options(sign_verify_off=1)
         ref = xb.Dataset(x).search(y, cfg)
-        monkeypatch.delenv("XYZB_SIGN_VERIFY")
+        engine_options(sign_verify_off=0)
         assert report_hits(got) == report_hits(ref), (n, gamma)
         assert got.top_k == ref.top_k and got.verified_pairs == ref.verified_pairs
         want = ck.oracle_search(x, y, cfg)
@@ -683,17 +636,14 @@ def test_sign_bit_verify_equals_fp32_verify(n, monkeypatch):
     assert total > 0
 
 
-def test_hashed_grouping_batches_and_regrow_are_invisible(monkeypatch):
+def test_hashed_grouping_batches_and_regrow_are_invisible(engine_options):
     """The hashed partition join under multi-batch runs and forced item /
     pair / hit buffer regrowth gives the unbatched, unregrown result."""
     xb = _engine()
     x, y = ck.ref_planted(1000, 2000, 4, 16, 0.9, 1)
     cfg = xb.SearchConfig(m=14, l=10, gamma=0.55, seed=7, top_k=10)  # 2^14 > 4p + 1024: sparse
     base = xb.Dataset(x).search(y, cfg)
-    monkeypatch.setenv("XYZB_BATCH_ENTRIES", "6000")
-    monkeypatch.setenv("XYZB_HIT_CAP", "7")
-    monkeypatch.setenv("XYZB_ITEM_CAP", "5")
-    monkeypatch.setenv("XYZB_PAIR_CAP", "100")
+    engine_options(batch_entries=6000, hit_cap=7, item_cap=5, pair_cap=100)
     other = xb.Dataset(x).search(y, cfg)
     assert report_hits(other) == report_hits(base) and other.top_k == base.top_k
     assert (other.candidates_enumerated, other.verified_pairs) == (base.candidates_enumerated, base.verified_pairs)

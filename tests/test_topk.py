@@ -74,10 +74,10 @@ def test_topk_candidates_toy_cfg1():
     assert (min(top.j, top.k), max(top.j, top.k)) == (4, 16)
 
 
-def test_topk_candidates_guard_aborts_and_batches(monkeypatch):
+def test_topk_candidates_guard_aborts_and_batches(engine_options):
     """Aborted runs contribute nothing; many small batches exercise the
     running threshold and the prune between batches."""
-    monkeypatch.setenv("XYZB_BATCH_ENTRIES", "900")
+    engine_options(batch_entries=900)
     x = ck.ref_rademacher(300, 450, 5, 9)
     y = np.where(np.arange(300) % 3 == 0, 1, -1).astype(np.int8)
     cfg = _xb().SearchConfig(m=5, l=30, gamma=0.9, seed=3, max_candidates_per_rep=6300, threads=1)

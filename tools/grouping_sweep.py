@@ -4,13 +4,13 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1610_05108_b200 as xb  # noqa: E402
-from paper_1610_05108_b200 import synth  # noqa: E402
+from paper_1610_05108_b200 import _lib, synth  # noqa: E402
 
 x, y, _ = synth.gwas()
 ds = xb.Dataset(x)
 for m in [int(a) for a in (sys.argv[1:] or ["16", "17", "18", "19", "20"])]:
-    for g in ("auto", "msplit", "cluster", "bucket", "sort"):
-        os.environ["XYZB_GROUPING"] = g
+    for g in ("auto", "msplit", "part", "sort"):
+        _lib.set_test_option("grouping", _lib.GROUPING[g])
         cfg = xb.SearchConfig(m=m, l=100, gamma=0.6, seed=7, top_k=100, estimate_complexity=False)
         try:
             for _ in range(2):
