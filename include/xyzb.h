@@ -231,10 +231,20 @@ int xyzb_equal_pairs(const uint64_t* x_keys, const uint64_t* z_keys, uint64_t p,
                      char* err, size_t errlen);
 
 /* Strengths of explicit (j,k) pairs under a response, as the reference's
- * pass-+1 strength function of the dataset's mode computes them. */
+ * pass-+1 strength function of the dataset's mode computes them, bit for bit
+ * (same evaluation order, no fused multiply-add): interaction_strength /
+ * weighted_interaction_strength (transforms.cpp:33-76) and the continuous-XY
+ * strength (search.cpp:273-287, 477-493). The drop-in's sample_strengths
+ * (search.cpp:229-291) draws its pairs on the host and evaluates them here. */
 int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params,
                         const uint32_t* pairs_jk, uint64_t n_pairs, double* strengths,
                         char* err, size_t errlen);
+
+/* count_agreements(z_j, x_k) of two binary datasets on one device
+ * (packed_matrix.cpp:37-47): interaction_strength(x, z, j, k) * n for an
+ * arbitrary packed Z (sample_strengths' binary overload, search.cpp:229-242). */
+int xyzb_pair_agreements(xyzb_dataset* z, xyzb_dataset* x, const uint32_t* pairs_jk, uint64_t n_pairs,
+                         uint64_t* agree, char* err, size_t errlen);
 
 /* One scored pair of the exhaustive search (oracle::ScoredPair, oracle.hpp:15-19). */
 typedef struct {

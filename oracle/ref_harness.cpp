@@ -301,6 +301,38 @@ int ref_pair_strengths(const xyzb_problem* prob, const xyzb_response* resp, int3
     });
 }
 
+// xyz::sample_strengths, the overload of `mode` (search.cpp:229-291), on
+// make_stream(seed, stream) — binary: Z = build_z(X, y_sign) as the CLI's
+// auto-M sample builds it (xyz_main.cpp:142-149) — and optimal_m(gamma, ...)
+// over the sample (search.cpp:189-220). In the drop-in build these resolve to
+// the GPU shim's sample_strengths.
+int ref_sample_strengths(const xyzb_problem* prob, const xyzb_response* resp, int32_t mode, int32_t transform,
+                         uint64_t n_samples, uint64_t seed, uint64_t stream, double gamma, double* out,
+                         uint64_t* m_out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const size_t n = prob->n_rows, p = prob->n_cols;
+        std::mt19937_64 rng = xyz::make_stream(seed, stream);
+        xyz::StrengthSample s;
+        if (mode == XYZB_MODE_BINARY) {
+            const xyz::PackedMatrix x = packed_from_words(prob->x_words, n, p);
+            const xyz::PackedMatrix z = xyz::build_z(x, std::span<const std::int8_t>(resp->y_sign, n));
+            s = xyz::sample_strengths(x, z, n_samples, rng);
+        } else if (mode == XYZB_MODE_CONTINUOUS_Y) {
+            const xyz::PackedMatrix x = packed_from_words(prob->x_words, n, p);
+            s = xyz::sample_strengths(x, std::span<const double>(resp->y_real, n), n_samples, rng);
+        } else {
+            const xyz::RealMatrix x = real_from_colmajor(prob->x_real, n, p);
+            const xyz::RealVector y(resp->y_real, resp->y_real + n);
+            s = xyz::sample_strengths(x, y,
+                                      transform == XYZB_TRANSFORM_UNBIASED ? xyz::BinarizeTransform::unbiased
+                                                                           : xyz::BinarizeTransform::sign,
+                                      n_samples, rng);
+        }
+        std::copy(s.strengths.begin(), s.strengths.end(), out);
+        *m_out = xyz::optimal_m(gamma, s, n, p).m;
+    });
+}
+
 // ---- synthetic generators (synthetic.cpp:12-69), fixture generation only ----
 
 int ref_rademacher_matrix(uint64_t n, uint64_t p, uint64_t seed, uint64_t stream,

@@ -137,6 +137,8 @@ SIGNATURES = {
                                    C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
     "xyzb_pair_strengths": (C.c_int, [_P, C.POINTER(Response), C.POINTER(Params), C.POINTER(C.c_uint32),
                                       C.c_uint64, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
+    "xyzb_pair_agreements": (C.c_int, [_P, _P, C.POINTER(C.c_uint32), C.c_uint64, C.POINTER(C.c_uint64), C.c_char_p,
+                                       C.c_size_t]),
     "xyzb_brute_force": (C.c_int, [_P, C.POINTER(C.c_int8), C.c_int32, C.c_double, C.c_int32, C.c_uint64,
                                    C.c_uint64, C.c_int32, C.POINTER(C.POINTER(ScoredPair)), C.POINTER(C.c_uint64),
                                    C.POINTER(C.c_uint64), C.POINTER(C.POINTER(C.c_uint64)), C.c_char_p,

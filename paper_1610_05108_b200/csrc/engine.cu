@@ -1568,46 +1568,68 @@ double estimate_complexity(SearchCtx& c, Fn&& device_strengths) {
     return np + double(c.q->l) * (double(c.M) * pd + pd * std::log(pd) + double(c.n) * e1);
 }
 
-// Pass-+1 strengths of explicit pairs on the device (estimate + primitive).
-__global__ void pair_strengths_kernel(const u32* __restrict__ pairs, u64 cnt, int mode, int unbiased,
-                                      const u64* __restrict__ Xc, u32 Wp, const u64* __restrict__ yk,
-                                      const u64* __restrict__ spos, const double* __restrict__ wabs,
-                                      const float* __restrict__ Xc32, u64 n4, const double* __restrict__ y, u32 n,
-                                      double norm, double* __restrict__ out) {
-    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= cnt) return;
-    const u32 j = pairs[2 * warp], k = pairs[2 * warp + 1];
-    if (mode == XYZB_MODE_BINARY) {
-        u32 a = 0;
-        for (u32 w = lane; w < Wp; w += 32) a += __popcll(Xc[u64(j) * Wp + w] ^ Xc[u64(k) * Wp + w] ^ yk[w]);
-        a = warp_sum(a);
-        if (lane == 0) out[warp] = double(a) / double(n);
-    } else if (mode == XYZB_MODE_CONTINUOUS_Y) {
-        double acc = 0.0;
-        for (u32 w = lane; w < Wp; w += 32) {
-            u64 m = Xc[u64(j) * Wp + w] ^ Xc[u64(k) * Wp + w] ^ spos[w];
-            while (m) {
-                const int b = __ffsll(static_cast<long long>(m)) - 1;
-                acc += wabs[u64(w) * 64 + b];
-                m &= m - 1;
+// Pass-+1 strengths of explicit pairs on the device (the complexity
+// estimate, xyzb_pair_strengths, the drop-in's sample_strengths), one thread
+// per pair in the reference's own evaluation order so every strength is
+// bit-identical to the host's:
+//   binary:        agree / n (interaction_strength, transforms.cpp:33-40);
+//   continuous-Y:  sum of |y_i| over the set bits of x_j ^ x_k ^ s, words and
+//                  bits ascending, / ||y||_1 (transforms.cpp:42-76);
+//   continuous-XY: 0.5 + sum_i y_i t(x_ij) t(x_ik) / (2 ||y||_1), rows
+//                  ascending, each product rounded left to right with no
+//                  fused multiply-add (search.cpp:477-493 and :273-287, built
+//                  without -march, i.e. no FMA contraction on the host).
+template <class T>
+__global__ void pair_strengths_exact(const u32* __restrict__ pairs, u64 cnt, int mode, int unbiased,
+                                     const u64* __restrict__ Xc, u32 Wp, u32 W, const u64* __restrict__ yk,
+                                     const u64* __restrict__ spos, const double* __restrict__ wabs,
+                                     const T* __restrict__ Xr, u64 ld, const double* __restrict__ y, u32 n,
+                                     double norm, double* __restrict__ out) {
+    for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < cnt; t += u64(gridDim.x) * blockDim.x) {
+        const u32 j = pairs[2 * t], k = pairs[2 * t + 1];
+        if (mode == XYZB_MODE_BINARY) {
+            const u64 *a = Xc + u64(j) * Wp, *b = Xc + u64(k) * Wp;
+            u32 agree = 0;
+            for (u32 w = 0; w < W; ++w) agree += __popcll(a[w] ^ b[w] ^ yk[w]);
+            out[t] = double(agree) / double(n);
+        } else if (mode == XYZB_MODE_CONTINUOUS_Y) {
+            const u64 *a = Xc + u64(j) * Wp, *b = Xc + u64(k) * Wp;
+            double acc = 0.0;
+            for (u32 w = 0; w < W; ++w) {
+                u64 m = a[w] ^ b[w] ^ spos[w];
+                while (m) {
+                    const int bit = __ffsll(static_cast<long long>(m)) - 1;
+                    acc = __dadd_rn(acc, wabs[u64(w) * 64 + bit]);
+                    m &= m - 1;
+                }
             }
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) out[warp] = acc / norm;
-    } else {
-        double acc = 0.0;
-        for (u64 i = lane; i < n4; i += 32) {
-            const float a = Xc32[u64(j) * n4 + i], b = Xc32[u64(k) * n4 + i];
-            if (unbiased) {
-                acc = fma(y[i], double(a) * double(b), acc);
-            } else {
-                const double ta = a > 0.f ? 1.0 : (a < 0.f ? -1.0 : 0.0), tb = b > 0.f ? 1.0 : (b < 0.f ? -1.0 : 0.0);
-                acc = fma(y[i], ta * tb, acc);
+            out[t] = acc / norm;
+        } else {
+            const T *a = Xr + u64(j) * ld, *b = Xr + u64(k) * ld;
+            double acc = 0.0;
+            for (u32 i = 0; i < n; ++i) {
+                const double u = double(a[i]), v = double(b[i]);
+                if (unbiased) {
+                    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(y[i], u), v));
+                } else {
+                    const double tu = u > 0.0 ? 1.0 : (u < 0.0 ? -1.0 : 0.0);
+                    const double tv = v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0);
+                    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(y[i], tu), tv));
+                }
             }
+            out[t] = __dadd_rn(0.5, acc / (2.0 * norm));
         }
-        acc = warp_sum(acc);
-        if (lane == 0) out[warp] = 0.5 + acc / (2.0 * norm);
+    }
+}
+
+// agree(z_j, x_k) of two binary datasets (count_agreements, packed_matrix.cpp:37-47)
+__global__ void pair_agreements_kernel(const u32* __restrict__ pairs, u64 cnt, const u64* __restrict__ Z, u32 Wz,
+                                       const u64* __restrict__ X, u32 Wx, u32 W, u64 n, u64* __restrict__ out) {
+    for (u64 t = u64(blockIdx.x) * blockDim.x + threadIdx.x; t < cnt; t += u64(gridDim.x) * blockDim.x) {
+        const u64 *a = Z + u64(pairs[2 * t]) * Wz, *b = X + u64(pairs[2 * t + 1]) * Wx;
+        u64 dis = 0;
+        for (u32 w = 0; w < W; ++w) dis += __popcll(a[w] ^ b[w]);
+        out[t] = n - dis;
     }
 }
 
@@ -1620,18 +1642,27 @@ void device_pair_strengths(SearchCtx& c, const u32* pairs, u64 cnt, double* out)
     ds->pairs_dev.ensure(cnt * 8);
     ds->strengths_dev.ensure(cnt * 8);
     XYZB_CUDA(cudaMemcpyAsync(ds->pairs_dev.p, pairs, cnt * 8, cudaMemcpyHostToDevice, st));
-    pair_strengths_kernel<<<static_cast<u32>(ceil_div(cnt * 32, 256)), 256, 0, st>>>(
-        ds->pairs_dev.as<u32>(), cnt, c.mode, c.q->transform == XYZB_TRANSFORM_UNBIASED, ds->Xc.as<u64>(),
-        static_cast<u32>(ds->Wp), ds->yk_bits.as<u64>(), ds->spos.as<u64>(), ds->wabs.as<double>(),
-        ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(), static_cast<u32>(c.n), c.norm,
-        ds->strengths_dev.as<double>());
+    const u32 grid = grid_for(cnt, 128, kSMs * 32);
+    const int unb = c.q->transform == XYZB_TRANSFORM_UNBIASED;
+    if (ds->binary || ds->f32_src)
+        pair_strengths_exact<float><<<grid, 128, 0, st>>>(
+            ds->pairs_dev.as<u32>(), cnt, c.mode, unb, ds->Xc.as<u64>(), static_cast<u32>(ds->Wp),
+            static_cast<u32>(ds->W), ds->yk_bits.as<u64>(), ds->spos.as<u64>(), ds->wabs.as<double>(),
+            ds->Xc32.as<float>(), ds->n4, ds->yreal.as<double>(), static_cast<u32>(c.n), c.norm,
+            ds->strengths_dev.as<double>());
+    else  // the caller's fp64 values
+        pair_strengths_exact<double><<<grid, 128, 0, st>>>(
+            ds->pairs_dev.as<u32>(), cnt, c.mode, unb, ds->Xc.as<u64>(), static_cast<u32>(ds->Wp),
+            static_cast<u32>(ds->W), ds->yk_bits.as<u64>(), ds->spos.as<u64>(), ds->wabs.as<double>(),
+            ds->Xsrc64.as<double>(), ds->n, ds->yreal.as<double>(), static_cast<u32>(c.n), c.norm,
+            ds->strengths_dev.as<double>());
     XYZB_LAUNCH_CHECK();
     c.launches[XYZB_STAGE_ESTIMATE] += 1;
     XYZB_CUDA(cudaMemcpyAsync(out, ds->strengths_dev.p, cnt * 8, cudaMemcpyDeviceToHost, st));
     XYZB_CUDA(cudaStreamSynchronize(st));
 }
 
-void check_mode(const xyzb_dataset* ds, const xyzb_params* q, const xyzb_response* resp) {
+void check_mode(const xyzb_dataset* ds, const xyzb_params* q, const xyzb_response* resp, bool unit_check = true) {
     if (q->mode == XYZB_MODE_BINARY) {
         if (!ds->binary) throw data_error("xyz_search: real X requires continuous-XY mode");
         if (!resp || !resp->y_sign) throw data_error("xyz_search: packed X with sign Y requires binary mode");
@@ -1641,7 +1672,7 @@ void check_mode(const xyzb_dataset* ds, const xyzb_params* q, const xyzb_respons
     } else {
         if (ds->binary) throw data_error("xyz_search: packed X with real Y requires continuous-Y mode");
         if (!resp || !resp->y_real) throw data_error("xyz_search: real X requires continuous-XY mode");
-        if (q->transform == XYZB_TRANSFORM_UNBIASED && !ds->in_unit)
+        if (unit_check && q->transform == XYZB_TRANSFORM_UNBIASED && !ds->in_unit)
             throw data_error(
                 "xyz_search: unbiased transform needs entries in [-1,1]; apply rescale_rows or cap_entries first");
     }
@@ -2050,6 +2081,35 @@ extern "C" int xyzb_project_keys(xyzb_dataset* ds, const uint32_t* draws, uint64
     });
 }
 
+extern "C" int xyzb_pair_agreements(xyzb_dataset* z, xyzb_dataset* x, const uint32_t* pairs_jk, uint64_t n_pairs,
+                                    uint64_t* agree, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!z || !x || (n_pairs && (!pairs_jk || !agree))) throw data_error("xyzb_pair_agreements: null argument");
+        if (!z->binary || !x->binary) throw data_error("xyzb_pair_agreements: needs binary datasets");
+        if (z->n != x->n) throw data_error("interaction_strength: row count mismatch");
+        if (z->device != x->device) throw data_error("xyzb_pair_agreements: datasets on different devices");
+        for (u64 t = 0; t < n_pairs; ++t) {
+            if (pairs_jk[2 * t] >= z->p) throw data_error("interaction_strength: index j out of range");
+            if (pairs_jk[2 * t + 1] >= x->p) throw data_error("interaction_strength: index k out of range");
+        }
+        if (n_pairs == 0) return;
+        DeviceGuard dg(x->device);
+        StreamScope ss(x->stream);
+        const cudaStream_t st = x->stream;
+        XYZB_CUDA(cudaStreamSynchronize(z->stream));  // z's upload is complete
+        DevBuf pd, od;
+        pd.ensure(n_pairs * 8);
+        od.ensure(n_pairs * 8);
+        XYZB_CUDA(cudaMemcpyAsync(pd.p, pairs_jk, n_pairs * 8, cudaMemcpyHostToDevice, st));
+        pair_agreements_kernel<<<grid_for(n_pairs, 128, kSMs * 32), 128, 0, st>>>(
+            pd.as<u32>(), n_pairs, z->Xc.as<u64>(), static_cast<u32>(z->Wp), x->Xc.as<u64>(),
+            static_cast<u32>(x->Wp), static_cast<u32>(x->W), x->n, od.as<u64>());
+        XYZB_LAUNCH_CHECK();
+        XYZB_CUDA(cudaMemcpyAsync(agree, od.p, n_pairs * 8, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 extern "C" int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* params,
                                    const uint32_t* pairs_jk, uint64_t n_pairs, double* strengths, char* err,
                                    size_t errlen) {
@@ -2057,7 +2117,7 @@ extern "C" int xyzb_pair_strengths(xyzb_dataset* ds, const xyzb_response* resp, 
         if (!ds || !params) throw data_error("pair_strengths: null argument");
         DeviceGuard dg(ds->device);
         StreamScope ss(ds->stream);
-        check_mode(ds, params, resp);
+        check_mode(ds, params, resp, false);  // strengths only: the transform's [-1, 1] domain is the search's
         SearchCtx c;
         c.ds = ds;
         c.q = params;

@@ -122,6 +122,16 @@ class Dataset:
                                                 out.ctypes.data_as(C.POINTER(C.c_double)), err, _abi.ERRBUF), err)
         return out
 
+    def pair_agreements(self, z: "Dataset", pairs) -> np.ndarray:
+        """count_agreements(z_j, x_k) with this dataset as X (xyzb_pair_agreements)."""
+        pairs = np.ascontiguousarray(pairs, np.uint32).reshape(-1, 2)
+        out = np.zeros(len(pairs), np.uint64)
+        err = _abi.errbuf()
+        raise_for(self._lib.xyzb_pair_agreements(z.handle, self._h, pairs.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                 len(pairs), out.ctypes.data_as(C.POINTER(C.c_uint64)), err,
+                                                 _abi.ERRBUF), err)
+        return out
+
     def merge(self, parts: Sequence[_abi.Result], config: SearchConfig) -> SearchReport:
         arr = (_abi.Result * len(parts))(*parts)
         params = config.to_params()

@@ -105,7 +105,7 @@ struct DatasetCache {
     ~DatasetCache() {
         if (ds) xyzb_dataset_destroy(ds);
     }
-    xyzb_dataset* get(const uint64_t* words, const double* real, size_t n_, size_t p_) {
+    xyzb_dataset* get(const uint64_t* words, const double* real, size_t n_, size_t p_, bool single = false) {
         const void* ptr_ = words ? static_cast<const void*>(words) : static_cast<const void*>(real);
         const size_t bytes = words ? p_ * ((n_ + 63) / 64) * 8 : n_ * p_ * 8;
         const uint64_t f = fingerprint(ptr_, bytes);
@@ -117,7 +117,8 @@ struct DatasetCache {
         prob.n_cols = p_;
         prob.x_words = words;
         prob.x_real = real;
-        const std::vector<int32_t> devs = gpu_devices();  // X replicated on each; runs sharded over them
+        std::vector<int32_t> devs = gpu_devices();  // X replicated on each; runs sharded over them
+        if (single) devs.resize(1);
         prob.device = devs[0];
         prob.devices = devs.data();
         prob.n_devices = devs.size();
@@ -134,6 +135,13 @@ struct DatasetCache {
 };
 
 DatasetCache& cache() {
+    static DatasetCache c;
+    return c;
+}
+
+// The Z matrix of sample_strengths' binary overload (the CLI's auto-M sample,
+// xyz_main.cpp:142-149), resident beside X.
+DatasetCache& zcache() {
     static DatasetCache c;
     return c;
 }
@@ -210,40 +218,41 @@ SearchReport run_gpu(const uint64_t* words, const double* real, size_t n, size_t
     return rep;
 }
 
-// Uniform (j, k), j != k, k redrawn on collision (search.cpp:229-238). The
-// pairs are drawn first, in the reference's RNG order; their strengths are
-// independent, so large samples are evaluated on up to 16 host threads (the
-// same arithmetic per pair: results identical to a serial loop). The Lasso
-// draws 2000 pairs of a 1000-row matrix for each of its ~50 screens.
-template <class F>
-StrengthSample draw_pairs(size_t p, size_t count, std::mt19937_64& rng, F&& strength) {
+// Uniform (j, k), j != k, k redrawn on collision (search.cpp:229-238), in
+// the reference's RNG order. `check(j, k)` runs after each draw: the
+// reference evaluates each pair right after drawing it, so an argument error
+// leaves the caller's generator exactly where the reference leaves it.
+template <class Check>
+std::vector<uint32_t> draw_pairs(size_t p, size_t count, std::mt19937_64& rng, Check&& check) {
     if (count < 1) throw data_error("sample_strengths: need n_samples >= 1");
+    if (p > 0xffffffffull) throw data_error("sample_strengths: too many columns for the GPU engine");
     std::uniform_int_distribution<size_t> dist(0, p - 1);
-    std::vector<std::pair<size_t, size_t>> jk(count);
+    std::vector<uint32_t> jk(2 * count);
     for (size_t t = 0; t < count; ++t) {
         const size_t j = dist(rng);
         size_t k = dist(rng);
         while (p > 1 && k == j) k = dist(rng);
-        jk[t] = {j, k};
+        check(j, k);
+        jk[2 * t] = static_cast<uint32_t>(j);
+        jk[2 * t + 1] = static_cast<uint32_t>(k);
     }
+    return jk;
+}
+
+// The drawn pairs' strengths on the device, bit-identical to the host's
+// (xyzb_pair_strengths evaluates each pair in the reference's order).
+StrengthSample device_strengths(xyzb_dataset* ds, const xyzb_response& resp, int32_t mode, int32_t transform,
+                                const std::vector<uint32_t>& jk) {
+    xyzb_params q;
+    xyzb_params_init(&q);
+    q.mode = mode;
+    q.transform = transform;
     StrengthSample s;
-    s.strengths.resize(count);
-    auto work = [&](size_t a, size_t b) {
-        for (size_t t = a; t < b; ++t) s.strengths[t] = strength(jk[t].first, jk[t].second);
-    };
-    // the first pair on the calling thread: a strength function that rejects
-    // its inputs (shape checks) throws here, where the caller can catch it
-    work(0, 1);
-    const size_t rest = count - 1;
-    const size_t nthr = rest < 512 ? 1 : std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency()));
-    if (nthr <= 1) {
-        work(1, count);
-    } else {
-        std::vector<std::thread> pool;
-        for (size_t q = 1; q < nthr; ++q) pool.emplace_back(work, 1 + rest * q / nthr, 1 + rest * (q + 1) / nthr);
-        work(1, 1 + rest / nthr);
-        for (auto& th : pool) th.join();
-    }
+    s.strengths.resize(jk.size() / 2);
+    char err[1024] = {0};
+    const int code = xyzb_pair_strengths(ds, &resp, &q, jk.data(), s.strengths.size(), s.strengths.data(), err,
+                                         sizeof err);
+    if (code != XYZB_OK) rethrow(code, err);
     return s;
 }
 
@@ -342,16 +351,45 @@ double runtime_exponent(double gamma, double gamma0) {
     return 1.0 + std::log(gamma) / std::log(gamma0);
 }
 
+// sample_strengths (search.cpp:229-291): the pairs are drawn on the host in
+// the reference's RNG order, their strengths computed on the GPU (one thread
+// per pair, the reference's evaluation order: bit-identical samples, so
+// optimal_m / expected_complexity decide exactly as the reference does).
 StrengthSample sample_strengths(const PackedMatrix& x, const PackedMatrix& z, std::size_t n_samples,
                                 std::mt19937_64& rng) {
-    return draw_pairs(x.n_cols(), n_samples, rng,
-                      [&](size_t j, size_t k) { return interaction_strength(x, z, j, k); });
+    const auto jk = draw_pairs(x.n_cols(), n_samples, rng, [&](size_t j, size_t k) {
+        // interaction_strength's argument checks (transforms.cpp:33-38), at the first failing pair
+        if (j >= z.n_cols()) throw data_error("interaction_strength: index j out of range");
+        if (k >= x.n_cols()) throw data_error("interaction_strength: index k out of range");
+        if (x.n_rows() != z.n_rows()) throw data_error("interaction_strength: row count mismatch");
+    });
+    std::lock_guard<std::mutex> lock(cache().mu);
+    std::lock_guard<std::mutex> zlock(zcache().mu);
+    xyzb_dataset* xd = cache().get(x.column_words(0).data(), nullptr, x.n_rows(), x.n_cols());
+    xyzb_dataset* zd = zcache().get(z.column_words(0).data(), nullptr, z.n_rows(), z.n_cols(), true);
+    std::vector<uint64_t> agree(n_samples);
+    char err[1024] = {0};
+    const int code = xyzb_pair_agreements(zd, xd, jk.data(), n_samples, agree.data(), err, sizeof err);
+    if (code != XYZB_OK) rethrow(code, err);
+    StrengthSample s;
+    s.strengths.resize(n_samples);
+    for (size_t t = 0; t < n_samples; ++t)
+        s.strengths[t] = static_cast<double>(agree[t]) / static_cast<double>(x.n_rows());
+    return s;
 }
 
 StrengthSample sample_strengths(const PackedMatrix& x, std::span<const double> y, std::size_t n_samples,
                                 std::mt19937_64& rng) {
-    return draw_pairs(x.n_cols(), n_samples, rng,
-                      [&](size_t j, size_t k) { return weighted_interaction_strength(x, y, j, k); });
+    const auto jk = draw_pairs(x.n_cols(), n_samples, rng, [&](size_t, size_t) {
+        // weighted_interaction_strength's checks (transforms.cpp:44-53), thrown at the first pair
+        if (y.size() != x.n_rows()) throw data_error("weighted_interaction_strength: response length mismatch");
+        if (abs_sum(y) <= 0.0) throw data_error("weighted_interaction_strength: zero response vector");
+    });
+    std::lock_guard<std::mutex> lock(cache().mu);
+    xyzb_dataset* ds = cache().get(x.column_words(0).data(), nullptr, x.n_rows(), x.n_cols());
+    xyzb_response resp{};
+    resp.y_real = y.data();
+    return device_strengths(ds, resp, XYZB_MODE_CONTINUOUS_Y, XYZB_TRANSFORM_NONE, jk);
 }
 
 StrengthSample sample_strengths(const RealMatrix& x, const RealVector& y, BinarizeTransform transform,
@@ -359,17 +397,16 @@ StrengthSample sample_strengths(const RealMatrix& x, const RealVector& y, Binari
     if (n_samples < 1) throw data_error("sample_strengths: need n_samples >= 1");
     if (transform == BinarizeTransform::none)
         throw data_error("sample_strengths: continuous data needs a binarize transform");
-    const size_t n = x.n_rows();
-    const double norm = abs_sum(y);
-    if (norm <= 0.0) throw data_error("sample_strengths: zero response vector");
-    const bool unbiased = transform == BinarizeTransform::unbiased;
-    auto sgn = [](double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); };
-    return draw_pairs(x.n_cols(), n_samples, rng, [&](size_t j, size_t k) {
-        const auto a = x.column(j), b = x.column(k);
-        double acc = 0.0;
-        for (size_t i = 0; i < n; ++i) acc += unbiased ? y[i] * a[i] * b[i] : y[i] * sgn(a[i]) * sgn(b[i]);
-        return 0.5 + acc / (2.0 * norm);
-    });
+    if (abs_sum(y) <= 0.0) throw data_error("sample_strengths: zero response vector");
+    if (y.size() < x.n_rows()) throw data_error("sample_strengths: response shorter than the matrix");
+    const auto jk = draw_pairs(x.n_cols(), n_samples, rng, [](size_t, size_t) {});
+    std::lock_guard<std::mutex> lock(cache().mu);
+    xyzb_dataset* ds = cache().get(nullptr, x.values().data(), x.n_rows(), x.n_cols());
+    xyzb_response resp{};
+    resp.y_real = y.data();
+    return device_strengths(ds, resp, XYZB_MODE_CONTINUOUS_XY,
+                            transform == BinarizeTransform::unbiased ? XYZB_TRANSFORM_UNBIASED : XYZB_TRANSFORM_SIGN,
+                            jk);
 }
 
 // ---- the three entry points (search.cpp:325-506) on the GPU ----

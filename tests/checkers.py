@@ -65,6 +65,9 @@ _REF_SIGS = {
     "ref_write_dataset": (C.c_int, [C.c_char_p, C.c_int32, _U64P, _F64P, C.c_uint64, C.c_uint64, C.c_char_p,
                                     C.c_size_t]),
     "ref_read_dataset": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _U64P, _U64P, C.c_char_p, C.c_size_t]),
+    "ref_sample_strengths": (C.c_int, [C.POINTER(_abi.Problem), C.POINTER(_abi.Response), C.c_int32, C.c_int32,
+                                       C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, _F64P, _U64P, C.c_char_p,
+                                       C.c_size_t]),
     "ref_brute_force": (C.c_int, [_U64P, C.c_uint64, C.c_uint64, C.POINTER(C.c_int8), C.c_int32, C.c_double,
                                   C.c_int32, C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(_U32P), C.POINTER(_F64P),
                                   _U64P, _U64P, C.POINTER(_U64P), C.c_char_p, C.c_size_t]),
@@ -456,3 +459,19 @@ def ref_topk_candidates(x, y, cfg, k, gamma_start=0.6, step=0.01, threads=None):
 
 def hit_tuples(hits):
     return [(h.j, h.k, h.strength, h.found_at_repetition, h.sign) for h in hits]
+
+
+def sample_strengths(lib, x, y, mode, transform, n_samples, seed=7, stream=0xdead, gamma=0.6):
+    """xyz::sample_strengths + optimal_m through a harness library (the
+    reference core, or the drop-in where they run on the GPU):
+    (strengths, optimal M)."""
+    if isinstance(x, RealMatrix):
+        x = x.as_float64()
+    prob = make_problem(x)
+    resp, keep = make_response(y)
+    out = np.zeros(n_samples, np.float64)
+    m = C.c_uint64()
+    err = _abi.errbuf()
+    _check(lib.ref_sample_strengths(C.byref(prob), C.byref(resp), mode, transform, n_samples, seed, stream, gamma,
+                                    out.ctypes.data_as(_F64P), C.byref(m), err, _abi.ERRBUF), err)
+    return out, m.value

@@ -203,3 +203,49 @@ def test_dropin_search_over_two_device_replicas(monkeypatch):
     assert ok, msg
     assert (got.repetitions_run, got.candidates_enumerated, got.estimated_c) == \
         (want.repetitions_run, want.candidates_enumerated, want.estimated_c)
+
+
+@pytest.mark.parametrize("mode", ["binary", "continuous_y", "sign", "unbiased"])
+def test_dropin_sample_strengths_bit_exact_on_the_gpu(mode):
+    """sample_strengths (search.cpp:229-291) in the drop-in draws its pairs on
+    the host in the reference's RNG order and evaluates them on the GPU in the
+    reference's order: every strength bit-identical, so optimal_m (the CLI's
+    auto-M, xyz_main.cpp:142-167; the Lasso screen's M, lasso.cpp:184-192)
+    picks the reference's M. Binary: Z = build_z(X, y) as the CLI builds it;
+    unbiased: the Lasso's rescaled design (entries in [-1, 1])."""
+    from paper_1610_05108_b200 import _abi
+    rng = np.random.default_rng(3)
+    n, p = 1000, 4000
+    if mode in ("binary", "continuous_y"):
+        x = ck.ref_rademacher(n, p, 21, 4)
+        y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8) if mode == "binary" else rng.standard_normal(n)
+        if mode == "continuous_y":
+            y[::17] = 0.0
+        m, t = (_abi.MODE_BINARY if mode == "binary" else _abi.MODE_CONTINUOUS_Y), _abi.TRANSFORM_NONE
+    else:
+        g = ck.ref_gaussian(n, p, 5, 6)
+        y = rng.standard_normal(n)
+        if mode == "unbiased":
+            x, y = ck.ref_rescale_rows(g, y)
+        else:
+            xv = g.values.copy()
+            xv[rng.random(xv.shape) < 0.02] = 0.0
+            from paper_1610_05108_b200 import RealMatrix
+            x = RealMatrix(xv)
+        m, t = _abi.MODE_CONTINUOUS_XY, (_abi.TRANSFORM_UNBIASED if mode == "unbiased" else _abi.TRANSFORM_SIGN)
+    for count, gamma in ((2000, 0.506), (40000, 0.6)):
+        want, want_m = ck.sample_strengths(ck.ref_lib(), x, y, m, t, count, gamma=gamma)
+        got, got_m = ck.sample_strengths(ck.dropin_lib(), x, y, m, t, count, gamma=gamma)
+        assert np.array_equal(got, want), (mode, count, np.max(np.abs(got - want)))
+        assert got_m == want_m
+
+
+def test_dropin_sample_strengths_errors_like_the_reference():
+    from paper_1610_05108_b200 import _abi
+    x = ck.ref_rademacher(100, 50, 1, 1)
+    zero = np.zeros(100)
+    for lib in (ck.ref_lib(), ck.dropin_lib()):
+        with pytest.raises(ck.CheckerError, match="zero response vector"):
+            ck.sample_strengths(lib, x, zero, _abi.MODE_CONTINUOUS_Y, _abi.TRANSFORM_NONE, 10)
+        with pytest.raises(ck.CheckerError, match="need n_samples >= 1"):
+            ck.sample_strengths(lib, x, np.ones(100), _abi.MODE_CONTINUOUS_Y, _abi.TRANSFORM_NONE, 0)

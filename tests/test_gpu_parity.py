@@ -70,8 +70,8 @@ def test_search_matches_reference_fixture(name, grouping, engine_options):
         assert rep.estimated_c == float(z["estimated_c"])
     else:
         compare_continuous(report_hits(rep), expected_hits(z), cfg.gamma)
-        if cfg.estimate_complexity:
-            assert abs(rep.estimated_c - float(z["estimated_c"])) <= 1e-6 * abs(float(z["estimated_c"]))
+        if cfg.estimate_complexity:  # the strength sample is bit-exact in every mode (reference order, no FMA)
+            assert rep.estimated_c == float(z["estimated_c"])
     # engine counter = the restatement's canonical count; >= the reference's deduplicated count
     orc = ck.oracle_search(x, y, cfg)
     assert rep.verified_pairs == orc.verified_pairs
@@ -149,6 +149,40 @@ def test_pair_strengths_vs_oracle(mode):
             want = ck.oracle_pair_strengths(x, y, 1, 0, pairs)
             got = xb.Dataset(x).pair_strengths(y, cfg, pairs)
             np.testing.assert_allclose(got, want, rtol=1e-12)
+
+
+@pytest.mark.parametrize("mode", ["binary", "continuous_y", "sign", "unbiased", "sign_f32", "unbiased_f32"])
+def test_pair_strengths_bit_exact_vs_reference(mode):
+    """xyzb_pair_strengths evaluates each pair in the reference's own order
+    with no fused multiply-add: bit-identical to interaction_strength /
+    weighted_interaction_strength / the continuous-XY strength on the host
+    (fp64 datasets from x_real, and x_real32 datasets, whose values the
+    reference gets as doubles)."""
+    xb = _engine()
+    rng = np.random.default_rng(12)
+    n, p = 777, 300
+    pairs = rng.integers(0, p, (5000, 2)).astype(np.uint32)
+    if mode in ("binary", "continuous_y"):
+        x = ck.ref_rademacher(n, p, 7, 7)
+        y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8) if mode == "binary" else rng.normal(size=n)
+        m, t = (0, 0) if mode == "binary" else (1, 0)
+        cfg = xb.SearchConfig(mode="binary" if mode == "binary" else "continuous_y")
+        ds = xb.Dataset(x)
+    else:
+        tr = mode.split("_")[0]
+        xv = rng.uniform(-1, 1, (p, n))
+        xv[rng.random(xv.shape) < 0.05] = 0.0
+        if mode.endswith("f32"):
+            x = xb.RealMatrix(xv.astype(np.float32), dtype=np.float32)
+        else:
+            x = xb.RealMatrix(xv)
+        y = rng.normal(size=n)
+        m, t = 2, (1 if tr == "sign" else 2)
+        cfg = xb.SearchConfig(mode="continuous_xy", transform=tr)
+        ds = xb.Dataset(x)
+    got = ds.pair_strengths(y, cfg, pairs)
+    want = ck.ref_pair_strengths(x, y, m, t, pairs if m else pairs[:, ::-1].copy())
+    assert np.array_equal(got, want), np.max(np.abs(got - want))
 
 
 def test_binary_random_sweep_vs_oracle():
