@@ -52,6 +52,21 @@ using namespace xyzb;
 
 namespace {
 
+// ------------------------------------------------------------ test options --
+// Process-wide options the unit tests set through xyzb_test_set_option
+// (include/xyzb_testing.h) to force rare paths — buffer regrowth, multi-batch
+// runs, a grouping path outside its default range, the multi-kernel merge,
+// the fp32 verify beside the sign-bit one. 0 = the engine's own choice.
+struct TestOptions {
+    std::atomic<long long> batch_entries{0}, hit_cap{0}, item_cap{0}, pair_cap{0}, grouping{0}, merge_large{0},
+        sign_verify_off{0}, trace{0}, brute_cuda{0};
+};
+TestOptions& topt() {
+    static TestOptions* o = new TestOptions();  // leaked on purpose (outlives static destructors)
+    return *o;
+}
+enum { kGroupAuto = 0, kGroupSort = 1, kGroupPart = 2, kGroupMsplit = 3 };
+
 // ------------------------------------------------------------ buffers --
 
 // Caching allocator: device blocks (per device) and pinned host blocks are
@@ -71,7 +86,9 @@ struct BlockPool {
         b = granule(b);
         {
             std::lock_guard<std::mutex> lk(mu);
-            for (auto it = free_.lower_bound(b); it != free_.end() && it->first <= 2 * b + (8u << 20); ++it) {
+            // a cached block at most 1/8 (+ 1 MiB) larger: a 50 MB request must not take the 80 MB block
+            // another buffer of the next search needs (a pool miss costs a synchronising cudaMalloc)
+            for (auto it = free_.lower_bound(b); it != free_.end() && it->first <= b + b / 8 + (1u << 20); ++it) {
                 if (it->second.first == dev) {
                     void* p = it->second.second;
                     b = it->first;
@@ -81,6 +98,7 @@ struct BlockPool {
             }
         }
         void* p = nullptr;
+        if (topt().trace.load()) std::fprintf(stderr, "[xyzb] pool miss: %s %zu bytes\n", dev >= 0 ? "cudaMalloc" : "cudaMallocHost", b);
         cudaError_t err = dev >= 0 ? cudaMalloc(&p, b) : cudaMallocHost(&p, b);
         if (err != cudaSuccess) {
             cudaGetLastError();
@@ -143,8 +161,12 @@ struct DevBuf {
                 int cur = 0;
                 cudaGetDevice(&cur);
                 cudaSetDevice(dev);
-                if (st) cudaStreamSynchronize(st);
-                else cudaDeviceSynchronize();
+                if (st) {
+                    cudaStreamSynchronize(st);
+                } else {
+                    if (topt().trace.load()) std::fprintf(stderr, "[xyzb] device-wide sync on release (%zu bytes)\n", bytes);
+                    cudaDeviceSynchronize();
+                }
                 cudaSetDevice(cur);
             }
             pool().give(p, bytes, dev);
@@ -190,20 +212,6 @@ struct HostBuf {  // pinned
 
 u64 round_up(u64 a, u64 m) { return (a + m - 1) / m * m; }
 
-// ------------------------------------------------------------ test options --
-// Process-wide options the unit tests set through xyzb_test_set_option
-// (include/xyzb_testing.h) to force rare paths — buffer regrowth, multi-batch
-// runs, a grouping path outside its default range, the multi-kernel merge,
-// the fp32 verify beside the sign-bit one. 0 = the engine's own choice.
-struct TestOptions {
-    std::atomic<long long> batch_entries{0}, hit_cap{0}, item_cap{0}, pair_cap{0}, grouping{0}, merge_large{0},
-        sign_verify_off{0}, trace{0}, brute_cuda{0};
-};
-TestOptions& topt() {
-    static TestOptions* o = new TestOptions();  // leaked on purpose (outlives static destructors)
-    return *o;
-}
-enum { kGroupAuto = 0, kGroupSort = 1, kGroupPart = 2, kGroupMsplit = 3 };
 
 // event-timed stage accounting on the dataset stream
 struct StageClock {
@@ -867,11 +875,25 @@ void plan_runs(SearchCtx& c, const uint32_t* draws) {
     }
 }
 
+// The sign transform's verify functor (bit planes + the exact fp32 fallback);
+// converts the response to fp32 on the dataset stream first.
+kern::SignStrength sign_strength(SearchCtx& c) {
+    xyzb_dataset* ds = c.ds;
+    ds->yreal32.ensure(ds->n4 * 4);
+    real::to_f32<<<grid_for(ds->n4, 256, 256), 256, 0, ds->stream>>>(ds->yreal.as<double>(), ds->n4,
+                                                                     ds->yreal32.as<float>());
+    XYZB_LAUNCH_CHECK();
+    kern::RealStrength<false> f{ds->Xc32.as<float>(), ds->n4, ds->yreal32.as<float>(), c.norm, c.gamma};
+    return kern::SignStrength{ds->Spos.as<u64>(), ds->Snz.as<u64>(), ds->W, ds->yplanes.as<u64>(), c.qsum,
+                              ds->has_zero, c.qinv, c.norm, c.gamma, c.qdelta, f};
+}
+
 // Top-K over all candidates, after a batch's verify (topk_kernels.cuh): the
 // pair-list path picks an emission threshold from the batch's rank histogram
 // and appends the pairs at or above it; then the hit buffer is pruned to the
 // occurrences at or above the K-th distinct key's rank bin.
-void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, const u32* np, u64* launches) {
+void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, const u32* np, u64* launches,
+                      const kern::SignStrength* sg = nullptr) {
     xyzb_dataset* ds = c.ds;
     cudaStream_t st = ds->stream;
     auto* S = ds->tk_state.as<topk::State>();
@@ -885,10 +907,14 @@ void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, c
         XYZB_LAUNCH_CHECK();
         topk::emit_select<<<1, 1024, 0, st>>>(ds->tk_hist.as<u32>(), c.tk_shift, target, S, c.tk_level >= 2);
         XYZB_LAUNCH_CHECK();
-        topk::emit_pairs<<<kSMs * 8, 256, 0, st>>>(ds->pairs.as<kern::PairRec>(), ds->tk_sint.as<u32>(), np,
-                                                   static_cast<u32>(c.pair_cap), A.nitems, A.item_cap, S, A.xkeys,
-                                                   A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap,
-                                                   static_cast<u32>(c.n));
+        if (sg)  // sign transform: exact re-verification of the pairs that may reach E
+            topk::emit_pairs_sign<<<kSMs * 8, 256, 0, st>>>(A, ds->pairs.as<kern::PairRec>(), np,
+                                                            static_cast<u32>(c.pair_cap), *sg, S);
+        else
+            topk::emit_pairs<<<kSMs * 8, 256, 0, st>>>(ds->pairs.as<kern::PairRec>(), ds->tk_sint.as<u32>(), np,
+                                                       static_cast<u32>(c.pair_cap), A.nitems, A.item_cap, S,
+                                                       A.xkeys, A.key64, A.S, A.rid, A.hits, A.hit_count, A.hit_cap,
+                                                       static_cast<u32>(c.n));
         XYZB_LAUNCH_CHECK();
         *launches += 3;
     } else {
@@ -1015,7 +1041,10 @@ void run_batches(SearchCtx& c) {
     XYZB_CUDA(cudaMemsetAsync(ds->nblocks.p, 0, nbatches * 4, st));
     c.item_cap = item_cap;
     c.nbatches = nbatches;
-    const bool pair_path = c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128;
+    // the sign transform's bit-plane verify over the pair list: columns of <= 2048 rows (lane w holds
+    // word w of the sign bits and of the response planes)
+    const bool sign_pairs = xy && !unbiased && ds->Spos.p && ds->W <= 32 && !topt().sign_verify_off.load();
+    const bool pair_path = (c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128) || sign_pairs;
     if (pair_path) {
         c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, B * p) * c.pair_scale);
         if (const long long e = topt().pair_cap.load())  // tests force the pair-list regrow path
@@ -1285,6 +1314,24 @@ void run_batches(SearchCtx& c) {
                                                       static_cast<u32>(c.pair_cap), sv);
             XYZB_LAUNCH_CHECK();
             c.launches[XYZB_STAGE_JOIN] += 1;
+            cudaEvent_t ev0 = clk.mark();
+            clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
+            if (sign_pairs) {
+                const kern::SignStrength g = sign_strength(c);
+                kern::verify_pairs_sign<kern::kSignQB><<<vgrid, 256, 0, st>>>(A, ds->pairs.as<kern::PairRec>(), np,
+                                                                              static_cast<u32>(c.pair_cap), g);
+                XYZB_LAUNCH_CHECK();
+                c.sign_verify = true;
+                c.launches[XYZB_STAGE_VERIFY] += 1;
+                cudaEvent_t ev1 = clk.mark();
+                clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
+                c.verify_spans.push_back({ev0, ev1});
+                if (c.topk_all) {
+                    topk_after_batch(c, true, A, np, &c.launches[XYZB_STAGE_MERGE], &g);
+                    clk.span(XYZB_STAGE_MERGE, ev1, clk.mark());
+                }
+                continue;
+            }
             const u64 W2 = ds->Wp / 2;
             // team of G lanes, NIT 16-byte chunks of each column per lane, measured on B200
             // (tools/sweep_verify.py, tools/l2_window2.cu): long columns (>= 512 B) take 8..32-lane
@@ -1301,8 +1348,6 @@ void run_batches(SearchCtx& c) {
             const u32 Wp = static_cast<u32>(ds->Wp);
             const u64* Y = ds->yk_bits.as<u64>();
             const u32 n32 = static_cast<u32>(c.n);
-            cudaEvent_t ev0 = clk.mark();
-            clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
 #define XYZB_VP(GG, NN)                                                                                          \
     do {                                                                                                         \
         if (simple)                                                                                              \

@@ -1383,5 +1383,106 @@ __global__ void __launch_bounds__(256, 4) verify_items_sign(VerifyArgs A, SignSt
     }
 }
 
+// Pair-list hit of a real-valued strength (the sign transform's pair walk).
+__device__ __noinline__ void append_pair_hit_real(const VerifyArgs& A, PairRec pr, double s) {
+    u32 j = pr.pa, k = pr.pb;
+    if ((pr.pad & 2u) && j > k) {
+        const u32 t = j;
+        j = k;
+        k = t;
+    }
+    const u64 i = u64(pr.run) * A.S + j;
+    DevHit h;
+    h.order = A.key64 ? static_cast<const u64*>(A.xkeys)[i] : u64(static_cast<const u32*>(A.xkeys)[i]);
+    h.s = s;
+    h.j = j;
+    h.k = k;
+    h.rid = A.rid[pr.run];
+    h.sint = -1;
+    const u32 slot = atomicAdd(A.hit_count, 1u);
+    if (slot < A.hit_cap) A.hits[slot] = h;
+}
+
+// Sign-transform verify over the pair list (columns of <= 2048 rows: lane w
+// holds word w of the column sign bits and of every response plane). A warp
+// takes 32 consecutive pair records with one coalesced load, then walks them
+// with the next pair's sign words already in flight while the current pair
+// is reduced (SignStrength: quantised strength, exact fp32 re-verification
+// within the quantisation bound of the threshold). Top-K over all candidates,
+// first phase (running threshold still 0): every pair's rank lower bound
+// rank(s_q - delta) goes to sint_out instead (topk::emit_pairs_sign emits).
+template <int QB>
+__global__ void __launch_bounds__(256, 4) verify_pairs_sign(VerifyArgs A, const PairRec* __restrict__ pairs,
+                                                             const u32* __restrict__ npairs, u32 pair_cap,
+                                                             SignStrength f) {
+    const int lane = threadIdx.x & 31;
+    const bool act = u64(lane) < f.Wn;
+    u64 pl[QB + 1];
+#pragma unroll
+    for (int b = 0; b <= QB; ++b) pl[b] = act ? f.planes[u64(b) * f.Wn + lane] : 0ull;
+    const u32 P = *A.nitems > A.item_cap ? 0u : min(*npairs, pair_cap);
+    const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
+    const bool ranks = A.sint_out && rthr == 0;
+    const double gate = A.rank_thr ? double(rthr) / double(1u << kRealRankBits) : f.gamma;
+    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    const u64* Sp = f.Spos;
+    const u64* Sz = f.Snz;
+    const u64 Wn = f.Wn;
+    for (u64 c0 = warp * 32; c0 < P; c0 += nwarps * 32) {
+        const u32 cnt = u32(minu(32, P - c0));
+        const PairRec mine = u32(lane) < cnt ? pairs[c0 + lane] : PairRec{0, 0, 0, 0};
+        u32 j = __shfl_sync(0xffffffffu, mine.pa, 0), k = __shfl_sync(0xffffffffu, mine.pb, 0);
+        u64 pj = act ? __ldg(Sp + u64(j) * Wn + lane) : 0ull, pk = act ? __ldg(Sp + u64(k) * Wn + lane) : 0ull;
+        u64 zj = ~0ull, zk = ~0ull;
+        if (f.zeros && act) {
+            zj = __ldg(Sz + u64(j) * Wn + lane);
+            zk = __ldg(Sz + u64(k) * Wn + lane);
+        }
+        for (u32 t = 0; t < cnt; ++t) {
+            u32 j1 = 0, k1 = 0;
+            u64 pj1 = 0, pk1 = 0, zj1 = ~0ull, zk1 = ~0ull;
+            if (t + 1 < cnt) {  // the next pair's words in flight while this one is reduced
+                j1 = __shfl_sync(0xffffffffu, mine.pa, t + 1);
+                k1 = __shfl_sync(0xffffffffu, mine.pb, t + 1);
+                if (act) {
+                    pj1 = __ldg(Sp + u64(j1) * Wn + lane);
+                    pk1 = __ldg(Sp + u64(k1) * Wn + lane);
+                    if (f.zeros) {
+                        zj1 = __ldg(Sz + u64(j1) * Wn + lane);
+                        zk1 = __ldg(Sz + u64(k1) * Wn + lane);
+                    }
+                }
+            }
+            int a = 0;
+            if (act) {
+                const u64 both = f.zeros ? (zj & zk) : ~0ull;
+                a = 2 * plane_sum_reg<QB>(pl, both & ~(pj ^ pk));
+                if (f.zeros) a -= plane_sum_reg<QB>(pl, both);
+            }
+            a = warp_sum(a);
+            long long acc = a;
+            if (!f.zeros) acc -= f.qsum;
+            const u32 run = __shfl_sync(0xffffffffu, mine.run, t);
+            const bool pos_pass = A.run_sign[run] > 0;
+            double s = 0.5 + (pos_pass ? 1.0 : -1.0) * (double(acc) * f.inv_scale) / (2.0 * f.norm);
+            if (ranks) {
+                if (u32(lane) == t) A.sint_out[c0 + t] = strength_rank(fmax(0.0, s - f.delta), 0u, 0);
+            } else if (s >= gate - f.delta) {  // warp-uniform: exact fp32 re-verification
+                s = f.exact(j, k, pos_pass, lane, 0xffffffffu);
+                const PairRec r{j, k, run, __shfl_sync(0xffffffffu, mine.pad, t)};
+                if (lane == 0 && (A.rank_thr ? strength_rank(s, 0u, 0) >= rthr : f.exact.hit(s)))
+                    append_pair_hit_real(A, r, s);
+            }
+            j = j1;
+            k = k1;
+            pj = pj1;
+            pk = pk1;
+            zj = zj1;
+            zk = zk1;
+        }
+    }
+}
+
 } // namespace kern
 } // namespace xyzb

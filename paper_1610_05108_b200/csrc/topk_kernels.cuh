@@ -189,6 +189,34 @@ __global__ void __launch_bounds__(256) emit_pairs(const PairRec* __restrict__ pa
     }
 }
 
+// Sign-transform pair list: the pairs whose exact strength may reach E
+// (rank lower bound at or above rank(E - 2 delta)) are re-verified exactly,
+// one warp per pair, and appended at or above E.
+__global__ void __launch_bounds__(256) emit_pairs_sign(kern::VerifyArgs A, const PairRec* __restrict__ pairs,
+                                                       const u32* __restrict__ npairs, u32 pair_cap,
+                                                       kern::SignStrength f, const State* __restrict__ st) {
+    if (st->thr > 0) return;  // appended by the verify
+    const u32 P = batch_pairs(npairs, pair_cap, A.nitems, A.item_cap);
+    const u32 E = st->emit;
+    const double lo_s = double(E) / double(1u << kern::kRealRankBits) - 2.0 * f.delta;
+    const u32 lo = kern::strength_rank(lo_s > 0.0 ? lo_s : 0.0, 0u, 0);
+    const int lane = threadIdx.x & 31;
+    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 c0 = warp * 32; c0 < P; c0 += nwarps * 32) {
+        const u64 i = c0 + lane;
+        u32 bal = __ballot_sync(0xffffffffu, i < P && A.sint_out[i] >= lo);
+        while (bal) {
+            const int t = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const PairRec r = pairs[c0 + t];
+            const bool pos_pass = A.run_sign[r.run] > 0;
+            const double s = f.exact(r.pa, r.pb, pos_pass, lane, 0xffffffffu);
+            if (lane == 0 && kern::strength_rank(s, 0u, 0) >= E) kern::append_pair_hit_real(A, r, s);
+        }
+    }
+}
+
 // ---- prune: distinct keys by rank, raise thr, keep occurrences >= thr ----
 
 __global__ void prune_insert(const DevHit* __restrict__ hits, const u32* __restrict__ hit_count, u32 hit_cap,
