@@ -267,6 +267,15 @@ int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t has_gamma, 
                      uint64_t top_k, uint64_t histogram_bins, int32_t force, xyzb_scored_pair** pairs,
                      uint64_t* n_pairs, uint64_t* pairs_scanned, uint64_t** histogram, char* err, size_t errlen);
 
+/* oracle::brute_force_search(PackedMatrix, span<const double>, BruteForceOptions)
+ * (oracle.hpp:40-41, oracle.cpp:93-100): the weighted strength of every pair
+ * j < k, bit-identical to scalar_weighted_strength (rows in order, fp64). Same
+ * options, outputs and errors as xyzb_brute_force; y: n_rows doubles. */
+int xyzb_brute_force_weighted(xyzb_dataset* ds, const double* y, int32_t has_gamma, double gamma, int32_t has_top_k,
+                              uint64_t top_k, uint64_t histogram_bins, int32_t force, xyzb_scored_pair** pairs,
+                              uint64_t* n_pairs, uint64_t* pairs_scanned, uint64_t** histogram, char* err,
+                              size_t errlen);
+
 /* ---- xyz-regression helpers (the loop around the screen) ----
  * A device-resident design for lasso_path (lasso.hpp:136-141): X (n x p,
  * column-major fp64, the caller's RealMatrix values) and the column means of

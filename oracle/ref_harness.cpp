@@ -431,6 +431,36 @@ int ref_brute_force(const uint64_t* x_words, uint64_t n, uint64_t p, const int8_
     });
 }
 
+// oracle::brute_force_search, continuous-response overload (oracle.cpp:93-100).
+int ref_brute_force_weighted(const uint64_t* x_words, uint64_t n, uint64_t p, const double* y, int32_t has_gamma,
+                             double gamma, int32_t has_top_k, uint64_t top_k, uint64_t bins, int32_t force,
+                             uint32_t** out_jk, double** out_s, uint64_t* n_out, uint64_t* scanned,
+                             uint64_t** out_hist, char* err, size_t errlen) {
+    *out_jk = nullptr;
+    *out_s = nullptr;
+    *out_hist = nullptr;
+    return guarded(err, errlen, [&] {
+        const xyz::PackedMatrix x = packed_from_words(x_words, n, p);
+        xyz::oracle::BruteForceOptions o;
+        if (has_gamma) o.gamma = gamma;
+        if (has_top_k) o.top_k = top_k;
+        o.histogram_bins = bins;
+        o.force = force != 0;
+        const auto r = xyz::oracle::brute_force_search(x, std::span<const double>(y, n), o);
+        *n_out = r.pairs.size();
+        *scanned = r.pairs_scanned;
+        *out_jk = static_cast<uint32_t*>(std::malloc(std::max<size_t>(1, 2 * r.pairs.size()) * 4));
+        *out_s = static_cast<double*>(std::malloc(std::max<size_t>(1, r.pairs.size()) * 8));
+        for (size_t t = 0; t < r.pairs.size(); ++t) {
+            (*out_jk)[2 * t] = r.pairs[t].j;
+            (*out_jk)[2 * t + 1] = r.pairs[t].k;
+            (*out_s)[t] = r.pairs[t].strength;
+        }
+        *out_hist = static_cast<uint64_t*>(std::malloc(std::max<size_t>(1, r.histogram.size()) * 8));
+        for (size_t t = 0; t < r.histogram.size(); ++t) (*out_hist)[t] = r.histogram[t];
+    });
+}
+
 // lasso_path (lasso.cpp:447-597) with the config fields the benchmarks pin.
 // Output: per fit t, lambda[t], mains in [main_off[t], main_off[t+1]) of
 // (main_idx, main_val), pairs in [pair_off[t], pair_off[t+1]) of (pair_j,

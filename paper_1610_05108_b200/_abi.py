@@ -143,6 +143,10 @@ SIGNATURES = {
                                    C.c_uint64, C.c_int32, C.POINTER(C.POINTER(ScoredPair)), C.POINTER(C.c_uint64),
                                    C.POINTER(C.c_uint64), C.POINTER(C.POINTER(C.c_uint64)), C.c_char_p,
                                    C.c_size_t]),
+    "xyzb_brute_force_weighted": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int32, C.c_double, C.c_int32, C.c_uint64,
+                                            C.c_uint64, C.c_int32, C.POINTER(C.POINTER(ScoredPair)),
+                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                            C.POINTER(C.POINTER(C.c_uint64)), C.c_char_p, C.c_size_t]),
     "xyzb_design_create": (C.c_int, [C.POINTER(C.c_double), C.c_uint64, C.c_uint64, C.POINTER(C.c_double), C.c_int32,
                                      C.POINTER(_P), C.c_char_p, C.c_size_t]),
     "xyzb_design_destroy": (None, [_P]),

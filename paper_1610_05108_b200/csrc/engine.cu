@@ -13,6 +13,7 @@
 // No CPU fallback: every stage runs on the GPU; without a device the calls
 // fail with XYZB_E_CUDA.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -212,6 +213,15 @@ struct HostBuf {  // pinned
 
 u64 round_up(u64 a, u64 m) { return (a + m - 1) / m * m; }
 
+
+// NVTX range over a host-side region (search, batch, stage launches): the
+// engine's phases on an Nsight Systems timeline; free without a tool attached.
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 // event-timed stage accounting on the dataset stream
 struct StageClock {
@@ -894,6 +904,7 @@ kern::SignStrength sign_strength(SearchCtx& c) {
 // occurrences at or above the K-th distinct key's rank bin.
 void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, const u32* np, u64* launches,
                       const kern::SignStrength* sg = nullptr) {
+    Nvtx nv("xyzb:topk");
     xyzb_dataset* ds = c.ds;
     cudaStream_t st = ds->stream;
     auto* S = ds->tk_state.as<topk::State>();
@@ -1093,6 +1104,7 @@ void run_batches(SearchCtx& c) {
     const int bits = static_cast<int>(M);
     for (u64 b0 = 0, batch_idx = 0; b0 < R; b0 += B, ++batch_idx) {
         const u64 nb = std::min(B, R - b0);
+        Nvtx nv_batch("xyzb:batch");
         const u32* rows = ds->rows.as<u32>() + b0 * M;
         const u32* rid = ds->rid.as<u32>() + b0;
         const int8_t* rsign = ds->rsign.as<int8_t>() + b0;
@@ -1275,6 +1287,7 @@ void run_batches(SearchCtx& c) {
         if (!part_path && !c.pairs_in_sort)  // sorted / bucket paths: sorted keys + indices read by count and emit
             c.bytes[XYZB_STAGE_JOIN] += nb * p * (sizeof(K) + 4) * 2;
         // ---- verify ----
+        Nvtx nv_verify("xyzb:verify");
         kern::VerifyArgs A;
         A.items = ds->items.as<kern::Item>();
         A.nitems = nitems;
@@ -1456,6 +1469,7 @@ double topk_filter(std::vector<xyzb_hit>& hits, std::vector<u64>& order, std::ve
 // rank for top-K; copy the report arrays to the host.
 void merge_hits(SearchCtx& c, u32 H, u32 rmax, std::vector<xyzb_hit>& hits_out, std::vector<u64>& order_out,
                 std::vector<u64>& topk_out) {
+    Nvtx nv("xyzb:merge");
     xyzb_dataset* ds = c.ds;
     cudaStream_t st = ds->stream;
     hits_out.clear();
@@ -1725,6 +1739,7 @@ void check_mode(const xyzb_dataset* ds, const xyzb_params* q, const xyzb_respons
 
 void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q, const uint32_t* draws,
                xyzb_result* out) {
+    Nvtx nv("xyzb_search");
     const auto t0 = std::chrono::steady_clock::now();
     validate_params(q);
     DeviceGuard dg(ds->device);
@@ -2206,6 +2221,206 @@ CUtensorMap operand_map(void* base, u64 rows, u64 Kp, u32 box_rows) {
     return m;
 }
 
+namespace {
+namespace brutew {
+
+// The exhaustive oracle's continuous-response overload (oracle.cpp:93-100,
+// scalar_weighted_strength): the weighted strength of every pair j < k,
+// rows in order and fp64 adds (bit-identical to the host's loop), 16 x 16
+// pair tiles of the upper triangle walked by persistent CTAs. PASS 0: the
+// caller's histogram (shared per CTA when it fits) and, for top-K, a 2^20-bin
+// histogram of the kept strengths (the host derives the top-K cutoff from
+// it); PASS 1: the kept pairs at or above the cut, appended.
+constexpr int kTile = 16;
+constexpr int kFineBits = 20;
+constexpr u32 kSmemBins = 8192;
+
+struct Out {
+    u32 j, k;
+    double s;
+};
+
+__device__ __forceinline__ u32 fine_bin(double s) {
+    const double x = s * double(1u << kFineBits);
+    return x <= 0.0 ? 0u : (x >= double(1u << kFineBits) ? (1u << kFineBits) : u32(x));
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(kTile * kTile) weighted_pairs(
+    const u64* __restrict__ Xc, u32 Wp, u32 W, u32 p, const u64* __restrict__ sb, const double* __restrict__ wabs,
+    double norm, u32 bins, unsigned long long* __restrict__ uhist, int has_gamma, double gamma, int fine,
+    unsigned int* __restrict__ fhist, unsigned long long* __restrict__ kept, double cut, Out* __restrict__ out,
+    u32* __restrict__ nout, u32 cap) {
+    extern __shared__ u32 sh[];
+    const bool shist = PASS == 0 && bins > 0 && bins <= kSmemBins;
+    if (shist) {
+        for (u32 b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+        __syncthreads();
+    }
+    const u64 T = (u64(p) + kTile - 1) / kTile;
+    const u64 ntiles = T * (T + 1) / 2;
+    u64 mykept = 0;
+    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // tile -> (tj, tk), tj <= tk: row tj starts at tj*T - tj*(tj-1)/2
+        u64 tj = u64((2.0 * double(T) + 1.0 - sqrt((2.0 * double(T) + 1.0) * (2.0 * double(T) + 1.0) - 8.0 * double(tile))) / 2.0);
+        while (tj > 0 && tj * T - tj * (tj - 1) / 2 > tile) --tj;
+        while ((tj + 1) * T - (tj + 1) * tj / 2 <= tile) ++tj;
+        const u64 tk = tj + (tile - (tj * T - tj * (tj - 1) / 2));
+        const u32 j = u32(tj * kTile + threadIdx.x / kTile), k = u32(tk * kTile + threadIdx.x % kTile);
+        const bool valid = j < k && k < p;
+        double s = -1.0;
+        if (valid) {
+            const u64 *a = Xc + u64(j) * Wp, *b = Xc + u64(k) * Wp;
+            double acc = 0.0;
+            for (u32 w = 0; w < W; ++w) {
+                u64 m = a[w] ^ b[w] ^ sb[w];
+                while (m) {
+                    const int bit = __ffsll(static_cast<long long>(m)) - 1;
+                    acc = __dadd_rn(acc, wabs[u64(w) * 64 + bit]);
+                    m &= m - 1;
+                }
+            }
+            s = acc / norm;
+        }
+        const bool keep = valid && (!has_gamma || s >= gamma);
+        if (PASS == 0) {
+            if (valid && bins) {
+                u64 bin = u64(s * double(bins));
+                if (bin >= bins) bin = bins - 1;
+                if (shist) atomicAdd(sh + bin, 1u);
+                else atomicAdd(uhist + bin, 1ull);
+            }
+            if (keep) {
+                ++mykept;
+                if (fine) atomicAdd(fhist + fine_bin(s), 1u);
+            }
+        } else if (keep && s >= cut) {
+            const u32 slot = atomicAdd(nout, 1u);
+            if (slot < cap) out[slot] = Out{j, k, s};
+        }
+    }
+    if (PASS == 0) {
+        if (mykept) atomicAdd(kept, static_cast<unsigned long long>(mykept));
+        if (shist) {
+            __syncthreads();
+            for (u32 b = threadIdx.x; b < bins; b += blockDim.x)
+                if (sh[b]) atomicAdd(uhist + b, static_cast<unsigned long long>(sh[b]));
+        }
+    }
+}
+
+} // namespace brutew
+} // namespace
+
+extern "C" int xyzb_brute_force_weighted(xyzb_dataset* ds, const double* y, int32_t has_gamma, double gamma,
+                                         int32_t has_top_k, uint64_t top_k, uint64_t histogram_bins, int32_t force,
+                                         xyzb_scored_pair** pairs, uint64_t* n_pairs, uint64_t* pairs_scanned,
+                                         uint64_t** histogram, char* err, size_t errlen) {
+    if (pairs) *pairs = nullptr;
+    if (n_pairs) *n_pairs = 0;
+    if (pairs_scanned) *pairs_scanned = 0;
+    if (histogram) *histogram = nullptr;
+    return guarded(err, errlen, [&] {
+        if (!ds || !y || !pairs || !n_pairs || !pairs_scanned || !histogram)
+            throw data_error("brute_force_search: null argument");
+        if (!ds->binary) throw data_error("brute_force_search: the GPU brute force takes binary datasets");
+        const u64 n = ds->n, p = ds->p, W = ds->W, Wp = ds->Wp;
+        if (p > 20000 && !force)  // check_guard (oracle.cpp:16-22)
+            throw guard_error("brute_force_search: p = " + std::to_string(p) +
+                              " exceeds the 20000 guard; pass force to run anyway");
+        if (p > 0xffffffffull) throw data_error("brute_force_search: matrix too large");
+        double norm = 0.0;  // scalar_weighted_strength's norm, rows in order
+        for (u64 i = 0; i < n; ++i) norm += std::abs(y[i]);
+        if (p >= 2 && norm <= 0.0) throw data_error("scalar_weighted_strength: zero response vector");
+        *pairs_scanned = p * (p - 1) / 2;
+        u64* h = nullptr;
+        if (histogram_bins > 0) {
+            h = static_cast<u64*>(std::calloc(histogram_bins, 8));
+            if (!h) throw internal_error("brute_force_search: out of host memory");
+            *histogram = h;
+        }
+        if (p < 2) return;
+        DeviceGuard dg(ds->device);
+        const cudaStream_t st = ds->stream;
+        StreamScope ss(st);
+        std::vector<u64> hs(Wp + Wp * 64, 0ull);
+        double* hw = reinterpret_cast<double*>(hs.data() + Wp);
+        for (u64 i = 0; i < n; ++i) {
+            if (y[i] > 0.0) hs[i >> 6] |= 1ull << (i & 63);
+            hw[i] = std::abs(y[i]);
+        }
+        DevBuf yb, uh, fh, cnt, ob, no;
+        yb.ensure(hs.size() * 8);
+        XYZB_CUDA(cudaMemcpyAsync(yb.p, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice, st));
+        const u64* sb = yb.as<u64>();
+        const double* wabs = reinterpret_cast<const double*>(yb.as<u64>() + Wp);
+        const bool fine = has_top_k != 0;
+        const u64 nfine = (u64(1) << brutew::kFineBits) + 1;
+        uh.ensure(std::max<u64>(1, histogram_bins) * 8);
+        fh.ensure(fine ? nfine * 4 : 4);
+        cnt.ensure(8);
+        XYZB_CUDA(cudaMemsetAsync(uh.p, 0, std::max<u64>(1, histogram_bins) * 8, st));
+        if (fine) XYZB_CUDA(cudaMemsetAsync(fh.p, 0, nfine * 4, st));
+        XYZB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+        const u32 grid = kSMs * 8;
+        const size_t shb = histogram_bins > 0 && histogram_bins <= brutew::kSmemBins ? histogram_bins * 4 : 0;
+        brutew::weighted_pairs<0><<<grid, brutew::kTile * brutew::kTile, shb, st>>>(
+            ds->Xc.as<u64>(), u32(Wp), u32(W), u32(p), sb, wabs, norm, u32(histogram_bins),
+            uh.as<unsigned long long>(), has_gamma, gamma, fine ? 1 : 0, fh.as<unsigned int>(),
+            cnt.as<unsigned long long>(), 0.0, nullptr, nullptr, 0u);
+        XYZB_LAUNCH_CHECK();
+        u64 kept = 0;
+        std::vector<unsigned int> fhist(fine ? nfine : 0);
+        if (histogram_bins) XYZB_CUDA(cudaMemcpyAsync(h, uh.p, histogram_bins * 8, cudaMemcpyDeviceToHost, st));
+        if (fine) XYZB_CUDA(cudaMemcpyAsync(fhist.data(), fh.p, nfine * 4, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaMemcpyAsync(&kept, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        if (!has_gamma && !has_top_k) return;
+        // the emission cut: every kept pair (gamma), or the fine bin holding the K-th kept strength
+        double cut = -1.0;
+        u64 emit = kept;
+        if (has_top_k) {
+            const u64 want = std::min<u64>(top_k, kept);
+            if (want == 0) return;
+            u64 acc = 0, b = nfine;
+            while (b-- > 0) {
+                acc += fhist[b];
+                if (acc >= want) break;
+            }
+            cut = double(b) / double(u64(1) << brutew::kFineBits);  // the bin's lower edge
+            emit = acc;
+        }
+        if (emit > 0xffffffffull) throw internal_error("brute_force_search: more than 2^32 pairs above the cut");
+        ob.ensure(std::max<u64>(1, emit) * sizeof(brutew::Out));
+        no.ensure(4);
+        XYZB_CUDA(cudaMemsetAsync(no.p, 0, 4, st));
+        brutew::weighted_pairs<1><<<grid, brutew::kTile * brutew::kTile, 0, st>>>(
+            ds->Xc.as<u64>(), u32(Wp), u32(W), u32(p), sb, wabs, norm, 0u, nullptr, has_gamma, gamma, 0, nullptr,
+            nullptr, cut, ob.as<brutew::Out>(), no.as<u32>(), u32(emit));
+        XYZB_LAUNCH_CHECK();
+        std::vector<brutew::Out> got(emit);
+        u32 nget = 0;
+        if (emit) XYZB_CUDA(cudaMemcpyAsync(got.data(), ob.p, emit * sizeof(brutew::Out), cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaMemcpyAsync(&nget, no.p, 4, cudaMemcpyDeviceToHost, st));
+        XYZB_CUDA(cudaStreamSynchronize(st));
+        if (nget != emit) throw internal_error("brute_force_search: emitted pair count differs from the histogram");
+        const auto by_jk = [](const brutew::Out& a, const brutew::Out& b) { return a.j != b.j ? a.j < b.j : a.k < b.k; };
+        if (has_top_k) {  // scan_all_pairs (oracle.cpp:45-53): strength desc, (j, k) asc; the K best, then (j, k)
+            std::sort(got.begin(), got.end(), [&](const brutew::Out& a, const brutew::Out& b) {
+                if (a.s != b.s) return a.s > b.s;
+                return by_jk(a, b);
+            });
+            got.resize(std::min<u64>(top_k, got.size()));
+        }
+        std::sort(got.begin(), got.end(), by_jk);
+        auto* outp = static_cast<xyzb_scored_pair*>(std::malloc(std::max<size_t>(1, got.size()) * sizeof(xyzb_scored_pair)));
+        if (!outp) throw internal_error("brute_force_search: out of host memory");
+        for (size_t t = 0; t < got.size(); ++t) outp[t] = xyzb_scored_pair{got[t].j, got[t].k, got[t].s};
+        *pairs = outp;
+        *n_pairs = got.size();
+    });
+}
+
 extern "C" int xyzb_brute_force(xyzb_dataset* ds, const int8_t* y_sign, int32_t has_gamma, double gamma,
                                 int32_t has_top_k, uint64_t top_k, uint64_t histogram_bins, int32_t force,
                                 xyzb_scored_pair** pairs, uint64_t* n_pairs, uint64_t* pairs_scanned,
@@ -2459,6 +2674,7 @@ std::pair<u64, u64> shard_bounds(u64 L, u64 g, u64 G) { return {1 + L * g / G, 1
 // search.cpp:59-111).
 void multi_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q, const uint32_t* draws,
                   xyzb_result* out) {
+    Nvtx nv("xyzb_search:devices");
     const auto t0 = std::chrono::steady_clock::now();
     validate_params(q);
     std::vector<xyzb_dataset*> devs{ds};
@@ -2629,6 +2845,7 @@ int xyzb_dataset_create(const xyzb_problem* pr, xyzb_dataset** out, char* err, s
             if (d < 0 || d >= ndev)
                 throw data_error("xyzb_dataset_create: device " + std::to_string(d) + " outside [0, " +
                                  std::to_string(ndev) + ")");
+        Nvtx nv("xyzb_dataset_create");
         std::unique_ptr<xyzb_dataset> ds(new xyzb_dataset());
         ds->device = devs[0];
         if (const long long e = topt().hit_cap.load())  // tests force the hit-buffer regrow path

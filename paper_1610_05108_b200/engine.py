@@ -221,11 +221,13 @@ class OracleResult(NamedTuple):
 
 def brute_force_search(x, y, gamma: Optional[float] = None, top_k: Optional[int] = None, histogram_bins: int = 0,
                        force: bool = False, device: int = 0) -> OracleResult:
-    """oracle::brute_force_search, binary overload (oracle.hpp:36-37,
-    oracle.cpp:84-91), on the GPU: exact strengths of all p(p-1)/2 pairs.
-    `x` is a PackedMatrix or a binary Dataset; y the +-1 response."""
+    """oracle::brute_force_search (oracle.hpp:36-41, oracle.cpp:84-100) on
+    the GPU: exact strengths of all p(p-1)/2 pairs. `x` is a PackedMatrix or a
+    binary Dataset; y the +-1 response (int8: tensor-core Gram product) or a
+    real response (the weighted strength, bit-identical to the host's)."""
     ds = x if isinstance(x, Dataset) else dataset_for(x, device)
-    yy = np.ascontiguousarray(y, np.int8)
+    weighted = np.asarray(y).dtype != np.int8  # the continuous-response overload (oracle.cpp:93-100)
+    yy = np.ascontiguousarray(y, np.float64 if weighted else np.int8)
     if yy.shape[0] != ds.n_rows:
         raise DataError("brute_force_search: response length mismatch")
     lib = ds._lib
@@ -233,11 +235,12 @@ def brute_force_search(x, y, gamma: Optional[float] = None, top_k: Optional[int]
     hist = C.POINTER(C.c_uint64)()
     npairs, scanned = C.c_uint64(), C.c_uint64()
     err = _abi.errbuf()
-    raise_for(lib.xyzb_brute_force(ds.handle, yy.ctypes.data_as(C.POINTER(C.c_int8)), int(gamma is not None),
-                                   float(gamma) if gamma is not None else 0.0, int(top_k is not None),
-                                   int(top_k) if top_k is not None else 0, int(histogram_bins), int(bool(force)),
-                                   C.byref(pairs), C.byref(npairs), C.byref(scanned), C.byref(hist), err,
-                                   _abi.ERRBUF), err)
+    fn = lib.xyzb_brute_force_weighted if weighted else lib.xyzb_brute_force
+    yp = yy.ctypes.data_as(C.POINTER(C.c_double) if weighted else C.POINTER(C.c_int8))
+    raise_for(fn(ds.handle, yp, int(gamma is not None), float(gamma) if gamma is not None else 0.0,
+                 int(top_k is not None), int(top_k) if top_k is not None else 0, int(histogram_bins),
+                 int(bool(force)), C.byref(pairs), C.byref(npairs), C.byref(scanned), C.byref(hist), err,
+                 _abi.ERRBUF), err)
     try:
         out = [ScoredPair(pairs[i].j, pairs[i].k, pairs[i].strength) for i in range(npairs.value)]
         h = [int(hist[i]) for i in range(histogram_bins)] if histogram_bins and hist else []

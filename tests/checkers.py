@@ -65,6 +65,10 @@ _REF_SIGS = {
     "ref_write_dataset": (C.c_int, [C.c_char_p, C.c_int32, _U64P, _F64P, C.c_uint64, C.c_uint64, C.c_char_p,
                                     C.c_size_t]),
     "ref_read_dataset": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _U64P, _U64P, C.c_char_p, C.c_size_t]),
+    "ref_brute_force_weighted": (C.c_int, [_U64P, C.c_uint64, C.c_uint64, _F64P, C.c_int32, C.c_double,
+                                           C.c_int32, C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(_U32P),
+                                           C.POINTER(_F64P), _U64P, _U64P, C.POINTER(_U64P), C.c_char_p,
+                                           C.c_size_t]),
     "ref_sample_strengths": (C.c_int, [C.POINTER(_abi.Problem), C.POINTER(_abi.Response), C.c_int32, C.c_int32,
                                        C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, _F64P, _U64P, C.c_char_p,
                                        C.c_size_t]),
@@ -411,13 +415,16 @@ def ref_read_dataset(path):
 
 
 def ref_brute_force(x: PackedMatrix, y, gamma=None, top_k=None, histogram_bins=0, force=False):
-    """oracle::brute_force_search of the reference: ([(j, k, s)], pairs_scanned, [hist])."""
+    """oracle::brute_force_search of the reference: ([(j, k, s)], pairs_scanned, [hist]);
+    the continuous-response overload when y is not int8."""
     lib = ref_lib()
-    yy = np.ascontiguousarray(y, np.int8)
+    weighted = np.asarray(y).dtype != np.int8
+    yy = np.ascontiguousarray(y, np.float64 if weighted else np.int8)
     jk, s, h = _U32P(), _F64P(), _U64P()
     n, scanned = C.c_uint64(), C.c_uint64()
     err = _abi.errbuf()
-    code = lib.ref_brute_force(_u64p(x.words), x.n_rows, x.n_cols, yy.ctypes.data_as(C.POINTER(C.c_int8)),
+    fn = lib.ref_brute_force_weighted if weighted else lib.ref_brute_force
+    code = fn(_u64p(x.words), x.n_rows, x.n_cols, yy.ctypes.data_as(_F64P if weighted else C.POINTER(C.c_int8)),
                                int(gamma is not None), float(gamma or 0.0), int(top_k is not None), int(top_k or 0),
                                int(histogram_bins), int(force), C.byref(jk), C.byref(s), C.byref(n),
                                C.byref(scanned), C.byref(h), err, _abi.ERRBUF)

@@ -93,3 +93,44 @@ def test_xyz_hits_are_oracle_hits_at_config2_size():
         assert key in oracle and oracle[key] == h.strength
     top = xb.brute_force_search(ds, y, top_k=1, force=True).pairs[0]
     assert top.strength >= max(h.strength for h in pos)
+
+
+def _weighted_instances():
+    rng = np.random.default_rng(9)
+    xb = _engine()
+    x, _ = ck.ref_planted(300, 200, 3, 7, 0.9, 2)
+    yield "planted_gauss", x, rng.standard_normal(300)
+    for n in (20, 64, 65, 127):
+        xs = rng.choice(np.array([-1, 1], np.int8), size=(n, 90))
+        y = rng.standard_normal(n)
+        y[::5] = 0.0  # zero responses carry no weight
+        yield f"random_n{n}", xb.PackedMatrix.from_signs(xs), y
+    xs = rng.choice(np.array([-1, 1], np.int8), size=(100, 120))
+    yield "integer_weights_ties", xb.PackedMatrix.from_signs(xs), rng.integers(-3, 4, 100).astype(np.float64)
+
+
+@pytest.mark.parametrize("opt", OPTIONS, ids=[str(o) for o in OPTIONS])
+def test_weighted_brute_force_matches_the_reference(opt):
+    """The continuous-response overload (oracle.cpp:93-100): every strength
+    bit-identical to scalar_weighted_strength, same selection, ties and
+    histogram."""
+    xb = _engine()
+    for name, x, y in _weighted_instances():
+        want_pairs, want_scanned, want_hist = ck.ref_brute_force(x, y, force=True, **opt)
+        got = xb.brute_force_search(x, y, force=True, **opt)
+        assert got.pairs_scanned == want_scanned, name
+        assert [(p.j, p.k, p.strength) for p in got.pairs] == want_pairs, name
+        assert got.histogram == want_hist, name
+
+
+def test_weighted_brute_force_guard_and_zero_response():
+    xb = _engine()
+    rng = np.random.default_rng(2)
+    x = xb.PackedMatrix.from_signs(rng.choice(np.array([-1, 1], np.int8), size=(8, 20001)))
+    with pytest.raises(xb.GuardError):
+        xb.brute_force_search(x, np.ones(8), top_k=1)
+    small = xb.PackedMatrix.from_signs(rng.choice(np.array([-1, 1], np.int8), size=(8, 30)))
+    with pytest.raises(ck.CheckerError, match="zero response vector"):
+        ck.ref_brute_force(small, np.zeros(8), top_k=1)
+    with pytest.raises(xb.DataError, match="zero response vector"):
+        xb.brute_force_search(small, np.zeros(8), top_k=1)
