@@ -12,7 +12,8 @@
  *                   M <= 24, 3 = the cluster of 16-bit tables for M = 19, 20
  *                   and sparse bucket spaces
  *   merge_large     the multi-kernel merge instead of the single-CTA merge
- *   sign_verify_off the fp32-column verify instead of the sign-bit verify
+ *   sign_verify_off the exact verifies instead of the bit-plane ones (the sign
+ *                   transform's fp32 columns; continuous-Y's fp64 set-bit sums)
  *   trace           host-side phase times of dataset creation on stderr
  *   brute_cuda      the CUDA-core exhaustive oracle instead of tcgen05
  * Returns XYZB_OK, or XYZB_E_DATA for an unknown name.

@@ -734,6 +734,8 @@ struct SearchCtx {
     // the sign transform's quantised response (bit planes, SignStrength)
     int qB = kern::kSignQB;
     double qinv = 0.0, qdelta = 0.0;
+    // the weighted verify's quantised |y| (continuous-Y, WeightedQ)
+    double wqinv = 0.0, wqdelta = 0.0;
     long long qsum = 0;
     bool sign_verify = false;  // the bit-plane verify ran
     bool no_hash = false;  // a hashed partition overflowed: the sparse grouping runs on the sorted path
@@ -816,6 +818,25 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
         XYZB_CUDA(cudaMemcpyAsync(ds->spos.p, sp, Wp * 8, cudaMemcpyHostToDevice, st));
         XYZB_CUDA(cudaMemcpyAsync(ds->sneg.p, sn, Wp * 8, cudaMemcpyHostToDevice, st));
         XYZB_CUDA(cudaMemcpyAsync(ds->wabs.p, w, nb * 8, cudaMemcpyHostToDevice, st));
+        // |y| quantised to kWeightQB-bit unsigned planes (WeightedQ): q_i = rint(|y_i| scale)
+        double ymax = 0.0;
+        for (u64 i = 0; i < n; ++i) ymax = std::max(ymax, std::abs(y[i]));
+        constexpr int QB = kern::kWeightQB;
+        const double scale = (std::ldexp(1.0, QB) - 1.0) / ymax;
+        const u64 W = ds->W;
+        ds->h_planes.ensure(u64(QB) * W * 8);
+        u64* pl = ds->h_planes.as<u64>();
+        std::memset(pl, 0, u64(QB) * W * 8);
+        for (u64 i = 0; i < n; ++i) {
+            const u64 q = static_cast<u64>(std::llrint(std::abs(y[i]) * scale));
+            for (int b = 0; b < QB; ++b)
+                if ((q >> b) & 1ull) pl[u64(b) * W + (i >> 6)] |= 1ull << (i & 63);
+        }
+        c.wqinv = 1.0 / scale;
+        // |quantised - exact| <= n / (2 scale) over ||y||_1; + slack for the fp64 sums
+        c.wqdelta = double(n) / (2.0 * scale * norm) + 1e-9;
+        ds->yplanes.ensure(u64(QB) * W * 8);
+        XYZB_CUDA(cudaMemcpyAsync(ds->yplanes.p, pl, u64(QB) * W * 8, cudaMemcpyHostToDevice, st));
         return;
     }
     double* yp = reinterpret_cast<double*>(hp);
@@ -903,7 +924,7 @@ kern::SignStrength sign_strength(SearchCtx& c) {
 // and appends the pairs at or above it; then the hit buffer is pruned to the
 // occurrences at or above the K-th distinct key's rank bin.
 void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, const u32* np, u64* launches,
-                      const kern::SignStrength* sg = nullptr) {
+                      const kern::SignStrength* sg = nullptr, const kern::WeightedQ* wq = nullptr) {
     Nvtx nv("xyzb:topk");
     xyzb_dataset* ds = c.ds;
     cudaStream_t st = ds->stream;
@@ -919,8 +940,11 @@ void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, c
         topk::emit_select<<<1, 1024, 0, st>>>(ds->tk_hist.as<u32>(), c.tk_shift, target, S, c.tk_level >= 2);
         XYZB_LAUNCH_CHECK();
         if (sg)  // sign transform: exact re-verification of the pairs that may reach E
-            topk::emit_pairs_sign<<<kSMs * 8, 256, 0, st>>>(A, ds->pairs.as<kern::PairRec>(), np,
-                                                            static_cast<u32>(c.pair_cap), *sg, S);
+            topk::emit_pairs_requant<<<kSMs * 8, 256, 0, st>>>(A, ds->pairs.as<kern::PairRec>(), np,
+                                                               static_cast<u32>(c.pair_cap), *sg, S);
+        else if (wq)  // weighted: likewise
+            topk::emit_pairs_requant<<<kSMs * 8, 256, 0, st>>>(A, ds->pairs.as<kern::PairRec>(), np,
+                                                               static_cast<u32>(c.pair_cap), *wq, S);
         else
             topk::emit_pairs<<<kSMs * 8, 256, 0, st>>>(ds->pairs.as<kern::PairRec>(), ds->tk_sint.as<u32>(), np,
                                                        static_cast<u32>(c.pair_cap), A.nitems, A.item_cap, S,
@@ -1055,7 +1079,9 @@ void run_batches(SearchCtx& c) {
     // the sign transform's bit-plane verify over the pair list: columns of <= 2048 rows (lane w holds
     // word w of the sign bits and of the response planes)
     const bool sign_pairs = xy && !unbiased && ds->Spos.p && ds->W <= 32 && !topt().sign_verify_off.load();
-    const bool pair_path = (c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128) || sign_pairs;
+    // the weighted (continuous-Y) verify over the pair list: rows <= 2048, |y| as bit planes
+    const bool weighted_pairs = c.mode == XYZB_MODE_CONTINUOUS_Y && ds->W <= 32 && !topt().sign_verify_off.load();
+    const bool pair_path = (c.mode == XYZB_MODE_BINARY && ds->Wp / 2 <= 128) || sign_pairs || weighted_pairs;
     if (pair_path) {
         c.pair_cap = std::min<u64>(0xffffffffull, std::max<u64>(u64(1) << 20, B * p) * c.pair_scale);
         if (const long long e = topt().pair_cap.load())  // tests force the pair-list regrow path
@@ -1341,6 +1367,25 @@ void run_batches(SearchCtx& c) {
                 c.verify_spans.push_back({ev0, ev1});
                 if (c.topk_all) {
                     topk_after_batch(c, true, A, np, &c.launches[XYZB_STAGE_MERGE], &g);
+                    clk.span(XYZB_STAGE_MERGE, ev1, clk.mark());
+                }
+                continue;
+            }
+            if (weighted_pairs) {
+                const kern::WeightedQ g{ds->Xc.as<u64>(), static_cast<u32>(ds->Wp), ds->W, ds->spos.as<u64>(),
+                                        ds->sneg.as<u64>(), ds->yplanes.as<u64>(), c.wqinv, c.norm, c.gamma, c.wqdelta,
+                                        kern::WeightedStrength{ds->Xc.as<u64>(), static_cast<u32>(ds->Wp),
+                                                               ds->spos.as<u64>(), ds->sneg.as<u64>(),
+                                                               ds->wabs.as<double>(), c.norm, c.gamma}};
+                kern::verify_pairs_weighted<kern::kWeightQB><<<vgrid, 256, 0, st>>>(
+                    A, ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), g);
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_VERIFY] += 1;
+                cudaEvent_t ev1 = clk.mark();
+                clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
+                c.verify_spans.push_back({ev0, ev1});
+                if (c.topk_all) {
+                    topk_after_batch(c, true, A, np, &c.launches[XYZB_STAGE_MERGE], nullptr, &g);
                     clk.span(XYZB_STAGE_MERGE, ev1, clk.mark());
                 }
                 continue;

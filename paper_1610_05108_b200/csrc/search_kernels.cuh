@@ -1410,7 +1410,7 @@ __device__ __noinline__ void append_pair_hit_real(const VerifyArgs& A, PairRec p
 // is reduced (SignStrength: quantised strength, exact fp32 re-verification
 // within the quantisation bound of the threshold). Top-K over all candidates,
 // first phase (running threshold still 0): every pair's rank lower bound
-// rank(s_q - delta) goes to sint_out instead (topk::emit_pairs_sign emits).
+// rank(s_q - delta) goes to sint_out instead (topk::emit_pairs_requant emits).
 template <int QB>
 __global__ void __launch_bounds__(256, 4) verify_pairs_sign(VerifyArgs A, const PairRec* __restrict__ pairs,
                                                              const u32* __restrict__ npairs, u32 pair_cap,
@@ -1480,6 +1480,87 @@ __global__ void __launch_bounds__(256, 4) verify_pairs_sign(VerifyArgs A, const 
             pk = pk1;
             zj = zj1;
             zk = zk1;
+        }
+    }
+}
+
+// Continuous-Y (weighted) strengths from bit planes (A9,
+// transforms.cpp:42-76): s = S(x_j ^ x_k ^ s_pass) / ||y||_1 with S(m) the sum
+// of |y| over the rows of mask m. |y| is quantised once per search to QB-bit
+// unsigned integers q_i = rint(|y_i| scale) held as bit planes, so
+// S(m) ~ sum_b 2^b popc(P_b & m) / scale within n / (2 scale) — a per-pair
+// cost of 2 column words and QB popcounts per 64 rows instead of a
+// dependent fp64 load per set bit. A pair within delta of the threshold is
+// re-verified with the exact fp64 sum (WeightedStrength), so hits and their
+// strengths are those of the exact verify.
+constexpr int kWeightQB = 12;
+struct WeightedQ {
+    const u64* Xc;
+    u32 Wp;
+    u64 Wn;
+    const u64 *spos, *sneg;  // [Wp] response sign bits of the + / - pass
+    const u64* planes;       // [QB][Wn] bit planes of q
+    double inv_scale, norm, gamma, delta;
+    WeightedStrength exact;
+};
+
+// Pair-list walk of the quantised weighted verify (rows <= 2048: lane w
+// holds word w of both columns and of every plane), the next pair's words in
+// flight; the top-K first phase writes rank lower bounds like the sign walk.
+template <int QB>
+__global__ void __launch_bounds__(256, 4) verify_pairs_weighted(VerifyArgs A, const PairRec* __restrict__ pairs,
+                                                                 const u32* __restrict__ npairs, u32 pair_cap,
+                                                                 WeightedQ f) {
+    const int lane = threadIdx.x & 31;
+    const bool act = u64(lane) < f.Wn;
+    u64 pl[QB];
+#pragma unroll
+    for (int b = 0; b < QB; ++b) pl[b] = act ? f.planes[u64(b) * f.Wn + lane] : 0ull;
+    const u64 sp = act ? f.spos[lane] : 0ull, sn = act ? f.sneg[lane] : 0ull;
+    const u32 P = *A.nitems > A.item_cap ? 0u : min(*npairs, pair_cap);
+    const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
+    const bool ranks = A.sint_out && rthr == 0;
+    const double gate = A.rank_thr ? double(rthr) / double(1u << kRealRankBits) : f.gamma;
+    const u64 warp = (u64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    const u64* X = f.Xc;
+    const u32 Wp = f.Wp;
+    for (u64 c0 = warp * 32; c0 < P; c0 += nwarps * 32) {
+        const u32 cnt = u32(minu(32, P - c0));
+        const PairRec mine = u32(lane) < cnt ? pairs[c0 + lane] : PairRec{0, 0, 0, 0};
+        u32 j = __shfl_sync(0xffffffffu, mine.pa, 0), k = __shfl_sync(0xffffffffu, mine.pb, 0);
+        u64 xj = act ? __ldg(X + u64(j) * Wp + lane) : 0ull, xk = act ? __ldg(X + u64(k) * Wp + lane) : 0ull;
+        for (u32 t = 0; t < cnt; ++t) {
+            u32 j1 = 0, k1 = 0;
+            u64 xj1 = 0, xk1 = 0;
+            if (t + 1 < cnt) {
+                j1 = __shfl_sync(0xffffffffu, mine.pa, t + 1);
+                k1 = __shfl_sync(0xffffffffu, mine.pb, t + 1);
+                if (act) {
+                    xj1 = __ldg(X + u64(j1) * Wp + lane);
+                    xk1 = __ldg(X + u64(k1) * Wp + lane);
+                }
+            }
+            const u32 run = __shfl_sync(0xffffffffu, mine.run, t);
+            const bool pos_pass = A.run_sign[run] > 0;
+            const u64 m = xj ^ xk ^ (pos_pass ? sp : sn);
+            int a = 0;
+#pragma unroll
+            for (int b = 0; b < QB; ++b) a += __popcll(pl[b] & m) << b;
+            a = warp_sum(a);
+            double s = double(a) * f.inv_scale / f.norm;
+            if (ranks) {
+                if (u32(lane) == t) A.sint_out[c0 + t] = strength_rank(fmax(0.0, s - f.delta), 0u, 0);
+            } else if (s >= gate - f.delta) {  // warp-uniform: the exact fp64 sum
+                s = f.exact(j, k, pos_pass, lane, 0xffffffffu);
+                const PairRec r{j, k, run, __shfl_sync(0xffffffffu, mine.pad, t)};
+                if (lane == 0 && (A.rank_thr ? strength_rank(s, 0u, 0) >= rthr : f.exact.hit(s)))
+                    append_pair_hit_real(A, r, s);
+            }
+            j = j1;
+            k = k1;
+            xj = xj1;
+            xk = xk1;
         }
     }
 }

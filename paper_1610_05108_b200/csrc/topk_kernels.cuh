@@ -189,12 +189,13 @@ __global__ void __launch_bounds__(256) emit_pairs(const PairRec* __restrict__ pa
     }
 }
 
-// Sign-transform pair list: the pairs whose exact strength may reach E
-// (rank lower bound at or above rank(E - 2 delta)) are re-verified exactly,
-// one warp per pair, and appended at or above E.
-__global__ void __launch_bounds__(256) emit_pairs_sign(kern::VerifyArgs A, const PairRec* __restrict__ pairs,
-                                                       const u32* __restrict__ npairs, u32 pair_cap,
-                                                       kern::SignStrength f, const State* __restrict__ st) {
+// Quantised pair walks (sign transform, weighted): the pairs whose exact
+// strength may reach E (rank lower bound at or above rank(E - 2 delta)) are
+// re-verified exactly, one warp per pair, and appended at or above E.
+template <class F>  // kern::SignStrength / kern::WeightedQ: delta + exact(j, k, pos_pass, lane, mask)
+__global__ void __launch_bounds__(256) emit_pairs_requant(kern::VerifyArgs A, const PairRec* __restrict__ pairs,
+                                                          const u32* __restrict__ npairs, u32 pair_cap, F f,
+                                                          const State* __restrict__ st) {
     if (st->thr > 0) return;  // appended by the verify
     const u32 P = batch_pairs(npairs, pair_cap, A.nitems, A.item_cap);
     const u32 E = st->emit;
