@@ -448,12 +448,15 @@ inline size_t part_join_smem(int lb) { return ((size_t(1) << lb) + kPjThreads * 
 // Sparse bucket spaces (2^M >> p, e.g. config 3: M = 20, p = 5e4): a dense
 // 2^lb table per partition would be mostly empty, so the partition's local
 // keys go into an open-addressing hash table in shared memory instead
-// (kHsSlots slots for at most kHsCap records, load <= 1/2): a slot holds a
-// key and its count, the insertion's count atomic returns the record's rank,
-// and the scan over the slots gives every key its grouped range. A key's
-// partner w ^ 1 is found by probing. A partition above kHsCap records (a
-// skewed key distribution) is not processed: the kernel raises *ovf and the
-// host redoes the search on the sorted path.
+// (kHsSlots slots for at most kHsCap records, load <= 1/2). A slot holds a
+// key PAIR g = w >> 1 — a key w and its partner w ^ 1 (the T map, PartMap)
+// share the slot — with both counts in one word (even key low 16 bits, odd
+// key high 16 bits): the insertion's count atomic returns each record's rank,
+// and a block's partner count sits in the same slot, so no partner probe is
+// needed. The occupied slots are listed as they are claimed, and the table
+// passes walk that list only. A partition above kHsCap records (a skewed key
+// distribution) is not processed: the kernel raises *ovf and the host redoes
+// the search on the sorted path.
 constexpr int kHsThreads = 512;
 constexpr int kHsPer = 4;
 constexpr u32 kHsCap = kHsThreads * kHsPer;  // 2048 records per partition
@@ -472,14 +475,6 @@ __device__ __forceinline__ u32 hs_hash(u32 u) {
     return u >> 20;
 }
 
-__device__ __forceinline__ u32 hs_find(const u32* tk, u32 u) {
-    for (u32 h = hs_hash(u);; h = (h + 1) & (kHsSlots - 1)) {
-        const u32 k = tk[h];
-        if (k == u) return h;
-        if (k == kHsEmpty) return kHsEmpty;
-    }
-}
-
 template <int EMIT>
 __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __restrict__ pe, const u32* __restrict__ pbeg,
                                                              u64 p, int M, int lb, const u32* __restrict__ xorc,
@@ -490,13 +485,14 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
                                                              PairRec* __restrict__ pairs, u32 pair_cap,
                                                              u32* __restrict__ ovf) {
     extern __shared__ __align__(16) u32 hsm[];
-    u32* tk = hsm;                  // [kHsSlots] keys
-    u32* tc = tk + kHsSlots;        // [kHsSlots] counts
-    u32* ts = tc + kHsSlots;        // [kHsSlots] grouped starts of the keys that are in a block
+    u32* tk = hsm;                  // [kHsSlots] key pairs g = w >> 1
+    u32* tc = tk + kHsSlots;        // [kHsSlots] counts: even key (low 16 bits), odd key (high 16 bits)
+    u32* occ = tc + kHsSlots;       // [kHsCap] occupied slots
+    u32* ts = occ + kHsCap;         // [kHsSlots] grouped start of the slot's records that are in a block
     u32* sg = ts + kHsSlots;        // [kHsCap] grouped columns
-    u32* heads = sg + kHsCap;       // [kHsCap] slots of the block heads
+    u32* heads = sg + kHsCap;       // [kHsCap] block heads: slot * 2 + key parity
     __shared__ u32 ws[68];
-    __shared__ u32 s_nheads, s_cursor;
+    __shared__ u32 s_nheads, s_cursor, s_nocc;
     __shared__ u64 red[2][kHsThreads / 32];
     const u32 b = blockIdx.y, d = blockIdx.x;
     const int k = M - lb;
@@ -519,11 +515,11 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
     for (u32 i = threadIdx.x; i < kHsSlots; i += blockDim.x) {
         tk[i] = kHsEmpty;
         tc[i] = 0;
-        if (EMIT) ts[i] = kHsEmpty;
     }
     if (threadIdx.x == 0) {
         s_nheads = 0;
         s_cursor = 0;
+        s_nocc = 0;
     }
     __syncthreads();
     const uint2* e = pe + u64(b) * p + beg;
@@ -538,34 +534,36 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
     for (int q = 0; q < kHsPer; ++q) {
         const u32 i = q * blockDim.x + threadIdx.x;
         if (i < cnt) {
-            const u32 u = v[q].x;  // the whole key w (partitions are hashed, M <= 31: never kHsEmpty)
-            u32 h = hs_hash(u);
+            const u32 u = v[q].x;  // the whole key w (partitions are hashed, M <= 31)
+            const u32 g = u >> 1;
+            u32 h = hs_hash(g);
             for (;;) {
-                const u32 old = atomicCAS(tk + h, kHsEmpty, u);
-                if (old == kHsEmpty || old == u) break;
+                const u32 old = atomicCAS(tk + h, kHsEmpty, g);
+                if (old == kHsEmpty) {
+                    occ[atomicAdd(&s_nocc, 1u)] = h;
+                    break;
+                }
+                if (old == g) break;
                 h = (h + 1) & (kHsSlots - 1);
             }
             slot[q] = h;
-            rk[q] = atomicAdd(tc + h, 1u);
+            const u32 sh = (u & 1u) << 4;
+            rk[q] = (atomicAdd(tc + h, 1u << sh) >> sh) & 0xffffu;
         }
     }
     __syncthreads();
+    const u32 nocc = s_nocc;
     if (!EMIT) {
         u64 pa = 0, wa = 0;
-        for (u32 s0 = threadIdx.x; s0 < kHsSlots; s0 += blockDim.x) {
-            const u32 u = tk[s0];
-            if (u == kHsEmpty) continue;
-            const u64 cx = tc[s0];
+        for (u32 o = threadIdx.x; o < nocc; o += blockDim.x) {
+            const u32 t2 = tc[occ[o]];
+            const u64 ce = t2 & 0xffffu, co = t2 >> 16;
             if (c == 0) {
-                pa += cx * cx;
-                wa += cx * (cx - 1) / 2;
-            } else if (!(u & 1u)) {
-                const u32 h2 = hs_find(tk, u | 1u);
-                if (h2 != kHsEmpty) {
-                    const u64 cz = tc[h2];
-                    pa += 2 * cx * cz;
-                    wa += cx * cz;
-                }
+                pa += ce * ce + co * co;
+                wa += (ce ? ce * (ce - 1) / 2 : 0) + (co ? co * (co - 1) / 2 : 0);
+            } else {
+                pa += 2 * ce * co;
+                wa += ce * co;
             }
         }
         pa = warp_sum(pa);
@@ -586,26 +584,27 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
         }
         return;
     }
-    // Only keys that are in a block are grouped: each block head (c == 0: a key
-    // with >= 2 records; else an even key whose partner key is present)
-    // reserves its grouped range with a shared atomic (order is irrelevant);
-    // records of keys in no block are dropped — no pair references them.
-    for (u32 h = threadIdx.x; h < kHsSlots; h += blockDim.x) {
-        const u32 u = tk[h];
-        if (u == kHsEmpty) continue;
+    // Only keys that are in a block are grouped: c == 0, a key with >= 2
+    // records (a diagonal block); else a slot holding both keys of the pair.
+    // A slot reserves one grouped range (order is irrelevant): its even key's
+    // records first, then the odd key's; records of keys in no block are
+    // dropped — no pair references them.
+    for (u32 o = threadIdx.x; o < nocc; o += blockDim.x) {
+        const u32 h = occ[o];
+        const u32 t2 = tc[h];
+        const u32 ce = t2 & 0xffffu, co = t2 >> 16;
+        u32 ne = 0, no = 0;
         if (c == 0) {
-            const u32 cx = tc[h];
-            if (cx < 2) continue;
-            heads[atomicAdd(&s_nheads, 1u)] = h;
-            ts[h] = atomicAdd(&s_cursor, cx);
-        } else if (!(u & 1u)) {
-            const u32 h2 = hs_find(tk, u | 1u);
-            if (h2 == kHsEmpty) continue;
-            heads[atomicAdd(&s_nheads, 1u)] = h;
-            const u32 base = atomicAdd(&s_cursor, tc[h] + tc[h2]);
-            ts[h] = base;
-            ts[h2] = base + tc[h];
+            ne = ce >= 2 ? ce : 0u;
+            no = co >= 2 ? co : 0u;
+            if (ne) heads[atomicAdd(&s_nheads, 1u)] = 2 * h;
+            if (no) heads[atomicAdd(&s_nheads, 1u)] = 2 * h + 1;
+        } else if (ce && co) {
+            ne = ce;
+            no = co;
+            heads[atomicAdd(&s_nheads, 1u)] = 2 * h;
         }
+        ts[h] = (ne + no) ? atomicAdd(&s_cursor, ne + no) : kHsEmpty;
     }
     __syncthreads();
     const u32 nheads = s_nheads, used = s_cursor;
@@ -613,7 +612,16 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
 #pragma unroll
     for (int q = 0; q < kHsPer; ++q) {
         const u32 i = q * blockDim.x + threadIdx.x;
-        if (i < cnt && ts[slot[q]] != kHsEmpty) sg[ts[slot[q]] + rk[q]] = v[q].y;
+        if (i < cnt) {
+            const u32 h = slot[q], base = ts[h];
+            if (base == kHsEmpty) continue;
+            const u32 t2 = tc[h];
+            const u32 ce = t2 & 0xffffu, co = t2 >> 16;
+            const bool odd = v[q].x & 1u;
+            if (c == 0 && (odd ? co : ce) < 2) continue;  // a lone key of a c == 0 run
+            const u32 odd_off = c == 0 ? (ce >= 2 ? ce : 0u) : ce;
+            sg[base + (odd ? odd_off : 0u) + rk[q]] = v[q].y;
+        }
     }
     __syncthreads();
     const u64 off = u64(b) * p;
@@ -621,20 +629,24 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
     const PartMap pm(c);
     auto block_of = [&](u32 t) {
         HeadBlock hb;
-        const u32 h = heads[t];
-        const u32 cx0 = tc[h];
+        const u32 hh = heads[t], h = hh >> 1;
+        const u32 t2 = tc[h];
+        const u32 ce = t2 & 0xffffu, co = t2 >> 16;
+        const u32 base = beg + ts[h];
         if (c == 0) {
-            hb.pairs = u64(cx0) * cx0;
-            hb.work = u64(cx0) * (cx0 - 1) / 2;
-            hb.hs = beg + ts[h]; hb.hc = cx0; hb.ss = hb.hs; hb.sc = cx0; hb.flags = 3u;
+            const bool odd = hh & 1u;
+            const u32 cx = odd ? co : ce;
+            const u32 bx = base + (odd ? (ce >= 2 ? ce : 0u) : 0u);
+            hb.pairs = u64(cx) * cx;
+            hb.work = u64(cx) * (cx - 1) / 2;
+            hb.hs = bx; hb.hc = cx; hb.ss = bx; hb.sc = cx; hb.flags = 3u;
             return hb;
         }
-        const u32 u = tk[h];
-        const u32 h2 = hs_find(tk, u | 1u);
-        const u32 ve = pm.inv(u);
+        const u32 ue = tk[h] << 1;  // the even key of the pair
+        const u32 ve = pm.inv(ue);
         const bool even_x = ve < (ve ^ c);
-        const u32 hx = even_x ? h : h2, hz = even_x ? h2 : h;
-        const u32 bx = beg + ts[hx], cx = tc[hx], bz = beg + ts[hz], cz = tc[hz];
+        const u32 bx = even_x ? base : base + ce, cx = even_x ? ce : co;
+        const u32 bz = even_x ? base + ce : base, cz = even_x ? co : ce;
         hb.pairs = 2ull * cx * cz;
         hb.work = u64(cx) * cz;
         if (cx <= cz) {
@@ -668,9 +680,11 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
                      grouped, sg, beg);
 }
 
-// Dynamic shared memory of the hashed join: keys + counts (+ starts, grouped
-// columns and block heads for the emitting kernel).
-inline size_t part_hash_smem(bool emit) { return size_t(2 * kHsSlots + (emit ? kHsSlots + 2 * kHsCap : 0)) * 4; }
+// Dynamic shared memory of the hashed join: keys + counts + occupied slots
+// (+ starts, grouped columns and block heads for the emitting kernel).
+inline size_t part_hash_smem(bool emit) {
+    return size_t(2 * kHsSlots + kHsCap + (emit ? kHsSlots + 2 * kHsCap : 0)) * 4;
+}
 
 // Partition digits of the hashed path: mean partition <= 0.85 kHsCap (a
 // balanced partition stays below kHsCap by > 6 standard deviations).
