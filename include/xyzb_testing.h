@@ -16,6 +16,11 @@
  *                   transform's fp32 columns; continuous-Y's fp64 set-bit sums)
  *   trace           host-side phase times of dataset creation on stderr
  *   brute_cuda      the CUDA-core exhaustive oracle instead of tcgen05
+ *   binned          1 = the binned verify (binned_verify.cuh) for any binary
+ *                   search it supports, -1 = never (the per-batch verify)
+ *   binned_wshift   z-side windows of 2^value columns (several windows at
+ *                   small p)
+ *   binned_cap      initial window-region capacity in pairs (the regrow path)
  * Returns XYZB_OK, or XYZB_E_DATA for an unknown name.
  */
 #ifndef XYZB_TESTING_H

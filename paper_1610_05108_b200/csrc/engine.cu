@@ -48,6 +48,7 @@
 #include "real_kernels.cuh"
 #include "scan.cuh"
 #include "search_kernels.cuh"
+#include "binned_verify.cuh"
 
 using namespace xyzb;
 
@@ -60,7 +61,7 @@ namespace {
 // the fp32 verify beside the sign-bit one. 0 = the engine's own choice.
 struct TestOptions {
     std::atomic<long long> batch_entries{0}, hit_cap{0}, item_cap{0}, pair_cap{0}, grouping{0}, merge_large{0},
-        sign_verify_off{0}, trace{0}, brute_cuda{0};
+        sign_verify_off{0}, trace{0}, brute_cuda{0}, binned{0}, binned_wshift{0}, binned_cap{0};
 };
 TestOptions& topt() {
     static TestOptions* o = new TestOptions();  // leaked on purpose (outlives static destructors)
@@ -285,6 +286,9 @@ struct xyzb_dataset {
     DevBuf pairs_dev, strengths_dev;
     // top-K over all candidates (topk_kernels.cuh)
     DevBuf tk_state, tk_hist, tk_dhist, tk_sint, tk_table, hits2, tk_cnt2;
+    // binned verify (binned_verify.cuh): per-window regions, bins by x-side tile, cursors
+    DevBuf bin_s1, bin_f, bin_cur1, bin_gh, bin_boff, bin_cur2, bin_zero;
+    u64 bin_hint = 0;  // largest window count seen by a search on this dataset (sizes the regions)
     HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
     StageClock clock;
     u32 hit_cap = 1u << 16;
@@ -745,6 +749,10 @@ struct SearchCtx {
     int tk_level = 0;      // 0: emission target 4K + 256; 1: 64K + 4096; 2: emit everything >= thr
     int tk_shift = 0;      // rank bin shift
     u64 tk_table = 0;      // dedup table slots (power of two)
+    // binned verify (X >> L2): pairs of all batches bucketed by (z window, x tile), verified at the end
+    bool binned = false;
+    int wshift = 0, nkt = 0;
+    u64 nbj = 0, cap_kt = 0, bin_scale = 1;
     RunPlan plan;
     xyzb_result* out;
     u64 launches[XYZB_NUM_STAGES] = {};
@@ -923,13 +931,14 @@ kern::SignStrength sign_strength(SearchCtx& c) {
 // pair-list path picks an emission threshold from the batch's rank histogram
 // and appends the pairs at or above it; then the hit buffer is pruned to the
 // occurrences at or above the K-th distinct key's rank bin.
+void topk_prune(SearchCtx& c, const kern::VerifyArgs& A, u64* launches);
+
 void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, const u32* np, u64* launches,
                       const kern::SignStrength* sg = nullptr, const kern::WeightedQ* wq = nullptr) {
     Nvtx nv("xyzb:topk");
     xyzb_dataset* ds = c.ds;
     cudaStream_t st = ds->stream;
     auto* S = ds->tk_state.as<topk::State>();
-    const int binary = c.mode == XYZB_MODE_BINARY ? 1 : 0;
     if (pair_path) {
         const u64 K = c.q->top_k;
         const u32 target = c.tk_level == 0 ? u32(std::min<u64>(4 * K + 256, 0x7fffffffull))
@@ -957,7 +966,15 @@ void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, c
         XYZB_LAUNCH_CHECK();
         *launches += 1;
     }
-    // prune: distinct keys by rank bin, raise the threshold, keep the occurrences at or above it
+    topk_prune(c, A, launches);
+}
+
+// prune: distinct keys by rank bin, raise the threshold, keep the occurrences at or above it
+void topk_prune(SearchCtx& c, const kern::VerifyArgs& A, u64* launches) {
+    xyzb_dataset* ds = c.ds;
+    cudaStream_t st = ds->stream;
+    auto* S = ds->tk_state.as<topk::State>();
+    const int binary = c.mode == XYZB_MODE_BINARY ? 1 : 0;
     XYZB_CUDA(cudaMemsetAsync(ds->tk_table.p, 0xff, c.tk_table * 8, st));
     XYZB_CUDA(cudaMemsetAsync(ds->tk_cnt2.p, 0, 4, st));
     topk::prune_insert<<<grid_for(ds->hit_cap, 256, kSMs * 4), 256, 0, st>>>(
@@ -974,6 +991,97 @@ void topk_after_batch(SearchCtx& c, bool pair_path, const kern::VerifyArgs& A, c
                                                                           ds->tk_cnt2.as<u32>(), A.hits, A.hit_count);
     XYZB_LAUNCH_CHECK();
     *launches += 4;
+}
+
+// Binned verify (binned_verify.cuh), after every batch's pairs sit in their
+// z-side windows: bins by x-side tile (counting sort), then one persistent
+// verify per window; top-K over all candidates treats each window like a
+// batch (the first window writes ranks, emits at E, prunes; later windows
+// append at or above the running threshold).
+void binned_verify(SearchCtx& c) {
+    xyzb_dataset* ds = c.ds;
+    cudaStream_t st = ds->stream;
+    StageClock& clk = ds->clock;
+    const u32 nbj = static_cast<u32>(c.nbj);
+    const int nkt = c.nkt;
+    const u32 chunks = static_cast<u32>(ceil_div(c.cap_kt, bins::kChunk2));
+    cudaEvent_t e0 = clk.mark();
+    XYZB_CUDA(cudaMemsetAsync(ds->bin_gh.p, 0, u64(nkt) * nbj * 4, st));
+    func_smem(bins::bin_hist2, size_t(nbj) * 4);
+    bins::bin_hist2<<<kSMs * 2, bins::kScatterThreads, size_t(nbj) * 4, st>>>(
+        ds->bin_s1.as<u64>(), c.cap_kt, ds->bin_cur1.as<u32>(), nkt, chunks, nbj, ds->bin_gh.as<u32>());
+    XYZB_LAUNCH_CHECK();
+    bins::bin_scan2<<<nkt, 1024, 0, st>>>(ds->bin_gh.as<u32>(), nbj, ds->bin_boff.as<u32>(), ds->bin_cur2.as<u32>());
+    XYZB_LAUNCH_CHECK();
+    func_smem(bins::bin_scatter2, size_t(nbj) * 8);
+    bins::bin_scatter2<<<kSMs, bins::kScatterThreads, size_t(nbj) * 8, st>>>(
+        ds->bin_s1.as<u64>(), c.cap_kt, ds->bin_cur1.as<u32>(), nkt, chunks, nbj, ds->bin_cur2.as<u32>(),
+        ds->bin_f.as<u64>());
+    XYZB_LAUNCH_CHECK();
+    c.launches[XYZB_STAGE_JOIN] += 3;
+    clk.span(XYZB_STAGE_JOIN, e0, clk.mark());
+    bins::BinVerifyArgs A;
+    A.Xc = ds->Xc.as<u64>();
+    A.Wp = static_cast<u32>(ds->Wp);
+    A.Yw = ds->yk_bits.as<u64>();
+    A.n = static_cast<u32>(c.n);
+    A.astar = c.astar;
+    A.p = c.p;
+    A.nbj = nbj;
+    A.rid = ds->rid.as<u32>();
+    A.hits = ds->hits.as<kern::DevHit>();
+    A.hit_count = ds->hit_count.as<u32>();
+    A.hit_cap = ds->hit_cap;
+    A.krows = ds->rows.as<u32>();
+    A.kM = static_cast<int>(c.M);
+    A.sint_out = c.topk_all ? ds->tk_sint.as<u32>() : nullptr;
+    A.rank_thr = c.topk_all ? &ds->tk_state.as<topk::State>()->thr : nullptr;
+    const int ns = static_cast<int>(ceil_div(ds->Wp / 2, 16));
+    const size_t smem = bins::verify_smem(A.Wp);
+    const bool full = ds->Wp / 2 == u64(16 * ns);  // every lane's slices inside the column
+    auto* vk = ns <= 1 ? (full ? bins::verify_binned<1, true> : bins::verify_binned<1, false>)
+             : ns == 2 ? (full ? bins::verify_binned<2, true> : bins::verify_binned<2, false>)
+             : ns == 3 ? (full ? bins::verify_binned<3, true> : bins::verify_binned<3, false>)
+             : ns == 4 ? (full ? bins::verify_binned<4, true> : bins::verify_binned<4, false>)
+                       : (full ? bins::verify_binned<5, true> : bins::verify_binned<5, false>);
+    func_smem(vk, smem);
+    // the prune reads the hit buffer through VerifyArgs
+    kern::VerifyArgs PA{};
+    PA.hits = A.hits;
+    PA.hit_count = A.hit_count;
+    PA.hit_cap = A.hit_cap;
+    for (int kt = 0; kt < nkt; ++kt) {
+        Nvtx nv_verify("xyzb:verify");
+        A.F = ds->bin_f.as<u64>() + u64(kt) * c.cap_kt;
+        A.boff = ds->bin_boff.as<u32>() + u64(kt) * (nbj + 1);
+        cudaEvent_t ev0 = clk.mark();
+        vk<<<kSMs, bins::kVerifyThreads, smem, st>>>(A);
+        XYZB_LAUNCH_CHECK();
+        c.launches[XYZB_STAGE_VERIFY] += 1;
+        cudaEvent_t ev1 = clk.mark();
+        clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
+        c.verify_spans.push_back({ev0, ev1});
+        if (c.topk_all) {
+            Nvtx nv("xyzb:topk");
+            auto* S = ds->tk_state.as<topk::State>();
+            const u64 K = c.q->top_k;
+            const u32 target = c.tk_level == 0 ? u32(std::min<u64>(4 * K + 256, 0x7fffffffull))
+                                               : u32(std::min<u64>(64 * K + 4096, 0x7fffffffull));
+            const u32* cnt = A.boff + nbj;  // the window's pair count
+            topk::rank_hist<<<kSMs * 2, 512, 0, st>>>(ds->tk_sint.as<u32>(), cnt, static_cast<u32>(c.cap_kt),
+                                                      ds->bin_zero.as<u32>(), 1u, S, c.tk_shift,
+                                                      ds->tk_hist.as<u32>());
+            XYZB_LAUNCH_CHECK();
+            topk::emit_select<<<1, 1024, 0, st>>>(ds->tk_hist.as<u32>(), c.tk_shift, target, S, c.tk_level >= 2);
+            XYZB_LAUNCH_CHECK();
+            bins::emit_binned<<<kSMs * 8, 256, 0, st>>>(A.F, ds->tk_sint.as<u32>(), cnt, S, A.rid, A.krows, A.kM,
+                                                        A.Xc, A.Wp, A.hits, A.hit_count, A.hit_cap, A.n);
+            XYZB_LAUNCH_CHECK();
+            c.launches[XYZB_STAGE_MERGE] += 3;
+            topk_prune(c, PA, &c.launches[XYZB_STAGE_MERGE]);
+            clk.span(XYZB_STAGE_MERGE, ev1, clk.mark());
+        }
+    }
 }
 
 template <class K>
@@ -1090,6 +1198,38 @@ void run_batches(SearchCtx& c) {
         if (c.topk_all) ds->tk_sint.ensure(c.pair_cap * 4);
         ds->npairs.ensure(nbatches * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->npairs.p, 0, nbatches * 4, st));
+    }
+    // binned verify (binned_verify.cuh): binary columns of <= 80 16-byte slices, X much larger than L2
+    {
+        const long long bsel = topt().binned.load();  // 1 forces it (tests), -1 disables it
+        const bool ok = c.mode == XYZB_MODE_BINARY && pair_path && !sign_pairs && !weighted_pairs &&
+                        ds->Wp / 2 <= 80 && p <= (u64(1) << 20) && R < (u64(1) << bins::kRunBits);
+        c.binned = ok && (bsel == 1 || (bsel == 0 && p * ds->Wp * 8 >= (u64(512) << 20)));
+    }
+    if (c.binned) {
+        int ws = 20;  // z-side windows of ~84 MB (L2-resident while their bins are verified)
+        while (ws > 10 && (u64(1) << ws) * ds->Wp * 8 > (u64(88) << 20)) --ws;
+        if (const long long w = topt().binned_wshift.load()) ws = static_cast<int>(w);
+        while (ceil_div(p, u64(1) << ws) > 256) ++ws;
+        c.wshift = ws;
+        c.nkt = static_cast<int>(ceil_div(p, u64(1) << ws));
+        c.nbj = ceil_div(p, bins::kBinJT);
+        // region capacity: the dataset's largest window count so far (+25 %), else the batches' pair capacity
+        const u64 est = ds->bin_hint ? ds->bin_hint + ds->bin_hint / 4 + 4096 : ceil_div(nbatches * c.pair_cap, c.nkt);
+        c.cap_kt = std::min<u64>(0xffffffffull, est * c.bin_scale);
+        if (const long long cap = topt().binned_cap.load())  // tests force the region regrow path
+            if (c.bin_scale == 1) c.cap_kt = std::max<u64>(1, u64(cap));
+        const u64 nk = u64(c.nkt);
+        ds->bin_s1.ensure(nk * c.cap_kt * 8);
+        ds->bin_f.ensure(nk * c.cap_kt * 8);
+        ds->bin_cur1.ensure(nk * 4);
+        ds->bin_gh.ensure(nk * c.nbj * 4);
+        ds->bin_boff.ensure(nk * (c.nbj + 1) * 4);
+        ds->bin_cur2.ensure(nk * c.nbj * 4);
+        ds->bin_zero.ensure(4);
+        XYZB_CUDA(cudaMemsetAsync(ds->bin_cur1.p, 0, nk * 4, st));
+        XYZB_CUDA(cudaMemsetAsync(ds->bin_zero.p, 0, 4, st));
+        if (c.topk_all) ds->tk_sint.ensure(c.cap_kt * 4);
     }
     const u32 hmax = 8u;  // held columns per item (pair expansion chunks)
     // Grouping + join, by the run's bucket space 2^M against p:
@@ -1355,6 +1495,15 @@ void run_batches(SearchCtx& c) {
             c.launches[XYZB_STAGE_JOIN] += 1;
             cudaEvent_t ev0 = clk.mark();
             clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
+            if (c.binned) {  // the batch's pairs go to their z-side windows; verified after the last batch
+                bins::bin_scatter1<<<kSMs * 4, bins::kS1Threads, 0, st>>>(
+                    ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), A.nitems, A.item_cap,
+                    static_cast<u32>(b0), rsign, c.wshift, c.nkt, ds->bin_s1.as<u64>(), c.cap_kt, ds->bin_cur1.as<u32>());
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_JOIN] += 1;
+                clk.span(XYZB_STAGE_JOIN, ev0, clk.mark());
+                continue;
+            }
             if (sign_pairs) {
                 const kern::SignStrength g = sign_strength(c);
                 kern::verify_pairs_sign<kern::kSignQB><<<vgrid, 256, 0, st>>>(A, ds->pairs.as<kern::PairRec>(), np,
@@ -1486,6 +1635,7 @@ void run_batches(SearchCtx& c) {
             clk.span(XYZB_STAGE_MERGE, e4, clk.mark());
         }
     }
+    if (c.binned) binned_verify(c);
 }
 
 // Top-K over all candidates: the merged list holds every first occurrence at
@@ -1860,7 +2010,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         // status block (pinned): H, merge counts, items and pairs per batch, per-run counters
         const size_t o_cnt = 8, o_items = 16, o_pairs = o_items + 4 * nbt, o_enum = round_up(o_pairs + 4 * nbt, 8),
                      o_ver = o_enum + 8 * Rall, o_ovf = o_ver + 8 * Rall, o_tk = o_ovf + 8,
-                     sbytes = o_tk + sizeof(topk::State);
+                     o_bin = round_up(o_tk + sizeof(topk::State), 8), sbytes = o_bin + 4 * u64(c.nkt) + 8;
         ds->h_status.ensure(sbytes);
         char* hs = ds->h_status.as<char>();
         XYZB_CUDA(cudaMemcpyAsync(hs, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
@@ -1874,6 +2024,8 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         if (c.topk_all)
             XYZB_CUDA(cudaMemcpyAsync(hs + o_tk, ds->tk_state.p, sizeof(topk::State), cudaMemcpyDeviceToHost,
                                       ds->stream));
+        if (c.binned)
+            XYZB_CUDA(cudaMemcpyAsync(hs + o_bin, ds->bin_cur1.p, 4 * u64(c.nkt), cudaMemcpyDeviceToHost, ds->stream));
         tr.mark("search:launch");
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         tr.mark("search:device");
@@ -1893,6 +2045,14 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                 c.pair_scale *= std::max<u64>(2, ceil_div(pneed, c.pair_cap));
             }
         }
+        bool bin_redo = false;
+        if (c.binned) {  // a window region overflowed: size the regions from the counts seen and redo
+            const u32* cur = reinterpret_cast<const u32*>(hs + o_bin);
+            const u64 mx = *std::max_element(cur, cur + c.nkt);
+            ds->bin_hint = mx;
+            bin_redo = mx > c.cap_kt;
+            if (bin_redo) c.bin_scale = 2;
+        }
         const bool povf = *reinterpret_cast<const u32*>(hs + o_ovf) != 0;
         if (povf) c.no_hash = true;  // a hashed partition overflowed: redo on the sorted path
         bool tk_redo = false;
@@ -1908,7 +2068,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                 tk_redo = true;
             }
         }
-        if (!povf && !tk_redo && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
+        if (!povf && !tk_redo && !bin_redo && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
             std::memcpy(enumerated.data(), hs + o_enum, Rall * 8);
             std::memcpy(verified.data(), hs + o_ver, Rall * 8);
             if (c.pair_cap) {  // the pair list (16 B per canonical pair) is written by the join
@@ -1916,6 +2076,8 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                 u64 tot = 0;
                 for (u64 b = 0; b < nbt; ++b) tot += np[b];
                 c.bytes[c.pairs_in_sort ? XYZB_STAGE_SORT : XYZB_STAGE_JOIN] += 16 * tot;
+                // binned: level 1 reads 16 B and writes 8 B per pair, level 2 reads 8 B three times and writes 8 B
+                if (c.binned) c.bytes[XYZB_STAGE_JOIN] += 56 * tot;
                 if (c.topk_all) c.bytes[XYZB_STAGE_MERGE] += 8 * tot;  // pair ranks read by the histogram + emission
             }
             break;
@@ -3096,6 +3258,9 @@ int xyzb_test_set_option(const char* name, long long value) {
                                    : s == "sign_verify_off" ? &o.sign_verify_off
                                    : s == "trace"           ? &o.trace
                                    : s == "brute_cuda"      ? &o.brute_cuda
+                                   : s == "binned"          ? &o.binned
+                                   : s == "binned_wshift"   ? &o.binned_wshift
+                                   : s == "binned_cap"      ? &o.binned_cap
                                                             : nullptr;
     if (!slot) return XYZB_E_DATA;
     slot->store(value);

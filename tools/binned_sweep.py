@@ -1,0 +1,33 @@
+"""Measurement (round 2): config 4's binned verify under window sizes and L2
+eviction policies (engine test options binned_wshift / binned_policy);
+device time of one search, best of 3, and the verify's share."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from paper_1610_05108_b200 import _lib  # noqa: E402
+
+bench.select("large")
+import paper_1610_05108_b200 as xb  # noqa: E402
+
+x, y, _ = bench.make_data()
+cfg = bench.search_config(bench.WORKLOAD["l"])
+ds = xb.Dataset(x)
+ds.search(y, cfg)
+ref = None
+for ws in [int(a) for a in sys.argv[1].split(",")]:
+    for pol in [int(a) for a in sys.argv[2].split(",")]:
+        _lib.set_test_option("binned_wshift", ws)
+        pass
+        best = None
+        for _ in range(3):
+            r = ds.search(y, cfg)
+            if best is None or r.device_ms < best.device_ms:
+                best = r
+        key = [(h.j, h.k, h.strength, h.found_at_repetition) for h in best.top_hits()]
+        ref = ref or key
+        print(f"wshift {ws} policy {pol}: {best.device_ms:.2f} ms  verify {best.stage_ms['verify']:.2f}  "
+              f"join {best.stage_ms['join']:.2f}  same top-K {key == ref}", flush=True)

@@ -40,11 +40,12 @@ def reduce(args):
         hdr.index("Metric Unit")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
              "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
-    tot = {"dram__bytes_read.sum": 0.0, "dram__bytes_write.sum": 0.0, "gpu__time_duration.sum": 0.0}
+    tot = {"dram__bytes_read.sum": 0.0, "dram__bytes_write.sum": 0.0, "gpu__time_duration.sum": 0.0,
+           "lts__t_bytes.sum": 0.0}
     launches = 0
     kernel = ""
     for r in rows[1:]:
-        if "verify_pairs" not in r[ki]:
+        if "verify_pairs" not in r[ki] and "verify_binned" not in r[ki]:
             continue
         m = r[mi]
         if m in tot:
