@@ -26,6 +26,9 @@ gwas|toy|cont|lasso|brute` selects configs 2, 1, 3, 5 and the exhaustive oracle.
             launches / their CUDA-event time, against MEASURED_PEAKS hbm_gbs;
             `algorithmic` beside it: 2 columns per canonical candidate + Y
             (SURVEY 8d), which L2 partly serves (columns shared inside a block).
+            Config 4's binned verify reads one column per pair through L2 and
+            one from shared memory: `l2_roofline` holds its L2 rate against a
+            live gather probe on a window-sized X.
   cpu_baseline  the reference CPU path (oracle/_ref, unmodified reference core)
             on a bounded sample of the same workload, rank 0, N=1.
 
@@ -73,7 +76,8 @@ STAGE_BOUND = {"project": "hbm/l2: M row-plane words read + keys written",
                        "fused group + join kernel (configs 1-2: issue-bound, shared-memory atomics)",
                "join": "partition join (config 4: records read twice, pair list written) or the pair expansion of "
                        "large blocks",
-               "verify": "hbm gather (config 4: X 1.256 GB >> L2); l2 gather when X fits in L2 (see l2_roofline)",
+               "verify": "config 4: binned verify (x tile in shared memory, z column from the L2-resident window; "
+                         "see l2_roofline); config 2: l2 gather (X resident)",
                "merge": "top-K over all candidates: rank histogram, emission, distinct-key prune per batch + the "
                         "final merge"}
 E2E_INFLIGHT = 4  # (X, y) jobs in flight in the end-to-end measurement (tools/e2e_pipeline.py: 1-4 measured)
@@ -228,6 +232,15 @@ def gather_peak(device, ncols, words):
         return g.value if rc == 0 else None
     except OSError:
         return None
+
+
+def binned_verify():
+    """The engine's binned verify runs for binary X of >= 512 MB with columns of <= 80 16-byte slices
+    (engine.cu, run_batches): config 4."""
+    words = (WORKLOAD["n"] + 63) // 64
+    wp = (words + 3) // 4 * 4
+    return WORKLOAD["mode"] == "binary" and WORKLOAD["p"] * wp * 8 >= (512 << 20) and wp // 2 <= 80 \
+        and WORKLOAD["p"] <= (1 << 20)
 
 
 def ncu_traffic():
@@ -550,7 +563,9 @@ def main():
         alg = (verify_bytes / verify_launches) / ((verify_ms / verify_launches) / 1e3) / 1e9 if verify_launches \
             else 0.0
         traffic = ncu_traffic()
-        kern_name = ("verify_pairs_simple (pair-list verify)" if WORKLOAD["mode"] == "binary" else
+        binned = binned_verify()
+        kern_name = ("verify_binned (x tile in shared memory, z window in L2)" if binned else
+                     "verify_pairs_simple (pair-list verify)" if WORKLOAD["mode"] == "binary" else
                      "verify_items_sign (sign bits x response bit planes)" if WORKLOAD.get("transform") == "sign"
                      else "verify_items_real<RealStrength>")
         roof = {"bound": "hbm", "kernel": kern_name, "peak": hbm, "peak_source": src, "unit": "GB/s",
@@ -558,6 +573,21 @@ def main():
                                 "bytes_per_launch": verify_bytes / max(1, verify_launches),
                                 "note": "2 columns per canonical candidate + Y (SURVEY 8d); L2 serves the columns a "
                                         "block's pairs share, so this exceeds the DRAM rate"}}
+        if binned and verify_launches:
+            # binned verify: per pair one column through L2 (the z window) + one 8-byte record; the x tile is in
+            # shared memory. Its ceiling is the L2 -> SM gather rate, measured live on an X of one window's size.
+            words = (WORKLOAD["n"] + 63) // 64
+            wcols = 1 << 16
+            g = gather_peak(local, wcols, words)
+            col = ((words + 3) // 4 * 4) * 8
+            l2_bytes = (verified_mine / verify_launches) * (col + 8)
+            ach_l2 = l2_bytes / ((verify_ms / verify_launches) / 1e3) / 1e9
+            l2_roof = {"bound": "l2 (z window resident, x tile in shared memory)", "kernel": kern_name,
+                       "achieved": ach_l2, "peak": g, "unit": "GB/s", "frac": ach_l2 / g if g else None,
+                       "bytes_per_launch": l2_bytes,
+                       "note": "1 column + 1 record per pair through L2 over the launch's CUDA-event time",
+                       "peak_source": f"measured live: random column-pair gather + XOR-popcount probe on an X of "
+                                      f"{wcols} columns x {col} B (one window; paper_1610_05108_b200/csrc/probe.cu)"}
         if traffic and traffic.get("dram_bytes_per_pair") and verify_launches:
             dram_launch = traffic["dram_bytes_per_pair"] * (verified_mine / verify_launches)
             ach = dram_launch / ((verify_ms / verify_launches) / 1e3) / 1e9

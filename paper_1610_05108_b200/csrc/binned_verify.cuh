@@ -5,27 +5,35 @@
 //
 // The per-batch verify reads both columns of a candidate from DRAM (~1.29
 // columns per pair, the in-block reuse limit). Here the
-// search's canonical pairs are instead collected over ALL batches and
-// bucketed by (kt, jt): kt = the z-side column's window of 2^wshift columns
-// (sized to stay L2-resident, ~84 MB), jt = the x-side column's tile of
-// kBinJT columns. The verify walks the bins kt-major with one persistent
+// search's canonical pairs are instead collected over ALL batches into bins
+// (kt, jt): kt = the z-side column's window of 2^wshift columns (sized to
+// stay L2-resident, ~84 MB), jt = the x-side column's tile of kBinJT
+// columns. The verify walks the bins kt-major with one persistent
 // 1024-thread CTA per SM: the bin's x-side tile sits in shared memory
 // (cp.async, double-buffered, pre-XORed with Y), the z-side columns come
 // from the current window in L2 (evict_last). Per pair: one column from L2,
-// one from shared memory; DRAM reads ~ one window pass + one tile pass per
-// window (tools/tile_probe.cu: 3.9e8 random pairs in 50 ms against 85-98 ms
-// for DRAM gathers).
+// one from shared memory; DRAM ~ one window pass + one tile pass per window
+// (tools/tile_probe.cu; ncu: 275 DRAM bytes per pair against 1619).
+//
+// Two steps put the pairs in bins: per batch, each pair is appended to its
+// bucket (window, tile >> 7; 2048 buckets at config 4, fixed capacity from
+// the previous search's mean fill, one global reservation per CTA chunk and
+// bucket); after the last batch, one CTA per bucket splits it by the tile's
+// low 7 bits. A pair whose bucket is full goes to an overflow list, verified
+// afterwards by a plain gather; an overflowing list makes the host redo the
+// search with a larger one.
 //
 // Pair records (u64): x-side column (24 bits) | z-side column (24) | diagonal
 // flag (1, at bit 48) | the run's pass is negative (1, bit 49) | global run
 // index in execution order (14, at bit 50).
-//   bin_scatter1  (per batch)  the batch's pair list -> per-window regions
-//   bin_hist2 / bin_scan2 / bin_scatter2 (end of the search)  each window's
-//                 region -> bins by x-side tile (counting sort, shared
-//                 histograms, one global reservation per (chunk, bin))
+//   bin_append   (per batch)  the batch's pair list -> buckets (or the overflow list)
+//   bin_sort     (end)        each bucket -> its 128 tiles' runs
+//   bin_scan     (end)        per window, exclusive offsets of the tile fills
+//                             (compact rank indices for the top-K first phase)
 //   verify_binned (per window) strengths; hits (or, top-K first phase, the
 //                 rank of every pair) exactly as verify_pairs_simple
-//   emit_binned   top-K first phase: append the pairs at or above E
+//   verify_list  the overflow list (warp per pair)
+//   emit_bins / emit_list  top-K first phase: append the pairs at or above E
 #pragma once
 
 #include "common.cuh"
@@ -41,8 +49,6 @@ using kern::PairRec;
 constexpr int kBinJT = 64;           // x-side columns per tile (shared memory: 64 x 1280 B at n = 1e4)
 constexpr int kBinJTShift = 6;
 constexpr int kVerifyThreads = 1024;  // one CTA per SM
-constexpr int kScatterThreads = 1024;
-constexpr u32 kChunk2 = 131072;       // records per level-2 chunk (8 per bin at p = 1e6)
 constexpr int kColBits = 24;          // columns < 2^24
 constexpr int kRunBits = 14;          // runs < 2^14 per search
 
@@ -55,86 +61,169 @@ __device__ __forceinline__ u32 rec_diag(u64 r) { return u32(r >> 48) & 1u; }
 __device__ __forceinline__ u32 rec_neg(u64 r) { return u32(r >> 49) & 1u; }
 __device__ __forceinline__ u32 rec_run(u64 r) { return u32(r >> 50); }
 
-// ---- level 1: a batch's pair list -> per-window regions (kt = z column >> wshift) ----
-// CTA chunks of 8 records per thread; shared counts per window, one global
-// reservation per (chunk, window); a region past its capacity raises the
-// cursor beyond cap (the host regrows and redoes the search).
-constexpr int kS1Threads = 256, kS1PerThread = 8;
-__global__ void __launch_bounds__(kS1Threads) bin_scatter1(const PairRec* __restrict__ pairs,
-                                                           const u32* __restrict__ npairs, u32 pair_cap,
-                                                           const u32* __restrict__ nitems, u32 item_cap, u32 run0,
-                                                           const int8_t* __restrict__ run_sign, int wshift, int nkt, u64* __restrict__ S1, u64 cap_kt,
-                                                           u32* __restrict__ cur1) {
-    __shared__ u32 h[256];
-    __shared__ u32 base[256];
+// ---- per batch: the pair list -> buckets (window, x-side tile >> 7) ----
+// A CTA takes chunks of kAppendChunk records: shared counts per bucket, one
+// global reservation per (chunk, bucket) (~16 records each at config 4), a
+// second sweep over the (L2-resident) chunk writes each record at its
+// bucket's reserved run. A full bucket sends the record to the overflow list.
+constexpr int kHiBits = 7;                  // x-side tiles per bucket: 128
+constexpr u32 kMaxBuckets = 4096;           // windows x buckets per window (shared counters)
+constexpr u32 kAppendChunk = 32768;
+constexpr int kAppendThreads = 512, kAppendPerThread = 8;
+constexpr u32 kMaxRunsPerBatch = 4096;      // a batch's run signs in shared memory
+
+__device__ __forceinline__ u32 bucket_of(u32 pa, u32 pb, int wshift, u32 nbh) {
+    return (pb >> wshift) * nbh + (pa >> (kBinJTShift + kHiBits));
+}
+
+__global__ void __launch_bounds__(kAppendThreads) bin_append(const PairRec* __restrict__ pairs,
+                                                             const u32* __restrict__ npairs, u32 pair_cap,
+                                                             const u32* __restrict__ nitems, u32 item_cap, u32 run0,
+                                                             const int8_t* __restrict__ run_sign, u32 nruns,
+                                                             int wshift, u32 nbh, u32 nbuckets, u64* __restrict__ B,
+                                                             u32 cap_bucket, u32* __restrict__ bcnt,
+                                                             u64* __restrict__ ovf, u32 ovf_cap,
+                                                             u32* __restrict__ ovf_n) {
+    constexpr int R = kAppendPerThread;
+    constexpr u32 STEP = kAppendThreads * R;  // records in flight per CTA sweep step
+    __shared__ u32 cnt[kMaxBuckets], base[kMaxBuckets];
+    __shared__ int8_t neg[kMaxRunsPerBatch];
     const u32 P = topk::batch_pairs(npairs, pair_cap, nitems, item_cap);
-    constexpr u32 CH = kS1Threads * kS1PerThread;
-    for (u32 i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    for (u32 t = threadIdx.x; t < nbuckets; t += blockDim.x) cnt[t] = 0;
+    for (u32 t = threadIdx.x; t < nruns; t += blockDim.x) neg[t] = run_sign[t] < 0 ? 1 : 0;
     __syncthreads();
-    for (u64 c0 = u64(blockIdx.x) * CH; c0 < P; c0 += u64(gridDim.x) * CH) {
-        u64 rec[kS1PerThread];
-        u32 kt[kS1PerThread], rk[kS1PerThread];
+    const uint4* P4 = reinterpret_cast<const uint4*>(pairs);
+    for (u64 c0 = u64(blockIdx.x) * kAppendChunk; c0 < P; c0 += u64(gridDim.x) * kAppendChunk) {
+        const u64 c1 = minu(P, c0 + kAppendChunk);
+        // sweep 1: bucket counts (R records in flight per thread)
+        for (u64 s0 = c0; s0 < c1; s0 += STEP) {
+            uint2 ab[R];
 #pragma unroll
-        for (int u = 0; u < kS1PerThread; ++u) {
-            const u64 i = c0 + u64(u) * kS1Threads + threadIdx.x;
-            kt[u] = 0xffffffffu;
-            if (i < P) {
-                const PairRec pr = pairs[i];
-                rec[u] = rec_make(pr.pa, pr.pb, (pr.pad >> 1) & 1u, run_sign[pr.run] < 0 ? 1u : 0u, run0 + pr.run);
-                kt[u] = pr.pb >> wshift;
-                rk[u] = atomicAdd(&h[kt[u]], 1u);
+            for (int u = 0; u < R; ++u) {
+                const u64 i = s0 + u64(u) * kAppendThreads + threadIdx.x;
+                ab[u] = i < c1 ? __ldg(reinterpret_cast<const uint2*>(pairs + i)) : make_uint2(0xffffffffu, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < R; ++u)
+                if (ab[u].x != 0xffffffffu) atomicAdd(&cnt[bucket_of(ab[u].x, ab[u].y, wshift, nbh)], 1u);
+        }
+        __syncthreads();
+        for (u32 t = threadIdx.x; t < nbuckets; t += blockDim.x) {
+            const u32 c = cnt[t];
+            base[t] = c ? atomicAdd(bcnt + t, c) : 0u;
+            cnt[t] = 0;  // reused as the chunk's rank counters
+        }
+        __syncthreads();
+        // sweep 2: records to their bucket runs
+        for (u64 s0 = c0; s0 < c1; s0 += STEP) {
+            uint4 pr[R];
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const u64 i = s0 + u64(u) * kAppendThreads + threadIdx.x;
+                pr[u] = i < c1 ? __ldg(P4 + i) : make_uint4(0xffffffffu, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                if (pr[u].x == 0xffffffffu) continue;
+                const u32 bk = bucket_of(pr[u].x, pr[u].y, wshift, nbh);
+                const u64 rec = rec_make(pr[u].x, pr[u].y, (pr[u].w >> 1) & 1u, neg[pr[u].z], run0 + pr[u].z);
+                const u32 pos = base[bk] + atomicAdd(&cnt[bk], 1u);
+                if (pos < cap_bucket) {
+                    B[u64(bk) * cap_bucket + pos] = rec;
+                } else {
+                    const u32 o = atomicAdd(ovf_n, 1u);
+                    if (o < ovf_cap) ovf[o] = rec;
+                }
             }
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < nkt; t += blockDim.x) {
-            const u32 cnt = h[t];
-            base[t] = cnt ? atomicAdd(cur1 + t, cnt) : 0u;
-            h[t] = 0;
-        }
+        for (u32 t = threadIdx.x; t < nbuckets; t += blockDim.x) cnt[t] = 0;
         __syncthreads();
+    }
+}
+
+// ---- end of the search: each bucket sorted by the low 7 bits of its x-side tile ----
+// One CTA per bucket: counts per tile (shared), the tiles' starts, then the
+// records scattered into their tile's run (order within a tile immaterial).
+// bstart / bfill: per (window, tile), relative to the window's first bucket.
+__global__ void __launch_bounds__(1024) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
+                                                 const u32* __restrict__ bcnt, u32 nbh, u32 nbj,
+                                                 u64* __restrict__ D, u32* __restrict__ bstart,
+                                                 u32* __restrict__ bfill) {
+    constexpr u32 T = 1u << kHiBits;
+    constexpr int R = 8;
+    constexpr u32 STEP = 1024 * R;
+    __shared__ u32 h[T], st[T];
+    const u32 bk = blockIdx.x;
+    const u32 kt = bk / nbh, hi = bk % nbh;
+    const u32 cnt = min(bcnt[bk], cap_bucket);
+    const u64* src = B + u64(bk) * cap_bucket;
+    if (threadIdx.x < T) h[threadIdx.x] = 0;
+    __syncthreads();
+    for (u32 s0 = 0; s0 < cnt; s0 += STEP) {
+        u64 r[R];
 #pragma unroll
-        for (int u = 0; u < kS1PerThread; ++u) {
-            if (kt[u] == 0xffffffffu) continue;
-            const u64 pos = u64(base[kt[u]]) + rk[u];
-            if (pos < cap_kt) S1[u64(kt[u]) * cap_kt + pos] = rec[u];
+        for (int u = 0; u < R; ++u) {
+            const u32 i = s0 + u * 1024 + threadIdx.x;
+            r[u] = i < cnt ? __ldg(src + i) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+            if (r[u] != ~0ull) atomicAdd(&h[(rec_a(r[u]) >> kBinJTShift) & (T - 1)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of 128 counts, 4 per lane
+        const int lane = threadIdx.x;
+        u32 c[4], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            c[q] = h[lane * 4 + q];
+            tot += c[q];
+        }
+        u32 incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        u32 ex = incl - tot;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            st[lane * 4 + q] = ex;
+            ex += c[q];
         }
     }
-}
-
-// ---- level 2: each window's region -> bins by x-side tile ----
-// Work items (window, chunk) flattened window-major; chunks past the region's
-// count are skipped. hist: per-chunk shared counts added to gh[kt][jt].
-__global__ void __launch_bounds__(kScatterThreads) bin_hist2(const u64* __restrict__ S1, u64 cap_kt,
-                                                             const u32* __restrict__ cur1, int nkt, u32 chunks_per_kt,
-                                                             u32 nbj, u32* __restrict__ gh) {
-    extern __shared__ u32 h2[];
-    for (u32 w = blockIdx.x; w < u32(nkt) * chunks_per_kt; w += gridDim.x) {
-        const u32 kt = w / chunks_per_kt, ch = w % chunks_per_kt;
-        const u64 cnt = minu(cur1[kt], cap_kt);
-        const u64 r0 = u64(ch) * kChunk2;
-        if (r0 >= cnt) continue;  // uniform over the CTA
-        const u64 r1 = minu(cnt, r0 + kChunk2);
-        for (u32 i = threadIdx.x; i < nbj; i += blockDim.x) h2[i] = 0;
-        __syncthreads();
-        const u64* src = S1 + u64(kt) * cap_kt;
-        for (u64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicAdd(&h2[rec_a(src[i]) >> kBinJTShift], 1u);
-        __syncthreads();
-        u32* g = gh + u64(kt) * nbj;
-        for (u32 i = threadIdx.x; i < nbj; i += blockDim.x)
-            if (h2[i]) atomicAdd(g + i, h2[i]);
-        __syncthreads();
+    __syncthreads();
+    if (threadIdx.x < T) {
+        const u32 jt = hi * T + threadIdx.x;
+        if (jt < nbj) {
+            bstart[u64(kt) * nbj + jt] = hi * cap_bucket + st[threadIdx.x];
+            bfill[u64(kt) * nbj + jt] = h[threadIdx.x];
+        }
+        h[threadIdx.x] = st[threadIdx.x];  // cursors
+    }
+    __syncthreads();
+    u64* dst = D + u64(bk) * cap_bucket;
+    for (u32 s0 = 0; s0 < cnt; s0 += STEP) {
+        u64 r[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const u32 i = s0 + u * 1024 + threadIdx.x;
+            r[u] = i < cnt ? __ldg(src + i) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+            if (r[u] != ~0ull) dst[atomicAdd(&h[(rec_a(r[u]) >> kBinJTShift) & (T - 1)], 1u)] = r[u];
     }
 }
 
-// One CTA per window: exclusive scan of its bin counts -> boff[kt][0..nbj]
-// (boff[kt][nbj] = the window's total) and the scatter cursors.
-__global__ void __launch_bounds__(1024) bin_scan2(const u32* __restrict__ gh, u32 nbj, u32* __restrict__ boff,
-                                                  u32* __restrict__ cur2) {
+// One CTA per window: exclusive scan of the tiles' fills -> boff[kt][0..nbj]
+// (compact rank indices; boff[kt][nbj] = the window's pairs held in buckets).
+__global__ void __launch_bounds__(1024) bin_scan(const u32* __restrict__ fill, u32 nbj, u32* __restrict__ boff) {
     __shared__ u32 ws[33];
     const u32 kt = blockIdx.x;
-    const u32* g = gh + u64(kt) * nbj;
+    const u32* g = fill + u64(kt) * nbj;
     u32* bo = boff + u64(kt) * (nbj + 1);
-    u32* cu = cur2 + u64(kt) * nbj;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 per = (nbj + blockDim.x - 1) / blockDim.x;
     const u32 s0 = threadIdx.x * per, s1 = min(nbj, s0 + per);
@@ -163,58 +252,21 @@ __global__ void __launch_bounds__(1024) bin_scan2(const u32* __restrict__ gh, u3
     u32 run = ws[wid] + incl - loc;
     for (u32 i = s0; i < s1; ++i) {
         bo[i] = run;
-        cu[i] = run;
         run += g[i];
     }
     if (threadIdx.x == 0) bo[nbj] = ws[32];
 }
 
-// Scatter: per chunk, shared counts -> one reservation per nonzero bin ->
-// second pass over the (L2-resident) chunk writes each record at its bin's
-// reserved base + a shared rank. Order within a bin is immaterial.
-__global__ void __launch_bounds__(kScatterThreads) bin_scatter2(const u64* __restrict__ S1, u64 cap_kt,
-                                                                const u32* __restrict__ cur1, int nkt,
-                                                                u32 chunks_per_kt, u32 nbj, u32* __restrict__ cur2,
-                                                                u64* __restrict__ F) {
-    extern __shared__ u32 h2[];  // [nbj] counts, then bases; [nbj] ranks
-    u32* rk = h2 + nbj;
-    for (u32 w = blockIdx.x; w < u32(nkt) * chunks_per_kt; w += gridDim.x) {
-        const u32 kt = w / chunks_per_kt, ch = w % chunks_per_kt;
-        const u64 cnt = minu(cur1[kt], cap_kt);
-        const u64 r0 = u64(ch) * kChunk2;
-        if (r0 >= cnt) continue;
-        const u64 r1 = minu(cnt, r0 + kChunk2);
-        for (u32 i = threadIdx.x; i < nbj; i += blockDim.x) {
-            h2[i] = 0;
-            rk[i] = 0;
-        }
-        __syncthreads();
-        const u64* src = S1 + u64(kt) * cap_kt;
-        for (u64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicAdd(&h2[rec_a(src[i]) >> kBinJTShift], 1u);
-        __syncthreads();
-        u32* cu = cur2 + u64(kt) * nbj;
-        for (u32 i = threadIdx.x; i < nbj; i += blockDim.x)
-            if (h2[i]) h2[i] = atomicAdd(cu + i, h2[i]);
-        __syncthreads();
-        u64* dst = F + u64(kt) * cap_kt;
-        for (u64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-            const u64 r = src[i];
-            const u32 jt = rec_a(r) >> kBinJTShift;
-            dst[h2[jt] + atomicAdd(&rk[jt], 1u)] = r;
-        }
-        __syncthreads();
-    }
-}
-
-// ---- verify one window's bins ----
+// ---- verify ----
 struct BinVerifyArgs {
     const u64* Xc;
     u32 Wp;
     const u64* Yw;
     u32 n, astar;
     u64 p;
-    const u64* F;       // the window's region (bins by x-side tile)
-    const u32* boff;    // the window's bin offsets [nbj + 1]
+    const u64* F;       // the window's first bucket (sorted by tile)
+    const u32* bstart;  // the window's tiles: first record, relative to F
+    const u32* boff;    // the window's compact tile offsets [nbj + 1] (fill = boff[jt + 1] - boff[jt])
     u32 nbj;
     const u32* rid;          // global run ids by run index
     DevHit* hits;
@@ -222,7 +274,7 @@ struct BinVerifyArgs {
     u32 hit_cap;
     const u32* krows;  // the runs' draws [R][M]: x-side keys of hits
     int kM;
-    u32* sint_out;        // top-K first phase: rank of every pair of this window (thr == 0)
+    u32* sint_out;        // top-K first phase: rank of every pair of this window at its compact index (thr == 0)
     const u32* rank_thr;  // top-K running threshold (nullptr: hits mode)
 };
 
@@ -279,7 +331,8 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        const u32 r0 = A.boff[jt], r1 = A.boff[jt + 1];
+        const u32 rbase = A.boff[jt], r0 = 0, r1 = A.boff[jt + 1] - rbase;  // the bin's fill
+        const u64* Fb = A.F + A.bstart[jt];
         ulonglong2* tile = tiles + u32(s) * tile_elems;
         if (r1 > r0) {
             // pre-XOR the response into the x-side tile: popc(a ^ y ^ b) per pair
@@ -299,7 +352,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
 #pragma unroll
             for (int r = 0; r < PR; ++r) {
                 const u32 q = r0 + warp * TPW * PR + tw * PR + r;
-                nrec[r] = q < r1 ? __ldg(A.F + q) : 0ull;
+                nrec[r] = q < r1 ? __ldg(Fb + q) : 0ull;
             }
             for (u32 q0 = r0 + warp * TPW * PR; q0 < r1; q0 += STRIDE) {  // warp-uniform
                 const u32 qb = q0 + tw * PR;
@@ -319,7 +372,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
 #pragma unroll
                 for (int r = 0; r < PR; ++r) {
                     const u32 q = qb + STRIDE + r;
-                    nrec[r] = q < r1 ? __ldg(A.F + q) : 0ull;
+                    nrec[r] = q < r1 ? __ldg(Fb + q) : 0ull;
                 }
 #pragma unroll
                 for (int r = 0; r < PR; ++r) {
@@ -339,7 +392,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
                     if (tl == 0 && q < r1) {
                         const u32 si = rec_neg(rec[r]) ? A.n - acc : acc;  // the run's sign (search.cpp:25-36)
                         if (ranks) {
-                            A.sint_out[q] = si;
+                            A.sint_out[rbase + q] = si;
                         } else if (si >= astar) {
                             PairRec pr{rec_a(rec[r]), rec_b(rec[r]), rec_run(rec[r]), rec_diag(rec[r]) << 1};
                             kern::append_pair_hit(nullptr, 0, 0, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, A.n,
@@ -353,14 +406,99 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
     }
 }
 
-// Top-K first phase over a window: append its pairs with rank >= E (as topk::emit_pairs).
-__global__ void __launch_bounds__(256) emit_binned(const u64* __restrict__ F, const u32* __restrict__ sint,
-                                                   const u32* __restrict__ count, const topk::State* __restrict__ st,
-                                                   const u32* __restrict__ rid, const u32* __restrict__ krows, int kM,
-                                                   const u64* __restrict__ Xc, u32 Wp, DevHit* __restrict__ hits,
-                                                   u32* __restrict__ hit_count, u32 hit_cap, u32 n) {
+__device__ __forceinline__ void emit_rec(u64 rc, u32 r, const u32* __restrict__ rid, const u32* __restrict__ krows,
+                                         int kM, const u64* __restrict__ Xc, u32 Wp, DevHit* __restrict__ hits,
+                                         u32 slot, u32 n) {
+    u32 j = rec_a(rc), k = rec_b(rc);
+    if (rec_diag(rc) && j > k) {
+        const u32 t = j;
+        j = k;
+        k = t;
+    }
+    const u32 run = rec_run(rc);
+    DevHit h;
+    h.order = kern::key_of_column(krows + u64(run) * kM, kM, Xc, Wp, j);
+    h.s = double(r) / double(n);
+    h.j = j;
+    h.k = k;
+    h.rid = rid[run];
+    h.sint = int32_t(r);
+    hits[slot] = h;
+}
+
+// Top-K first phase over a window: append its pairs with rank >= E (as
+// topk::emit_pairs); warp per bin, warp-aggregated slots.
+__global__ void __launch_bounds__(256) emit_bins(const u64* __restrict__ F, const u32* __restrict__ bstart,
+                                                 const u32* __restrict__ boff,
+                                                 u32 nbj, const u32* __restrict__ sint,
+                                                 const topk::State* __restrict__ st, const u32* __restrict__ rid,
+                                                 const u32* __restrict__ krows, int kM, const u64* __restrict__ Xc,
+                                                 u32 Wp, DevHit* __restrict__ hits, u32* __restrict__ hit_count,
+                                                 u32 hit_cap, u32 n) {
     if (st->thr > 0) return;
-    const u32 P = *count;
+    const u32 E = st->emit;
+    const int lane = threadIdx.x & 31;
+    const u32 gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (u32 jt = gw; jt < nbj; jt += nw) {
+        const u32 b0 = boff[jt], fill = boff[jt + 1] - b0;
+        for (u32 i0 = 0; i0 < fill; i0 += 32) {
+            const u32 i = i0 + lane;
+            const u32 r = i < fill ? sint[b0 + i] : 0u;
+            const bool take = i < fill && r >= E;
+            const u32 bal = __ballot_sync(0xffffffffu, take);
+            if (!bal) continue;
+            u32 base = 0;
+            if (lane == __ffs(bal) - 1) base = atomicAdd(hit_count, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+            const u32 slot = base + __popc(bal & lanemask_lt());
+            if (take && slot < hit_cap) emit_rec(F[bstart[jt] + i], r, rid, krows, kM, Xc, Wp, hits, slot, n);
+        }
+    }
+}
+
+// The overflow list: warp per pair, both columns gathered (lane w: slices w, w + 32, w + 64).
+__global__ void __launch_bounds__(256) verify_list(BinVerifyArgs A, const u64* __restrict__ list,
+                                                   const u32* __restrict__ count, u32 cap) {
+    const int lane = threadIdx.x & 31;
+    const u32 W2 = A.Wp / 2;
+    const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(A.Xc);
+    const ulonglong2* Y2 = reinterpret_cast<const ulonglong2*>(A.Yw);
+    const u32 P = min(*count, cap);
+    const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
+    const bool ranks = A.sint_out != nullptr && rthr == 0;
+    const u32 astar = max(A.astar, rthr);
+    const u32 gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (u32 q = gw; q < P; q += nw) {
+        const u64 rc = list[q];
+        const ulonglong2* a = X2 + u64(rec_a(rc)) * W2;
+        const ulonglong2* b = X2 + u64(rec_b(rc)) * W2;
+        u32 acc = 0;
+        for (u32 w = lane; w < W2; w += 32) {
+            const ulonglong2 x = __ldg(a + w), z = __ldg(b + w), y = __ldg(Y2 + w);
+            acc += __popcll(x.x ^ z.x ^ y.x) + __popcll(x.y ^ z.y ^ y.y);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const u32 si = rec_neg(rc) ? A.n - acc : acc;
+            if (ranks) {
+                A.sint_out[q] = si;
+            } else if (si >= astar) {
+                PairRec pr{rec_a(rc), rec_b(rc), rec_run(rc), rec_diag(rc) << 1};
+                kern::append_pair_hit(nullptr, 0, 0, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, A.n, A.krows,
+                                      A.kM, A.Xc, A.Wp);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) emit_list(const u64* __restrict__ list, const u32* __restrict__ sint,
+                                                 const u32* __restrict__ count, u32 cap,
+                                                 const topk::State* __restrict__ st, const u32* __restrict__ rid,
+                                                 const u32* __restrict__ krows, int kM, const u64* __restrict__ Xc,
+                                                 u32 Wp, DevHit* __restrict__ hits, u32* __restrict__ hit_count,
+                                                 u32 hit_cap, u32 n) {
+    if (st->thr > 0) return;
+    const u32 P = min(*count, cap);
     const u32 E = st->emit;
     const int lane = threadIdx.x & 31;
     for (u64 i0 = u64(blockIdx.x) * blockDim.x; i0 < P; i0 += u64(gridDim.x) * blockDim.x) {
@@ -372,27 +510,8 @@ __global__ void __launch_bounds__(256) emit_binned(const u64* __restrict__ F, co
         u32 base = 0;
         if (lane == __ffs(bal) - 1) base = atomicAdd(hit_count, __popc(bal));
         base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
-        if (take) {
-            const u32 slot = base + __popc(bal & lanemask_lt());
-            if (slot < hit_cap) {
-                const u64 rc = F[i];
-                u32 j = rec_a(rc), k = rec_b(rc);
-                if (rec_diag(rc) && j > k) {
-                    const u32 t = j;
-                    j = k;
-                    k = t;
-                }
-                const u32 run = rec_run(rc);
-                DevHit h;
-                h.order = kern::key_of_column(krows + u64(run) * kM, kM, Xc, Wp, j);
-                h.s = double(r) / double(n);
-                h.j = j;
-                h.k = k;
-                h.rid = rid[run];
-                h.sint = int32_t(r);
-                hits[slot] = h;
-            }
-        }
+        const u32 slot = base + __popc(bal & lanemask_lt());
+        if (take && slot < hit_cap) emit_rec(list[i], r, rid, krows, kM, Xc, Wp, hits, slot, n);
     }
 }
 

@@ -287,8 +287,9 @@ struct xyzb_dataset {
     // top-K over all candidates (topk_kernels.cuh)
     DevBuf tk_state, tk_hist, tk_dhist, tk_sint, tk_table, hits2, tk_cnt2;
     // binned verify (binned_verify.cuh): per-window regions, bins by x-side tile, cursors
-    DevBuf bin_s1, bin_f, bin_cur1, bin_gh, bin_boff, bin_cur2, bin_zero;
-    u64 bin_hint = 0;  // largest window count seen by a search on this dataset (sizes the regions)
+    DevBuf bin_b, bin_d, bin_cnt, bin_start, bin_fill, bin_boff, bin_ovf, bin_ovfn, bin_zero;
+    u64 bin_hint = 0;      // mean bucket fill of the last binned search on this dataset (sizes the buckets)
+    u64 bin_ovf_hint = 0;  // overflow-list size that last sufficed
     HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
     StageClock clock;
     u32 hit_cap = 1u << 16;
@@ -752,7 +753,7 @@ struct SearchCtx {
     // binned verify (X >> L2): pairs of all batches bucketed by (z window, x tile), verified at the end
     bool binned = false;
     int wshift = 0, nkt = 0;
-    u64 nbj = 0, cap_kt = 0, bin_scale = 1;
+    u64 nbj = 0, nbh = 0, cap_bucket = 0, ovf_cap = 0;
     RunPlan plan;
     xyzb_result* out;
     u64 launches[XYZB_NUM_STAGES] = {};
@@ -1004,21 +1005,15 @@ void binned_verify(SearchCtx& c) {
     StageClock& clk = ds->clock;
     const u32 nbj = static_cast<u32>(c.nbj);
     const int nkt = c.nkt;
-    const u32 chunks = static_cast<u32>(ceil_div(c.cap_kt, bins::kChunk2));
     cudaEvent_t e0 = clk.mark();
-    XYZB_CUDA(cudaMemsetAsync(ds->bin_gh.p, 0, u64(nkt) * nbj * 4, st));
-    func_smem(bins::bin_hist2, size_t(nbj) * 4);
-    bins::bin_hist2<<<kSMs * 2, bins::kScatterThreads, size_t(nbj) * 4, st>>>(
-        ds->bin_s1.as<u64>(), c.cap_kt, ds->bin_cur1.as<u32>(), nkt, chunks, nbj, ds->bin_gh.as<u32>());
+    const u32 nbuckets = static_cast<u32>(u64(nkt) * c.nbh);
+    bins::bin_sort<<<nbuckets, 1024, 0, st>>>(ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket), ds->bin_cnt.as<u32>(),
+                                              static_cast<u32>(c.nbh), nbj, ds->bin_d.as<u64>(), ds->bin_start.as<u32>(),
+                                              ds->bin_fill.as<u32>());
     XYZB_LAUNCH_CHECK();
-    bins::bin_scan2<<<nkt, 1024, 0, st>>>(ds->bin_gh.as<u32>(), nbj, ds->bin_boff.as<u32>(), ds->bin_cur2.as<u32>());
+    bins::bin_scan<<<nkt, 1024, 0, st>>>(ds->bin_fill.as<u32>(), nbj, ds->bin_boff.as<u32>());
     XYZB_LAUNCH_CHECK();
-    func_smem(bins::bin_scatter2, size_t(nbj) * 8);
-    bins::bin_scatter2<<<kSMs, bins::kScatterThreads, size_t(nbj) * 8, st>>>(
-        ds->bin_s1.as<u64>(), c.cap_kt, ds->bin_cur1.as<u32>(), nkt, chunks, nbj, ds->bin_cur2.as<u32>(),
-        ds->bin_f.as<u64>());
-    XYZB_LAUNCH_CHECK();
-    c.launches[XYZB_STAGE_JOIN] += 3;
+    c.launches[XYZB_STAGE_JOIN] += 2;
     clk.span(XYZB_STAGE_JOIN, e0, clk.mark());
     bins::BinVerifyArgs A;
     A.Xc = ds->Xc.as<u64>();
@@ -1050,9 +1045,33 @@ void binned_verify(SearchCtx& c) {
     PA.hits = A.hits;
     PA.hit_count = A.hit_count;
     PA.hit_cap = A.hit_cap;
+    auto topk_phase = [&](cudaEvent_t ev1, const u32* cnt, u32 cap, const u64* list, const u32* boff) {
+        Nvtx nv("xyzb:topk");
+        auto* S = ds->tk_state.as<topk::State>();
+        const u64 K = c.q->top_k;
+        const u32 target = c.tk_level == 0 ? u32(std::min<u64>(4 * K + 256, 0x7fffffffull))
+                                           : u32(std::min<u64>(64 * K + 4096, 0x7fffffffull));
+        topk::rank_hist<<<kSMs * 2, 512, 0, st>>>(ds->tk_sint.as<u32>(), cnt, cap, ds->bin_zero.as<u32>(), 1u, S,
+                                                  c.tk_shift, ds->tk_hist.as<u32>());
+        XYZB_LAUNCH_CHECK();
+        topk::emit_select<<<1, 1024, 0, st>>>(ds->tk_hist.as<u32>(), c.tk_shift, target, S, c.tk_level >= 2);
+        XYZB_LAUNCH_CHECK();
+        if (list)
+            bins::emit_list<<<kSMs * 8, 256, 0, st>>>(list, ds->tk_sint.as<u32>(), cnt, cap, S, A.rid, A.krows, A.kM,
+                                                      A.Xc, A.Wp, A.hits, A.hit_count, A.hit_cap, A.n);
+        else
+            bins::emit_bins<<<kSMs * 8, 256, 0, st>>>(A.F, A.bstart, boff, nbj, ds->tk_sint.as<u32>(), S, A.rid,
+                                                      A.krows, A.kM, A.Xc, A.Wp, A.hits, A.hit_count, A.hit_cap,
+                                                      A.n);
+        XYZB_LAUNCH_CHECK();
+        c.launches[XYZB_STAGE_MERGE] += 3;
+        topk_prune(c, PA, &c.launches[XYZB_STAGE_MERGE]);
+        clk.span(XYZB_STAGE_MERGE, ev1, clk.mark());
+    };
     for (int kt = 0; kt < nkt; ++kt) {
         Nvtx nv_verify("xyzb:verify");
-        A.F = ds->bin_f.as<u64>() + u64(kt) * c.cap_kt;
+        A.F = ds->bin_d.as<u64>() + u64(kt) * c.nbh * c.cap_bucket;
+        A.bstart = ds->bin_start.as<u32>() + u64(kt) * nbj;
         A.boff = ds->bin_boff.as<u32>() + u64(kt) * (nbj + 1);
         cudaEvent_t ev0 = clk.mark();
         vk<<<kSMs, bins::kVerifyThreads, smem, st>>>(A);
@@ -1061,27 +1080,18 @@ void binned_verify(SearchCtx& c) {
         cudaEvent_t ev1 = clk.mark();
         clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
         c.verify_spans.push_back({ev0, ev1});
-        if (c.topk_all) {
-            Nvtx nv("xyzb:topk");
-            auto* S = ds->tk_state.as<topk::State>();
-            const u64 K = c.q->top_k;
-            const u32 target = c.tk_level == 0 ? u32(std::min<u64>(4 * K + 256, 0x7fffffffull))
-                                               : u32(std::min<u64>(64 * K + 4096, 0x7fffffffull));
-            const u32* cnt = A.boff + nbj;  // the window's pair count
-            topk::rank_hist<<<kSMs * 2, 512, 0, st>>>(ds->tk_sint.as<u32>(), cnt, static_cast<u32>(c.cap_kt),
-                                                      ds->bin_zero.as<u32>(), 1u, S, c.tk_shift,
-                                                      ds->tk_hist.as<u32>());
-            XYZB_LAUNCH_CHECK();
-            topk::emit_select<<<1, 1024, 0, st>>>(ds->tk_hist.as<u32>(), c.tk_shift, target, S, c.tk_level >= 2);
-            XYZB_LAUNCH_CHECK();
-            bins::emit_binned<<<kSMs * 8, 256, 0, st>>>(A.F, ds->tk_sint.as<u32>(), cnt, S, A.rid, A.krows, A.kM,
-                                                        A.Xc, A.Wp, A.hits, A.hit_count, A.hit_cap, A.n);
-            XYZB_LAUNCH_CHECK();
-            c.launches[XYZB_STAGE_MERGE] += 3;
-            topk_prune(c, PA, &c.launches[XYZB_STAGE_MERGE]);
-            clk.span(XYZB_STAGE_MERGE, ev1, clk.mark());
-        }
+        if (c.topk_all) topk_phase(ev1, A.boff + nbj, 0xffffffffu, nullptr, A.boff);  // the window's pairs held in bins
     }
+    // pairs whose bin was full
+    cudaEvent_t ev0 = clk.mark();
+    bins::verify_list<<<kSMs * 8, 256, 0, st>>>(A, ds->bin_ovf.as<u64>(), ds->bin_ovfn.as<u32>(),
+                                                static_cast<u32>(c.ovf_cap));
+    XYZB_LAUNCH_CHECK();
+    c.launches[XYZB_STAGE_VERIFY] += 1;
+    cudaEvent_t ev1 = clk.mark();
+    clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
+    if (c.topk_all)
+        topk_phase(ev1, ds->bin_ovfn.as<u32>(), static_cast<u32>(c.ovf_cap), ds->bin_ovf.as<u64>(), nullptr);
 }
 
 template <class K>
@@ -1121,7 +1131,7 @@ void run_batches(SearchCtx& c) {
     // batch size: B*p entries under the budget (about 64 B of scratch each)
     u64 budget = u64(1) << 26;  // the batch_entries test option forces multi-batch runs
     if (const long long e = topt().batch_entries.load()) budget = std::max<u64>(1, u64(e));
-    const u64 B = std::max<u64>(1, std::min<u64>(R, budget / std::max<u64>(p, 1)));
+    const u64 B = std::max<u64>(1, std::min<u64>({R, budget / std::max<u64>(p, 1), u64(bins::kMaxRunsPerBatch)}));
     const u64 cap = B * p;
     for (int i = 0; i < 2; ++i) {
         ds->keys[i].ensure(cap * sizeof(K));
@@ -1210,26 +1220,36 @@ void run_batches(SearchCtx& c) {
         int ws = 20;  // z-side windows of ~84 MB (L2-resident while their bins are verified)
         while (ws > 10 && (u64(1) << ws) * ds->Wp * 8 > (u64(88) << 20)) --ws;
         if (const long long w = topt().binned_wshift.load()) ws = static_cast<int>(w);
-        while (ceil_div(p, u64(1) << ws) > 256) ++ws;
+        while (ceil_div(p, u64(1) << ws) * ceil_div(ceil_div(p, bins::kBinJT), u64(1) << bins::kHiBits) >
+               bins::kMaxBuckets)
+            ++ws;
         c.wshift = ws;
         c.nkt = static_cast<int>(ceil_div(p, u64(1) << ws));
         c.nbj = ceil_div(p, bins::kBinJT);
-        // region capacity: the dataset's largest window count so far (+25 %), else the batches' pair capacity
-        const u64 est = ds->bin_hint ? ds->bin_hint + ds->bin_hint / 4 + 4096 : ceil_div(nbatches * c.pair_cap, c.nkt);
-        c.cap_kt = std::min<u64>(0xffffffffull, est * c.bin_scale);
-        if (const long long cap = topt().binned_cap.load())  // tests force the region regrow path
-            if (c.bin_scale == 1) c.cap_kt = std::max<u64>(1, u64(cap));
-        const u64 nk = u64(c.nkt);
-        ds->bin_s1.ensure(nk * c.cap_kt * 8);
-        ds->bin_f.ensure(nk * c.cap_kt * 8);
-        ds->bin_cur1.ensure(nk * 4);
-        ds->bin_gh.ensure(nk * c.nbj * 4);
-        ds->bin_boff.ensure(nk * (c.nbj + 1) * 4);
-        ds->bin_cur2.ensure(nk * c.nbj * 4);
+        c.nbh = ceil_div(c.nbj, u64(1) << bins::kHiBits);
+        const u64 nbk = u64(c.nkt) * c.nbh;
+        // bucket capacity: 1.25x the last search's mean fill (+4096), else the batches' pair capacity spread evenly
+        const u64 mean = ds->bin_hint ? ds->bin_hint : ceil_div(nbatches * c.pair_cap, 2 * nbk);
+        c.cap_bucket = std::min<u64>(0xffffffffull / nbk, mean + mean / 4 + 4096);
+        c.ovf_cap = std::min<u64>(0xffffffffull,
+                                  std::max<u64>({u64(1) << 20, nbk * c.cap_bucket / 16, ds->bin_ovf_hint}));
+        if (const long long cap = topt().binned_cap.load()) {  // tests: tiny buckets and overflow list (redo path)
+            c.cap_bucket = std::max<u64>(1, u64(cap));
+            c.ovf_cap = std::max<u64>(c.cap_bucket, ds->bin_ovf_hint);
+        }
+        ds->bin_b.ensure(nbk * c.cap_bucket * 8);
+        ds->bin_d.ensure(nbk * c.cap_bucket * 8);
+        ds->bin_cnt.ensure(nbk * 4);
+        ds->bin_start.ensure(u64(c.nkt) * c.nbj * 4);
+        ds->bin_fill.ensure(u64(c.nkt) * c.nbj * 4);
+        ds->bin_boff.ensure(u64(c.nkt) * (c.nbj + 1) * 4);
+        ds->bin_ovf.ensure(c.ovf_cap * 8);
+        ds->bin_ovfn.ensure(4);
         ds->bin_zero.ensure(4);
-        XYZB_CUDA(cudaMemsetAsync(ds->bin_cur1.p, 0, nk * 4, st));
+        XYZB_CUDA(cudaMemsetAsync(ds->bin_cnt.p, 0, nbk * 4, st));
+        XYZB_CUDA(cudaMemsetAsync(ds->bin_ovfn.p, 0, 4, st));
         XYZB_CUDA(cudaMemsetAsync(ds->bin_zero.p, 0, 4, st));
-        if (c.topk_all) ds->tk_sint.ensure(c.cap_kt * 4);
+        if (c.topk_all) ds->tk_sint.ensure(std::max(c.nbh * c.cap_bucket, c.ovf_cap) * 4);
     }
     const u32 hmax = 8u;  // held columns per item (pair expansion chunks)
     // Grouping + join, by the run's bucket space 2^M against p:
@@ -1496,9 +1516,11 @@ void run_batches(SearchCtx& c) {
             cudaEvent_t ev0 = clk.mark();
             clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
             if (c.binned) {  // the batch's pairs go to their z-side windows; verified after the last batch
-                bins::bin_scatter1<<<kSMs * 4, bins::kS1Threads, 0, st>>>(
+                bins::bin_append<<<kSMs * 4, bins::kAppendThreads, 0, st>>>(
                     ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), A.nitems, A.item_cap,
-                    static_cast<u32>(b0), rsign, c.wshift, c.nkt, ds->bin_s1.as<u64>(), c.cap_kt, ds->bin_cur1.as<u32>());
+                    static_cast<u32>(b0), rsign, static_cast<u32>(nb), c.wshift, static_cast<u32>(c.nbh),
+                    static_cast<u32>(u64(c.nkt) * c.nbh), ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket),
+                    ds->bin_cnt.as<u32>(), ds->bin_ovf.as<u64>(), static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_JOIN] += 1;
                 clk.span(XYZB_STAGE_JOIN, ev0, clk.mark());
@@ -2010,7 +2032,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         // status block (pinned): H, merge counts, items and pairs per batch, per-run counters
         const size_t o_cnt = 8, o_items = 16, o_pairs = o_items + 4 * nbt, o_enum = round_up(o_pairs + 4 * nbt, 8),
                      o_ver = o_enum + 8 * Rall, o_ovf = o_ver + 8 * Rall, o_tk = o_ovf + 8,
-                     o_bin = round_up(o_tk + sizeof(topk::State), 8), sbytes = o_bin + 4 * u64(c.nkt) + 8;
+                     o_bin = round_up(o_tk + sizeof(topk::State), 8), sbytes = o_bin + 8;
         ds->h_status.ensure(sbytes);
         char* hs = ds->h_status.as<char>();
         XYZB_CUDA(cudaMemcpyAsync(hs, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
@@ -2025,7 +2047,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             XYZB_CUDA(cudaMemcpyAsync(hs + o_tk, ds->tk_state.p, sizeof(topk::State), cudaMemcpyDeviceToHost,
                                       ds->stream));
         if (c.binned)
-            XYZB_CUDA(cudaMemcpyAsync(hs + o_bin, ds->bin_cur1.p, 4 * u64(c.nkt), cudaMemcpyDeviceToHost, ds->stream));
+            XYZB_CUDA(cudaMemcpyAsync(hs + o_bin, ds->bin_ovfn.p, 4, cudaMemcpyDeviceToHost, ds->stream));
         tr.mark("search:launch");
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         tr.mark("search:device");
@@ -2046,12 +2068,18 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             }
         }
         bool bin_redo = false;
-        if (c.binned) {  // a window region overflowed: size the regions from the counts seen and redo
-            const u32* cur = reinterpret_cast<const u32*>(hs + o_bin);
-            const u64 mx = *std::max_element(cur, cur + c.nkt);
-            ds->bin_hint = mx;
-            bin_redo = mx > c.cap_kt;
-            if (bin_redo) c.bin_scale = 2;
+        if (c.binned) {  // bins sized from this search's mean fill next time; an overflowing list: redo
+            const u32 on = *reinterpret_cast<const u32*>(hs + o_bin);
+            if (c.pair_cap) {
+                const u32* np = reinterpret_cast<const u32*>(hs + o_pairs);
+                u64 tot = 0;
+                for (u64 b = 0; b < nbt; ++b) tot += std::min<u64>(np[b], c.pair_cap);
+                ds->bin_hint = std::max<u64>(1, tot / (u64(c.nkt) * c.nbh));
+            }
+            if (on > c.ovf_cap) {
+                ds->bin_ovf_hint = 2 * u64(on);
+                bin_redo = true;
+            }
         }
         const bool povf = *reinterpret_cast<const u32*>(hs + o_ovf) != 0;
         if (povf) c.no_hash = true;  // a hashed partition overflowed: redo on the sorted path
@@ -2077,6 +2105,8 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                 for (u64 b = 0; b < nbt; ++b) tot += np[b];
                 c.bytes[c.pairs_in_sort ? XYZB_STAGE_SORT : XYZB_STAGE_JOIN] += 16 * tot;
                 // binned: level 1 reads 16 B and writes 8 B per pair, level 2 reads 8 B three times and writes 8 B
+                // binned: the append reads the (pa, pb) words and the record, writes 8 B; the bucket split reads
+                // 8 B twice and writes 8 B
                 if (c.binned) c.bytes[XYZB_STAGE_JOIN] += 56 * tot;
                 if (c.topk_all) c.bytes[XYZB_STAGE_MERGE] += 8 * tot;  // pair ranks read by the histogram + emission
             }
