@@ -26,7 +26,8 @@
 // Pair records (u64): x-side column (24 bits) | z-side column (24) | diagonal
 // flag (1, at bit 48) | the run's pass is negative (1, bit 49) | global run
 // index in execution order (14, at bit 50).
-//   bin_append   (per batch)  the batch's pair list -> buckets (or the overflow list)
+//   bin_window   (per batch)  the batch's pair list -> windows (or the overflow list)
+//   bin_split    (end)        each window -> buckets by x-side tile >> 7
 //   bin_sort     (end)        each bucket -> its 128 tiles' runs
 //   bin_scan     (end)        per window, exclusive offsets of the tile fills
 //                             (compact rank indices for the top-K first phase)
@@ -61,123 +62,234 @@ __device__ __forceinline__ u32 rec_diag(u64 r) { return u32(r >> 48) & 1u; }
 __device__ __forceinline__ u32 rec_neg(u64 r) { return u32(r >> 49) & 1u; }
 __device__ __forceinline__ u32 rec_run(u64 r) { return u32(r >> 50); }
 
-// ---- per batch: the pair list -> buckets (window, x-side tile >> 7) ----
-// A CTA takes chunks of kAppendChunk records: shared counts per bucket, one
-// global reservation per (chunk, bucket) (~16 records each at config 4), a
-// second sweep over the (L2-resident) chunk writes each record at its
-// bucket's reserved run. A full bucket sends the record to the overflow list.
+// ---- partition passes: records -> fixed-capacity regions ----
+// A CTA takes one contiguous range (long runs per region and reservation):
+// sweep 1 counts its records per region in shared memory, one global
+// reservation per (CTA, region); sweep 2 takes steps of kPartThreads x R
+// records (R loads in flight per thread), groups each step by region in
+// shared memory (an unstable local counting sort: order inside a region is
+// immaterial) and writes every region's run contiguously, so the stores are
+// whole sectors instead of one scattered 8-byte store per record (ncu: the
+// scattered form was bound on L2 store transactions). A record whose region
+// is full goes to the overflow list.
 constexpr int kHiBits = 7;                  // x-side tiles per bucket: 128
-constexpr u32 kMaxBuckets = 4096;           // windows x buckets per window (shared counters)
-constexpr u32 kAppendChunk = 32768;
-constexpr int kAppendThreads = 512, kAppendPerThread = 8;
+constexpr u32 kMaxRegions = 256;            // regions per partition pass (shared counters)
+constexpr int kPartThreads = 512, kPartPerThread = 8;
+constexpr u32 kPartStep = kPartThreads * kPartPerThread;
 constexpr u32 kMaxRunsPerBatch = 4096;      // a batch's run signs in shared memory
 
-__device__ __forceinline__ u32 bucket_of(u32 pa, u32 pb, int wshift, u32 nbh) {
-    return (pb >> wshift) * nbh + (pa >> (kBinJTShift + kHiBits));
+struct PartSmem {
+    u64 buf[kPartStep];
+    u32 lcnt[kMaxRegions], lstart[kMaxRegions], runo[kMaxRegions];
+    u32 total;
+};
+
+// One sweep-2 step: rec[u] (valid when rg[u] < nreg) -> dst regions of `cap`
+// records at runo[rg] (the CTA's reservation, advanced per step).
+template <int THREADS, int R, class RegionOf>
+__device__ __forceinline__ void scatter_step(PartSmem& sm, const u64 (&rec)[R], const u32 (&rg)[R], u32 nreg,
+                                             RegionOf region_of, u64* __restrict__ dst, u64 stride, u32 cap,
+                                             u64* __restrict__ ovf, u32 ovf_cap, u32* __restrict__ ovf_n) {
+    u32 rk[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+        if (rg[u] < nreg) rk[u] = atomicAdd(&sm.lcnt[rg[u]], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the step's region counts (<= 256, 8 per lane)
+        const int lane = threadIdx.x;
+        constexpr int PER = kMaxRegions / 32;
+        u32 c[PER], tot = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const u32 g = lane * PER + q;
+            c[q] = g < nreg ? sm.lcnt[g] : 0u;
+            tot += c[q];
+        }
+        u32 incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        u32 ex = incl - tot;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const u32 g = lane * PER + q;
+            if (g < nreg) sm.lstart[g] = ex;
+            ex += c[q];
+        }
+        if (lane == 31) sm.total = incl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+        if (rg[u] < nreg) sm.buf[sm.lstart[rg[u]] + rk[u]] = rec[u];
+    __syncthreads();
+    const u32 total = sm.total;
+    for (u32 e = threadIdx.x; e < total; e += THREADS) {
+        const u64 r = sm.buf[e];
+        const u32 g = region_of(r);
+        const u32 pos = sm.runo[g] + (e - sm.lstart[g]);
+        if (pos < cap) {
+            dst[u64(g) * stride + pos] = r;
+        } else {
+            const u32 o = atomicAdd(ovf_n, 1u);
+            if (o < ovf_cap) ovf[o] = r;
+        }
+    }
+    __syncthreads();
+    for (u32 g = threadIdx.x; g < nreg; g += THREADS) {
+        sm.runo[g] += sm.lcnt[g];
+        sm.lcnt[g] = 0;
+    }
+    __syncthreads();
 }
 
-__global__ void __launch_bounds__(kAppendThreads) bin_append(const PairRec* __restrict__ pairs,
-                                                             const u32* __restrict__ npairs, u32 pair_cap,
-                                                             const u32* __restrict__ nitems, u32 item_cap, u32 run0,
-                                                             const int8_t* __restrict__ run_sign, u32 nruns,
-                                                             int wshift, u32 nbh, u32 nbuckets, u64* __restrict__ B,
-                                                             u32 cap_bucket, u32* __restrict__ bcnt,
-                                                             u64* __restrict__ ovf, u32 ovf_cap,
-                                                             u32* __restrict__ ovf_n) {
-    constexpr int R = kAppendPerThread;
-    constexpr u32 STEP = kAppendThreads * R;  // records in flight per CTA sweep step
-    __shared__ u32 cnt[kMaxBuckets], base[kMaxBuckets];
+// Sweep 1's counts -> the CTA's reservations (runo) in the global region counters.
+template <int THREADS>
+__device__ __forceinline__ void reserve(PartSmem& sm, u32 nreg, u32* __restrict__ gcnt) {
+    __syncthreads();
+    for (u32 g = threadIdx.x; g < nreg; g += THREADS) {
+        sm.runo[g] = sm.lcnt[g] ? atomicAdd(gcnt + g, sm.lcnt[g]) : 0u;
+        sm.lcnt[g] = 0;
+    }
+    __syncthreads();
+}
+
+// Per batch: the batch's pair list -> z-side windows (region = kt). With a
+// small fan-out (16 windows at config 4) one sweep suffices: each step of
+// kPartStep records (held in registers) is counted per window in shared
+// memory, reserved with one global atomic per window and written at base +
+// shared rank (runs of ~256 records).
+__global__ void __launch_bounds__(kPartThreads) bin_window(const PairRec* __restrict__ pairs,
+                                                           const u32* __restrict__ npairs, u32 pair_cap,
+                                                           const u32* __restrict__ nitems, u32 item_cap, u32 run0,
+                                                           const int8_t* __restrict__ run_sign, u32 nruns,
+                                                           int wshift, u32 nkt, u64* __restrict__ S, u32 cap_kt,
+                                                           u32* __restrict__ wcnt, u64* __restrict__ ovf, u32 ovf_cap,
+                                                           u32* __restrict__ ovf_n) {
+    constexpr int R = kPartPerThread;
+    __shared__ u32 cnt[kMaxRegions], base[kMaxRegions];
     __shared__ int8_t neg[kMaxRunsPerBatch];
     const u32 P = topk::batch_pairs(npairs, pair_cap, nitems, item_cap);
-    for (u32 t = threadIdx.x; t < nbuckets; t += blockDim.x) cnt[t] = 0;
+    for (u32 t = threadIdx.x; t < nkt; t += blockDim.x) cnt[t] = 0;
     for (u32 t = threadIdx.x; t < nruns; t += blockDim.x) neg[t] = run_sign[t] < 0 ? 1 : 0;
     __syncthreads();
     const uint4* P4 = reinterpret_cast<const uint4*>(pairs);
-    for (u64 c0 = u64(blockIdx.x) * kAppendChunk; c0 < P; c0 += u64(gridDim.x) * kAppendChunk) {
-        const u64 c1 = minu(P, c0 + kAppendChunk);
-        // sweep 1: bucket counts (R records in flight per thread)
-        for (u64 s0 = c0; s0 < c1; s0 += STEP) {
-            uint2 ab[R];
+    for (u64 s0 = u64(blockIdx.x) * kPartStep; s0 < P; s0 += u64(gridDim.x) * kPartStep) {
+        u64 rec[R];
+        u32 kt[R], rk[R];
 #pragma unroll
-            for (int u = 0; u < R; ++u) {
-                const u64 i = s0 + u64(u) * kAppendThreads + threadIdx.x;
-                ab[u] = i < c1 ? __ldg(reinterpret_cast<const uint2*>(pairs + i)) : make_uint2(0xffffffffu, 0);
-            }
+        for (int u = 0; u < R; ++u) {
+            const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
+            const uint4 pr = i < P ? __ldg(P4 + i) : make_uint4(0, 0, 0, 0);
+            rec[u] = rec_make(pr.x, pr.y, (pr.w >> 1) & 1u, neg[pr.z], run0 + pr.z);
+            kt[u] = i < P ? pr.y >> wshift : 0xffffffffu;
+        }
 #pragma unroll
-            for (int u = 0; u < R; ++u)
-                if (ab[u].x != 0xffffffffu) atomicAdd(&cnt[bucket_of(ab[u].x, ab[u].y, wshift, nbh)], 1u);
+        for (int u = 0; u < R; ++u)
+            if (kt[u] != 0xffffffffu) rk[u] = atomicAdd(&cnt[kt[u]], 1u);
+        __syncthreads();
+        for (u32 t = threadIdx.x; t < nkt; t += blockDim.x) {
+            base[t] = cnt[t] ? atomicAdd(wcnt + t, cnt[t]) : 0u;
+            cnt[t] = 0;
         }
         __syncthreads();
-        for (u32 t = threadIdx.x; t < nbuckets; t += blockDim.x) {
-            const u32 c = cnt[t];
-            base[t] = c ? atomicAdd(bcnt + t, c) : 0u;
-            cnt[t] = 0;  // reused as the chunk's rank counters
-        }
-        __syncthreads();
-        // sweep 2: records to their bucket runs
-        for (u64 s0 = c0; s0 < c1; s0 += STEP) {
-            uint4 pr[R];
 #pragma unroll
-            for (int u = 0; u < R; ++u) {
-                const u64 i = s0 + u64(u) * kAppendThreads + threadIdx.x;
-                pr[u] = i < c1 ? __ldg(P4 + i) : make_uint4(0xffffffffu, 0, 0, 0);
-            }
-#pragma unroll
-            for (int u = 0; u < R; ++u) {
-                if (pr[u].x == 0xffffffffu) continue;
-                const u32 bk = bucket_of(pr[u].x, pr[u].y, wshift, nbh);
-                const u64 rec = rec_make(pr[u].x, pr[u].y, (pr[u].w >> 1) & 1u, neg[pr[u].z], run0 + pr[u].z);
-                const u32 pos = base[bk] + atomicAdd(&cnt[bk], 1u);
-                if (pos < cap_bucket) {
-                    B[u64(bk) * cap_bucket + pos] = rec;
-                } else {
-                    const u32 o = atomicAdd(ovf_n, 1u);
-                    if (o < ovf_cap) ovf[o] = rec;
-                }
+        for (int u = 0; u < R; ++u) {
+            if (kt[u] == 0xffffffffu) continue;
+            const u32 pos = base[kt[u]] + rk[u];
+            if (pos < cap_kt) {
+                S[u64(kt[u]) * cap_kt + pos] = rec[u];
+            } else {
+                const u32 o = atomicAdd(ovf_n, 1u);
+                if (o < ovf_cap) ovf[o] = rec[u];
             }
         }
-        __syncthreads();
-        for (u32 t = threadIdx.x; t < nbuckets; t += blockDim.x) cnt[t] = 0;
-        __syncthreads();
     }
 }
 
-// ---- end of the search: each bucket sorted by the low 7 bits of its x-side tile ----
-// One CTA per bucket: counts per tile (shared), the tiles' starts, then the
-// records scattered into their tile's run (order within a tile immaterial).
-// bstart / bfill: per (window, tile), relative to the window's first bucket.
-__global__ void __launch_bounds__(1024) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
-                                                 const u32* __restrict__ bcnt, u32 nbh, u32 nbj,
-                                                 u64* __restrict__ D, u32* __restrict__ bstart,
-                                                 u32* __restrict__ bfill) {
+// End of the search: each window -> buckets by x-side tile >> 7 (region =
+// kt * nbh + hi). ctas_per_kt CTAs per window, one contiguous range each.
+__global__ void __launch_bounds__(kPartThreads) bin_split(const u64* __restrict__ S, u32 cap_kt,
+                                                          const u32* __restrict__ wcnt, u32 ctas_per_kt, u32 nbh,
+                                                          u64* __restrict__ B, u32 cap_bucket,
+                                                          u32* __restrict__ bcnt, u64* __restrict__ ovf, u32 ovf_cap,
+                                                          u32* __restrict__ ovf_n) {
+    constexpr int R = kPartPerThread;
+    constexpr int SH = kBinJTShift + kHiBits;
+    __shared__ PartSmem sm;
+    const u32 kt = blockIdx.x / ctas_per_kt, part = blockIdx.x % ctas_per_kt;
+    const u32 n = min(wcnt[kt], cap_kt);
+    const u64 chunk = ceil_div(ceil_div(n, ctas_per_kt), kPartStep) * kPartStep;
+    const u64 c0 = u64(part) * chunk, c1 = minu(n, c0 + chunk);
+    if (c0 >= c1) return;
+    const u64* src = S + u64(kt) * cap_kt;
+    for (u32 t = threadIdx.x; t < nbh; t += blockDim.x) sm.lcnt[t] = 0;
+    __syncthreads();
+    for (u64 s0 = c0; s0 < c1; s0 += kPartStep) {
+        u32 h[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
+            h[u] = i < c1 ? rec_a(__ldg(src + i)) >> SH : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+            if (h[u] != 0xffffffffu) atomicAdd(&sm.lcnt[h[u]], 1u);
+    }
+    reserve<kPartThreads>(sm, nbh, bcnt + u64(kt) * nbh);
+    auto region_of = [](u64 r) { return rec_a(r) >> SH; };
+    u64* dst = B + u64(kt) * nbh * cap_bucket;
+    for (u64 s0 = c0; s0 < c1; s0 += kPartStep) {
+        u64 rec[R];
+        u32 rg[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
+            rec[u] = i < c1 ? __ldg(src + i) : 0ull;
+            rg[u] = i < c1 ? rec_a(rec[u]) >> SH : 0xffffffffu;
+        }
+        scatter_step<kPartThreads, R>(sm, rec, rg, nbh, region_of, dst, cap_bucket, cap_bucket, ovf, ovf_cap,
+                                      ovf_n);
+    }
+}
+
+// ---- end of the search: each bucket split by the low 7 bits of its x-side tile ----
+// One CTA per bucket: counts per tile, the tiles' starts (bstart / bfill per
+// (window, tile), relative to the window's first bucket), then the records
+// grouped per step and written as runs into their tile.
+__global__ void __launch_bounds__(kPartThreads) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
+                                                         const u32* __restrict__ bcnt, u32 nbh, u32 nbj,
+                                                         u64* __restrict__ D, u32* __restrict__ bstart,
+                                                         u32* __restrict__ bfill) {
     constexpr u32 T = 1u << kHiBits;
-    constexpr int R = 8;
-    constexpr u32 STEP = 1024 * R;
-    __shared__ u32 h[T], st[T];
+    constexpr int R = kPartPerThread;
+    __shared__ PartSmem sm;
     const u32 bk = blockIdx.x;
     const u32 kt = bk / nbh, hi = bk % nbh;
     const u32 cnt = min(bcnt[bk], cap_bucket);
     const u64* src = B + u64(bk) * cap_bucket;
-    if (threadIdx.x < T) h[threadIdx.x] = 0;
+    if (threadIdx.x < T) sm.lcnt[threadIdx.x] = 0;
     __syncthreads();
-    for (u32 s0 = 0; s0 < cnt; s0 += STEP) {
-        u64 r[R];
+    for (u32 s0 = 0; s0 < cnt; s0 += kPartStep) {
+        u32 lo[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
-            const u32 i = s0 + u * 1024 + threadIdx.x;
-            r[u] = i < cnt ? __ldg(src + i) : ~0ull;
+            const u32 i = s0 + u * kPartThreads + threadIdx.x;
+            lo[u] = i < cnt ? (rec_a(__ldg(src + i)) >> kBinJTShift) & (T - 1) : 0xffffffffu;
         }
 #pragma unroll
         for (int u = 0; u < R; ++u)
-            if (r[u] != ~0ull) atomicAdd(&h[(rec_a(r[u]) >> kBinJTShift) & (T - 1)], 1u);
+            if (lo[u] != 0xffffffffu) atomicAdd(&sm.lcnt[lo[u]], 1u);
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of 128 counts, 4 per lane
+    if (threadIdx.x < 32) {  // the tiles' starts inside the bucket: exclusive scan of 128 counts
         const int lane = threadIdx.x;
         u32 c[4], tot = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            c[q] = h[lane * 4 + q];
+            c[q] = sm.lcnt[lane * 4 + q];
             tot += c[q];
         }
         u32 incl = tot;
@@ -189,7 +301,7 @@ __global__ void __launch_bounds__(1024) bin_sort(const u64* __restrict__ B, u32 
         u32 ex = incl - tot;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            st[lane * 4 + q] = ex;
+            sm.runo[lane * 4 + q] = ex;
             ex += c[q];
         }
     }
@@ -197,23 +309,24 @@ __global__ void __launch_bounds__(1024) bin_sort(const u64* __restrict__ B, u32 
     if (threadIdx.x < T) {
         const u32 jt = hi * T + threadIdx.x;
         if (jt < nbj) {
-            bstart[u64(kt) * nbj + jt] = hi * cap_bucket + st[threadIdx.x];
-            bfill[u64(kt) * nbj + jt] = h[threadIdx.x];
+            bstart[u64(kt) * nbj + jt] = hi * cap_bucket + sm.runo[threadIdx.x];
+            bfill[u64(kt) * nbj + jt] = sm.lcnt[threadIdx.x];
         }
-        h[threadIdx.x] = st[threadIdx.x];  // cursors
+        sm.lcnt[threadIdx.x] = 0;
     }
     __syncthreads();
-    u64* dst = D + u64(bk) * cap_bucket;
-    for (u32 s0 = 0; s0 < cnt; s0 += STEP) {
-        u64 r[R];
+    auto region_of = [](u64 r) { return (rec_a(r) >> kBinJTShift) & (T - 1); };
+    u64* dst = D + u64(bk) * cap_bucket;  // every tile inside this bucket: positions are its start + rank
+    for (u32 s0 = 0; s0 < cnt; s0 += kPartStep) {
+        u64 rec[R];
+        u32 rg[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
-            const u32 i = s0 + u * 1024 + threadIdx.x;
-            r[u] = i < cnt ? __ldg(src + i) : ~0ull;
+            const u32 i = s0 + u * kPartThreads + threadIdx.x;
+            rec[u] = i < cnt ? __ldg(src + i) : 0ull;
+            rg[u] = i < cnt ? (rec_a(rec[u]) >> kBinJTShift) & (T - 1) : 0xffffffffu;
         }
-#pragma unroll
-        for (int u = 0; u < R; ++u)
-            if (r[u] != ~0ull) dst[atomicAdd(&h[(rec_a(r[u]) >> kBinJTShift) & (T - 1)], 1u)] = r[u];
+        scatter_step<kPartThreads, R>(sm, rec, rg, T, region_of, dst, 0, cap_bucket, nullptr, 0u, nullptr);
     }
 }
 
@@ -279,6 +392,12 @@ struct BinVerifyArgs {
 };
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return u32(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ u64 ld_stream(const u64* p, u64 pol) {
+    u64 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
 
 __device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2* p, u64 pol) {
     ulonglong2 v;
@@ -352,7 +471,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
 #pragma unroll
             for (int r = 0; r < PR; ++r) {
                 const u32 q = r0 + warp * TPW * PR + tw * PR + r;
-                nrec[r] = q < r1 ? __ldg(Fb + q) : 0ull;
+                nrec[r] = q < r1 ? ld_stream(Fb + q, tpol) : 0ull;  // records stream (evict_first)
             }
             for (u32 q0 = r0 + warp * TPW * PR; q0 < r1; q0 += STRIDE) {  // warp-uniform
                 const u32 qb = q0 + tw * PR;
@@ -372,7 +491,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
 #pragma unroll
                 for (int r = 0; r < PR; ++r) {
                     const u32 q = qb + STRIDE + r;
-                    nrec[r] = q < r1 ? __ldg(Fb + q) : 0ull;
+                    nrec[r] = q < r1 ? ld_stream(Fb + q, tpol) : 0ull;  // records stream (evict_first)
                 }
 #pragma unroll
                 for (int r = 0; r < PR; ++r) {

@@ -287,7 +287,7 @@ struct xyzb_dataset {
     // top-K over all candidates (topk_kernels.cuh)
     DevBuf tk_state, tk_hist, tk_dhist, tk_sint, tk_table, hits2, tk_cnt2;
     // binned verify (binned_verify.cuh): per-window regions, bins by x-side tile, cursors
-    DevBuf bin_b, bin_d, bin_cnt, bin_start, bin_fill, bin_boff, bin_ovf, bin_ovfn, bin_zero;
+    DevBuf bin_s, bin_wcnt, bin_b, bin_d, bin_cnt, bin_start, bin_fill, bin_boff, bin_ovf, bin_ovfn, bin_zero;
     u64 bin_hint = 0;      // mean bucket fill of the last binned search on this dataset (sizes the buckets)
     u64 bin_ovf_hint = 0;  // overflow-list size that last sufficed
     HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
@@ -753,7 +753,7 @@ struct SearchCtx {
     // binned verify (X >> L2): pairs of all batches bucketed by (z window, x tile), verified at the end
     bool binned = false;
     int wshift = 0, nkt = 0;
-    u64 nbj = 0, nbh = 0, cap_bucket = 0, ovf_cap = 0;
+    u64 nbj = 0, nbh = 0, cap_kt = 0, cap_bucket = 0, ovf_cap = 0;
     RunPlan plan;
     xyzb_result* out;
     u64 launches[XYZB_NUM_STAGES] = {};
@@ -1007,13 +1007,19 @@ void binned_verify(SearchCtx& c) {
     const int nkt = c.nkt;
     cudaEvent_t e0 = clk.mark();
     const u32 nbuckets = static_cast<u32>(u64(nkt) * c.nbh);
-    bins::bin_sort<<<nbuckets, 1024, 0, st>>>(ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket), ds->bin_cnt.as<u32>(),
+    const u32 cpk = static_cast<u32>(ceil_div(kSMs * 4, nkt));  // CTAs per window
+    bins::bin_split<<<cpk * nkt, bins::kPartThreads, 0, st>>>(
+        ds->bin_s.as<u64>(), static_cast<u32>(c.cap_kt), ds->bin_wcnt.as<u32>(), cpk, static_cast<u32>(c.nbh),
+        ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket), ds->bin_cnt.as<u32>(), ds->bin_ovf.as<u64>(),
+        static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
+    XYZB_LAUNCH_CHECK();
+    bins::bin_sort<<<nbuckets, bins::kPartThreads, 0, st>>>(ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket), ds->bin_cnt.as<u32>(),
                                               static_cast<u32>(c.nbh), nbj, ds->bin_d.as<u64>(), ds->bin_start.as<u32>(),
                                               ds->bin_fill.as<u32>());
     XYZB_LAUNCH_CHECK();
     bins::bin_scan<<<nkt, 1024, 0, st>>>(ds->bin_fill.as<u32>(), nbj, ds->bin_boff.as<u32>());
     XYZB_LAUNCH_CHECK();
-    c.launches[XYZB_STAGE_JOIN] += 2;
+    c.launches[XYZB_STAGE_JOIN] += 3;
     clk.span(XYZB_STAGE_JOIN, e0, clk.mark());
     bins::BinVerifyArgs A;
     A.Xc = ds->Xc.as<u64>();
@@ -1220,23 +1226,26 @@ void run_batches(SearchCtx& c) {
         int ws = 20;  // z-side windows of ~84 MB (L2-resident while their bins are verified)
         while (ws > 10 && (u64(1) << ws) * ds->Wp * 8 > (u64(88) << 20)) --ws;
         if (const long long w = topt().binned_wshift.load()) ws = static_cast<int>(w);
-        while (ceil_div(p, u64(1) << ws) * ceil_div(ceil_div(p, bins::kBinJT), u64(1) << bins::kHiBits) >
-               bins::kMaxBuckets)
-            ++ws;
+        while (ceil_div(p, u64(1) << ws) > bins::kMaxRegions) ++ws;
         c.wshift = ws;
         c.nkt = static_cast<int>(ceil_div(p, u64(1) << ws));
         c.nbj = ceil_div(p, bins::kBinJT);
         c.nbh = ceil_div(c.nbj, u64(1) << bins::kHiBits);
         const u64 nbk = u64(c.nkt) * c.nbh;
-        // bucket capacity: 1.25x the last search's mean fill (+4096), else the batches' pair capacity spread evenly
+        // capacities: 1.25x the last search's mean fills (+ slack), else the batches' pair capacity spread evenly
         const u64 mean = ds->bin_hint ? ds->bin_hint : ceil_div(nbatches * c.pair_cap, 2 * nbk);
         c.cap_bucket = std::min<u64>(0xffffffffull / nbk, mean + mean / 4 + 4096);
+        c.cap_kt = std::min<u64>(0xffffffffull / u64(c.nkt), c.nbh * mean + c.nbh * mean / 4 + 65536);
         c.ovf_cap = std::min<u64>(0xffffffffull,
                                   std::max<u64>({u64(1) << 20, nbk * c.cap_bucket / 16, ds->bin_ovf_hint}));
-        if (const long long cap = topt().binned_cap.load()) {  // tests: tiny buckets and overflow list (redo path)
+        if (const long long cap = topt().binned_cap.load()) {  // tests: tiny regions and overflow list (redo path)
             c.cap_bucket = std::max<u64>(1, u64(cap));
+            c.cap_kt = c.cap_bucket * c.nbh;
             c.ovf_cap = std::max<u64>(c.cap_bucket, ds->bin_ovf_hint);
         }
+        ds->bin_s.ensure(u64(c.nkt) * c.cap_kt * 8);
+        ds->bin_wcnt.ensure(u64(c.nkt) * 4);
+        XYZB_CUDA(cudaMemsetAsync(ds->bin_wcnt.p, 0, u64(c.nkt) * 4, st));
         ds->bin_b.ensure(nbk * c.cap_bucket * 8);
         ds->bin_d.ensure(nbk * c.cap_bucket * 8);
         ds->bin_cnt.ensure(nbk * 4);
@@ -1516,11 +1525,11 @@ void run_batches(SearchCtx& c) {
             cudaEvent_t ev0 = clk.mark();
             clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
             if (c.binned) {  // the batch's pairs go to their z-side windows; verified after the last batch
-                bins::bin_append<<<kSMs * 4, bins::kAppendThreads, 0, st>>>(
+                bins::bin_window<<<kSMs * 4, bins::kPartThreads, 0, st>>>(
                     ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), A.nitems, A.item_cap,
-                    static_cast<u32>(b0), rsign, static_cast<u32>(nb), c.wshift, static_cast<u32>(c.nbh),
-                    static_cast<u32>(u64(c.nkt) * c.nbh), ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket),
-                    ds->bin_cnt.as<u32>(), ds->bin_ovf.as<u64>(), static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
+                    static_cast<u32>(b0), rsign, static_cast<u32>(nb), c.wshift, static_cast<u32>(c.nkt),
+                    ds->bin_s.as<u64>(), static_cast<u32>(c.cap_kt), ds->bin_wcnt.as<u32>(), ds->bin_ovf.as<u64>(),
+                    static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_JOIN] += 1;
                 clk.span(XYZB_STAGE_JOIN, ev0, clk.mark());
@@ -2105,9 +2114,9 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                 for (u64 b = 0; b < nbt; ++b) tot += np[b];
                 c.bytes[c.pairs_in_sort ? XYZB_STAGE_SORT : XYZB_STAGE_JOIN] += 16 * tot;
                 // binned: level 1 reads 16 B and writes 8 B per pair, level 2 reads 8 B three times and writes 8 B
-                // binned: the append reads the (pa, pb) words and the record, writes 8 B; the bucket split reads
-                // 8 B twice and writes 8 B
-                if (c.binned) c.bytes[XYZB_STAGE_JOIN] += 56 * tot;
+                // binned: the window pass reads the z column and the record and writes 8 B; the bucket and tile
+                // splits each read 8 B twice and write 8 B
+                if (c.binned) c.bytes[XYZB_STAGE_JOIN] += 72 * tot;
                 if (c.topk_all) c.bytes[XYZB_STAGE_MERGE] += 8 * tot;  // pair ranks read by the histogram + emission
             }
             break;

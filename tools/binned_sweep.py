@@ -1,6 +1,8 @@
-"""Measurement (round 2): config 4's binned verify under window sizes and L2
-eviction policies (engine test options binned_wshift / binned_policy);
-device time of one search, best of 3, and the verify's share."""
+"""Measurement (round 2): config 4's binned verify under z-window sizes
+(engine test option binned_wshift); device time of one search, best of 3, the
+verify and join stages, and the top-K against the first setting's.
+  python tools/binned_sweep.py 15,16,17
+"""
 import os
 import sys
 
@@ -19,15 +21,13 @@ ds = xb.Dataset(x)
 ds.search(y, cfg)
 ref = None
 for ws in [int(a) for a in sys.argv[1].split(",")]:
-    for pol in [int(a) for a in sys.argv[2].split(",")]:
-        _lib.set_test_option("binned_wshift", ws)
-        pass
-        best = None
-        for _ in range(3):
-            r = ds.search(y, cfg)
-            if best is None or r.device_ms < best.device_ms:
-                best = r
-        key = [(h.j, h.k, h.strength, h.found_at_repetition) for h in best.top_hits()]
-        ref = ref or key
-        print(f"wshift {ws} policy {pol}: {best.device_ms:.2f} ms  verify {best.stage_ms['verify']:.2f}  "
-              f"join {best.stage_ms['join']:.2f}  same top-K {key == ref}", flush=True)
+    _lib.set_test_option("binned_wshift", ws)
+    best = None
+    for _ in range(3):
+        r = ds.search(y, cfg)
+        if best is None or r.device_ms < best.device_ms:
+            best = r
+    key = [(h.j, h.k, h.strength, h.found_at_repetition) for h in best.top_hits()]
+    ref = ref or key
+    print(f"wshift {ws}: {best.device_ms:.2f} ms  verify {best.stage_ms['verify']:.2f}  "
+          f"join {best.stage_ms['join']:.2f}  same top-K {key == ref}", flush=True)
