@@ -566,7 +566,7 @@ def main():
         binned = binned_verify()
         kern_name = ("verify_binned (x tile in shared memory, z window in L2)" if binned else
                      "verify_pairs_simple (pair-list verify)" if WORKLOAD["mode"] == "binary" else
-                     "verify_items_sign (sign bits x response bit planes)" if WORKLOAD.get("transform") == "sign"
+                     "verify_pairs_sign (sign bits x response bit planes)" if WORKLOAD.get("transform") == "sign"
                      else "verify_items_real<RealStrength>")
         roof = {"bound": "hbm", "kernel": kern_name, "peak": hbm, "peak_source": src, "unit": "GB/s",
                 "algorithmic": {"achieved": alg, "frac": alg / hbm if hbm else None,
