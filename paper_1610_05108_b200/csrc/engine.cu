@@ -1963,11 +1963,27 @@ void check_mode(const xyzb_dataset* ds, const xyzb_params* q, const xyzb_respons
     }
 }
 
+// The binned verify (binned_verify.cuh) sizes its z windows to stay resident
+// in L2 and keeps one CTA per SM: two such searches interleaving on a device
+// evict each other's windows. They take the device in turn (uploads, dataset
+// creation and every other search still overlap them).
+bool binned_eligible(const xyzb_dataset* ds, const xyzb_params* q) {
+    const long long bsel = topt().binned.load();
+    if (bsel < 0 || q->mode != XYZB_MODE_BINARY || !ds->binary || ds->Wp / 2 > 80 || ds->p > (u64(1) << 20))
+        return false;
+    return bsel == 1 || ds->p * ds->Wp * 8 >= (u64(512) << 20);
+}
+std::mutex& device_search_mutex(int dev) {
+    static std::mutex mu[64];
+    return mu[dev & 63];
+}
+
 void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q, const uint32_t* draws,
                xyzb_result* out) {
     Nvtx nv("xyzb_search");
     const auto t0 = std::chrono::steady_clock::now();
     validate_params(q);
+    std::unique_lock<std::mutex> turn;  // taken just before the first kernel, released once the results are home
     DeviceGuard dg(ds->device);
     StreamScope ss(ds->stream);
     Trace tr(ds->stream, false);
@@ -2015,6 +2031,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     u32 fusedK = 0xffffffffu, fusedKK = 0;
     u32 fcap = 0;
     cudaEvent_t ev_dev_end = nullptr;  // end of the device work (results resident in HBM)
+    if (binned_eligible(ds, q)) turn = std::unique_lock<std::mutex>(device_search_mutex(ds->device));
     for (int attempt = 0; attempt < 8; ++attempt) {
         ds->clock.spans.resize(spans0);
         if (c.M <= 31) run_batches<u32>(c); else run_batches<u64>(c);  // u32 holds M bits + the side bit
@@ -2175,6 +2192,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         ds->clock.span(XYZB_STAGE_MERGE, ev_m0, ev_m1);
         ev_dev_end = ev_m1;
     }
+    if (turn.owns_lock()) turn.unlock();
     out->gamma_effective = c.gamma;
     if (c.topk_all) out->gamma_effective = topk_filter(hits, order, topk);
     out->devices_used = 1;
