@@ -119,3 +119,24 @@ def test_binned_guard_aborts(engine_options):
     assert ok, msg
     assert _counters(got) == _counters(ref)
     assert 0 < got.aborted_repetitions < got.repetitions_run
+
+
+def test_binned_overflow_list_in_topk_mode(engine_options):
+    """Small window / bucket regions: part of every window's pairs go to the
+    overflow list (verified by the plain gather, the last top-K phase), the
+    rest through the bins; the top-K over all candidates is unchanged."""
+    xb = _xb()
+    x, y = _data(6000, 2500, 21)
+    cfg = xb.SearchConfig(m=9, l=8, gamma=0.6, seed=13, top_k=200, top_k_mode="candidates",
+                          estimate_complexity=False, threads=1)
+    engine_options(binned=-1)
+    base = xb.Dataset(x).search(y, cfg)
+    engine_options(binned=1, binned_wshift=9, binned_cap=400)
+    ds = xb.Dataset(x)
+    for _ in range(2):  # the first search regrows the overflow list; the second runs with it
+        got = ds.search(y, cfg)
+        assert got.gamma_effective == base.gamma_effective
+        ok, msg = ck.same_hits(got, base)
+        assert ok, msg
+        assert got.top_k == base.top_k
+        assert _counters(got) == _counters(base)
