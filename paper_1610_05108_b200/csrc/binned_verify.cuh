@@ -330,6 +330,58 @@ __global__ void __launch_bounds__(kPartThreads) bin_sort(const u64* __restrict__
     }
 }
 
+// Each tile's records ordered by their x column (6 bits), in place: one CTA
+// per tile, the records in registers, shared counts and ranks, written back
+// through shared memory. A tile above kTileSortMax records stays unordered
+// (the verify is exact either way; the order only lets consecutive pairs
+// share the x column's shared-memory reads).
+constexpr int kTileSortThreads = 256;
+constexpr u32 kTileSortMax = 2048;
+__global__ void __launch_bounds__(kTileSortThreads) tile_sort(u64* __restrict__ D, u32 cap_bucket, u32 nbh, u32 nbj,
+                                                              const u32* __restrict__ bstart,
+                                                              const u32* __restrict__ bfill) {
+    constexpr int R = kTileSortMax / kTileSortThreads;
+    constexpr u32 C = 1u << kBinJTShift;
+    __shared__ u64 buf[kTileSortMax];
+    __shared__ u32 cnt[C], st[C];
+    const u32 t = blockIdx.x;
+    const u32 kt = t / nbj;
+    const u32 fill = bfill[t];
+    if (fill < 3 || fill > kTileSortMax) return;
+    u64* rp = D + u64(kt) * nbh * cap_bucket + bstart[t];
+    if (threadIdx.x < C) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    u64 r[R];
+    u32 rk[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+        const u32 i = u * kTileSortThreads + threadIdx.x;
+        r[u] = i < fill ? rp[i] : 0ull;
+        if (i < fill) rk[u] = atomicAdd(&cnt[rec_a(r[u]) & (C - 1)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const u32 c0 = cnt[2 * lane], c1 = cnt[2 * lane + 1];
+        u32 incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        st[2 * lane] = incl - c0 - c1;
+        st[2 * lane + 1] = incl - c1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+        const u32 i = u * kTileSortThreads + threadIdx.x;
+        if (i < fill) buf[st[rec_a(r[u]) & (C - 1)] + rk[u]] = r[u];
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < fill; i += kTileSortThreads) rp[i] = buf[i];
+}
+
 // One CTA per window: exclusive scan of the tiles' fills -> boff[kt][0..nbj]
 // (compact rank indices; boff[kt][nbj] = the window's pairs held in buckets).
 __global__ void __launch_bounds__(1024) bin_scan(const u32* __restrict__ fill, u32 nbj, u32* __restrict__ boff) {
@@ -493,23 +545,34 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
                     const u32 q = qb + STRIDE + r;
                     nrec[r] = q < r1 ? ld_stream(Fb + q, tpol) : 0ull;  // records stream (evict_first)
                 }
+                // the team's pairs are consecutive records of a tile sorted by x column (tile_sort): a pair
+                // whose x column equals the previous pair's reuses its shared-memory slices
+                u32 jl[PR], acc[PR];
+#pragma unroll
+                for (int r = 0; r < PR; ++r) {
+                    jl[r] = qb + r < r1 ? rec_a(rec[r]) - c0 : 0u;
+                    acc[r] = 0;
+                }
+#pragma unroll
+                for (int it = 0; it < NS; ++it) {
+                    if (FULL || it * G + tl < W2) {
+                        ulonglong2 av = tile[jl[0] * W2 + it * G + tl];
+                        acc[0] += __popcll(av.x ^ kv[0][it].x) + __popcll(av.y ^ kv[0][it].y);
+#pragma unroll
+                        for (int r = 1; r < PR; ++r) {
+                            if (jl[r] != jl[r - 1]) av = tile[jl[r] * W2 + it * G + tl];
+                            acc[r] += __popcll(av.x ^ kv[r][it].x) + __popcll(av.y ^ kv[r][it].y);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < PR; ++r) {
                     const u32 q = qb + r;
-                    const u32 jl = q < r1 ? rec_a(rec[r]) - c0 : 0u;
-                    const ulonglong2* a = tile + jl * W2 + tl;
-                    u32 acc = 0;
+                    u32 a = acc[r];
 #pragma unroll
-                    for (int it = 0; it < NS; ++it) {
-                        if (FULL || it * G + tl < W2) {
-                            const ulonglong2 av = a[it * G];
-                            acc += __popcll(av.x ^ kv[r][it].x) + __popcll(av.y ^ kv[r][it].y);
-                        }
-                    }
-#pragma unroll
-                    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    for (int o = G / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
                     if (tl == 0 && q < r1) {
-                        const u32 si = rec_neg(rec[r]) ? A.n - acc : acc;  // the run's sign (search.cpp:25-36)
+                        const u32 si = rec_neg(rec[r]) ? A.n - a : a;  // the run's sign (search.cpp:25-36)
                         if (ranks) {
                             A.sint_out[rbase + q] = si;
                         } else if (si >= astar) {

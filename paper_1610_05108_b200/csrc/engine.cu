@@ -1017,9 +1017,13 @@ void binned_verify(SearchCtx& c) {
                                               static_cast<u32>(c.nbh), nbj, ds->bin_d.as<u64>(), ds->bin_start.as<u32>(),
                                               ds->bin_fill.as<u32>());
     XYZB_LAUNCH_CHECK();
+    bins::tile_sort<<<static_cast<u32>(u64(nkt) * nbj), bins::kTileSortThreads, 0, st>>>(
+        ds->bin_d.as<u64>(), static_cast<u32>(c.cap_bucket), static_cast<u32>(c.nbh), nbj, ds->bin_start.as<u32>(),
+        ds->bin_fill.as<u32>());
+    XYZB_LAUNCH_CHECK();
     bins::bin_scan<<<nkt, 1024, 0, st>>>(ds->bin_fill.as<u32>(), nbj, ds->bin_boff.as<u32>());
     XYZB_LAUNCH_CHECK();
-    c.launches[XYZB_STAGE_JOIN] += 3;
+    c.launches[XYZB_STAGE_JOIN] += 4;
     clk.span(XYZB_STAGE_JOIN, e0, clk.mark());
     bins::BinVerifyArgs A;
     A.Xc = ds->Xc.as<u64>();
