@@ -20,8 +20,9 @@ cfg = bench.search_config(bench.WORKLOAD["l"])
 ds = xb.Dataset(x)
 ds.search(y, cfg)
 ref = None
+opt = sys.argv[2] if len(sys.argv) > 2 else "binned_wshift"
 for ws in [int(a) for a in sys.argv[1].split(",")]:
-    _lib.set_test_option("binned_wshift", ws)
+    _lib.set_test_option(opt, ws)
     best = None
     for _ in range(3):
         r = ds.search(y, cfg)
@@ -29,5 +30,5 @@ for ws in [int(a) for a in sys.argv[1].split(",")]:
             best = r
     key = [(h.j, h.k, h.strength, h.found_at_repetition) for h in best.top_hits()]
     ref = ref or key
-    print(f"wshift {ws}: {best.device_ms:.2f} ms  verify {best.stage_ms['verify']:.2f}  "
+    print(f"{opt} {ws}: {best.device_ms:.2f} ms  verify {best.stage_ms['verify']:.2f}  "
           f"join {best.stage_ms['join']:.2f}  same top-K {key == ref}", flush=True)
