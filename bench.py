@@ -588,6 +588,11 @@ def main():
                        "note": "1 column + 1 record per pair through L2 over the launch's CUDA-event time",
                        "peak_source": f"measured live: random column-pair gather + XOR-popcount probe on an X of "
                                       f"{wcols} columns x {col} B (one window; paper_1610_05108_b200/csrc/probe.cu)"}
+        if binned:
+            roof["note"] = ("binned verify (csrc/binned_verify.cuh): the x tile sits in shared memory and the z column "
+                            "comes from an L2-resident window, so DRAM carries ~256 B per pair instead of 1619 B "
+                            "(the per-batch verify, 0.97 of HBM at 98 ms); the kernel is bound on-chip (ncu: L1/TEX "
+                            "87 %, profiles/r02_verify_binned_ncu.json), see l2_roofline")
         if traffic and traffic.get("dram_bytes_per_pair") and verify_launches:
             dram_launch = traffic["dram_bytes_per_pair"] * (verified_mine / verify_launches)
             ach = dram_launch / ((verify_ms / verify_launches) / 1e3) / 1e9
