@@ -468,6 +468,37 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// Small transfers between page-locked host memory and the device as a kernel
+// (zero-copy through UVA: the SMs read or write the pinned host buffer over
+// PCIe). They do not queue on the copy engines behind other jobs' large X
+// uploads: with several (X, y) jobs in flight a search's few-KB response,
+// plan and status copies otherwise wait out another job's 400 MB - 1.3 GB
+// upload (e2e traces: 1.4 ms searches taking 4-25 ms).
+__global__ void zc_copy_kernel(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, size_t n) {
+    const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x, nt = size_t(gridDim.x) * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        const size_t n16 = n / 16;
+        for (size_t i = tid; i < n16; i += nt)
+            reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+        for (size_t i = n16 * 16 + tid; i < n; i += nt) dst[i] = src[i];
+    } else {
+        for (size_t i = tid; i < n; i += nt) dst[i] = src[i];
+    }
+}
+
+// dst / src: one side device memory, the other page-locked host memory.
+void small_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    if (bytes > (size_t(4) << 20)) {
+        XYZB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+        return;
+    }
+    const u32 grid = static_cast<u32>(std::min<u64>(64, ceil_div(bytes, 256 * 16)));
+    zc_copy_kernel<<<grid, 256, 0, st>>>(static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst),
+                                         bytes);
+    XYZB_LAUNCH_CHECK();
+}
+
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     constexpr size_t kChunk = size_t(16) << 20;
     if (bytes <= (size_t(1) << 20) || is_pinned(src)) {
@@ -787,7 +818,7 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
             if (v > 0) bits[i >> 6] |= 1ull << (i & 63);
         }
         ds->yk_bits.ensure(Wp * 8);
-        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits, Wp * 8, cudaMemcpyHostToDevice, st));
+        small_copy(ds->yk_bits.p, bits, Wp * 8, st);
         return;
     }
     const double* y = resp->y_real;
@@ -805,7 +836,7 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
     double* cum = reinterpret_cast<double*>(hp);
     ws.copy_cumulative(cum);
     ds->cum.ensure(n * 8);
-    XYZB_CUDA(cudaMemcpyAsync(ds->cum.p, cum, n * 8, cudaMemcpyHostToDevice, st));
+    small_copy(ds->cum.p, cum, n * 8, st);
     hp += n * 8;
     if (c.mode == XYZB_MODE_CONTINUOUS_Y) {
         u64* bits = reinterpret_cast<u64*>(hp);
@@ -823,10 +854,10 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
         ds->spos.ensure(Wp * 8);
         ds->sneg.ensure(Wp * 8);
         ds->wabs.ensure(nb * 8);
-        XYZB_CUDA(cudaMemcpyAsync(ds->yk_bits.p, bits, Wp * 8, cudaMemcpyHostToDevice, st));
-        XYZB_CUDA(cudaMemcpyAsync(ds->spos.p, sp, Wp * 8, cudaMemcpyHostToDevice, st));
-        XYZB_CUDA(cudaMemcpyAsync(ds->sneg.p, sn, Wp * 8, cudaMemcpyHostToDevice, st));
-        XYZB_CUDA(cudaMemcpyAsync(ds->wabs.p, w, nb * 8, cudaMemcpyHostToDevice, st));
+        small_copy(ds->yk_bits.p, bits, Wp * 8, st);
+        small_copy(ds->spos.p, sp, Wp * 8, st);
+        small_copy(ds->sneg.p, sn, Wp * 8, st);
+        small_copy(ds->wabs.p, w, nb * 8, st);
         // |y| quantised to kWeightQB-bit unsigned planes (WeightedQ): q_i = rint(|y_i| scale)
         double ymax = 0.0;
         for (u64 i = 0; i < n; ++i) ymax = std::max(ymax, std::abs(y[i]));
@@ -845,14 +876,14 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
         // |quantised - exact| <= n / (2 scale) over ||y||_1; + slack for the fp64 sums
         c.wqdelta = double(n) / (2.0 * scale * norm) + 1e-9;
         ds->yplanes.ensure(u64(QB) * W * 8);
-        XYZB_CUDA(cudaMemcpyAsync(ds->yplanes.p, pl, u64(QB) * W * 8, cudaMemcpyHostToDevice, st));
+        small_copy(ds->yplanes.p, pl, u64(QB) * W * 8, st);
         return;
     }
     double* yp = reinterpret_cast<double*>(hp);
     std::memset(yp, 0, n4 * 8);
     std::copy(y, y + n, yp);
     ds->yreal.ensure(n4 * 8);
-    XYZB_CUDA(cudaMemcpyAsync(ds->yreal.p, yp, n4 * 8, cudaMemcpyHostToDevice, st));
+    small_copy(ds->yreal.p, yp, n4 * 8, st);
     if (c.q->transform == XYZB_TRANSFORM_SIGN) {
         // q_i = rint(y_i * scale) as two's-complement bit planes 0..B over the row words (SignStrength)
         double ymax = 0.0;
@@ -876,7 +907,7 @@ void upload_response(SearchCtx& c, const xyzb_response* resp) {
         // |quantised - exact| <= 1.5 n / (2 scale norm); + 1e-6 for the fp32 columns of RealStrength
         c.qdelta = 1.5 * double(n) / (2.0 * scale * norm) + 1e-6;
         ds->yplanes.ensure(u64(B + 1) * W * 8);
-        XYZB_CUDA(cudaMemcpyAsync(ds->yplanes.p, pl, u64(B + 1) * W * 8, cudaMemcpyHostToDevice, st));
+        small_copy(ds->yplanes.p, pl, u64(B + 1) * W * 8, st);
     }
 }
 
@@ -1157,21 +1188,23 @@ void run_batches(SearchCtx& c) {
     const bool host_rows = !c.plan.rows.empty();
     // per-batch counters live in their own pinned slots: a later batch must not
     // overwrite a value an earlier, still-queued copy has not read yet
-    const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 2 * R * 4 + 96;
+    const size_t hbytes = R * 4 + R + R * 8 + (host_rows ? R * M * 4 : 0) + 2 * R * 4 + 96 + Rall;
     ds->h_rows.ensure(hbytes);
     char* hp = ds->h_rows.as<char>();
     std::memcpy(hp, c.plan.rid.data(), R * 4);
     std::memcpy(hp + R * 4, c.plan.sign.data(), R);
     std::memcpy(hp + R * 5, c.plan.stream.data(), R * 8);
     if (host_rows) std::memcpy(hp + R * 13, c.plan.rows.data(), R * M * 4);
-    XYZB_CUDA(cudaMemcpyAsync(ds->sign_by_rid.p, c.plan.sign_by_rid.data(), Rall, cudaMemcpyHostToDevice, st));
+    char* hsr = hp + hbytes - Rall;  // the signs by run id, staged in the pinned block too
+    std::memcpy(hsr, c.plan.sign_by_rid.data(), Rall);
+    small_copy(ds->sign_by_rid.p, hsr, Rall, st);
     ds->rid.ensure(R * 4);
     ds->rsign.ensure(R);
     ds->streams.ensure(R * 8);
     ds->rows.ensure(R * M * 4);
-    XYZB_CUDA(cudaMemcpyAsync(ds->rid.p, hp, R * 4, cudaMemcpyHostToDevice, st));
-    XYZB_CUDA(cudaMemcpyAsync(ds->rsign.p, hp + R * 4, R, cudaMemcpyHostToDevice, st));
-    XYZB_CUDA(cudaMemcpyAsync(ds->streams.p, hp + R * 5, R * 8, cudaMemcpyHostToDevice, st));
+    small_copy(ds->rid.p, hp, R * 4, st);
+    small_copy(ds->rsign.p, hp + R * 4, R, st);
+    small_copy(ds->streams.p, hp + R * 5, R * 8, st);
     const bool xy = c.mode == XYZB_MODE_CONTINUOUS_XY;
     const bool unbiased = xy && c.q->transform == XYZB_TRANSFORM_UNBIASED;
     const bool coins = xy && !unbiased && ds->has_zero;
@@ -1179,7 +1212,7 @@ void run_batches(SearchCtx& c) {
     // ---- draws (device RNG, or the caller's rows) ----
     cudaEvent_t ed0 = clk.mark();
     if (host_rows) {
-        XYZB_CUDA(cudaMemcpyAsync(ds->rows.p, hp + R * 13, R * M * 4, cudaMemcpyHostToDevice, st));
+        small_copy(ds->rows.p, hp + R * 13, R * M * 4, st);
     } else {
         draws::draw_runs<<<static_cast<u32>(R), 32, 0, st>>>(
             static_cast<u32>(R), ds->streams.as<u64>(), c.q->seed, c.n, int(M), c.weighted ? ds->cum.as<double>() : nullptr,
@@ -1348,7 +1381,7 @@ void run_batches(SearchCtx& c) {
                 if (coins) {
                     u32* cnt = reinterpret_cast<u32*>(hp + hbytes - 96 - 2 * R * 4) + 2 * batch_idx + 1;
                     *cnt = static_cast<u32>(nb * p);
-                    XYZB_CUDA(cudaMemcpyAsync(ds->zcnt_n.p, cnt, 4, cudaMemcpyHostToDevice, st));
+                    small_copy(ds->zcnt_n.p, cnt, 4, st);
                     scan::exclusive<u32>(ds->zcount.as<u32>(), ds->zcnt_n.as<u32>(), ds->zoff.as<u32>(),
                                          reinterpret_cast<u32*>(ds->partial.p), st, &c.launches[XYZB_STAGE_PROJECT]);
                     real::sign_coins<K><<<static_cast<u32>(nb), real::kMtThreads, 0, st>>>(
@@ -2065,19 +2098,18 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                      o_bin = round_up(o_tk + sizeof(topk::State), 8), sbytes = o_bin + 8;
         ds->h_status.ensure(sbytes);
         char* hs = ds->h_status.as<char>();
-        XYZB_CUDA(cudaMemcpyAsync(hs, ds->hit_count.p, 4, cudaMemcpyDeviceToHost, ds->stream));
-        if (top_counts) XYZB_CUDA(cudaMemcpyAsync(hs + o_cnt, top_counts, 8, cudaMemcpyDeviceToHost, ds->stream));
-        XYZB_CUDA(cudaMemcpyAsync(hs + o_items, ds->nblocks.p, nbt * 4, cudaMemcpyDeviceToHost, ds->stream));
+        small_copy(hs, ds->hit_count.p, 4, ds->stream);
+        if (top_counts) small_copy(hs + o_cnt, top_counts, 8, ds->stream);
+        small_copy(hs + o_items, ds->nblocks.p, nbt * 4, ds->stream);
         if (c.pair_cap)
-            XYZB_CUDA(cudaMemcpyAsync(hs + o_pairs, ds->npairs.p, nbt * 4, cudaMemcpyDeviceToHost, ds->stream));
-        XYZB_CUDA(cudaMemcpyAsync(hs + o_enum, ds->enumerated.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
-        XYZB_CUDA(cudaMemcpyAsync(hs + o_ver, ds->verified.p, Rall * 8, cudaMemcpyDeviceToHost, ds->stream));
-        XYZB_CUDA(cudaMemcpyAsync(hs + o_ovf, ds->povf.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+            small_copy(hs + o_pairs, ds->npairs.p, nbt * 4, ds->stream);
+        small_copy(hs + o_enum, ds->enumerated.p, Rall * 8, ds->stream);
+        small_copy(hs + o_ver, ds->verified.p, Rall * 8, ds->stream);
+        small_copy(hs + o_ovf, ds->povf.p, 4, ds->stream);
         if (c.topk_all)
-            XYZB_CUDA(cudaMemcpyAsync(hs + o_tk, ds->tk_state.p, sizeof(topk::State), cudaMemcpyDeviceToHost,
-                                      ds->stream));
+            small_copy(hs + o_tk, ds->tk_state.p, sizeof(topk::State), ds->stream);
         if (c.binned)
-            XYZB_CUDA(cudaMemcpyAsync(hs + o_bin, ds->bin_ovfn.p, 4, cudaMemcpyDeviceToHost, ds->stream));
+            small_copy(hs + o_bin, ds->bin_ovfn.p, 4, ds->stream);
         tr.mark("search:launch");
         XYZB_CUDA(cudaStreamSynchronize(ds->stream));
         tr.mark("search:device");
@@ -2169,9 +2201,9 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             const size_t hb = u64(fusedK) * sizeof(xyzb_hit), ob = u64(fusedK) * 8, tb = u64(fusedKK) * 8;
             ds->h_merge.ensure(hb + ob + tb + 8);
             char* hp = ds->h_merge.as<char>();
-            XYZB_CUDA(cudaMemcpyAsync(hp, ds->fin.p, hb, cudaMemcpyDeviceToHost, ds->stream));
-            XYZB_CUDA(cudaMemcpyAsync(hp + hb, ds->fin_order.p, ob, cudaMemcpyDeviceToHost, ds->stream));
-            if (tb) XYZB_CUDA(cudaMemcpyAsync(hp + hb + ob, ds->topidx.p, tb, cudaMemcpyDeviceToHost, ds->stream));
+            small_copy(hp, ds->fin.p, hb, ds->stream);
+            small_copy(hp + hb, ds->fin_order.p, ob, ds->stream);
+            if (tb) small_copy(hp + hb + ob, ds->topidx.p, tb, ds->stream);
             XYZB_CUDA(cudaStreamSynchronize(ds->stream));
             std::memcpy(hits.data(), hp, hb);
             std::memcpy(order.data(), hp + hb, ob);
