@@ -107,3 +107,23 @@ def test_bad_device_list_is_a_data_error():
     x = ck.ref_rademacher(64, 10, 1, 1)
     with pytest.raises(xb.DataError):
         xb.Dataset(x, devices=[0, 99])
+
+
+@pytest.mark.parametrize("topk_mode", ["hits", "candidates"])
+def test_binned_replicas_equal_single_device(engine_options, topk_mode):
+    """The binned verify on replicas: each shard bins and verifies its own
+    runs; binned searches on one device take it in turn (the replicas here
+    share device 0), so the shards serialise without deadlock."""
+    xb = _xb()
+    x = ck.ref_rademacher(5000, 3000, 9, 4)
+    y = np.where(np.random.default_rng(2).random(5000) < 0.5, 1, -1).astype(np.int8)
+    engine_options(binned=1, binned_wshift=10)
+    cfg = xb.SearchConfig(m=10, l=12, gamma=0.52, seed=3, top_k=40, top_k_mode=topk_mode, threads=1,
+                          estimate_complexity=False)
+    one = xb.Dataset(x).search(y, cfg)
+    got = xb.Dataset(x, devices=[0, 0, 0]).search(y, cfg)
+    _same(got, one)
+    assert got.devices_used == 3
+    if topk_mode == "hits":
+        ok, msg = ck.same_hits(got, ck.ref_search(x, y, cfg))
+        assert ok, msg
