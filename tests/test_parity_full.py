@@ -119,3 +119,25 @@ def test_cfg3_full_size_within_tolerance():
     assert len(tk.top_k) == 1000
     g, rep, _ = ck.ref_topk_candidates(x, y, cfg, 1000, gamma_start=0.55, step=0.005, threads=THREADS)
     _compare_continuous_topk(tk, rep.hits, 1000)
+
+
+def test_cfg4_bench_workload_binned_equals_per_batch_verify(cfg4_data, engine_options):
+    """The bench's exact config-4 workload (L = 400 per pass, 800 runs, top-K
+    = 1000 over all ~3.9e8 verified candidates): the binned verify the bench
+    times against the per-batch verify (pinned to the reference above at
+    L = 4) — identical top-K list, effective gamma and counters."""
+    xb = _xb()
+    x, y, _ = cfg4_data
+    cfg = xb.SearchConfig(m=20, l=400, gamma=0.55, seed=7, top_k=1000, top_k_mode="candidates",
+                          estimate_complexity=False, threads=1)
+    ds = xb.Dataset(x)
+    binned = ds.search(y, cfg)
+    engine_options(binned=-1)
+    per_batch = ds.search(y, cfg)
+    assert len(binned.top_k) == 1000
+    assert binned.gamma_effective == per_batch.gamma_effective
+    assert ck.hit_tuples(binned.top_hits()) == ck.hit_tuples(per_batch.top_hits())
+    ok, msg = ck.same_hits(binned, per_batch)
+    assert ok, msg
+    for f in ("repetitions_run", "aborted_repetitions", "candidates_enumerated", "verified_pairs"):
+        assert getattr(binned, f) == getattr(per_batch, f), f
