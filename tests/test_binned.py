@@ -49,6 +49,23 @@ def test_binned_hits_equal_reference(engine_options, n, p, m, l, gamma, wshift):
     assert len(got.hits) > 0
 
 
+# every grouping path feeds the binned verify: the hashed partition join (sparse 2^24 space), the
+# sorted path with 64-bit keys (M = 40: next to no candidates), the split grouping; n = 64 is one word
+@pytest.mark.parametrize("n,p,m,l,gamma", [(3000, 4000, 24, 4, 0.5), (3000, 3000, 40, 3, 0.5),
+                                            (64, 3000, 12, 6, 0.7), (2000, 5000, 14, 3, 0.53)])
+def test_binned_grouping_paths_equal_reference(engine_options, n, p, m, l, gamma):
+    xb = _xb()
+    x, y = _data(n, p, 3 * n + p + m)
+    engine_options(binned=1, binned_wshift=10)
+    cfg = xb.SearchConfig(m=m, l=l, gamma=gamma, seed=9, top_k=15, estimate_complexity=False, threads=1)
+    got = xb.Dataset(x).search(y, cfg)
+    ref = ck.ref_search(x, y, cfg)
+    ok, msg = ck.same_hits(got, ref)
+    assert ok, msg
+    assert got.top_k == ref.top_k
+    assert _counters(got) == _counters(ref)
+
+
 def test_binned_planted_pair_and_stop_after_first_hit(engine_options):
     xb = _xb()
     x, y = ck.ref_planted(6000, 3000, 11, 2900, 0.8, 9)
