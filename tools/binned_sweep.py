@@ -1,7 +1,7 @@
 """Measurement (round 2): config 4's binned verify under z-window sizes
 (engine test option binned_wshift); device time of one search, best of 3, the
 verify and join stages, and the top-K against the first setting's.
-  python tools/binned_sweep.py 15,16,17
+  python tools/binned_sweep.py 15,16,17 [option] [config]
 """
 import os
 import sys
@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 from paper_1610_05108_b200 import _lib  # noqa: E402
 
-bench.select("large")
+bench.select(sys.argv[3] if len(sys.argv) > 3 else "large")
 import paper_1610_05108_b200 as xb  # noqa: E402
 
 x, y, _ = bench.make_data()
