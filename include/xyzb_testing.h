@@ -21,6 +21,9 @@
  *   binned_wshift   z-side windows of 2^value columns (several windows at
  *                   small p)
  *   binned_cap      initial window-region capacity in pairs (the regrow path)
+ *   one_pass_join   1 = the binned verify's one-pass partition join even when
+ *                   runs are expected near the guard (aborted runs' pairs are
+ *                   then dropped while binned)
  * Returns XYZB_OK, or XYZB_E_DATA for an unknown name.
  */
 #ifndef XYZB_TESTING_H

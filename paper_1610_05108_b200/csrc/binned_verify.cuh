@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kPartThreads) bin_window(const PairRec* __rest
                                                            const u32* __restrict__ npairs, u32 pair_cap,
                                                            const u32* __restrict__ nitems, u32 item_cap, u32 run0,
                                                            const int8_t* __restrict__ run_sign, u32 nruns,
+                                                           const u64* __restrict__ tot, u64 guard,
                                                            int wshift, u32 nkt, u64* __restrict__ S, u32 cap_kt,
                                                            u32* __restrict__ wcnt, u64* __restrict__ ovf, u32 ovf_cap,
                                                            u32* __restrict__ ovf_n) {
@@ -173,7 +174,9 @@ __global__ void __launch_bounds__(kPartThreads) bin_window(const PairRec* __rest
     __shared__ int8_t neg[kMaxRunsPerBatch];
     const u32 P = topk::batch_pairs(npairs, pair_cap, nitems, item_cap);
     for (u32 t = threadIdx.x; t < nkt; t += blockDim.x) cnt[t] = 0;
-    for (u32 t = threadIdx.x; t < nruns; t += blockDim.x) neg[t] = run_sign[t] < 0 ? 1 : 0;
+    // bit 0: the run's pass is negative; bit 1: the run is over the guard (a one-pass join emitted it anyway)
+    for (u32 t = threadIdx.x; t < nruns; t += blockDim.x)
+        neg[t] = int8_t((run_sign[t] < 0 ? 1 : 0) | (tot[t] > guard ? 2 : 0));
     __syncthreads();
     const uint4* P4 = reinterpret_cast<const uint4*>(pairs);
     for (u64 s0 = u64(blockIdx.x) * kPartStep; s0 < P; s0 += u64(gridDim.x) * kPartStep) {
@@ -183,8 +186,8 @@ __global__ void __launch_bounds__(kPartThreads) bin_window(const PairRec* __rest
         for (int u = 0; u < R; ++u) {
             const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
             const uint4 pr = i < P ? __ldg(P4 + i) : make_uint4(0, 0, 0, 0);
-            rec[u] = rec_make(pr.x, pr.y, (pr.w >> 1) & 1u, neg[pr.z], run0 + pr.z);
-            kt[u] = i < P ? pr.y >> wshift : 0xffffffffu;
+            rec[u] = rec_make(pr.x, pr.y, (pr.w >> 1) & 1u, neg[pr.z] & 1, run0 + pr.z);
+            kt[u] = i < P && !(neg[pr.z] & 2) ? pr.y >> wshift : 0xffffffffu;
         }
 #pragma unroll
         for (int u = 0; u < R; ++u)

@@ -61,7 +61,7 @@ namespace {
 // the fp32 verify beside the sign-bit one. 0 = the engine's own choice.
 struct TestOptions {
     std::atomic<long long> batch_entries{0}, hit_cap{0}, item_cap{0}, pair_cap{0}, grouping{0}, merge_large{0},
-        sign_verify_off{0}, trace{0}, brute_cuda{0}, binned{0}, binned_wshift{0}, binned_cap{0};
+        sign_verify_off{0}, trace{0}, brute_cuda{0}, binned{0}, binned_wshift{0}, binned_cap{0}, one_pass_join{0};
 };
 TestOptions& topt() {
     static TestOptions* o = new TestOptions();  // leaked on purpose (outlives static destructors)
@@ -783,6 +783,7 @@ struct SearchCtx {
     u64 tk_table = 0;      // dedup table slots (power of two)
     // binned verify (X >> L2): pairs of all batches bucketed by (z window, x tile), verified at the end
     bool binned = false;
+    bool no_one_pass = false;  // a one-pass join overflowed the pair list: the redo counts first
     int wshift = 0, nkt = 0;
     u64 nbj = 0, nbh = 0, cap_kt = 0, cap_bucket = 0, ovf_cap = 0;
     RunPlan plan;
@@ -1333,6 +1334,12 @@ void run_batches(SearchCtx& c) {
         ds->slots.ensure(kSMs * 4);
         XYZB_CUDA(cudaMemsetAsync(ds->slots.p, 0, kSMs * 4, st));
     }
+    // the binned verify bins the pairs after the join, so a dense partition join can emit in the same pass
+    // as it counts |E_r| when the runs are expected far below the guard (p^2 / 2^M <= guard / 8): a run that
+    // still turns out over the guard has its pairs dropped by bin_window
+    const bool one_pass_join = c.binned && part_path && !part_hash && !c.no_one_pass &&
+                               (double(p) * double(p) / std::ldexp(1.0, int(M)) <= double(c.guard) / 8.0 ||
+                                topt().one_pass_join.load() == 1);
     const int bits = static_cast<int>(M);
     for (u64 b0 = 0, batch_idx = 0; b0 < R; b0 += B, ++batch_idx) {
         const u64 nb = std::min(B, R - b0);
@@ -1417,8 +1424,8 @@ void run_batches(SearchCtx& c) {
                                        ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(), nitems,
                                        static_cast<u32>(item_cap), npairs_b, ds->pairs.as<kern::PairRec>(),
                                        static_cast<u32>(c.pair_cap), ds->pgrp.as<u32>(), ds->pent.as<uint2>(),
-                                       ds->povf.as<u32>(), st);
-                c.launches[XYZB_STAGE_JOIN] += 2;
+                                       ds->povf.as<u32>(), st, one_pass_join);
+                c.launches[XYZB_STAGE_JOIN] += one_pass_join ? 1 : 2;
             } else {
                 throw internal_error("xyzb: partitioned grouping needs 32-bit keys");
             }
@@ -1564,7 +1571,8 @@ void run_batches(SearchCtx& c) {
             if (c.binned) {  // the batch's pairs go to their z-side windows; verified after the last batch
                 bins::bin_window<<<kSMs * 4, bins::kPartThreads, 0, st>>>(
                     ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), A.nitems, A.item_cap,
-                    static_cast<u32>(b0), rsign, static_cast<u32>(nb), c.wshift, static_cast<u32>(c.nkt),
+                    static_cast<u32>(b0), rsign, static_cast<u32>(nb), ds->tot.as<u64>(), c.guard, c.wshift,
+                    static_cast<u32>(c.nkt),
                     ds->bin_s.as<u64>(), static_cast<u32>(c.cap_kt), ds->bin_wcnt.as<u32>(), ds->bin_ovf.as<u64>(),
                     static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
                 XYZB_LAUNCH_CHECK();
@@ -2125,6 +2133,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             const u32* np = reinterpret_cast<const u32*>(hs + o_pairs);
             pneed = *std::max_element(np, np + nbt);
             if (pneed > c.pair_cap) {
+                c.no_one_pass = true;  // an aborted run's pairs (a one-pass join) may be what overflowed
                 if (c.pair_cap == 0xffffffffull) throw internal_error("xyzb: candidate pairs exceed 2^32 in one batch");
                 c.pair_scale *= std::max<u64>(2, ceil_div(pneed, c.pair_cap));
             }
@@ -3354,6 +3363,7 @@ int xyzb_test_set_option(const char* name, long long value) {
                                    : s == "binned"          ? &o.binned
                                    : s == "binned_wshift"   ? &o.binned_wshift
                                    : s == "binned_cap"      ? &o.binned_cap
+                                   : s == "one_pass_join"   ? &o.one_pass_join
                                                             : nullptr;
     if (!slot) return XYZB_E_DATA;
     slot->store(value);

@@ -22,6 +22,9 @@
 //   part_join<0>  per (run, partition): bucket counts of the 2^lb local
 //                 buckets in shared memory -> |E_r| incl. the diagonal and
 //                 the canonical work (guard, pair_search.hpp:91-94)
+//   part_join<2>  both in one pass (the binned verify, when the expected |E_r|
+//                 is far below the guard): the pairs of a run that turns out
+//                 aborted are dropped when they are binned (bin_window)
 //   part_join<1>  per (run, partition) of a kept run: counts, scan, scatter of
 //                 the columns into the run's grouped array, then the blocks
 //                 (pairs of small blocks written warp-cooperatively, items for
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     const u32 D = 1u << k, L = 1u << lb, lmask = L - 1u;
     const u32 mask = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
     const u32 c = xorc[b] & mask;
-    if (EMIT && tot[b] > guard) return;  // aborted run: nothing to emit (uniform per CTA)
+    if (EMIT == 1 && tot[b] > guard) return;  // aborted run: nothing to emit (uniform per CTA)
     const u32 beg = pbeg[u64(b) * (D + 1) + d], end = pbeg[u64(b) * (D + 1) + d + 1];
     const u32 cnt = end - beg;
     const uint2* e = pe + u64(b) * p + beg;
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     if (cnt < 2) {
         // no block with work; a lone column of a c == 0 run still counts its
         // diagonal pair in |E_r| (pair_search.cpp:48-49)
-        if (!EMIT && c == 0 && threadIdx.x == 0 && cnt == 1)
+        if (EMIT != 1 && c == 0 && threadIdx.x == 0 && cnt == 1)
             atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), 1ull);
         return;
     }
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     // c != 0: buckets u (even) and u | 1 form one block; c == 0: every bucket
     // is a diagonal block. li walks the block heads.
     const u32 NL = c ? L / 2 : L;
-    if (!EMIT) {
+    if (EMIT != 1) {  // |E_r| incl. the diagonal and the canonical work (EMIT = 2: then emit regardless)
         u64 pa = 0, wa = 0;
         for (u32 li = threadIdx.x; li < NL; li += blockDim.x) {
             if (c == 0) {
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
             if (a) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(a));
             if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
         }
-        return;
+        if (EMIT == 0) return;
     }
     // bucket starts, scatter (T ends as bucket ends), then the blocks
     part_table_scan(T, L, ws);
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
         return;
     }
     if (cnt < 2) {
-        if (!EMIT && c == 0 && threadIdx.x == 0 && cnt == 1)
+        if (EMIT != 1 && c == 0 && threadIdx.x == 0 && cnt == 1)
             atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), 1ull);
         return;
     }
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
             if (a) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(a));
             if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
         }
-        return;
+        if (EMIT == 0) return;
     }
     // Only keys that are in a block are grouped: c == 0, a key with >= 2
     // records (a diagonal block); else a slot holding both keys of the pair.
@@ -721,7 +724,7 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, b
 inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* xorc, u64 guard, u32 hmax,
                              u32* grouped, u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap,
                              u32* npairs, PairRec* pairs, u32 pair_cap, const u32* scratch, const uint2* pe,
-                             u32* ovf, cudaStream_t st) {
+                             u32* ovf, cudaStream_t st, bool one_pass = false) {
     const int lb = M - k;
     const u64 D = u64(1) << k;
     const u32* pbeg = scratch + 2 * B * D;
@@ -736,6 +739,14 @@ inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* x
         XYZB_LAUNCH_CHECK();
         part_join_hash<1><<<gj, kHsThreads, part_hash_smem(true), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot, work_run,
                                                      items, nitems, item_cap, npairs, pairs, pair_cap, ovf);
+        XYZB_LAUNCH_CHECK();
+        return;
+    }
+    if (one_pass) {
+        func_smem(part_join<2>, 64 << 10);
+        part_join<2><<<gj, kPjThreads, part_join_smem(lb), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
+                                                                work_run, items, nitems, item_cap, npairs, pairs,
+                                                                pair_cap);
         XYZB_LAUNCH_CHECK();
         return;
     }

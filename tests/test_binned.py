@@ -157,3 +157,28 @@ def test_binned_overflow_list_in_topk_mode(engine_options):
         assert ok, msg
         assert got.top_k == base.top_k
         assert _counters(got) == _counters(base)
+
+
+@pytest.mark.parametrize("mode", ["hits", "candidates"])
+def test_binned_one_pass_join_with_aborted_runs(engine_options, mode):
+    """The one-pass partition join (|E_r| counted while the pairs are
+    emitted) forced where about half the runs go over the guard: their pairs
+    are dropped when binned, counters and hits equal the reference's."""
+    xb = _xb()
+    x, y = _data(5000, 3000, 31)
+    engine_options(binned=1, binned_wshift=10, grouping="part", one_pass_join=1)
+    cfg = xb.SearchConfig(m=8, l=8, gamma=0.53, seed=6, top_k=25, top_k_mode=mode, estimate_complexity=False,
+                          threads=1, max_candidates_per_rep=10 ** 12)
+    ds = xb.Dataset(x)
+    free = ds.search(y, cfg)
+    cfg = replace(cfg, max_candidates_per_rep=free.candidates_enumerated // free.repetitions_run)
+    got = ds.search(y, cfg)
+    assert 0 < got.aborted_repetitions < got.repetitions_run
+    engine_options(one_pass_join=0, binned=-1)
+    base = xb.Dataset(x).search(y, cfg)
+    ok, msg = ck.same_hits(got, base)
+    assert ok, msg
+    assert got.top_k == base.top_k and _counters(got) == _counters(base)
+    if mode == "hits":
+        ok, msg = ck.same_hits(got, ck.ref_search(x, y, cfg))
+        assert ok, msg
