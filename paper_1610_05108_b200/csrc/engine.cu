@@ -1337,6 +1337,8 @@ void run_batches(SearchCtx& c) {
     // the binned verify bins the pairs after the join, so a dense partition join can emit in the same pass
     // as it counts |E_r| when the runs are expected far below the guard (p^2 / 2^M <= guard / 8): a run that
     // still turns out over the guard has its pairs dropped by bin_window
+    // binary keys of the partition path: the projection counts the partition sizes itself
+    const bool fused_count = part_path && !xy && sizeof(K) == 4 && M <= 31;
     const bool one_pass_join = c.binned && part_path && !part_hash && !c.no_one_pass &&
                                (double(p) * double(p) / std::ldexp(1.0, int(M)) <= double(c.guard) / 8.0 ||
                                 topt().one_pass_join.load() == 1);
@@ -1350,7 +1352,20 @@ void run_batches(SearchCtx& c) {
         K* k0 = ds->keys[0].as<K>();
         cudaEvent_t e0 = clk.mark();
         // ---- project ----
-        if (!xy) {
+        if (!xy && fused_count) {  // xorc first, then the keys with the partition sizes counted on the fly
+            if constexpr (sizeof(K) == 4) {
+                kern::ykey_xorc<K><<<static_cast<u32>(ceil_div(nb, 128)), 128, 0, st>>>(
+                    rows, int(M), ds->yk_bits.as<u64>(), rsign, static_cast<u32>(nb), ds->xorc.as<K>());
+                XYZB_LAUNCH_CHECK();
+                XYZB_CUDA(cudaMemsetAsync(ds->pgrp.p, 0, (nb << pk) * 4, st));
+                dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
+                kern::project_count<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), k0,
+                                                       ds->xorc.as<K>(), int(M) - pk, part_hash ? 1 : 0,
+                                                       ds->pgrp.as<u32>());
+                XYZB_LAUNCH_CHECK();
+                c.launches[XYZB_STAGE_PROJECT] += 2;
+            }
+        } else if (!xy) {
             dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
             kern::project_bits_t<K><<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), k0);
             XYZB_LAUNCH_CHECK();
@@ -1413,8 +1428,9 @@ void run_batches(SearchCtx& c) {
             // ---- group: partition pass (per-run partitions that hold both sides of every block) ----
             if constexpr (sizeof(K) == 4) {
                 kern::part_partition_launch(k0, nb, p, int(M), pk, part_hash, ds->xorc.as<K>(), ds->tot.as<u64>(),
-                                            ds->work_run.as<u64>(), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st);
-                c.launches[XYZB_STAGE_SORT] += 3;
+                                            ds->work_run.as<u64>(), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st,
+                                            fused_count);
+                c.launches[XYZB_STAGE_SORT] += fused_count ? 2 : 3;
                 e2 = clk.mark();
                 clk.span(XYZB_STAGE_SORT, e1, e2);
                 c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);  // keys read twice, records written

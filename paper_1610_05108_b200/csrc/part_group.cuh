@@ -152,6 +152,51 @@ __device__ __forceinline__ void part_tile(const u32* __restrict__ keys, u64 p, i
     }
 }
 
+// The projection (project_bits_t's u32 form) with the partition count fused:
+// each thread's 32 keys are counted into a shared histogram of partition
+// digits right after the transpose, so part_count's re-read of the keys is
+// not needed (xorc must be computed before: ykey_xorc runs first).
+__global__ void __launch_bounds__(128) project_count(const u32* __restrict__ Xr, u64 P32, u64 p,
+                                                     const u32* __restrict__ rows, int M, u32* __restrict__ keys,
+                                                     const u32* __restrict__ xorc, int lb, int hashed,
+                                                     u32* __restrict__ pcnt) {
+    __shared__ u32 srow[64];
+    __shared__ u32 h[1u << kPgMaxK];
+    const u64 b = blockIdx.y;
+    const int k = M - lb;
+    const u32 D = 1u << k;
+    const u32 mask = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
+    if (threadIdx.x < M) srow[threadIdx.x] = rows[b * M + threadIdx.x];
+    for (u32 d = threadIdx.x; d < D; d += blockDim.x) h[d] = 0;
+    __syncthreads();
+    const u64 word = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (word < P32) {
+        const u64 col0 = word * 32;
+        const u32 ncol = u32(minu(32, p - col0));
+        u32 a[32];
+#pragma unroll
+        for (int s = 0; s < 32; ++s) a[s] = s < M ? __ldg(Xr + u64(srow[s]) * P32 + word) : 0u;
+        transpose32(a);
+        u32* out = keys + b * p + col0;
+        if (ncol == 32 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            uint4* o4 = reinterpret_cast<uint4*>(out);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) o4[c] = make_uint4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (u32(c) < ncol) out[c] = a[c];
+        }
+        const PartMap pm(xorc[b] & mask);
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (u32(c) < ncol) atomicAdd(&h[part_digit(pm.fwd(a[c] & mask), lb, k, hashed != 0)], 1u);
+    }
+    __syncthreads();
+    for (u32 d = threadIdx.x; d < D; d += blockDim.x)
+        if (h[d]) atomicAdd(pcnt + b * D + d, h[d]);
+}
+
 __global__ void __launch_bounds__(kPgThreads) part_count(const u32* __restrict__ keys, u64 p, int M, int lb,
                                                          int hashed, const u32* __restrict__ xorc,
                                                          u32* __restrict__ pcnt) {
@@ -701,8 +746,10 @@ inline int part_digits_hash(int M, u64 p) {
 // pcnt / cursor B * 2^k u32, pbeg B * (2^k + 1) u32; pe: B * p (w, column).
 inline u64 part_scratch_words(int k, u64 B) { return B * ((u64(1) << k) * 3 + 1); }
 
+// counted: the partition sizes are already in scratch[0, B * 2^k) (project_count)
 inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, bool hashed, const u32* xorc,
-                                  u64* tot, u64* work_run, u32* scratch, uint2* pe, cudaStream_t st) {
+                                  u64* tot, u64* work_run, u32* scratch, uint2* pe, cudaStream_t st,
+                                  bool counted = false) {
     const int lb = M - k;
     const u64 D = u64(1) << k;
     u32* pcnt = scratch;
@@ -710,10 +757,12 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, b
     u32* pbeg = scratch + 2 * B * D;
     func_smem(part_count, 64 << 10);
     func_smem(part_scatter, 64 << 10);
-    XYZB_CUDA(cudaMemsetAsync(pcnt, 0, B * D * 4, st));
     dim3 gt(static_cast<u32>(ceil_div(p, kPgTile)), static_cast<u32>(B));
-    part_count<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, hashed ? 1 : 0, xorc, pcnt);
-    XYZB_LAUNCH_CHECK();
+    if (!counted) {
+        XYZB_CUDA(cudaMemsetAsync(pcnt, 0, B * D * 4, st));
+        part_count<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, hashed ? 1 : 0, xorc, pcnt);
+        XYZB_LAUNCH_CHECK();
+    }
     part_scan<<<static_cast<u32>(B), 1024, 0, st>>>(pcnt, k, p, pbeg, cursor, tot, work_run);
     XYZB_LAUNCH_CHECK();
     part_scatter<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, hashed ? 1 : 0, xorc, cursor, pe);
