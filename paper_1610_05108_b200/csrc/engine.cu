@@ -1339,6 +1339,9 @@ void run_batches(SearchCtx& c) {
     // still turns out over the guard has its pairs dropped by bin_window
     // binary keys of the partition path: the projection counts the partition sizes itself
     const bool fused_count = part_path && !xy && sizeof(K) == 4 && M <= 31;
+    // ... and with the binned verify nothing reads the keys afterwards (hits recompute a key from the draws):
+    // the partition records come from the row planes directly
+    const bool keyless = fused_count && c.binned;
     const bool one_pass_join = c.binned && part_path && !part_hash && !c.no_one_pass &&
                                (double(p) * double(p) / std::ldexp(1.0, int(M)) <= double(c.guard) / 8.0 ||
                                 topt().one_pass_join.load() == 1);
@@ -1359,9 +1362,9 @@ void run_batches(SearchCtx& c) {
                 XYZB_LAUNCH_CHECK();
                 XYZB_CUDA(cudaMemsetAsync(ds->pgrp.p, 0, (nb << pk) * 4, st));
                 dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
-                kern::project_count<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), k0,
-                                                       ds->xorc.as<K>(), int(M) - pk, part_hash ? 1 : 0,
-                                                       ds->pgrp.as<u32>());
+                auto* pc = keyless ? kern::project_count<false> : kern::project_count<true>;
+                pc<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), k0, ds->xorc.as<K>(),
+                                      int(M) - pk, part_hash ? 1 : 0, ds->pgrp.as<u32>());
                 XYZB_LAUNCH_CHECK();
                 c.launches[XYZB_STAGE_PROJECT] += 2;
             }
@@ -1429,8 +1432,16 @@ void run_batches(SearchCtx& c) {
             if constexpr (sizeof(K) == 4) {
                 kern::part_partition_launch(k0, nb, p, int(M), pk, part_hash, ds->xorc.as<K>(), ds->tot.as<u64>(),
                                             ds->work_run.as<u64>(), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st,
-                                            fused_count);
+                                            fused_count, !keyless);
                 c.launches[XYZB_STAGE_SORT] += fused_count ? 2 : 3;
+                if (keyless) {  // the records straight from the row planes (no key array)
+                    const u64 D = u64(1) << pk;
+                    dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
+                    kern::project_scatter<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M),
+                                                             ds->xorc.as<K>(), int(M) - pk, part_hash ? 1 : 0,
+                                                             ds->pgrp.as<u32>() + nb * D, ds->pent.as<uint2>());
+                    XYZB_LAUNCH_CHECK();
+                }
                 e2 = clk.mark();
                 clk.span(XYZB_STAGE_SORT, e1, e2);
                 c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);  // keys read twice, records written

@@ -156,6 +156,7 @@ __device__ __forceinline__ void part_tile(const u32* __restrict__ keys, u64 p, i
 // each thread's 32 keys are counted into a shared histogram of partition
 // digits right after the transpose, so part_count's re-read of the keys is
 // not needed (xorc must be computed before: ykey_xorc runs first).
+template <bool STORE_KEYS>
 __global__ void __launch_bounds__(128) project_count(const u32* __restrict__ Xr, u64 P32, u64 p,
                                                      const u32* __restrict__ rows, int M, u32* __restrict__ keys,
                                                      const u32* __restrict__ xorc, int lb, int hashed,
@@ -177,15 +178,17 @@ __global__ void __launch_bounds__(128) project_count(const u32* __restrict__ Xr,
 #pragma unroll
         for (int s = 0; s < 32; ++s) a[s] = s < M ? __ldg(Xr + u64(srow[s]) * P32 + word) : 0u;
         transpose32(a);
-        u32* out = keys + b * p + col0;
-        if (ncol == 32 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-            uint4* o4 = reinterpret_cast<uint4*>(out);
+        if (STORE_KEYS) {
+            u32* out = keys + b * p + col0;
+            if (ncol == 32 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+                uint4* o4 = reinterpret_cast<uint4*>(out);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) o4[c] = make_uint4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
-        } else {
+                for (int c = 0; c < 8; ++c) o4[c] = make_uint4(a[4 * c], a[4 * c + 1], a[4 * c + 2], a[4 * c + 3]);
+            } else {
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (u32(c) < ncol) out[c] = a[c];
+                for (int c = 0; c < 32; ++c)
+                    if (u32(c) < ncol) out[c] = a[c];
+            }
         }
         const PartMap pm(xorc[b] & mask);
 #pragma unroll
@@ -195,6 +198,53 @@ __global__ void __launch_bounds__(128) project_count(const u32* __restrict__ Xr,
     __syncthreads();
     for (u32 d = threadIdx.x; d < D; d += blockDim.x)
         if (h[d]) atomicAdd(pcnt + b * D + d, h[d]);
+}
+
+// The partition scatter from the row planes directly (binned verify: nothing
+// reads the keys afterwards): each thread projects its 32 columns again, the
+// CTA counts its keys per partition in shared memory (the atomic's return is
+// the key's rank; order inside a partition is immaterial), reserves one range
+// per (CTA, partition) at the run's cursors (part_scan) and writes the
+// (w, column) records there.
+__global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ Xr, u64 P32, u64 p,
+                                                       const u32* __restrict__ rows, int M,
+                                                       const u32* __restrict__ xorc, int lb, int hashed,
+                                                       u32* __restrict__ cursor, uint2* __restrict__ pe) {
+    __shared__ u32 srow[64];
+    __shared__ u32 h[1u << kPgMaxK];
+    const u64 b = blockIdx.y;
+    const int k = M - lb;
+    const u32 D = 1u << k;
+    const u32 mask = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
+    if (threadIdx.x < M) srow[threadIdx.x] = rows[b * M + threadIdx.x];
+    for (u32 d = threadIdx.x; d < D; d += blockDim.x) h[d] = 0;
+    __syncthreads();
+    const u64 word = u64(blockIdx.x) * blockDim.x + threadIdx.x;
+    const u64 col0 = word * 32;
+    const u32 ncol = word < P32 ? u32(minu(32, p - col0)) : 0u;
+    const PartMap pm(xorc[b] & mask);
+    u32 a[32], dr[32];  // key, then (digit << 16 | rank within the CTA's digit)
+    if (word < P32) {
+#pragma unroll
+        for (int s2 = 0; s2 < 32; ++s2) a[s2] = s2 < M ? __ldg(Xr + u64(srow[s2]) * P32 + word) : 0u;
+        transpose32(a);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            a[c] = pm.fwd(a[c] & mask);
+            if (u32(c) < ncol) {
+                const u32 d = part_digit(a[c], lb, k, hashed != 0);
+                dr[c] = (d << 16) | atomicAdd(&h[d], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (u32 d = threadIdx.x; d < D; d += blockDim.x)
+        h[d] = h[d] ? atomicAdd(cursor + b * D + d, h[d]) : 0u;
+    __syncthreads();
+    uint2* out = pe + b * p;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+        if (u32(c) < ncol) out[h[dr[c] >> 16] + (dr[c] & 0xffffu)] = make_uint2(a[c], u32(col0) + c);
 }
 
 __global__ void __launch_bounds__(kPgThreads) part_count(const u32* __restrict__ keys, u64 p, int M, int lb,
@@ -749,7 +799,7 @@ inline u64 part_scratch_words(int k, u64 B) { return B * ((u64(1) << k) * 3 + 1)
 // counted: the partition sizes are already in scratch[0, B * 2^k) (project_count)
 inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, bool hashed, const u32* xorc,
                                   u64* tot, u64* work_run, u32* scratch, uint2* pe, cudaStream_t st,
-                                  bool counted = false) {
+                                  bool counted = false, bool scatter = true) {
     const int lb = M - k;
     const u64 D = u64(1) << k;
     u32* pcnt = scratch;
@@ -765,6 +815,7 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, b
     }
     part_scan<<<static_cast<u32>(B), 1024, 0, st>>>(pcnt, k, p, pbeg, cursor, tot, work_run);
     XYZB_LAUNCH_CHECK();
+    if (!scatter) return;  // project_scatter writes the records
     part_scatter<<<gt, kPgThreads, part_tile_smem(k), st>>>(keys, p, M, lb, hashed ? 1 : 0, xorc, cursor, pe);
     XYZB_LAUNCH_CHECK();
 }
