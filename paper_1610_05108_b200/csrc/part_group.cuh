@@ -238,13 +238,38 @@ __global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ X
         }
     }
     __syncthreads();
-    for (u32 d = threadIdx.x; d < D; d += blockDim.x)
-        h[d] = h[d] ? atomicAdd(cursor + b * D + d, h[d]) : 0u;
+    // the CTA's keys grouped by partition in shared memory (lstart: exclusive scan of the counts), then every
+    // partition's run written contiguously at its reserved global range
+    __shared__ u32 lstart[1u << kPgMaxK], gbase[1u << kPgMaxK];
+    __shared__ uint2 buf[128 * 32];
+    __shared__ u32 ws[33];
+    {
+        const u32 per = (D + blockDim.x - 1) / blockDim.x;
+        const u32 d0 = threadIdx.x * per, d1 = min(D, d0 + per);
+        u32 loc = 0;
+        for (u32 d = d0; d < d1; ++d) {
+            gbase[d] = h[d] ? atomicAdd(cursor + b * D + d, h[d]) : 0u;
+            loc += h[d];
+        }
+        u32 tot;
+        u32 run = block_exclusive(loc, ws, &tot);
+        for (u32 d = d0; d < d1; ++d) {
+            lstart[d] = run;
+            run += h[d];
+        }
+    }
     __syncthreads();
-    uint2* out = pe + b * p;
 #pragma unroll
     for (int c = 0; c < 32; ++c)
-        if (u32(c) < ncol) out[h[dr[c] >> 16] + (dr[c] & 0xffffu)] = make_uint2(a[c], u32(col0) + c);
+        if (u32(c) < ncol) buf[lstart[dr[c] >> 16] + (dr[c] & 0xffffu)] = make_uint2(a[c], u32(col0) + c);
+    __syncthreads();
+    const u32 nk = u32(minu(u64(blockDim.x) * 32, p - u64(blockIdx.x) * blockDim.x * 32));
+    uint2* out = pe + b * p;
+    for (u32 e = threadIdx.x; e < nk; e += blockDim.x) {
+        const uint2 r = buf[e];
+        const u32 d = part_digit(r.x, lb, k, hashed != 0);
+        out[gbase[d] + (e - lstart[d])] = r;
+    }
 }
 
 __global__ void __launch_bounds__(kPgThreads) part_count(const u32* __restrict__ keys, u64 p, int M, int lb,
