@@ -462,132 +462,156 @@ __device__ __forceinline__ ulonglong2 ld_keep(const ulonglong2* p, u64 pol) {
     return v;
 }
 
-// Team of 16 lanes per pair, NS 16-byte slices per lane (W2 = Wp/2 <= 16 NS),
-// two pairs in flight per team; the loops are warp-uniform (full-warp shuffles).
+// The x tiles come from X ^ Y (xor_response, once per search) by TMA bulk
+// copies (cp.async.bulk, L2 evict_first) into a two-deep ring with mbarrier
+// "full" phases, so there is no shared-memory XOR pass and no CTA barrier: a
+// warp done with a tile moves on to the next one while slower warps finish
+// (47.0 -> 41.0 ms at config 4 against a cp.async + __syncthreads form), and
+// the last warp done with a buffer refills it. Teams of 16 lanes per pair,
+// NS 16-byte slices per lane (W2 = Wp/2 <= 16 NS), two pairs in flight per
+// team, the next records loaded one iteration ahead; the loops are
+// warp-uniform (full-warp shuffles). Tiles are ordered by x column
+// (tile_sort), so a team's second pair usually reuses the first's x slices.
+__global__ void __launch_bounds__(256) xor_response(const ulonglong2* __restrict__ X, const ulonglong2* __restrict__ Y,
+                                                    u32 W2, u64 total, ulonglong2* __restrict__ Xy) {
+    for (u64 e = u64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += u64(gridDim.x) * blockDim.x) {
+        const ulonglong2 x = __ldg(X + e), y = __ldg(Y + e % W2);
+        Xy[e] = make_ulonglong2(x.x ^ y.x, x.y ^ y.y);
+    }
+}
+
 template <int NS, bool FULL>
-__global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs A) {
+__global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs A, const u64* __restrict__ Xy) {
     constexpr int G = 16, PR = 2, TPW = 32 / G, NWARPS = kVerifyThreads / 32;
     extern __shared__ __align__(128) ulonglong2 tiles[];  // [2][kBinJT][W2]
+    __shared__ __align__(8) u64 full[2];
+    __shared__ u32 done[2];
     const u32 W2 = A.Wp / 2;
     const u32 tile_elems = u32(kBinJT) * W2;
     const int lane = threadIdx.x & 31, tl = lane & (G - 1);
     const u32 warp = threadIdx.x >> 5, tw = (threadIdx.x / G) % TPW;
     const ulonglong2* X2 = reinterpret_cast<const ulonglong2*>(A.Xc);
-    const ulonglong2* Y2 = reinterpret_cast<const ulonglong2*>(A.Yw);
+    const ulonglong2* XY2 = reinterpret_cast<const ulonglong2*>(Xy);
     u64 pol = 0, tpol = 0;  // the window stays (evict_last), the tiles stream through (evict_first)
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(tpol));
     const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
     const bool ranks = A.sint_out != nullptr && rthr == 0;
     const u32 astar = max(A.astar, rthr);
-    auto load_tile = [&](u32 jt, int s) {
+    if (threadIdx.x == 0) {
+        for (int bb = 0; bb < 2; ++bb) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[bb])));
+            done[bb] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const u32 nmine = blockIdx.x < A.nbj ? (A.nbj - 1 - blockIdx.x) / gridDim.x + 1 : 0u;
+    auto issue = [&](u32 i) {  // one thread: the tile of this CTA's i-th bin into buffer i & 1
+        const u32 jt = blockIdx.x + i * gridDim.x;
+        const int bb = i & 1;
         const u32 c0 = jt << kBinJTShift;
         const u32 ncol = u32(minu(A.p - c0, kBinJT));
-        const bool any = A.boff[jt + 1] > A.boff[jt];
-        if (any) {
-            const ulonglong2* src = X2 + u64(c0) * W2;
-            ulonglong2* dst = tiles + u32(s) * tile_elems;
-            for (u32 e = threadIdx.x; e < ncol * W2; e += blockDim.x)
-                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + e)),
-                             "l"(src + e), "l"(tpol)
-                             : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        const u32 bytes = A.boff[jt + 1] > A.boff[jt] ? ncol * W2 * 16 : 0u;
+        const u32 bar = smem_u32(&full[bb]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        if (bytes)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+                "[%3], %4;" ::"r"(smem_u32(tiles + bb * tile_elems)),
+                "l"(XY2 + u64(c0) * W2), "r"(bytes), "r"(bar), "l"(tpol)
+                : "memory");
     };
-    if (blockIdx.x < A.nbj) load_tile(blockIdx.x, 0);
-    u32 i = 0;
-    for (u32 jt = blockIdx.x; jt < A.nbj; jt += gridDim.x, ++i) {
-        const int s = i & 1;
-        if (jt + gridDim.x < A.nbj) {
-            load_tile(jt + gridDim.x, s ^ 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
-        const u32 rbase = A.boff[jt], r0 = 0, r1 = A.boff[jt + 1] - rbase;  // the bin's fill
+    if (threadIdx.x == 0) {
+        if (nmine > 0) issue(0);
+        if (nmine > 1) issue(1);
+    }
+    for (u32 i = 0; i < nmine; ++i) {
+        const u32 jt = blockIdx.x + i * gridDim.x;
+        const int bb = i & 1;
+        const u32 rbase = A.boff[jt], r1 = A.boff[jt + 1] - rbase;  // the bin's fill
         const u64* Fb = A.F + A.bstart[jt];
-        ulonglong2* tile = tiles + u32(s) * tile_elems;
-        if (r1 > r0) {
-            // pre-XOR the response into the x-side tile: popc(a ^ y ^ b) per pair
-            const u32 ncol = u32(minu(A.p - (u64(jt) << kBinJTShift), kBinJT));
-            for (u32 e = threadIdx.x; e < ncol * W2; e += blockDim.x) {
-                const ulonglong2 y = __ldg(Y2 + e % W2);
-                ulonglong2 v = tile[e];
-                v.x ^= y.x;
-                v.y ^= y.y;
-                tile[e] = v;
-            }
-            __syncthreads();
-            const u32 c0 = jt << kBinJTShift;
-            constexpr u32 STRIDE = NWARPS * TPW * PR;
-            // the next iteration's records are loaded one iteration ahead (record -> column is a dependent chain)
-            u64 nrec[PR];
+        {
+            u32 ok = 0;
+            while (!ok)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                             : "=r"(ok) : "r"(smem_u32(&full[bb])), "r"((i >> 1) & 1u) : "memory");
+        }
+        const ulonglong2* tile = tiles + bb * tile_elems;
+        const u32 c0 = jt << kBinJTShift;
+        constexpr u32 STRIDE = NWARPS * TPW * PR;
+        u64 nrec[PR];
+#pragma unroll
+        for (int r = 0; r < PR; ++r) {
+            const u32 q = warp * TPW * PR + tw * PR + r;
+            nrec[r] = q < r1 ? ld_stream(Fb + q, tpol) : 0ull;
+        }
+        for (u32 q0 = warp * TPW * PR; q0 < r1; q0 += STRIDE) {  // warp-uniform
+            const u32 qb = q0 + tw * PR;
+            ulonglong2 kv[PR][NS];
+            u64 rec[PR];
 #pragma unroll
             for (int r = 0; r < PR; ++r) {
-                const u32 q = r0 + warp * TPW * PR + tw * PR + r;
-                nrec[r] = q < r1 ? ld_stream(Fb + q, tpol) : 0ull;  // records stream (evict_first)
-            }
-            for (u32 q0 = r0 + warp * TPW * PR; q0 < r1; q0 += STRIDE) {  // warp-uniform
-                const u32 qb = q0 + tw * PR;
-                ulonglong2 kv[PR][NS];
-                u64 rec[PR];
-#pragma unroll
-                for (int r = 0; r < PR; ++r) {
-                    const u32 q = qb + r;
-                    rec[r] = nrec[r];
-                    const ulonglong2* kc = X2 + u64(rec_b(rec[r])) * W2;
-#pragma unroll
-                    for (int it = 0; it < NS; ++it) {
-                        const u32 wi = it * G + tl;
-                        kv[r][it] = (q < r1 && (FULL || wi < W2)) ? ld_keep(kc + wi, pol) : make_ulonglong2(0, 0);
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < PR; ++r) {
-                    const u32 q = qb + STRIDE + r;
-                    nrec[r] = q < r1 ? ld_stream(Fb + q, tpol) : 0ull;  // records stream (evict_first)
-                }
-                // the team's pairs are consecutive records of a tile sorted by x column (tile_sort): a pair
-                // whose x column equals the previous pair's reuses its shared-memory slices
-                u32 jl[PR], acc[PR];
-#pragma unroll
-                for (int r = 0; r < PR; ++r) {
-                    jl[r] = qb + r < r1 ? rec_a(rec[r]) - c0 : 0u;
-                    acc[r] = 0;
-                }
+                const u32 q = qb + r;
+                rec[r] = nrec[r];
+                const ulonglong2* kc = X2 + u64(rec_b(rec[r])) * W2;
 #pragma unroll
                 for (int it = 0; it < NS; ++it) {
-                    if (FULL || it * G + tl < W2) {
-                        ulonglong2 av = tile[jl[0] * W2 + it * G + tl];
-                        acc[0] += __popcll(av.x ^ kv[0][it].x) + __popcll(av.y ^ kv[0][it].y);
+                    const u32 wi = it * G + tl;
+                    kv[r][it] = (q < r1 && (FULL || wi < W2)) ? ld_keep(kc + wi, pol) : make_ulonglong2(0, 0);
+                }
+            }
 #pragma unroll
-                        for (int r = 1; r < PR; ++r) {
-                            if (jl[r] != jl[r - 1]) av = tile[jl[r] * W2 + it * G + tl];
-                            acc[r] += __popcll(av.x ^ kv[r][it].x) + __popcll(av.y ^ kv[r][it].y);
-                        }
+            for (int r = 0; r < PR; ++r) {
+                const u32 q = qb + STRIDE + r;
+                nrec[r] = q < r1 ? ld_stream(Fb + q, tpol) : 0ull;
+            }
+            u32 jl[PR], acc[PR];
+#pragma unroll
+            for (int r = 0; r < PR; ++r) {
+                jl[r] = qb + r < r1 ? rec_a(rec[r]) - c0 : 0u;
+                acc[r] = 0;
+            }
+#pragma unroll
+            for (int it = 0; it < NS; ++it) {
+                if (FULL || it * G + tl < W2) {
+                    ulonglong2 av = tile[jl[0] * W2 + it * G + tl];
+                    acc[0] += __popcll(av.x ^ kv[0][it].x) + __popcll(av.y ^ kv[0][it].y);
+#pragma unroll
+                    for (int r = 1; r < PR; ++r) {
+                        if (jl[r] != jl[r - 1]) av = tile[jl[r] * W2 + it * G + tl];
+                        acc[r] += __popcll(av.x ^ kv[r][it].x) + __popcll(av.y ^ kv[r][it].y);
                     }
                 }
+            }
 #pragma unroll
-                for (int r = 0; r < PR; ++r) {
-                    const u32 q = qb + r;
-                    u32 a = acc[r];
+            for (int r = 0; r < PR; ++r) {
+                const u32 q = qb + r;
+                u32 a = acc[r];
 #pragma unroll
-                    for (int o = G / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-                    if (tl == 0 && q < r1) {
-                        const u32 si = rec_neg(rec[r]) ? A.n - a : a;  // the run's sign (search.cpp:25-36)
-                        if (ranks) {
-                            A.sint_out[rbase + q] = si;
-                        } else if (si >= astar) {
-                            PairRec pr{rec_a(rec[r]), rec_b(rec[r]), rec_run(rec[r]), rec_diag(rec[r]) << 1};
-                            kern::append_pair_hit(nullptr, 0, 0, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, A.n,
-                                                  A.krows, A.kM, A.Xc, A.Wp);
-                        }
+                for (int o = G / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                if (tl == 0 && q < r1) {
+                    const u32 si = rec_neg(rec[r]) ? A.n - a : a;
+                    if (ranks) {
+                        A.sint_out[rbase + q] = si;
+                    } else if (si >= astar) {
+                        PairRec pr{rec_a(rec[r]), rec_b(rec[r]), rec_run(rec[r]), rec_diag(rec[r]) << 1};
+                        kern::append_pair_hit(nullptr, 0, 0, A.rid, A.hits, A.hit_count, A.hit_cap, pr, si, A.n,
+                                              A.krows, A.kM, A.Xc, A.Wp);
                     }
                 }
             }
         }
-        __syncthreads();  // the tile buffer is refilled next iteration
+        // this warp is done with buffer bb: the last warp refills it with the tile of bin i + 2
+        __syncwarp();
+        if (lane == 0) {
+            const u32 d = atomicAdd(&done[bb], 1u);
+            if (d == NWARPS - 1) {
+                done[bb] = 0;
+                if (i + 2 < nmine) issue(i + 2);
+            }
+        }
     }
 }
 

@@ -287,7 +287,7 @@ struct xyzb_dataset {
     // top-K over all candidates (topk_kernels.cuh)
     DevBuf tk_state, tk_hist, tk_dhist, tk_sint, tk_table, hits2, tk_cnt2;
     // binned verify (binned_verify.cuh): per-window regions, bins by x-side tile, cursors
-    DevBuf bin_s, bin_wcnt, bin_b, bin_d, bin_cnt, bin_start, bin_fill, bin_boff, bin_ovf, bin_ovfn, bin_zero;
+    DevBuf bin_xy, bin_s, bin_wcnt, bin_b, bin_d, bin_cnt, bin_start, bin_fill, bin_boff, bin_ovf, bin_ovfn, bin_zero;
     u64 bin_hint = 0;      // mean bucket fill of the last binned search on this dataset (sizes the buckets)
     u64 bin_ovf_hint = 0;  // overflow-list size that last sufficed
     HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
@@ -1082,6 +1082,15 @@ void binned_verify(SearchCtx& c) {
              : ns == 4 ? (full ? bins::verify_binned<4, true> : bins::verify_binned<4, false>)
                        : (full ? bins::verify_binned<5, true> : bins::verify_binned<5, false>);
     func_smem(vk, smem);
+    // the x tiles of this search: X ^ Y (the response XORed in once, so the tiles need no pass of their own)
+    cudaEvent_t ex0 = clk.mark();
+    ds->bin_xy.ensure(c.p * ds->Wp * 8);
+    bins::xor_response<<<kSMs * 16, 256, 0, st>>>(ds->Xc.as<ulonglong2>(), ds->yk_bits.as<ulonglong2>(),
+                                                  static_cast<u32>(ds->Wp / 2), c.p * (ds->Wp / 2),
+                                                  ds->bin_xy.as<ulonglong2>());
+    XYZB_LAUNCH_CHECK();
+    c.launches[XYZB_STAGE_VERIFY] += 1;
+    clk.span(XYZB_STAGE_VERIFY, ex0, clk.mark());
     // the prune reads the hit buffer through VerifyArgs
     kern::VerifyArgs PA{};
     PA.hits = A.hits;
@@ -1116,7 +1125,7 @@ void binned_verify(SearchCtx& c) {
         A.bstart = ds->bin_start.as<u32>() + u64(kt) * nbj;
         A.boff = ds->bin_boff.as<u32>() + u64(kt) * (nbj + 1);
         cudaEvent_t ev0 = clk.mark();
-        vk<<<kSMs, bins::kVerifyThreads, smem, st>>>(A);
+        vk<<<kSMs, bins::kVerifyThreads, smem, st>>>(A, ds->bin_xy.as<u64>());
         XYZB_LAUNCH_CHECK();
         c.launches[XYZB_STAGE_VERIFY] += 1;
         cudaEvent_t ev1 = clk.mark();
