@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kPartThreads) bin_split(const u64* __restrict_
 // One CTA per bucket: counts per tile, the tiles' starts (bstart / bfill per
 // (window, tile), relative to the window's first bucket), then the records
 // grouped per step and written as runs into their tile.
-__global__ void __launch_bounds__(kPartThreads) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
+__global__ void __launch_bounds__(kPartThreads, 3) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
                                                          const u32* __restrict__ bcnt, u32 nbh, u32 nbj,
                                                          u64* __restrict__ D, u32* __restrict__ bstart,
                                                          u32* __restrict__ bfill) {
