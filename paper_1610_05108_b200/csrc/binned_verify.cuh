@@ -8,20 +8,23 @@
 // search's canonical pairs are instead collected over ALL batches into bins
 // (kt, jt): kt = the z-side column's window of 2^wshift columns (sized to
 // stay L2-resident, ~84 MB), jt = the x-side column's tile of kBinJT
-// columns. The verify walks the bins kt-major with one persistent
-// 1024-thread CTA per SM: the bin's x-side tile sits in shared memory
-// (cp.async, double-buffered, pre-XORed with Y), the z-side columns come
-// from the current window in L2 (evict_last). Per pair: one column from L2,
-// one from shared memory; DRAM ~ one window pass + one tile pass per window
-// (tools/tile_probe.cu; ncu: 275 DRAM bytes per pair against 1619).
+// columns. The verify walks the bins of one window per launch with one
+// persistent 1024-thread CTA per SM: the bin's x-side tile (from X ^ Y) sits
+// in shared memory (TMA bulk copies into a two-deep mbarrier ring, no CTA
+// barrier), the z-side columns come from the current window in L2
+// (evict_last). Per pair: one column from L2, one from shared memory; DRAM
+// ~ one window pass + one tile pass per window (tools/tile_probe.cu; ncu: 244
+// DRAM bytes per pair against 1619).
 //
-// Two steps put the pairs in bins: per batch, each pair is appended to its
-// bucket (window, tile >> 7; 2048 buckets at config 4, fixed capacity from
-// the previous search's mean fill, one global reservation per CTA chunk and
-// bucket); after the last batch, one CTA per bucket splits it by the tile's
-// low 7 bits. A pair whose bucket is full goes to an overflow list, verified
-// afterwards by a plain gather; an overflowing list makes the host redo the
-// search with a larger one.
+// Three partition passes put the pairs in bins, each a small fan-out so the
+// writes stay long runs: per batch, each pair goes to its z-side window (16
+// regions at config 4); after the last batch, each window is split by the
+// x-side tile >> 7 (128 buckets), and one CTA per bucket splits it by the
+// tile's low 7 bits; tile_sort then orders every tile by x column. Regions
+// have fixed capacities from the previous search's mean fills; a pair whose
+// region is full goes to an overflow list, verified afterwards by a plain
+// gather; an overflowing list makes the host redo the search with a larger
+// one.
 //
 // Pair records (u64): x-side column (24 bits) | z-side column (24) | diagonal
 // flag (1, at bit 48) | the run's pass is negative (1, bit 49) | global run
@@ -29,8 +32,10 @@
 //   bin_window   (per batch)  the batch's pair list -> windows (or the overflow list)
 //   bin_split    (end)        each window -> buckets by x-side tile >> 7
 //   bin_sort     (end)        each bucket -> its 128 tiles' runs
+//   tile_sort    (end)        each tile ordered by x column, in place
 //   bin_scan     (end)        per window, exclusive offsets of the tile fills
 //                             (compact rank indices for the top-K first phase)
+//   xor_response (end)        X ^ Y, the source of the x tiles
 //   verify_binned (per window) strengths; hits (or, top-K first phase, the
 //                 rank of every pair) exactly as verify_pairs_simple
 //   verify_list  the overflow list (warp per pair)
