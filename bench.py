@@ -234,6 +234,28 @@ def gather_peak(device, ncols, words):
         return None
 
 
+def stage_roofline(stage, stage_b, steps, roof):
+    """Per stage: algorithmic bytes / event time, against the measured HBM copy bandwidth. The
+    verify's algorithmic bytes (2 columns per pair) are mostly served on chip (L2 re-reads, shared-memory
+    tiles), so its HBM fraction is taken from the DRAM bytes ncu measured (`roofline.traffic`), with the
+    algorithmic rate beside it."""
+    hbm = peaks()[0]
+    out = {}
+    for kk in ("project", "sort", "join", "verify", "merge"):
+        if not stage_b.get(kk) or not stage.get(kk):
+            continue
+        gbps = stage_b[kk] / (stage[kk] / 1e3) / 1e9
+        e = {"algorithmic_bytes": stage_b[kk] / steps, "gbps": gbps, "frac_of_hbm": gbps / hbm,
+             "bound": STAGE_BOUND[kk]}
+        if kk == "verify" and roof.get("traffic"):
+            e = {"algorithmic_bytes": stage_b[kk] / steps, "algorithmic_gbps": gbps,
+                 "dram_gbps": roof["achieved"], "frac_of_hbm": roof["frac"],
+                 "note": "frac_of_hbm from the measured DRAM bytes (roofline.traffic); the algorithmic rate counts "
+                         "on-chip re-reads", "bound": STAGE_BOUND[kk]}
+        out[kk] = e
+    return out
+
+
 def binned_verify():
     """The engine's binned verify runs for binary X of >= 512 MB with columns of <= 80 16-byte slices
     (engine.cu, run_batches): config 4."""
@@ -590,9 +612,10 @@ def main():
                                       f"{wcols} columns x {col} B (one window; paper_1610_05108_b200/csrc/probe.cu)"}
         if binned:
             roof["note"] = ("binned verify (csrc/binned_verify.cuh): the x tile sits in shared memory and the z column "
-                            "comes from an L2-resident window, so DRAM carries ~256 B per pair instead of 1619 B "
-                            "(the per-batch verify, 0.97 of HBM at 98 ms); the kernel is bound on-chip (ncu: L1/TEX "
-                            "87 %, profiles/r02_verify_binned_ncu.json), see l2_roofline")
+                            "comes from an L2-resident window, so DRAM carries ~244 B per pair instead of 1619 B "
+                            "(the per-batch verify, 0.97 of HBM at 98 ms); the kernel is bound on-chip, latency at "
+                            "two pairs in flight per team (ncu: L1/TEX 75 %, L2 55 %, DRAM 28 %, "
+                            "profiles/r02_verify_binned_ncu.json), see l2_roofline")
         if traffic and traffic.get("dram_bytes_per_pair") and verify_launches:
             dram_launch = traffic["dram_bytes_per_pair"] * (verified_mine / verify_launches)
             ach = dram_launch / ((verify_ms / verify_launches) / 1e3) / 1e9
@@ -614,12 +637,7 @@ def main():
             "stage_ms_per_step": {kk: v / args.steps for kk, v in stage.items()},
             "exchange_ms_per_step": ex_ms / args.steps if world > 1 else 0.0,
             # per-stage algorithmic bytes over the stage's event time, vs measured HBM
-            "stage_roofline": {kk: {"algorithmic_bytes": stage_b[kk] / args.steps,
-                                    "gbps": stage_b[kk] / (stage[kk] / 1e3) / 1e9 if stage.get(kk) else None,
-                                    "frac_of_hbm": (stage_b[kk] / (stage[kk] / 1e3) / 1e9) / peaks()[0]
-                                    if stage.get(kk) else None,
-                                    "bound": STAGE_BOUND[kk]}
-                               for kk in ("project", "sort", "join", "verify", "merge") if stage_b.get(kk)},
+            "stage_roofline": stage_roofline(stage, stage_b, args.steps, roof),
             "gpu_launches": launches,
             "roofline": roof,
             "clocks": clk.summary(),
