@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kPartThreads, 3) bin_sort(const u64* __restric
 // share the x column's shared-memory reads).
 constexpr int kTileSortThreads = 256;
 constexpr u32 kTileSortMax = 2048;
-__global__ void __launch_bounds__(kTileSortThreads) tile_sort(u64* __restrict__ D, u32 cap_bucket, u32 nbh, u32 nbj,
+__global__ void __launch_bounds__(kTileSortThreads, 8) tile_sort(u64* __restrict__ D, u32 cap_bucket, u32 nbh, u32 nbj,
                                                               const u32* __restrict__ bstart,
                                                               const u32* __restrict__ bfill) {
     constexpr int R = kTileSortMax / kTileSortThreads;
