@@ -312,7 +312,8 @@ def same_hits(a, b, strength_tol=0.0):
 
 # ---- the drop-in build: reference core with search.cpp replaced by the GPU shim ----
 
-DROPIN_SO = os.path.join(ROOT, "build", "dropin", "libxyz_core_gpu.so")
+# the test harness over the drop-in (it pulls build/dropin/libxyz_core_gpu.so in)
+DROPIN_SO = os.path.join(ROOT, "build", "dropin", "libxyz_core_gpu_harness.so")
 
 
 class LassoOut(C.Structure):
