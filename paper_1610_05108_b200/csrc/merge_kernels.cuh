@@ -150,17 +150,38 @@ constexpr int kSmallMerge = 4096;
 constexpr int kSmallThreads = 1024;
 
 // In-place bitonic sort of idx[0..N) (N a power of two) by less(a, b).
+// Element i lives with thread i % blockDim.x, so the compare-exchange
+// partners i ^ j of the stages j < 32 share a warp: those stages run in
+// registers (one shuffle each, no barrier); only j >= 32 goes through shared
+// memory with a CTA barrier (N = 4096: 40 barriers instead of 78).
 template <class Less>
 __device__ __forceinline__ void bitonic(u32* idx, int N, Less less) {
+    if (N < 32) {  // partial warps: every stage through shared memory
+        for (int k = 2; k <= N; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const int i = threadIdx.x, l = i ^ j;
+                if (i < N && l > i) {
+                    const u32 a = idx[i], b = idx[l];
+                    const bool up = (i & k) == 0;
+                    if (up ? less(b, a) : less(a, b)) {
+                        idx[i] = b;
+                        idx[l] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        return;
+    }
     for (int k = 2; k <= N; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
+        int j = k >> 1;
+        for (; j >= 32; j >>= 1) {
             for (int i = threadIdx.x; i < N; i += blockDim.x) {
                 const int l = i ^ j;
                 if (l > i) {
                     const u32 a = idx[i], b = idx[l];
                     const bool up = (i & k) == 0;
-                    const bool swap = up ? less(b, a) : less(a, b);
-                    if (swap) {
+                    if (up ? less(b, a) : less(a, b)) {
                         idx[i] = b;
                         idx[l] = a;
                     }
@@ -168,6 +189,18 @@ __device__ __forceinline__ void bitonic(u32* idx, int N, Less less) {
             }
             __syncthreads();
         }
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {  // whole warps: N is a multiple of 32
+            u32 mine = idx[i];
+            const bool up = (i & k) == 0;
+            for (int jj = j; jj > 0; jj >>= 1) {
+                const u32 other = __shfl_xor_sync(0xffffffffu, mine, jj);
+                const bool lower = (i & jj) == 0;
+                const u32 a = lower ? mine : other, b = lower ? other : mine;
+                if (up ? less(b, a) : less(a, b)) mine = other;
+            }
+            idx[i] = mine;
+        }
+        __syncthreads();
     }
 }
 

@@ -472,7 +472,6 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
             if (i < cnt) sg[T[v[q].x & lmask] + rk[q]] = v[q].y;
         }
         __syncthreads();
-        for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) grouped[off + beg + i] = sg[i];  // coalesced
     } else {
         for (u32 i0 = 0; i0 < cnt; i0 += kPjPerThread * blockDim.x) {
 #pragma unroll
@@ -548,6 +547,10 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     u32 ibase = block_exclusive(my_items, ws, &ti);
     u32 pbase = block_exclusive(my_pairs, ws + 33, &tp);
     if (ti == 0 && tp == 0) return;
+    // only items (large blocks, expanded later) read the global grouped array:
+    // inline pairs carry their columns, taken from shared memory here
+    if (inreg && ti)
+        for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) grouped[off + beg + i] = sg[i];  // coalesced
     if (threadIdx.x == 0) {
         ws[66] = ti ? atomicAdd(nitems, ti) : 0u;
         ws[67] = (pair_list && tp) ? atomicAdd(npairs, tp) : 0u;
