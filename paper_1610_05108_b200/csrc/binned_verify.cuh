@@ -449,6 +449,9 @@ struct BinVerifyArgs {
     int kM;
     u32* sint_out;        // top-K first phase: rank of every pair of this window at its compact index (thr == 0)
     const u32* rank_thr;  // top-K running threshold (nullptr: hits mode)
+    u32* rank_fail;       // top-K state's failure bits (topk::State::fail)
+    u32 phase_follows;    // top-K: this window's ranks are consumed by a phase right after it (else bit 2 of
+                          // *rank_fail is raised when the window still runs in the rank-writing first phase)
 };
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return u32(__cvta_generic_to_shared(p)); }
@@ -503,6 +506,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_binned(BinVerifyArgs
     const u32 rthr = A.rank_thr ? *A.rank_thr : 0u;
     const bool ranks = A.sint_out != nullptr && rthr == 0;
     const u32 astar = max(A.astar, rthr);
+    if (ranks && !A.phase_follows && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.rank_fail, 4u);
     if (threadIdx.x == 0) {
         for (int bb = 0; bb < 2; ++bb) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[bb])));

@@ -783,6 +783,8 @@ struct SearchCtx {
     u64 tk_table = 0;      // dedup table slots (power of two)
     // binned verify (X >> L2): pairs of all batches bucketed by (z window, x tile), verified at the end
     bool binned = false;
+    bool tk_all_windows = false;  // binned top-K: a phase after every window (the redo when the first window's
+                                  // phase left the threshold at 0)
     bool no_one_pass = false;  // a one-pass join overflowed the pair list: the redo counts first
     int wshift = 0, nkt = 0;
     u64 nbj = 0, nbh = 0, cap_kt = 0, cap_bucket = 0, ovf_cap = 0;
@@ -1073,6 +1075,8 @@ void binned_verify(SearchCtx& c) {
     A.kM = static_cast<int>(c.M);
     A.sint_out = c.topk_all ? ds->tk_sint.as<u32>() : nullptr;
     A.rank_thr = c.topk_all ? &ds->tk_state.as<topk::State>()->thr : nullptr;
+    A.rank_fail = c.topk_all ? &ds->tk_state.as<topk::State>()->fail : nullptr;
+    A.phase_follows = 1;
     const int ns = static_cast<int>(ceil_div(ds->Wp / 2, 16));
     const size_t smem = bins::verify_smem(A.Wp);
     const bool full = ds->Wp / 2 == u64(16 * ns);  // every lane's slices inside the column
@@ -1124,6 +1128,11 @@ void binned_verify(SearchCtx& c) {
         A.F = ds->bin_d.as<u64>() + u64(kt) * c.nbh * c.cap_bucket;
         A.bstart = ds->bin_start.as<u32>() + u64(kt) * nbj;
         A.boff = ds->bin_boff.as<u32>() + u64(kt) * (nbj + 1);
+        // top-K: the first window's phase sets the threshold, later windows append at or above it and the
+        // last phase (after the overflow list) prunes; a later window that still finds the threshold at 0
+        // flags the search, which is then redone with a phase after every window
+        const bool phase = c.topk_all && (kt == 0 || c.tk_all_windows);
+        A.phase_follows = phase ? 1u : 0u;
         cudaEvent_t ev0 = clk.mark();
         vk<<<kSMs, bins::kVerifyThreads, smem, st>>>(A, ds->bin_xy.as<u64>());
         XYZB_LAUNCH_CHECK();
@@ -1131,9 +1140,10 @@ void binned_verify(SearchCtx& c) {
         cudaEvent_t ev1 = clk.mark();
         clk.span(XYZB_STAGE_VERIFY, ev0, ev1);
         c.verify_spans.push_back({ev0, ev1});
-        if (c.topk_all) topk_phase(ev1, A.boff + nbj, 0xffffffffu, nullptr, A.boff);  // the window's pairs held in bins
+        if (phase) topk_phase(ev1, A.boff + nbj, 0xffffffffu, nullptr, A.boff);  // the window's pairs held in bins
     }
     // pairs whose bin was full
+    A.phase_follows = 1;
     cudaEvent_t ev0 = clk.mark();
     bins::verify_list<<<kSMs * 8, 256, 0, st>>>(A, ds->bin_ovf.as<u64>(), ds->bin_ovfn.as<u32>(),
                                                 static_cast<u32>(c.ovf_cap));
@@ -1443,12 +1453,14 @@ void run_batches(SearchCtx& c) {
                                             ds->work_run.as<u64>(), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st,
                                             fused_count, !keyless);
                 c.launches[XYZB_STAGE_SORT] += fused_count ? 2 : 3;
+                // keyless: 4-byte records (local bucket | column) where both fit 32 bits
+                const bool packed = keyless && kern::part_packed_ok(int(M) - pk, p, part_hash);
                 if (keyless) {  // the records straight from the row planes (no key array)
                     const u64 D = u64(1) << pk;
                     dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
-                    kern::project_scatter<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M),
-                                                             ds->xorc.as<K>(), int(M) - pk, part_hash ? 1 : 0,
-                                                             ds->pgrp.as<u32>() + nb * D, ds->pent.as<uint2>());
+                    auto* ps = packed ? kern::project_scatter<true> : kern::project_scatter<false>;
+                    ps<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), ds->xorc.as<K>(), int(M) - pk,
+                                          part_hash ? 1 : 0, ds->pgrp.as<u32>() + nb * D, ds->pent.as<uint2>());
                     XYZB_LAUNCH_CHECK();
                 }
                 e2 = clk.mark();
@@ -1460,7 +1472,7 @@ void run_batches(SearchCtx& c) {
                                        ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(), nitems,
                                        static_cast<u32>(item_cap), npairs_b, ds->pairs.as<kern::PairRec>(),
                                        static_cast<u32>(c.pair_cap), ds->pgrp.as<u32>(), ds->pent.as<uint2>(),
-                                       ds->povf.as<u32>(), st, one_pass_join);
+                                       ds->povf.as<u32>(), st, one_pass_join, packed);
                 c.launches[XYZB_STAGE_JOIN] += one_pass_join ? 1 : 2;
             } else {
                 throw internal_error("xyzb: partitioned grouping needs 32-bit keys");
@@ -2196,6 +2208,10 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             std::memcpy(&ts, hs + o_tk, sizeof(ts));
             if (ts.fail & 2u) {  // the hit buffer overflowed during a batch
                 H = std::max(H, ts.max_hits);
+                tk_redo = true;
+            }
+            if (ts.fail & 4u) {  // binned: a window after the first ran with the threshold still at 0
+                c.tk_all_windows = true;
                 tk_redo = true;
             }
             if (ts.fail & 1u) {  // a batch's dropped band could hold top-K keys: emit more

@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "cta_group.cuh"
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(128) project_count(const u32* __restrict__ Xr,
 // the key's rank; order inside a partition is immaterial), reserves one range
 // per (CTA, partition) at the run's cursors (part_scan) and writes the
 // (w, column) records there.
+template <bool PACKED>
 __global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ Xr, u64 P32, u64 p,
                                                        const u32* __restrict__ rows, int M,
                                                        const u32* __restrict__ xorc, int lb, int hashed,
@@ -264,12 +266,28 @@ __global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ X
         if (u32(c) < ncol) buf[lstart[dr[c] >> 16] + (dr[c] & 0xffffu)] = make_uint2(a[c], u32(col0) + c);
     __syncthreads();
     const u32 nk = u32(minu(u64(blockDim.x) * 32, p - u64(blockIdx.x) * blockDim.x * 32));
+    if (PACKED) {  // 4-byte records: (local bucket << (32 - lb)) | column (the partition is the record's place)
+        u32* out = reinterpret_cast<u32*>(pe) + b * p;
+        const int cb = 32 - lb;
+        const u32 lmask = (1u << lb) - 1u;
+        for (u32 e = threadIdx.x; e < nk; e += blockDim.x) {
+            const uint2 r = buf[e];
+            const u32 d = r.x >> lb;
+            out[gbase[d] + (e - lstart[d])] = ((r.x & lmask) << cb) | r.y;
+        }
+        return;
+    }
     uint2* out = pe + b * p;
     for (u32 e = threadIdx.x; e < nk; e += blockDim.x) {
         const uint2 r = buf[e];
         const u32 d = part_digit(r.x, lb, k, hashed != 0);
         out[gbase[d] + (e - lstart[d])] = r;
     }
+}
+
+// 4-byte partition records fit when the local bucket (lb bits) and the column share 32 bits (dense partitions).
+inline bool part_packed_ok(int lb, u64 p, bool hashed) {
+    return !hashed && lb >= 1 && lb <= 16 && p <= (u64(1) << (32 - lb));
 }
 
 __global__ void __launch_bounds__(kPgThreads) part_count(const u32* __restrict__ keys, u64 p, int M, int lb,
@@ -365,7 +383,7 @@ __device__ __forceinline__ void part_table_scan(u32* T, u32 n, u32* ws) {
     __syncthreads();
 }
 
-template <int EMIT>
+template <int EMIT, bool PACKED = false>
 __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restrict__ pe, const u32* __restrict__ pbeg,
                                                         u64 p, int M, int lb, const u32* __restrict__ xorc, u64 guard,
                                                         u32 hmax, u32* __restrict__ grouped, u64* __restrict__ tot,
@@ -384,7 +402,16 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     if (EMIT == 1 && tot[b] > guard) return;  // aborted run: nothing to emit (uniform per CTA)
     const u32 beg = pbeg[u64(b) * (D + 1) + d], end = pbeg[u64(b) * (D + 1) + d + 1];
     const u32 cnt = end - beg;
-    const uint2* e = pe + u64(b) * p + beg;
+    // records: (w, column), or packed (local bucket << (32 - lb)) | column (project_scatter<true>)
+    using Rec = typename std::conditional<PACKED, u32, uint2>::type;
+    const Rec* e = reinterpret_cast<const Rec*>(pe) + u64(b) * p + beg;
+    const int cb = 32 - lb;
+    auto bucket_of = [&](const Rec& r) -> u32 {
+        if constexpr (PACKED) return r >> cb; else return r.x & lmask;
+    };
+    auto column_of = [&](const Rec& r) -> u32 {
+        if constexpr (PACKED) return r & ((1u << cb) - 1u); else return r.y;
+    };
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (cnt < 2) {
         // no block with work; a lone column of a c == 0 run still counts its
@@ -399,30 +426,31 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     // returns each entry's rank in its bucket, so the scatter needs no second
     // pass), else two streaming passes
     const bool inreg = cnt <= kPjPerThread * blockDim.x;
-    uint2 v[kPjPerThread];
+    Rec v[kPjPerThread];
     u32 rk[kPjPerThread];
     if (inreg) {
 #pragma unroll
         for (int q = 0; q < kPjPerThread; ++q) {
             const u32 i = q * blockDim.x + threadIdx.x;
-            v[q] = i < cnt ? __ldg(e + i) : make_uint2(0, 0);
+            v[q] = i < cnt ? __ldg(e + i) : Rec{};
         }
 #pragma unroll
         for (int q = 0; q < kPjPerThread; ++q) {
             const u32 i = q * blockDim.x + threadIdx.x;
-            if (i < cnt) rk[q] = atomicAdd(T + (v[q].x & lmask), 1u);
+            if (i < cnt) rk[q] = atomicAdd(T + bucket_of(v[q]), 1u);
         }
     } else {
         for (u32 i0 = 0; i0 < cnt; i0 += kPjPerThread * blockDim.x) {
 #pragma unroll
             for (int q = 0; q < kPjPerThread; ++q) {
                 const u32 i = i0 + q * blockDim.x + threadIdx.x;
-                v[q].x = i < cnt ? __ldg(&e[i].x) : 0u;
+                if constexpr (PACKED) v[q] = i < cnt ? __ldg(e + i) : 0u;
+                else v[q].x = i < cnt ? __ldg(&e[i].x) : 0u;
             }
 #pragma unroll
             for (int q = 0; q < kPjPerThread; ++q) {
                 const u32 i = i0 + q * blockDim.x + threadIdx.x;
-                if (i < cnt) atomicAdd(T + (v[q].x & lmask), 1u);
+                if (i < cnt) atomicAdd(T + bucket_of(v[q]), 1u);
             }
         }
     }
@@ -469,7 +497,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
 #pragma unroll
         for (int q = 0; q < kPjPerThread; ++q) {
             const u32 i = q * blockDim.x + threadIdx.x;
-            if (i < cnt) sg[T[v[q].x & lmask] + rk[q]] = v[q].y;
+            if (i < cnt) sg[T[bucket_of(v[q])] + rk[q]] = column_of(v[q]);
         }
         __syncthreads();
     } else {
@@ -477,12 +505,12 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
 #pragma unroll
             for (int q = 0; q < kPjPerThread; ++q) {
                 const u32 i = i0 + q * blockDim.x + threadIdx.x;
-                v[q] = i < cnt ? __ldg(e + i) : make_uint2(0, 0);
+                v[q] = i < cnt ? __ldg(e + i) : Rec{};
             }
 #pragma unroll
             for (int q = 0; q < kPjPerThread; ++q) {
                 const u32 i = i0 + q * blockDim.x + threadIdx.x;
-                if (i < cnt) grouped[off + beg + atomicAdd(T + (v[q].x & lmask), 1u)] = v[q].y;
+                if (i < cnt) grouped[off + beg + atomicAdd(T + bucket_of(v[q]), 1u)] = column_of(v[q]);
             }
         }
         __syncthreads();
@@ -852,12 +880,10 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, b
 inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* xorc, u64 guard, u32 hmax,
                              u32* grouped, u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap,
                              u32* npairs, PairRec* pairs, u32 pair_cap, const u32* scratch, const uint2* pe,
-                             u32* ovf, cudaStream_t st, bool one_pass = false) {
+                             u32* ovf, cudaStream_t st, bool one_pass = false, bool packed = false) {
     const int lb = M - k;
     const u64 D = u64(1) << k;
     const u32* pbeg = scratch + 2 * B * D;
-    func_smem(part_join<0>, 64 << 10);
-    func_smem(part_join<1>, 64 << 10);
     dim3 gj(static_cast<u32>(D), static_cast<u32>(B));
     if (hash) {
         func_smem(part_join_hash<0>, part_hash_smem(true));
@@ -870,22 +896,24 @@ inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* x
         XYZB_LAUNCH_CHECK();
         return;
     }
-    if (one_pass) {
-        func_smem(part_join<2>, 64 << 10);
-        part_join<2><<<gj, kPjThreads, part_join_smem(lb), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
-                                                                work_run, items, nitems, item_cap, npairs, pairs,
-                                                                pair_cap);
+    auto launch = [&](auto kernel, size_t smem) {
+        func_smem(kernel, 64 << 10);
+        kernel<<<gj, kPjThreads, smem, st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot, work_run, items, nitems,
+                                             item_cap, npairs, pairs, pair_cap);
         XYZB_LAUNCH_CHECK();
+    };
+    if (one_pass) {
+        if (packed) launch(part_join<2, true>, part_join_smem(lb));
+        else launch(part_join<2, false>, part_join_smem(lb));
         return;
     }
-    part_join<0><<<gj, kPjThreads, (size_t(1) << lb) * 4, st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
-                                                            work_run, items, nitems, item_cap, npairs, pairs,
-                                                            pair_cap);
-    XYZB_LAUNCH_CHECK();
-    part_join<1><<<gj, kPjThreads, part_join_smem(lb), st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot,
-                                                            work_run, items, nitems, item_cap, npairs, pairs,
-                                                            pair_cap);
-    XYZB_LAUNCH_CHECK();
+    if (packed) {
+        launch(part_join<0, true>, (size_t(1) << lb) * 4);
+        launch(part_join<1, true>, part_join_smem(lb));
+    } else {
+        launch(part_join<0, false>, (size_t(1) << lb) * 4);
+        launch(part_join<1, false>, part_join_smem(lb));
+    }
 }
 
 } // namespace kern

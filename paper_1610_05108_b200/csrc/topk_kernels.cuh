@@ -44,7 +44,8 @@ constexpr u32 kBins = 1u << kBinsLog;
 struct State {
     u32 thr;        // retained threshold (rank units, a bin edge)
     u32 emit;       // this batch's emission threshold
-    u32 fail;       // bit 0: a dropped band may hold top-K keys; bit 1: hit buffer overflow
+    u32 fail;       // bit 0: a dropped band may hold top-K keys; bit 1: hit buffer overflow; bit 2 (binned
+                    // verify): a window without a phase of its own ran with thr still 0 (redo, phase per window)
     u32 max_hits;   // largest hit count seen (regrow)
     u32 distinct;   // distinct keys at or above thr after the last prune
     u32 pad[3];
