@@ -72,10 +72,11 @@ WORKLOADS = {
 WORKLOAD = WORKLOADS["large"]
 # what bounds each stage
 STAGE_BOUND = {"project": "hbm/l2: M row-plane words read + keys written",
-               "sort": "grouping: partition pass (config 4: keys read twice, (w, column) records written) or the "
-                       "fused group + join kernel (configs 1-2: issue-bound, shared-memory atomics)",
-               "join": "partition join (config 4: records read twice, pair list written) or the pair expansion of "
-                       "large blocks",
+               "sort": "grouping: partition pass (config 4: the row planes projected once more, 4-byte (bucket, "
+                       "column) records written into fixed-capacity partitions) or the fused group + join kernel "
+                       "(configs 1-2: issue-bound, shared-memory atomics)",
+               "join": "partition join (config 4: records read once, pair list written, then the binning passes) "
+                       "or the pair expansion of large blocks",
                "verify": "config 4: binned verify (x tile in shared memory, z column from the L2-resident window; "
                          "see l2_roofline); config 2: l2 gather (X resident)",
                "merge": "top-K over all candidates: rank histogram, emission, distinct-key prune per batch + the "
@@ -533,6 +534,7 @@ def main():
         one_step()
     barrier()
     dev_ms, verify_ms, verify_bytes, verify_launches, launches, runs, verified = 0.0, 0.0, 0, 0, 0, 0, 0
+    attempts = 0  # device passes per search (1 unless a capacity was outgrown and the search redone)
     ex_ms = 0.0  # all-gather + merge of the per-rank top-K lists (N > 1), CUDA events on torch's stream
     stage, stage_b = {}, {}
     t_wall = 0.0
@@ -550,6 +552,7 @@ def main():
             verify_bytes += r.stage_bytes["verify"]
             verify_launches += r.verify_launches
             launches += r.kernel_launches
+            attempts = max(attempts, r.attempts)
             runs += r.runs_executed
             verified += r.verified_pairs
             for kk, v in r.stage_ms.items():
@@ -638,7 +641,7 @@ def main():
             "exchange_ms_per_step": ex_ms / args.steps if world > 1 else 0.0,
             # per-stage algorithmic bytes over the stage's event time, vs measured HBM
             "stage_roofline": stage_roofline(stage, stage_b, args.steps, roof),
-            "gpu_launches": launches,
+            "gpu_launches": launches, "search_attempts": attempts,
             "roofline": roof,
             "clocks": clk.summary(),
             "l2_roofline": l2_roof,
@@ -708,6 +711,7 @@ def main():
             if pipe_runs:
                 out["e2e"] = {"value": pipe_runs / pipe_s, "unit": "runs/s", "h2d_bytes_per_step": h2d,
                               "d2h_bytes_per_step": d2h, "serial_value": serial, "clocks": e2e_clk.summary(),
+                              "search_attempts": rr.attempts,
                               "note": "every step: a fresh Dataset (H2D of X from pinned host memory + bit "
                                       f"transpose) + search + top-K to host; {E2E_INFLIGHT} steps in flight on "
                                       f"{E2E_INFLIGHT} host threads (wall clock over all steps); serial_value: one "

@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define XYZB_ABI_VERSION 2
+#define XYZB_ABI_VERSION 3
 
 /* status codes */
 enum {
@@ -184,6 +184,9 @@ typedef struct {
     uint64_t verify_launches;
     double gamma_effective;      /* the hit test's gamma (XYZB_TOPK_CANDIDATES: the K-th strength) */
     uint64_t devices_used;       /* devices the runs were sharded over */
+    uint64_t attempts;           /* times the device ran the search: 1, or more after a buffer or partition
+                                    capacity was outgrown and the search redone (device_ms covers them all);
+                                    sharded: the largest of the shards */
 } xyzb_result;
 
 /* ---- lifecycle ---- */

@@ -24,6 +24,9 @@
  *   one_pass_join   1 = the binned verify's one-pass partition join even when
  *                   runs are expected near the guard (aborted runs' pairs are
  *                   then dropped while binned)
+ *   part_fixed      the keyless partition pass with fixed-capacity regions (no
+ *                   count pass): -1 = never, N > 0 = N records per partition
+ *                   (a small N overflows: the counted redo)
  * Returns XYZB_OK, or XYZB_E_DATA for an unknown name.
  */
 #ifndef XYZB_TESTING_H

@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 OK, E_DATA, E_GUARD, E_SOLVER, E_CUDA, E_INTERNAL = 0, 3, 4, 5, 10, 11
 MODE_BINARY, MODE_CONTINUOUS_Y, MODE_CONTINUOUS_XY = 0, 1, 2
@@ -97,6 +97,7 @@ class Result(C.Structure):
         ("verify_launches", C.c_uint64),
         ("gamma_effective", C.c_double),
         ("devices_used", C.c_uint64),
+        ("attempts", C.c_uint64),
     ]
 
 

@@ -61,7 +61,7 @@ namespace {
 // the fp32 verify beside the sign-bit one. 0 = the engine's own choice.
 struct TestOptions {
     std::atomic<long long> batch_entries{0}, hit_cap{0}, item_cap{0}, pair_cap{0}, grouping{0}, merge_large{0},
-        sign_verify_off{0}, trace{0}, brute_cuda{0}, binned{0}, binned_wshift{0}, binned_cap{0}, one_pass_join{0};
+        sign_verify_off{0}, trace{0}, brute_cuda{0}, binned{0}, binned_wshift{0}, binned_cap{0}, one_pass_join{0}, part_fixed{0};
 };
 TestOptions& topt() {
     static TestOptions* o = new TestOptions();  // leaked on purpose (outlives static destructors)
@@ -293,6 +293,7 @@ struct xyzb_dataset {
     HostBuf h_rows, h_state, h_small, h_merge, h_status, h_planes;
     StageClock clock;
     u32 hit_cap = 1u << 16;
+    int part_fixed_fails = 0;  // searches of this dataset whose fixed-capacity partition pass overflowed
     // X replicated on further devices (xyzb_problem.devices[1..]): the search shards its runs over them
     std::vector<std::unique_ptr<xyzb_dataset>> replicas;
     ~xyzb_dataset();
@@ -785,6 +786,8 @@ struct SearchCtx {
     bool binned = false;
     bool tk_all_windows = false;  // binned top-K: a phase after every window (the redo when the first window's
                                   // phase left the threshold at 0)
+    u64 attempts = 0;            // device passes over the search (redos after an outgrown capacity)
+    bool no_fixed_part = false;  // a fixed-capacity partition overflowed: the redo counts the partitions first
     bool no_one_pass = false;  // a one-pass join overflowed the pair list: the redo counts first
     int wshift = 0, nkt = 0;
     u64 nbj = 0, nbh = 0, cap_kt = 0, cap_bucket = 0, ovf_cap = 0;
@@ -1172,7 +1175,7 @@ void run_batches(SearchCtx& c) {
     ds->hit_count.ensure(8);
     XYZB_CUDA(cudaMemsetAsync(ds->hit_count.p, 0, 4, st));
     ds->povf.ensure(8);
-    XYZB_CUDA(cudaMemsetAsync(ds->povf.p, 0, 4, st));
+    XYZB_CUDA(cudaMemsetAsync(ds->povf.p, 0, 8, st));  // [0] hashed partition overflow, [1] fixed partition overflow
     ds->hits.ensure(sizeof(kern::DevHit) * u64(ds->hit_cap));
     if (c.topk_all) {
         ds->hits2.ensure(sizeof(kern::DevHit) * u64(ds->hit_cap));
@@ -1361,6 +1364,19 @@ void run_batches(SearchCtx& c) {
     // ... and with the binned verify nothing reads the keys afterwards (hits recompute a key from the draws):
     // the partition records come from the row planes directly
     const bool keyless = fused_count && c.binned;
+    // keyless: 4-byte records (local bucket | column) where both fit 32 bits ...
+    const bool packed = keyless && kern::part_packed_ok(int(M) - pk, p, part_hash);
+    // ... and no count pass at all: every partition owns a fixed region of 2.5 x its mean size (+ 64) — a run
+    // that drew a row twice has two equal key bits, and when both are partition digits half of its partitions
+    // hold twice the mean (about two of config 4's 800 runs; their sizes spread by a few percent more where
+    // neighbouring columns are correlated). An overflow (three equal digit bits, or keys far from uniform)
+    // is flagged on the device and the search redone with counted partitions; after two such searches the
+    // dataset counts from then on
+    const long long fsel = topt().part_fixed.load();
+    const bool fixed_part = packed && !c.no_fixed_part && ds->part_fixed_fails < 2 && fsel >= 0;
+    const u64 pmean = ceil_div(p, u64(1) << pk);
+    const u32 fixed_cap = !fixed_part ? 0u : fsel > 0 ? static_cast<u32>(fsel) : static_cast<u32>(2 * pmean + pmean / 2 + 64);
+    if (fixed_part) ds->pent.ensure(std::max<u64>(cap * 8, (B << pk) * u64(fixed_cap) * 4 + 16));
     const bool one_pass_join = c.binned && part_path && !part_hash && !c.no_one_pass &&
                                (double(p) * double(p) / std::ldexp(1.0, int(M)) <= double(c.guard) / 8.0 ||
                                 topt().one_pass_join.load() == 1);
@@ -1381,11 +1397,13 @@ void run_batches(SearchCtx& c) {
                 XYZB_LAUNCH_CHECK();
                 XYZB_CUDA(cudaMemsetAsync(ds->pgrp.p, 0, (nb << pk) * 4, st));
                 dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
-                auto* pc = keyless ? kern::project_count<false> : kern::project_count<true>;
-                pc<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), k0, ds->xorc.as<K>(),
-                                      int(M) - pk, part_hash ? 1 : 0, ds->pgrp.as<u32>());
-                XYZB_LAUNCH_CHECK();
-                c.launches[XYZB_STAGE_PROJECT] += 2;
+                if (!fixed_part) {
+                    auto* pc = keyless ? kern::project_count<false> : kern::project_count<true>;
+                    pc<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), k0, ds->xorc.as<K>(),
+                                          int(M) - pk, part_hash ? 1 : 0, ds->pgrp.as<u32>());
+                    XYZB_LAUNCH_CHECK();
+                }
+                c.launches[XYZB_STAGE_PROJECT] += fixed_part ? 1 : 2;
             }
         } else if (!xy) {
             dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
@@ -1449,30 +1467,35 @@ void run_batches(SearchCtx& c) {
         if (part_path) {
             // ---- group: partition pass (per-run partitions that hold both sides of every block) ----
             if constexpr (sizeof(K) == 4) {
+                auto scatter_records = [&](u32* cursor) {  // the records straight from the row planes (no key array)
+                    dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
+                    auto* ps = packed ? kern::project_scatter<true> : kern::project_scatter<false>;
+                    ps<<<g, 128, kern::project_scatter_smem(pk), st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), ds->xorc.as<K>(), int(M) - pk,
+                                          part_hash ? 1 : 0, cursor, ds->pent.as<uint2>(), fixed_cap,
+                                          ds->povf.as<u32>() + 1);
+                    XYZB_LAUNCH_CHECK();
+                };
+                // fixed regions: the scatter's cursors (zeroed above) end as the partition sizes, scanned after
+                if (fixed_part) scatter_records(ds->pgrp.as<u32>());
                 kern::part_partition_launch(k0, nb, p, int(M), pk, part_hash, ds->xorc.as<K>(), ds->tot.as<u64>(),
                                             ds->work_run.as<u64>(), ds->pgrp.as<u32>(), ds->pent.as<uint2>(), st,
                                             fused_count, !keyless);
                 c.launches[XYZB_STAGE_SORT] += fused_count ? 2 : 3;
-                // keyless: 4-byte records (local bucket | column) where both fit 32 bits
-                const bool packed = keyless && kern::part_packed_ok(int(M) - pk, p, part_hash);
-                if (keyless) {  // the records straight from the row planes (no key array)
-                    const u64 D = u64(1) << pk;
-                    dim3 g(static_cast<u32>(ceil_div(ds->P32, 128)), static_cast<u32>(nb));
-                    auto* ps = packed ? kern::project_scatter<true> : kern::project_scatter<false>;
-                    ps<<<g, 128, 0, st>>>(ds->Xr.as<u32>(), ds->P32, p, rows, int(M), ds->xorc.as<K>(), int(M) - pk,
-                                          part_hash ? 1 : 0, ds->pgrp.as<u32>() + nb * D, ds->pent.as<uint2>());
-                    XYZB_LAUNCH_CHECK();
-                }
+                if (keyless && !fixed_part) scatter_records(ds->pgrp.as<u32>() + (nb << pk));
                 e2 = clk.mark();
                 clk.span(XYZB_STAGE_SORT, e1, e2);
-                c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);  // keys read twice, records written
-                c.bytes[XYZB_STAGE_JOIN] += nb * p * 8 * 2;                 // records read by both join passes
+                const u64 rec_bytes = packed ? 4 : 8;
+                if (keyless)  // M row-plane words per 32 columns (twice with a count pass), records written
+                    c.bytes[XYZB_STAGE_SORT] += nb * ((fixed_part ? 1 : 2) * M * ds->P32 * 4 + p * rec_bytes);
+                else  // keys read twice, records written
+                    c.bytes[XYZB_STAGE_SORT] += nb * p * (2 * sizeof(K) + 8);
+                c.bytes[XYZB_STAGE_JOIN] += nb * p * rec_bytes * (one_pass_join ? 1 : 2);  // records read per join pass
                 // ---- join: per (run, partition) bucket tables in shared memory; |E_r|, guard, blocks ----
                 kern::part_join_launch(nb, p, int(M), pk, part_hash, ds->xorc.as<K>(), c.guard, hmax, vb[0],
                                        ds->tot.as<u64>(), ds->work_run.as<u64>(), ds->items.as<kern::Item>(), nitems,
                                        static_cast<u32>(item_cap), npairs_b, ds->pairs.as<kern::PairRec>(),
                                        static_cast<u32>(c.pair_cap), ds->pgrp.as<u32>(), ds->pent.as<uint2>(),
-                                       ds->povf.as<u32>(), st, one_pass_join, packed);
+                                       ds->povf.as<u32>(), st, one_pass_join, packed, fixed_cap);
                 c.launches[XYZB_STAGE_JOIN] += one_pass_join ? 1 : 2;
             } else {
                 throw internal_error("xyzb: partitioned grouping needs 32-bit keys");
@@ -2127,6 +2150,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     if (binned_eligible(ds, q)) turn = std::unique_lock<std::mutex>(device_search_mutex(ds->device));
     for (int attempt = 0; attempt < 8; ++attempt) {
         ds->clock.spans.resize(spans0);
+        c.attempts += 1;
         if (c.M <= 31) run_batches<u32>(c); else run_batches<u64>(c);  // u32 holds M bits + the side bit
         const u64 nbt = c.nbatches;
         u32* top_counts = nullptr;
@@ -2161,7 +2185,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
             small_copy(hs + o_pairs, ds->npairs.p, nbt * 4, ds->stream);
         small_copy(hs + o_enum, ds->enumerated.p, Rall * 8, ds->stream);
         small_copy(hs + o_ver, ds->verified.p, Rall * 8, ds->stream);
-        small_copy(hs + o_ovf, ds->povf.p, 4, ds->stream);
+        small_copy(hs + o_ovf, ds->povf.p, 8, ds->stream);
         if (c.topk_all)
             small_copy(hs + o_tk, ds->tk_state.p, sizeof(topk::State), ds->stream);
         if (c.binned)
@@ -2202,6 +2226,11 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
         }
         const bool povf = *reinterpret_cast<const u32*>(hs + o_ovf) != 0;
         if (povf) c.no_hash = true;  // a hashed partition overflowed: redo on the sorted path
+        const bool fovf = reinterpret_cast<const u32*>(hs + o_ovf)[1] != 0;
+        if (fovf) {  // a fixed-capacity partition overflowed: count the partitions
+            c.no_fixed_part = true;
+            ds->part_fixed_fails += 1;
+        }
         bool tk_redo = false;
         if (c.topk_all) {
             topk::State ts;
@@ -2219,7 +2248,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
                 tk_redo = true;
             }
         }
-        if (!povf && !tk_redo && !bin_redo && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
+        if (!povf && !fovf && !tk_redo && !bin_redo && H <= ds->hit_cap && need <= c.item_cap && pneed <= c.pair_cap) {
             std::memcpy(enumerated.data(), hs + o_enum, Rall * 8);
             std::memcpy(verified.data(), hs + o_ver, Rall * 8);
             if (c.pair_cap) {  // the pair list (16 B per canonical pair) is written by the join
@@ -2293,6 +2322,7 @@ void do_search(xyzb_dataset* ds, const xyzb_response* resp, const xyzb_params* q
     out->gamma_effective = c.gamma;
     if (c.topk_all) out->gamma_effective = topk_filter(hits, order, topk);
     out->devices_used = 1;
+    out->attempts = c.attempts;
     // counters over executed runs (in pass/rep order)
     u64 reps = 0, enumc = 0, aborted = 0, ver = 0;
     for (u32 r : c.plan.rid) {
@@ -2996,6 +3026,7 @@ void merge_parts(xyzb_dataset* ds, const xyzb_result* parts, u64 n_parts, const 
             out->verify_kernel_ms += r.verify_kernel_ms;
             out->verify_launches += r.verify_launches;
             out->devices_used = std::max<u64>(out->devices_used, r.devices_used);
+            out->attempts = std::max<u64>(out->attempts, r.attempts);
         }
         if (all.size() > 0xffffffffull) throw internal_error("xyzb_merge_results: too many hits");
         const u32 H = static_cast<u32>(all.size());
@@ -3416,6 +3447,7 @@ int xyzb_test_set_option(const char* name, long long value) {
                                    : s == "binned_wshift"   ? &o.binned_wshift
                                    : s == "binned_cap"      ? &o.binned_cap
                                    : s == "one_pass_join"   ? &o.one_pass_join
+                                   : s == "part_fixed"      ? &o.part_fixed
                                                             : nullptr;
     if (!slot) return XYZB_E_DATA;
     slot->store(value);

@@ -207,16 +207,25 @@ __global__ void __launch_bounds__(128) project_count(const u32* __restrict__ Xr,
 // the key's rank; order inside a partition is immaterial), reserves one range
 // per (CTA, partition) at the run's cursors (part_scan) and writes the
 // (w, column) records there.
+// fixed_cap != 0 (PACKED only): no count pass ran — partition d of run b owns
+// the fixed region [(b D + d) fixed_cap, +fixed_cap) of the record array, the
+// cursors start at 0 and end as the partition sizes (part_scan turns them into
+// the compact positions of the grouped columns afterwards); a record beyond its
+// region is dropped and *fixed_ovf raised (the host redoes the search counted).
 template <bool PACKED>
-__global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ Xr, u64 P32, u64 p,
+__global__ void __launch_bounds__(128, 6) project_scatter(const u32* __restrict__ Xr, u64 P32, u64 p,
                                                        const u32* __restrict__ rows, int M,
                                                        const u32* __restrict__ xorc, int lb, int hashed,
-                                                       u32* __restrict__ cursor, uint2* __restrict__ pe) {
+                                                       u32* __restrict__ cursor, uint2* __restrict__ pe,
+                                                       u32 fixed_cap = 0, u32* __restrict__ fixed_ovf = nullptr) {
     __shared__ u32 srow[64];
-    __shared__ u32 h[1u << kPgMaxK];
+    extern __shared__ u32 ps_dyn[];  // h, lstart, gbase: 2^k words each (project_scatter_smem)
     const u64 b = blockIdx.y;
     const int k = M - lb;
     const u32 D = 1u << k;
+    u32* h = ps_dyn;
+    u32* lstart = ps_dyn + D;
+    u32* gbase = ps_dyn + 2 * D;
     const u32 mask = M >= 32 ? 0xffffffffu : (1u << M) - 1u;
     if (threadIdx.x < M) srow[threadIdx.x] = rows[b * M + threadIdx.x];
     for (u32 d = threadIdx.x; d < D; d += blockDim.x) h[d] = 0;
@@ -242,7 +251,6 @@ __global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ X
     __syncthreads();
     // the CTA's keys grouped by partition in shared memory (lstart: exclusive scan of the counts), then every
     // partition's run written contiguously at its reserved global range
-    __shared__ u32 lstart[1u << kPgMaxK], gbase[1u << kPgMaxK];
     __shared__ uint2 buf[128 * 32];
     __shared__ u32 ws[33];
     {
@@ -267,9 +275,22 @@ __global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ X
     __syncthreads();
     const u32 nk = u32(minu(u64(blockDim.x) * 32, p - u64(blockIdx.x) * blockDim.x * 32));
     if (PACKED) {  // 4-byte records: (local bucket << (32 - lb)) | column (the partition is the record's place)
-        u32* out = reinterpret_cast<u32*>(pe) + b * p;
         const int cb = 32 - lb;
         const u32 lmask = (1u << lb) - 1u;
+        if (fixed_cap) {
+            u32* out = reinterpret_cast<u32*>(pe) + b * D * fixed_cap;
+            bool over = false;
+            for (u32 e = threadIdx.x; e < nk; e += blockDim.x) {
+                const uint2 r = buf[e];
+                const u32 d = r.x >> lb;
+                const u32 pos = gbase[d] + (e - lstart[d]);
+                if (pos < fixed_cap) out[u64(d) * fixed_cap + pos] = ((r.x & lmask) << cb) | r.y;
+                else over = true;
+            }
+            if (over) *fixed_ovf = 1u;
+            return;
+        }
+        u32* out = reinterpret_cast<u32*>(pe) + b * p;
         for (u32 e = threadIdx.x; e < nk; e += blockDim.x) {
             const uint2 r = buf[e];
             const u32 d = r.x >> lb;
@@ -284,6 +305,8 @@ __global__ void __launch_bounds__(128) project_scatter(const u32* __restrict__ X
         out[gbase[d] + (e - lstart[d])] = r;
     }
 }
+
+inline size_t project_scatter_smem(int k) { return (size_t(3) << k) * 4; }
 
 // 4-byte partition records fit when the local bucket (lb bits) and the column share 32 bits (dense partitions).
 inline bool part_packed_ok(int lb, u64 p, bool hashed) {
@@ -390,7 +413,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
                                                         u64* __restrict__ work_run, Item* __restrict__ items,
                                                         u32* __restrict__ nitems, u32 item_cap,
                                                         u32* __restrict__ npairs, PairRec* __restrict__ pairs,
-                                                        u32 pair_cap) {
+                                                        u32 pair_cap, u32 fixed_cap) {
     extern __shared__ __align__(16) u32 T[];  // 2^lb local buckets
     __shared__ u32 ws[68];
     __shared__ u64 red[2][kPjThreads / 32];
@@ -401,10 +424,13 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     const u32 c = xorc[b] & mask;
     if (EMIT == 1 && tot[b] > guard) return;  // aborted run: nothing to emit (uniform per CTA)
     const u32 beg = pbeg[u64(b) * (D + 1) + d], end = pbeg[u64(b) * (D + 1) + d + 1];
-    const u32 cnt = end - beg;
-    // records: (w, column), or packed (local bucket << (32 - lb)) | column (project_scatter<true>)
+    // records: (w, column), or packed (local bucket << (32 - lb)) | column (project_scatter<true>), then
+    // either in partition order at the run's positions or in the partition's fixed region (fixed_cap;
+    // an overflowing partition keeps its first fixed_cap records and the search is redone)
     using Rec = typename std::conditional<PACKED, u32, uint2>::type;
-    const Rec* e = reinterpret_cast<const Rec*>(pe) + u64(b) * p + beg;
+    const u32 cnt = fixed_cap ? min(end - beg, fixed_cap) : end - beg;
+    const Rec* e = reinterpret_cast<const Rec*>(pe) +
+                   (fixed_cap ? (u64(b) * D + d) * fixed_cap : u64(b) * p + beg);
     const int cb = 32 - lb;
     auto bucket_of = [&](const Rec& r) -> u32 {
         if constexpr (PACKED) return r >> cb; else return r.x & lmask;
@@ -880,7 +906,8 @@ inline void part_partition_launch(const u32* keys, u64 B, u64 p, int M, int k, b
 inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* xorc, u64 guard, u32 hmax,
                              u32* grouped, u64* tot, u64* work_run, Item* items, u32* nitems, u32 item_cap,
                              u32* npairs, PairRec* pairs, u32 pair_cap, const u32* scratch, const uint2* pe,
-                             u32* ovf, cudaStream_t st, bool one_pass = false, bool packed = false) {
+                             u32* ovf, cudaStream_t st, bool one_pass = false, bool packed = false,
+                             u32 fixed_cap = 0) {
     const int lb = M - k;
     const u64 D = u64(1) << k;
     const u32* pbeg = scratch + 2 * B * D;
@@ -899,7 +926,7 @@ inline void part_join_launch(u64 B, u64 p, int M, int k, bool hash, const u32* x
     auto launch = [&](auto kernel, size_t smem) {
         func_smem(kernel, 64 << 10);
         kernel<<<gj, kPjThreads, smem, st>>>(pe, pbeg, p, M, lb, xorc, guard, hmax, grouped, tot, work_run, items, nitems,
-                                             item_cap, npairs, pairs, pair_cap);
+                                             item_cap, npairs, pairs, pair_cap, fixed_cap);
         XYZB_LAUNCH_CHECK();
     };
     if (one_pass) {

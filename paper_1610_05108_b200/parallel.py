@@ -17,7 +17,7 @@ from . import _abi
 from .report import SearchConfig, SearchReport
 
 _COUNTERS = ("repetitions_run", "candidates_checked", "candidates_enumerated", "aborted_repetitions",
-             "runs_executed", "verified_pairs", "kernel_launches", "verify_launches", "devices_used")
+             "runs_executed", "verified_pairs", "kernel_launches", "verify_launches", "devices_used", "attempts")
 _FLOATS = ("wall_time_s", "estimated_c", "gamma0", "device_ms", "verify_kernel_ms", "gamma_effective")
 _HIT_DT = np.dtype({"names": ["j", "k", "strength", "rep", "sign"], "formats": ["<u4", "<u4", "<f8", "<u4", "<i4"],
                     "offsets": [0, 4, 8, 16, 20], "itemsize": C.sizeof(_abi.Hit)})

@@ -101,6 +101,7 @@ class SearchReport:
     verify_launches: int = 0
     gamma_effective: float = 0.0
     devices_used: int = 0
+    attempts: int = 1
 
     def hit_array(self) -> np.ndarray:
         """Hits as a structured array (j, k, strength, rep, sign)."""
@@ -132,7 +133,7 @@ def report_from_result(res: _abi.Result) -> SearchReport:
     for name in ("repetitions_run", "candidates_checked", "candidates_enumerated", "aborted_repetitions",
                  "wall_time_s", "estimated_c", "gamma0", "m_used", "l_used", "runs_executed",
                  "verified_pairs", "device_ms", "kernel_launches", "verify_kernel_ms", "verify_launches",
-                 "gamma_effective", "devices_used"):
+                 "gamma_effective", "devices_used", "attempts"):
         setattr(r, name, getattr(res, name))
     r.stage_ms = {k: float(res.stage_ms[i]) for i, k in enumerate(_abi.STAGE_NAMES)}
     r.stage_bytes = {k: int(res.stage_bytes[i]) for i, k in enumerate(_abi.STAGE_NAMES)}

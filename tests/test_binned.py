@@ -182,3 +182,33 @@ def test_binned_one_pass_join_with_aborted_runs(engine_options, mode):
     if mode == "hits":
         ok, msg = ck.same_hits(got, ck.ref_search(x, y, cfg))
         assert ok, msg
+
+
+@pytest.mark.parametrize("mode", ["hits", "candidates"])
+def test_binned_fixed_capacity_partitions(engine_options, mode):
+    """The keyless partition pass without its count pass (fixed-capacity
+    regions of 4-byte records, config 4's default): equal to the counted pass
+    and to the reference; a capacity the partitions overflow is flagged on the
+    device and the search redone counted."""
+    xb = _xb()
+    x, y = _data(5000, 6000, 47)
+    cfg = xb.SearchConfig(m=12, l=6, gamma=0.525, seed=8, top_k=25, top_k_mode=mode, estimate_complexity=False,
+                          threads=1)
+    engine_options(binned=1, binned_wshift=11, grouping="part", part_fixed=-1)
+    counted = xb.Dataset(x).search(y, cfg)
+    engine_options(part_fixed=0)
+    fixed = xb.Dataset(x).search(y, cfg)
+    engine_options(part_fixed=8)  # 8 records per partition: every partition overflows
+    ds = xb.Dataset(x)
+    redone = ds.search(y, cfg)
+    engine_options(part_fixed=0)
+    again = ds.search(y, cfg)  # one overflow does not switch the dataset to counting
+    for got in (fixed, redone, again):
+        ok, msg = ck.same_hits(got, counted)
+        assert ok, msg
+        assert got.top_k == counted.top_k and _counters(got) == _counters(counted)
+    assert len(counted.hits) > 0
+    assert redone.attempts == fixed.attempts + 1 and again.attempts == fixed.attempts
+    if mode == "hits":
+        ok, msg = ck.same_hits(fixed, ck.ref_search(x, y, cfg))
+        assert ok, msg
