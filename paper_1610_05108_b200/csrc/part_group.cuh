@@ -370,6 +370,31 @@ __global__ void __launch_bounds__(1024) part_scan(const u32* __restrict__ pcnt, 
 // Exclusive scan of the n counters in place (each warp owns a contiguous
 // segment walked in conflict-free 32-word steps): counters -> bucket starts.
 __device__ __forceinline__ void part_table_scan(u32* T, u32 n, u32* ws) {
+    if (n >= 4 * blockDim.x && n % (4 * blockDim.x) == 0) {
+        // large tables (2^12 buckets on 512 threads): every thread scans its own run of n / blockDim
+        // consecutive counters with 16-byte accesses, one block scan of the thread sums in between
+        const u32 per4 = n / (4 * blockDim.x);
+        uint4* T4 = reinterpret_cast<uint4*>(T) + threadIdx.x * per4;
+        u32 loc = 0;
+        for (u32 q = 0; q < per4; ++q) {
+            const uint4 v = T4[q];
+            loc += v.x + v.y + v.z + v.w;
+        }
+        u32 total;
+        u32 run = block_exclusive(loc, ws, &total);
+        for (u32 q = 0; q < per4; ++q) {
+            const uint4 v = T4[q];
+            uint4 o;
+            o.x = run;
+            o.y = o.x + v.x;
+            o.z = o.y + v.y;
+            o.w = o.z + v.z;
+            run = o.w + v.w;
+            T4[q] = o;
+        }
+        __syncthreads();
+        return;
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const u32 nw = blockDim.x >> 5;
     const u32 seg = max(32u, (n + nw - 1) / nw);
@@ -446,7 +471,11 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
             atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), 1ull);
         return;
     }
-    for (u32 i = threadIdx.x; i < L; i += blockDim.x) T[i] = 0;
+    if (L >= 4) {
+        for (u32 i = threadIdx.x; i < L / 4; i += blockDim.x) reinterpret_cast<uint4*>(T)[i] = make_uint4(0, 0, 0, 0);
+    } else {
+        for (u32 i = threadIdx.x; i < L; i += blockDim.x) T[i] = 0;
+    }
     __syncthreads();
     // entries of the partition: in registers when they fit (the count's atomic
     // returns each entry's rank in its bucket, so the scatter needs no second
@@ -484,7 +513,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     // c != 0: buckets u (even) and u | 1 form one block; c == 0: every bucket
     // is a diagonal block. li walks the block heads.
     const u32 NL = c ? L / 2 : L;
-    if (EMIT != 1) {  // |E_r| incl. the diagonal and the canonical work (EMIT = 2: then emit regardless)
+    if (EMIT == 0) {  // |E_r| incl. the diagonal and the canonical work (EMIT = 2: summed in the emission count walk)
         u64 pa = 0, wa = 0;
         for (u32 li = threadIdx.x; li < NL; li += blockDim.x) {
             if (c == 0) {
@@ -513,7 +542,7 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
             if (a) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(a));
             if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
         }
-        if (EMIT == 0) return;
+        return;
     }
     // bucket starts, scatter (T ends as bucket ends), then the blocks
     part_table_scan(T, L, ws);
@@ -590,12 +619,41 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     };
     const bool pair_list = npairs != nullptr;
     u32 my_items = 0, my_pairs = 0;
+    u64 pa = 0, wa = 0;
     for (u32 li = threadIdx.x; li < NL; li += blockDim.x) {
         const HeadBlock hb = block_of(li);
         u32 ne, np, nsc;
         emit_count(hb, hmax, pair_list, ne, np, nsc);
         my_items += ne;
         my_pairs += np;
+        if (EMIT == 2) {
+            pa += hb.pairs;
+            wa += hb.work;
+        }
+    }
+    if (EMIT == 2) {  // the run's |E_r| incl. the diagonal and canonical work (the guard is applied when binned)
+        if (c == 0)  // diagonal blocks: a lone column still counts its j == k pair (block_of leaves it out)
+            for (u32 li = threadIdx.x; li < NL; li += blockDim.x) {
+                u32 bx, cx;
+                group(li, bx, cx);
+                if (cx == 1) pa += 1;
+            }
+        pa = warp_sum(pa);
+        wa = warp_sum(wa);
+        if (lane == 0) {
+            red[0][wid] = pa;
+            red[1][wid] = wa;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u64 a = 0, w = 0;
+            for (int q = 0; q < nw; ++q) {
+                a += red[0][q];
+                w += red[1][q];
+            }
+            if (a) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(a));
+            if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
+        }
     }
     u32 ti, tp;
     u32 ibase = block_exclusive(my_items, ws, &ti);
@@ -762,7 +820,7 @@ __global__ void __launch_bounds__(kHsThreads) part_join_hash(const uint2* __rest
             if (a) atomicAdd(reinterpret_cast<unsigned long long*>(tot + b), static_cast<unsigned long long>(a));
             if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
         }
-        if (EMIT == 0) return;
+        return;
     }
     // Only keys that are in a block are grouped: c == 0, a key with >= 2
     // records (a diagonal block); else a slot holding both keys of the pair.
