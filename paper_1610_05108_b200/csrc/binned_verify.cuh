@@ -166,7 +166,7 @@ __device__ __forceinline__ void reserve(PartSmem& sm, u32 nreg, u32* __restrict_
 // kPartStep records (held in registers) is counted per window in shared
 // memory, reserved with one global atomic per window and written at base +
 // shared rank (runs of ~256 records).
-__global__ void __launch_bounds__(kPartThreads) bin_window(const PairRec* __restrict__ pairs,
+__global__ void __launch_bounds__(kPartThreads, 3) bin_window(const PairRec* __restrict__ pairs,
                                                            const u32* __restrict__ npairs, u32 pair_cap,
                                                            const u32* __restrict__ nitems, u32 item_cap, u32 run0,
                                                            const int8_t* __restrict__ run_sign, u32 nruns,

@@ -671,10 +671,10 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
     ibase += ws[66];
     pbase += ws[67];
     if (inreg)
-        emit_blocks_coop(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped,
+        emit_blocks_warp(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped,
                          sg, beg);
     else
-        emit_blocks_coop(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped,
+        emit_blocks_warp(block_of, NL, b, hmax, p, pair_list, ibase, pbase, items, item_cap, pairs, pair_cap, grouped,
                          grouped + off, 0u);
 }
 

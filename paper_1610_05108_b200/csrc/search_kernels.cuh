@@ -439,6 +439,85 @@ __device__ __forceinline__ void emit_blocks_coop(BlockOf block_of, u32 T, u32 b,
     }
 }
 
+// The same pass with every inline block written by the whole warp: the 32
+// heads of a warp step hold ~30 pairs in ~12 non-empty blocks (Poisson
+// buckets), so a lane walking its own block leaves most of the warp idle.
+// The warp owns the contiguous slot range of its 32 threads (pbase is a
+// thread-major exclusive scan); within it each step lays its blocks out lane
+// after lane, and pair idx of the step goes to the lane idx % 32: the owner
+// block by a binary search over the lanes' inclusive inline counts, its
+// fields by shuffles, one 16-byte record per lane.
+template <class BlockOf>
+__device__ __forceinline__ void emit_blocks_warp(BlockOf block_of, u32 T, u32 b, u32 hmax, u64 p, bool pair_list,
+                                                 u32 ibase, u32 pbase, Item* __restrict__ items, u32 item_cap,
+                                                 PairRec* __restrict__ pairs, u32 pair_cap,
+                                                 const u32* __restrict__ grouped, const u32* gl, u32 gbias) {
+    const int lane = threadIdx.x & 31;
+    uint4* dst = reinterpret_cast<uint4*>(pairs);
+    u32 woff = __shfl_sync(0xffffffffu, pbase, 0);
+    for (u32 li0 = 0; li0 < T; li0 += blockDim.x) {
+        const u32 li = li0 + threadIdx.x;
+        HeadBlock hb;
+        if (li < T) hb = block_of(li);
+        u32 ne, np, nsc;
+        emit_count(hb, hmax, pair_list, ne, np, nsc);
+        const bool inl = pair_list && hb.work != 0 && hb.work <= kInlinePairs;
+        const u32 ni = inl ? np : 0u;
+        u32 ea = np, ei = ni;  // inclusive warp scans of all pairs / inline pairs
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t1 = __shfl_up_sync(0xffffffffu, ea, o), t2 = __shfl_up_sync(0xffffffffu, ei, o);
+            if (lane >= o) {
+                ea += t1;
+                ei += t2;
+            }
+        }
+        const u32 tot_all = __shfl_sync(0xffffffffu, ea, 31), tot_inl = __shfl_sync(0xffffffffu, ei, 31);
+        const u32 xa = ea - np;  // this lane's first slot within the warp's share of the step
+        if (ne) {  // large blocks: items (their pairs are expanded later at it.pad)
+            emit_write(hb, b, hmax, pair_list, ne, nsc, ibase, woff + xa, items, item_cap, pairs, pair_cap, p, grouped);
+            ibase += ne;
+        }
+        for (u32 idx0 = 0; idx0 < tot_inl; idx0 += 32) {
+            const u32 idx = idx0 + lane;
+            u32 ow = 0;  // owner lane: the first whose inclusive inline count exceeds idx
+#pragma unroll
+            for (int stp = 16; stp > 0; stp >>= 1) {
+                const u32 v = __shfl_sync(0xffffffffu, ei, int(ow + stp - 1));
+                if (v <= idx) ow += stp;
+            }
+            ow = min(ow, 31u);
+            const u32 o_hs = __shfl_sync(0xffffffffu, hb.hs, ow), o_hc = __shfl_sync(0xffffffffu, hb.hc, ow);
+            const u32 o_ss = __shfl_sync(0xffffffffu, hb.ss, ow), o_sc = __shfl_sync(0xffffffffu, hb.sc, ow);
+            const u32 o_fl = __shfl_sync(0xffffffffu, hb.flags, ow);
+            const u32 o_xa = __shfl_sync(0xffffffffu, xa, ow);
+            const u32 o_ei = __shfl_sync(0xffffffffu, ei - ni, ow);  // owner's first inline index
+            if (idx < tot_inl) {
+                u32 l = idx - o_ei, h = 0, q;
+                const bool diag = o_fl & 2u;
+                if (diag) {  // pairs (h, q), h < q < hc
+                    while (l >= o_hc - 1 - h) {
+                        l -= o_hc - 1 - h;
+                        ++h;
+                    }
+                    q = h + 1 + l;
+                } else {
+                    // l < 32, o_sc <= 32: the fp32 quotient of l + 0.5 is at least 1/64 from an integer
+                    h = __float2uint_rz((float(l) + 0.5f) * __frcp_rn(float(o_sc)));
+                    q = l - h * o_sc;
+                }
+                const u32 slot = woff + o_xa + (idx - o_ei);
+                if (slot < pair_cap) {
+                    const u32 hcol = gl[o_hs + h - gbias], scol = gl[o_ss + q - gbias];
+                    const bool first_held = diag || (o_fl & 1u);
+                    dst[slot] = make_uint4(first_held ? hcol : scol, first_held ? scol : hcol, b, o_fl);
+                }
+            }
+        }
+        woff += tot_all;
+    }
+}
+
 // Emit the canonical work items of one block (per thread; CTA-aggregated
 // slot reservation). Item t of a block: held chunk t / nsc (<= hmax
 // columns), streamed chunk t % nsc (<= kStreamChunk columns), so one big
