@@ -67,6 +67,8 @@ __device__ __forceinline__ u32 rec_diag(u64 r) { return u32(r >> 48) & 1u; }
 __device__ __forceinline__ u32 rec_neg(u64 r) { return u32(r >> 49) & 1u; }
 __device__ __forceinline__ u32 rec_run(u64 r) { return u32(r >> 50); }
 
+__device__ __forceinline__ u32 smem_u32(const void* p) { return u32(__cvta_generic_to_shared(p)); }
+
 // ---- partition passes: records -> fixed-capacity regions ----
 // A CTA takes one contiguous range (long runs per region and reservation):
 // sweep 1 counts its records per region in shared memory, one global
@@ -166,7 +168,7 @@ __device__ __forceinline__ void reserve(PartSmem& sm, u32 nreg, u32* __restrict_
 // kPartStep records (held in registers) is counted per window in shared
 // memory, reserved with one global atomic per window and written at base +
 // shared rank (runs of ~256 records).
-__global__ void __launch_bounds__(kPartThreads, 3) bin_window(const PairRec* __restrict__ pairs,
+__global__ void __launch_bounds__(kPartThreads) bin_window(const PairRec* __restrict__ pairs,
                                                            const u32* __restrict__ npairs, u32 pair_cap,
                                                            const u32* __restrict__ nitems, u32 item_cap, u32 run0,
                                                            const int8_t* __restrict__ run_sign, u32 nruns,
@@ -184,16 +186,33 @@ __global__ void __launch_bounds__(kPartThreads, 3) bin_window(const PairRec* __r
         neg[t] = int8_t((run_sign[t] < 0 ? 1 : 0) | (tot[t] > guard ? 2 : 0));
     __syncthreads();
     const uint4* P4 = reinterpret_cast<const uint4*>(pairs);
-    for (u64 s0 = u64(blockIdx.x) * kPartStep; s0 < P; s0 += u64(gridDim.x) * kPartStep) {
-        u64 rec[R];
-        u32 kt[R], rk[R];
+    // the next step's records travel (cp.async) into thread-private slots of shared memory while the
+    // current step is counted, reserved and written: a thread reads back only what it fetched itself
+    extern __shared__ __align__(16) uint4 stage[];  // [kPartStep]
+    auto fetch = [&](u64 s0) {
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
-            const uint4 pr = i < P ? __ldg(P4 + i) : make_uint4(0, 0, 0, 0);
+            if (i < P)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(stage + u * kPartThreads + threadIdx.x)),
+                             "l"(P4 + i)
+                             : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (u64(blockIdx.x) * kPartStep < P) fetch(u64(blockIdx.x) * kPartStep);
+    for (u64 s0 = u64(blockIdx.x) * kPartStep; s0 < P; s0 += u64(gridDim.x) * kPartStep) {
+        u64 rec[R];
+        u32 kt[R], rk[R];
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
+            const uint4 pr = i < P ? stage[u * kPartThreads + threadIdx.x] : make_uint4(0, 0, 0, 0);
             rec[u] = rec_make(pr.x, pr.y, (pr.w >> 1) & 1u, neg[pr.z] & 1, run0 + pr.z);
             kt[u] = i < P && !(neg[pr.z] & 2) ? pr.y >> wshift : 0xffffffffu;
         }
+        if (s0 + u64(gridDim.x) * kPartStep < P) fetch(s0 + u64(gridDim.x) * kPartStep);
 #pragma unroll
         for (int u = 0; u < R; ++u)
             if (kt[u] != 0xffffffffu) rk[u] = atomicAdd(&cnt[kt[u]], 1u);
@@ -453,8 +472,6 @@ struct BinVerifyArgs {
     u32 phase_follows;    // top-K: this window's ranks are consumed by a phase right after it (else bit 2 of
                           // *rank_fail is raised when the window still runs in the rank-writing first phase)
 };
-
-__device__ __forceinline__ u32 smem_u32(const void* p) { return u32(__cvta_generic_to_shared(p)); }
 
 __device__ __forceinline__ u64 ld_stream(const u64* p, u64 pol) {
     u64 v;
@@ -733,6 +750,7 @@ __global__ void __launch_bounds__(256) emit_list(const u64* __restrict__ list, c
     }
 }
 
+inline size_t bin_window_smem() { return size_t(kPartStep) * 16; }
 inline size_t verify_smem(u32 Wp) { return size_t(2) * kBinJT * (Wp / 2) * 16; }
 
 } // namespace bins

@@ -1640,7 +1640,8 @@ void run_batches(SearchCtx& c) {
             cudaEvent_t ev0 = clk.mark();
             clk.span(XYZB_STAGE_JOIN, e3, ev0);  // pair expansion belongs to the join
             if (c.binned) {  // the batch's pairs go to their z-side windows; verified after the last batch
-                bins::bin_window<<<kSMs * 3, bins::kPartThreads, 0, st>>>(
+                func_smem(bins::bin_window, bins::bin_window_smem());
+                bins::bin_window<<<kSMs * 4, bins::kPartThreads, bins::bin_window_smem(), st>>>(
                     ds->pairs.as<kern::PairRec>(), np, static_cast<u32>(c.pair_cap), A.nitems, A.item_cap,
                     static_cast<u32>(b0), rsign, static_cast<u32>(nb), ds->tot.as<u64>(), c.guard, c.wshift,
                     static_cast<u32>(c.nkt),
