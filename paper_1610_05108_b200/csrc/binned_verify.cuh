@@ -93,15 +93,20 @@ struct PartSmem {
 
 // One sweep-2 step: rec[u] (valid when rg[u] < nreg) -> dst regions of `cap`
 // records at runo[rg] (the CTA's reservation, advanced per step).
+// gcnt != nullptr: no count sweep ran — the step reserves its own ranges in the global region counters (one
+// atomic per non-empty region and step) instead of advancing a reservation of the whole CTA.
 template <int THREADS, int R, class RegionOf>
 __device__ __forceinline__ void scatter_step(PartSmem& sm, const u64 (&rec)[R], const u32 (&rg)[R], u32 nreg,
                                              RegionOf region_of, u64* __restrict__ dst, u64 stride, u32 cap,
-                                             u64* __restrict__ ovf, u32 ovf_cap, u32* __restrict__ ovf_n) {
+                                             u64* __restrict__ ovf, u32 ovf_cap, u32* __restrict__ ovf_n,
+                                             u32* __restrict__ gcnt = nullptr) {
     u32 rk[R];
 #pragma unroll
     for (int u = 0; u < R; ++u)
         if (rg[u] < nreg) rk[u] = atomicAdd(&sm.lcnt[rg[u]], 1u);
     __syncthreads();
+    if (gcnt)
+        for (u32 g = threadIdx.x; g < nreg; g += THREADS) sm.runo[g] = sm.lcnt[g] ? atomicAdd(gcnt + g, sm.lcnt[g]) : 0u;
     if (threadIdx.x < 32) {  // exclusive scan of the step's region counts (<= 256, 8 per lane)
         const int lane = threadIdx.x;
         constexpr int PER = kMaxRegions / 32;
@@ -146,11 +151,29 @@ __device__ __forceinline__ void scatter_step(PartSmem& sm, const u64 (&rec)[R], 
     }
     __syncthreads();
     for (u32 g = threadIdx.x; g < nreg; g += THREADS) {
-        sm.runo[g] += sm.lcnt[g];
+        if (!gcnt) sm.runo[g] += sm.lcnt[g];
         sm.lcnt[g] = 0;
     }
     __syncthreads();
 }
+
+// Sweep 2's loads one step ahead: the next step's records travel (cp.async)
+// into thread-private slots of dynamic shared memory (kPartStep x 8 B) while
+// the current step is grouped and written; a thread reads back only what it
+// fetched itself, so no barrier is involved.
+__device__ __forceinline__ void step_fetch(u64* stage, const u64* __restrict__ src, u64 s0, u64 end) {
+#pragma unroll
+    for (int u = 0; u < kPartPerThread; ++u) {
+        const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
+        if (i < end)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stage + u * kPartThreads + threadIdx.x)),
+                         "l"(src + i)
+                         : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void step_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+inline size_t step_stage_smem() { return size_t(kPartStep) * 8; }
 
 // Sweep 1's counts -> the CTA's reservations (runo) in the global region counters.
 template <int THREADS>
@@ -254,31 +277,24 @@ __global__ void __launch_bounds__(kPartThreads) bin_split(const u64* __restrict_
     const u64* src = S + u64(kt) * cap_kt;
     for (u32 t = threadIdx.x; t < nbh; t += blockDim.x) sm.lcnt[t] = 0;
     __syncthreads();
-    for (u64 s0 = c0; s0 < c1; s0 += kPartStep) {
-        u32 h[R];
-#pragma unroll
-        for (int u = 0; u < R; ++u) {
-            const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
-            h[u] = i < c1 ? rec_a(__ldg(src + i)) >> SH : 0xffffffffu;
-        }
-#pragma unroll
-        for (int u = 0; u < R; ++u)
-            if (h[u] != 0xffffffffu) atomicAdd(&sm.lcnt[h[u]], 1u);
-    }
-    reserve<kPartThreads>(sm, nbh, bcnt + u64(kt) * nbh);
+    // one sweep: every step of kPartStep records reserves its runs in the buckets itself
     auto region_of = [](u64 r) { return rec_a(r) >> SH; };
     u64* dst = B + u64(kt) * nbh * cap_bucket;
+    extern __shared__ __align__(16) u64 stage8[];  // [kPartStep]
+    step_fetch(stage8, src, c0, c1);
     for (u64 s0 = c0; s0 < c1; s0 += kPartStep) {
         u64 rec[R];
         u32 rg[R];
+        step_wait();
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const u64 i = s0 + u64(u) * kPartThreads + threadIdx.x;
-            rec[u] = i < c1 ? __ldg(src + i) : 0ull;
+            rec[u] = i < c1 ? stage8[u * kPartThreads + threadIdx.x] : 0ull;
             rg[u] = i < c1 ? rec_a(rec[u]) >> SH : 0xffffffffu;
         }
+        if (s0 + kPartStep < c1) step_fetch(stage8, src, s0 + kPartStep, c1);
         scatter_step<kPartThreads, R>(sm, rec, rg, nbh, region_of, dst, cap_bucket, cap_bucket, ovf, ovf_cap,
-                                      ovf_n);
+                                      ovf_n, bcnt + u64(kt) * nbh);
     }
 }
 

@@ -1045,7 +1045,8 @@ void binned_verify(SearchCtx& c) {
     cudaEvent_t e0 = clk.mark();
     const u32 nbuckets = static_cast<u32>(u64(nkt) * c.nbh);
     const u32 cpk = static_cast<u32>(ceil_div(kSMs * 4, nkt));  // CTAs per window
-    bins::bin_split<<<cpk * nkt, bins::kPartThreads, 0, st>>>(
+    func_smem(bins::bin_split, bins::step_stage_smem());
+    bins::bin_split<<<cpk * nkt, bins::kPartThreads, bins::step_stage_smem(), st>>>(
         ds->bin_s.as<u64>(), static_cast<u32>(c.cap_kt), ds->bin_wcnt.as<u32>(), cpk, static_cast<u32>(c.nbh),
         ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket), ds->bin_cnt.as<u32>(), ds->bin_ovf.as<u64>(),
         static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
