@@ -20,11 +20,11 @@
 // writes stay long runs: per batch, each pair goes to its z-side window (16
 // regions at config 4); after the last batch, each window is split by the
 // x-side tile >> 7 (128 buckets), and one CTA per bucket splits it by the
-// tile's low 7 bits; tile_sort then orders every tile by x column. Regions
-// have fixed capacities from the previous search's mean fills; a pair whose
-// region is full goes to an overflow list, verified afterwards by a plain
-// gather; an overflowing list makes the host redo the search with a larger
-// one.
+// tile's low 7 bits (every tile a fixed 1/128 of the bucket's region);
+// tile_sort then orders every tile by x column. Regions have fixed
+// capacities from the previous search's mean fills; a pair whose region is
+// full goes to an overflow list, verified afterwards by a plain gather; an
+// overflowing list makes the host redo the search with a larger one.
 //
 // Pair records (u64): x-side column (24 bits) | z-side column (24) | diagonal
 // flag (1, at bit 48) | the run's pass is negative (1, bit 49) | global run
@@ -70,15 +70,14 @@ __device__ __forceinline__ u32 rec_run(u64 r) { return u32(r >> 50); }
 __device__ __forceinline__ u32 smem_u32(const void* p) { return u32(__cvta_generic_to_shared(p)); }
 
 // ---- partition passes: records -> fixed-capacity regions ----
-// A CTA takes one contiguous range (long runs per region and reservation):
-// sweep 1 counts its records per region in shared memory, one global
-// reservation per (CTA, region); sweep 2 takes steps of kPartThreads x R
-// records (R loads in flight per thread), groups each step by region in
-// shared memory (an unstable local counting sort: order inside a region is
-// immaterial) and writes every region's run contiguously, so the stores are
-// whole sectors instead of one scattered 8-byte store per record (ncu: the
-// scattered form was bound on L2 store transactions). A record whose region
-// is full goes to the overflow list.
+// Every pass is one sweep over steps of kPartThreads x R records (R loads in
+// flight per thread; bin_window and bin_split prefetch the next step by
+// cp.async): a step is grouped by region in shared memory (an unstable local
+// counting sort: order inside a region is immaterial), reserves its runs with
+// one global atomic per non-empty region and writes every region's run
+// contiguously, so the stores are whole sectors instead of one scattered
+// 8-byte store per record (ncu: the scattered form was bound on L2 store
+// transactions). A record whose region is full goes to the overflow list.
 constexpr int kHiBits = 7;                  // x-side tiles per bucket: 128
 constexpr u32 kMaxRegions = 256;            // regions per partition pass (shared counters)
 constexpr int kPartThreads = 512, kPartPerThread = 8;
@@ -91,22 +90,20 @@ struct PartSmem {
     u32 total;
 };
 
-// One sweep-2 step: rec[u] (valid when rg[u] < nreg) -> dst regions of `cap`
-// records at runo[rg] (the CTA's reservation, advanced per step).
-// gcnt != nullptr: no count sweep ran — the step reserves its own ranges in the global region counters (one
-// atomic per non-empty region and step) instead of advancing a reservation of the whole CTA.
+// One step: rec[u] (valid when rg[u] < nreg) -> dst regions of `cap` records;
+// the step reserves its runs in the global region counters gcnt (one atomic
+// per non-empty region).
 template <int THREADS, int R, class RegionOf>
 __device__ __forceinline__ void scatter_step(PartSmem& sm, const u64 (&rec)[R], const u32 (&rg)[R], u32 nreg,
                                              RegionOf region_of, u64* __restrict__ dst, u64 stride, u32 cap,
                                              u64* __restrict__ ovf, u32 ovf_cap, u32* __restrict__ ovf_n,
-                                             u32* __restrict__ gcnt = nullptr) {
+                                             u32* __restrict__ gcnt) {
     u32 rk[R];
 #pragma unroll
     for (int u = 0; u < R; ++u)
         if (rg[u] < nreg) rk[u] = atomicAdd(&sm.lcnt[rg[u]], 1u);
     __syncthreads();
-    if (gcnt)
-        for (u32 g = threadIdx.x; g < nreg; g += THREADS) sm.runo[g] = sm.lcnt[g] ? atomicAdd(gcnt + g, sm.lcnt[g]) : 0u;
+    for (u32 g = threadIdx.x; g < nreg; g += THREADS) sm.runo[g] = sm.lcnt[g] ? atomicAdd(gcnt + g, sm.lcnt[g]) : 0u;
     if (threadIdx.x < 32) {  // exclusive scan of the step's region counts (<= 256, 8 per lane)
         const int lane = threadIdx.x;
         constexpr int PER = kMaxRegions / 32;
@@ -150,10 +147,7 @@ __device__ __forceinline__ void scatter_step(PartSmem& sm, const u64 (&rec)[R], 
         }
     }
     __syncthreads();
-    for (u32 g = threadIdx.x; g < nreg; g += THREADS) {
-        if (!gcnt) sm.runo[g] += sm.lcnt[g];
-        sm.lcnt[g] = 0;
-    }
+    for (u32 g = threadIdx.x; g < nreg; g += THREADS) sm.lcnt[g] = 0;
     __syncthreads();
 }
 
@@ -174,17 +168,6 @@ __device__ __forceinline__ void step_fetch(u64* stage, const u64* __restrict__ s
 }
 __device__ __forceinline__ void step_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 inline size_t step_stage_smem() { return size_t(kPartStep) * 8; }
-
-// Sweep 1's counts -> the CTA's reservations (runo) in the global region counters.
-template <int THREADS>
-__device__ __forceinline__ void reserve(PartSmem& sm, u32 nreg, u32* __restrict__ gcnt) {
-    __syncthreads();
-    for (u32 g = threadIdx.x; g < nreg; g += THREADS) {
-        sm.runo[g] = sm.lcnt[g] ? atomicAdd(gcnt + g, sm.lcnt[g]) : 0u;
-        sm.lcnt[g] = 0;
-    }
-    __syncthreads();
-}
 
 // Per batch: the batch's pair list -> z-side windows (region = kt). With a
 // small fan-out (16 windows at config 4) one sweep suffices: each step of
@@ -299,13 +282,17 @@ __global__ void __launch_bounds__(kPartThreads) bin_split(const u64* __restrict_
 }
 
 // ---- end of the search: each bucket split by the low 7 bits of its x-side tile ----
-// One CTA per bucket: counts per tile, the tiles' starts (bstart / bfill per
-// (window, tile), relative to the window's first bucket), then the records
-// grouped per step and written as runs into their tile.
+// One CTA per bucket, one sweep: every tile owns a fixed region of
+// cap_bucket / 128 records inside the bucket (bstart, relative to the window's
+// first bucket); each step of kPartStep records is grouped by tile in shared
+// memory, reserves its runs in the tiles' fill counters (bfill, zeroed by the
+// host; one atomic per non-empty tile and step) and writes them contiguously.
+// A record beyond its tile's region goes to the overflow list.
 __global__ void __launch_bounds__(kPartThreads, 3) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
                                                          const u32* __restrict__ bcnt, u32 nbh, u32 nbj,
                                                          u64* __restrict__ D, u32* __restrict__ bstart,
-                                                         u32* __restrict__ bfill) {
+                                                         u32* __restrict__ bfill, u64* __restrict__ ovf, u32 ovf_cap,
+                                                         u32* __restrict__ ovf_n) {
     constexpr u32 T = 1u << kHiBits;
     constexpr int R = kPartPerThread;
     __shared__ PartSmem sm;
@@ -313,53 +300,16 @@ __global__ void __launch_bounds__(kPartThreads, 3) bin_sort(const u64* __restric
     const u32 kt = bk / nbh, hi = bk % nbh;
     const u32 cnt = min(bcnt[bk], cap_bucket);
     const u64* src = B + u64(bk) * cap_bucket;
-    if (threadIdx.x < T) sm.lcnt[threadIdx.x] = 0;
-    __syncthreads();
-    for (u32 s0 = 0; s0 < cnt; s0 += kPartStep) {
-        u32 lo[R];
-#pragma unroll
-        for (int u = 0; u < R; ++u) {
-            const u32 i = s0 + u * kPartThreads + threadIdx.x;
-            lo[u] = i < cnt ? (rec_a(__ldg(src + i)) >> kBinJTShift) & (T - 1) : 0xffffffffu;
-        }
-#pragma unroll
-        for (int u = 0; u < R; ++u)
-            if (lo[u] != 0xffffffffu) atomicAdd(&sm.lcnt[lo[u]], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {  // the tiles' starts inside the bucket: exclusive scan of 128 counts
-        const int lane = threadIdx.x;
-        u32 c[4], tot = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            c[q] = sm.lcnt[lane * 4 + q];
-            tot += c[q];
-        }
-        u32 incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        u32 ex = incl - tot;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            sm.runo[lane * 4 + q] = ex;
-            ex += c[q];
-        }
-    }
-    __syncthreads();
+    const u32 cap_tile = cap_bucket / T;
     if (threadIdx.x < T) {
-        const u32 jt = hi * T + threadIdx.x;
-        if (jt < nbj) {
-            bstart[u64(kt) * nbj + jt] = hi * cap_bucket + sm.runo[threadIdx.x];
-            bfill[u64(kt) * nbj + jt] = sm.lcnt[threadIdx.x];
-        }
         sm.lcnt[threadIdx.x] = 0;
+        const u32 jt = hi * T + threadIdx.x;
+        if (jt < nbj) bstart[u64(kt) * nbj + jt] = hi * cap_bucket + threadIdx.x * cap_tile;
     }
     __syncthreads();
     auto region_of = [](u64 r) { return (rec_a(r) >> kBinJTShift) & (T - 1); };
-    u64* dst = D + u64(bk) * cap_bucket;  // every tile inside this bucket: positions are its start + rank
+    u64* dst = D + u64(bk) * cap_bucket;
+    u32* gfill = bfill + u64(kt) * nbj + u64(hi) * T;  // tiles past nbj hold no records: never touched
     for (u32 s0 = 0; s0 < cnt; s0 += kPartStep) {
         u64 rec[R];
         u32 rg[R];
@@ -369,8 +319,10 @@ __global__ void __launch_bounds__(kPartThreads, 3) bin_sort(const u64* __restric
             rec[u] = i < cnt ? __ldg(src + i) : 0ull;
             rg[u] = i < cnt ? (rec_a(rec[u]) >> kBinJTShift) & (T - 1) : 0xffffffffu;
         }
-        scatter_step<kPartThreads, R>(sm, rec, rg, T, region_of, dst, 0, cap_bucket, nullptr, 0u, nullptr);
+        scatter_step<kPartThreads, R>(sm, rec, rg, T, region_of, dst, cap_tile, cap_tile, ovf, ovf_cap, ovf_n, gfill);
     }
+    // the counters ran past the regions of overflowing tiles: the fills the later passes read are clamped
+    if (threadIdx.x < T && hi * T + threadIdx.x < nbj) atomicMin(&gfill[threadIdx.x], cap_tile);
 }
 
 // Each tile's records ordered by their x column (6 bits), in place: one CTA
