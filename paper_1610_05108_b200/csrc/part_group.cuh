@@ -29,6 +29,14 @@
 //                 the columns into the run's grouped array, then the blocks
 //                 (pairs of small blocks written warp-cooperatively, items for
 //                 large ones) exactly as the fused kernels emit them.
+// Under the binned verify nothing reads the keys afterwards, so the records
+// come straight from the row planes (project_scatter: no key array), as 4
+// bytes each — (local bucket << (32 - lb)) | column, the partition being the
+// record's place — where both fit (part_packed_ok), and then without a count
+// pass: every (run, partition) owns a fixed region of 2.5x the mean partition
+// size, the scatter's cursors end as the partition sizes and part_scan runs
+// after it. An overflowing region is flagged on the device and the host
+// redoes the search with counted partitions (engine.cu).
 // The order inside a bucket is not deterministic (atomics); nothing depends on
 // it: pair-list hits carry columns and the merge orders hits by (rid, v, j, k).
 #pragma once
