@@ -61,6 +61,49 @@ __device__ __forceinline__ u32 block_exclusive(u32 x, u32* ws, u32* total) {
     return r;
 }
 
+// Two scans behind the same three barriers (items and pairs of a join's emission): ws >= 66 u32.
+__device__ __forceinline__ void block_exclusive2(u32 x, u32 y, u32* ws, u32& ex, u32& ey, u32* tx, u32* ty) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u32 ix = x, iy = y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 a = __shfl_up_sync(0xffffffffu, ix, o), b = __shfl_up_sync(0xffffffffu, iy, o);
+        if (lane >= o) {
+            ix += a;
+            iy += b;
+        }
+    }
+    if (lane == 31) {
+        ws[wid] = ix;
+        ws[33 + wid] = iy;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const u32 wx = lane < nw ? ws[lane] : 0u, wy = lane < nw ? ws[33 + lane] : 0u;
+        u32 jx = wx, jy = wy;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 a = __shfl_up_sync(0xffffffffu, jx, o), b = __shfl_up_sync(0xffffffffu, jy, o);
+            if (lane >= o) {
+                jx += a;
+                jy += b;
+            }
+        }
+        ws[lane] = jx - wx;
+        ws[33 + lane] = jy - wy;
+        if (lane == 31) {
+            ws[32] = jx;
+            ws[65] = jy;
+        }
+    }
+    __syncthreads();
+    ex = ws[wid] + ix - x;
+    ey = ws[33 + wid] + iy - y;
+    *tx = ws[32];
+    *ty = ws[65];
+    __syncthreads();  // ws reusable
+}
+
 // 16-bit counters in shared memory + chunk bases.
 struct SmemTab16 {
     u32* w;      // 2^(M-1) words (two buckets each)

@@ -663,9 +663,8 @@ __global__ void __launch_bounds__(kPjThreads, 3) part_join(const uint2* __restri
             if (w) atomicAdd(reinterpret_cast<unsigned long long*>(work_run + b), static_cast<unsigned long long>(w));
         }
     }
-    u32 ti, tp;
-    u32 ibase = block_exclusive(my_items, ws, &ti);
-    u32 pbase = block_exclusive(my_pairs, ws + 33, &tp);
+    u32 ti, tp, ibase, pbase;
+    block_exclusive2(my_items, my_pairs, ws, ibase, pbase, &ti, &tp);
     if (ti == 0 && tp == 0) return;
     // only items (large blocks, expanded later) read the global grouped array:
     // inline pairs carry their columns, taken from shared memory here
