@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kPartThreads) bin_split(const u64* __restrict_
 // memory, reserves its runs in the tiles' fill counters (bfill, zeroed by the
 // host; one atomic per non-empty tile and step) and writes them contiguously.
 // A record beyond its tile's region goes to the overflow list.
-__global__ void __launch_bounds__(kPartThreads, 3) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
+__global__ void __launch_bounds__(kPartThreads, 2) bin_sort(const u64* __restrict__ B, u32 cap_bucket,
                                                          const u32* __restrict__ bcnt, u32 nbh, u32 nbj,
                                                          u64* __restrict__ D, u32* __restrict__ bstart,
                                                          u32* __restrict__ bfill, u64* __restrict__ ovf, u32 ovf_cap,
@@ -310,15 +310,19 @@ __global__ void __launch_bounds__(kPartThreads, 3) bin_sort(const u64* __restric
     auto region_of = [](u64 r) { return (rec_a(r) >> kBinJTShift) & (T - 1); };
     u64* dst = D + u64(bk) * cap_bucket;
     u32* gfill = bfill + u64(kt) * nbj + u64(hi) * T;  // tiles past nbj hold no records: never touched
+    extern __shared__ __align__(16) u64 stage8[];  // [kPartStep]: the next step's records (step_fetch)
+    step_fetch(stage8, src, 0, cnt);
     for (u32 s0 = 0; s0 < cnt; s0 += kPartStep) {
         u64 rec[R];
         u32 rg[R];
+        step_wait();
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const u32 i = s0 + u * kPartThreads + threadIdx.x;
-            rec[u] = i < cnt ? __ldg(src + i) : 0ull;
+            rec[u] = i < cnt ? stage8[u * kPartThreads + threadIdx.x] : 0ull;
             rg[u] = i < cnt ? (rec_a(rec[u]) >> kBinJTShift) & (T - 1) : 0xffffffffu;
         }
+        if (s0 + kPartStep < cnt) step_fetch(stage8, src, s0 + kPartStep, cnt);
         scatter_step<kPartThreads, R>(sm, rec, rg, T, region_of, dst, cap_tile, cap_tile, ovf, ovf_cap, ovf_n, gfill);
     }
     // the counters ran past the regions of overflowing tiles: the fills the later passes read are clamped

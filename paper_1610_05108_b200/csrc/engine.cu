@@ -1052,7 +1052,8 @@ void binned_verify(SearchCtx& c) {
         static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
     XYZB_LAUNCH_CHECK();
     XYZB_CUDA(cudaMemsetAsync(ds->bin_fill.p, 0, u64(nkt) * nbj * 4, st));
-    bins::bin_sort<<<nbuckets, bins::kPartThreads, 0, st>>>(ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket), ds->bin_cnt.as<u32>(),
+    func_smem(bins::bin_sort, bins::step_stage_smem());
+    bins::bin_sort<<<nbuckets, bins::kPartThreads, bins::step_stage_smem(), st>>>(ds->bin_b.as<u64>(), static_cast<u32>(c.cap_bucket), ds->bin_cnt.as<u32>(),
                                               static_cast<u32>(c.nbh), nbj, ds->bin_d.as<u64>(), ds->bin_start.as<u32>(),
                                               ds->bin_fill.as<u32>(), ds->bin_ovf.as<u64>(),
                                               static_cast<u32>(c.ovf_cap), ds->bin_ovfn.as<u32>());
